@@ -1,0 +1,242 @@
+/*
+ * lora_server.h -- C-ABI of the B200-native multi-LoRA delta hot path
+ * (InfiniLoRA, arxiv 2604.07173: the LoRA Server's data-parallel compute).
+ *
+ * Citations: P:n = PAPER.md line n (section / equation / figure).
+ *
+ * The operation (Sec. 2.2, Sec. 2.3, Fig. 4b, Sec. 4.1):
+ *   for every activation row i carrying adapter id a_i and routed expert e_i,
+ *       y[i,:] += s_{a_i} * (x[i,:] A_{a_i,e_i}) B_{a_i,e_i}
+ *   A_{a,e} in R^{h_in x r}, B_{a,e} in R^{r x h_out} (paper orientation),
+ *   rows with a_i = -1 carry no LoRA and are left bit-identical.
+ * Steps: a1 segment (stable sort by key a*E+e) -> a2 shrink
+ * v = x A -> a3 expand d = s v B -> a4 scatter-accumulate y[perm] += d.
+ *
+ * Terms
+ *   slot  one LoRA'd projection (e.g. layer 0 "gate" 4096->14336 with E=8
+ *         experts, or layer 3 "q" 4096->4096 with E=1).  The paper's
+ *         adapter space n x l x e is (adapter, slot, expert) here.
+ *   unit  (slot, adapter a, expert e): one A/B pair; unit id in a slot = a*E+e.
+ *   row   one activation vector; for MoE a (token, routed expert) pair, so a
+ *         batch of b tokens with top-k routing has T = b*k rows.
+ *
+ * Conventions (all functions)
+ *   - bf16 tensors are passed as raw 16-bit patterns (uint16).
+ *   - Every function returns lora_status_t and never throws / aborts.
+ *   - Host-detectable argument errors enqueue NOTHING and return
+ *     LORA_ERR_INVALID_ARG (or _UNSUPPORTED); lora_last_error() explains.
+ *   - Device-detectable id errors (adapter id outside [-1, n_adapters) or
+ *     expert id outside [0, E)) skip the row (treated as a = -1) and set a
+ *     sticky device flag, reported by lora_server_check() -- or immediately
+ *     if the environment variable LORA_DEBUG_SYNC=1 is set.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Single-GPU apply is fully asynchronous: no host synchronisation, no
+ *     allocation, so it can be captured into a CUDA graph.
+ *   - A server / plan handle is not thread-safe.  A plan owns its workspace,
+ *     so concurrent applies need one plan per stream.
+ */
+#ifndef LORA_SERVER_H_
+#define LORA_SERVER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lora_server lora_server_t; /* opaque */
+typedef struct lora_plan lora_plan_t;     /* opaque, reusable segmentation + workspace */
+
+typedef enum {
+  LORA_OK = 0,
+  LORA_ERR_INVALID_ARG = 1,
+  LORA_ERR_OOM = 2,
+  LORA_ERR_CUDA = 3,
+  LORA_ERR_ID_OUT_OF_RANGE = 4,
+  LORA_ERR_UNSUPPORTED = 5,
+  LORA_ERR_NCCL = 6
+} lora_status_t;
+
+typedef enum { LORA_BF16 = 0, LORA_FP32 = 1 } lora_dtype_t;
+
+typedef struct {
+  int32_t n_slots;           /* number of LoRA'd projections, >= 1 */
+  const int32_t *h_in;       /* [n_slots] input width;  multiple of 64 */
+  const int32_t *h_out;      /* [n_slots] output width; multiple of 64 */
+  const int32_t *n_experts;  /* [n_slots] E (1 for dense slots), >= 1 */
+  int32_t rank;              /* r, uniform (one rank per model): 8, 16, 32 or 64 */
+  int32_t n_adapters;        /* global adapter count n */
+  const float *scale;        /* [n_adapters] host fp32 s_a; NULL => all 1.0 (R1) */
+  int32_t max_rows;          /* capacity (rows) of the internal plan; 0 < max_rows <= 16384 */
+  int32_t device;            /* CUDA device ordinal */
+} lora_config_t;
+
+/* ------------------------------------------------------------------------- */
+/* Server: weight store                                                       */
+/* ------------------------------------------------------------------------- */
+
+/* Create a server and allocate its device weight store (all units of all
+ * slots).  A / B may be NULL (weights stay zero until lora_server_load or
+ * lora_server_fill_synthetic); otherwise A[slot] points to bf16 bits laid out
+ * [n_adapters][E][h_in][r] and B[slot] to [n_adapters][E][r][h_out] (P:165
+ * orientation), in device memory if weights_on_device != 0 else host memory.
+ * The weights are copied into library-owned memory (re-laid-out for the
+ * kernels); the caller may free its buffers when the call returns.
+ * Errors: INVALID_ARG (bad config), UNSUPPORTED (rank or widths), OOM, CUDA. */
+lora_status_t lora_server_create(const lora_config_t *cfg, const void *const *A, const void *const *B,
+                                 int weights_on_device, lora_server_t **out);
+
+/* Overwrite adapters [adapter_begin, adapter_begin+n) of one slot.  A / B use
+ * the create() layout restricted to those adapters ([n][E][h_in][r] and
+ * [n][E][r][h_out]).  Synchronises `stream` before returning.  On a sharded
+ * server, adapters the rank does not own are skipped. */
+lora_status_t lora_server_load(lora_server_t *s, int32_t slot, int32_t adapter_begin, int32_t n,
+                               const void *A, const void *B, int on_device, void *stream);
+
+/* Fill every unit of every slot from the counter-based generator described in
+ * DESIGN.md "Input recipe" (seeded, bf16-exact values; used for benchmarks
+ * whose weights do not fit through PCIe).  Async on `stream`. */
+lora_status_t lora_server_fill_synthetic(lora_server_t *s, uint64_t seed, void *stream);
+
+/* Synchronise the device, free everything. */
+lora_status_t lora_server_destroy(lora_server_t *s);
+
+/* Segments with more than `n` rows go to the tcgen05/TMEM kernels, the rest
+ * to the CUDA-core kernels (default: env LORA_SMALL_SEG_MAX, else 8).  n < 0
+ * forces the CUDA-core path for every segment.  The tcgen05 path needs
+ * rank 64; other ranks always use the CUDA-core path.  Takes effect at the
+ * next lora_plan_build. */
+lora_status_t lora_server_set_small_seg_max(lora_server_t *s, int32_t n);
+
+/* Sticky device error check: synchronises `stream`; returns
+ * LORA_ERR_ID_OUT_OF_RANGE (and clears the flag) if any apply since the last
+ * check met an out-of-range id, LORA_ERR_CUDA on a CUDA error, else LORA_OK. */
+lora_status_t lora_server_check(lora_server_t *s, void *stream);
+
+/* Human-readable reason for the last failing call on `s` (NULL => the calling
+ * thread's last create / argument error).  Never NULL. */
+const char *lora_last_error(const lora_server_t *s);
+
+/* ------------------------------------------------------------------------- */
+/* Plans: a1 segmentation, reusable across the slots of one unit of work       */
+/* ------------------------------------------------------------------------- */
+
+/* Allocate a plan for up to max_rows rows (<= 16384) plus the workspace of
+ * every slot (so one plan serves any sequence of slots). */
+lora_status_t lora_plan_create(lora_server_t *s, int32_t max_rows, lora_plan_t **out);
+lora_status_t lora_plan_destroy(lora_plan_t *p);
+
+/* a1: stable segmentation of T rows (device pointers adapter_ids[T],
+ * expert_ids[T] or NULL => e = 0) by key a*E + e with E = n_experts; rows with
+ * a = -1 are dropped; ties broken by ascending row index (R9).
+ * Builds perm / seg_offsets / seg_keys and the device work lists; the segment
+ * count stays on the device.  T = 0 is a no-op plan.  Async. */
+lora_status_t lora_plan_build(lora_server_t *s, lora_plan_t *p, const int32_t *adapter_ids,
+                              const int32_t *expert_ids, int32_t T, int32_t n_experts, void *stream);
+
+/* Copy the plan's indices out (bit-exact contract): perm[n_valid],
+ * seg_offsets[n_segs+1], seg_keys[n_segs] into DEVICE buffers sized
+ * max_rows / max_rows+1 / max_rows; n_valid / n_segs into HOST ints.
+ * Synchronises `stream`. */
+lora_status_t lora_plan_export(const lora_plan_t *p, int32_t *perm, int32_t *seg_offsets,
+                               int32_t *seg_keys, int32_t *n_valid, int32_t *n_segs, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* Apply: a2 shrink, a3 expand, a4 scatter-accumulate                          */
+/* ------------------------------------------------------------------------- */
+
+/* One slot: y[T][h_out] (bf16 or fp32, device, read-modify-written in place)
+ * += s * (x A) B for the rows of plan p; x is bf16 [T][h_in] (device).  The
+ * slot's E must equal the plan's n_experts.  x and y must not overlap. */
+lora_status_t lora_apply_plan(lora_server_t *s, const lora_plan_t *p, int32_t slot, const void *x,
+                              void *y, lora_dtype_t y_dtype, void *stream);
+
+/* Several slots sharing one plan in ONE set of launches (e.g. gate, up, down
+ * of a MoE layer, or the 128 q/k/v/o slots of a Llama decode step).  slots[n]
+ * must be distinct; x[i] / y[i] as in lora_apply_plan (x pointers may repeat,
+ * y pointers must be distinct).  slots / x / y are host arrays. */
+lora_status_t lora_apply_plan_multi(lora_server_t *s, const lora_plan_t *p, int32_t n,
+                                    const int32_t *slots, const void *const *x, void *const *y,
+                                    lora_dtype_t y_dtype, void *stream);
+
+/* Convenience: plan_build on the server's internal plan + apply_plan. */
+lora_status_t lora_apply(lora_server_t *s, int32_t slot, const void *x, const int32_t *adapter_ids,
+                         const int32_t *expert_ids, void *y, lora_dtype_t y_dtype, int32_t T,
+                         void *stream);
+
+/* End-to-end entry with HOST buffers (pinned for full async speed): copies
+ * the ids and the n slots' x / y host->device into library staging buffers,
+ * builds the internal plan, applies, and copies every y back device->host,
+ * all on `stream`, with the per-slot copies overlapped with compute on an
+ * internal copy stream.  Returns after enqueueing; the caller synchronises
+ * `stream` before reading y.  Capacity: T <= max_rows.  x[i] pointers may
+ * repeat (the copy is made once). */
+lora_status_t lora_apply_multi_host(lora_server_t *s, int32_t n, const int32_t *slots,
+                                    const void *const *x_host, const int32_t *adapter_ids_host,
+                                    const int32_t *expert_ids_host, void *const *y_host,
+                                    lora_dtype_t y_dtype, int32_t T, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* Sharded LoRA Server: LoRA Data Parallel (Sec. 4.1, Table 1 DP row) */
+/* ------------------------------------------------------------------------- */
+
+/* 128-byte NCCL unique id for rank 0 to broadcast (torch.distributed is the
+ * bootstrap).  Fails with LORA_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+lora_status_t lora_nccl_unique_id(void *out128);
+
+/* Create the rank-`rank` member of a world-`world` sharded server.  Adapter a
+ * is owned by rank a mod world; each rank stores only its adapters.  Every
+ * rank must call this collectively with the same config. */
+lora_status_t lora_server_create_sharded(const lora_config_t *cfg, int32_t rank, int32_t world,
+                                         const void *nccl_unique_id, lora_server_t **out);
+
+/* Collective apply on a sharded server: every rank passes its OWN rows
+ * (T local rows, device pointers, same slot list on every rank).  Rows are
+ * routed to the owner of their adapter (NCCL all-to-all over NVLink),
+ * applied there, and the deltas are returned and added into the caller's y.
+ * One host synchronisation (the count exchange). */
+lora_status_t lora_apply_sharded(lora_server_t *s, int32_t n, const int32_t *slots,
+                                 const void *const *x, const int32_t *adapter_ids,
+                                 const int32_t *expert_ids, void *const *y, lora_dtype_t y_dtype,
+                                 int32_t T, void *stream);
+
+/* Host-only helper (no GPU needed): given the world x world send-count
+ * matrix counts[src*world+dst], fill this rank's send offsets
+ * send_off[world+1] (into its owner-bucketed send buffer) and receive
+ * offsets recv_off[world+1] (receive order: by source rank ascending).
+ * Used by the sharded apply and by the CPU multi-process tests. */
+lora_status_t lora_shard_layout(const int64_t *counts, int32_t world, int32_t rank,
+                                int64_t *send_off, int64_t *recv_off);
+
+/* Synthetic activation rows for benchmarks and tests: dst is bf16 [rows][width]
+ * (device), element (i, c) = the counter-based generator of DESIGN.md "Input
+ * recipe" with major = row_base + i, minor = c, the given tag and shift.  Async. */
+lora_status_t lora_synth_fill_rows(void *dst, int64_t rows, int32_t width, uint64_t seed, uint32_t tag,
+                                   int32_t shift, int64_t row_base, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* Profiling: per-launch CUDA events on the launching stream                  */
+/* ------------------------------------------------------------------------- */
+
+/* Start recording a (start, end) event pair around every kernel launch of
+ * this server (up to max_launches launches; <= 0 disables).  Clears records. */
+lora_status_t lora_profile_enable(lora_server_t *s, int32_t max_launches);
+
+/* Synchronise on the recorded events and return, per kernel kind k <
+ * n_kinds, the number of launches and their summed device time in ms
+ * (launches[k], total_ms[k]; host arrays).  Clears the records. */
+lora_status_t lora_profile_read(lora_server_t *s, int32_t n_kinds, int32_t *launches, double *total_ms);
+
+/* Name of kernel kind k (0 segment, 1 simt_shrink, 2 tc05_shrink,
+ * 3 simt_expand, 4 tc05_expand, 5 shard_bucket, 6 shard_gather,
+ * 7 shard_scatter_add); "unknown" otherwise. */
+const char *lora_kernel_name(int32_t kind);
+
+/* Library version string. */
+const char *lora_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LORA_SERVER_H_ */

@@ -130,6 +130,46 @@ def unit_B_bits(seed: int, slot: int, unit: int, r: int, h_out: int) -> np.ndarr
     return hash_bf16_bits(seed, tag_of(KIND_B, slot), unit, minor, shift_B(r)).reshape(r, h_out)
 
 
+_CGEN = None
+
+
+def _cgen():
+    """Compiled copy of the same generator (lora_inputs/_gen.c), for large sets."""
+    global _CGEN
+    if _CGEN is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, so = os.path.join(here, "_gen.c"), os.path.join(here, "_gen.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-o", so, src])
+        lib = ctypes.CDLL(so)
+        lib.gen_bf16_rows.restype = None
+        lib.gen_bf16_rows.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
+        _CGEN = lib
+    return _CGEN
+
+
+def gen_rows_fast(seed: int, tag: int, majors: Sequence[int], n_minor: int, shift: int) -> np.ndarray:
+    """bf16 bits [len(majors)][n_minor], minor = 0..n_minor-1 (C generator)."""
+    majors = np.ascontiguousarray(np.asarray(majors, dtype=np.uint64))
+    out = np.empty((majors.size, n_minor), np.uint16)
+    _cgen().gen_bf16_rows(int(seed), int(tag), majors.ctypes.data, majors.size, n_minor, int(shift),
+                          out.ctypes.data)
+    return out
+
+
+def units_A_bits(seed: int, slot: int, units: Sequence[int], h_in: int, r: int) -> np.ndarray:
+    """Stack of unit_A_bits for many units: [U][h_in][r]."""
+    return gen_rows_fast(seed, tag_of(KIND_A, slot), units, h_in * r, shift_A(h_in)).reshape(-1, h_in, r)
+
+
+def units_B_bits(seed: int, slot: int, units: Sequence[int], r: int, h_out: int) -> np.ndarray:
+    return gen_rows_fast(seed, tag_of(KIND_B, slot), units, r * h_out, shift_B(r)).reshape(-1, r, h_out)
+
+
 def rows_bits(seed: int, kind: int, index: int, rows: Sequence[int], width: int, shift: int) -> np.ndarray:
     """bf16 bits [len(rows)][width] of an activation-like tensor; major = row id."""
     rows = np.asarray(rows, dtype=U64).reshape(-1, 1)

@@ -153,6 +153,15 @@ def apply_slot(cfg: li.Config, slot_index: int, batch: li.Batch, rows: Optional[
     Inputs come from lora_inputs' counter-based generator: x rows (xbuf of the
     slot), units (touched only), y0 ("random" or "zero").  Returns y rows as
     float32 (y_dtype fp32) or bf16 bits (bf16)."""
+    args = prepare_slot(cfg, slot_index, batch, rows, y0, seed)
+    return lora_apply_rows(*args, n_threads=n_threads)
+
+
+def prepare_slot(cfg: li.Config, slot_index: int, batch: li.Batch, rows: Optional[Sequence[int]] = None,
+                 y0: str = "random", seed: Optional[int] = None):
+    """Regenerate the inputs of ``apply_slot`` -> args of ``lora_apply_rows``
+    (x, unit_of_row, scale_of_row, A, B, y); lets callers time the oracle's
+    arithmetic without the input generation."""
     seed = cfg.seed if seed is None else seed
     slot = cfg.slots[slot_index]
     rows = np.arange(batch.n_rows) if rows is None else np.asarray(rows, dtype=np.int64)
@@ -160,12 +169,9 @@ def apply_slot(cfg: li.Config, slot_index: int, batch: li.Batch, rows: Optional[
     e = batch.expert_ids[rows]
     uor, units, sor = unit_tables(a, e, slot.n_experts, cfg.n_adapters, cfg.scale())
     r = cfg.rank
-    A = np.empty((units.size, slot.h_in, r), np.uint16)
-    B = np.empty((units.size, r, slot.h_out), np.uint16)
-    for i, u in enumerate(units):
-        A[i] = li.unit_A_bits(seed, slot_index, int(u), slot.h_in, r)
-        B[i] = li.unit_B_bits(seed, slot_index, int(u), r, slot.h_out)
-    x = li.x_rows_bits(seed, slot.xbuf, rows, slot.h_in)
+    A = li.units_A_bits(seed, slot_index, units, slot.h_in, r)
+    B = li.units_B_bits(seed, slot_index, units, r, slot.h_out)
+    x = li.gen_rows_fast(seed, li.tag_of(li.KIND_X, slot.xbuf), rows, slot.h_in, li.shift_x())
     if y0 == "random":
         y = li.y0_rows_bits(seed, slot_index, rows, slot.h_out)
         if cfg.y_dtype == "fp32":
@@ -173,7 +179,7 @@ def apply_slot(cfg: li.Config, slot_index: int, batch: li.Batch, rows: Optional[
     else:
         y = np.zeros((rows.size, slot.h_out), np.float32 if cfg.y_dtype == "fp32" else np.uint16)
     y = np.ascontiguousarray(y)
-    return lora_apply_rows(x, uor, sor, A, B, y, n_threads)
+    return x, uor, sor, A, B, y
 
 
 # ----------------------------------------------------------------------------

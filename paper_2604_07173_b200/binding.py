@@ -1,0 +1,260 @@
+"""Thin ctypes binding of include/lora_server.h -- argument marshalling only.
+
+Every function here has the C-ABI name and forwards to liblora_server.so; all
+compute runs in the library's sm_100a kernels.  torch tensors are accepted
+wherever the C-ABI takes a pointer (``.data_ptr()``) and torch streams wherever
+it takes a ``cudaStream_t`` (``.cuda_stream``).  There is no CPU fallback: if
+the library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblora_server.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_07173_b200.build` "
+                      "(there is no CPU fallback for the LoRA kernels)")
+lib = ctypes.CDLL(LIB_PATH)
+
+LORA_OK, LORA_ERR_INVALID_ARG, LORA_ERR_OOM, LORA_ERR_CUDA = 0, 1, 2, 3
+LORA_ERR_ID_OUT_OF_RANGE, LORA_ERR_UNSUPPORTED, LORA_ERR_NCCL = 4, 5, 6
+LORA_BF16, LORA_FP32 = 0, 1
+STATUS = {0: "LORA_OK", 1: "LORA_ERR_INVALID_ARG", 2: "LORA_ERR_OOM", 3: "LORA_ERR_CUDA",
+          4: "LORA_ERR_ID_OUT_OF_RANGE", 5: "LORA_ERR_UNSUPPORTED", 6: "LORA_ERR_NCCL"}
+
+
+class LoraConfig(ctypes.Structure):
+    _fields_ = [("n_slots", ctypes.c_int32), ("h_in", ctypes.POINTER(ctypes.c_int32)),
+                ("h_out", ctypes.POINTER(ctypes.c_int32)), ("n_experts", ctypes.POINTER(ctypes.c_int32)),
+                ("rank", ctypes.c_int32), ("n_adapters", ctypes.c_int32),
+                ("scale", ctypes.POINTER(ctypes.c_float)), ("max_rows", ctypes.c_int32),
+                ("device", ctypes.c_int32)]
+
+
+_vp, _i32, _i64, _u64, _u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32
+_pp = ctypes.POINTER(ctypes.c_void_p)
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+# name -> (restype, argtypes); must match include/lora_server.h exactly
+SIGNATURES = {
+    "lora_server_create": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _pp, _pp, ctypes.c_int, _pp]),
+    "lora_server_load": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_int, _vp]),
+    "lora_server_fill_synthetic": (ctypes.c_int, [_vp, _u64, _vp]),
+    "lora_server_destroy": (ctypes.c_int, [_vp]),
+    "lora_server_set_small_seg_max": (ctypes.c_int, [_vp, _i32]),
+    "lora_server_check": (ctypes.c_int, [_vp, _vp]),
+    "lora_last_error": (ctypes.c_char_p, [_vp]),
+    "lora_plan_create": (ctypes.c_int, [_vp, _i32, _pp]),
+    "lora_plan_destroy": (ctypes.c_int, [_vp]),
+    "lora_plan_build": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp]),
+    "lora_plan_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _pi32, _pi32, _vp]),
+    "lora_apply_plan": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, ctypes.c_int, _vp]),
+    "lora_apply_plan_multi": (ctypes.c_int, [_vp, _vp, _i32, _pi32, _pp, _pp, ctypes.c_int, _vp]),
+    "lora_apply": (ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_int, _i32, _vp]),
+    "lora_apply_multi_host": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
+    "lora_nccl_unique_id": (ctypes.c_int, [_vp]),
+    "lora_server_create_sharded": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _pp]),
+    "lora_apply_sharded": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
+    "lora_shard_layout": (ctypes.c_int, [_pi64, _i32, _i32, _pi64, _pi64]),
+    "lora_synth_fill_rows": (ctypes.c_int, [_vp, _i64, _i32, _u64, _u32, _i32, _i64, _vp]),
+    "lora_profile_enable": (ctypes.c_int, [_vp, _i32]),
+    "lora_profile_read": (ctypes.c_int, [_vp, _i32, _pi32, ctypes.POINTER(ctypes.c_double)]),
+    "lora_kernel_name": (ctypes.c_char_p, [_i32]),
+    "lora_version": (ctypes.c_char_p, []),
+}
+N_KERNEL_KINDS = 8
+for _name, (_res, _args) in SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class LoraError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if hasattr(t, "ctypes"):          # numpy array (host)
+        return t.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(t)}")
+
+
+def _stream(s) -> Optional[int]:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def _check(rc: int, handle=None):
+    if rc != LORA_OK:
+        msg = lib.lora_last_error(handle)
+        raise LoraError(rc, msg.decode() if msg else "")
+
+
+def _ptr_array(items):
+    arr = (ctypes.c_void_p * len(items))()
+    for i, t in enumerate(items):
+        arr[i] = _ptr(t)
+    return arr
+
+
+def make_config(h_in: Sequence[int], h_out: Sequence[int], n_experts: Sequence[int], rank: int, n_adapters: int,
+                scale=None, max_rows: int = 4096, device: int = 0):
+    n = len(h_in)
+    keep = {"h_in": (ctypes.c_int32 * n)(*h_in), "h_out": (ctypes.c_int32 * n)(*h_out),
+            "E": (ctypes.c_int32 * n)(*n_experts)}
+    keep["scale"] = (ctypes.c_float * n_adapters)(*[float(v) for v in scale]) if scale is not None else None
+    cfg = LoraConfig(n, keep["h_in"], keep["h_out"], keep["E"], rank, n_adapters,
+                     keep["scale"] if keep["scale"] is not None else None, max_rows, device)
+    cfg._keep = keep  # keep the arrays alive
+    return cfg
+
+
+# ----------------------------------------------------------------------------
+# C-ABI functions (same names)
+# ----------------------------------------------------------------------------
+def lora_server_create(cfg: LoraConfig, A=None, B=None, weights_on_device: bool = True) -> int:
+    out = ctypes.c_void_p()
+    a = _ptr_array(A) if A is not None else None
+    b = _ptr_array(B) if B is not None else None
+    _check(lib.lora_server_create(ctypes.byref(cfg), a, b, int(weights_on_device), ctypes.byref(out)))
+    return out.value
+
+
+def lora_server_load(s: int, slot: int, adapter_begin: int, n: int, A, B, on_device: bool = True, stream=None):
+    _check(lib.lora_server_load(s, slot, adapter_begin, n, _ptr(A), _ptr(B), int(on_device), _stream(stream)), s)
+
+
+def lora_server_fill_synthetic(s: int, seed: int, stream=None):
+    _check(lib.lora_server_fill_synthetic(s, seed, _stream(stream)), s)
+
+
+def lora_server_destroy(s: int):
+    _check(lib.lora_server_destroy(s))
+
+
+def lora_server_set_small_seg_max(s: int, n: int):
+    _check(lib.lora_server_set_small_seg_max(s, n), s)
+
+
+def lora_server_check(s: int, stream=None) -> int:
+    return lib.lora_server_check(s, _stream(stream))
+
+
+def lora_last_error(s: Optional[int]) -> str:
+    return lib.lora_last_error(s).decode()
+
+
+def lora_plan_create(s: int, max_rows: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.lora_plan_create(s, max_rows, ctypes.byref(out)), s)
+    return out.value
+
+
+def lora_plan_destroy(p: int):
+    _check(lib.lora_plan_destroy(p))
+
+
+def lora_plan_build(s: int, p: int, adapter_ids, expert_ids, T: int, n_experts: int, stream=None):
+    _check(lib.lora_plan_build(s, p, _ptr(adapter_ids), _ptr(expert_ids), T, n_experts, _stream(stream)), s)
+
+
+def lora_plan_export(s: int, p: int, perm, seg_offsets, seg_keys, stream=None):
+    nv, ns = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.lora_plan_export(p, _ptr(perm), _ptr(seg_offsets), _ptr(seg_keys), ctypes.byref(nv),
+                                ctypes.byref(ns), _stream(stream)), s)
+    return nv.value, ns.value
+
+
+def lora_apply_plan(s: int, p: int, slot: int, x, y, y_dtype: int, stream=None):
+    _check(lib.lora_apply_plan(s, p, slot, _ptr(x), _ptr(y), y_dtype, _stream(stream)), s)
+
+
+def lora_apply_plan_multi(s: int, p: int, slots: Sequence[int], x, y, y_dtype: int, stream=None):
+    n = len(slots)
+    sl = (ctypes.c_int32 * n)(*slots)
+    _check(lib.lora_apply_plan_multi(s, p, n, sl, _ptr_array(x), _ptr_array(y), y_dtype, _stream(stream)), s)
+
+
+def lora_apply(s: int, slot: int, x, adapter_ids, expert_ids, y, y_dtype: int, T: int, stream=None):
+    _check(lib.lora_apply(s, slot, _ptr(x), _ptr(adapter_ids), _ptr(expert_ids), _ptr(y), y_dtype, T,
+                          _stream(stream)), s)
+
+
+def lora_apply_multi_host(s: int, slots: Sequence[int], x_host, adapter_ids_host, expert_ids_host, y_host,
+                          y_dtype: int, T: int, stream=None):
+    n = len(slots)
+    sl = (ctypes.c_int32 * n)(*slots)
+    _check(lib.lora_apply_multi_host(s, n, sl, _ptr_array(x_host), _ptr(adapter_ids_host), _ptr(expert_ids_host),
+                                     _ptr_array(y_host), y_dtype, T, _stream(stream)), s)
+
+
+def lora_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.lora_nccl_unique_id(buf))
+    return buf.raw
+
+
+def lora_server_create_sharded(cfg: LoraConfig, rank: int, world: int, unique_id: bytes) -> int:
+    out = ctypes.c_void_p()
+    idb = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _check(lib.lora_server_create_sharded(ctypes.byref(cfg), rank, world, idb, ctypes.byref(out)))
+    return out.value
+
+
+def lora_apply_sharded(s: int, slots: Sequence[int], x, adapter_ids, expert_ids, y, y_dtype: int, T: int,
+                       stream=None):
+    n = len(slots)
+    sl = (ctypes.c_int32 * n)(*slots)
+    _check(lib.lora_apply_sharded(s, n, sl, _ptr_array(x), _ptr(adapter_ids), _ptr(expert_ids), _ptr_array(y),
+                                  y_dtype, T, _stream(stream)), s)
+
+
+def lora_shard_layout(counts, world: int, rank: int):
+    """counts: flat sequence of world*world ints (src-major). Returns (send_off, recv_off)."""
+    c = (ctypes.c_int64 * (world * world))(*[int(v) for v in counts])
+    so = (ctypes.c_int64 * (world + 1))()
+    ro = (ctypes.c_int64 * (world + 1))()
+    _check(lib.lora_shard_layout(c, world, rank, so, ro))
+    return list(so), list(ro)
+
+
+def lora_synth_fill_rows(dst, rows: int, width: int, seed: int, tag: int, shift: int, row_base: int = 0,
+                         stream=None):
+    _check(lib.lora_synth_fill_rows(_ptr(dst), rows, width, seed, tag, shift, row_base, _stream(stream)))
+
+
+def lora_profile_enable(s: int, max_launches: int):
+    _check(lib.lora_profile_enable(s, max_launches), s)
+
+
+def lora_profile_read(s: int):
+    """-> {kernel name: (launches, total_ms)} for kinds with launches."""
+    n = N_KERNEL_KINDS
+    la = (ctypes.c_int32 * n)()
+    ms = (ctypes.c_double * n)()
+    _check(lib.lora_profile_read(s, n, la, ms), s)
+    return {lora_kernel_name(k): (int(la[k]), float(ms[k])) for k in range(n) if la[k] > 0}
+
+
+def lora_kernel_name(kind: int) -> str:
+    return lib.lora_kernel_name(kind).decode()
+
+
+def lora_version() -> str:
+    return lib.lora_version().decode()

@@ -1,0 +1,85 @@
+// kernels.h -- internal (non-ABI) declarations shared by the .cu files of the
+// CUDA path: device-side plan view, per-launch task descriptors, launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lora {
+
+constexpr int kMaxPlanRows = 16384;  // single-CTA segmenter capacity (128 KB of composites)
+constexpr int kGroupRows = 8;        // rows per CUDA-core work group
+constexpr int kTileRows = 128;       // rows per tcgen05 tile (UMMA M / N)
+constexpr int kMaxTasks = 96;        // slots per multi-slot launch (param space)
+
+enum { kCntValid = 0, kCntSegs = 1, kCntGroups = 2, kCntTiles = 3, kCntWords = 8 };
+
+// Device view of a plan (all device pointers).
+struct PlanDev {
+  int32_t* perm;     // [max_rows]   sorted position -> original row
+  int32_t* seg_off;  // [max_rows+1]
+  int32_t* seg_key;  // [max_rows]   key a*E+e
+  int32_t* counts;   // [kCntWords]
+  int4* groups;      // [max_rows]   CUDA-core groups {row_begin, nrows, key, seg}
+  int4* tiles;       // [max_rows]   tcgen05 tiles    {row_begin, nrows, key, seg}
+  float* vpart;      // shrink partial sums, per slot region [n_kc][max_rows][r]
+  int max_rows;
+};
+
+struct SegParams {
+  int small_max;   // segments with more rows than this go to tcgen05 (if enabled)
+  int tc_enabled;  // rank 64 and not forced off
+  int tile_rows;
+};
+
+// One slot inside a (multi-slot) launch.
+struct SlotTask {
+  const uint16_t* At;  // weight store, shrink operand
+  const uint16_t* Bt;  // weight store, expand operand
+  const uint16_t* x;   // bf16 [T][h_in]
+  void* y;             // bf16 / fp32 [T][h_out]
+  long long vpart_off; // float offset of this slot's partial-sum region
+  int h_in, h_out, E;
+  int KI, SJ, n_kc;    // shrink: j-range per item, j per stage, items per row group
+  int CI, SC, n_ci;    // expand: c-range per item, c rows per stage, items per row group
+  int kc_base, ci_base;// prefix over tasks of n_kc / n_ci
+};
+
+struct MultiArgs {
+  int n_tasks;
+  int total_kc, total_ci;  // sums of n_kc / n_ci
+  int y_fp32;
+  int y_store;             // 1: write fp32 delta s*(xA)B into y (sharded delta mode), 0: y += delta
+  int world;               // adapter striping (unit = (a/world)*E + e)
+  const float* scale;      // [n_adapters] s_a
+  SlotTask t[kMaxTasks];
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,
+                           int world, int shard_rank, const SegParams& sp, const PlanDev& pd, int* err_flag,
+                           cudaStream_t stream);
+cudaError_t launch_simt_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+cudaError_t launch_simt_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+bool tc_available();
+
+// synthetic fill / weight relayout (synth_fill.cu)
+cudaError_t launch_fill_store(uint16_t* At, uint16_t* Bt, int h_in, int h_out, int E, int r, long long units,
+                              int slot, unsigned long long seed, int world, int shard_rank, int n_adapters,
+                              cudaStream_t stream);
+cudaError_t launch_fill_rows(uint16_t* dst, long long rows, int width, unsigned long long seed, unsigned tag,
+                             int shift, long long row_base, cudaStream_t stream);
+cudaError_t launch_relayout_A(const uint16_t* src, uint16_t* At, long long units, int h_in, int r,
+                              cudaStream_t stream);
+cudaError_t launch_relayout_B(const uint16_t* src, uint16_t* Bt, long long units, int h_out, int r,
+                              cudaStream_t stream);
+
+// simt kernel smem requirement (for host-side validation)
+int simt_shrink_smem(int rank);
+int simt_expand_smem(int rank);
+int simt_sj_max(int rank);
+int simt_sc_max(int rank);
+
+}  // namespace lora

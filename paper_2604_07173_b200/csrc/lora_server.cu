@@ -1,0 +1,694 @@
+// lora_server.cu -- the C-ABI (include/lora_server.h) and the host runtime:
+// weight store, plans/workspace, size-based path dispatch.
+//
+// Operation: y[i,:] += s_{a_i} * (x[i,:] A_{a_i,e_i}) B_{a_i,e_i}
+// (Sec. 2.2, Sec. 2.3, Fig. 4b, Sec. 4.1).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "server.h"
+
+using namespace lora;
+
+namespace {
+thread_local std::string g_thread_error = "";
+
+bool env_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && v[0] && std::strcmp(v, "0") != 0;
+}
+
+// largest divisor of n that is a multiple of `mult` and <= cap (>= mult; n % mult == 0)
+int best_divisor(int n, int mult, int cap) {
+  int best = mult;
+  for (int d = mult; d <= n && d <= cap; d += mult)
+    if (n % d == 0) best = d;
+  return best;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+}  // namespace
+
+namespace lora {
+
+lora_status_t fail(lora_server* s, lora_status_t st, const std::string& msg) {
+  if (s)
+    s->last_error = msg;
+  else
+    g_thread_error = msg;
+  g_thread_error = msg;
+  return st;
+}
+
+lora_status_t cuda_fail(lora_server* s, cudaError_t e, const char* where) {
+  return fail(s, LORA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace lora
+
+#define CK(s, call)                                          \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return lora::cuda_fail((s), _e, #call); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// server
+// ---------------------------------------------------------------------------
+static lora_status_t validate_config(const lora_config_t* cfg) {
+  if (!cfg) return fail(nullptr, LORA_ERR_INVALID_ARG, "cfg is NULL");
+  if (cfg->n_slots < 1 || !cfg->h_in || !cfg->h_out || !cfg->n_experts)
+    return fail(nullptr, LORA_ERR_INVALID_ARG, "n_slots < 1 or NULL shape arrays");
+  if (cfg->rank != 8 && cfg->rank != 16 && cfg->rank != 32 && cfg->rank != 64)
+    return fail(nullptr, LORA_ERR_UNSUPPORTED, "rank must be 8, 16, 32 or 64");
+  if (cfg->n_adapters < 1) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_adapters < 1");
+  if (cfg->max_rows < 1 || cfg->max_rows > kMaxPlanRows)
+    return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows must be in [1, 16384]");
+  for (int i = 0; i < cfg->n_slots; ++i) {
+    if (cfg->h_in[i] < 64 || cfg->h_in[i] % 64 || cfg->h_out[i] < 64 || cfg->h_out[i] % 64)
+      return fail(nullptr, LORA_ERR_UNSUPPORTED, "h_in / h_out must be positive multiples of 64");
+    if (cfg->n_experts[i] < 1) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_experts < 1");
+    if ((long long)cfg->n_adapters * cfg->n_experts[i] >= (1LL << 31))
+      return fail(nullptr, LORA_ERR_UNSUPPORTED, "n_adapters * E must fit in int32");
+  }
+  if (cfg->scale)
+    for (int a = 0; a < cfg->n_adapters; ++a)
+      if (!std::isfinite(cfg->scale[a])) return fail(nullptr, LORA_ERR_INVALID_ARG, "non-finite scale");
+  return LORA_OK;
+}
+
+static void free_server(lora_server* s) {
+  if (!s) return;
+  if (s->internal_plan) plan_destroy_impl(s->internal_plan);
+  for (auto& sl : s->slots) {
+    cudaFree(sl.At);
+    cudaFree(sl.Bt);
+  }
+  cudaFree(s->d_scale);
+  cudaFree(s->d_err);
+  cudaFree(s->h2d_buf);
+  for (auto ev : s->events) cudaEventDestroy(ev);
+  for (auto ev : s->prof_pool) cudaEventDestroy(ev);
+  if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+  delete s;
+}
+
+// allocate the store; world/rank select the owned adapters (a mod world == rank)
+static lora_status_t create_common(const lora_config_t* cfg, int world, int rank, lora_server** out) {
+  lora_status_t v = validate_config(cfg);
+  if (v != LORA_OK) return v;
+  if (!out) return fail(nullptr, LORA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
+    return fail(nullptr, LORA_ERR_CUDA, "no such CUDA device");
+  CK(nullptr, cudaSetDevice(cfg->device));
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cfg->device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cfg->device);
+  if (major != 10 || minor != 0)
+    return fail(nullptr, LORA_ERR_UNSUPPORTED, "this library is built for sm_100a (B200) only");
+
+  lora_server* s = new (std::nothrow) lora_server();
+  if (!s) return fail(nullptr, LORA_ERR_OOM, "host allocation failed");
+  s->device = cfg->device;
+  s->r = cfg->rank;
+  s->n_adapters = cfg->n_adapters;
+  s->world = world;
+  s->shard_rank = rank;
+  s->n_adapters_local = (cfg->n_adapters - rank + world - 1) / world;
+  s->max_rows = cfg->max_rows;
+  s->debug_sync = env_flag("LORA_DEBUG_SYNC");
+  if (const char* e = std::getenv("LORA_SMALL_SEG_MAX")) s->small_seg_max = std::atoi(e);
+  cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
+
+  const int r = cfg->rank;
+  int kc_prefix = 0;
+  for (int i = 0; i < cfg->n_slots; ++i) {
+    SlotInfo sl;
+    sl.h_in = cfg->h_in[i];
+    sl.h_out = cfg->h_out[i];
+    sl.E = cfg->n_experts[i];
+    sl.units = (long long)s->n_adapters_local * sl.E;
+    // shrink items of ~128 KB of A, expand items of ~128 KB of B
+    sl.KI = best_divisor(sl.h_in, 64, std::max(64, 65536 / r));
+    sl.SJ = best_divisor(sl.KI, 64, simt_sj_max(r));
+    sl.n_kc = sl.h_in / sl.KI;
+    sl.CI = best_divisor(sl.h_out, 64, std::max(64, 65536 / r));
+    sl.SC = best_divisor(sl.CI, 64, simt_sc_max(r));
+    sl.n_ci = sl.h_out / sl.CI;
+    sl.kc_prefix = kc_prefix;
+    kc_prefix += sl.n_kc;
+    const size_t a_bytes = (size_t)sl.units * sl.h_in * r * 2, b_bytes = (size_t)sl.units * sl.h_out * r * 2;
+    if (cudaMalloc(&sl.At, a_bytes) != cudaSuccess || cudaMalloc(&sl.Bt, b_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      s->slots.push_back(sl);
+      free_server(s);
+      return fail(nullptr, LORA_ERR_OOM, "weight store allocation failed (slot " + std::to_string(i) + ")");
+    }
+    s->slots.push_back(sl);
+    if (cudaMemset(sl.At, 0, a_bytes) != cudaSuccess || cudaMemset(sl.Bt, 0, b_bytes) != cudaSuccess) {
+      free_server(s);
+      return fail(nullptr, LORA_ERR_CUDA, "cudaMemset of the store failed");
+    }
+  }
+  s->total_kc = kc_prefix;
+  std::vector<float> sc(cfg->n_adapters, 1.0f);
+  if (cfg->scale) std::memcpy(sc.data(), cfg->scale, sizeof(float) * cfg->n_adapters);
+  if (cudaMalloc(&s->d_scale, sizeof(float) * cfg->n_adapters) != cudaSuccess ||
+      cudaMalloc(&s->d_err, sizeof(int)) != cudaSuccess) {
+    free_server(s);
+    return fail(nullptr, LORA_ERR_OOM, "allocation failed");
+  }
+  cudaMemcpy(s->d_scale, sc.data(), sizeof(float) * cfg->n_adapters, cudaMemcpyHostToDevice);
+  cudaMemset(s->d_err, 0, sizeof(int));
+  lora_status_t ps = plan_create_impl(s, cfg->max_rows, &s->internal_plan);
+  if (ps != LORA_OK) {
+    std::string m = s->last_error;
+    free_server(s);
+    return fail(nullptr, ps, m);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    free_server(s);
+    return fail(nullptr, LORA_ERR_CUDA, "device synchronisation after create failed");
+  }
+  *out = s;
+  return LORA_OK;
+}
+
+lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out) {
+  return create_common(cfg, world, rank, out);
+}
+
+// delta mode for the sharded owner: y[i] receives fp32 s*(xA)B (stored, not added)
+lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
+                                void* const* d, cudaStream_t st) {
+  return apply_multi_impl(s, p, n, slots, x, d, LORA_FP32, st, true);
+}
+
+static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, const void* A, const void* B,
+                               int on_device, cudaStream_t st) {
+  SlotInfo& sl = s->slots[slot];
+  const int r = s->r;
+  const size_t a_unit = (size_t)sl.h_in * r, b_unit = (size_t)sl.h_out * r;  // elements
+  // stage one adapter at a time (E units) through a device buffer, relayout into the store
+  uint16_t* stage = nullptr;
+  const size_t stage_elems = (size_t)sl.E * std::max(a_unit, b_unit);
+  CK(s, cudaMalloc(&stage, stage_elems * 2));
+  lora_status_t rc = LORA_OK;
+  for (int i = 0; i < n && rc == LORA_OK; ++i) {
+    const int a = a_begin + i;
+    if (a % s->world != s->shard_rank) continue;  // not owned by this rank
+    const long long lu = (long long)(a / s->world) * sl.E;
+    for (int pass = 0; pass < 2; ++pass) {
+      const void* src = pass == 0 ? A : B;
+      if (!src) continue;
+      const size_t ue = pass == 0 ? a_unit : b_unit;
+      const uint16_t* from = static_cast<const uint16_t*>(src) + (size_t)i * sl.E * ue;
+      cudaError_t e = cudaMemcpyAsync(stage, from, (size_t)sl.E * ue * 2,
+                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess)
+        e = pass == 0 ? launch_relayout_A(stage, sl.At + lu * a_unit, sl.E, sl.h_in, r, st)
+                      : launch_relayout_B(stage, sl.Bt + lu * b_unit, sl.E, sl.h_out, r, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = cuda_fail(s, e, "lora_server_load");
+    }
+  }
+  cudaFree(stage);
+  return rc;
+}
+
+extern "C" lora_status_t lora_server_create(const lora_config_t* cfg, const void* const* A, const void* const* B,
+                                            int weights_on_device, lora_server_t** out) {
+  lora_status_t st = create_common(cfg, 1, 0, out);
+  if (st != LORA_OK) return st;
+  lora_server* s = *out;
+  for (int i = 0; i < cfg->n_slots; ++i) {
+    const void* a = A ? A[i] : nullptr;
+    const void* b = B ? B[i] : nullptr;
+    if (!a && !b) continue;
+    st = load_slot(s, i, 0, cfg->n_adapters, a, b, weights_on_device, nullptr);
+    if (st != LORA_OK) {
+      std::string m = s->last_error;
+      free_server(s);
+      *out = nullptr;
+      return fail(nullptr, st, m);
+    }
+  }
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_server_load(lora_server_t* s, int32_t slot, int32_t adapter_begin, int32_t n,
+                                          const void* A, const void* B, int on_device, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (slot < 0 || slot >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot");
+  if (adapter_begin < 0 || n < 0 || (long long)adapter_begin + n > s->n_adapters)
+    return fail(s, LORA_ERR_INVALID_ARG, "adapter range out of bounds");
+  if (!A && !B) return fail(s, LORA_ERR_INVALID_ARG, "A and B are both NULL");
+  CK(s, cudaSetDevice(s->device));
+  return load_slot(s, slot, adapter_begin, n, A, B, on_device, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" lora_status_t lora_server_fill_synthetic(lora_server_t* s, uint64_t seed, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  CK(s, cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (size_t i = 0; i < s->slots.size(); ++i) {
+    SlotInfo& sl = s->slots[i];
+    CK(s, launch_fill_store(sl.At, sl.Bt, sl.h_in, sl.h_out, sl.E, s->r, sl.units, (int)i, seed, s->world,
+                            s->shard_rank, s->n_adapters, st));
+  }
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_server_destroy(lora_server_t* s) {
+  if (!s) return LORA_OK;
+  cudaSetDevice(s->device);
+  cudaDeviceSynchronize();
+  lora_shard_free(s);
+  free_server(s);
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_server_set_small_seg_max(lora_server_t* s, int32_t n) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  s->small_seg_max = n;
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_server_check(lora_server_t* s, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  CK(s, cudaSetDevice(s->device));
+  CK(s, cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  int flag = 0;
+  CK(s, cudaMemcpy(&flag, s->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    CK(s, cudaMemset(s->d_err, 0, sizeof(int)));
+    return fail(s, LORA_ERR_ID_OUT_OF_RANGE, "an adapter or expert id was out of range (row skipped)");
+  }
+  return LORA_OK;
+}
+
+extern "C" const char* lora_last_error(const lora_server_t* s) {
+  return s ? s->last_error.c_str() : g_thread_error.c_str();
+}
+
+extern "C" const char* lora_version(void) { return "infinilora-b200 0.1 (sm_100a)"; }
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+namespace lora {
+
+lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
+  if (max_rows < 1 || max_rows > kMaxPlanRows) return fail(s, LORA_ERR_UNSUPPORTED, "max_rows must be in [1, 16384]");
+  lora_plan* p = new (std::nothrow) lora_plan();
+  if (!p) return fail(s, LORA_ERR_OOM, "host allocation failed");
+  p->s = s;
+  p->max_rows = max_rows;
+  p->world = s->world;
+  PlanDev& d = p->dev;
+  d.max_rows = max_rows;
+  bool ok = cudaMalloc(&d.perm, sizeof(int32_t) * max_rows) == cudaSuccess &&
+            cudaMalloc(&d.seg_off, sizeof(int32_t) * (max_rows + 1)) == cudaSuccess &&
+            cudaMalloc(&d.seg_key, sizeof(int32_t) * max_rows) == cudaSuccess &&
+            cudaMalloc(&d.counts, sizeof(int32_t) * kCntWords) == cudaSuccess &&
+            cudaMalloc(&d.groups, sizeof(int4) * max_rows) == cudaSuccess &&
+            cudaMalloc(&d.tiles, sizeof(int4) * max_rows) == cudaSuccess &&
+            cudaMalloc(&d.vpart, sizeof(float) * (size_t)s->total_kc * max_rows * s->r) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    plan_destroy_impl(p);
+    return fail(s, LORA_ERR_OOM, "plan allocation failed");
+  }
+  cudaMemset(d.counts, 0, sizeof(int32_t) * kCntWords);
+  cudaMemset(d.seg_off, 0, sizeof(int32_t) * (max_rows + 1));
+  *out = p;
+  return LORA_OK;
+}
+
+void plan_destroy_impl(lora_plan* p) {
+  if (!p) return;
+  cudaFree(p->dev.perm);
+  cudaFree(p->dev.seg_off);
+  cudaFree(p->dev.seg_key);
+  cudaFree(p->dev.counts);
+  cudaFree(p->dev.groups);
+  cudaFree(p->dev.tiles);
+  cudaFree(p->dev.vpart);
+  delete p;
+}
+
+static bool tc_enabled(const lora_server* s) { return tc_available() && s->r == 64 && s->small_seg_max >= 0; }
+
+lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapter_ids, const int32_t* expert_ids,
+                              int T, int E, cudaStream_t st) {
+  if (T < 0 || T > p->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");
+  if (E < 1) return fail(s, LORA_ERR_INVALID_ARG, "n_experts < 1");
+  if (T > 0 && !adapter_ids) return fail(s, LORA_ERR_INVALID_ARG, "adapter_ids is NULL");
+  SegParams sp;
+  sp.small_max = s->small_seg_max < 0 ? kMaxPlanRows : s->small_seg_max;
+  sp.tc_enabled = tc_enabled(s) ? 1 : 0;
+  sp.tile_rows = kTileRows;
+  CK(s, cudaSetDevice(s->device));
+  const int pi = prof_start(s, st);
+  CK(s, launch_segment(adapter_ids, expert_ids, T, E, s->n_adapters, s->world, s->shard_rank, sp, p->dev, s->d_err,
+                       st));
+  prof_stop(s, pi, kKSegment, st);
+  p->n_experts = E;
+  p->T = T;
+  if (s->debug_sync) {
+    CK(s, cudaStreamSynchronize(st));
+    int flag = 0;
+    CK(s, cudaMemcpy(&flag, s->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+      cudaMemset(s->d_err, 0, sizeof(int));
+      return fail(s, LORA_ERR_ID_OUT_OF_RANGE, "an adapter or expert id was out of range (LORA_DEBUG_SYNC)");
+    }
+  }
+  return LORA_OK;
+}
+
+lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
+                               void* const* y, lora_dtype_t y_dtype, cudaStream_t st, bool store) {
+  if (!p || p->s != s) return fail(s, LORA_ERR_INVALID_ARG, "plan does not belong to this server");
+  if (p->n_experts < 0) return fail(s, LORA_ERR_INVALID_ARG, "plan was never built");
+  if (n < 0 || (n > 0 && (!slots || !x || !y))) return fail(s, LORA_ERR_INVALID_ARG, "bad slot list");
+  if (y_dtype != LORA_BF16 && y_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "y_dtype");
+  std::set<int> seen;
+  std::set<const void*> ys;
+  for (int i = 0; i < n; ++i) {
+    const int sl = slots[i];
+    if (sl < 0 || sl >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
+    if (!seen.insert(sl).second) return fail(s, LORA_ERR_INVALID_ARG, "duplicate slot in one multi apply");
+    if (s->slots[sl].E != p->n_experts)
+      return fail(s, LORA_ERR_INVALID_ARG, "slot n_experts differs from the plan's n_experts");
+    if (p->T > 0) {
+      if (!x[i] || !y[i]) return fail(s, LORA_ERR_INVALID_ARG, "x or y is NULL");
+      if (!aligned16(x[i]) || !aligned16(y[i])) return fail(s, LORA_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
+      if (!ys.insert(y[i]).second) return fail(s, LORA_ERR_INVALID_ARG, "y pointers must be distinct");
+      const SlotInfo& si = s->slots[sl];
+      const char* xb = static_cast<const char*>(x[i]);
+      const char* yb = static_cast<const char*>(y[i]);
+      const size_t xl = (size_t)p->T * si.h_in * 2, yl = (size_t)p->T * si.h_out * (y_dtype == LORA_FP32 ? 4 : 2);
+      if (xb < yb + yl && yb < xb + xl) return fail(s, LORA_ERR_INVALID_ARG, "x and y overlap");
+    }
+  }
+  if (n == 0 || p->T == 0) return LORA_OK;
+  CK(s, cudaSetDevice(s->device));
+  const bool tc = tc_enabled(s);
+  for (int b0 = 0; b0 < n; b0 += kMaxTasks) {
+    const int nb = std::min(kMaxTasks, n - b0);
+    MultiArgs args;
+    std::memset(&args, 0, sizeof(args));
+    args.n_tasks = nb;
+    args.y_fp32 = y_dtype == LORA_FP32;
+    args.y_store = store ? 1 : 0;
+    args.world = s->world;
+    args.scale = s->d_scale;
+    int kc = 0, ci = 0;
+    for (int i = 0; i < nb; ++i) {
+      const SlotInfo& si = s->slots[slots[b0 + i]];
+      SlotTask& t = args.t[i];
+      t.At = si.At;
+      t.Bt = si.Bt;
+      t.x = static_cast<const uint16_t*>(x[b0 + i]);
+      t.y = y[b0 + i];
+      t.vpart_off = (long long)si.kc_prefix * p->max_rows * s->r;
+      t.h_in = si.h_in;
+      t.h_out = si.h_out;
+      t.E = si.E;
+      t.KI = si.KI;
+      t.SJ = si.SJ;
+      t.n_kc = si.n_kc;
+      t.CI = si.CI;
+      t.SC = si.SC;
+      t.n_ci = si.n_ci;
+      t.kc_base = kc;
+      t.ci_base = ci;
+      kc += si.n_kc;
+      ci += si.n_ci;
+    }
+    args.total_kc = kc;
+    args.total_ci = ci;
+    const int grid = s->sm_count;
+    int pi = prof_start(s, st);
+    CK(s, launch_simt_shrink(s->r, args, p->dev, grid, st));
+    prof_stop(s, pi, kKSimtShrink, st);
+    if (tc) {
+      pi = prof_start(s, st);
+      CK(s, launch_tc_shrink(args, p->dev, grid, st));
+      prof_stop(s, pi, kKTcShrink, st);
+    }
+    pi = prof_start(s, st);
+    CK(s, launch_simt_expand(s->r, args, p->dev, grid, st));
+    prof_stop(s, pi, kKSimtExpand, st);
+    if (tc) {
+      pi = prof_start(s, st);
+      CK(s, launch_tc_expand(args, p->dev, grid, st));
+      prof_stop(s, pi, kKTcExpand, st);
+    }
+  }
+  if (s->debug_sync) {
+    CK(s, cudaStreamSynchronize(st));
+    int flag = 0;
+    CK(s, cudaMemcpy(&flag, s->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+      cudaMemset(s->d_err, 0, sizeof(int));
+      return fail(s, LORA_ERR_ID_OUT_OF_RANGE, "an adapter or expert id was out of range (LORA_DEBUG_SYNC)");
+    }
+  }
+  return LORA_OK;
+}
+
+}  // namespace lora
+
+extern "C" lora_status_t lora_plan_create(lora_server_t* s, int32_t max_rows, lora_plan_t** out) {
+  if (!s || !out) return fail(s, LORA_ERR_INVALID_ARG, "NULL argument");
+  CK(s, cudaSetDevice(s->device));
+  return plan_create_impl(s, max_rows, out);
+}
+
+extern "C" lora_status_t lora_plan_destroy(lora_plan_t* p) {
+  if (!p) return LORA_OK;
+  cudaSetDevice(p->s->device);
+  cudaDeviceSynchronize();
+  plan_destroy_impl(p);
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_plan_build(lora_server_t* s, lora_plan_t* p, const int32_t* adapter_ids,
+                                         const int32_t* expert_ids, int32_t T, int32_t n_experts, void* stream) {
+  if (!s || !p) return fail(s, LORA_ERR_INVALID_ARG, "NULL server or plan");
+  if (p->s != s) return fail(s, LORA_ERR_INVALID_ARG, "plan does not belong to this server");
+  return plan_build_impl(s, p, adapter_ids, expert_ids, T, n_experts, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" lora_status_t lora_plan_export(const lora_plan_t* p, int32_t* perm, int32_t* seg_offsets,
+                                          int32_t* seg_keys, int32_t* n_valid, int32_t* n_segs, void* stream) {
+  if (!p || !n_valid || !n_segs) return fail(nullptr, LORA_ERR_INVALID_ARG, "NULL argument");
+  lora_server* s = p->s;
+  CK(s, cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t cnt[kCntWords];
+  CK(s, cudaMemcpyAsync(cnt, p->dev.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+  CK(s, cudaStreamSynchronize(st));
+  *n_valid = cnt[kCntValid];
+  *n_segs = cnt[kCntSegs];
+  if (perm && cnt[kCntValid] > 0)
+    CK(s, cudaMemcpyAsync(perm, p->dev.perm, sizeof(int32_t) * cnt[kCntValid], cudaMemcpyDeviceToDevice, st));
+  if (seg_offsets)
+    CK(s, cudaMemcpyAsync(seg_offsets, p->dev.seg_off, sizeof(int32_t) * (cnt[kCntSegs] + 1),
+                          cudaMemcpyDeviceToDevice, st));
+  if (seg_keys && cnt[kCntSegs] > 0)
+    CK(s, cudaMemcpyAsync(seg_keys, p->dev.seg_key, sizeof(int32_t) * cnt[kCntSegs], cudaMemcpyDeviceToDevice, st));
+  CK(s, cudaStreamSynchronize(st));
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_apply_plan(lora_server_t* s, const lora_plan_t* p, int32_t slot, const void* x, void* y,
+                                         lora_dtype_t y_dtype, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  const void* xs[1] = {x};
+  void* ys[1] = {y};
+  return apply_multi_impl(s, p, 1, &slot, xs, ys, y_dtype, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" lora_status_t lora_apply_plan_multi(lora_server_t* s, const lora_plan_t* p, int32_t n, const int32_t* slots,
+                                               const void* const* x, void* const* y, lora_dtype_t y_dtype,
+                                               void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  return apply_multi_impl(s, p, n, slots, x, y, y_dtype, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" lora_status_t lora_apply(lora_server_t* s, int32_t slot, const void* x, const int32_t* adapter_ids,
+                                    const int32_t* expert_ids, void* y, lora_dtype_t y_dtype, int32_t T,
+                                    void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  if (slot < 0 || slot >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  lora_status_t rc = plan_build_impl(s, s->internal_plan, adapter_ids, expert_ids, T, s->slots[slot].E, st);
+  if (rc != LORA_OK) return rc;
+  const void* xs[1] = {x};
+  void* ys[1] = {y};
+  return apply_multi_impl(s, s->internal_plan, 1, &slot, xs, ys, y_dtype, st);
+}
+
+// ---------------------------------------------------------------------------
+// end-to-end with host buffers
+// ---------------------------------------------------------------------------
+extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, const int32_t* slots,
+                                               const void* const* x_host, const int32_t* adapter_ids_host,
+                                               const int32_t* expert_ids_host, void* const* y_host,
+                                               lora_dtype_t y_dtype, int32_t T, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  if (n < 1 || !slots || !x_host || !y_host || (T > 0 && !adapter_ids_host))
+    return fail(s, LORA_ERR_INVALID_ARG, "NULL argument");
+  if (T < 0 || T > s->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");
+  if (y_dtype != LORA_BF16 && y_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "y_dtype");
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
+    if (s->slots[slots[i]].E != s->slots[slots[0]].E)
+      return fail(s, LORA_ERR_INVALID_ARG, "all slots of one call must share n_experts");
+  }
+  if (T == 0) return LORA_OK;
+  CK(s, cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t ysz = y_dtype == LORA_FP32 ? 4 : 2;
+  // layout of the staging buffer: ids | distinct x | y per slot (256-byte aligned pieces)
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  std::vector<const void*> xd;  // distinct x host pointers
+  std::vector<int> x_of(n);
+  for (int i = 0; i < n; ++i) {
+    auto it = std::find(xd.begin(), xd.end(), x_host[i]);
+    if (it == xd.end()) {
+      x_of[i] = (int)xd.size();
+      xd.push_back(x_host[i]);
+    } else {
+      x_of[i] = (int)(it - xd.begin());
+    }
+  }
+  std::vector<size_t> x_off(xd.size()), y_off(n);
+  size_t off = al((size_t)T * 4) * 2;
+  std::vector<int> x_hin(xd.size());
+  for (int i = 0; i < n; ++i) x_hin[x_of[i]] = s->slots[slots[i]].h_in;
+  for (size_t j = 0; j < xd.size(); ++j) {
+    x_off[j] = off;
+    off += al((size_t)T * x_hin[j] * 2);
+  }
+  for (int i = 0; i < n; ++i) {
+    y_off[i] = off;
+    off += al((size_t)T * s->slots[slots[i]].h_out * ysz);
+  }
+  if (off > s->h2d_bytes) {
+    cudaStreamSynchronize(st);
+    cudaFree(s->h2d_buf);
+    s->h2d_buf = nullptr;
+    s->h2d_bytes = 0;
+    CK(s, cudaMalloc(&s->h2d_buf, off));
+    s->h2d_bytes = off;
+  }
+  char* base = static_cast<char*>(s->h2d_buf);
+  int32_t* d_ad = reinterpret_cast<int32_t*>(base);
+  int32_t* d_ex = reinterpret_cast<int32_t*>(base + al((size_t)T * 4));
+  CK(s, cudaMemcpyAsync(d_ad, adapter_ids_host, (size_t)T * 4, cudaMemcpyHostToDevice, st));
+  if (expert_ids_host) CK(s, cudaMemcpyAsync(d_ex, expert_ids_host, (size_t)T * 4, cudaMemcpyHostToDevice, st));
+  for (size_t j = 0; j < xd.size(); ++j)
+    CK(s, cudaMemcpyAsync(base + x_off[j], xd[j], (size_t)T * x_hin[j] * 2, cudaMemcpyHostToDevice, st));
+  std::vector<const void*> xs(n);
+  std::vector<void*> ys(n);
+  for (int i = 0; i < n; ++i) {
+    CK(s, cudaMemcpyAsync(base + y_off[i], y_host[i], (size_t)T * s->slots[slots[i]].h_out * ysz,
+                          cudaMemcpyHostToDevice, st));
+    xs[i] = base + x_off[x_of[i]];
+    ys[i] = base + y_off[i];
+  }
+  lora_status_t rc = plan_build_impl(s, s->internal_plan, d_ad, expert_ids_host ? d_ex : nullptr, T,
+                                     s->slots[slots[0]].E, st);
+  if (rc != LORA_OK) return rc;
+  rc = apply_multi_impl(s, s->internal_plan, n, slots, xs.data(), ys.data(), y_dtype, st);
+  if (rc != LORA_OK) return rc;
+  for (int i = 0; i < n; ++i)
+    CK(s, cudaMemcpyAsync(y_host[i], ys[i], (size_t)T * s->slots[slots[i]].h_out * ysz, cudaMemcpyDeviceToHost, st));
+  return LORA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// per-launch profiling with CUDA events on the launching stream
+// ---------------------------------------------------------------------------
+int prof_start(lora_server* s, cudaStream_t st) {
+  if (!s->prof_on || s->prof_recs.size() * 2 + 2 > s->prof_pool.size()) return -1;
+  const int i = (int)s->prof_recs.size() * 2;
+  if (cudaEventRecord(s->prof_pool[i], st) != cudaSuccess) return -1;
+  return i;
+}
+
+void prof_stop(lora_server* s, int idx, int kind, cudaStream_t st) {
+  if (idx < 0) return;
+  if (cudaEventRecord(s->prof_pool[idx + 1], st) == cudaSuccess) s->prof_recs.push_back({idx, kind});
+}
+
+extern "C" lora_status_t lora_profile_enable(lora_server_t* s, int32_t max_launches) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  CK(s, cudaSetDevice(s->device));
+  s->prof_recs.clear();
+  if (max_launches <= 0) {
+    s->prof_on = false;
+    return LORA_OK;
+  }
+  while ((int)s->prof_pool.size() < 2 * max_launches) {
+    cudaEvent_t e;
+    CK(s, cudaEventCreate(&e));
+    s->prof_pool.push_back(e);
+  }
+  s->prof_on = true;
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_profile_read(lora_server_t* s, int32_t n_kinds, int32_t* launches, double* total_ms) {
+  if (!s || !launches || !total_ms || n_kinds < 1) return fail(s, LORA_ERR_INVALID_ARG, "bad argument");
+  CK(s, cudaSetDevice(s->device));
+  for (int k = 0; k < n_kinds; ++k) {
+    launches[k] = 0;
+    total_ms[k] = 0.0;
+  }
+  for (auto& r : s->prof_recs) {
+    CK(s, cudaEventSynchronize(s->prof_pool[r.first + 1]));
+    float ms = 0.f;
+    CK(s, cudaEventElapsedTime(&ms, s->prof_pool[r.first], s->prof_pool[r.first + 1]));
+    if (r.second < n_kinds) {
+      launches[r.second] += 1;
+      total_ms[r.second] += ms;
+    }
+  }
+  s->prof_recs.clear();
+  return LORA_OK;
+}
+
+extern "C" const char* lora_kernel_name(int32_t kind) {
+  static const char* names[kKNumKinds] = {"segment",        "simt_shrink",   "tc05_shrink",  "simt_expand",
+                                          "tc05_expand",    "shard_bucket",  "shard_gather", "shard_scatter_add"};
+  return (kind >= 0 && kind < kKNumKinds) ? names[kind] : "unknown";
+}
+
+// synthetic activation rows (benchmarks / tests): dst bf16 [rows][width]
+extern "C" lora_status_t lora_synth_fill_rows(void* dst, int64_t rows, int32_t width, uint64_t seed, uint32_t tag,
+                                              int32_t shift, int64_t row_base, void* stream) {
+  if (!dst || rows < 0 || width < 1) return fail(nullptr, LORA_ERR_INVALID_ARG, "bad argument");
+  cudaError_t e = launch_fill_rows(static_cast<uint16_t*>(dst), rows, width, seed, tag, shift, row_base,
+                                   static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "lora_synth_fill_rows");
+  return LORA_OK;
+}

@@ -1,0 +1,83 @@
+// server.h -- internal C++ definitions of the opaque C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/lora_server.h"
+#include "kernels.h"
+
+struct SlotInfo {
+  int h_in = 0, h_out = 0, E = 1;
+  long long units = 0;     // local units = local adapters * E
+  uint16_t* At = nullptr;  // store, shrink operand
+  uint16_t* Bt = nullptr;  // store, expand operand
+  int KI = 0, SJ = 0, n_kc = 0;
+  int CI = 0, SC = 0, n_ci = 0;
+  int kc_prefix = 0;       // sum of n_kc over previous slots (workspace offset)
+};
+
+struct ShardState;  // shard.cu
+
+struct lora_server {
+  int device = 0;
+  int r = 0;
+  int n_adapters = 0;
+  int n_adapters_local = 0;
+  int max_rows = 0;
+  int sm_count = 148;
+  int small_seg_max = 8;
+  int world = 1, shard_rank = 0;
+  bool debug_sync = false;
+  std::vector<SlotInfo> slots;
+  int total_kc = 0;        // sum of n_kc over all slots
+  float* d_scale = nullptr;
+  int* d_err = nullptr;
+  lora_plan_t* internal_plan = nullptr;
+  std::string last_error;
+  // staging for lora_apply_multi_host (grown lazily)
+  void* h2d_buf = nullptr;
+  size_t h2d_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> events;
+  ShardState* shard = nullptr;
+  // per-launch CUDA-event profiling (lora_profile_enable / lora_profile_read)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_pool;
+  std::vector<std::pair<int, int>> prof_recs;  // (event index, kernel kind)
+};
+
+// kernel kinds reported by lora_profile_read
+enum { kKSegment = 0, kKSimtShrink = 1, kKTcShrink = 2, kKSimtExpand = 3, kKTcExpand = 4, kKShardBucket = 5,
+       kKShardGather = 6, kKShardScatter = 7, kKNumKinds = 8 };
+int prof_start(lora_server* s, cudaStream_t st);
+void prof_stop(lora_server* s, int idx, int kind, cudaStream_t st);
+
+struct lora_plan {
+  lora_server* s = nullptr;
+  lora::PlanDev dev{};
+  int max_rows = 0;
+  int n_experts = -1;  // E the plan was last built with (-1: never built)
+  int T = 0;
+  int world = 1;
+};
+
+namespace lora {
+lora_status_t fail(lora_server* s, lora_status_t st, const std::string& msg);
+lora_status_t cuda_fail(lora_server* s, cudaError_t e, const char* where);
+lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
+                               const void* const* x, void* const* y, lora_dtype_t y_dtype, cudaStream_t st,
+                               bool store = false);
+lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapter_ids, const int32_t* expert_ids,
+                              int T, int E, cudaStream_t st);
+lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out);
+void plan_destroy_impl(lora_plan* p);
+}  // namespace lora
+
+// shard.cu / lora_server.cu cross-file helpers (C++ linkage)
+void lora_shard_free(lora_server* s);
+lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out);
+lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
+                                const void* const* x, void* const* d, cudaStream_t st);

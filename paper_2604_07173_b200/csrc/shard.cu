@@ -1,0 +1,421 @@
+// shard.cu -- the Sharded LoRA Server: LoRA Data Parallel over NCCL / NVLink.
+//
+// P:288-291 (Sec. 4.1, Table 1 DP row): "evenly distribute LoRA adapters
+// across the server GPUs ... activations from client GPUs must be routed
+// accordingly ... the server GPUs perform a collective coordination step to
+// determine which activations should be processed by which GPUs."
+//
+// One collective apply (every rank, same slot list):
+//   1. owner-bucket the local rows, owner(a) = a mod G (stable, local order)
+//   2. all-gather of the G send counts -> full G x G matrix; ONE D2H sync
+//   3. grouped ncclSend/ncclRecv: x rows (each distinct x) + adapter/expert ids
+//      (receive order: source rank ascending, then the source's local order)
+//   4. local plan + apply in delta mode (fp32 delta written, not added)
+//   5. reverse grouped send/recv of the fp32 deltas
+//   6. y[origin row] = round(y + delta): one rounding, so the result is
+//      bit-identical to the unsharded apply (R18).
+// NCCL is loaded with dlopen("libnccl.so.2") (the copy torch already loaded),
+// so the library itself has no link-time NCCL dependency.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "server.h"
+
+using namespace lora;
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    api.err = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+    return api;
+  }
+#define SYM(field, name)                                                     \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));         \
+  if (!api.field) {                                                          \
+    api.err = std::string("missing NCCL symbol ") + name;                    \
+    return api;                                                              \
+  }
+  SYM(GetUniqueId, "ncclGetUniqueId");
+  SYM(CommInitRank, "ncclCommInitRank");
+  SYM(CommDestroy, "ncclCommDestroy");
+  SYM(GroupStart, "ncclGroupStart");
+  SYM(GroupEnd, "ncclGroupEnd");
+  SYM(Send, "ncclSend");
+  SYM(Recv, "ncclRecv");
+  SYM(AllGather, "ncclAllGather");
+  SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+  api.ok = true;
+  return api;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+constexpr int kBucketThreads = 1024;
+
+// Stable owner bucketing of T local rows (single CTA; T <= 16384).
+// send_idx[pos] = local row; counts[o] = rows for owner o.  Rows with a = -1
+// (or out of range, flagged) are not sent.
+__global__ void __launch_bounds__(kBucketThreads, 1)
+    bucket_kernel(const int32_t* __restrict__ ad, int T, int world, int n_adapters, int32_t* __restrict__ send_idx,
+                  int32_t* __restrict__ counts, int* __restrict__ err) {
+  __shared__ int s_tmp[40];
+  __shared__ int s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunk = (T + kBucketThreads - 1) / kBucketThreads;
+  const int r0 = min(tid * chunk, T), r1 = min(r0 + chunk, T);
+  if (tid == 0) s_base = 0;
+  int bad = 0;
+  for (int r = r0; r < r1; ++r) {
+    const int a = ad[r];
+    if (a < -1 || a >= n_adapters) bad = 1;
+  }
+  if (bad) atomicOr(err, 1);
+  __syncthreads();
+  for (int o = 0; o < world; ++o) {
+    int c = 0;
+    for (int r = r0; r < r1; ++r) {
+      const int a = ad[r];
+      c += (a >= 0 && a < n_adapters && a % world == o);
+    }
+    // block exclusive scan of c
+    int x = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) s_tmp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = s_tmp[lane];
+      for (int d = 1; d < 32; d <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= d) w += y;
+      }
+      s_tmp[lane] = w;
+    }
+    __syncthreads();
+    int pos = s_base + (warp ? s_tmp[warp - 1] : 0) + x - c;
+    const int tot = s_tmp[31];
+    for (int r = r0; r < r1; ++r) {
+      const int a = ad[r];
+      if (a >= 0 && a < n_adapters && a % world == o) send_idx[pos++] = r;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      counts[o] = tot;
+      s_base += tot;
+    }
+    __syncthreads();
+  }
+}
+
+// out[j][:] = in[idx[j]][:]  (rows of `width` 4-byte words)
+__global__ void gather_rows_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                   const int32_t* __restrict__ idx, int n, int width) {
+  const long long total = (long long)n * width;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long j = i / width;
+    const int c = (int)(i - j * width);
+    out[i] = in[(long long)idx[j] * width + c];
+  }
+}
+
+// y[idx[j]][c] = round(y + d[j][c])  (d fp32)
+__global__ void scatter_add_kernel(void* __restrict__ y, int y_fp32, const float* __restrict__ d,
+                                   const int32_t* __restrict__ idx, int n, int width) {
+  const long long total = (long long)n * width;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long j = i / width;
+    const int c = (int)(i - j * width);
+    const long long o = (long long)idx[j] * width + c;
+    if (y_fp32) {
+      float* p = reinterpret_cast<float*>(y) + o;
+      *p = *p + d[i];
+    } else {
+      uint16_t* p = reinterpret_cast<uint16_t*>(y) + o;
+      *p = f32_to_bf16_rne(bf16_to_f32(*p) + d[i]);
+    }
+  }
+}
+
+int grid_of(long long n) {
+  long long g = (n + 255) / 256;
+  return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
+}  // namespace
+
+struct ShardState {
+  ncclComm_t comm = nullptr;
+  // device scratch (grown on demand)
+  void* buf = nullptr;
+  size_t bytes = 0;
+  lora_plan* plan = nullptr;  // owner-side plan over received rows (capacity max_rows * world)
+};
+
+void lora_shard_free(lora_server* s) {
+  if (!s || !s->shard) return;
+  if (s->shard->comm && nccl().ok) nccl().CommDestroy(s->shard->comm);
+  cudaFree(s->shard->buf);
+  if (s->shard->plan) plan_destroy_impl(s->shard->plan);
+  delete s->shard;
+  s->shard = nullptr;
+}
+
+extern "C" lora_status_t lora_shard_layout(const int64_t* counts, int32_t world, int32_t rank, int64_t* send_off,
+                                           int64_t* recv_off) {
+  if (!counts || !send_off || !recv_off || world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_shard_layout: bad argument");
+  send_off[0] = 0;
+  recv_off[0] = 0;
+  for (int p = 0; p < world; ++p) {
+    if (counts[(size_t)rank * world + p] < 0 || counts[(size_t)p * world + rank] < 0)
+      return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_shard_layout: negative count");
+    send_off[p + 1] = send_off[p] + counts[(size_t)rank * world + p];  // my rows for owner p
+    recv_off[p + 1] = recv_off[p] + counts[(size_t)p * world + rank];  // rows source p sends me
+  }
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, LORA_ERR_INVALID_ARG, "NULL out");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(nullptr, LORA_ERR_NCCL, api.err);
+  ncclUniqueId id;
+  ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, LORA_ERR_NCCL, api.GetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, int32_t rank, int32_t world,
+                                                    const void* nccl_unique_id, lora_server_t** out) {
+  if (!cfg || !out || !nccl_unique_id || world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded: bad argument");
+  if ((long long)cfg->max_rows * world > kMaxPlanRows)
+    return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows * world must be <= 16384 (owner-side plan capacity)");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(nullptr, LORA_ERR_NCCL, api.err);
+  lora_status_t st = create_common_sharded(cfg, world, rank, out);
+  if (st != LORA_OK) return st;
+  lora_server* s = *out;
+  s->shard = new ShardState();
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, 128);
+  cudaSetDevice(s->device);
+  ncclResult_t r = api.CommInitRank(&s->shard->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    std::string m = std::string("ncclCommInitRank: ") + api.GetErrorString(r);
+    lora_server_destroy(s);
+    *out = nullptr;
+    return fail(nullptr, LORA_ERR_NCCL, m);
+  }
+  st = plan_create_impl(s, cfg->max_rows * world, &s->shard->plan);
+  if (st != LORA_OK) {
+    std::string m = s->last_error;
+    lora_server_destroy(s);
+    *out = nullptr;
+    return fail(nullptr, st, m);
+  }
+  return LORA_OK;
+}
+
+#define CKS(call)                                                 \
+  do {                                                            \
+    cudaError_t _e = (call);                                      \
+    if (_e != cudaSuccess) return cuda_fail(s, _e, #call);        \
+  } while (0)
+#define CKN(call)                                                                        \
+  do {                                                                                   \
+    ncclResult_t _r = (call);                                                            \
+    if (_r != ncclSuccess) return fail(s, LORA_ERR_NCCL, std::string(#call ": ") + api.GetErrorString(_r)); \
+  } while (0)
+
+extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const int32_t* slots, const void* const* x,
+                                            const int32_t* adapter_ids, const int32_t* expert_ids, void* const* y,
+                                            lora_dtype_t y_dtype, int32_t T, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (!s->shard) return fail(s, LORA_ERR_INVALID_ARG, "not a sharded server");
+  if (n < 1 || !slots || !x || !y || (T > 0 && !adapter_ids)) return fail(s, LORA_ERR_INVALID_ARG, "NULL argument");
+  if (T < 0 || T > s->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");
+  if (y_dtype != LORA_BF16 && y_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "y_dtype");
+  const int E = s->slots[slots[0]].E;
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
+    if (s->slots[slots[i]].E != E) return fail(s, LORA_ERR_INVALID_ARG, "slots of one call must share n_experts");
+  }
+  NcclApi& api = nccl();
+  const int G = s->world, me = s->shard_rank;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CKS(cudaSetDevice(s->device));
+
+  // distinct x buffers
+  std::vector<const void*> xd;
+  std::vector<int> x_of(n);
+  for (int i = 0; i < n; ++i) {
+    int j = 0;
+    while (j < (int)xd.size() && xd[j] != x[i]) ++j;
+    if (j == (int)xd.size()) xd.push_back(x[i]);
+    x_of[i] = j;
+  }
+  std::vector<int> x_hin(xd.size());
+  for (int i = 0; i < n; ++i) x_hin[x_of[i]] = s->slots[slots[i]].h_in;
+
+  // scratch layout (worst case: every rank sends every row to me -> G*T rows)
+  const long long Rmax = (long long)s->max_rows * G;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  size_t off = 0;
+  const size_t o_counts = off; off += al(sizeof(int32_t) * G * (G + 1));
+  const size_t o_send_idx = off; off += al(sizeof(int32_t) * s->max_rows);
+  const size_t o_ids_send = off; off += al(sizeof(int32_t) * 2 * s->max_rows);
+  const size_t o_ids_recv = off; off += al(sizeof(int32_t) * 2 * Rmax);
+  std::vector<size_t> o_xs(xd.size()), o_xr(xd.size());
+  for (size_t j = 0; j < xd.size(); ++j) {
+    o_xs[j] = off; off += al((size_t)s->max_rows * x_hin[j] * 2);
+    o_xr[j] = off; off += al((size_t)Rmax * x_hin[j] * 2);
+  }
+  std::vector<size_t> o_d(n), o_dr(n);
+  for (int i = 0; i < n; ++i) {
+    o_d[i] = off; off += al((size_t)Rmax * s->slots[slots[i]].h_out * 4);        // owner-side deltas
+    o_dr[i] = off; off += al((size_t)s->max_rows * s->slots[slots[i]].h_out * 4); // returned deltas
+  }
+  ShardState* sh = s->shard;
+  if (off > sh->bytes) {
+    cudaStreamSynchronize(st);
+    cudaFree(sh->buf);
+    sh->buf = nullptr;
+    sh->bytes = 0;
+    CKS(cudaMalloc(&sh->buf, off));
+    sh->bytes = off;
+  }
+  char* base = static_cast<char*>(sh->buf);
+  int32_t* d_counts = reinterpret_cast<int32_t*>(base + o_counts);  // [G] mine, then [G][G] gathered
+  int32_t* d_send_idx = reinterpret_cast<int32_t*>(base + o_send_idx);
+  int32_t* d_ids_send = reinterpret_cast<int32_t*>(base + o_ids_send);  // [2][T] (a | e) in send order
+  int32_t* d_ids_recv = reinterpret_cast<int32_t*>(base + o_ids_recv);
+
+  // 1. bucket
+  if (T > 0) {
+    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, T, G, s->n_adapters, d_send_idx, d_counts, s->d_err);
+  } else {
+    CKS(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * G, st));
+  }
+  CKS(cudaGetLastError());
+  // 2. counts exchange (all-gather) + the one host sync
+  CKN(api.AllGather(d_counts, d_counts + G, G, ncclInt32, sh->comm, st));
+  std::vector<int32_t> cnt(G * G);
+  CKS(cudaMemcpyAsync(cnt.data(), d_counts + G, sizeof(int32_t) * G * G, cudaMemcpyDeviceToHost, st));
+  CKS(cudaStreamSynchronize(st));
+  std::vector<int64_t> c64(cnt.begin(), cnt.end()), so(G + 1), ro(G + 1);
+  lora_status_t lr = lora_shard_layout(c64.data(), G, me, so.data(), ro.data());
+  if (lr != LORA_OK) return fail(s, lr, "count exchange produced an invalid matrix");
+  const int n_send = (int)so[G], n_recv = (int)ro[G];
+  if (n_recv > Rmax) return fail(s, LORA_ERR_INVALID_ARG, "received rows exceed capacity");
+
+  // 3. pack + dispatch
+  if (n_send > 0) {
+    gather_rows_kernel<<<grid_of(n_send), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(adapter_ids),
+                                                         reinterpret_cast<uint32_t*>(d_ids_send), d_send_idx, n_send,
+                                                         1);
+    if (expert_ids)
+      gather_rows_kernel<<<grid_of(n_send), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(expert_ids),
+                                                           reinterpret_cast<uint32_t*>(d_ids_send + s->max_rows),
+                                                           d_send_idx, n_send, 1);
+    else
+      CKS(cudaMemsetAsync(d_ids_send + s->max_rows, 0, sizeof(int32_t) * n_send, st));
+    for (size_t j = 0; j < xd.size(); ++j)
+      gather_rows_kernel<<<grid_of((long long)n_send * x_hin[j] / 2), 256, 0, st>>>(
+          static_cast<const uint32_t*>(xd[j]), reinterpret_cast<uint32_t*>(base + o_xs[j]), d_send_idx, n_send,
+          x_hin[j] / 2);
+    CKS(cudaGetLastError());
+  }
+  CKN(api.GroupStart());
+  for (int p = 0; p < G; ++p) {
+    const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
+    if (ns) {
+      CKN(api.Send(d_ids_send + so[p], ns, ncclInt32, p, sh->comm, st));
+      CKN(api.Send(d_ids_send + s->max_rows + so[p], ns, ncclInt32, p, sh->comm, st));
+      for (size_t j = 0; j < xd.size(); ++j)
+        CKN(api.Send(base + o_xs[j] + so[p] * x_hin[j] * 2, ns * x_hin[j], ncclBfloat16, p, sh->comm, st));
+    }
+    if (nr) {
+      CKN(api.Recv(d_ids_recv + ro[p], nr, ncclInt32, p, sh->comm, st));
+      CKN(api.Recv(d_ids_recv + Rmax + ro[p], nr, ncclInt32, p, sh->comm, st));
+      for (size_t j = 0; j < xd.size(); ++j)
+        CKN(api.Recv(base + o_xr[j] + ro[p] * x_hin[j] * 2, nr * x_hin[j], ncclBfloat16, p, sh->comm, st));
+    }
+  }
+  CKN(api.GroupEnd());
+
+  // 4. owner-side plan + delta-mode apply (fp32 delta stored)
+  lora_status_t rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, st);
+  if (rc != LORA_OK) return rc;
+  if (n_recv > 0) {
+    // rows whose adapter had no LoRA never arrive, so every received row is written
+    std::vector<const void*> xs(n);
+    std::vector<void*> ds(n);
+    for (int i = 0; i < n; ++i) {
+      xs[i] = base + o_xr[x_of[i]];
+      ds[i] = base + o_d[i];
+    }
+    rc = apply_multi_delta(s, sh->plan, n, slots, xs.data(), ds.data(), st);
+    if (rc != LORA_OK) return rc;
+  }
+
+  // 5. return deltas (reverse direction)
+  CKN(api.GroupStart());
+  for (int p = 0; p < G; ++p) {
+    const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
+    for (int i = 0; i < n; ++i) {
+      const int ho = s->slots[slots[i]].h_out;
+      if (nr) CKN(api.Send(base + o_d[i] + ro[p] * ho * 4, nr * ho, ncclFloat32, p, sh->comm, st));
+      if (ns) CKN(api.Recv(base + o_dr[i] + so[p] * ho * 4, ns * ho, ncclFloat32, p, sh->comm, st));
+    }
+  }
+  CKN(api.GroupEnd());
+
+  // 6. scatter-add at the origin
+  if (n_send > 0) {
+    for (int i = 0; i < n; ++i) {
+      const int ho = s->slots[slots[i]].h_out;
+      scatter_add_kernel<<<grid_of((long long)n_send * ho), 256, 0, st>>>(
+          y[i], y_dtype == LORA_FP32, reinterpret_cast<const float*>(base + o_dr[i]), d_send_idx, n_send, ho);
+    }
+    CKS(cudaGetLastError());
+  }
+  if (s->debug_sync) {
+    CKS(cudaStreamSynchronize(st));
+  }
+  return LORA_OK;
+}

@@ -1,0 +1,391 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars: segment/permutation indices bit-exact; exact-integer
+probes bit-exact on every kernel path; floating point within
+max|err| <= 1e-2*max|y| + 1e-3 (north_star), per slot; invariants bit-exact.
+Small sizes compare every element; BASELINE.json's full sizes compare sampled
+rows (the oracle computes them one by one), in the launch configuration that
+bench.py times (multi-slot apply over one plan).
+"""
+import numpy as np
+import pytest
+import torch
+
+import lora_inputs as li
+import oracle
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+from tests import gpu_util as U  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def B():
+    return U.binding()
+
+
+# ---------------------------------------------------------------------------
+# a1 segmentation: bit-exact
+# ---------------------------------------------------------------------------
+def _plan_indices(B, s, ad, ex, T, E, max_rows):
+    p = B.lora_plan_create(s, max_rows)
+    try:
+        B.lora_plan_build(s, p, ad, ex, T, E)
+        perm = torch.empty(max_rows, dtype=torch.int32, device=U.DEV)
+        off = torch.empty(max_rows + 1, dtype=torch.int32, device=U.DEV)
+        keys = torch.empty(max_rows, dtype=torch.int32, device=U.DEV)
+        nv, ns = B.lora_plan_export(s, p, perm, off, keys)
+        return perm[:nv].cpu().numpy(), off[:ns + 1].cpu().numpy(), keys[:ns].cpu().numpy()
+    finally:
+        B.lora_plan_destroy(p)
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_dense", "llama_decode", "mixtral_decode", "mixtral_prefill",
+                                  "mixtral_sharded"])
+def test_segment_bit_exact_configs(B, name):
+    cfg = li.CONFIGS[name]
+    b = li.make_batch(cfg)
+    # weights are irrelevant to a1: a small store with the config's adapter/expert space
+    seg_cfg = li.Config(cfg.name, cfg.index, (li.Slot("s", 64, 64, cfg.n_experts, 0),), 8, cfg.n_adapters,
+                        cfg.n_experts, cfg.top_k, cfg.n_tokens, "fp32")
+    s = U.make_server(B, seg_cfg, max_rows=max(b.n_rows, 1), fill=False)
+    try:
+        ad, ex = U.ids_dev(b)
+        perm, off, keys = _plan_indices(B, s, ad, ex, b.n_rows, cfg.n_experts, b.n_rows)
+        rp, ro, rk = oracle.segment(b.adapter_ids, b.expert_ids, cfg.n_experts)
+        np.testing.assert_array_equal(perm, rp)
+        np.testing.assert_array_equal(off, ro)
+        np.testing.assert_array_equal(keys, rk)
+    finally:
+        B.lora_server_destroy(s)
+
+
+ADVERSARIAL = {
+    "all_dropped": lambda rng: (np.full(100, -1), np.zeros(100)),
+    "empty": lambda rng: (np.zeros(0), np.zeros(0)),
+    "single": lambda rng: (np.array([37]), np.array([3])),
+    "one_key": lambda rng: (np.full(5000, 7), np.full(5000, 2)),
+    "all_distinct": lambda rng: (rng.permutation(4096), np.zeros(4096)),
+    "top_of_range": lambda rng: (np.full(300, 4095), np.full(300, 3)),
+    "max_rows_random": lambda rng: (rng.integers(-1, 4096, 16384), rng.integers(0, 4, 16384)),
+    "ragged_1023": lambda rng: (rng.integers(-1, 50, 1023), rng.integers(0, 4, 1023)),
+}
+
+
+@pytest.mark.parametrize("case", sorted(ADVERSARIAL))
+def test_segment_bit_exact_adversarial(B, case):
+    rng = np.random.default_rng(11)
+    a, e = ADVERSARIAL[case](rng)
+    a, e = a.astype(np.int32), e.astype(np.int32)
+    E = 4
+    cfg = li.Config("adv", 9, (li.Slot("s", 64, 64, E, 0),), 8, 4096, E, 1, max(len(a), 1), "fp32")
+    s = U.make_server(B, cfg, max_rows=16384, fill=False)
+    try:
+        ad = torch.from_numpy(a).to(U.DEV)
+        ex = torch.from_numpy(e).to(U.DEV)
+        perm, off, keys = _plan_indices(B, s, ad, ex, len(a), E, 16384)
+        rp, ro, rk = oracle.segment(a, e, E)
+        np.testing.assert_array_equal(perm, rp)
+        np.testing.assert_array_equal(off, ro)
+        np.testing.assert_array_equal(keys, rk)
+    finally:
+        B.lora_server_destroy(s)
+
+
+# ---------------------------------------------------------------------------
+# generator identity (the CUDA fill implements the same recipe)
+# ---------------------------------------------------------------------------
+def test_fill_rows_matches_generator(B):
+    x = torch.empty((37, 320), dtype=torch.int16, device=U.DEV)
+    B.lora_synth_fill_rows(x, 37, 320, 1234, li.tag_of(li.KIND_X, 5), li.shift_x(), 1000)
+    ref = li.x_rows_bits(1234, 5, np.arange(1000, 1037), 320)
+    np.testing.assert_array_equal(x.cpu().numpy().view(np.uint16), ref)
+
+
+@pytest.mark.parametrize("rank", [8, 16, 32, 64])
+def test_fill_store_equals_loaded_weights(B, rank):
+    """Server filled on device == server loaded from numpy-generated weights (bit-exact y)."""
+    E, n_ad, h_in, h_out, T = 2, 3, 128, 192, 40
+    cfg = li.Config("fill", 7, (li.Slot("s", h_in, h_out, E, 0),), rank, n_ad, E, 1, T, "fp32")
+    A = np.stack([li.unit_A_bits(cfg.seed, 0, u, h_in, rank) for u in range(n_ad * E)])
+    Bw = np.stack([li.unit_B_bits(cfg.seed, 0, u, rank, h_out) for u in range(n_ad * E)])
+    c = B.make_config([h_in], [h_out], [E], rank, n_ad, cfg.scale(), T, 0)
+    s1 = B.lora_server_create(c, [A], [Bw], weights_on_device=False)
+    s2 = U.make_server(B, cfg)
+    try:
+        rng = np.random.default_rng(1)
+        a = torch.from_numpy(rng.integers(-1, n_ad, T).astype(np.int32)).to(U.DEV)
+        e = torch.from_numpy(rng.integers(0, E, T).astype(np.int32)).to(U.DEV)
+        x = U.x_dev(B, cfg, 0, T)
+        y1 = U.y0_dev(B, cfg, 0, T)
+        y2 = y1.clone()
+        B.lora_apply(s1, 0, x, a, e, y1, B.LORA_FP32, T)
+        B.lora_apply(s2, 0, x, a, e, y2, B.LORA_FP32, T)
+        torch.cuda.synchronize()
+        assert torch.equal(y1.view(torch.int32), y2.view(torch.int32))
+    finally:
+        B.lora_server_destroy(s1)
+        B.lora_server_destroy(s2)
+
+
+# ---------------------------------------------------------------------------
+# exact-integer probes: bit-exact on every kernel path
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("rank,small_max", [(8, None), (16, None), (64, -1), (64, 0), (64, 4)])
+def test_exact_integer_probes(B, rank, small_max):
+    rng = np.random.default_rng(rank * 10 + (3 if small_max is None else small_max + 2))
+    E, n_ad, h_in, h_out, T = 2, 5, 64, 128, 300
+    Ai = rng.integers(-1, 2, (n_ad * E, h_in, rank))
+    Bi = rng.integers(-1, 2, (n_ad * E, rank, h_out))
+    xi = rng.integers(-2, 3, (T, h_in))
+    yi = rng.integers(-50, 51, (T, h_out)).astype(np.float32)
+    a = rng.integers(-1, n_ad, T).astype(np.int32)
+    a[:120] = 1                      # one large segment (tcgen05 path when enabled)
+    e = rng.integers(0, E, T).astype(np.int32)
+    scale = np.array([0.5, 1.0, 2.0, 0.5, 1.0], np.float32)
+    bits = lambda v: li.f32_to_bf16_bits_exact(np.asarray(v, np.float32))
+    c = B.make_config([h_in], [h_out], [E], rank, n_ad, scale, T, 0)
+    s = B.lora_server_create(c, [bits(Ai)], [bits(Bi)], weights_on_device=False)
+    try:
+        if small_max is not None:
+            B.lora_server_set_small_seg_max(s, small_max)
+        x = torch.from_numpy(bits(xi).view(np.int16)).to(U.DEV)
+        y = torch.from_numpy(yi.copy()).to(U.DEV)
+        B.lora_apply(s, 0, x, torch.from_numpy(a).to(U.DEV), torch.from_numpy(e).to(U.DEV), y, B.LORA_FP32, T)
+        torch.cuda.synchronize()
+        exp = yi.astype(np.float64).copy()
+        for i in range(T):
+            if a[i] >= 0:
+                u = a[i] * E + e[i]
+                exp[i] += float(scale[a[i]]) * ((xi[i] @ Ai[u]) @ Bi[u])
+        np.testing.assert_array_equal(y.cpu().numpy(), exp.astype(np.float32))
+    finally:
+        B.lora_server_destroy(s)
+
+
+# ---------------------------------------------------------------------------
+# float parity against the oracle
+# ---------------------------------------------------------------------------
+def _run_multi(B, s, cfg, batch, slot_ids, y0="random", host=False):
+    T = batch.n_rows
+    ad, ex = U.ids_dev(batch)
+    E = cfg.slots[slot_ids[0]].n_experts
+    xs = {}
+    for i in slot_ids:
+        xb = cfg.slots[i].xbuf
+        if xb not in xs:
+            xs[xb] = U.x_dev(B, cfg, i, T)
+    ys = [U.y0_dev(B, cfg, i, T, y0) for i in slot_ids]
+    dt = B.LORA_FP32 if cfg.y_dtype == "fp32" else B.LORA_BF16
+    p = B.lora_plan_create(s, T)
+    try:
+        B.lora_plan_build(s, p, ad, ex if E > 1 else None, T, E)
+        B.lora_apply_plan_multi(s, p, list(slot_ids), [xs[cfg.slots[i].xbuf] for i in slot_ids], ys, dt)
+        torch.cuda.synchronize()
+        assert B.lora_server_check(s) == B.LORA_OK
+    finally:
+        B.lora_plan_destroy(p)
+    return ys
+
+
+@pytest.mark.parametrize("name,y0,small_max", [("tiny", "random", None), ("tiny", "zero", None),
+                                                ("tiny_dense", "random", None), ("tiny", "random", -1)])
+def test_tiny_all_elements(B, name, y0, small_max):
+    cfg = li.CONFIGS[name]
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg, small_max=small_max)
+    try:
+        (y,) = _run_multi(B, s, cfg, b, [0], y0)
+        ref = oracle.apply_slot(cfg, 0, b, y0=y0)
+        U.assert_parity(y, ref, name)
+        # rows with a = -1 untouched, bit-exact
+        none = b.adapter_ids < 0
+        if y0 == "random":
+            y00 = U.y0_dev(B, cfg, 0, b.n_rows, y0)
+            assert torch.equal(y[torch.from_numpy(none).to(U.DEV)].view(torch.int32),
+                               y00[torch.from_numpy(none).to(U.DEV)].view(torch.int32))
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_llama_decode_two_layers_all_rows(B):
+    cfg = li.CONFIGS["llama_decode"]
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg, n_slots=8)
+    try:
+        ys = _run_multi(B, s, cfg, b, list(range(8)))
+        for i in range(8):
+            ref = oracle.apply_slot(cfg, i, b, n_threads=0)
+            U.assert_parity(ys[i], ref, f"llama slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+@pytest.mark.parametrize("name,small_max", [("mixtral_decode", None), ("mixtral_decode", -1),
+                                            ("mixtral_prefill", None)])
+def test_mixtral_sampled_rows(B, name, small_max):
+    cfg = li.CONFIGS[name]
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg, small_max=small_max)
+    try:
+        ys = _run_multi(B, s, cfg, b, [0, 1, 2])
+        rows = U.sample_rows(b, 40, E=cfg.n_experts)
+        for i in range(3):
+            ref = oracle.apply_slot(cfg, i, b, rows=rows)
+            U.assert_parity(ys[i][torch.from_numpy(rows).to(U.DEV)], ref, f"{name} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+@pytest.mark.slow
+def test_mixtral_sharded_config_at_g1_sampled(B):
+    """Config 5 on one GPU (116 GB of weights), the bench's N=1 workload."""
+    cfg = li.CONFIGS["mixtral_sharded"]
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        ys = _run_multi(B, s, cfg, b, [0, 1, 2])
+        rows = U.sample_rows(b, 24, E=cfg.n_experts)
+        for i in range(3):
+            ref = oracle.apply_slot(cfg, i, b, rows=rows)
+            U.assert_parity(ys[i][torch.from_numpy(rows).to(U.DEV)], ref, f"sharded-g1 slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+# ---------------------------------------------------------------------------
+# invariants and API equivalences (bit-exact)
+# ---------------------------------------------------------------------------
+def _mid_cfg(rank=64, T=600):
+    return li.Config("mid", 8, (li.Slot("a", 512, 768, 4, 0), li.Slot("b", 768, 512, 4, 1)), rank, 24, 4, 2,
+                     T // 2, "bf16")
+
+
+def test_determinism_and_multi_equals_single(B):
+    cfg = _mid_cfg()
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        y_multi = _run_multi(B, s, cfg, b, [0, 1])
+        y_again = _run_multi(B, s, cfg, b, [0, 1])
+        for u, v in zip(y_multi, y_again):
+            assert torch.equal(u, v)
+        for i in range(2):
+            (y1,) = _run_multi(B, s, cfg, b, [i])
+            assert torch.equal(y1, y_multi[i])
+            ref = oracle.apply_slot(cfg, i, b)
+            U.assert_parity(y1, ref, f"mid slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_permutation_equivariance_bit_exact(B):
+    cfg = _mid_cfg()
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        T = b.n_rows
+        (y,) = _run_multi(B, s, cfg, b, [0])
+        perm = np.random.default_rng(3).permutation(T)
+        ad = torch.from_numpy(b.adapter_ids[perm]).to(U.DEV)
+        ex = torch.from_numpy(b.expert_ids[perm]).to(U.DEV)
+        pt = torch.from_numpy(perm).to(U.DEV)
+        x = U.x_dev(B, cfg, 0, T)[pt].contiguous()
+        yp = U.y0_dev(B, cfg, 0, T)[pt].contiguous()
+        B.lora_apply(s, 0, x, ad, ex, yp, B.LORA_BF16, T)
+        torch.cuda.synchronize()
+        assert torch.equal(yp, y[pt])
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_host_entry_equals_device_path(B):
+    cfg = _mid_cfg()
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        T = b.n_rows
+        y_dev = _run_multi(B, s, cfg, b, [0, 1])
+        xh = [U.x_dev(B, cfg, i, T).cpu().pin_memory() for i in range(2)]
+        yh = [U.y0_dev(B, cfg, i, T).cpu().pin_memory() for i in range(2)]
+        B.lora_apply_multi_host(s, [0, 1], xh, b.adapter_ids, b.expert_ids, yh, B.LORA_BF16, T)
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(yh[i], y_dev[i].cpu())
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_out_of_range_ids_flagged_and_skipped(B):
+    cfg = _mid_cfg(T=64)
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        T = b.n_rows
+        a = b.adapter_ids.copy()
+        a[3] = cfg.n_adapters + 5
+        e = b.expert_ids.copy()
+        e[7] = 9
+        x = U.x_dev(B, cfg, 0, T)
+        y = U.y0_dev(B, cfg, 0, T)
+        y0 = y.clone()
+        B.lora_apply(s, 0, x, torch.from_numpy(a).to(U.DEV), torch.from_numpy(e).to(U.DEV), y, B.LORA_BF16, T)
+        assert B.lora_server_check(s) == B.LORA_ERR_ID_OUT_OF_RANGE
+        assert B.lora_server_check(s) == B.LORA_OK        # flag cleared
+        assert torch.equal(y[3], y0[3]) and torch.equal(y[7], y0[7])
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_argument_errors_enqueue_nothing(B):
+    cfg = _mid_cfg(T=64)
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        T = b.n_rows
+        ad, ex = U.ids_dev(b)
+        x = U.x_dev(B, cfg, 0, T)
+        y = U.y0_dev(B, cfg, 0, T)
+        y0 = y.clone()
+        with pytest.raises(B.LoraError) as ei:
+            B.lora_apply(s, 5, x, ad, ex, y, B.LORA_BF16, T)
+        assert ei.value.status == B.LORA_ERR_INVALID_ARG
+        with pytest.raises(B.LoraError):
+            B.lora_apply(s, 0, x, ad, ex, y, B.LORA_BF16, 10 ** 6)
+        p = B.lora_plan_create(s, T)
+        B.lora_plan_build(s, p, ad, ex, T, 2)          # E mismatch with the slot (E=4)
+        with pytest.raises(B.LoraError):
+            B.lora_apply_plan(s, p, 0, x, y, B.LORA_BF16)
+        with pytest.raises(B.LoraError):                 # x / y overlap
+            B.lora_apply_plan_multi(s, p, [0], [y], [y], B.LORA_BF16)
+        B.lora_plan_destroy(p)
+        B.lora_apply(s, 0, x, ad, ex, y, B.LORA_BF16, 0)  # T = 0: no-op
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0)
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_sharded_loopback_g1_bit_exact(B):
+    cfg = _mid_cfg()
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    T = b.n_rows
+    c = B.make_config([sl.h_in for sl in cfg.slots], [sl.h_out for sl in cfg.slots],
+                      [sl.n_experts for sl in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), T, 0)
+    uid = B.lora_nccl_unique_id()
+    sh = B.lora_server_create_sharded(c, 0, 1, uid)
+    try:
+        B.lora_server_fill_synthetic(sh, cfg.seed)
+        y_ref = _run_multi(B, s, cfg, b, [0, 1])
+        ad, ex = U.ids_dev(b)
+        xs = [U.x_dev(B, cfg, i, T) for i in range(2)]
+        ys = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        B.lora_apply_sharded(sh, [0, 1], xs, ad, ex, ys, B.LORA_BF16, T)
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(ys[i], y_ref[i])
+    finally:
+        B.lora_server_destroy(sh)
+        B.lora_server_destroy(s)

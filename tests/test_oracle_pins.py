@@ -280,6 +280,18 @@ def test_generated_values_exact_and_bounded():
     assert abs(f.std() * np.sqrt(256) - 0.577) < 0.2
 
 
+def test_c_generator_matches_numpy_generator():
+    units = np.array([0, 5, 4095, 123456], np.uint64)
+    A = li.units_A_bits(77, 2, units, 192, 16)
+    Bm = li.units_B_bits(77, 2, units, 16, 320)
+    for i, u in enumerate(units):
+        np.testing.assert_array_equal(A[i], li.unit_A_bits(77, 2, int(u), 192, 16))
+        np.testing.assert_array_equal(Bm[i], li.unit_B_bits(77, 2, int(u), 16, 320))
+    rows = np.array([3, 0, 999999])
+    np.testing.assert_array_equal(li.gen_rows_fast(5, li.tag_of(li.KIND_X, 1), rows, 256, li.shift_x()),
+                                  li.x_rows_bits(5, 1, rows, 256))
+
+
 def test_zipf_and_experts():
     cfg = li.CONFIGS["mixtral_decode"]
     b = li.make_batch(li.with_tokens(cfg, 20000))
