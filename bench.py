@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: multi-LoRA delta tokens/s (InfiniLoRA LoRA-Server hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+One *step* = one pass of the whole hot path over one batch: a1 segmentation
+(lora_plan_build) + a2-a4 for every slot of the unit of work (gate, up, down
+of one Mixtral MoE layer, multi-slot apply).  Default workload: BASELINE.json
+config 5 (mixtral_sharded: 2048 adapters, 4096 tokens -> 8192 rows), the
+config the metric is quoted on at 1/2/4/8 GPUs; it fits one B200 (116 GB of
+weights).  N=1 runs the unsharded server; N>1 runs the adapter-sharded server
+(owner(a) = a mod N, NCCL all-to-all over NVLink), launched by torchrun.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import lora_inputs as li  # noqa: E402
+
+METRIC = "multi-LoRA delta tokens/s at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+UNIT = "tokens/s"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1660.1)), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+# ---------------------------------------------------------------------------
+def algorithmic(cfg: li.Config, batch: li.Batch, slots):
+    a = batch.adapter_ids.astype(np.int64)
+    valid = a >= 0
+    T, Tv = batch.n_rows, int(valid.sum())
+    ysz = 4 if cfg.y_dtype == "fp32" else 2
+    r = cfg.rank
+    out = {"segment": T * 8, "shrink": 0, "expand": 0, "flops": 0, "units": {}}
+    for i in slots:
+        sl = cfg.slots[i]
+        U = int(np.unique(a[valid] * sl.n_experts + batch.expert_ids[valid]).size)
+        out["units"][sl.name] = U
+        out["shrink"] += U * sl.h_in * r * 2 + Tv * sl.h_in * 2
+        out["expand"] += U * sl.h_out * r * 2 + Tv * sl.h_out * 2 * ysz
+        out["flops"] += 2 * Tv * r * (sl.h_in + sl.h_out)
+    out["total"] = out["segment"] + out["shrink"] + out["expand"]
+    out["rows_valid"] = Tv
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for l in self.lines:
+            p = [v.strip() for v in l.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (rank 0, N=1 only) and the --impl reference arm
+# ---------------------------------------------------------------------------
+def oracle_sample(cfg, batch, slots, n_tokens):
+    """Prepared oracle inputs for the first n_tokens tokens (all slots)."""
+    from oracle import oracle as orc
+    rows = np.arange(n_tokens * batch.top_k)
+    return [orc.prepare_slot(cfg, i, batch, rows) for i in slots]
+
+
+def oracle_time(prepared):
+    from oracle import oracle as orc
+    t0 = time.perf_counter()
+    for (x, uor, sor, A, B, y) in prepared:
+        orc.lora_apply_rows(x, uor, sor, A, B, y.copy())
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, batch, slots, budget_s=10.0):
+    """Grow the token sample until one oracle pass costs ~budget_s (or the batch ends)."""
+    from oracle import oracle as orc
+    n = 16
+    best = None
+    while True:
+        prep = oracle_sample(cfg, batch, slots, n)
+        dt = oracle_time(prep)
+        best = (n, dt)
+        if dt >= budget_s / 4 or n >= batch.n_tokens:
+            break
+        n = min(batch.n_tokens, max(n * 2, int(n * (budget_s / 4) / max(dt, 1e-3))))
+    n, dt = best
+    return {"value": n / dt, "unit": UNIT, "cores": orc.max_threads(), "kind": "oracle",
+            "sample": f"first {n} of {batch.n_tokens} tokens ({n * batch.top_k} rows) of the {cfg.name} batch, "
+                      f"{len(slots)} slots; plain-C fp64 oracle, OpenMP over rows; input generation excluded; "
+                      f"one pass = {dt:.2f} s"}
+
+
+def run_reference(args, cfg, batch, slots):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    # size one step at ~0.2 s of oracle compute
+    n = 8
+    while True:
+        prep = oracle_sample(cfg, batch, slots, n)
+        dt = oracle_time(prep)
+        if dt >= 0.2 or n >= batch.n_tokens:
+            break
+        n = min(batch.n_tokens, n * 2)
+    for _ in range(args.warmup):
+        oracle_time(prep)
+    times = [oracle_time(prep) for _ in range(args.steps)]
+    ms = 1e3 * float(np.mean(times))
+    value = n / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg.name, "global_batch": cfg.n_tokens, "sample_tokens": n,
+                       "rows": n * batch.top_k, "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc.max_threads(), "kind": "oracle",
+                             "sample": f"first {n} of {cfg.n_tokens} tokens of {cfg.name}, {len(slots)} slots, "
+                                       f"input generation excluded"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg, batch, slots):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_07173_b200 import binding as B
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    k = batch.top_k
+    T_glob = batch.n_rows
+    t0, t1 = (cfg.n_tokens * rank) // world, (cfg.n_tokens * (rank + 1)) // world
+    r0, r1 = t0 * k, t1 * k
+    T = r1 - r0
+    E = cfg.slots[slots[0]].n_experts
+    dt_code = B.LORA_FP32 if cfg.y_dtype == "fp32" else B.LORA_BF16
+    ysz = 4 if cfg.y_dtype == "fp32" else 2
+
+    c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots],
+                      [s.n_experts for s in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), max(T, 1), local)
+    if world > 1:
+        uid = [B.lora_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        s = B.lora_server_create_sharded(c, rank, world, uid[0])
+    else:
+        s = B.lora_server_create(c)
+    B.lora_server_fill_synthetic(s, cfg.seed, stream)
+
+    # device-resident inputs (this rank's rows, global row ids for the generator)
+    xs = {}
+    for i in slots:
+        sl = cfg.slots[i]
+        if sl.xbuf not in xs:
+            x = torch.empty((T, sl.h_in), dtype=torch.int16, device=dev)
+            B.lora_synth_fill_rows(x, T, sl.h_in, cfg.seed, li.tag_of(li.KIND_X, sl.xbuf), li.shift_x(), r0, stream)
+            xs[sl.xbuf] = x
+    x_list = [xs[cfg.slots[i].xbuf] for i in slots]
+    ys = []
+    for i in slots:
+        sl = cfg.slots[i]
+        y = torch.empty((T, sl.h_out), dtype=torch.int16, device=dev)
+        B.lora_synth_fill_rows(y, T, sl.h_out, cfg.seed, li.tag_of(li.KIND_Y0, i), li.shift_y0(), r0, stream)
+        if ysz == 4:
+            y = ((y.to(torch.int32) << 16).view(torch.float32)).contiguous()
+        ys.append(y)
+    ad = torch.from_numpy(batch.adapter_ids[r0:r1].copy()).to(dev)
+    ex = torch.from_numpy(batch.expert_ids[r0:r1].copy()).to(dev)
+    plan = B.lora_plan_create(s, max(T, 1)) if world == 1 else None
+
+    def step():
+        if world == 1:
+            B.lora_plan_build(s, plan, ad, ex if E > 1 else None, T, E, stream)
+            B.lora_apply_plan_multi(s, plan, slots, x_list, ys, dt_code, stream)
+        else:
+            B.lora_apply_sharded(s, slots, x_list, ad, ex if E > 1 else None, ys, dt_code, T, stream)
+
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    B.lora_profile_enable(s, args.steps * 8 + 16)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    prof = B.lora_profile_read(s)
+    B.lora_profile_enable(s, 0)
+    ms = ms_local
+    if world > 1:
+        tms = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        ms = float(tms.item())
+    value = cfg.n_tokens / (ms / 1e3)
+
+    # e2e through the C-ABI with host buffers (N=1: lora_apply_multi_host)
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        xh = {xb: xs[xb].cpu().pin_memory() for xb in xs}
+        xh_list = [xh[cfg.slots[i].xbuf] for i in slots]
+        yh = [y.cpu().pin_memory() for y in ys]
+        adh = batch.adapter_ids.copy()
+        exh = batch.expert_ids.copy()
+        h2d = adh.nbytes + (exh.nbytes if E > 1 else 0) + sum(v.numel() * 2 for v in xh.values()) + \
+            sum(y.numel() * ysz for y in yh)
+        d2h = sum(y.numel() * ysz for y in yh)
+        B.lora_apply_multi_host(s, slots, xh_list, adh, exh if E > 1 else None, yh, dt_code, T, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            B.lora_apply_multi_host(s, slots, xh_list, adh, exh if E > 1 else None, yh, dt_code, T, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        e2e = {"value": cfg.n_tokens / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems, "api": "lora_apply_multi_host (pinned host)"}
+
+    if rank != 0:
+        B.lora_server_destroy(s)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    hbm_peak, tc_peak, peak_src = load_peaks()
+    alg = algorithmic(cfg, batch, slots)
+    kern = {}
+    for name, (n, tot) in prof.items():
+        kern[name] = {"launches": n, "ms_per_launch": tot / n, "ms_per_step": tot / args.steps}
+    # dominant kernel: most device time per step; algorithmic bytes per launch
+    per_kind_bytes = {"simt_shrink": alg["shrink"], "simt_expand": alg["expand"], "segment": alg["segment"]}
+    roofline = None
+    if kern and world == 1:
+        dom = max(kern, key=lambda n: kern[n]["ms_per_step"])
+        bytes_per_launch = per_kind_bytes.get(dom, 0) * args.steps / kern[dom]["launches"]
+        achieved = bytes_per_launch / (kern[dom]["ms_per_launch"] * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(cfg.name, {}).get(dom)
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom,
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
+                    "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS}
+        for n in kern:
+            b = per_kind_bytes.get(n)
+            if b:
+                kern[n]["algorithmic_GBs"] = b * args.steps / kern[n]["launches"] / (kern[n]["ms_per_launch"] * 1e-3) / 1e9
+    launches = sum(v["launches"] for v in kern.values())
+    step_gbs = alg["total"] / (ms * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (counter-hash weights/activations, Zipf(1.2) adapter ids, top-2 uniform experts)",
+            "config": {"workload": cfg.name, "global_batch": cfg.n_tokens, "rows": T_glob, "slots": len(slots),
+                       "rank": cfg.rank, "adapters": cfg.n_adapters,
+                       "parallelism": f"adapter-sharded dp{world} (NCCL all-to-all)" if world > 1 else "single GPU",
+                       "l2": f"inputs larger than L2 ({alg['total'] / 1e9:.1f} GB touched per step)"},
+            "e2e": e2e,
+            "gpu_launches": launches if world == 1 else None,
+            "roofline": roofline,
+            "step_hbm": {"algorithmic_GB": alg["total"] / 1e9, "achieved_GBs": step_gbs,
+                         "frac_measured": step_gbs / hbm_peak, "frac_nominal_8TBs": step_gbs / NOMINAL_HBM_GBS,
+                         "tflops": alg["flops"] / (ms * 1e-3) / 1e12},
+            "kernels": kern,
+            "clocks": clk.summary()}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg, batch, slots, args.cpu_seconds)
+        except Exception as e:  # the baseline is a report, never the product path
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    print(json.dumps(line), flush=True)
+    B.lora_server_destroy(s)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="mixtral_sharded", choices=sorted(li.CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = li.CONFIGS[args.workload]
+    batch = li.make_batch(cfg)
+    slots = list(range(len(cfg.slots)))
+    if args.impl == "reference":
+        return run_reference(args, cfg, batch, slots)
+    return run_ours(args, cfg, batch, slots)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

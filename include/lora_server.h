@@ -142,6 +142,11 @@ lora_status_t lora_plan_build(lora_server_t *s, lora_plan_t *p, const int32_t *a
 lora_status_t lora_plan_export(const lora_plan_t *p, int32_t *perm, int32_t *seg_offsets,
                                int32_t *seg_keys, int32_t *n_valid, int32_t *n_segs, void *stream);
 
+/* Work-list sizes of the last build (host ints, synchronises `stream`):
+ * out[0] valid rows, out[1] segments, out[2] CUDA-core row groups (<= 8 rows),
+ * out[3] tcgen05 row tiles (<= 128 rows). */
+lora_status_t lora_plan_stats(const lora_plan_t *p, int32_t *out4, void *stream);
+
 /* ------------------------------------------------------------------------- */
 /* Apply: a2 shrink, a3 expand, a4 scatter-accumulate                          */
 /* ------------------------------------------------------------------------- */

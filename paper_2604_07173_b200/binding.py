@@ -53,6 +53,7 @@ SIGNATURES = {
     "lora_plan_destroy": (ctypes.c_int, [_vp]),
     "lora_plan_build": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp]),
     "lora_plan_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _pi32, _pi32, _vp]),
+    "lora_plan_stats": (ctypes.c_int, [_vp, _pi32, _vp]),
     "lora_apply_plan": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, ctypes.c_int, _vp]),
     "lora_apply_plan_multi": (ctypes.c_int, [_vp, _vp, _i32, _pi32, _pp, _pp, ctypes.c_int, _vp]),
     "lora_apply": (ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_int, _i32, _vp]),
@@ -179,6 +180,13 @@ def lora_plan_export(s: int, p: int, perm, seg_offsets, seg_keys, stream=None):
     _check(lib.lora_plan_export(p, _ptr(perm), _ptr(seg_offsets), _ptr(seg_keys), ctypes.byref(nv),
                                 ctypes.byref(ns), _stream(stream)), s)
     return nv.value, ns.value
+
+
+def lora_plan_stats(s: int, p: int, stream=None):
+    """-> (n_valid, n_segs, n_groups, n_tiles)"""
+    out = (ctypes.c_int32 * 4)()
+    _check(lib.lora_plan_stats(p, out, _stream(stream)), s)
+    return tuple(out)
 
 
 def lora_apply_plan(s: int, p: int, slot: int, x, y, y_dtype: int, stream=None):

@@ -347,7 +347,13 @@ void plan_destroy_impl(lora_plan* p) {
   delete p;
 }
 
-static bool tc_enabled(const lora_server* s) { return tc_available() && s->r == 64 && s->small_seg_max >= 0; }
+// tcgen05 path: rank 64, every slot's item widths multiples of the 128-wide MMA tiles
+static bool tc_enabled(const lora_server* s) {
+  if (!tc_available() || s->r != 64 || s->small_seg_max < 0) return false;
+  for (const auto& sl : s->slots)
+    if (sl.KI % 128 || sl.CI % 128) return false;
+  return true;
+}
 
 lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapter_ids, const int32_t* expert_ids,
                               int T, int E, cudaStream_t st) {
@@ -511,6 +517,21 @@ extern "C" lora_status_t lora_plan_export(const lora_plan_t* p, int32_t* perm, i
   if (seg_keys && cnt[kCntSegs] > 0)
     CK(s, cudaMemcpyAsync(seg_keys, p->dev.seg_key, sizeof(int32_t) * cnt[kCntSegs], cudaMemcpyDeviceToDevice, st));
   CK(s, cudaStreamSynchronize(st));
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_plan_stats(const lora_plan_t* p, int32_t* out4, void* stream) {
+  if (!p || !out4) return fail(nullptr, LORA_ERR_INVALID_ARG, "NULL argument");
+  lora_server* s = p->s;
+  CK(s, cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t cnt[kCntWords];
+  CK(s, cudaMemcpyAsync(cnt, p->dev.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+  CK(s, cudaStreamSynchronize(st));
+  out4[0] = cnt[kCntValid];
+  out4[1] = cnt[kCntSegs];
+  out4[2] = cnt[kCntGroups];
+  out4[3] = cnt[kCntTiles];
   return LORA_OK;
 }
 

@@ -1,10 +1,582 @@
-// tc05.cu -- tcgen05/TMEM kernels for large segments (placeholder until the
-// tensor-core path lands; tc_available() keeps the dispatcher on CUDA cores).
+// tc05.cu -- a2 shrink and a3+a4 expand on the 5th-generation tensor cores
+// (tcgen05.mma, accumulators in TMEM) for LARGE segments.
+//
+// A segment with more than `small_seg_max` rows of one unit is a real dense
+// contraction (prefill: 474-893 rows per unit; decode: the Zipf head).  The
+// paper's SGMV "aggregat[es] tokens that share the same LoRA adapter into a
+// single GEMM" on Hopper wgmma with swap-AB; here it is
+// tcgen05 with one elected issuing thread, TMEM accumulators and mbarrier
+// pipelines:
+//
+//   shrink item (task, kc, tile<=128 rows):
+//       D[128 rows x 64] (TMEM, fp32) = X_tile[128 x KI] . A_u[KI x 64]
+//       A operand = gathered activation rows (cp.async, manual 128B swizzle)
+//       B operand = pre-swizzled At store tiles (1-D TMA bulk copy)
+//       epilogue: TMEM -> regs -> vpart[kc][row][0:64] (fp32 partial sums)
+//   expand item (task, ci, tile<=128 rows), swap-AB so TMEM lanes = columns:
+//       D[128 cols x N rows] = Bt[128 cols x 64] . v^T[64 x N]   (per 128-col sub-tile)
+//       A operand = pre-swizzled Bt store rows (1-D TMA bulk copy)
+//       B operand = v tile (sum of vpart over kc, rounded to bf16, swizzled)
+//       epilogue: TMEM -> regs -> y[perm[n]][c] = round(y + s_a * D)  (coalesced over c)
+//
+// UMMA operands are K-major SWIZZLE_128B (rows of 128 B, 8-row groups 1024 B
+// apart); the instruction descriptor selects bf16 x bf16 -> fp32.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace lora {
-bool tc_available() { return false; }
-cudaError_t launch_tc_shrink(const MultiArgs&, const PlanDev&, int, cudaStream_t) { return cudaSuccess; }
-cudaError_t launch_tc_expand(const MultiArgs&, const PlanDev&, int, cudaStream_t) { return cudaSuccess; }
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// tcgen05 PTX wrappers
+// ---------------------------------------------------------------------------
+LORA_DEVINL void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+LORA_DEVINL void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+LORA_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+LORA_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] . B[smem]; bf16 inputs, fp32 accumulate
+LORA_DEVINL void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
+LORA_DEVINL void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns -> 16 registers
+LORA_DEVINL void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 format)
+LORA_DEVINL uint64_t sw128_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                            // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                  // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: bf16 x bf16 -> fp32, both K-major, shape M x N
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+LORA_DEVINL void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+LORA_DEVINL uint8_t* align1024(uint8_t* p) {
+  const uint32_t a = smem_u32(p);
+  return p + (((a + 1023u) & ~1023u) - a);
+}
+
+LORA_DEVINL int find_task_kc(const MultiArgs& args, int g) {
+  int t = 0;
+  while (t + 1 < args.n_tasks && args.t[t + 1].kc_base <= g) ++t;
+  return t;
+}
+LORA_DEVINL int find_task_ci(const MultiArgs& args, int g) {
+  int t = 0;
+  while (t + 1 < args.n_tasks && args.t[t + 1].ci_base <= g) ++t;
+  return t;
+}
+LORA_DEVINL long long unit_of_key(int key, int E, int world) {
+  const int a = key / E, e = key - a * E;
+  return (long long)(a / world) * E + e;
+}
+
+constexpr int R = 64;  // tcgen05 path rank
+
+// ===========================================================================
+// shrink
+// ===========================================================================
+struct ShrinkCfg {
+  static constexpr int EPI_WARPS = 4;   // warps 0-3: epilogue (TMEM lanes 0-127)
+  static constexpr int MMA_WARP = 4;    // warp 4: TMEM alloc + MMA issue
+  static constexpr int PROD_WARP0 = 5;  // warps 5-8: activation gather (+ weight bulk copy)
+  static constexpr int PROD_THREADS = 128;
+  static constexpr int THREADS = 9 * 32;
+  static constexpr int KSTEP = 64;                         // K per SW128 atom
+  static constexpr int KS_PER_STAGE = 2;                   // k-steps per stage
+  static constexpr int X_SUB = kTileRows * 128;            // 16 KB per k-step
+  static constexpr int W_SUB = R * 128;                    // 8 KB per k-step
+  static constexpr int STAGE = KS_PER_STAGE * (X_SUB + W_SUB);
+  static constexpr int NST = 4;
+  static constexpr int LAG = 2;                            // cp.async groups kept in flight
+  static constexpr int ACC_COLS = 64;                      // N = r
+  static constexpr int TMEM_COLS = 128;                    // 2 accumulators
+  static constexpr int SMEM = 1024 + NST * STAGE + 256;
+};
+
+__global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
+    tc_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
+  using C = ShrinkCfg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::NST * C::STAGE);
+  uint64_t* full = bars;                  // [NST]  producers -> MMA
+  uint64_t* empty = bars + C::NST;        // [NST]  MMA commit -> producers
+  uint64_t* tfull = bars + 2 * C::NST;    // [2]    MMA commit -> epilogue
+  uint64_t* tempty = tfull + 2;           // [2]    epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(&full[s], C::PROD_THREADS + 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], C::EPI_WARPS * 32);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int n_tiles = pd.counts[kCntTiles];
+  const long long n_items = (long long)n_tiles * args.total_kc;
+
+  if (warp >= C::PROD_WARP0) {
+    // ===================== producers: gather X rows, bulk-copy W =====================
+    const int pt = threadIdx.x - C::PROD_WARP0 * 32;  // 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    int pend_stage[C::LAG + 1];
+    int npend = 0;
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int kcg = (int)(it / n_tiles), ti = (int)(it - (long long)kcg * n_tiles);
+      const SlotTask& t = args.t[find_task_kc(args, kcg)];
+      const int kc = kcg - t.kc_base;
+      const int4 tile = pd.tiles[ti];
+      const long long unit = unit_of_key(tile.z, t.E, args.world);
+      const uint16_t* wbase = t.At + (unit * (t.h_in >> 6) + ((kc * t.KI) >> 6)) * (long long)(R * 64);
+      // this thread's rows / chunks: 128 rows x 8 chunks per k-step, 1024 copies / 128 threads
+      const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
+      for (int st = 0; st < n_st; ++st) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sbase = smem + stage * C::STAGE;
+        if (pt == 0) {
+          mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
+          bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB,
+                   wbase + (long long)st * C::KS_PER_STAGE * (R * 64), C::KS_PER_STAGE * C::W_SUB, &full[stage]);
+        }
+        const long long j0 = (long long)kc * t.KI + (long long)st * C::KS_PER_STAGE * C::KSTEP;
+#pragma unroll
+        for (int ks = 0; ks < C::KS_PER_STAGE; ++ks) {
+          uint8_t* xs = sbase + ks * C::X_SUB;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int idx = pt + i * C::PROD_THREADS;  // 0..1023
+            const int n = idx >> 3, q = idx & 7;
+            const bool valid = n < tile.y;
+            const long long row = valid ? pd.perm[tile.x + n] : 0;
+            const uint16_t* src = t.x + row * t.h_in + j0 + ks * C::KSTEP + q * 8;
+            cp_async16(xs + n * 128 + ((q ^ (n & 7)) << 4), src, valid ? 16u : 0u);
+          }
+        }
+        cp_async_commit();
+        pend_stage[npend++] = stage;
+        if (npend > C::LAG) {
+          cp_async_wait<C::LAG>();
+          fence_proxy_async_smem();
+          mbar_arrive(&full[pend_stage[0]]);
+          for (int q = 0; q < npend - 1; ++q) pend_stage[q] = pend_stage[q + 1];
+          --npend;
+        }
+        if (++stage == C::NST) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    for (int q = 0; q < npend; ++q) mbar_arrive(&full[pend_stage[q]]);
+  } else if (warp == C::MMA_WARP) {
+    // ===================== MMA issuer =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    constexpr uint32_t idesc = idesc_bf16(128, C::ACC_COLS);
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int kcg = (int)(it / n_tiles);
+      const SlotTask& t = args.t[find_task_kc(args, kcg)];
+      const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
+      for (int st = 0; st < n_st; ++st) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sbase = smem_u32(smem + stage * C::STAGE);
+#pragma unroll
+          for (int ks = 0; ks < C::KS_PER_STAGE; ++ks) {
+            const uint32_t xa = sbase + ks * C::X_SUB;
+            const uint32_t wa = sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::W_SUB;
+#pragma unroll
+            for (int k = 0; k < C::KSTEP / 16; ++k) {
+              umma_bf16(d_tmem, sw128_desc(xa + k * 32), sw128_desc(wa + k * 32), idesc,
+                        (st > 0 || ks > 0 || k > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty[stage]);
+          if (st == n_st - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == C::NST) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue: TMEM -> vpart =====================
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int row_in_tile = warp * 32 + lane;  // TMEM lane
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int kcg = (int)(it / n_tiles), ti = (int)(it - (long long)kcg * n_tiles);
+      const SlotTask& t = args.t[find_task_kc(args, kcg)];
+      const int kc = kcg - t.kc_base;
+      const int4 tile = pd.tiles[ti];
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      float v[C::ACC_COLS];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS;
+#pragma unroll
+      for (int c = 0; c < C::ACC_COLS; c += 16) tmem_ld16(taddr + c, v + c);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (row_in_tile < tile.y) {
+        float4* dst = reinterpret_cast<float4*>(pd.vpart + t.vpart_off +
+                                                ((long long)kc * pd.max_rows + tile.x + row_in_tile) * R);
+#pragma unroll
+        for (int c = 0; c < C::ACC_COLS / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ===========================================================================
+// expand (swap-AB)
+// ===========================================================================
+struct ExpandCfg {
+  static constexpr int EPI_WARPS = 4;   // warps 0-3: epilogue (TMEM lane = output column)
+  static constexpr int TMA_WARP = 4;    // warp 4: Bt bulk copies
+  static constexpr int MMA_WARP = 5;    // warp 5: TMEM alloc + MMA
+  static constexpr int VB_WARP0 = 6;    // warps 6-9: v-tile builders
+  static constexpr int VB_THREADS = 128;
+  static constexpr int THREADS = 10 * 32;
+  static constexpr int MSUB = 128;                     // output columns per MMA (M)
+  static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
+  static constexpr int NST = 6;
+  static constexpr int V_TILE = kTileRows * 128;       // 16 KB (N <= 128 rows x 64 bf16)
+  static constexpr int NACC = 2;
+  static constexpr int ACC_COLS = kTileRows;           // N columns per accumulator
+  static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 256
+  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 2048;
+};
+
+__global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
+    tc_expand_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
+  using C = ExpandCfg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* vtile = smem + C::NST * C::B_SUB;  // [2][V_TILE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vtile + 2 * C::V_TILE);
+  uint64_t* full = bars;                      // [NST] Bt landed
+  uint64_t* empty = bars + C::NST;            // [NST] MMA done with Bt stage
+  uint64_t* vfull = bars + 2 * C::NST;        // [2]  v tile built
+  uint64_t* vempty = vfull + 2;               // [2]  MMA done with v tile
+  uint64_t* tfull = vempty + 2;               // [2]  accumulator ready
+  uint64_t* tempty = tfull + 2;               // [2]  accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* rowtab = reinterpret_cast<int*>(tmem_slot + 4);  // [2][kTileRows] y row offsets / h_out
+
+  const int warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&vfull[a], C::VB_THREADS);
+      mbar_init(&vempty[a], 1 + C::EPI_WARPS * 32);  // MMA commit + every epilogue thread
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], C::EPI_WARPS * 32);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int n_tiles = pd.counts[kCntTiles];
+  const long long n_items = (long long)n_tiles * args.total_ci;
+
+  if (warp == C::TMA_WARP) {
+    // ===================== Bt producer =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
+        const SlotTask& t = args.t[find_task_ci(args, cig)];
+        const int ci = cig - t.ci_base;
+        const int4 tile = pd.tiles[ti];
+        const long long unit = unit_of_key(tile.z, t.E, args.world);
+        const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
+        const int n_sub = t.CI / C::MSUB;
+        for (int sb = 0; sb < n_sub; ++sb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::B_SUB);
+          bulk_g2s_hint(smem + stage * C::B_SUB, bbase + (long long)sb * C::MSUB * R, C::B_SUB, &full[stage], pol);
+          if (++stage == C::NST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= C::VB_WARP0) {
+    // ===================== v-tile builders =====================
+    const int vt = threadIdx.x - C::VB_WARP0 * 32;  // 0..127
+    int vb = 0;
+    uint32_t vphase = 0;
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
+      const SlotTask& t = args.t[find_task_ci(args, cig)];
+      const int4 tile = pd.tiles[ti];
+      const int npad = (tile.y + 15) & ~15;
+      mbar_wait(&vempty[vb], vphase ^ 1);
+      uint8_t* vs = vtile + vb * C::V_TILE;
+      const float* vp = pd.vpart + t.vpart_off + (long long)tile.x * R;
+      const long long kstride = (long long)pd.max_rows * R;
+      for (int idx = vt; idx < npad * 8; idx += C::VB_THREADS) {
+        const int n = idx >> 3, q = idx & 7;
+        uint4 w = make_uint4(0, 0, 0, 0);
+        if (n < tile.y) {
+          float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int kc = 0; kc < t.n_kc; ++kc) {
+            const float4* src = reinterpret_cast<const float4*>(vp + kc * kstride + n * R + q * 8);
+            const float4 a = src[0], b = src[1];
+            s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+            s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+          }
+          w.x = f32_to_bf16_rne(s[0]) | ((uint32_t)f32_to_bf16_rne(s[1]) << 16);
+          w.y = f32_to_bf16_rne(s[2]) | ((uint32_t)f32_to_bf16_rne(s[3]) << 16);
+          w.z = f32_to_bf16_rne(s[4]) | ((uint32_t)f32_to_bf16_rne(s[5]) << 16);
+          w.w = f32_to_bf16_rne(s[6]) | ((uint32_t)f32_to_bf16_rne(s[7]) << 16);
+        }
+        *reinterpret_cast<uint4*>(vs + n * 128 + ((q ^ (n & 7)) << 4)) = w;
+      }
+      // y row offsets for the epilogue
+      for (int n = vt; n < kTileRows; n += C::VB_THREADS)
+        rowtab[vb * kTileRows + n] = n < tile.y ? pd.perm[tile.x + n] : 0;
+      fence_proxy_async_smem();
+      mbar_arrive(&vfull[vb]);
+      if (++vb == 2) {
+        vb = 0;
+        vphase ^= 1;
+      }
+    }
+  } else if (warp == C::MMA_WARP) {
+    // ===================== MMA issuer =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int vb = 0;
+    uint32_t vphase = 0;
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
+      const SlotTask& t = args.t[find_task_ci(args, cig)];
+      const int4 tile = pd.tiles[ti];
+      const int npad = (tile.y + 15) & ~15;
+      const uint32_t idesc = idesc_bf16(C::MSUB, npad);
+      const int n_sub = t.CI / C::MSUB;
+      mbar_wait(&vfull[vb], vphase);
+      const uint32_t va = smem_u32(vtile + vb * C::V_TILE);
+      for (int sb = 0; sb < n_sub; ++sb) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ba = smem_u32(smem + stage * C::B_SUB);
+          const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
+#pragma unroll
+          for (int k = 0; k < R / 16; ++k)
+            umma_bf16(d_tmem, sw128_desc(ba + k * 32), sw128_desc(va + k * 32), idesc, k > 0 ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          umma_commit(&tfull[acc]);
+          if (sb == n_sub - 1) umma_commit(&vempty[vb]);
+        }
+        __syncwarp();
+        if (++stage == C::NST) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++acc == C::NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      if (++vb == 2) {
+        vb = 0;
+        vphase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue: y[perm[n]][c] += s_a * D[c][n] =====================
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int vb = 0;
+    uint32_t vphase = 0;
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
+      const SlotTask& t = args.t[find_task_ci(args, cig)];
+      const int ci = cig - t.ci_base;
+      const int4 tile = pd.tiles[ti];
+      const float s_a = args.scale[tile.z / t.E];
+      const int n_sub = t.CI / C::MSUB;
+      // the row table of this item's v buffer is valid once vfull completed (MMA waited on it too)
+      mbar_wait(&vfull[vb], vphase);
+      const int* rows = rowtab + vb * kTileRows;
+      for (int sb = 0; sb < n_sub; ++sb) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const long long c = (long long)ci * t.CI + (long long)sb * C::MSUB + warp * 32 + lane;
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS;
+        for (int n0 = 0; n0 < tile.y; n0 += 16) {
+          float d[16];
+          tmem_ld16(taddr + n0, d);
+          const int nn = min(16, tile.y - n0);
+          if (args.y_store) {
+            float* y = reinterpret_cast<float*>(t.y);
+            for (int j = 0; j < nn; ++j) y[(long long)rows[n0 + j] * t.h_out + c] = s_a * d[j];
+          } else if (args.y_fp32) {
+            float* y = reinterpret_cast<float*>(t.y);
+            float old[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nn) old[j] = y[(long long)rows[n0 + j] * t.h_out + c];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nn) y[(long long)rows[n0 + j] * t.h_out + c] = old[j] + s_a * d[j];
+          } else {
+            uint16_t* y = reinterpret_cast<uint16_t*>(t.y);
+            uint16_t old[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nn) old[j] = y[(long long)rows[n0 + j] * t.h_out + c];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nn) y[(long long)rows[n0 + j] * t.h_out + c] = f32_to_bf16_rne(bf16_to_f32(old[j]) + s_a * d[j]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == C::NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      mbar_arrive(&vempty[vb]);  // done with this item's row table
+      if (++vb == 2) {
+        vb = 0;
+        vphase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <typename K>
+cudaError_t set_smem_once(K kernel, int bytes, unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(mask & (1ull << dev))) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    mask |= 1ull << dev;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+bool tc_available() { return true; }
+
+cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
+  static unsigned long long mask = 0;
+  cudaError_t e = set_smem_once(tc_shrink_kernel, ShrinkCfg::SMEM, mask);
+  if (e != cudaSuccess) return e;
+  tc_shrink_kernel<<<grid, ShrinkCfg::THREADS, ShrinkCfg::SMEM, stream>>>(args, pd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
+  static unsigned long long mask = 0;
+  cudaError_t e = set_smem_once(tc_expand_kernel, ExpandCfg::SMEM, mask);
+  if (e != cudaSuccess) return e;
+  tc_expand_kernel<<<grid, ExpandCfg::THREADS, ExpandCfg::SMEM, stream>>>(args, pd);
+  return cudaGetLastError();
+}
+
 }  // namespace lora

@@ -135,7 +135,7 @@ def test_fill_store_equals_loaded_weights(B, rank):
 @pytest.mark.parametrize("rank,small_max", [(8, None), (16, None), (64, -1), (64, 0), (64, 4)])
 def test_exact_integer_probes(B, rank, small_max):
     rng = np.random.default_rng(rank * 10 + (3 if small_max is None else small_max + 2))
-    E, n_ad, h_in, h_out, T = 2, 5, 64, 128, 300
+    E, n_ad, h_in, h_out, T = 2, 5, 128, 256, 300   # widths multiple of 128: tcgen05-eligible
     Ai = rng.integers(-1, 2, (n_ad * E, h_in, rank))
     Bi = rng.integers(-1, 2, (n_ad * E, rank, h_out))
     xi = rng.integers(-2, 3, (T, h_in))
@@ -152,8 +152,19 @@ def test_exact_integer_probes(B, rank, small_max):
             B.lora_server_set_small_seg_max(s, small_max)
         x = torch.from_numpy(bits(xi).view(np.int16)).to(U.DEV)
         y = torch.from_numpy(yi.copy()).to(U.DEV)
-        B.lora_apply(s, 0, x, torch.from_numpy(a).to(U.DEV), torch.from_numpy(e).to(U.DEV), y, B.LORA_FP32, T)
+        p = B.lora_plan_create(s, T)
+        B.lora_plan_build(s, p, torch.from_numpy(a).to(U.DEV), torch.from_numpy(e).to(U.DEV), T, E)
+        nv, ns, ng, nt = B.lora_plan_stats(s, p)
+        # the requested kernel path is the one that ran
+        if rank != 64 or small_max == -1:
+            assert nt == 0 and ng > 0
+        elif small_max == 0:
+            assert ng == 0 and nt > 0
+        else:
+            assert ng > 0 and nt > 0
+        B.lora_apply_plan(s, p, 0, x, y, B.LORA_FP32)
         torch.cuda.synchronize()
+        B.lora_plan_destroy(p)
         exp = yi.astype(np.float64).copy()
         for i in range(T):
             if a[i] >= 0:
