@@ -306,23 +306,25 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
 }
 
 // ===========================================================================
-// expand (swap-AB)
+// expand (swap-AB), y staged through shared memory by TMA bulk copies
 // ===========================================================================
 struct ExpandCfg {
   static constexpr int EPI_WARPS = 4;   // warps 0-3: epilogue (TMEM lane = output column)
   static constexpr int TMA_WARP = 4;    // warp 4: Bt bulk copies
   static constexpr int MMA_WARP = 5;    // warp 5: TMEM alloc + MMA
   static constexpr int VB_WARP0 = 6;    // warps 6-9: v-tile builders
+  static constexpr int YL_WARP = 10;    // warp 10: y-tile loader (bulk copies, one per row)
   static constexpr int VB_THREADS = 128;
-  static constexpr int THREADS = 10 * 32;
+  static constexpr int THREADS = 11 * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (M)
   static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
-  static constexpr int NST = 6;
+  static constexpr int NST = 3;
   static constexpr int V_TILE = kTileRows * 128;       // 16 KB (N <= 128 rows x 64 bf16)
+  static constexpr int Y_TILE = kTileRows * MSUB * 4;  // 64 KB (128 rows x 128 cols, fp32 worst case)
   static constexpr int NACC = 2;
   static constexpr int ACC_COLS = kTileRows;           // N columns per accumulator
   static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 256
-  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 2048;
+  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 2 * Y_TILE + 2048;
 };
 
 __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
@@ -330,18 +332,23 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   using C = ExpandCfg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* vtile = smem + C::NST * C::B_SUB;  // [2][V_TILE]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vtile + 2 * C::V_TILE);
-  uint64_t* full = bars;                      // [NST] Bt landed
-  uint64_t* empty = bars + C::NST;            // [NST] MMA done with Bt stage
-  uint64_t* vfull = bars + 2 * C::NST;        // [2]  v tile built
-  uint64_t* vempty = vfull + 2;               // [2]  MMA done with v tile
-  uint64_t* tfull = vempty + 2;               // [2]  accumulator ready
-  uint64_t* tempty = tfull + 2;               // [2]  accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* rowtab = reinterpret_cast<int*>(tmem_slot + 4);  // [2][kTileRows] y row offsets / h_out
+  uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE]
+  uint8_t* ytile = vtile + 2 * C::V_TILE;      // [2][Y_TILE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ytile + 2 * C::Y_TILE);
+  uint64_t* full = bars;                       // [NST] Bt landed
+  uint64_t* empty = bars + C::NST;             // [NST] MMA done with Bt stage
+  uint64_t* vfull = bars + 2 * C::NST;         // [2]  v tile + row table built
+  uint64_t* vempty = vfull + 2;                // [2]  MMA, epilogue and y loader done with the item
+  uint64_t* tfull = vempty + 2;                // [2]  accumulator ready
+  uint64_t* tempty = tfull + 2;                // [2]  accumulator drained
+  uint64_t* yfull = tempty + 2;                // [2]  y tile landed
+  uint64_t* yempty = yfull + 2;                // [2]  y tile written back (smem free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yempty + 2);
+  int* rowtab = reinterpret_cast<int*>(tmem_slot + 4);  // [2][kTileRows] y row of each tile row
 
   const int warp = warp_id(), lane = lane_id();
+  const int esz = (args.y_fp32 || args.y_store) ? 4 : 2;
+  const int rowbytes = C::MSUB * esz;          // y bytes per row per sub-tile
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(&full[s], 1);
@@ -349,9 +356,11 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&vfull[a], C::VB_THREADS);
-      mbar_init(&vempty[a], 1 + C::EPI_WARPS * 32);  // MMA commit + every epilogue thread
+      mbar_init(&vempty[a], 1 + C::EPI_WARPS * 32 + 1);
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], C::EPI_WARPS * 32);
+      mbar_init(&yfull[a], 1);
+      mbar_init(&yempty[a], C::EPI_WARPS * 32);
     }
     fence_mbar_init();
   }
@@ -389,6 +398,43 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         }
       }
     }
+  } else if (warp == C::YL_WARP) {
+    // ===================== y-tile loader =====================
+    int vb = 0, yb = 0;
+    uint32_t vphase = 0, yphase = 0;
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
+      const SlotTask& t = args.t[find_task_ci(args, cig)];
+      const int ci = cig - t.ci_base;
+      const int4 tile = pd.tiles[ti];
+      const int n_sub = t.CI / C::MSUB;
+      mbar_wait(&vfull[vb], vphase);
+      const int* rows = rowtab + vb * kTileRows;
+      for (int sb = 0; sb < n_sub; ++sb) {
+        mbar_wait(&yempty[yb], yphase ^ 1);
+        if (args.y_store) {
+          if (lane == 0) mbar_arrive(&yfull[yb]);
+        } else {
+          if (lane == 0) mbar_arrive_expect_tx(&yfull[yb], (uint32_t)(tile.y * rowbytes));
+          __syncwarp();
+          const long long c0 = (long long)ci * t.CI + (long long)sb * C::MSUB;
+          const char* ybase = static_cast<const char*>(t.y);
+          for (int n = lane; n < tile.y; n += 32)
+            bulk_g2s(ytile + yb * C::Y_TILE + n * rowbytes, ybase + ((long long)rows[n] * t.h_out + c0) * esz,
+                     rowbytes, &yfull[yb]);
+        }
+        __syncwarp();
+        if (++yb == 2) {
+          yb = 0;
+          yphase ^= 1;
+        }
+      }
+      if (lane == 0) mbar_arrive(&vempty[vb]);
+      if (++vb == 2) {
+        vb = 0;
+        vphase ^= 1;
+      }
+    }
   } else if (warp >= C::VB_WARP0) {
     // ===================== v-tile builders =====================
     const int vt = threadIdx.x - C::VB_WARP0 * 32;  // 0..127
@@ -421,7 +467,6 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         }
         *reinterpret_cast<uint4*>(vs + n * 128 + ((q ^ (n & 7)) << 4)) = w;
       }
-      // y row offsets for the epilogue
       for (int n = vt; n < kTileRows; n += C::VB_THREADS)
         rowtab[vb * kTileRows + n] = n < tile.y ? pd.perm[tile.x + n] : 0;
       fence_proxy_async_smem();
@@ -478,11 +523,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue: y[perm[n]][c] += s_a * D[c][n] =====================
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int vb = 0;
-    uint32_t vphase = 0;
+    // ===================== epilogue: y tile (smem) += s_a * D, bulk-stored back =====================
+    int acc = 0, yb = 0, vb = 0;
+    uint32_t acc_phase = 0, yphase = 0, vphase = 0;
+    const int et = threadIdx.x;  // 0..127 = output column within the sub-tile
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
       const SlotTask& t = args.t[find_task_ci(args, cig)];
@@ -490,46 +534,50 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const int4 tile = pd.tiles[ti];
       const float s_a = args.scale[tile.z / t.E];
       const int n_sub = t.CI / C::MSUB;
-      // the row table of this item's v buffer is valid once vfull completed (MMA waited on it too)
       mbar_wait(&vfull[vb], vphase);
-      const int* rows = rowtab + vb * kTileRows;
+      const int my_row = et < tile.y ? rowtab[vb * kTileRows + et] : 0;
       for (int sb = 0; sb < n_sub; ++sb) {
         mbar_wait(&tfull[acc], acc_phase);
+        mbar_wait(&yfull[yb], yphase);
         tc_fence_after();
-        const long long c = (long long)ci * t.CI + (long long)sb * C::MSUB + warp * 32 + lane;
+        uint8_t* ys = ytile + yb * C::Y_TILE;
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS;
         for (int n0 = 0; n0 < tile.y; n0 += 16) {
           float d[16];
           tmem_ld16(taddr + n0, d);
           const int nn = min(16, tile.y - n0);
           if (args.y_store) {
-            float* y = reinterpret_cast<float*>(t.y);
-            for (int j = 0; j < nn; ++j) y[(long long)rows[n0 + j] * t.h_out + c] = s_a * d[j];
+            float* yrow = reinterpret_cast<float*>(ys) + et;
+            for (int j = 0; j < nn; ++j) yrow[(n0 + j) * C::MSUB] = s_a * d[j];
           } else if (args.y_fp32) {
-            float* y = reinterpret_cast<float*>(t.y);
-            float old[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nn) old[j] = y[(long long)rows[n0 + j] * t.h_out + c];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nn) y[(long long)rows[n0 + j] * t.h_out + c] = old[j] + s_a * d[j];
+            float* yrow = reinterpret_cast<float*>(ys) + et;
+            for (int j = 0; j < nn; ++j) yrow[(n0 + j) * C::MSUB] += s_a * d[j];
           } else {
-            uint16_t* y = reinterpret_cast<uint16_t*>(t.y);
-            uint16_t old[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nn) old[j] = y[(long long)rows[n0 + j] * t.h_out + c];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nn) y[(long long)rows[n0 + j] * t.h_out + c] = f32_to_bf16_rne(bf16_to_f32(old[j]) + s_a * d[j]);
+            uint16_t* yrow = reinterpret_cast<uint16_t*>(ys) + et;
+            for (int j = 0; j < nn; ++j) {
+              uint16_t* p = yrow + (n0 + j) * C::MSUB;
+              *p = f32_to_bf16_rne(bf16_to_f32(*p) + s_a * d[j]);
+            }
           }
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
+        fence_proxy_async_smem();              // smem writes -> visible to the bulk store (async proxy)
+        named_bar_sync(1, C::EPI_WARPS * 32);
+        if (et < tile.y) {
+          const long long c0 = (long long)ci * t.CI + (long long)sb * C::MSUB;
+          bulk_s2g(static_cast<char*>(t.y) + ((long long)my_row * t.h_out + c0) * esz, ys + et * rowbytes, rowbytes);
+          bulk_commit();
+          bulk_wait_read<0>();
+        }
+        mbar_arrive(&yempty[yb]);
         if (++acc == C::NACC) {
           acc = 0;
           acc_phase ^= 1;
+        }
+        if (++yb == 2) {
+          yb = 0;
+          yphase ^= 1;
         }
       }
       mbar_arrive(&vempty[vb]);  // done with this item's row table
@@ -538,6 +586,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         vphase ^= 1;
       }
     }
+    bulk_wait<0>();  // all y write-backs complete before exit
   }
   tc_fence_before();
   __syncthreads();

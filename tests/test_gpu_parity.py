@@ -135,7 +135,7 @@ def test_fill_store_equals_loaded_weights(B, rank):
 @pytest.mark.parametrize("rank,small_max", [(8, None), (16, None), (64, -1), (64, 0), (64, 4)])
 def test_exact_integer_probes(B, rank, small_max):
     rng = np.random.default_rng(rank * 10 + (3 if small_max is None else small_max + 2))
-    E, n_ad, h_in, h_out, T = 2, 5, 128, 256, 300   # widths multiple of 128: tcgen05-eligible
+    E, n_ad, h_in, h_out, T = 2, 40, 128, 256, 300   # widths multiple of 128: tcgen05-eligible
     Ai = rng.integers(-1, 2, (n_ad * E, h_in, rank))
     Bi = rng.integers(-1, 2, (n_ad * E, rank, h_out))
     xi = rng.integers(-2, 3, (T, h_in))
@@ -143,7 +143,7 @@ def test_exact_integer_probes(B, rank, small_max):
     a = rng.integers(-1, n_ad, T).astype(np.int32)
     a[:120] = 1                      # one large segment (tcgen05 path when enabled)
     e = rng.integers(0, E, T).astype(np.int32)
-    scale = np.array([0.5, 1.0, 2.0, 0.5, 1.0], np.float32)
+    scale = np.array([(0.5, 1.0, 2.0)[i % 3] for i in range(n_ad)], np.float32)
     bits = lambda v: li.f32_to_bf16_bits_exact(np.asarray(v, np.float32))
     c = B.make_config([h_in], [h_out], [E], rank, n_ad, scale, T, 0)
     s = B.lora_server_create(c, [bits(Ai)], [bits(Bi)], weights_on_device=False)
