@@ -47,20 +47,33 @@ def load_peaks():
 # ---------------------------------------------------------------------------
 # algorithmic bytes
 # ---------------------------------------------------------------------------
-def algorithmic(cfg: li.Config, batch: li.Batch, slots):
+def algorithmic(cfg: li.Config, batch: li.Batch, slots, small_max: int = 8):
+    """Algorithmic bytes per step, split by kernel.
+
+    Each touched unit's A and B are read once, each valid row's x once per
+    slot, its y read + written once; a segment of more than `small_max` rows
+    runs on the tcgen05 kernels (rank 64, 128-multiple widths), else on the
+    CUDA-core kernels -- the same dispatch rule the library applies."""
     a = batch.adapter_ids.astype(np.int64)
     valid = a >= 0
     T, Tv = batch.n_rows, int(valid.sum())
     ysz = 4 if cfg.y_dtype == "fp32" else 2
     r = cfg.rank
-    out = {"segment": T * 8, "shrink": 0, "expand": 0, "flops": 0, "units": {}}
+    tc_ok = r == 64 and small_max >= 0 and all(s.h_in % 128 == 0 and s.h_out % 128 == 0 for s in cfg.slots)
+    out = {"segment": T * 8, "simt_shrink": 0, "simt_expand": 0, "tc05_shrink": 0, "tc05_expand": 0,
+           "flops": 0, "units": {}}
     for i in slots:
         sl = cfg.slots[i]
-        U = int(np.unique(a[valid] * sl.n_experts + batch.expert_ids[valid]).size)
-        out["units"][sl.name] = U
-        out["shrink"] += U * sl.h_in * r * 2 + Tv * sl.h_in * 2
-        out["expand"] += U * sl.h_out * r * 2 + Tv * sl.h_out * 2 * ysz
+        _, cnt = np.unique(a[valid] * sl.n_experts + batch.expert_ids[valid], return_counts=True)
+        out["units"][sl.name] = int(cnt.size)
+        big = (cnt > small_max) if tc_ok else np.zeros(cnt.size, bool)
+        for path, m in (("simt", ~big), ("tc05", big)):
+            U, rows = int(m.sum()), int(cnt[m].sum())
+            out[path + "_shrink"] += U * sl.h_in * r * 2 + rows * sl.h_in * 2
+            out[path + "_expand"] += U * sl.h_out * r * 2 + rows * sl.h_out * 2 * ysz
         out["flops"] += 2 * Tv * r * (sl.h_in + sl.h_out)
+    out["shrink"] = out["simt_shrink"] + out["tc05_shrink"]
+    out["expand"] = out["simt_expand"] + out["tc05_expand"]
     out["total"] = out["segment"] + out["shrink"] + out["expand"]
     out["rows_valid"] = Tv
     return out
@@ -319,12 +332,12 @@ def run_ours(args, cfg, batch, slots):
         return 0
 
     hbm_peak, tc_peak, peak_src = load_peaks()
-    alg = algorithmic(cfg, batch, slots)
+    alg = algorithmic(cfg, batch, slots, int(os.environ.get("LORA_SMALL_SEG_MAX", "8")))
     kern = {}
     for name, (n, tot) in prof.items():
         kern[name] = {"launches": n, "ms_per_launch": tot / n, "ms_per_step": tot / args.steps}
     # dominant kernel: most device time per step; algorithmic bytes per launch
-    per_kind_bytes = {"simt_shrink": alg["shrink"], "simt_expand": alg["expand"], "segment": alg["segment"]}
+    per_kind_bytes = {k: alg[k] for k in ("segment", "simt_shrink", "simt_expand", "tc05_shrink", "tc05_expand")}
     roofline = None
     if kern and world == 1:
         dom = max(kern, key=lambda n: kern[n]["ms_per_step"])

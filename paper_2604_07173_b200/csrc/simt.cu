@@ -87,9 +87,10 @@ LORA_DEVINL void unpack8(const uint4& w, float* f) {
   f[6] = bf16lo(w.w); f[7] = bf16hi(w.w);
 }
 
-LORA_DEVINL float dot8_acc(float acc, const float* a, const float* b) {
+// packed fp32x2 FMA (FFMA2, sm_100): two products per instruction
+LORA_DEVINL float2 dot8_acc2(float2 acc, const float* a, const float* b) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc = fmaf(a[i], b[i], acc);
+  for (int i = 0; i < 8; i += 2) acc = __ffma2_rn(make_float2(a[i], a[i + 1]), make_float2(b[i], b[i + 1]), acc);
   return acc;
 }
 
@@ -105,18 +106,17 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
   const int kl = ct % C::KL, jg = ct / C::KL;
   const int n_st = t.h_in / t.SJ;
   const int nchunk = t.SJ >> 3;  // 16-byte chunks along j per stage
-  float acc[C::KPL][NR][2];
+  float2 acc[C::KPL][NR];
 #pragma unroll
   for (int kk = 0; kk < C::KPL; ++kk)
 #pragma unroll
-    for (int r = 0; r < NR; ++r) acc[kk][r][0] = acc[kk][r][1] = 0.f;
+    for (int r = 0; r < NR; ++r) acc[kk][r] = make_float2(0.f, 0.f);
 
   for (int st = 0; st < n_st; ++st) {
     mbar_wait(&full[stage], phase);
     const uint32_t a_s = smem_u32(smem + stage * C::S_STAGE);
     const uint32_t x_s = a_s + C::A_STAGE;
-    int par = 0;
-    for (int c = jg; c < nchunk; c += C::NJG, par ^= 1) {
+    for (int c = jg; c < nchunk; c += C::NJG) {
       const int tile = c >> 3, q = c & 7;
       float w[C::KPL][8];
 #pragma unroll
@@ -129,12 +129,7 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
         float xf[8];
         unpack8(lds128(x_s + r * (t.SJ * 2) + (c << 4)), xf);
 #pragma unroll
-        for (int kk = 0; kk < C::KPL; ++kk) {
-          if (par)
-            acc[kk][r][1] = dot8_acc(acc[kk][r][1], xf, w[kk]);
-          else
-            acc[kk][r][0] = dot8_acc(acc[kk][r][0], xf, w[kk]);
-        }
+        for (int kk = 0; kk < C::KPL; ++kk) acc[kk][r] = dot8_acc2(acc[kk][r], xf, w[kk]);
       }
     }
     __syncwarp();
@@ -150,7 +145,7 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
 #pragma unroll
   for (int kk = 0; kk < C::KPL; ++kk)
 #pragma unroll
-    for (int r = 0; r < NR; ++r) red[(jg * NR + r) * R + kl + kk * 32] = acc[kk][r][0] + acc[kk][r][1];
+    for (int r = 0; r < NR; ++r) red[(jg * NR + r) * R + kl + kk * 32] = acc[kk][r].x + acc[kk][r].y;
   named_bar_sync(1, C::NCT);
   float* vp = vpart_base + (long long)g.x * R;
   for (int idx = ct; idx < NR * R; idx += C::NCT) {
@@ -262,33 +257,30 @@ struct ExpandPos {
 template <int R, int NR>
 LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int cr, const ExpandPos& p, const uint32_t* yraw,
                               const int* yrow, int y_store, int y_fp32) {
-  float acc[NR][2];
+  float2 acc[NR][2];
 #pragma unroll
-  for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = 0.f;
+  for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int ch = 0; ch < R / 8; ++ch) {
-    float bf[8];
-    unpack8(lds128(b_s + cr * (R * 2) + (swz_row_chunk(cr, ch, R * 2) << 4)), bf);
+    const uint4 w = lds128(b_s + cr * (R * 2) + (swz_row_chunk(cr, ch, R * 2) << 4));
+    const float2 b0 = make_float2(bf16lo(w.x), bf16hi(w.x)), b1 = make_float2(bf16lo(w.y), bf16hi(w.y));
+    const float2 b2 = make_float2(bf16lo(w.z), bf16hi(w.z)), b3 = make_float2(bf16lo(w.w), bf16hi(w.w));
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const float4 v0 = lds128f(v_s + (r * R + ch * 8) * 4);
       const float4 v1 = lds128f(v_s + (r * R + ch * 8 + 4) * 4);
-      float a = acc[r][ch & 1];
-      a = fmaf(v0.x, bf[0], a);
-      a = fmaf(v0.y, bf[1], a);
-      a = fmaf(v0.z, bf[2], a);
-      a = fmaf(v0.w, bf[3], a);
-      a = fmaf(v1.x, bf[4], a);
-      a = fmaf(v1.y, bf[5], a);
-      a = fmaf(v1.z, bf[6], a);
-      a = fmaf(v1.w, bf[7], a);
+      float2 a = acc[r][ch & 1];
+      a = __ffma2_rn(make_float2(v0.x, v0.y), b0, a);
+      a = __ffma2_rn(make_float2(v0.z, v0.w), b1, a);
+      a = __ffma2_rn(make_float2(v1.x, v1.y), b2, a);
+      a = __ffma2_rn(make_float2(v1.z, v1.w), b3, a);
       acc[r][ch & 1] = a;
     }
   }
   const long long c = p.c0 + cr;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const float d = p.s_a * (acc[r][0] + acc[r][1]);
+    const float d = p.s_a * ((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
     const long long o = (long long)yrow[r] * p.h_out + c;
     if (y_store)
       reinterpret_cast<float*>(p.y)[o] = d;
@@ -375,12 +367,12 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
     p.perm_rows = pd.perm + g.x;
     p.s_a = args.scale[g.z / t.E];
   };
-  // raw y bits of the stage at `p` for this thread's column (kept raw: the
-  // conversion happens at use, so the load latency overlaps a whole stage)
-  auto load_y = [&](const ExpandPos& p, uint32_t (&yraw)[C::GR], int (&yrow)[C::GR]) {
-    if (p.it >= n_items) return;
-#pragma unroll
-    for (int r = 0; r < C::GR; ++r) yrow[r] = r < p.rows ? p.perm_rows[r] : 0;
+  // raw y bits of the stage at `p` for this thread's column.  Kept raw (the
+  // conversion happens at use), so the loads stay in flight across the next
+  // barrier wait and compute.
+  uint32_t yv[C::GR];
+  int yrow[C::GR];
+  auto load_y = [&](const ExpandPos& p) {
     if (args.y_store || ct >= p.sc) return;
     const long long c = p.c0 + ct;
 #pragma unroll
@@ -388,41 +380,37 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       if (r < p.rows) {
         const long long o = (long long)yrow[r] * p.h_out + c;
         if (args.y_fp32)
-          yraw[r] = reinterpret_cast<const uint32_t*>(p.y)[o];
+          yv[r] = reinterpret_cast<const uint32_t*>(p.y)[o];
         else
-          yraw[r] = reinterpret_cast<const uint16_t*>(p.y)[o];
+          yv[r] = reinterpret_cast<const uint16_t*>(p.y)[o];
       }
     }
   };
+  auto load_rows = [&](const ExpandPos& p) {
+#pragma unroll
+    for (int r = 0; r < C::GR; ++r) yrow[r] = r < p.rows ? p.perm_rows[r] : 0;
+  };
 
-  ExpandPos cur, nxt;
-  uint32_t ycur[C::GR], ynxt[C::GR];
-  int ocur[C::GR], onxt[C::GR];
+  ExpandPos cur;
   locate(blockIdx.x, cur);
-  load_y(cur, ycur, ocur);
+  if (cur.it < n_items) {
+    load_rows(cur);
+    load_y(cur);
+  }
   while (cur.it < n_items) {
-    if (cur.st + 1 < cur.n_st) {
-      nxt = cur;
-      nxt.st = cur.st + 1;
-      nxt.c0 = cur.c0 + cur.sc;
-    } else {
-      locate(cur.it + gridDim.x, nxt);
-    }
-    load_y(nxt, ynxt, onxt);  // one stage ahead
-
     mbar_wait(&full[stage], phase);
     const uint32_t b_s = smem_u32(smem + stage * C::E_STAGE);
     const uint32_t v_s = b_s + C::B_STAGE;
     if (ct < cur.sc) {
       switch (cur.rows) {
-        case 1: expand_stage<R, 1>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
-        case 2: expand_stage<R, 2>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
-        case 3: expand_stage<R, 3>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
-        case 4: expand_stage<R, 4>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
-        case 5: expand_stage<R, 5>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
-        case 6: expand_stage<R, 6>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
-        case 7: expand_stage<R, 7>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
-        default: expand_stage<R, 8>(b_s, v_s, ct, cur, ycur, ocur, args.y_store, args.y_fp32); break;
+        case 1: expand_stage<R, 1>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
+        case 2: expand_stage<R, 2>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
+        case 3: expand_stage<R, 3>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
+        case 4: expand_stage<R, 4>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
+        case 5: expand_stage<R, 5>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
+        case 6: expand_stage<R, 6>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
+        case 7: expand_stage<R, 7>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
+        default: expand_stage<R, 8>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
       }
     }
     __syncwarp();
@@ -431,12 +419,16 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       stage = 0;
       phase ^= 1;
     }
-    cur = nxt;
-#pragma unroll
-    for (int r = 0; r < C::GR; ++r) {
-      ycur[r] = ynxt[r];
-      ocur[r] = onxt[r];
+    // next stage of this item, or this CTA's next item; issue its y loads now
+    if (cur.st + 1 < cur.n_st) {
+      cur.st += 1;
+      cur.c0 += cur.sc;
+    } else {
+      locate(cur.it + gridDim.x, cur);
+      if (cur.it >= n_items) break;
+      load_rows(cur);
     }
+    load_y(cur);
   }
 }
 

@@ -309,13 +309,13 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
 // expand (swap-AB), y staged through shared memory by TMA bulk copies
 // ===========================================================================
 struct ExpandCfg {
-  static constexpr int EPI_WARPS = 4;   // warps 0-3: epilogue (TMEM lane = output column)
-  static constexpr int TMA_WARP = 4;    // warp 4: Bt bulk copies
-  static constexpr int MMA_WARP = 5;    // warp 5: TMEM alloc + MMA
-  static constexpr int VB_WARP0 = 6;    // warps 6-9: v-tile builders
-  static constexpr int YL_WARP = 10;    // warp 10: y-tile loader (bulk copies, one per row)
+  static constexpr int EPI_WARPS = 8;   // warps 0-7: epilogue (TMEM lane = output column; two row halves)
+  static constexpr int TMA_WARP = 8;    // warp 8: Bt bulk copies
+  static constexpr int MMA_WARP = 9;    // warp 9: TMEM alloc + MMA
+  static constexpr int VB_WARP0 = 10;   // warps 10-13: v-tile builders
+  static constexpr int YL_WARP = 14;    // warp 14: y-tile loader (bulk copies, one per row)
   static constexpr int VB_THREADS = 128;
-  static constexpr int THREADS = 11 * 32;
+  static constexpr int THREADS = 15 * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (M)
   static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
   static constexpr int NST = 3;
@@ -526,7 +526,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     // ===================== epilogue: y tile (smem) += s_a * D, bulk-stored back =====================
     int acc = 0, yb = 0, vb = 0;
     uint32_t acc_phase = 0, yphase = 0, vphase = 0;
-    const int et = threadIdx.x;  // 0..127 = output column within the sub-tile
+    const int et = threadIdx.x;              // 0..255
+    const int col = et & 127, half = et >> 7;  // output column within the sub-tile, row half
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
       const SlotTask& t = args.t[find_task_ci(args, cig)];
@@ -541,19 +542,20 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         mbar_wait(&yfull[yb], yphase);
         tc_fence_after();
         uint8_t* ys = ytile + yb * C::Y_TILE;
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS;
-        for (int n0 = 0; n0 < tile.y; n0 += 16) {
+        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + acc * C::ACC_COLS;
+        // this warp's row half: 16-row chunks n0 = 16*half, 16*half + 32, ...
+        for (int n0 = 16 * half; n0 < tile.y; n0 += 32) {
           float d[16];
           tmem_ld16(taddr + n0, d);
           const int nn = min(16, tile.y - n0);
           if (args.y_store) {
-            float* yrow = reinterpret_cast<float*>(ys) + et;
+            float* yrow = reinterpret_cast<float*>(ys) + col;
             for (int j = 0; j < nn; ++j) yrow[(n0 + j) * C::MSUB] = s_a * d[j];
           } else if (args.y_fp32) {
-            float* yrow = reinterpret_cast<float*>(ys) + et;
+            float* yrow = reinterpret_cast<float*>(ys) + col;
             for (int j = 0; j < nn; ++j) yrow[(n0 + j) * C::MSUB] += s_a * d[j];
           } else {
-            uint16_t* yrow = reinterpret_cast<uint16_t*>(ys) + et;
+            uint16_t* yrow = reinterpret_cast<uint16_t*>(ys) + col;
             for (int j = 0; j < nn; ++j) {
               uint16_t* p = yrow + (n0 + j) * C::MSUB;
               *p = f32_to_bf16_rne(bf16_to_f32(*p) + s_a * d[j]);
