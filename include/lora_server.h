@@ -235,7 +235,7 @@ lora_status_t lora_profile_read(lora_server_t *s, int32_t n_kinds, int32_t *laun
 
 /* Name of kernel kind k (0 segment, 1 simt_shrink, 2 tc05_shrink,
  * 3 simt_expand, 4 tc05_expand, 5 shard_bucket, 6 shard_gather,
- * 7 shard_scatter_add); "unknown" otherwise. */
+ * 7 shard_scatter_add, 8 tc05_vreduce); "unknown" otherwise. */
 const char *lora_kernel_name(int32_t kind);
 
 /* Library version string. */

@@ -68,7 +68,7 @@ SIGNATURES = {
     "lora_kernel_name": (ctypes.c_char_p, [_i32]),
     "lora_version": (ctypes.c_char_p, []),
 }
-N_KERNEL_KINDS = 8
+N_KERNEL_KINDS = 9
 for _name, (_res, _args) in SIGNATURES.items():
     _f = getattr(lib, _name)
     _f.restype = _res

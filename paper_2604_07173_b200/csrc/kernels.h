@@ -23,6 +23,8 @@ struct PlanDev {
   int4* groups;      // [max_rows]   CUDA-core groups {row_begin, nrows, key, seg}
   int4* tiles;       // [max_rows]   tcgen05 tiles    {row_begin, nrows, key, seg}
   float* vpart;      // shrink partial sums, per slot region [n_kc][max_rows][r]
+  uint16_t* vbf;     // tcgen05 path: complete v rounded to bf16, per slot region [max_rows][r]
+  int* tc_cnt;       // tcgen05 shrink arrival counters [kMaxTasks][max_rows] (self-resetting)
   int max_rows;
 };
 
@@ -39,6 +41,7 @@ struct SlotTask {
   const uint16_t* x;   // bf16 [T][h_in]
   void* y;             // bf16 / fp32 [T][h_out]
   long long vpart_off; // float offset of this slot's partial-sum region
+  long long vbf_off;   // element offset of this slot's bf16 v region
   int h_in, h_out, E;
   int KI, SJ, n_kc;    // shrink: j-range per item, j per stage, items per row group
   int CI, SC, n_ci;    // expand: c-range per item, c rows per stage, items per row group
@@ -62,6 +65,7 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
 cudaError_t launch_simt_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_simt_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 bool tc_available();
 

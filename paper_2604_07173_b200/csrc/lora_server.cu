@@ -323,13 +323,16 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
             cudaMalloc(&d.counts, sizeof(int32_t) * kCntWords) == cudaSuccess &&
             cudaMalloc(&d.groups, sizeof(int4) * max_rows) == cudaSuccess &&
             cudaMalloc(&d.tiles, sizeof(int4) * max_rows) == cudaSuccess &&
-            cudaMalloc(&d.vpart, sizeof(float) * (size_t)s->total_kc * max_rows * s->r) == cudaSuccess;
+            cudaMalloc(&d.vpart, sizeof(float) * (size_t)s->total_kc * max_rows * s->r) == cudaSuccess &&
+            cudaMalloc(&d.vbf, sizeof(uint16_t) * s->slots.size() * (size_t)max_rows * s->r) == cudaSuccess &&
+            cudaMalloc(&d.tc_cnt, sizeof(int) * (size_t)kMaxTasks * max_rows) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     plan_destroy_impl(p);
     return fail(s, LORA_ERR_OOM, "plan allocation failed");
   }
   cudaMemset(d.counts, 0, sizeof(int32_t) * kCntWords);
+  cudaMemset(d.tc_cnt, 0, sizeof(int) * (size_t)kMaxTasks * max_rows);
   cudaMemset(d.seg_off, 0, sizeof(int32_t) * (max_rows + 1));
   *out = p;
   return LORA_OK;
@@ -344,6 +347,8 @@ void plan_destroy_impl(lora_plan* p) {
   cudaFree(p->dev.groups);
   cudaFree(p->dev.tiles);
   cudaFree(p->dev.vpart);
+  cudaFree(p->dev.vbf);
+  cudaFree(p->dev.tc_cnt);
   delete p;
 }
 
@@ -429,6 +434,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       t.x = static_cast<const uint16_t*>(x[b0 + i]);
       t.y = y[b0 + i];
       t.vpart_off = (long long)si.kc_prefix * p->max_rows * s->r;
+      t.vbf_off = (long long)slots[b0 + i] * p->max_rows * s->r;
       t.h_in = si.h_in;
       t.h_out = si.h_out;
       t.E = si.E;
@@ -458,6 +464,9 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     CK(s, launch_simt_expand(s->r, args, p->dev, grid, st));
     prof_stop(s, pi, kKSimtExpand, st);
     if (tc) {
+      pi = prof_start(s, st);
+      CK(s, launch_tc_vreduce(args, p->dev, grid, st));
+      prof_stop(s, pi, kKTcVreduce, st);
       pi = prof_start(s, st);
       CK(s, launch_tc_expand(args, p->dev, grid, st));
       prof_stop(s, pi, kKTcExpand, st);
@@ -700,7 +709,8 @@ extern "C" lora_status_t lora_profile_read(lora_server_t* s, int32_t n_kinds, in
 
 extern "C" const char* lora_kernel_name(int32_t kind) {
   static const char* names[kKNumKinds] = {"segment",        "simt_shrink",   "tc05_shrink",  "simt_expand",
-                                          "tc05_expand",    "shard_bucket",  "shard_gather", "shard_scatter_add"};
+                                          "tc05_expand",    "shard_bucket",  "shard_gather", "shard_scatter_add",
+                                          "tc05_vreduce"};
   return (kind >= 0 && kind < kKNumKinds) ? names[kind] : "unknown";
 }
 

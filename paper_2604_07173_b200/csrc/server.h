@@ -51,7 +51,7 @@ struct lora_server {
 
 // kernel kinds reported by lora_profile_read
 enum { kKSegment = 0, kKSimtShrink = 1, kKTcShrink = 2, kKSimtExpand = 3, kKTcExpand = 4, kKShardBucket = 5,
-       kKShardGather = 6, kKShardScatter = 7, kKNumKinds = 8 };
+       kKShardGather = 6, kKShardScatter = 7, kKTcVreduce = 8, kKNumKinds = 9 };
 int prof_start(lora_server* s, cudaStream_t st);
 void prof_stop(lora_server* s, int idx, int kind, cudaStream_t st);
 

@@ -182,8 +182,18 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       const int4 tile = pd.tiles[ti];
       const long long unit = unit_of_key(tile.z, t.E, args.world);
       const uint16_t* wbase = t.At + (unit * (t.h_in >> 6) + ((kc * t.KI) >> 6)) * (long long)(R * 64);
-      // this thread's rows / chunks: 128 rows x 8 chunks per k-step, 1024 copies / 128 threads
+      // this thread's rows / chunks: 128 rows x 8 chunks per k-step, 1024 copies / 128 threads;
+      // thread pt always copies chunk q = pt & 7 of rows n = (pt >> 3) + 16 i
       const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
+      const uint16_t* xsrc[8];
+      uint32_t xbytes[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int n = (pt >> 3) + 16 * i;
+        const bool valid = n < tile.y;
+        xsrc[i] = t.x + (valid ? (long long)pd.perm[tile.x + n] * t.h_in : 0) + (long long)kc * t.KI + (pt & 7) * 8;
+        xbytes[i] = valid ? 16u : 0u;
+      }
       for (int st = 0; st < n_st; ++st) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sbase = smem + stage * C::STAGE;
@@ -192,18 +202,14 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
           bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB,
                    wbase + (long long)st * C::KS_PER_STAGE * (R * 64), C::KS_PER_STAGE * C::W_SUB, &full[stage]);
         }
-        const long long j0 = (long long)kc * t.KI + (long long)st * C::KS_PER_STAGE * C::KSTEP;
+        const int j0 = st * C::KS_PER_STAGE * C::KSTEP;
 #pragma unroll
         for (int ks = 0; ks < C::KS_PER_STAGE; ++ks) {
           uint8_t* xs = sbase + ks * C::X_SUB;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int idx = pt + i * C::PROD_THREADS;  // 0..1023
-            const int n = idx >> 3, q = idx & 7;
-            const bool valid = n < tile.y;
-            const long long row = valid ? pd.perm[tile.x + n] : 0;
-            const uint16_t* src = t.x + row * t.h_in + j0 + ks * C::KSTEP + q * 8;
-            cp_async16(xs + n * 128 + ((q ^ (n & 7)) << 4), src, valid ? 16u : 0u);
+            const int n = (pt >> 3) + 16 * i, q = pt & 7;
+            cp_async16(xs + n * 128 + ((q ^ (n & 7)) << 4), xsrc[i] + j0 + ks * C::KSTEP, xbytes[i]);
           }
         }
         cp_async_commit();
@@ -306,25 +312,75 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
 }
 
 // ===========================================================================
-// expand (swap-AB), y staged through shared memory by TMA bulk copies
+// v reduction: the tcgen05 shrink leaves n_kc fp32 partials per row; sum them
+// in fixed kc order, round once to bf16 and store each tile's rows already in
+// the SWIZZLE_128B K-major layout (row n of a tile: 16-byte chunk q at
+// q ^ (n & 7)), so the expand loads its MMA operand with one bulk copy.
+// ===========================================================================
+__global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
+  const int n_tiles = pd.counts[kCntTiles];
+  const long long per_task = (long long)n_tiles * kTileRows * (R / 8);
+  const long long total = per_task * args.n_tasks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int task = (int)(i / per_task);
+    const long long rem = i - (long long)task * per_task;
+    const int ti = (int)(rem / (kTileRows * (R / 8)));
+    const int within = (int)(rem - (long long)ti * (kTileRows * (R / 8)));
+    const int n = within >> 3, q = within & 7;
+    const int4 tile = pd.tiles[ti];
+    if (n >= tile.y) continue;
+    const SlotTask& t = args.t[task];
+    const float* src = pd.vpart + t.vpart_off + ((long long)tile.x + n) * R + q * 8;
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int kc = 0; kc < t.n_kc; ++kc) {
+      const float4* p4 = reinterpret_cast<const float4*>(src + (long long)kc * pd.max_rows * R);
+      const float4 a = p4[0], b = p4[1];
+      s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+      s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+    }
+    uint4 w;
+    w.x = f32_to_bf16_rne(s[0]) | ((uint32_t)f32_to_bf16_rne(s[1]) << 16);
+    w.y = f32_to_bf16_rne(s[2]) | ((uint32_t)f32_to_bf16_rne(s[3]) << 16);
+    w.z = f32_to_bf16_rne(s[4]) | ((uint32_t)f32_to_bf16_rne(s[5]) << 16);
+    w.w = f32_to_bf16_rne(s[6]) | ((uint32_t)f32_to_bf16_rne(s[7]) << 16);
+    *reinterpret_cast<uint4*>(pd.vbf + t.vbf_off + ((long long)tile.x + n) * R + ((q ^ (n & 7)) * 8)) = w;
+  }
+}
+
+LORA_DEVINL void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+LORA_DEVINL void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ===========================================================================
+// expand (swap-AB).  Per 128-column sub-tile: D[128 cols x N rows] in TMEM;
+// the epilogue moves D through a double-buffered fp32 staging tile in shared
+// memory (lane = column, conflict-free) and then read-modify-writes y with
+// 16-byte vector accesses, the y loads of the next sub-tile in flight.
 // ===========================================================================
 struct ExpandCfg {
-  static constexpr int EPI_WARPS = 8;   // warps 0-7: epilogue (TMEM lane = output column; two row halves)
-  static constexpr int TMA_WARP = 8;    // warp 8: Bt bulk copies
-  static constexpr int MMA_WARP = 9;    // warp 9: TMEM alloc + MMA
-  static constexpr int VB_WARP0 = 10;   // warps 10-13: v-tile builders
-  static constexpr int YL_WARP = 14;    // warp 14: y-tile loader (bulk copies, one per row)
-  static constexpr int VB_THREADS = 128;
-  static constexpr int THREADS = 15 * 32;
+  static constexpr int EPI_WARPS = 16;  // warps 0-15: epilogue (TMEM lanes by warp % 4, rows by warp / 4)
+  static constexpr int TMA_WARP = 16;   // warp 16: v tile + Bt bulk copies
+  static constexpr int MMA_WARP = 17;   // warp 17: TMEM alloc + MMA
+  static constexpr int THREADS = 18 * 32;
+  static constexpr int EPI_THREADS = EPI_WARPS * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (M)
   static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
   static constexpr int NST = 3;
   static constexpr int V_TILE = kTileRows * 128;       // 16 KB (N <= 128 rows x 64 bf16)
-  static constexpr int Y_TILE = kTileRows * MSUB * 4;  // 64 KB (128 rows x 128 cols, fp32 worst case)
+  static constexpr int STG_PITCH = MSUB * 4 + 16;      // fp32 staging row (+16 B: fewer bank conflicts)
+  static constexpr int STG = kTileRows * STG_PITCH;    // 66 KB
   static constexpr int NACC = 2;
   static constexpr int ACC_COLS = kTileRows;           // N columns per accumulator
   static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 256
-  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 2 * Y_TILE + 2048;
+  static constexpr int PF = kTileRows * (MSUB / 8) / EPI_THREADS;  // 16-byte bf16 chunks per thread per sub-tile (4)
+  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 2 * STG + 512;
 };
 
 __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
@@ -332,35 +388,28 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   using C = ExpandCfg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE]
-  uint8_t* ytile = vtile + 2 * C::V_TILE;      // [2][Y_TILE]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ytile + 2 * C::Y_TILE);
+  uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE] swizzled MMA operand
+  uint8_t* stg = vtile + 2 * C::V_TILE;        // [2][128][STG_PITCH] fp32 delta staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + 2 * C::STG);
   uint64_t* full = bars;                       // [NST] Bt landed
   uint64_t* empty = bars + C::NST;             // [NST] MMA done with Bt stage
-  uint64_t* vfull = bars + 2 * C::NST;         // [2]  v tile + row table built
-  uint64_t* vempty = vfull + 2;                // [2]  MMA, epilogue and y loader done with the item
+  uint64_t* vfull = bars + 2 * C::NST;         // [2]  v tile landed
+  uint64_t* vempty = vfull + 2;                // [2]  MMA done with the v tile
   uint64_t* tfull = vempty + 2;                // [2]  accumulator ready
   uint64_t* tempty = tfull + 2;                // [2]  accumulator drained
-  uint64_t* yfull = tempty + 2;                // [2]  y tile landed
-  uint64_t* yempty = yfull + 2;                // [2]  y tile written back (smem free)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yempty + 2);
-  int* rowtab = reinterpret_cast<int*>(tmem_slot + 4);  // [2][kTileRows] y row of each tile row
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = warp_id(), lane = lane_id();
-  const int esz = (args.y_fp32 || args.y_store) ? 4 : 2;
-  const int rowbytes = C::MSUB * esz;          // y bytes per row per sub-tile
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&vfull[a], C::VB_THREADS);
-      mbar_init(&vempty[a], 1 + C::EPI_WARPS * 32 + 1);
+      mbar_init(&vfull[a], 1);
+      mbar_init(&vempty[a], 1);
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], C::EPI_WARPS * 32);
-      mbar_init(&yfull[a], 1);
-      mbar_init(&yempty[a], C::EPI_WARPS * 32);
+      mbar_init(&tempty[a], C::EPI_THREADS);
     }
     fence_mbar_init();
   }
@@ -374,16 +423,24 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   const long long n_items = (long long)n_tiles * args.total_ci;
 
   if (warp == C::TMA_WARP) {
-    // ===================== Bt producer =====================
+    // ===================== producer: v tile + Bt sub-tiles =====================
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
+      int stage = 0, vb = 0;
+      uint32_t phase = 0, vphase = 0;
       for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
         const SlotTask& t = args.t[find_task_ci(args, cig)];
         const int ci = cig - t.ci_base;
         const int4 tile = pd.tiles[ti];
+        mbar_wait(&vempty[vb], vphase ^ 1);
+        mbar_arrive_expect_tx(&vfull[vb], (uint32_t)tile.y * 128);
+        bulk_g2s(vtile + vb * C::V_TILE, pd.vbf + t.vbf_off + (long long)tile.x * R, (uint32_t)tile.y * 128,
+                 &vfull[vb]);
+        if (++vb == 2) {
+          vb = 0;
+          vphase ^= 1;
+        }
         const long long unit = unit_of_key(tile.z, t.E, args.world);
         const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
         const int n_sub = t.CI / C::MSUB;
@@ -398,97 +455,15 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         }
       }
     }
-  } else if (warp == C::YL_WARP) {
-    // ===================== y-tile loader =====================
-    int vb = 0, yb = 0;
-    uint32_t vphase = 0, yphase = 0;
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
-      const SlotTask& t = args.t[find_task_ci(args, cig)];
-      const int ci = cig - t.ci_base;
-      const int4 tile = pd.tiles[ti];
-      const int n_sub = t.CI / C::MSUB;
-      mbar_wait(&vfull[vb], vphase);
-      const int* rows = rowtab + vb * kTileRows;
-      for (int sb = 0; sb < n_sub; ++sb) {
-        mbar_wait(&yempty[yb], yphase ^ 1);
-        if (args.y_store) {
-          if (lane == 0) mbar_arrive(&yfull[yb]);
-        } else {
-          if (lane == 0) mbar_arrive_expect_tx(&yfull[yb], (uint32_t)(tile.y * rowbytes));
-          __syncwarp();
-          const long long c0 = (long long)ci * t.CI + (long long)sb * C::MSUB;
-          const char* ybase = static_cast<const char*>(t.y);
-          for (int n = lane; n < tile.y; n += 32)
-            bulk_g2s(ytile + yb * C::Y_TILE + n * rowbytes, ybase + ((long long)rows[n] * t.h_out + c0) * esz,
-                     rowbytes, &yfull[yb]);
-        }
-        __syncwarp();
-        if (++yb == 2) {
-          yb = 0;
-          yphase ^= 1;
-        }
-      }
-      if (lane == 0) mbar_arrive(&vempty[vb]);
-      if (++vb == 2) {
-        vb = 0;
-        vphase ^= 1;
-      }
-    }
-  } else if (warp >= C::VB_WARP0) {
-    // ===================== v-tile builders =====================
-    const int vt = threadIdx.x - C::VB_WARP0 * 32;  // 0..127
-    int vb = 0;
-    uint32_t vphase = 0;
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
-      const SlotTask& t = args.t[find_task_ci(args, cig)];
-      const int4 tile = pd.tiles[ti];
-      const int npad = (tile.y + 15) & ~15;
-      mbar_wait(&vempty[vb], vphase ^ 1);
-      uint8_t* vs = vtile + vb * C::V_TILE;
-      const float* vp = pd.vpart + t.vpart_off + (long long)tile.x * R;
-      const long long kstride = (long long)pd.max_rows * R;
-      for (int idx = vt; idx < npad * 8; idx += C::VB_THREADS) {
-        const int n = idx >> 3, q = idx & 7;
-        uint4 w = make_uint4(0, 0, 0, 0);
-        if (n < tile.y) {
-          float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          for (int kc = 0; kc < t.n_kc; ++kc) {
-            const float4* src = reinterpret_cast<const float4*>(vp + kc * kstride + n * R + q * 8);
-            const float4 a = src[0], b = src[1];
-            s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
-            s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
-          }
-          w.x = f32_to_bf16_rne(s[0]) | ((uint32_t)f32_to_bf16_rne(s[1]) << 16);
-          w.y = f32_to_bf16_rne(s[2]) | ((uint32_t)f32_to_bf16_rne(s[3]) << 16);
-          w.z = f32_to_bf16_rne(s[4]) | ((uint32_t)f32_to_bf16_rne(s[5]) << 16);
-          w.w = f32_to_bf16_rne(s[6]) | ((uint32_t)f32_to_bf16_rne(s[7]) << 16);
-        }
-        *reinterpret_cast<uint4*>(vs + n * 128 + ((q ^ (n & 7)) << 4)) = w;
-      }
-      for (int n = vt; n < kTileRows; n += C::VB_THREADS)
-        rowtab[vb * kTileRows + n] = n < tile.y ? pd.perm[tile.x + n] : 0;
-      fence_proxy_async_smem();
-      mbar_arrive(&vfull[vb]);
-      if (++vb == 2) {
-        vb = 0;
-        vphase ^= 1;
-      }
-    }
   } else if (warp == C::MMA_WARP) {
     // ===================== MMA issuer =====================
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int vb = 0;
-    uint32_t vphase = 0;
+    int stage = 0, acc = 0, vb = 0;
+    uint32_t phase = 0, acc_phase = 0, vphase = 0;
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
       const SlotTask& t = args.t[find_task_ci(args, cig)];
       const int4 tile = pd.tiles[ti];
-      const int npad = (tile.y + 15) & ~15;
+      const int npad = (tile.y + 15) & ~15;  // rows >= tile.y hold stale data: their D columns are never read
       const uint32_t idesc = idesc_bf16(C::MSUB, npad);
       const int n_sub = t.CI / C::MSUB;
       mbar_wait(&vfull[vb], vphase);
@@ -523,11 +498,14 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue: y tile (smem) += s_a * D, bulk-stored back =====================
-    int acc = 0, yb = 0, vb = 0;
-    uint32_t acc_phase = 0, yphase = 0, vphase = 0;
-    const int et = threadIdx.x;              // 0..255
-    const int col = et & 127, half = et >> 7;  // output column within the sub-tile, row half
+    // ===================== epilogue =====================
+    int acc = 0, sbuf = 0;
+    uint32_t acc_phase = 0;
+    const int et = threadIdx.x;                   // 0..511
+    const int col = et & 127, quarter = et >> 7;  // TMEM lane (column) and row quarter for phase (1)
+    const bool bf16y = !(args.y_fp32 || args.y_store);
+    uint4 ypf[C::PF];                             // prefetched y chunks (bf16 mode)
+    int prow[C::PF];                              // y row of each chunk
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
       const SlotTask& t = args.t[find_task_ci(args, cig)];
@@ -535,60 +513,97 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const int4 tile = pd.tiles[ti];
       const float s_a = args.scale[tile.z / t.E];
       const int n_sub = t.CI / C::MSUB;
-      mbar_wait(&vfull[vb], vphase);
-      const int my_row = et < tile.y ? rowtab[vb * kTileRows + et] : 0;
+      const long long cbase = (long long)ci * t.CI;
+      // chunk j of this thread: row n = (et + j*512) / 16, columns 8*((et + j*512) % 16) ..+8
+#pragma unroll
+      for (int j = 0; j < C::PF; ++j) {
+        const int n = (et + j * C::EPI_THREADS) >> 4;
+        prow[j] = n < tile.y ? __ldg(pd.perm + tile.x + n) : 0;
+      }
+      auto issue_y = [&](int sb) {
+#pragma unroll
+        for (int j = 0; j < C::PF; ++j) {
+          const int q = et + j * C::EPI_THREADS, n = q >> 4, c8 = q & 15;
+          if (n < tile.y)
+            ypf[j] = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(t.y) + (long long)prow[j] * t.h_out +
+                                                     cbase + (long long)sb * C::MSUB + c8 * 8);
+        }
+      };
+      if (bf16y) issue_y(0);
       for (int sb = 0; sb < n_sub; ++sb) {
+        const long long c0 = cbase + (long long)sb * C::MSUB;
+        uint8_t* sg = stg + sbuf * C::STG;
+        // (1) TMEM -> staging (this warp: lanes 32*(warp%4).., rows 16*quarter + 64*k)
         mbar_wait(&tfull[acc], acc_phase);
-        mbar_wait(&yfull[yb], yphase);
         tc_fence_after();
-        uint8_t* ys = ytile + yb * C::Y_TILE;
-        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + acc * C::ACC_COLS;
-        // this warp's row half: 16-row chunks n0 = 16*half, 16*half + 32, ...
-        for (int n0 = 16 * half; n0 < tile.y; n0 += 32) {
-          float d[16];
-          tmem_ld16(taddr + n0, d);
-          const int nn = min(16, tile.y - n0);
-          if (args.y_store) {
-            float* yrow = reinterpret_cast<float*>(ys) + col;
-            for (int j = 0; j < nn; ++j) yrow[(n0 + j) * C::MSUB] = s_a * d[j];
-          } else if (args.y_fp32) {
-            float* yrow = reinterpret_cast<float*>(ys) + col;
-            for (int j = 0; j < nn; ++j) yrow[(n0 + j) * C::MSUB] += s_a * d[j];
-          } else {
-            uint16_t* yrow = reinterpret_cast<uint16_t*>(ys) + col;
-            for (int j = 0; j < nn; ++j) {
-              uint16_t* p = yrow + (n0 + j) * C::MSUB;
-              *p = f32_to_bf16_rne(bf16_to_f32(*p) + s_a * d[j]);
+        {
+          const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + acc * C::ACC_COLS;
+          uint32_t d0[16], d1[16];
+          const int n0 = 16 * quarter, n1 = n0 + 64;
+          if (n0 < tile.y) tmem_ld16_nowait(taddr + n0, d0);
+          if (n1 < tile.y) tmem_ld16_nowait(taddr + n1, d1);
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          float* srow = reinterpret_cast<float*>(sg) + col;
+          if (n0 < tile.y) {
+            const int nn = min(16, tile.y - n0);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nn) srow[(n0 + j) * (C::STG_PITCH / 4)] = s_a * __uint_as_float(d0[j]);
+          }
+          if (n1 < tile.y) {
+            const int nn = min(16, tile.y - n1);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nn) srow[(n1 + j) * (C::STG_PITCH / 4)] = s_a * __uint_as_float(d1[j]);
+          }
+        }
+        named_bar_sync(1, C::EPI_THREADS);
+        // (2) y read-modify-write from the staging tile
+        if (bf16y) {
+          uint4 ycur[C::PF];
+#pragma unroll
+          for (int j = 0; j < C::PF; ++j) ycur[j] = ypf[j];
+          if (sb + 1 < n_sub) issue_y(sb + 1);
+#pragma unroll
+          for (int j = 0; j < C::PF; ++j) {
+            const int q = et + j * C::EPI_THREADS, n = q >> 4, c8 = q & 15;
+            if (n < tile.y) {
+              const uint32_t sa = smem_u32(sg + n * C::STG_PITCH + c8 * 32);
+              const float4 e0 = lds128f(sa), e1 = lds128f(sa + 16);
+              const uint4 yv = ycur[j];
+              uint4 o;
+              o.x = f32_to_bf16_rne(bf16lo(yv.x) + e0.x) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.x) + e0.y) << 16);
+              o.y = f32_to_bf16_rne(bf16lo(yv.y) + e0.z) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.y) + e0.w) << 16);
+              o.z = f32_to_bf16_rne(bf16lo(yv.z) + e1.x) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.z) + e1.y) << 16);
+              o.w = f32_to_bf16_rne(bf16lo(yv.w) + e1.z) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.w) + e1.w) << 16);
+              *reinterpret_cast<uint4*>(static_cast<uint16_t*>(t.y) + (long long)prow[j] * t.h_out + c0 + c8 * 8) = o;
+            }
+          }
+        } else {
+          // fp32 y (parity) or fp32 delta store (sharded delta mode): 4 columns per 16-byte chunk
+          for (int q = et; q < tile.y * (C::MSUB / 4); q += C::EPI_THREADS) {
+            const int n = q >> 5, c4 = q & 31;
+            const float4 e = lds128f(smem_u32(sg + n * C::STG_PITCH + c4 * 16));
+            const long long row = __ldg(pd.perm + tile.x + n);
+            float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + row * t.h_out + c0 + c4 * 4);
+            if (args.y_store) {
+              *yp = e;
+            } else {
+              float4 o = *yp;
+              o.x += e.x; o.y += e.y; o.z += e.z; o.w += e.w;
+              *yp = o;
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        fence_proxy_async_smem();              // smem writes -> visible to the bulk store (async proxy)
-        named_bar_sync(1, C::EPI_WARPS * 32);
-        if (et < tile.y) {
-          const long long c0 = (long long)ci * t.CI + (long long)sb * C::MSUB;
-          bulk_s2g(static_cast<char*>(t.y) + ((long long)my_row * t.h_out + c0) * esz, ys + et * rowbytes, rowbytes);
-          bulk_commit();
-          bulk_wait_read<0>();
-        }
-        mbar_arrive(&yempty[yb]);
+        sbuf ^= 1;  // the other staging buffer; its previous readers passed this sub-tile's barrier
         if (++acc == C::NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
-        if (++yb == 2) {
-          yb = 0;
-          yphase ^= 1;
-        }
-      }
-      mbar_arrive(&vempty[vb]);  // done with this item's row table
-      if (++vb == 2) {
-        vb = 0;
-        vphase ^= 1;
       }
     }
-    bulk_wait<0>();  // all y write-backs complete before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -619,6 +634,11 @@ cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid,
   cudaError_t e = set_smem_once(tc_shrink_kernel, ShrinkCfg::SMEM, mask);
   if (e != cudaSuccess) return e;
   tc_shrink_kernel<<<grid, ShrinkCfg::THREADS, ShrinkCfg::SMEM, stream>>>(args, pd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
+  tc_vreduce_kernel<<<grid * 4, 256, 0, stream>>>(args, pd);
   return cudaGetLastError();
 }
 
