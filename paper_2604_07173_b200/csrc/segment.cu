@@ -6,10 +6,16 @@
 // adapter into a single GEMM" (App. A.2.2); the paper presumes the
 // segments, so this kernel is ours (R9 for the ordering contract).
 //
-// One CTA of 1024 threads.  Each row becomes the 64-bit composite
-// (key << 32) | row; composites are unique, so ANY correct sort of them is
-// the stable sort by key -- a bitonic network over <= 16384 composites held
-// in shared memory (128 KB) is deterministic and bit-exact.
+// One CTA of 1024 threads, everything in shared memory (T <= 16384).
+//  * Fast path: 32-bit composites (key << ib) | row with an LSD radix sort on
+//    the key bits, 4 bits per pass.  Each pass is a stable block-wide counting
+//    sort: thread t owns a contiguous block of elements, per-digit counts are
+//    packed 16 x 16 bit into four 64-bit words and scanned with warp shuffles.
+//    Rows enter in index order and every pass is stable, so ties keep the
+//    original row order -- bit-exact with the stable-sort definition.
+//  * Fallback (key bits + row bits > 32): 64-bit composites sorted with a
+//    bitonic network; composites are unique, so any correct sort of them is
+//    the stable sort by key.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -48,90 +54,298 @@ __device__ int block_exclusive_scan(int v, int* tmp, int* total) {
   return warp_excl + x - v;
 }
 
-__global__ void __launch_bounds__(kSegThreads, 1)
-    segment_kernel(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T,
-                   int P, int E, int n_adapters, int world, int shard_rank, SegParams sp, PlanDev pd,
-                   int* __restrict__ err_flag) {
-  extern __shared__ __align__(16) unsigned long long keys[];  // [P]
-  __shared__ int scan_tmp[40];
-  const int tid = threadIdx.x;
-  const unsigned long long kInvalid = ~0ull;
+// Reads one row's ids; returns the key (a*E+e), or -1 for "no LoRA" / out of
+// range (flagged through *bad).
+LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int i, int E,
+                        int n_adapters, int world, int shard_rank, int& bad) {
+  const int a = adapter_ids[i];
+  const int e = expert_ids ? expert_ids[i] : 0;
+  const bool in_range = (a >= -1) && (a < n_adapters) && (a < 0 || (e >= 0 && e < E)) &&
+                        (a < 0 || (a % world) == shard_rank);
+  if (!in_range) bad = 1;
+  return (in_range && a >= 0) ? a * E + e : -1;
+}
 
-  // 1. composites
-  int bad = 0;
-  for (int i = tid; i < P; i += kSegThreads) {
-    unsigned long long c = kInvalid;
-    if (i < T) {
-      const int a = adapter_ids[i];
-      const int e = expert_ids ? expert_ids[i] : 0;
-      const bool in_range = (a >= -1) && (a < n_adapters) && (a < 0 || (e >= 0 && e < E)) &&
-                            (a < 0 || (a % world) == shard_rank);
-      if (!in_range) bad = 1;
-      if (in_range && a >= 0) {
-        const unsigned key = (unsigned)a * (unsigned)E + (unsigned)e;
-        c = ((unsigned long long)key << 32) | (unsigned)i;
+// ---------------------------------------------------------------------------
+// radix path: 16 digit counters x 16 bit packed in four 64-bit words
+// ---------------------------------------------------------------------------
+struct Cnt16 {
+  unsigned long long w[4];
+};
+LORA_DEVINL void cnt_add(Cnt16& c, int d) {
+  const unsigned long long inc = 1ull << ((d & 3) * 16);
+  const int q = d >> 2;
+  c.w[0] += q == 0 ? inc : 0ull;
+  c.w[1] += q == 1 ? inc : 0ull;
+  c.w[2] += q == 2 ? inc : 0ull;
+  c.w[3] += q == 3 ? inc : 0ull;
+}
+LORA_DEVINL int cnt_get(const Cnt16& c, int d) {
+  const int q = d >> 2;
+  const unsigned long long w = q == 0 ? c.w[0] : q == 1 ? c.w[1] : q == 2 ? c.w[2] : c.w[3];
+  return (int)((w >> ((d & 3) * 16)) & 0xFFFFull);
+}
+
+// one stable counting-sort pass on digit (v >> shift) & 15; blocked layout
+template <int EPT>
+__device__ void radix_pass(const uint32_t* in, uint32_t* out, int shift, unsigned long long* wtot, int* dbase) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Cnt16 c = {{0, 0, 0, 0}};
+#pragma unroll 4
+  for (int r = 0; r < EPT; ++r) cnt_add(c, (in[tid * EPT + r] >> shift) & 15);
+  Cnt16 inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, inc.w[w], o);
+      if (lane >= o) inc.w[w] += t;
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) wtot[warp * 4 + w] = inc.w[w];
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) inc.w[w] -= c.w[w];  // exclusive prefix within the warp (no borrow across fields)
+  __syncthreads();
+  if (warp == 0) {
+    Cnt16 own, x;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) own.w[w] = x.w[w] = wtot[lane * 4 + w];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, x.w[w], o);
+        if (lane >= o) x.w[w] += t;
       }
     }
-    keys[i] = c;
+    __syncwarp();
+#pragma unroll
+    for (int w = 0; w < 4; ++w) wtot[lane * 4 + w] = x.w[w] - own.w[w];  // exclusive warp offsets
+    if (lane == 31) {
+      int base = 0;
+      for (int d = 0; d < 16; ++d) {
+        dbase[d] = base;
+        base += cnt_get(x, d);
+      }
+    }
+  }
+  __syncthreads();
+  Cnt16 pre;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) pre.w[w] = wtot[warp * 4 + w] + inc.w[w];
+#pragma unroll 4
+  for (int r = 0; r < EPT; ++r) {
+    const uint32_t v = in[tid * EPT + r];
+    const int d = (v >> shift) & 15;
+    out[dbase[d] + cnt_get(pre, d)] = v;
+    cnt_add(pre, d);
+  }
+  __syncthreads();
+}
+
+// builds composites and sorts them; returns the buffer holding the result
+template <int EPT>
+__device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids,
+                                int T, int E, int n_adapters, int world, int shard_rank, int K, int kb, int ib,
+                                uint32_t* A, uint32_t* B, unsigned long long* wtot, int* dbase, int* err_flag,
+                                int* n_valid_out, int* scan_tmp) {
+  const int tid = threadIdx.x;
+  int bad = 0, nv = 0;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = tid * EPT + r;
+    int key = -1;
+    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, world, shard_rank, bad);
+    nv += key >= 0;
+    A[i] = ((uint32_t)(key >= 0 ? key : K) << ib) | (uint32_t)i;
   }
   if (bad) atomicOr(err_flag, 1);
-  __syncthreads();
+  int total;
+  block_exclusive_scan(nv, scan_tmp, &total);
+  *n_valid_out = total;
+  uint32_t* in = A;
+  uint32_t* out = B;
+  for (int sh = 0; sh < kb; sh += 4) {
+    radix_pass<EPT>(in, out, ib + sh, wtot, dbase);
+    uint32_t* t = in;
+    in = out;
+    out = t;
+  }
+  return in;
+}
 
-  // 2. bitonic sort, ascending
+// ---------------------------------------------------------------------------
+// bitonic fallback on 64-bit composites
+// ---------------------------------------------------------------------------
+LORA_DEVINL unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
+LORA_DEVINL unsigned long long umax64(unsigned long long a, unsigned long long b) { return a < b ? b : a; }
+
+template <int EPT>
+__device__ void bitonic_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T,
+                             int E, int n_adapters, int world, int shard_rank, unsigned long long* sm, int* err_flag,
+                             int* n_valid_out, int* scan_tmp) {
+  constexpr int P = kSegThreads * EPT;
+  const int tid = threadIdx.x;
+  unsigned long long v[EPT];
+  int bad = 0, nv = 0;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = tid * EPT + r;
+    int key = -1;
+    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, world, shard_rank, bad);
+    nv += key >= 0;
+    v[r] = key >= 0 ? (((unsigned long long)(unsigned)key << 32) | (unsigned)i) : ~0ull;
+  }
+  if (bad) atomicOr(err_flag, 1);
+  int total;
+  block_exclusive_scan(nv, scan_tmp, &total);
+  *n_valid_out = total;
   for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < P; i += kSegThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long x = keys[i], y = keys[ixj];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) {
-            keys[i] = y;
-            keys[ixj] = x;
+    int j = k >> 1;
+    for (; j >= 32 * EPT; j >>= 1) {  // shared memory
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) sm[tid * EPT + r] = v[r];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const int i = tid * EPT + r;
+        const unsigned long long o = sm[i ^ j];
+        const bool take_min = ((i & j) == 0) == ((i & k) == 0);
+        v[r] = take_min ? umin64(v[r], o) : umax64(v[r], o);
+      }
+    }
+    for (; j >= EPT; j >>= 1) {  // warp shuffles
+      const int lj = j / EPT;
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const int i = tid * EPT + r;
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], lj);
+        const bool take_min = ((i & j) == 0) == ((i & k) == 0);
+        v[r] = take_min ? umin64(v[r], o) : umax64(v[r], o);
+      }
+    }
+#pragma unroll
+    for (int jj = EPT / 2; jj > 0; jj >>= 1) {  // registers
+      if (jj < k) {
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+          const int p = r ^ jj;
+          if (p > r) {
+            const bool up = ((tid * EPT + r) & k) == 0;
+            const unsigned long long a = v[r], b = v[p];
+            if ((a > b) == up) {
+              v[r] = b;
+              v[p] = a;
+            }
           }
         }
       }
-      __syncthreads();
     }
   }
-
-  // 3. n_valid = index of the first invalid composite
-  __shared__ int s_nvalid;
-  if (tid == 0) s_nvalid = (keys[0] == kInvalid) ? 0 : P;
   __syncthreads();
-  for (int i = tid; i + 1 < P; i += kSegThreads)
-    if (keys[i] != kInvalid && keys[i + 1] == kInvalid) s_nvalid = i + 1;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) sm[tid * EPT + r] = v[r];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// kernel
+// ---------------------------------------------------------------------------
+template <bool radix>
+__global__ void __launch_bounds__(kSegThreads, 1)
+    segment_kernel(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T, int P,
+                   int E, int n_adapters, int world, int shard_rank, int kb, int ib, SegParams sp, PlanDev pd,
+                   int* __restrict__ err_flag) {
+  extern __shared__ __align__(16) uint8_t seg_smem[];
+  __shared__ int scan_tmp[40];
+  __shared__ unsigned long long wtot[32 * 4];
+  __shared__ int dbase[16];
+  __shared__ int s_nvalid;
+  const int tid = threadIdx.x;
+  const int EPT = P / kSegThreads;
+
+  // 1.+2. composites + sort; afterwards key(j) / row(j) of sorted position j
+  const uint32_t* srt32 = nullptr;
+  const unsigned long long* srt64 = nullptr;
+  int* segoff_s;  // [P+1] segment offsets in shared memory
+  if constexpr (radix) {
+    uint32_t* A = reinterpret_cast<uint32_t*>(seg_smem);
+    uint32_t* B = A + P + 4;  // each buffer P+4 ints: the free one later holds P+1 segment offsets
+    const int K = n_adapters * E;
+    uint32_t* res = nullptr;
+    switch (EPT) {
+      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+    }
+    srt32 = res;
+    segoff_s = reinterpret_cast<int*>(res == A ? B : A);  // the free buffer (P + 1 ints reserved)
+  } else {
+    unsigned long long* S64 = reinterpret_cast<unsigned long long*>(seg_smem);
+    switch (EPT) {
+      case 1: bitonic_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: bitonic_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: bitonic_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: bitonic_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
+      default: bitonic_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
+    }
+    srt64 = S64;
+    segoff_s = reinterpret_cast<int*>(S64 + P);
+  }
   __syncthreads();
   const int n_valid = s_nvalid;
+  const uint32_t idx_mask = (1u << ib) - 1u;
+  auto key_at = [&](int j) -> int {
+    if constexpr (radix) return (int)(srt32[j] >> ib);
+    else return (int)(srt64[j] >> 32);
+  };
+  auto row_at = [&](int j) -> int {
+    if constexpr (radix) return (int)(srt32[j] & idx_mask);
+    else return (int)(srt64[j] & 0xffffffffu);
+  };
 
-  // 4. perm + segment heads (each thread a contiguous chunk, so the scan is in order)
+  // 3. perm + segment heads (each thread a contiguous chunk, so the scan is in order)
   const int chunk = (n_valid + kSegThreads - 1) / kSegThreads;
   const int j0 = min(tid * chunk, n_valid), j1 = min(j0 + chunk, n_valid);
   int heads = 0;
+  int prev = j0 > 0 ? key_at(j0 - 1) : -1;
   for (int j = j0; j < j1; ++j) {
-    const unsigned long long c = keys[j];
-    pd.perm[j] = (int32_t)(c & 0xffffffffu);
-    if (j == 0 || (keys[j - 1] >> 32) != (c >> 32)) ++heads;
+    const int k = key_at(j);
+    pd.perm[j] = row_at(j);
+    heads += (j == 0 || k != prev);
+    prev = k;
   }
   int S;
   int seg = block_exclusive_scan(heads, scan_tmp, &S);
+  prev = j0 > 0 ? key_at(j0 - 1) : -1;
   for (int j = j0; j < j1; ++j) {
-    const unsigned long long c = keys[j];
-    if (j == 0 || (keys[j - 1] >> 32) != (c >> 32)) {
+    const int k = key_at(j);
+    if (j == 0 || k != prev) {
+      segoff_s[seg] = j;
       pd.seg_off[seg] = j;
-      pd.seg_key[seg] = (int32_t)(c >> 32);
+      pd.seg_key[seg] = k;
       ++seg;
     }
+    prev = k;
   }
-  if (tid == 0) pd.seg_off[S] = n_valid;
-  __syncthreads();  // global writes of this block visible to the block
+  if (tid == 0) {
+    segoff_s[S] = n_valid;
+    pd.seg_off[S] = n_valid;
+  }
+  __syncthreads();
 
-  // 5. work lists: CUDA-core groups (<= kGroupRows rows) and tcgen05 tiles (<= sp.tile_rows)
+  // 4. work lists: CUDA-core groups (<= kGroupRows rows) and tcgen05 tiles (<= sp.tile_rows)
   const int schunk = (S + kSegThreads - 1) / kSegThreads;
   const int s0 = min(tid * schunk, S), s1 = min(s0 + schunk, S);
   int ng = 0, nt = 0;
   for (int s = s0; s < s1; ++s) {
-    const int size = pd.seg_off[s + 1] - pd.seg_off[s];
+    const int size = segoff_s[s + 1] - segoff_s[s];
     if (sp.tc_enabled && size > sp.small_max)
       nt += (size + sp.tile_rows - 1) / sp.tile_rows;
     else
@@ -141,7 +355,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   int g = block_exclusive_scan(ng, scan_tmp, &NG);
   int t = block_exclusive_scan(nt, scan_tmp, &NT);
   for (int s = s0; s < s1; ++s) {
-    const int b = pd.seg_off[s], size = pd.seg_off[s + 1] - b, key = pd.seg_key[s];
+    const int b = segoff_s[s], size = segoff_s[s + 1] - b, key = key_at(b);
     const bool tc = sp.tc_enabled && size > sp.small_max;
     const int cap = tc ? sp.tile_rows : kGroupRows;
     const int n = (size + cap - 1) / cap;
@@ -166,28 +380,41 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   }
 }
 
-}  // namespace
+int bits_for(long long v) {  // bits needed to represent v (v >= 0)
+  int b = 0;
+  while ((1LL << b) <= v) ++b;
+  return b;
+}
 
-int segment_smem_bytes(int P) { return P * 8; }
+}  // namespace
 
 cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,
                            int world, int shard_rank, const SegParams& sp, const PlanDev& pd, int* err_flag,
                            cudaStream_t stream) {
-  int P = 1;
+  int P = kSegThreads;  // at least one composite per thread
   while (P < T) P <<= 1;
-  if (P < 2) P = 2;
-  const int smem = segment_smem_bytes(P);
+  const int ib = bits_for(P - 1);
+  const int kb = bits_for((long long)n_adapters * E);  // key K = n_adapters*E marks "no LoRA" (sorts last)
+  const int radix = (ib + kb <= 32) ? 1 : 0;
+  // radix: two u32 buffers (+1 int for the last segment offset); bitonic: u64 buffer + P+1 ints
+  const int smem = radix ? (2 * P + 8) * 4 : P * 8 + (P + 1) * 4;
   static unsigned long long attr_set = 0;  // per-device bitmask
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set & (1ull << dev))) {
-    cudaError_t e = cudaFuncSetAttribute(segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         segment_smem_bytes(kMaxPlanRows));
+    const int mx = kMaxPlanRows * 8 + (kMaxPlanRows + 1) * 4;
+    cudaError_t e = cudaFuncSetAttribute(segment_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(segment_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
     attr_set |= 1ull << dev;
   }
-  segment_kernel<<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, world,
-                                                   shard_rank, sp, pd, err_flag);
+  if (radix)
+    segment_kernel<true><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, world,
+                                                           shard_rank, kb, ib, sp, pd, err_flag);
+  else
+    segment_kernel<false><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, world,
+                                                            shard_rank, kb, ib, sp, pd, err_flag);
   return cudaGetLastError();
 }
 
