@@ -236,9 +236,11 @@ def run_ours(args, cfg, batch, slots):
 
     c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots],
                       [s.n_experts for s in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), max(T, 1), local)
-    if world > 1:
+    sharded = world > 1 or args.force_sharded
+    if sharded:
         uid = [B.lora_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
         s = B.lora_server_create_sharded(c, rank, world, uid[0])
     else:
         s = B.lora_server_create(c)
@@ -263,10 +265,10 @@ def run_ours(args, cfg, batch, slots):
         ys.append(y)
     ad = torch.from_numpy(batch.adapter_ids[r0:r1].copy()).to(dev)
     ex = torch.from_numpy(batch.expert_ids[r0:r1].copy()).to(dev)
-    plan = B.lora_plan_create(s, max(T, 1)) if world == 1 else None
+    plan = B.lora_plan_create(s, max(T, 1)) if not sharded else None
 
     def step():
-        if world == 1:
+        if not sharded:
             B.lora_plan_build(s, plan, ad, ex if E > 1 else None, T, E, stream)
             B.lora_apply_plan_multi(s, plan, slots, x_list, ys, dt_code, stream)
         else:
@@ -278,7 +280,7 @@ def run_ours(args, cfg, batch, slots):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    B.lora_profile_enable(s, args.steps * 8 + 16)
+    B.lora_profile_enable(s, args.steps * 32 + 16)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         if world > 1:
@@ -303,7 +305,7 @@ def run_ours(args, cfg, batch, slots):
 
     # e2e through the C-ABI with host buffers (N=1: lora_apply_multi_host)
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if not sharded and args.e2e_steps > 0:
         xh = {xb: xs[xb].cpu().pin_memory() for xb in xs}
         xh_list = [xh[cfg.slots[i].xbuf] for i in slots]
         yh = [y.cpu().pin_memory() for y in ys]
@@ -323,6 +325,44 @@ def run_ours(args, cfg, batch, slots):
         ems = e0.elapsed_time(e1) / args.e2e_steps
         e2e = {"value": cfg.n_tokens / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems, "api": "lora_apply_multi_host (pinned host)"}
+    elif sharded and args.e2e_steps > 0:
+        # this rank's rows from pinned host memory -> lora_apply_sharded -> y back to the host
+        xh = {xb: xs[xb].cpu().pin_memory() for xb in xs}
+        yh = [y.cpu().pin_memory() for y in ys]
+        adh = ad.cpu().pin_memory()
+        exh = ex.cpu().pin_memory()
+        h2d = adh.numel() * 4 + (exh.numel() * 4 if E > 1 else 0) + sum(v.numel() * 2 for v in xh.values()) + \
+            sum(y.numel() * ysz for y in yh)
+        d2h = sum(y.numel() * ysz for y in yh)
+
+        def e2e_step():
+            for xb in xs:
+                xs[xb].copy_(xh[xb], non_blocking=True)
+            for y, yhh in zip(ys, yh):
+                y.copy_(yhh, non_blocking=True)
+            ad.copy_(adh, non_blocking=True)
+            ex.copy_(exh, non_blocking=True)
+            B.lora_apply_sharded(s, slots, x_list, ad, ex if E > 1 else None, ys, dt_code, T, stream)
+            for y, yhh in zip(ys, yh):
+                yhh.copy_(y, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier() if world > 1 else None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            t_ = torch.tensor([ems], device=dev)
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            ems = float(t_.item())
+        e2e = {"value": cfg.n_tokens / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems,
+               "api": "pinned host -> lora_apply_sharded -> host (per rank; bytes are this rank's)"}
 
     if rank != 0:
         B.lora_server_destroy(s)
@@ -339,7 +379,7 @@ def run_ours(args, cfg, batch, slots):
     # dominant kernel: most device time per step; algorithmic bytes per launch
     per_kind_bytes = {k: alg[k] for k in ("segment", "simt_shrink", "simt_expand", "tc05_shrink", "tc05_expand")}
     roofline = None
-    if kern and world == 1:
+    if kern and not sharded:
         dom = max(kern, key=lambda n: kern[n]["ms_per_step"])
         bytes_per_launch = per_kind_bytes.get(dom, 0) * args.steps / kern[dom]["launches"]
         achieved = bytes_per_launch / (kern[dom]["ms_per_launch"] * 1e-3) / 1e9
@@ -363,17 +403,17 @@ def run_ours(args, cfg, batch, slots):
             "data": "synthetic (counter-hash weights/activations, Zipf(1.2) adapter ids, top-2 uniform experts)",
             "config": {"workload": cfg.name, "global_batch": cfg.n_tokens, "rows": T_glob, "slots": len(slots),
                        "rank": cfg.rank, "adapters": cfg.n_adapters,
-                       "parallelism": f"adapter-sharded dp{world} (NCCL all-to-all)" if world > 1 else "single GPU",
+                       "parallelism": f"adapter-sharded dp{world} (NCCL all-to-all)" if sharded else "single GPU",
                        "l2": f"inputs larger than L2 ({alg['total'] / 1e9:.1f} GB touched per step)"},
             "e2e": e2e,
-            "gpu_launches": launches if world == 1 else None,
+            "gpu_launches": launches,
             "roofline": roofline,
             "step_hbm": {"algorithmic_GB": alg["total"] / 1e9, "achieved_GBs": step_gbs,
                          "frac_measured": step_gbs / hbm_peak, "frac_nominal_8TBs": step_gbs / NOMINAL_HBM_GBS,
                          "tflops": alg["flops"] / (ms * 1e-3) / 1e12},
             "kernels": kern,
             "clocks": clk.summary()}
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not sharded and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, batch, slots, args.cpu_seconds)
         except Exception as e:  # the baseline is a report, never the product path
@@ -396,6 +436,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the sharded server even at N=1 (NCCL loopback; tests the N>1 code path)")
     args = ap.parse_args()
     cfg = li.CONFIGS[args.workload]
     batch = li.make_batch(cfg)

@@ -21,12 +21,23 @@ LORA_DEVINL float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 LORA_DEVINL float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 LORA_DEVINL float bf16_to_f32(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
 
-// round-to-nearest-even fp32 -> bf16 bits (finite inputs; NaN kept quiet)
+// round-to-nearest-even fp32 -> bf16 bits (hardware cvt.rn, one instruction)
 LORA_DEVINL uint16_t f32_to_bf16_rne(float f) {
-  uint32_t u = __float_as_uint(f);
-  if ((u & 0x7F800000u) == 0x7F800000u) return uint16_t((u >> 16) | ((u & 0xFFFF) ? 0x40 : 0));
-  u += 0x7FFFu + ((u >> 16) & 1u);
-  return uint16_t(u >> 16);
+  uint16_t r;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(f));
+  return r;
+}
+
+// hardware round-to-nearest-even conversions (F2FP): one instruction per pair
+LORA_DEVINL uint32_t pack_bf16x2_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+LORA_DEVINL uint16_t bf16_rn(float f) {
+  uint16_t r;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(f));
+  return r;
 }
 
 LORA_DEVINL uint32_t smem_u32(const void* p) {

@@ -452,8 +452,24 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.total_kc = kc;
     args.total_ci = ci;
     const int grid = s->sm_count;
+    // The CUDA-core shrink hands out (task, group) items round-robin; order the
+    // tasks by decreasing h_in so the longest items go first and the tail of
+    // the launch is made of the shortest ones.
+    MultiArgs sargs = args;
+    {
+      std::vector<int> order(nb);
+      for (int i = 0; i < nb; ++i) order[i] = i;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int a, int b) { return args.t[a].h_in > args.t[b].h_in; });
+      int kc2 = 0;
+      for (int i = 0; i < nb; ++i) {
+        sargs.t[i] = args.t[order[i]];
+        sargs.t[i].kc_base = kc2;
+        kc2 += sargs.t[i].n_kc;
+      }
+    }
     int pi = prof_start(s, st);
-    CK(s, launch_simt_shrink(s->r, args, p->dev, grid, st));
+    CK(s, launch_simt_shrink(s->r, sargs, p->dev, grid, st));
     prof_stop(s, pi, kKSimtShrink, st);
     if (tc) {
       pi = prof_start(s, st);

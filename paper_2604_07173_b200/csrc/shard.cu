@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -146,6 +147,41 @@ __global__ void gather_rows_kernel(const uint32_t* __restrict__ in, uint32_t* __
     const long long j = i / width;
     const int c = (int)(i - j * width);
     out[i] = in[(long long)idx[j] * width + c];
+  }
+}
+
+// out[j][:] = in[idx[j]][:], rows of `chunks` 16-byte chunks; one block row per output row
+__global__ void gather_rows16_kernel(const uint4* __restrict__ in, uint4* __restrict__ out,
+                                     const int32_t* __restrict__ idx, int n, int chunks) {
+  for (int j = blockIdx.y; j < n; j += gridDim.y) {
+    const uint4* src = in + (long long)idx[j] * chunks;
+    uint4* dst = out + (long long)j * chunks;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += gridDim.x * blockDim.x) dst[c] = src[c];
+  }
+}
+
+// y[idx[j]][c..c+4] = round(y + d[j][c..c+4]) (d fp32), 4 columns per thread
+__global__ void scatter_add4_kernel(void* __restrict__ y, int y_fp32, const float4* __restrict__ d,
+                                    const int32_t* __restrict__ idx, int n, int width) {
+  const int q4 = width >> 2;
+  for (int j = blockIdx.y; j < n; j += gridDim.y) {
+    const long long row = idx[j];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < q4; c += gridDim.x * blockDim.x) {
+      const float4 v = d[(long long)j * q4 + c];
+      if (y_fp32) {
+        float4* p = reinterpret_cast<float4*>(y) + row * q4 + c;
+        float4 o = *p;
+        o.x += v.x; o.y += v.y; o.z += v.z; o.w += v.w;
+        *p = o;
+      } else {
+        uint2* p = reinterpret_cast<uint2*>(y) + row * q4 + c;
+        const uint2 o = *p;
+        uint2 r;
+        r.x = pack_bf16x2_rn(bf16lo(o.x) + v.x, bf16hi(o.x) + v.y);
+        r.y = pack_bf16x2_rn(bf16lo(o.y) + v.z, bf16hi(o.y) + v.w);
+        *p = r;
+      }
+    }
   }
 }
 
@@ -327,7 +363,9 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
 
   // 1. bucket
   if (T > 0) {
+    const int pi = prof_start(s, st);
     bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, T, G, s->n_adapters, d_send_idx, d_counts, s->d_err);
+    prof_stop(s, pi, kKShardBucket, st);
   } else {
     CKS(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * G, st));
   }
@@ -345,19 +383,27 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
 
   // 3. pack + dispatch
   if (n_send > 0) {
+    int pi = prof_start(s, st);
     gather_rows_kernel<<<grid_of(n_send), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(adapter_ids),
                                                          reinterpret_cast<uint32_t*>(d_ids_send), d_send_idx, n_send,
                                                          1);
-    if (expert_ids)
+    prof_stop(s, pi, kKShardGather, st);
+    if (expert_ids) {
+      pi = prof_start(s, st);
       gather_rows_kernel<<<grid_of(n_send), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(expert_ids),
                                                            reinterpret_cast<uint32_t*>(d_ids_send + s->max_rows),
                                                            d_send_idx, n_send, 1);
-    else
+      prof_stop(s, pi, kKShardGather, st);
+    } else {
       CKS(cudaMemsetAsync(d_ids_send + s->max_rows, 0, sizeof(int32_t) * n_send, st));
-    for (size_t j = 0; j < xd.size(); ++j)
-      gather_rows_kernel<<<grid_of((long long)n_send * x_hin[j] / 2), 256, 0, st>>>(
-          static_cast<const uint32_t*>(xd[j]), reinterpret_cast<uint32_t*>(base + o_xs[j]), d_send_idx, n_send,
-          x_hin[j] / 2);
+    }
+    for (size_t j = 0; j < xd.size(); ++j) {
+      pi = prof_start(s, st);
+      const int chunks = x_hin[j] / 8;  // 16-byte chunks per bf16 row
+      gather_rows16_kernel<<<dim3((chunks + 255) / 256, std::min(n_send, 65535)), 256, 0, st>>>(
+          static_cast<const uint4*>(xd[j]), reinterpret_cast<uint4*>(base + o_xs[j]), d_send_idx, n_send, chunks);
+      prof_stop(s, pi, kKShardGather, st);
+    }
     CKS(cudaGetLastError());
   }
   CKN(api.GroupStart());
@@ -409,8 +455,10 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   if (n_send > 0) {
     for (int i = 0; i < n; ++i) {
       const int ho = s->slots[slots[i]].h_out;
-      scatter_add_kernel<<<grid_of((long long)n_send * ho), 256, 0, st>>>(
-          y[i], y_dtype == LORA_FP32, reinterpret_cast<const float*>(base + o_dr[i]), d_send_idx, n_send, ho);
+      const int pi = prof_start(s, st);
+      scatter_add4_kernel<<<dim3((ho / 4 + 255) / 256, std::min(n_send, 65535)), 256, 0, st>>>(
+          y[i], y_dtype == LORA_FP32, reinterpret_cast<const float4*>(base + o_dr[i]), d_send_idx, n_send, ho);
+      prof_stop(s, pi, kKShardScatter, st);
     }
     CKS(cudaGetLastError());
   }

@@ -340,10 +340,10 @@ __global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__
       s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
     }
     uint4 w;
-    w.x = f32_to_bf16_rne(s[0]) | ((uint32_t)f32_to_bf16_rne(s[1]) << 16);
-    w.y = f32_to_bf16_rne(s[2]) | ((uint32_t)f32_to_bf16_rne(s[3]) << 16);
-    w.z = f32_to_bf16_rne(s[4]) | ((uint32_t)f32_to_bf16_rne(s[5]) << 16);
-    w.w = f32_to_bf16_rne(s[6]) | ((uint32_t)f32_to_bf16_rne(s[7]) << 16);
+    w.x = pack_bf16x2_rn(s[0], s[1]);
+    w.y = pack_bf16x2_rn(s[2], s[3]);
+    w.z = pack_bf16x2_rn(s[4], s[5]);
+    w.w = pack_bf16x2_rn(s[6], s[7]);
     *reinterpret_cast<uint4*>(pd.vbf + t.vbf_off + ((long long)tile.x + n) * R + ((q ^ (n & 7)) * 8)) = w;
   }
 }
@@ -574,10 +574,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
               const float4 e0 = lds128f(sa), e1 = lds128f(sa + 16);
               const uint4 yv = ycur[j];
               uint4 o;
-              o.x = f32_to_bf16_rne(bf16lo(yv.x) + e0.x) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.x) + e0.y) << 16);
-              o.y = f32_to_bf16_rne(bf16lo(yv.y) + e0.z) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.y) + e0.w) << 16);
-              o.z = f32_to_bf16_rne(bf16lo(yv.z) + e1.x) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.z) + e1.y) << 16);
-              o.w = f32_to_bf16_rne(bf16lo(yv.w) + e1.z) | ((uint32_t)f32_to_bf16_rne(bf16hi(yv.w) + e1.w) << 16);
+              o.x = pack_bf16x2_rn(bf16lo(yv.x) + e0.x, bf16hi(yv.x) + e0.y);
+              o.y = pack_bf16x2_rn(bf16lo(yv.y) + e0.z, bf16hi(yv.y) + e0.w);
+              o.z = pack_bf16x2_rn(bf16lo(yv.z) + e1.x, bf16hi(yv.z) + e1.y);
+              o.w = pack_bf16x2_rn(bf16lo(yv.w) + e1.z, bf16hi(yv.w) + e1.w);
               *reinterpret_cast<uint4*>(static_cast<uint16_t*>(t.y) + (long long)prow[j] * t.h_out + c0 + c8 * 8) = o;
             }
           }
