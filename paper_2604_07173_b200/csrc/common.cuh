@@ -163,6 +163,75 @@ LORA_DEVINL float4 lds128f(uint32_t addr) {
 }
 
 // ---------------------------------------------------------------------------
+// Dynamic work distribution for persistent kernels.
+//
+// One producer lane per CTA takes item indices from a global counter
+// (atomicAdd) and publishes them to the CTA's consumer warps through a
+// shared-memory ring guarded by mbarriers; -1 ends the stream.  CTAs that
+// start late (another kernel still holds their SM) simply take fewer items.
+// The last CTA to finish resets the counters, so every launch starts at 0.
+// ---------------------------------------------------------------------------
+template <int QD>
+struct WorkQueue {
+  long long* item;  // smem [QD]
+  uint64_t* full;   // smem [QD], 1 arrival (producer)
+  uint64_t* empty;  // smem [QD], one arrival per consumer warp
+  LORA_DEVINL void init(int consumer_warps) {
+    for (int i = 0; i < QD; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], consumer_warps);
+    }
+  }
+};
+
+struct QueuePos {
+  int slot = 0;
+  uint32_t phase = 0;
+  LORA_DEVINL void advance(int qd) {
+    if (++slot == qd) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+// producer lane: fetch the next item (or -1) and publish it
+template <int QD>
+LORA_DEVINL long long wq_push_next(WorkQueue<QD>& q, QueuePos& p, unsigned long long* counter, long long n_items) {
+  long long it = (long long)atomicAdd(counter, 1ull);
+  if (it >= n_items) it = -1;
+  mbar_wait(&q.empty[p.slot], p.phase ^ 1);
+  q.item[p.slot] = it;
+  mbar_arrive(&q.full[p.slot]);
+  p.advance(QD);
+  return it;
+}
+
+// consumer warp: take the next item (all lanes get it; lane 0 releases the slot)
+template <int QD>
+LORA_DEVINL long long wq_pop(WorkQueue<QD>& q, QueuePos& p) {
+  mbar_wait(&q.full[p.slot], p.phase);
+  const long long it = q.item[p.slot];
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&q.empty[p.slot]);
+  p.advance(QD);
+  return it;
+}
+
+// end of a persistent launch (call with all threads after a __syncthreads):
+// the last CTA resets the item counter and the done counter
+LORA_DEVINL void wq_finish(unsigned long long* counter, unsigned int* done) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *counter = 0ull;
+      *done = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Weight-store layout
 //
 //   At (shrink operand): [U][h_in/64][r][64] bf16.  Each [r][64] tile has

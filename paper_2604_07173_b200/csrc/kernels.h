@@ -13,6 +13,8 @@ constexpr int kTileRows = 128;       // rows per tcgen05 tile (UMMA M / N)
 constexpr int kMaxTasks = 96;        // slots per multi-slot launch (param space)
 
 enum { kCntValid = 0, kCntSegs = 1, kCntGroups = 2, kCntTiles = 3, kCntWords = 8 };
+// work-counter slots of the persistent kernels
+enum { kWqSimtShrink = 0, kWqSimtExpand = 1, kWqTcShrink = 2, kWqTcExpand = 3, kWorkSlots = 8 };
 
 // Device view of a plan (all device pointers).
 struct PlanDev {
@@ -25,6 +27,8 @@ struct PlanDev {
   float* vpart;      // shrink partial sums, per slot region [n_kc][max_rows][r]
   uint16_t* vbf;     // tcgen05 path: complete v rounded to bf16, per slot region [max_rows][r]
   int* tc_cnt;       // tcgen05 shrink arrival counters [kMaxTasks][max_rows] (self-resetting)
+  unsigned long long* wctr;  // [kWorkSlots] dynamic item counters of the persistent kernels (self-resetting)
+  unsigned int* wdone;       // [kWorkSlots] finished-CTA counters
   int max_rows;
 };
 

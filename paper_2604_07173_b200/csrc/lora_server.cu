@@ -98,6 +98,9 @@ static void free_server(lora_server* s) {
   for (auto ev : s->events) cudaEventDestroy(ev);
   for (auto ev : s->prof_pool) cudaEventDestroy(ev);
   if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+  if (s->side_stream) cudaStreamDestroy(s->side_stream);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   delete s;
 }
 
@@ -129,6 +132,13 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   s->debug_sync = env_flag("LORA_DEBUG_SYNC");
   if (const char* e = std::getenv("LORA_SMALL_SEG_MAX")) s->small_seg_max = std::atoi(e);
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    free_server(s);
+    return fail(nullptr, LORA_ERR_CUDA, "stream / event creation failed");
+  }
+  s->concurrent_tc = !env_flag("LORA_SERIAL");
 
   const int r = cfg->rank;
   int kc_prefix = 0;
@@ -325,7 +335,9 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
             cudaMalloc(&d.tiles, sizeof(int4) * max_rows) == cudaSuccess &&
             cudaMalloc(&d.vpart, sizeof(float) * (size_t)s->total_kc * max_rows * s->r) == cudaSuccess &&
             cudaMalloc(&d.vbf, sizeof(uint16_t) * s->slots.size() * (size_t)max_rows * s->r) == cudaSuccess &&
-            cudaMalloc(&d.tc_cnt, sizeof(int) * (size_t)kMaxTasks * max_rows) == cudaSuccess;
+            cudaMalloc(&d.tc_cnt, sizeof(int) * (size_t)kMaxTasks * max_rows) == cudaSuccess &&
+            cudaMalloc(&d.wctr, sizeof(unsigned long long) * kWorkSlots) == cudaSuccess &&
+            cudaMalloc(&d.wdone, sizeof(unsigned int) * kWorkSlots) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     plan_destroy_impl(p);
@@ -333,6 +345,8 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
   }
   cudaMemset(d.counts, 0, sizeof(int32_t) * kCntWords);
   cudaMemset(d.tc_cnt, 0, sizeof(int) * (size_t)kMaxTasks * max_rows);
+  cudaMemset(d.wctr, 0, sizeof(unsigned long long) * kWorkSlots);
+  cudaMemset(d.wdone, 0, sizeof(unsigned int) * kWorkSlots);
   cudaMemset(d.seg_off, 0, sizeof(int32_t) * (max_rows + 1));
   *out = p;
   return LORA_OK;
@@ -349,6 +363,8 @@ void plan_destroy_impl(lora_plan* p) {
   cudaFree(p->dev.vpart);
   cudaFree(p->dev.vbf);
   cudaFree(p->dev.tc_cnt);
+  cudaFree(p->dev.wctr);
+  cudaFree(p->dev.wdone);
   delete p;
 }
 
@@ -468,24 +484,36 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
         kc2 += sargs.t[i].n_kc;
       }
     }
-    int pi = prof_start(s, st);
+    // The tcgen05 chain and the CUDA-core chain touch disjoint rows: run the
+    // tcgen05 chain on the side stream (fork/join with events, graph-capturable)
+    // so its CTAs fill the SMs the persistent CUDA-core kernels leave idle.
+    const bool fork = tc && s->concurrent_tc;
+    cudaStream_t tst = fork ? s->side_stream : st;
+    if (fork) {
+      CK(s, cudaEventRecord(s->ev_fork, st));
+      CK(s, cudaStreamWaitEvent(tst, s->ev_fork, 0));
+    }
+    int pi;
+    if (tc) {
+      pi = prof_start(s, tst);
+      CK(s, launch_tc_shrink(args, p->dev, grid, tst));
+      prof_stop(s, pi, kKTcShrink, tst);
+      pi = prof_start(s, tst);
+      CK(s, launch_tc_vreduce(args, p->dev, grid, tst));
+      prof_stop(s, pi, kKTcVreduce, tst);
+      pi = prof_start(s, tst);
+      CK(s, launch_tc_expand(args, p->dev, grid, tst));
+      prof_stop(s, pi, kKTcExpand, tst);
+    }
+    pi = prof_start(s, st);
     CK(s, launch_simt_shrink(s->r, sargs, p->dev, grid, st));
     prof_stop(s, pi, kKSimtShrink, st);
-    if (tc) {
-      pi = prof_start(s, st);
-      CK(s, launch_tc_shrink(args, p->dev, grid, st));
-      prof_stop(s, pi, kKTcShrink, st);
-    }
     pi = prof_start(s, st);
     CK(s, launch_simt_expand(s->r, args, p->dev, grid, st));
     prof_stop(s, pi, kKSimtExpand, st);
-    if (tc) {
-      pi = prof_start(s, st);
-      CK(s, launch_tc_vreduce(args, p->dev, grid, st));
-      prof_stop(s, pi, kKTcVreduce, st);
-      pi = prof_start(s, st);
-      CK(s, launch_tc_expand(args, p->dev, grid, st));
-      prof_stop(s, pi, kKTcExpand, st);
+    if (fork) {
+      CK(s, cudaEventRecord(s->ev_join, tst));
+      CK(s, cudaStreamWaitEvent(st, s->ev_join, 0));
     }
   }
   if (s->debug_sync) {

@@ -33,6 +33,8 @@ namespace lora {
 
 namespace {
 
+constexpr int kQD = 4;  // work-queue depth (items published ahead of the consumers)
+
 template <int R>
 struct SimtCfg {
   static constexpr int NWC = 8;          // consumer warps
@@ -51,7 +53,7 @@ struct SimtCfg {
   static constexpr int RED_BYTES = NJG * GR * R * 4;
   static constexpr int NST_RAW = (SMEM_BUDGET - RED_BYTES) / S_STAGE;
   static constexpr int NST = NST_RAW > 8 ? 8 : (NST_RAW < 2 ? 2 : NST_RAW);
-  static constexpr int SHRINK_SMEM = 1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8;
+  static constexpr int SHRINK_SMEM = 1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8;
   // expand
   static constexpr int SC_MAX = NCT;        // one B row (output column) per consumer thread per stage
   static constexpr int B_STAGE = SC_MAX * R * 2;
@@ -59,7 +61,7 @@ struct SimtCfg {
   static constexpr int E_STAGE = B_STAGE + 1024 * ((V_BYTES + 1023) / 1024);
   static constexpr int NSTE_RAW = SMEM_BUDGET / E_STAGE;
   static constexpr int NSTE = NSTE_RAW > 16 ? 16 : NSTE_RAW;
-  static constexpr int EXPAND_SMEM = 1024 + NSTE * E_STAGE + 2 * NSTE * 8;
+  static constexpr int EXPAND_SMEM = 1024 + NSTE * E_STAGE + 2 * NSTE * 8 + 3 * kQD * 8;
   static_assert(S_STAGE % 1024 == 0 && E_STAGE % 1024 == 0, "stage alignment");
   static_assert(SHRINK_SMEM <= 112 * 1024 && EXPAND_SMEM <= 112 * 1024, "two CTAs per SM");
 };
@@ -165,12 +167,14 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   float* red = reinterpret_cast<float*>(smem + C::NST * C::S_STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NST * C::S_STAGE + C::RED_BYTES);
   uint64_t* empty = full + C::NST;
+  WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::NST), empty + C::NST + kQD, empty + C::NST + 2 * kQD};
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NWC);
     }
+    wq.init(C::NWC);
     fence_mbar_init();
   }
   __syncthreads();
@@ -185,7 +189,10 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      QueuePos qp;
+      for (;;) {
+        const long long it = wq_push_next(wq, qp, pd.wctr + kWqSimtShrink, n_items);
+        if (it < 0) break;
         const int ti = (int)(it / n_groups), gi = (int)(it - (long long)ti * n_groups);
         const SlotTask& t = args.t[ti];
         const int4 g = pd.groups[gi];
@@ -213,28 +220,32 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         }
       }
     }
-    return;
-  }
-
-  // ===================== consumers =====================
-  int stage = 0;
-  uint32_t phase = 0;
-  for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int ti = (int)(it / n_groups), gi = (int)(it - (long long)ti * n_groups);
-    const SlotTask& t = args.t[ti];
-    const int4 g = pd.groups[gi];
-    float* vb = pd.vpart + t.vpart_off;
-    switch (g.y) {
-      case 1: shrink_item<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-      case 2: shrink_item<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-      case 3: shrink_item<R, 3>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-      case 4: shrink_item<R, 4>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-      case 5: shrink_item<R, 5>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-      case 6: shrink_item<R, 6>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-      case 7: shrink_item<R, 7>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-      default: shrink_item<R, 8>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+  } else {
+    // ===================== consumers =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    QueuePos qp;
+    for (;;) {
+      const long long it = wq_pop(wq, qp);
+      if (it < 0) break;
+      const int ti = (int)(it / n_groups), gi = (int)(it - (long long)ti * n_groups);
+      const SlotTask& t = args.t[ti];
+      const int4 g = pd.groups[gi];
+      float* vb = pd.vpart + t.vpart_off;
+      switch (g.y) {
+        case 1: shrink_item<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 2: shrink_item<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 3: shrink_item<R, 3>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 4: shrink_item<R, 4>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 5: shrink_item<R, 5>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 6: shrink_item<R, 6>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 7: shrink_item<R, 7>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        default: shrink_item<R, 8>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+      }
     }
   }
+  __syncthreads();
+  wq_finish(pd.wctr + kWqSimtShrink, pd.wdone + kWqSimtShrink);
 }
 
 // ---------------------------------------------------------------------------
@@ -292,6 +303,11 @@ LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int cr, const ExpandPo
 }
 
 template <int R>
+__device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, const PlanDev& pd, uint8_t* smem,
+                                                      uint64_t* full, uint64_t* empty, WorkQueue<kQD>& wq,
+                                                      int n_groups, long long n_items);
+
+template <int R>
 __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
     simt_expand_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   using C = SimtCfg<R>;
@@ -299,12 +315,15 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   uint8_t* smem = align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NSTE * C::E_STAGE);
   uint64_t* empty = full + C::NSTE;
+  WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::NSTE), empty + C::NSTE + kQD,
+                    empty + C::NSTE + 2 * kQD};
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NSTE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NWC);
     }
+    wq.init(C::NWC);
     fence_mbar_init();
   }
   __syncthreads();
@@ -319,7 +338,10 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      QueuePos qp;
+      for (;;) {
+        const long long it = wq_push_next(wq, qp, pd.wctr + kWqSimtExpand, n_items);
+        if (it < 0) break;
         const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
         const SlotTask& t = args.t[find_task_ci(args, cig)];
         const int ci = cig - t.ci_base;
@@ -342,10 +364,20 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         }
       }
     }
-    return;
+  } else {
+    simt_expand_consumers<R>(args, pd, smem, full, empty, wq, n_groups, n_items);
   }
+  __syncthreads();
+  wq_finish(pd.wctr + kWqSimtExpand, pd.wdone + kWqSimtExpand);
+}
 
-  // ===================== consumers =====================
+// consumer warps of simt_expand_kernel
+template <int R>
+__device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, const PlanDev& pd, uint8_t* smem,
+                                                      uint64_t* full, uint64_t* empty, WorkQueue<kQD>& wq,
+                                                      int n_groups, long long n_items) {
+  using C = SimtCfg<R>;
+  const int lane = lane_id();
   const int ct = threadIdx.x;
   int stage = 0;
   uint32_t phase = 0;
@@ -391,8 +423,12 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
     for (int r = 0; r < C::GR; ++r) yrow[r] = r < p.rows ? p.perm_rows[r] : 0;
   };
 
+  QueuePos qp;
   ExpandPos cur;
-  locate(blockIdx.x, cur);
+  {
+    const long long it0 = wq_pop(wq, qp);
+    locate(it0 < 0 ? n_items : it0, cur);
+  }
   if (cur.it < n_items) {
     load_rows(cur);
     load_y(cur);
@@ -424,8 +460,9 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       cur.st += 1;
       cur.c0 += cur.sc;
     } else {
-      locate(cur.it + gridDim.x, cur);
-      if (cur.it >= n_items) break;
+      const long long nit = wq_pop(wq, qp);
+      if (nit < 0) break;
+      locate(nit, cur);
       load_rows(cur);
     }
     load_y(cur);
