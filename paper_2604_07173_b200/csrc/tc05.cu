@@ -113,6 +113,7 @@ LORA_DEVINL long long unit_of_key(int key, int E, int world) {
 }
 
 constexpr int R = 64;  // tcgen05 path rank
+constexpr int kQD = 4;  // work-queue depth
 
 // ===========================================================================
 // shrink
@@ -146,9 +147,13 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
   uint64_t* tfull = bars + 2 * C::NST;    // [2]    MMA commit -> epilogue
   uint64_t* tempty = tfull + 2;           // [2]    epilogue -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  long long* wq_items = reinterpret_cast<long long*>(tmem_slot + 2);
+  WorkQueue<kQD> wq{wq_items, reinterpret_cast<uint64_t*>(wq_items + kQD),
+                    reinterpret_cast<uint64_t*>(wq_items + kQD) + kQD};
 
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
+    wq.init(C::EPI_WARPS + 1 + 3);  // epilogue, MMA and the producer warps that pop (warp PROD_WARP0 fetches)
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(&full[s], C::PROD_THREADS + 1);
       mbar_init(&empty[s], 1);
@@ -175,7 +180,16 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
     uint32_t phase = 0;
     int pend_stage[C::LAG + 1];
     int npend = 0;
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    QueuePos qp;
+    for (;;) {
+      long long it = -1;
+      if (warp == C::PROD_WARP0) {
+        if (lane == 0) it = wq_push_next(wq, qp, pd.wctr + kWqTcShrink, n_items);
+        it = __shfl_sync(0xffffffffu, it, 0);
+      } else {
+        it = wq_pop(wq, qp);
+      }
+      if (it < 0) break;
       const int kcg = (int)(it / n_tiles), ti = (int)(it - (long long)kcg * n_tiles);
       const SlotTask& t = args.t[find_task_kc(args, kcg)];
       const int kc = kcg - t.kc_base;
@@ -237,7 +251,10 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr uint32_t idesc = idesc_bf16(128, C::ACC_COLS);
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    QueuePos qp;
+    for (;;) {
+      const long long it = wq_pop(wq, qp);
+      if (it < 0) break;
       const int kcg = (int)(it / n_tiles);
       const SlotTask& t = args.t[find_task_kc(args, kcg)];
       const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
@@ -278,7 +295,10 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const int row_in_tile = warp * 32 + lane;  // TMEM lane
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    QueuePos qp;
+    for (;;) {
+      const long long it = wq_pop(wq, qp);
+      if (it < 0) break;
       const int kcg = (int)(it / n_tiles), ti = (int)(it - (long long)kcg * n_tiles);
       const SlotTask& t = args.t[find_task_kc(args, kcg)];
       const int kc = kcg - t.kc_base;
@@ -305,6 +325,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  wq_finish(pd.wctr + kWqTcShrink, pd.wdone + kWqTcShrink);
   if (warp == C::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
@@ -398,9 +419,13 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   uint64_t* tfull = vempty + 2;                // [2]  accumulator ready
   uint64_t* tempty = tfull + 2;                // [2]  accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  long long* wq_items = reinterpret_cast<long long*>(tmem_slot + 2);
+  WorkQueue<kQD> wq{wq_items, reinterpret_cast<uint64_t*>(wq_items + kQD),
+                    reinterpret_cast<uint64_t*>(wq_items + kQD) + kQD};
 
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
+    wq.init(C::EPI_WARPS + 1);  // epilogue + MMA warps pop; the TMA warp fetches
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -428,7 +453,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const uint64_t pol = policy_evict_first();
       int stage = 0, vb = 0;
       uint32_t phase = 0, vphase = 0;
-      for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+      QueuePos qp;
+      for (;;) {
+        const long long it = wq_push_next(wq, qp, pd.wctr + kWqTcExpand, n_items);
+        if (it < 0) break;
         const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
         const SlotTask& t = args.t[find_task_ci(args, cig)];
         const int ci = cig - t.ci_base;
@@ -459,7 +487,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     // ===================== MMA issuer =====================
     int stage = 0, acc = 0, vb = 0;
     uint32_t phase = 0, acc_phase = 0, vphase = 0;
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    QueuePos qp;
+    for (;;) {
+      const long long it = wq_pop(wq, qp);
+      if (it < 0) break;
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
       const SlotTask& t = args.t[find_task_ci(args, cig)];
       const int4 tile = pd.tiles[ti];
@@ -506,7 +537,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     const bool bf16y = !(args.y_fp32 || args.y_store);
     uint4 ypf[C::PF];                             // prefetched y chunks (bf16 mode)
     int prow[C::PF];                              // y row of each chunk
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    QueuePos qp;
+    for (;;) {
+      const long long it = wq_pop(wq, qp);
+      if (it < 0) break;
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
       const SlotTask& t = args.t[find_task_ci(args, cig)];
       const int ci = cig - t.ci_base;
@@ -607,6 +641,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  wq_finish(pd.wctr + kWqTcExpand, pd.wdone + kWqTcExpand);
   if (warp == C::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
