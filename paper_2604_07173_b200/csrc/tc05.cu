@@ -380,27 +380,29 @@ LORA_DEVINL void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 LORA_DEVINL void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ===========================================================================
-// expand (swap-AB).  Per 128-column sub-tile: D[128 cols x N rows] in TMEM;
-// the epilogue moves D through a double-buffered fp32 staging tile in shared
-// memory (lane = column, conflict-free) and then read-modify-writes y with
-// 16-byte vector accesses, the y loads of the next sub-tile in flight.
+// expand (swap-AB).  Per 128-column sub-tile: D[128 cols x N rows] in TMEM
+// (four accumulators).  Two epilogue groups of 8 warps take alternate
+// sub-tiles, so two sub-tiles are in the epilogue at any time; each group
+// moves D through its fp32 staging tile in shared memory (lane = column,
+// conflict-free) and read-modify-writes y with 16-byte vector accesses, the
+// y loads of its next sub-tile in flight.
 // ===========================================================================
 struct ExpandCfg {
-  static constexpr int EPI_WARPS = 16;  // warps 0-15: epilogue (TMEM lanes by warp % 4, rows by warp / 4)
+  static constexpr int EPI_WARPS = 16;  // warps 0-15: epilogue, group = warp / 8
+  static constexpr int GROUP_THREADS = 256;
   static constexpr int TMA_WARP = 16;   // warp 16: v tile + Bt bulk copies
   static constexpr int MMA_WARP = 17;   // warp 17: TMEM alloc + MMA
   static constexpr int THREADS = 18 * 32;
-  static constexpr int EPI_THREADS = EPI_WARPS * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (M)
   static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
   static constexpr int NST = 3;
   static constexpr int V_TILE = kTileRows * 128;       // 16 KB (N <= 128 rows x 64 bf16)
   static constexpr int STG_PITCH = MSUB * 4 + 16;      // fp32 staging row (+16 B: fewer bank conflicts)
-  static constexpr int STG = kTileRows * STG_PITCH;    // 66 KB
-  static constexpr int NACC = 2;
+  static constexpr int STG = kTileRows * STG_PITCH;    // 66 KB per group
+  static constexpr int NACC = 4;
   static constexpr int ACC_COLS = kTileRows;           // N columns per accumulator
-  static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 256
-  static constexpr int PF = kTileRows * (MSUB / 8) / EPI_THREADS;  // 16-byte bf16 chunks per thread per sub-tile (4)
+  static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 512
+  static constexpr int PF = kTileRows * (MSUB / 8) / GROUP_THREADS;  // 16-byte bf16 chunks per thread (8)
   static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 2 * STG + 512;
 };
 
@@ -410,15 +412,15 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE] swizzled MMA operand
-  uint8_t* stg = vtile + 2 * C::V_TILE;        // [2][128][STG_PITCH] fp32 delta staging
+  uint8_t* stg = vtile + 2 * C::V_TILE;        // [group][128][STG_PITCH] fp32 delta staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + 2 * C::STG);
   uint64_t* full = bars;                       // [NST] Bt landed
   uint64_t* empty = bars + C::NST;             // [NST] MMA done with Bt stage
   uint64_t* vfull = bars + 2 * C::NST;         // [2]  v tile landed
   uint64_t* vempty = vfull + 2;                // [2]  MMA done with the v tile
-  uint64_t* tfull = vempty + 2;                // [2]  accumulator ready
-  uint64_t* tempty = tfull + 2;                // [2]  accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = vempty + 2;                // [NACC] accumulator ready
+  uint64_t* tempty = tfull + C::NACC;          // [NACC] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NACC);
   long long* wq_items = reinterpret_cast<long long*>(tmem_slot + 2);
   WorkQueue<kQD> wq{wq_items, reinterpret_cast<uint64_t*>(wq_items + kQD),
                     reinterpret_cast<uint64_t*>(wq_items + kQD) + kQD};
@@ -433,8 +435,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&vfull[a], 1);
       mbar_init(&vempty[a], 1);
+    }
+    for (int a = 0; a < C::NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], C::EPI_THREADS);
+      mbar_init(&tempty[a], C::GROUP_THREADS);
     }
     fence_mbar_init();
   }
@@ -485,8 +489,9 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     }
   } else if (warp == C::MMA_WARP) {
     // ===================== MMA issuer =====================
-    int stage = 0, acc = 0, vb = 0;
-    uint32_t phase = 0, acc_phase = 0, vphase = 0;
+    int stage = 0, vb = 0;
+    uint32_t phase = 0, vphase = 0;
+    long long k = 0;  // global sub-tile counter -> accumulator k % NACC
     QueuePos qp;
     for (;;) {
       const long long it = wq_pop(wq, qp);
@@ -499,16 +504,17 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const int n_sub = t.CI / C::MSUB;
       mbar_wait(&vfull[vb], vphase);
       const uint32_t va = smem_u32(vtile + vb * C::V_TILE);
-      for (int sb = 0; sb < n_sub; ++sb) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+      for (int sb = 0; sb < n_sub; ++sb, ++k) {
+        const int acc = (int)(k % C::NACC);
+        mbar_wait(&tempty[acc], (uint32_t)((k / C::NACC) & 1) ^ 1);
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t ba = smem_u32(smem + stage * C::B_SUB);
           const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
 #pragma unroll
-          for (int k = 0; k < R / 16; ++k)
-            umma_bf16(d_tmem, sw128_desc(ba + k * 32), sw128_desc(va + k * 32), idesc, k > 0 ? 1u : 0u);
+          for (int kk = 0; kk < R / 16; ++kk)
+            umma_bf16(d_tmem, sw128_desc(ba + kk * 32), sw128_desc(va + kk * 32), idesc, kk > 0 ? 1u : 0u);
           umma_commit(&empty[stage]);
           umma_commit(&tfull[acc]);
           if (sb == n_sub - 1) umma_commit(&vempty[vb]);
@@ -518,10 +524,6 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           stage = 0;
           phase ^= 1;
         }
-        if (++acc == C::NACC) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
       }
       if (++vb == 2) {
         vb = 0;
@@ -529,14 +531,16 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue =====================
-    int acc = 0, sbuf = 0;
-    uint32_t acc_phase = 0;
-    const int et = threadIdx.x;                   // 0..511
-    const int col = et & 127, quarter = et >> 7;  // TMEM lane (column) and row quarter for phase (1)
+    // ===================== epilogue (two groups, alternate sub-tiles) =====================
+    const int grp = warp >> 3, wl = warp & 7;
+    const int gt = threadIdx.x & 255;            // thread within the group
+    const int col = (wl & 3) * 32 + lane;        // TMEM lane = output column within the sub-tile
+    const int half = wl >> 2;                    // row half for phase (1)
     const bool bf16y = !(args.y_fp32 || args.y_store);
-    uint4 ypf[C::PF];                             // prefetched y chunks (bf16 mode)
-    int prow[C::PF];                              // y row of each chunk
+    uint8_t* sg = stg + grp * C::STG;
+    uint4 ypf[C::PF];                            // prefetched y chunks (bf16 mode)
+    int prow[C::PF];                             // y row of each chunk
+    long long k = 0;                             // global sub-tile counter (same as the MMA warp's)
     QueuePos qp;
     for (;;) {
       const long long it = wq_pop(wq, qp);
@@ -548,65 +552,55 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const float s_a = args.scale[tile.z / t.E];
       const int n_sub = t.CI / C::MSUB;
       const long long cbase = (long long)ci * t.CI;
-      // chunk j of this thread: row n = (et + j*512) / 16, columns 8*((et + j*512) % 16) ..+8
+      // chunk j of this thread: row n = (gt + j*256) / 16, columns 8*((gt + j*256) % 16) ..+8
 #pragma unroll
       for (int j = 0; j < C::PF; ++j) {
-        const int n = (et + j * C::EPI_THREADS) >> 4;
+        const int n = (gt + j * C::GROUP_THREADS) >> 4;
         prow[j] = n < tile.y ? __ldg(pd.perm + tile.x + n) : 0;
       }
       auto issue_y = [&](int sb) {
 #pragma unroll
         for (int j = 0; j < C::PF; ++j) {
-          const int q = et + j * C::EPI_THREADS, n = q >> 4, c8 = q & 15;
+          const int q = gt + j * C::GROUP_THREADS, n = q >> 4, c8 = q & 15;
           if (n < tile.y)
             ypf[j] = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(t.y) + (long long)prow[j] * t.h_out +
                                                      cbase + (long long)sb * C::MSUB + c8 * 8);
         }
       };
-      if (bf16y) issue_y(0);
-      for (int sb = 0; sb < n_sub; ++sb) {
+      const int first = (int)((grp - k) & 1);  // this group's first sub-tile in the item
+      if (bf16y && first < n_sub) issue_y(first);
+      for (int sb = first; sb < n_sub; sb += 2) {
+        const long long kk = k + sb;
+        const int acc = (int)(kk % C::NACC);
         const long long c0 = cbase + (long long)sb * C::MSUB;
-        uint8_t* sg = stg + sbuf * C::STG;
-        // (1) TMEM -> staging (this warp: lanes 32*(warp%4).., rows 16*quarter + 64*k)
-        mbar_wait(&tfull[acc], acc_phase);
+        // (1) TMEM -> staging (this warp: lanes 32*(wl%4).., rows 16*half + 32*i)
+        mbar_wait(&tfull[acc], (uint32_t)((kk / C::NACC) & 1));
         tc_fence_after();
         {
           const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + acc * C::ACC_COLS;
-          uint32_t d0[16], d1[16];
-          const int n0 = 16 * quarter, n1 = n0 + 64;
-          if (n0 < tile.y) tmem_ld16_nowait(taddr + n0, d0);
-          if (n1 < tile.y) tmem_ld16_nowait(taddr + n1, d1);
-          tmem_wait_ld();
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
           float* srow = reinterpret_cast<float*>(sg) + col;
-          if (n0 < tile.y) {
+          for (int n0 = 16 * half; n0 < tile.y; n0 += 32) {
+            uint32_t d0[16];
+            tmem_ld16_nowait(taddr + n0, d0);
+            tmem_wait_ld();
             const int nn = min(16, tile.y - n0);
 #pragma unroll
             for (int j = 0; j < 16; ++j)
               if (j < nn) srow[(n0 + j) * (C::STG_PITCH / 4)] = s_a * __uint_as_float(d0[j]);
           }
-          if (n1 < tile.y) {
-            const int nn = min(16, tile.y - n1);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nn) srow[(n1 + j) * (C::STG_PITCH / 4)] = s_a * __uint_as_float(d1[j]);
-          }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
         }
-        named_bar_sync(1, C::EPI_THREADS);
+        named_bar_sync(1 + grp, C::GROUP_THREADS);
         // (2) y read-modify-write from the staging tile
         if (bf16y) {
-          uint4 ycur[C::PF];
-#pragma unroll
-          for (int j = 0; j < C::PF; ++j) ycur[j] = ypf[j];
-          if (sb + 1 < n_sub) issue_y(sb + 1);
 #pragma unroll
           for (int j = 0; j < C::PF; ++j) {
-            const int q = et + j * C::EPI_THREADS, n = q >> 4, c8 = q & 15;
+            const int q = gt + j * C::GROUP_THREADS, n = q >> 4, c8 = q & 15;
             if (n < tile.y) {
               const uint32_t sa = smem_u32(sg + n * C::STG_PITCH + c8 * 32);
               const float4 e0 = lds128f(sa), e1 = lds128f(sa + 16);
-              const uint4 yv = ycur[j];
+              const uint4 yv = ypf[j];
               uint4 o;
               o.x = pack_bf16x2_rn(bf16lo(yv.x) + e0.x, bf16hi(yv.x) + e0.y);
               o.y = pack_bf16x2_rn(bf16lo(yv.y) + e0.z, bf16hi(yv.y) + e0.w);
@@ -615,9 +609,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
               *reinterpret_cast<uint4*>(static_cast<uint16_t*>(t.y) + (long long)prow[j] * t.h_out + c0 + c8 * 8) = o;
             }
           }
+          if (sb + 2 < n_sub) issue_y(sb + 2);  // in flight across the other group's sub-tile
         } else {
           // fp32 y (parity) or fp32 delta store (sharded delta mode): 4 columns per 16-byte chunk
-          for (int q = et; q < tile.y * (C::MSUB / 4); q += C::EPI_THREADS) {
+          for (int q = gt; q < tile.y * (C::MSUB / 4); q += C::GROUP_THREADS) {
             const int n = q >> 5, c4 = q & 31;
             const float4 e = lds128f(smem_u32(sg + n * C::STG_PITCH + c4 * 16));
             const long long row = __ldg(pd.perm + tile.x + n);
@@ -631,12 +626,9 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
             }
           }
         }
-        sbuf ^= 1;  // the other staging buffer; its previous readers passed this sub-tile's barrier
-        if (++acc == C::NACC) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
+        named_bar_sync(1 + grp, C::GROUP_THREADS);  // staging free for this group's next sub-tile
       }
+      k += n_sub;
     }
   }
   tc_fence_before();
