@@ -9,7 +9,8 @@ of one Mixtral MoE layer, multi-slot apply).  Default workload: BASELINE.json
 config 5 (mixtral_sharded: 2048 adapters, 4096 tokens -> 8192 rows), the
 config the metric is quoted on at 1/2/4/8 GPUs; it fits one B200 (116 GB of
 weights).  N=1 runs the unsharded server; N>1 runs the adapter-sharded server
-(owner(a) = a mod N, NCCL all-to-all over NVLink), launched by torchrun.
+(owner(a) = (a - h) mod N for a >= h, the h hottest adapters replicated on
+every rank; NCCL send/recv over NVLink), launched by torchrun.
 
 Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
 """
@@ -234,9 +235,23 @@ def run_ours(args, cfg, batch, slots):
     dt_code = B.LORA_FP32 if cfg.y_dtype == "fp32" else B.LORA_BF16
     ysz = 4 if cfg.y_dtype == "fp32" else 2
 
-    c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots],
-                      [s.n_experts for s in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), max(T, 1), local)
     sharded = world > 1 or args.force_sharded
+    if args.force_sharded and world == 1:
+        os.environ["LORA_SHARD_LOOPBACK"] = "1"  # every row through the NCCL exchange (to itself)
+    n_rep, rep_table = 0, None
+    if sharded:
+        # popularity-aware placement (R19): replicate the hottest
+        # adapters on every rank; auto = the host cost model's choice
+        from paper_2604_07173_b200 import placement as PL
+        ub, rb, xb = PL.slot_bytes([cfg.slots[i].h_in for i in slots], [cfg.slots[i].h_out for i in slots],
+                                   [cfg.slots[i].xbuf for i in slots], cfg.rank, ysz, ysz)
+        src = PL.sources_of_rows(cfg.n_tokens, k, world)
+        ch = PL.choose_n_replicated(batch.adapter_ids, batch.expert_ids if E > 1 else None, src, world, ub, rb, xb)
+        n_rep = ch["n_replicated"] if args.n_replicated < 0 else args.n_replicated
+        rep_table = {str(h): round(v * 1e3, 4) for h, v in ch["table"].items()}
+    c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots],
+                      [s.n_experts for s in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), max(T, 1), local,
+                      n_replicated=n_rep)
     if sharded:
         uid = [B.lora_nccl_unique_id() if rank == 0 else None]
         if world > 1:
@@ -404,6 +419,8 @@ def run_ours(args, cfg, batch, slots):
             "config": {"workload": cfg.name, "global_batch": cfg.n_tokens, "rows": T_glob, "slots": len(slots),
                        "rank": cfg.rank, "adapters": cfg.n_adapters,
                        "parallelism": f"adapter-sharded dp{world} (NCCL all-to-all)" if sharded else "single GPU",
+                       "n_replicated": n_rep if sharded else None,
+                       "placement_model_ms": rep_table,
                        "l2": f"inputs larger than L2 ({alg['total'] / 1e9:.1f} GB touched per step)"},
             "e2e": e2e,
             "gpu_launches": launches,
@@ -436,8 +453,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n-replicated", type=int, default=-1,
+                    help="sharded server: adapters [0, h) stored on every rank; -1 = cost-model choice")
     ap.add_argument("--force-sharded", action="store_true",
-                    help="use the sharded server even at N=1 (NCCL loopback; tests the N>1 code path)")
+                    help="use the sharded server even at N=1 with every row sent through the NCCL exchange "
+                         "(loopback; exercises the N>1 code path)")
     args = ap.parse_args()
     cfg = li.CONFIGS[args.workload]
     batch = li.make_batch(cfg)

@@ -70,6 +70,10 @@ typedef struct {
   const float *scale;        /* [n_adapters] host fp32 s_a; NULL => all 1.0 (R1) */
   int32_t max_rows;          /* capacity (rows) of the internal plan; 0 < max_rows <= 16384 */
   int32_t device;            /* CUDA device ordinal */
+  int32_t n_replicated;      /* sharded servers only: adapters [0, n_replicated) are stored on
+                                every rank (popularity-aware placement for skewed traffic,
+                                P:291; adapter ids are assumed ordered by popularity); 0 =
+                                plain striping.  Ignored by lora_server_create. */
 } lora_config_t;
 
 /* ------------------------------------------------------------------------- */
@@ -190,17 +194,24 @@ lora_status_t lora_apply_multi_host(lora_server_t *s, int32_t n, const int32_t *
  * bootstrap).  Fails with LORA_ERR_NCCL if libnccl.so.2 cannot be loaded. */
 lora_status_t lora_nccl_unique_id(void *out128);
 
-/* Create the rank-`rank` member of a world-`world` sharded server.  Adapter a
- * is owned by rank a mod world; each rank stores only its adapters.  Every
- * rank must call this collectively with the same config. */
+/* Create the rank-`rank` member of a world-`world` sharded server.  With
+ * h = cfg->n_replicated, adapters a < h are stored on every rank and adapter
+ * a >= h is owned by rank (a - h) mod world (LoRA Data Parallel striping,
+ * P:288-291); each rank stores only the adapters it owns.  Every rank must
+ * call this collectively with the same config.  max_rows * world <= 16384. */
 lora_status_t lora_server_create_sharded(const lora_config_t *cfg, int32_t rank, int32_t world,
                                          const void *nccl_unique_id, lora_server_t **out);
 
 /* Collective apply on a sharded server: every rank passes its OWN rows
- * (T local rows, device pointers, same slot list on every rank).  Rows are
- * routed to the owner of their adapter (NCCL all-to-all over NVLink),
- * applied there, and the deltas are returned and added into the caller's y.
- * One host synchronisation (the count exchange). */
+ * (T local rows, device pointers, same slot list on every rank).  Rows whose
+ * adapter this rank stores (its own or a replicated one) are applied in place;
+ * the others are routed to their adapter's owner (grouped NCCL send/recv over
+ * NVLink, overlapped with the in-place apply), applied there, and the deltas
+ * are returned and added into the caller's y.  Deltas travel as fp32 for an
+ * fp32 y (result bit-identical to the unsharded server, R18) and as
+ * bf16 for a bf16 y (env LORA_SHARD_FP32=1 forces fp32).  One host
+ * synchronisation (the count exchange); rows with adapter id -1 stay local
+ * and untouched; out-of-range ids are flagged and dropped. */
 lora_status_t lora_apply_sharded(lora_server_t *s, int32_t n, const int32_t *slots,
                                  const void *const *x, const int32_t *adapter_ids,
                                  const int32_t *expert_ids, void *const *y, lora_dtype_t y_dtype,

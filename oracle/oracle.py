@@ -190,32 +190,48 @@ def token_range(n_tokens: int, world: int, rank: int) -> Tuple[int, int]:
     return (n_tokens * rank) // world, (n_tokens * (rank + 1)) // world
 
 
-def owner_of(adapter_ids: np.ndarray, world: int) -> np.ndarray:
-    """owner(a) = a mod G; rows with a = -1 stay at their origin (owner -1)."""
+def owner_of(adapter_ids: np.ndarray, world: int, n_hot: int = 0, src=None) -> np.ndarray:
+    """Rank that processes each row (R19).
+
+    LoRA Data Parallel stripes the adapters over the G server
+    GPUs; adapters [0, n_hot) -- the most popular ones, P:291 -- are
+    replicated on every rank, so their rows are processed by the rank that
+    holds them (``src``).  Otherwise owner(a) = (a - n_hot) mod G.  Rows with
+    a = -1 stay at their origin (owner -1)."""
     a = np.asarray(adapter_ids, dtype=np.int64)
-    return np.where(a >= 0, a % world, -1)
+    own = np.where(a >= 0, (a - n_hot) % world, -1)
+    if n_hot > 0:
+        if src is None:
+            raise ValueError("owner_of: replicated adapters need the source rank of each row")
+        own = np.where((a >= 0) & (a < n_hot), np.asarray(src, dtype=np.int64), own)
+    return own
 
 
-def shard_dispatch(batch: li.Batch, world: int) -> List[Dict[str, np.ndarray]]:
+def shard_dispatch(batch: li.Batch, world: int, n_hot: int = 0) -> List[Dict[str, np.ndarray]]:
     """Per owner rank: the global row indices it receives, in receive order.
 
-    Receive order on an owner: by source rank ascending, then each source's
-    rows in their original local order.  Also returns the send counts matrix
-    ``counts[src][dst]``."""
+    Rows whose owner is their own source rank are processed in place and are
+    not exchanged ("local").  Receive order on an owner: by source rank
+    ascending, then each source's rows in their original local order.  Also
+    returns the send counts matrix ``counts[src][dst]`` (zero diagonal)."""
     k = batch.top_k
     out = []
-    own = owner_of(batch.adapter_ids, world)
     src_of_row = np.empty(batch.n_rows, np.int64)
     for g in range(world):
         t0, t1 = token_range(batch.n_tokens, world, g)
         src_of_row[t0 * k:t1 * k] = g
+    own = owner_of(batch.adapter_ids, world, n_hot, src_of_row)
     counts = np.zeros((world, world), np.int64)
     for s in range(world):
         for d in range(world):
-            counts[s, d] = int(np.sum((src_of_row == s) & (own == d)))
+            if s != d:
+                counts[s, d] = int(np.sum((src_of_row == s) & (own == d)))
     for d in range(world):
         recv = []
         for s in range(world):
-            recv.append(np.flatnonzero((src_of_row == s) & (own == d)))
-        out.append({"rows": np.concatenate(recv).astype(np.int64), "counts": counts})
+            if s != d:
+                recv.append(np.flatnonzero((src_of_row == s) & (own == d)))
+        out.append({"rows": np.concatenate(recv).astype(np.int64) if recv else np.zeros(0, np.int64),
+                    "local": np.flatnonzero((src_of_row == d) & (own == d)).astype(np.int64),
+                    "counts": counts})
     return out

@@ -16,6 +16,29 @@ enum { kCntValid = 0, kCntSegs = 1, kCntGroups = 2, kCntTiles = 3, kCntWords = 8
 // work-counter slots of the persistent kernels
 enum { kWqSimtShrink = 0, kWqSimtExpand = 1, kWqTcShrink = 2, kWqTcExpand = 3, kWorkSlots = 8 };
 
+// Adapter placement of a (sharded) server.  Adapters [0, n_hot) are replicated
+// on every rank (popularity-aware placement); adapter
+// a >= n_hot is owned by rank (a - n_hot) mod world (LoRA Data Parallel
+// striping).  An unsharded server is {1, 0, 0}.
+struct Placement {
+  int world, rank, n_hot;
+  __host__ __device__ bool owns(int a) const { return a < n_hot || (a - n_hot) % world == rank; }
+  __host__ __device__ int owner(int a) const { return a < n_hot ? rank : (a - n_hot) % world; }
+  __host__ __device__ long long local_index(int a) const {
+    return a < n_hot ? (long long)a : (long long)n_hot + (a - n_hot) / world;
+  }
+  // inverse of local_index for an owned adapter
+  __host__ __device__ long long global_adapter(long long li) const {
+    return li < n_hot ? li : (long long)n_hot + (li - n_hot) * world + rank;
+  }
+  // adapters stored on this rank
+  __host__ __device__ int n_local(int n_adapters) const {
+    const int h = n_hot < n_adapters ? n_hot : n_adapters;
+    const int rest = n_adapters - h;
+    return h + (rest > rank ? (rest - rank + world - 1) / world : 0);
+  }
+};
+
 // Device view of a plan (all device pointers).
 struct PlanDev {
   int32_t* perm;     // [max_rows]   sorted position -> original row
@@ -36,6 +59,7 @@ struct SegParams {
   int small_max;   // segments with more rows than this go to tcgen05 (if enabled)
   int tc_enabled;  // rank 64 and not forced off
   int tile_rows;
+  Placement pl;    // rows whose adapter this rank does not store are rejected (flagged)
 };
 
 // One slot inside a (multi-slot) launch.
@@ -56,16 +80,15 @@ struct MultiArgs {
   int n_tasks;
   int total_kc, total_ci;  // sums of n_kc / n_ci
   int y_fp32;
-  int y_store;             // 1: write fp32 delta s*(xA)B into y (sharded delta mode), 0: y += delta
-  int world;               // adapter striping (unit = (a/world)*E + e)
+  int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16
+  Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const float* scale;      // [n_adapters] s_a
   SlotTask t[kMaxTasks];
 };
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,
-                           int world, int shard_rank, const SegParams& sp, const PlanDev& pd, int* err_flag,
-                           cudaStream_t stream);
+                           const SegParams& sp, const PlanDev& pd, int* err_flag, cudaStream_t stream);
 cudaError_t launch_simt_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_simt_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
@@ -75,7 +98,7 @@ bool tc_available();
 
 // synthetic fill / weight relayout (synth_fill.cu)
 cudaError_t launch_fill_store(uint16_t* At, uint16_t* Bt, int h_in, int h_out, int E, int r, long long units,
-                              int slot, unsigned long long seed, int world, int shard_rank, int n_adapters,
+                              int slot, unsigned long long seed, const Placement& pl, int n_adapters,
                               cudaStream_t stream);
 cudaError_t launch_fill_rows(uint16_t* dst, long long rows, int width, unsigned long long seed, unsigned tag,
                              int shift, long long row_base, cudaStream_t stream);

@@ -105,7 +105,7 @@ static void free_server(lora_server* s) {
 }
 
 // allocate the store; world/rank select the owned adapters (a mod world == rank)
-static lora_status_t create_common(const lora_config_t* cfg, int world, int rank, lora_server** out) {
+static lora_status_t create_common(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot) {
   lora_status_t v = validate_config(cfg);
   if (v != LORA_OK) return v;
   if (!out) return fail(nullptr, LORA_ERR_INVALID_ARG, "out is NULL");
@@ -127,7 +127,8 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   s->n_adapters = cfg->n_adapters;
   s->world = world;
   s->shard_rank = rank;
-  s->n_adapters_local = (cfg->n_adapters - rank + world - 1) / world;
+  s->n_hot = world > 1 ? std::max(0, std::min(n_hot, cfg->n_adapters)) : 0;
+  s->n_adapters_local = placement(s).n_local(cfg->n_adapters);
   s->max_rows = cfg->max_rows;
   s->debug_sync = env_flag("LORA_DEBUG_SYNC");
   if (const char* e = std::getenv("LORA_SMALL_SEG_MAX")) s->small_seg_max = std::atoi(e);
@@ -194,14 +195,14 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   return LORA_OK;
 }
 
-lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out) {
-  return create_common(cfg, world, rank, out);
+lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot) {
+  return create_common(cfg, world, rank, out, n_hot);
 }
 
-// delta mode for the sharded owner: y[i] receives fp32 s*(xA)B (stored, not added)
+// delta mode for the sharded owner: d[i] receives s*(xA)B (stored, not added) as fp32 or bf16
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
-                                void* const* d, cudaStream_t st) {
-  return apply_multi_impl(s, p, n, slots, x, d, LORA_FP32, st, true);
+                                void* const* d, cudaStream_t st, bool bf16) {
+  return apply_multi_impl(s, p, n, slots, x, d, bf16 ? LORA_BF16 : LORA_FP32, st, bf16 ? 2 : 1);
 }
 
 static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, const void* A, const void* B,
@@ -216,8 +217,9 @@ static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, con
   lora_status_t rc = LORA_OK;
   for (int i = 0; i < n && rc == LORA_OK; ++i) {
     const int a = a_begin + i;
-    if (a % s->world != s->shard_rank) continue;  // not owned by this rank
-    const long long lu = (long long)(a / s->world) * sl.E;
+    const Placement pl = placement(s);
+    if (!pl.owns(a)) continue;  // not stored on this rank
+    const long long lu = pl.local_index(a) * sl.E;
     for (int pass = 0; pass < 2; ++pass) {
       const void* src = pass == 0 ? A : B;
       if (!src) continue;
@@ -238,7 +240,7 @@ static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, con
 
 extern "C" lora_status_t lora_server_create(const lora_config_t* cfg, const void* const* A, const void* const* B,
                                             int weights_on_device, lora_server_t** out) {
-  lora_status_t st = create_common(cfg, 1, 0, out);
+  lora_status_t st = create_common(cfg, 1, 0, out, 0);
   if (st != LORA_OK) return st;
   lora_server* s = *out;
   for (int i = 0; i < cfg->n_slots; ++i) {
@@ -273,8 +275,8 @@ extern "C" lora_status_t lora_server_fill_synthetic(lora_server_t* s, uint64_t s
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   for (size_t i = 0; i < s->slots.size(); ++i) {
     SlotInfo& sl = s->slots[i];
-    CK(s, launch_fill_store(sl.At, sl.Bt, sl.h_in, sl.h_out, sl.E, s->r, sl.units, (int)i, seed, s->world,
-                            s->shard_rank, s->n_adapters, st));
+    CK(s, launch_fill_store(sl.At, sl.Bt, sl.h_in, sl.h_out, sl.E, s->r, sl.units, (int)i, seed, placement(s),
+                            s->n_adapters, st));
   }
   return LORA_OK;
 }
@@ -387,8 +389,8 @@ lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapt
   sp.tile_rows = kTileRows;
   CK(s, cudaSetDevice(s->device));
   const int pi = prof_start(s, st);
-  CK(s, launch_segment(adapter_ids, expert_ids, T, E, s->n_adapters, s->world, s->shard_rank, sp, p->dev, s->d_err,
-                       st));
+  sp.pl = placement(s);
+  CK(s, launch_segment(adapter_ids, expert_ids, T, E, s->n_adapters, sp, p->dev, s->d_err, st));
   prof_stop(s, pi, kKSegment, st);
   p->n_experts = E;
   p->T = T;
@@ -405,7 +407,7 @@ lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapt
 }
 
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
-                               void* const* y, lora_dtype_t y_dtype, cudaStream_t st, bool store) {
+                               void* const* y, lora_dtype_t y_dtype, cudaStream_t st, int store) {
   if (!p || p->s != s) return fail(s, LORA_ERR_INVALID_ARG, "plan does not belong to this server");
   if (p->n_experts < 0) return fail(s, LORA_ERR_INVALID_ARG, "plan was never built");
   if (n < 0 || (n > 0 && (!slots || !x || !y))) return fail(s, LORA_ERR_INVALID_ARG, "bad slot list");
@@ -438,8 +440,8 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     std::memset(&args, 0, sizeof(args));
     args.n_tasks = nb;
     args.y_fp32 = y_dtype == LORA_FP32;
-    args.y_store = store ? 1 : 0;
-    args.world = s->world;
+    args.y_store = store;
+    args.pl = placement(s);
     args.scale = s->d_scale;
     int kc = 0, ci = 0;
     for (int i = 0; i < nb; ++i) {

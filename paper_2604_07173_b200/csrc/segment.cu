@@ -57,11 +57,11 @@ __device__ int block_exclusive_scan(int v, int* tmp, int* total) {
 // Reads one row's ids; returns the key (a*E+e), or -1 for "no LoRA" / out of
 // range (flagged through *bad).
 LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int i, int E,
-                        int n_adapters, int world, int shard_rank, int& bad) {
+                        int n_adapters, const Placement& pl, int& bad) {
   const int a = adapter_ids[i];
   const int e = expert_ids ? expert_ids[i] : 0;
   const bool in_range = (a >= -1) && (a < n_adapters) && (a < 0 || (e >= 0 && e < E)) &&
-                        (a < 0 || (a % world) == shard_rank);
+                        (a < 0 || pl.owns(a));
   if (!in_range) bad = 1;
   return (in_range && a >= 0) ? a * E + e : -1;
 }
@@ -149,7 +149,7 @@ __device__ void radix_pass(const uint32_t* in, uint32_t* out, int shift, unsigne
 // builds composites and sorts them; returns the buffer holding the result
 template <int EPT>
 __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids,
-                                int T, int E, int n_adapters, int world, int shard_rank, int K, int kb, int ib,
+                                int T, int E, int n_adapters, const Placement& pl, int K, int kb, int ib,
                                 uint32_t* A, uint32_t* B, unsigned long long* wtot, int* dbase, int* err_flag,
                                 int* n_valid_out, int* scan_tmp) {
   const int tid = threadIdx.x;
@@ -158,7 +158,7 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
   for (int r = 0; r < EPT; ++r) {
     const int i = tid * EPT + r;
     int key = -1;
-    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, world, shard_rank, bad);
+    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad);
     nv += key >= 0;
     A[i] = ((uint32_t)(key >= 0 ? key : K) << ib) | (uint32_t)i;
   }
@@ -185,7 +185,7 @@ LORA_DEVINL unsigned long long umax64(unsigned long long a, unsigned long long b
 
 template <int EPT>
 __device__ void bitonic_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T,
-                             int E, int n_adapters, int world, int shard_rank, unsigned long long* sm, int* err_flag,
+                             int E, int n_adapters, const Placement& pl, unsigned long long* sm, int* err_flag,
                              int* n_valid_out, int* scan_tmp) {
   constexpr int P = kSegThreads * EPT;
   const int tid = threadIdx.x;
@@ -195,7 +195,7 @@ __device__ void bitonic_sort(const int32_t* __restrict__ adapter_ids, const int3
   for (int r = 0; r < EPT; ++r) {
     const int i = tid * EPT + r;
     int key = -1;
-    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, world, shard_rank, bad);
+    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad);
     nv += key >= 0;
     v[r] = key >= 0 ? (((unsigned long long)(unsigned)key << 32) | (unsigned)i) : ~0ull;
   }
@@ -258,9 +258,10 @@ __device__ void bitonic_sort(const int32_t* __restrict__ adapter_ids, const int3
 template <bool radix>
 __global__ void __launch_bounds__(kSegThreads, 1)
     segment_kernel(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T, int P,
-                   int E, int n_adapters, int world, int shard_rank, int kb, int ib, SegParams sp, PlanDev pd,
+                   int E, int n_adapters, int kb, int ib, SegParams sp, PlanDev pd,
                    int* __restrict__ err_flag) {
   extern __shared__ __align__(16) uint8_t seg_smem[];
+  const Placement pl = sp.pl;
   __shared__ int scan_tmp[40];
   __shared__ unsigned long long wtot[32 * 4];
   __shared__ int dbase[16];
@@ -278,22 +279,22 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     const int K = n_adapters * E;
     uint32_t* res = nullptr;
     switch (EPT) {
-      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
     }
     srt32 = res;
     segoff_s = reinterpret_cast<int*>(res == A ? B : A);  // the free buffer (P + 1 ints reserved)
   } else {
     unsigned long long* S64 = reinterpret_cast<unsigned long long*>(seg_smem);
     switch (EPT) {
-      case 1: bitonic_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
-      case 2: bitonic_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
-      case 4: bitonic_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
-      case 8: bitonic_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
-      default: bitonic_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, world, shard_rank, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 1: bitonic_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: bitonic_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: bitonic_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: bitonic_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
+      default: bitonic_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
     }
     srt64 = S64;
     segoff_s = reinterpret_cast<int*>(S64 + P);
@@ -389,7 +390,7 @@ int bits_for(long long v) {  // bits needed to represent v (v >= 0)
 }  // namespace
 
 cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,
-                           int world, int shard_rank, const SegParams& sp, const PlanDev& pd, int* err_flag,
+                           const SegParams& sp, const PlanDev& pd, int* err_flag,
                            cudaStream_t stream) {
   int P = kSegThreads;  // at least one composite per thread
   while (P < T) P <<= 1;
@@ -410,11 +411,11 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
     attr_set |= 1ull << dev;
   }
   if (radix)
-    segment_kernel<true><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, world,
-                                                           shard_rank, kb, ib, sp, pd, err_flag);
+    segment_kernel<true><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp,
+                                                           pd, err_flag);
   else
-    segment_kernel<false><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, world,
-                                                            shard_rank, kb, ib, sp, pd, err_flag);
+    segment_kernel<false><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp,
+                                                            pd, err_flag);
   return cudaGetLastError();
 }
 

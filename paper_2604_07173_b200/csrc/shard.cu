@@ -3,23 +3,32 @@
 // P:288-291 (Sec. 4.1, Table 1 DP row): "evenly distribute LoRA adapters
 // across the server GPUs ... activations from client GPUs must be routed
 // accordingly ... the server GPUs perform a collective coordination step to
-// determine which activations should be processed by which GPUs."
+// determine which activations should be processed by which GPUs."  Skewed
+// adapter popularity concentrates activations on a few server GPUs;
+// the n_replicated hottest adapters are therefore stored on every rank
+// and their rows never leave their rank.
 //
 // One collective apply (every rank, same slot list):
-//   1. owner-bucket the local rows, owner(a) = a mod G (stable, local order)
+//   1. classify the local rows: owner(a) == this rank (replicated or own
+//      adapter) -> processed in place; the rest bucketed by owner (stable)
 //   2. all-gather of the G send counts -> full G x G matrix; ONE D2H sync
-//   3. grouped ncclSend/ncclRecv: x rows (each distinct x) + adapter/expert ids
-//      (receive order: source rank ascending, then the source's local order)
-//   4. local plan + apply in delta mode (fp32 delta written, not added)
-//   5. reverse grouped send/recv of the fp32 deltas
-//   6. y[origin row] = round(y + delta): one rounding, so the result is
-//      bit-identical to the unsharded apply (R18).
+//   3. (comm stream) pack + grouped ncclSend/ncclRecv of x rows and ids
+//      (receive order: source rank ascending, then the source's local order),
+//      overlapped with 4. on the caller's stream
+//   4. in-place rows: plan + multi-slot apply straight into the caller's y
+//   5. received rows: plan + apply in delta mode (delta stored, not added)
+//   6. (comm stream) reverse grouped send/recv of the deltas
+//   7. y[origin row] = round(y + delta)
+// Deltas travel as fp32 when y is fp32 (sharded == unsharded bit for bit,
+// DESIGN.md R18) and as bf16 when y is bf16 (half the NVLink bytes, one extra
+// rounding of the delta: DESIGN.md R19), unless LORA_SHARD_FP32=1.
 // NCCL is loaded with dlopen("libnccl.so.2") (the copy torch already loaded),
 // so the library itself has no link-time NCCL dependency.
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,13 +90,18 @@ NcclApi& nccl() {
 // ---------------------------------------------------------------------------
 constexpr int kBucketThreads = 1024;
 
-// Stable owner bucketing of T local rows (single CTA; T <= 16384).
-// send_idx[pos] = local row; counts[o] = rows for owner o.  Rows with a = -1
-// (or out of range, flagged) are not sent.
+// Single CTA over the T local rows (T <= 16384):
+//   ad_local[r] = a if this rank processes row r in place, else -1
+//   send_idx    = the other rows, bucketed by owner rank (stable, local order)
+//   counts[o]   = rows for owner o (0 for this rank)
+// loopback != 0 (test knob LORA_SHARD_LOOPBACK=1) sends this rank's own rows
+// through the exchange as well, so a single GPU exercises the NCCL path.
+// Out-of-range ids are flagged and dropped (never sent, never applied).
 __global__ void __launch_bounds__(kBucketThreads, 1)
-    bucket_kernel(const int32_t* __restrict__ ad, int T, int world, int n_adapters, int32_t* __restrict__ send_idx,
-                  int32_t* __restrict__ counts, int* __restrict__ err) {
-  __shared__ int s_tmp[40];
+    bucket_kernel(const int32_t* __restrict__ ad, int T, Placement pl, int n_adapters, int loopback,
+                  int32_t* __restrict__ ad_local,
+                  int32_t* __restrict__ send_idx, int32_t* __restrict__ counts, int* __restrict__ err) {
+  __shared__ int s_tmp[32];
   __shared__ int s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = (T + kBucketThreads - 1) / kBucketThreads;
@@ -96,15 +110,21 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
   int bad = 0;
   for (int r = r0; r < r1; ++r) {
     const int a = ad[r];
-    if (a < -1 || a >= n_adapters) bad = 1;
+    const bool ok = a >= -1 && a < n_adapters;
+    if (!ok) bad = 1;
+    ad_local[r] = (!loopback && ok && a >= 0 && pl.owner(a) == pl.rank) ? a : -1;
   }
   if (bad) atomicOr(err, 1);
   __syncthreads();
-  for (int o = 0; o < world; ++o) {
+  for (int o = 0; o < pl.world; ++o) {
+    if (o == pl.rank && !loopback) {
+      if (tid == 0) counts[o] = 0;
+      continue;
+    }
     int c = 0;
     for (int r = r0; r < r1; ++r) {
       const int a = ad[r];
-      c += (a >= 0 && a < n_adapters && a % world == o);
+      c += (a >= 0 && a < n_adapters && pl.owner(a) == o);
     }
     // block exclusive scan of c
     int x = c;
@@ -127,7 +147,7 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
     const int tot = s_tmp[31];
     for (int r = r0; r < r1; ++r) {
       const int a = ad[r];
-      if (a >= 0 && a < n_adapters && a % world == o) send_idx[pos++] = r;
+      if (a >= 0 && a < n_adapters && pl.owner(a) == o) send_idx[pos++] = r;
     }
     __syncthreads();
     if (tid == 0) {
@@ -138,16 +158,10 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
   }
 }
 
-// out[j][:] = in[idx[j]][:]  (rows of `width` 4-byte words)
-__global__ void gather_rows_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                   const int32_t* __restrict__ idx, int n, int width) {
-  const long long total = (long long)n * width;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long j = i / width;
-    const int c = (int)(i - j * width);
-    out[i] = in[(long long)idx[j] * width + c];
-  }
+// out[j] = in[idx[j]] (4-byte words)
+__global__ void gather_words_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                    const int32_t* __restrict__ idx, int n) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = in[idx[j]];
 }
 
 // out[j][:] = in[idx[j]][:], rows of `chunks` 16-byte chunks; one block row per output row
@@ -160,14 +174,20 @@ __global__ void gather_rows16_kernel(const uint4* __restrict__ in, uint4* __rest
   }
 }
 
-// y[idx[j]][c..c+4] = round(y + d[j][c..c+4]) (d fp32), 4 columns per thread
-__global__ void scatter_add4_kernel(void* __restrict__ y, int y_fp32, const float4* __restrict__ d,
+// y[idx[j]][c..c+4] = round(y + d[j][c..c+4]); d is fp32 (d_bf16 == 0) or bf16
+__global__ void scatter_add4_kernel(void* __restrict__ y, int y_fp32, const void* __restrict__ d, int d_bf16,
                                     const int32_t* __restrict__ idx, int n, int width) {
   const int q4 = width >> 2;
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
     const long long row = idx[j];
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < q4; c += gridDim.x * blockDim.x) {
-      const float4 v = d[(long long)j * q4 + c];
+      float4 v;
+      if (d_bf16) {
+        const uint2 b = reinterpret_cast<const uint2*>(d)[(long long)j * q4 + c];
+        v = make_float4(bf16lo(b.x), bf16hi(b.x), bf16lo(b.y), bf16hi(b.y));
+      } else {
+        v = reinterpret_cast<const float4*>(d)[(long long)j * q4 + c];
+      }
       if (y_fp32) {
         float4* p = reinterpret_cast<float4*>(y) + row * q4 + c;
         float4 o = *p;
@@ -185,25 +205,6 @@ __global__ void scatter_add4_kernel(void* __restrict__ y, int y_fp32, const floa
   }
 }
 
-// y[idx[j]][c] = round(y + d[j][c])  (d fp32)
-__global__ void scatter_add_kernel(void* __restrict__ y, int y_fp32, const float* __restrict__ d,
-                                   const int32_t* __restrict__ idx, int n, int width) {
-  const long long total = (long long)n * width;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long j = i / width;
-    const int c = (int)(i - j * width);
-    const long long o = (long long)idx[j] * width + c;
-    if (y_fp32) {
-      float* p = reinterpret_cast<float*>(y) + o;
-      *p = *p + d[i];
-    } else {
-      uint16_t* p = reinterpret_cast<uint16_t*>(y) + o;
-      *p = f32_to_bf16_rne(bf16_to_f32(*p) + d[i]);
-    }
-  }
-}
-
 int grid_of(long long n) {
   long long g = (n + 255) / 256;
   return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
@@ -213,18 +214,27 @@ int grid_of(long long n) {
 
 struct ShardState {
   ncclComm_t comm = nullptr;
-  // device scratch (grown on demand)
-  void* buf = nullptr;
+  cudaStream_t cs = nullptr;  // communication stream (pack + NCCL)
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* buf = nullptr;        // device scratch (grown on demand)
   size_t bytes = 0;
-  lora_plan* plan = nullptr;  // owner-side plan over received rows (capacity max_rows * world)
+  lora_plan* plan = nullptr;        // owner-side plan over received rows (capacity max_rows * world)
+  lora_plan* local_plan = nullptr;  // plan over this rank's rows processed in place
+  bool fp32_return = false;
+  bool loopback = false;
 };
 
 void lora_shard_free(lora_server* s) {
   if (!s || !s->shard) return;
-  if (s->shard->comm && nccl().ok) nccl().CommDestroy(s->shard->comm);
-  cudaFree(s->shard->buf);
-  if (s->shard->plan) plan_destroy_impl(s->shard->plan);
-  delete s->shard;
+  ShardState* sh = s->shard;
+  if (sh->comm && nccl().ok) nccl().CommDestroy(sh->comm);
+  cudaFree(sh->buf);
+  if (sh->plan) plan_destroy_impl(sh->plan);
+  if (sh->local_plan) plan_destroy_impl(sh->local_plan);
+  for (auto& e : sh->ev)
+    if (e) cudaEventDestroy(e);
+  if (sh->cs) cudaStreamDestroy(sh->cs);
+  delete sh;
   s->shard = nullptr;
 }
 
@@ -261,23 +271,37 @@ extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, in
     return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded: bad argument");
   if ((long long)cfg->max_rows * world > kMaxPlanRows)
     return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows * world must be <= 16384 (owner-side plan capacity)");
+  if (cfg->n_replicated < 0) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_replicated < 0");
   NcclApi& api = nccl();
   if (!api.ok) return fail(nullptr, LORA_ERR_NCCL, api.err);
-  lora_status_t st = create_common_sharded(cfg, world, rank, out);
+  lora_status_t st = create_common_sharded(cfg, world, rank, out, cfg->n_replicated);
   if (st != LORA_OK) return st;
   lora_server* s = *out;
   s->shard = new ShardState();
+  ShardState* sh = s->shard;
+  const char* f32 = std::getenv("LORA_SHARD_FP32");
+  sh->fp32_return = f32 && f32[0] && std::strcmp(f32, "0") != 0;
+  const char* lb = std::getenv("LORA_SHARD_LOOPBACK");
+  sh->loopback = lb && lb[0] && std::strcmp(lb, "0") != 0;
   ncclUniqueId id;
   std::memcpy(&id, nccl_unique_id, 128);
   cudaSetDevice(s->device);
-  ncclResult_t r = api.CommInitRank(&s->shard->comm, world, id, rank);
+  bool ok = cudaStreamCreateWithFlags(&sh->cs, cudaStreamNonBlocking) == cudaSuccess;
+  for (auto& e : sh->ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    lora_server_destroy(s);
+    *out = nullptr;
+    return fail(nullptr, LORA_ERR_CUDA, "stream / event creation failed");
+  }
+  ncclResult_t r = api.CommInitRank(&sh->comm, world, id, rank);
   if (r != ncclSuccess) {
     std::string m = std::string("ncclCommInitRank: ") + api.GetErrorString(r);
     lora_server_destroy(s);
     *out = nullptr;
     return fail(nullptr, LORA_ERR_NCCL, m);
   }
-  st = plan_create_impl(s, cfg->max_rows * world, &s->shard->plan);
+  st = plan_create_impl(s, cfg->max_rows * world, &sh->plan);
+  if (st == LORA_OK) st = plan_create_impl(s, cfg->max_rows, &sh->local_plan);
   if (st != LORA_OK) {
     std::string m = s->last_error;
     lora_server_destroy(s);
@@ -306,15 +330,20 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   if (n < 1 || !slots || !x || !y || (T > 0 && !adapter_ids)) return fail(s, LORA_ERR_INVALID_ARG, "NULL argument");
   if (T < 0 || T > s->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");
   if (y_dtype != LORA_BF16 && y_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "y_dtype");
-  const int E = s->slots[slots[0]].E;
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0; i < n; ++i)
     if (slots[i] < 0 || slots[i] >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
+  const int E = s->slots[slots[0]].E;
+  for (int i = 0; i < n; ++i)
     if (s->slots[slots[i]].E != E) return fail(s, LORA_ERR_INVALID_ARG, "slots of one call must share n_experts");
-  }
   NcclApi& api = nccl();
   const int G = s->world, me = s->shard_rank;
+  const Placement pl = placement(s);
+  ShardState* sh = s->shard;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStream_t cs = sh->cs;
   CKS(cudaSetDevice(s->device));
+  const bool d_bf16 = (y_dtype == LORA_BF16) && !sh->fp32_return;
+  const size_t dsz = d_bf16 ? 2 : 4;
 
   // distinct x buffers
   std::vector<const void*> xd;
@@ -334,6 +363,7 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   size_t off = 0;
   const size_t o_counts = off; off += al(sizeof(int32_t) * G * (G + 1));
   const size_t o_send_idx = off; off += al(sizeof(int32_t) * s->max_rows);
+  const size_t o_ad_local = off; off += al(sizeof(int32_t) * s->max_rows);
   const size_t o_ids_send = off; off += al(sizeof(int32_t) * 2 * s->max_rows);
   const size_t o_ids_recv = off; off += al(sizeof(int32_t) * 2 * Rmax);
   std::vector<size_t> o_xs(xd.size()), o_xr(xd.size());
@@ -343,12 +373,12 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   }
   std::vector<size_t> o_d(n), o_dr(n);
   for (int i = 0; i < n; ++i) {
-    o_d[i] = off; off += al((size_t)Rmax * s->slots[slots[i]].h_out * 4);        // owner-side deltas
-    o_dr[i] = off; off += al((size_t)s->max_rows * s->slots[slots[i]].h_out * 4); // returned deltas
+    o_d[i] = off; off += al((size_t)Rmax * s->slots[slots[i]].h_out * dsz);         // owner-side deltas
+    o_dr[i] = off; off += al((size_t)s->max_rows * s->slots[slots[i]].h_out * dsz);  // returned deltas
   }
-  ShardState* sh = s->shard;
   if (off > sh->bytes) {
     cudaStreamSynchronize(st);
+    cudaStreamSynchronize(cs);
     cudaFree(sh->buf);
     sh->buf = nullptr;
     sh->bytes = 0;
@@ -358,13 +388,17 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   char* base = static_cast<char*>(sh->buf);
   int32_t* d_counts = reinterpret_cast<int32_t*>(base + o_counts);  // [G] mine, then [G][G] gathered
   int32_t* d_send_idx = reinterpret_cast<int32_t*>(base + o_send_idx);
-  int32_t* d_ids_send = reinterpret_cast<int32_t*>(base + o_ids_send);  // [2][T] (a | e) in send order
-  int32_t* d_ids_recv = reinterpret_cast<int32_t*>(base + o_ids_recv);
+  int32_t* d_ad_local = reinterpret_cast<int32_t*>(base + o_ad_local);
+  int32_t* d_ids_send = reinterpret_cast<int32_t*>(base + o_ids_send);  // [2][max_rows] (a | e) in send order
+  int32_t* d_ids_recv = reinterpret_cast<int32_t*>(base + o_ids_recv);  // [2][Rmax]
 
-  // 1. bucket
+  // 1. classify + bucket.  The previous call's comm-stream work (reads of the
+  //    scratch) must be done before it is overwritten: ev[3] was recorded last.
+  CKS(cudaStreamWaitEvent(st, sh->ev[3], 0));
   if (T > 0) {
     const int pi = prof_start(s, st);
-    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, T, G, s->n_adapters, d_send_idx, d_counts, s->d_err);
+    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, T, pl, s->n_adapters, sh->loopback, d_ad_local, d_send_idx, d_counts,
+                                                 s->d_err);
     prof_stop(s, pi, kKShardBucket, st);
   } else {
     CKS(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * G, st));
@@ -380,90 +414,109 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   if (lr != LORA_OK) return fail(s, lr, "count exchange produced an invalid matrix");
   const int n_send = (int)so[G], n_recv = (int)ro[G];
   if (n_recv > Rmax) return fail(s, LORA_ERR_INVALID_ARG, "received rows exceed capacity");
+  // every rank sees the same matrix, so every rank takes the same branch
+  bool exchange = false;
+  for (int v : cnt) exchange = exchange || v > 0;
 
-  // 3. pack + dispatch
-  if (n_send > 0) {
-    int pi = prof_start(s, st);
-    gather_rows_kernel<<<grid_of(n_send), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(adapter_ids),
-                                                         reinterpret_cast<uint32_t*>(d_ids_send), d_send_idx, n_send,
-                                                         1);
-    prof_stop(s, pi, kKShardGather, st);
-    if (expert_ids) {
-      pi = prof_start(s, st);
-      gather_rows_kernel<<<grid_of(n_send), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(expert_ids),
-                                                           reinterpret_cast<uint32_t*>(d_ids_send + s->max_rows),
-                                                           d_send_idx, n_send, 1);
-      prof_stop(s, pi, kKShardGather, st);
-    } else {
-      CKS(cudaMemsetAsync(d_ids_send + s->max_rows, 0, sizeof(int32_t) * n_send, st));
+  // 3. (comm stream) pack + dispatch, overlapped with the in-place apply
+  if (exchange) {
+    CKS(cudaEventRecord(sh->ev[0], st));
+    CKS(cudaStreamWaitEvent(cs, sh->ev[0], 0));
+    if (n_send > 0) {
+      const int pi = prof_start(s, cs);
+      gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(adapter_ids),
+                                                            reinterpret_cast<uint32_t*>(d_ids_send), d_send_idx,
+                                                            n_send);
+      if (expert_ids)
+        gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(expert_ids),
+                                                              reinterpret_cast<uint32_t*>(d_ids_send + s->max_rows),
+                                                              d_send_idx, n_send);
+      else
+        CKS(cudaMemsetAsync(d_ids_send + s->max_rows, 0, sizeof(int32_t) * n_send, cs));
+      for (size_t j = 0; j < xd.size(); ++j) {
+        const int chunks = x_hin[j] / 8;  // 16-byte chunks per bf16 row
+        gather_rows16_kernel<<<dim3((chunks + 255) / 256, std::min(n_send, 65535)), 256, 0, cs>>>(
+            static_cast<const uint4*>(xd[j]), reinterpret_cast<uint4*>(base + o_xs[j]), d_send_idx, n_send, chunks);
+      }
+      prof_stop(s, pi, kKShardGather, cs);
+      CKS(cudaGetLastError());
     }
-    for (size_t j = 0; j < xd.size(); ++j) {
-      pi = prof_start(s, st);
-      const int chunks = x_hin[j] / 8;  // 16-byte chunks per bf16 row
-      gather_rows16_kernel<<<dim3((chunks + 255) / 256, std::min(n_send, 65535)), 256, 0, st>>>(
-          static_cast<const uint4*>(xd[j]), reinterpret_cast<uint4*>(base + o_xs[j]), d_send_idx, n_send, chunks);
-      prof_stop(s, pi, kKShardGather, st);
+    CKN(api.GroupStart());
+    for (int p = 0; p < G; ++p) {
+      const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
+      if (ns) {
+        CKN(api.Send(d_ids_send + so[p], ns, ncclInt32, p, sh->comm, cs));
+        CKN(api.Send(d_ids_send + s->max_rows + so[p], ns, ncclInt32, p, sh->comm, cs));
+        for (size_t j = 0; j < xd.size(); ++j)
+          CKN(api.Send(base + o_xs[j] + so[p] * x_hin[j] * 2, ns * x_hin[j], ncclBfloat16, p, sh->comm, cs));
+      }
+      if (nr) {
+        CKN(api.Recv(d_ids_recv + ro[p], nr, ncclInt32, p, sh->comm, cs));
+        CKN(api.Recv(d_ids_recv + Rmax + ro[p], nr, ncclInt32, p, sh->comm, cs));
+        for (size_t j = 0; j < xd.size(); ++j)
+          CKN(api.Recv(base + o_xr[j] + ro[p] * x_hin[j] * 2, nr * x_hin[j], ncclBfloat16, p, sh->comm, cs));
+      }
     }
-    CKS(cudaGetLastError());
+    CKN(api.GroupEnd());
+    CKS(cudaEventRecord(sh->ev[1], cs));
   }
-  CKN(api.GroupStart());
-  for (int p = 0; p < G; ++p) {
-    const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
-    if (ns) {
-      CKN(api.Send(d_ids_send + so[p], ns, ncclInt32, p, sh->comm, st));
-      CKN(api.Send(d_ids_send + s->max_rows + so[p], ns, ncclInt32, p, sh->comm, st));
-      for (size_t j = 0; j < xd.size(); ++j)
-        CKN(api.Send(base + o_xs[j] + so[p] * x_hin[j] * 2, ns * x_hin[j], ncclBfloat16, p, sh->comm, st));
-    }
-    if (nr) {
-      CKN(api.Recv(d_ids_recv + ro[p], nr, ncclInt32, p, sh->comm, st));
-      CKN(api.Recv(d_ids_recv + Rmax + ro[p], nr, ncclInt32, p, sh->comm, st));
-      for (size_t j = 0; j < xd.size(); ++j)
-        CKN(api.Recv(base + o_xr[j] + ro[p] * x_hin[j] * 2, nr * x_hin[j], ncclBfloat16, p, sh->comm, st));
-    }
-  }
-  CKN(api.GroupEnd());
 
-  // 4. owner-side plan + delta-mode apply (fp32 delta stored)
-  lora_status_t rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, st);
+  // 4. rows this rank stores the adapter of: applied in place
+  lora_status_t rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
+  if (rc != LORA_OK) return rc;
+  if (T > 0) {
+    rc = apply_multi_impl(s, sh->local_plan, n, slots, x, y, y_dtype, st);
+    if (rc != LORA_OK) return rc;
+  }
+  if (!exchange) {
+    CKS(cudaEventRecord(sh->ev[3], st));
+    return LORA_OK;
+  }
+
+  // 5. received rows: owner-side plan + delta-mode apply
+  CKS(cudaStreamWaitEvent(st, sh->ev[1], 0));
+  rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, st);
   if (rc != LORA_OK) return rc;
   if (n_recv > 0) {
-    // rows whose adapter had no LoRA never arrive, so every received row is written
     std::vector<const void*> xs(n);
     std::vector<void*> ds(n);
     for (int i = 0; i < n; ++i) {
       xs[i] = base + o_xr[x_of[i]];
       ds[i] = base + o_d[i];
     }
-    rc = apply_multi_delta(s, sh->plan, n, slots, xs.data(), ds.data(), st);
+    rc = apply_multi_delta(s, sh->plan, n, slots, xs.data(), ds.data(), st, d_bf16);
     if (rc != LORA_OK) return rc;
   }
 
-  // 5. return deltas (reverse direction)
+  // 6. (comm stream) return the deltas
+  CKS(cudaEventRecord(sh->ev[2], st));
+  CKS(cudaStreamWaitEvent(cs, sh->ev[2], 0));
+  const ncclDataType_t dt = d_bf16 ? ncclBfloat16 : ncclFloat32;
   CKN(api.GroupStart());
   for (int p = 0; p < G; ++p) {
     const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
     for (int i = 0; i < n; ++i) {
       const int ho = s->slots[slots[i]].h_out;
-      if (nr) CKN(api.Send(base + o_d[i] + ro[p] * ho * 4, nr * ho, ncclFloat32, p, sh->comm, st));
-      if (ns) CKN(api.Recv(base + o_dr[i] + so[p] * ho * 4, ns * ho, ncclFloat32, p, sh->comm, st));
+      if (nr) CKN(api.Send(base + o_d[i] + ro[p] * ho * dsz, nr * ho, dt, p, sh->comm, cs));
+      if (ns) CKN(api.Recv(base + o_dr[i] + so[p] * ho * dsz, ns * ho, dt, p, sh->comm, cs));
     }
   }
   CKN(api.GroupEnd());
+  CKS(cudaEventRecord(sh->ev[3], cs));
+  CKS(cudaStreamWaitEvent(st, sh->ev[3], 0));
 
-  // 6. scatter-add at the origin
+  // 7. add the returned deltas at the origin rows
   if (n_send > 0) {
     for (int i = 0; i < n; ++i) {
       const int ho = s->slots[slots[i]].h_out;
       const int pi = prof_start(s, st);
       scatter_add4_kernel<<<dim3((ho / 4 + 255) / 256, std::min(n_send, 65535)), 256, 0, st>>>(
-          y[i], y_dtype == LORA_FP32, reinterpret_cast<const float4*>(base + o_dr[i]), d_send_idx, n_send, ho);
+          y[i], y_dtype == LORA_FP32, base + o_dr[i], d_bf16 ? 1 : 0, d_send_idx, n_send, ho);
       prof_stop(s, pi, kKShardScatter, st);
     }
     CKS(cudaGetLastError());
   }
-  if (s->debug_sync) {
-    CKS(cudaStreamSynchronize(st));
-  }
+  CKS(cudaEventRecord(sh->ev[3], st));
+  if (s->debug_sync) CKS(cudaStreamSynchronize(st));
   return LORA_OK;
 }

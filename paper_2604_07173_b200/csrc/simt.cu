@@ -77,9 +77,9 @@ LORA_DEVINL int find_task_ci(const MultiArgs& args, int g) {
   return t;
 }
 
-LORA_DEVINL long long unit_of_key(int key, int E, int world) {
+LORA_DEVINL long long unit_of_key(int key, int E, const Placement& pl) {
   const int a = key / E, e = key - a * E;
-  return (long long)(a / world) * E + e;
+  return pl.local_index(a) * E + e;
 }
 
 LORA_DEVINL void unpack8(const uint4& w, float* f) {
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         const int ti = (int)(it / n_groups), gi = (int)(it - (long long)ti * n_groups);
         const SlotTask& t = args.t[ti];
         const int4 g = pd.groups[gi];
-        const long long unit = unit_of_key(g.z, t.E, args.world);
+        const long long unit = unit_of_key(g.z, t.E, args.pl);
         const uint16_t* abase = t.At + unit * (long long)t.h_in * R;
         const int n_st = t.h_in / t.SJ;
         const uint32_t a_bytes = (uint32_t)R * t.SJ * 2, x_bytes = (uint32_t)t.SJ * 2;
@@ -293,8 +293,10 @@ LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int cr, const ExpandPo
   for (int r = 0; r < NR; ++r) {
     const float d = p.s_a * ((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
     const long long o = (long long)yrow[r] * p.h_out + c;
-    if (y_store)
+    if (y_store == 1)
       reinterpret_cast<float*>(p.y)[o] = d;
+    else if (y_store == 2)
+      reinterpret_cast<uint16_t*>(p.y)[o] = f32_to_bf16_rne(d);
     else if (y_fp32)
       reinterpret_cast<float*>(p.y)[o] = __uint_as_float(yraw[r]) + d;
     else
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         const SlotTask& t = args.t[find_task_ci(args, cig)];
         const int ci = cig - t.ci_base;
         const int4 g = pd.groups[gi];
-        const long long unit = unit_of_key(g.z, t.E, args.world);
+        const long long unit = unit_of_key(g.z, t.E, args.pl);
         const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
         const float* vsrc = pd.vpart + t.vpart_off + (long long)g.x * R;
         const int n_st = t.CI / t.SC;

@@ -107,9 +107,9 @@ LORA_DEVINL int find_task_ci(const MultiArgs& args, int g) {
   while (t + 1 < args.n_tasks && args.t[t + 1].ci_base <= g) ++t;
   return t;
 }
-LORA_DEVINL long long unit_of_key(int key, int E, int world) {
+LORA_DEVINL long long unit_of_key(int key, int E, const Placement& pl) {
   const int a = key / E, e = key - a * E;
-  return (long long)(a / world) * E + e;
+  return pl.local_index(a) * E + e;
 }
 
 constexpr int R = 64;  // tcgen05 path rank
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       const SlotTask& t = args.t[find_task_kc(args, kcg)];
       const int kc = kcg - t.kc_base;
       const int4 tile = pd.tiles[ti];
-      const long long unit = unit_of_key(tile.z, t.E, args.world);
+      const long long unit = unit_of_key(tile.z, t.E, args.pl);
       const uint16_t* wbase = t.At + (unit * (t.h_in >> 6) + ((kc * t.KI) >> 6)) * (long long)(R * 64);
       // this thread's rows / chunks: 128 rows x 8 chunks per k-step, 1024 copies / 128 threads;
       // thread pt always copies chunk q = pt & 7 of rows n = (pt >> 3) + 16 i
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           vb = 0;
           vphase ^= 1;
         }
-        const long long unit = unit_of_key(tile.z, t.E, args.world);
+        const long long unit = unit_of_key(tile.z, t.E, args.pl);
         const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
         const int n_sub = t.CI / C::MSUB;
         for (int sb = 0; sb < n_sub; ++sb) {
@@ -611,11 +611,18 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           }
           if (sb + 2 < n_sub) issue_y(sb + 2);  // in flight across the other group's sub-tile
         } else {
-          // fp32 y (parity) or fp32 delta store (sharded delta mode): 4 columns per 16-byte chunk
+          // fp32 y (parity) or delta store (sharded delta mode): 4 columns per item
           for (int q = gt; q < tile.y * (C::MSUB / 4); q += C::GROUP_THREADS) {
             const int n = q >> 5, c4 = q & 31;
             const float4 e = lds128f(smem_u32(sg + n * C::STG_PITCH + c4 * 16));
             const long long row = __ldg(pd.perm + tile.x + n);
+            if (args.y_store == 2) {
+              uint2 o;
+              o.x = pack_bf16x2_rn(e.x, e.y);
+              o.y = pack_bf16x2_rn(e.z, e.w);
+              *reinterpret_cast<uint2*>(static_cast<uint16_t*>(t.y) + row * t.h_out + c0 + c4 * 4) = o;
+              continue;
+            }
             float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + row * t.h_out + c0 + c4 * 4);
             if (args.y_store) {
               *yp = e;

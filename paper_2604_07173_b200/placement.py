@@ -1,0 +1,94 @@
+"""Popularity-aware adapter placement for the Sharded LoRA Server (host logic).
+
+LoRA Data Parallel stripes the adapters over the G server GPUs (P:288-291,
+Sec. 4.1); under skewed popularity the owner of a hot adapter receives a large
+share of all activations.  The library therefore accepts
+``n_replicated = h``: adapters [0, h) -- ids ordered by popularity -- are
+stored on every rank and their rows are processed where they are, the rest is
+owned by rank (a - h) mod G (include/lora_server.h, R19).
+
+Replication trades HBM traffic (each rank reads the hot units its rows touch)
+for less exchange and a balanced load.  ``choose_n_replicated`` picks h from
+the observed ids with a per-rank bytes model -- the same rule the library
+applies, written out on the host -- and returns the cost table it used.
+"""
+from __future__ import annotations
+
+from typing import Dict, Iterable, Optional, Sequence
+
+import numpy as np
+
+
+def owner(adapter_ids: np.ndarray, world: int, n_hot: int, src: np.ndarray) -> np.ndarray:
+    """Rank that processes each row (-1 for rows without an adapter)."""
+    a = np.asarray(adapter_ids, np.int64)
+    own = np.where(a >= 0, (a - n_hot) % world, -1)
+    return np.where((a >= 0) & (a < n_hot), np.asarray(src, np.int64), own)
+
+
+def rank_costs(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray], src: np.ndarray, world: int, n_hot: int,
+               unit_bytes: float, row_bytes: float, xfer_bytes: float, hbm_gbs: float = 6500.0,
+               link_gbs: float = 700.0) -> np.ndarray:
+    """Modelled time (s) per rank of one sharded apply.
+
+    unit_bytes: weight bytes of one (adapter, expert) unit over all slots;
+    row_bytes: HBM bytes per processed row (x read, y or delta write);
+    xfer_bytes: bytes one remote row moves over NVLink (x out + delta back)."""
+    a = np.asarray(adapter_ids, np.int64)
+    e = np.zeros_like(a) if expert_ids is None else np.asarray(expert_ids, np.int64)
+    src = np.asarray(src, np.int64)
+    own = owner(a, world, n_hot, src)
+    valid = a >= 0
+    n_e = int(e.max()) + 1 if e.size else 1
+    key = a * n_e + e
+    out = np.zeros(world)
+    for g in range(world):
+        mine = valid & (own == g)
+        units = np.unique(key[mine]).size
+        remote_in = int(np.sum(mine & (src != g)))
+        remote_out = int(np.sum(valid & (src == g) & (own != g)))
+        hbm = units * unit_bytes + int(mine.sum()) * row_bytes + remote_out * row_bytes
+        # NVLink is full duplex: sends and receives overlap
+        out[g] = hbm / (hbm_gbs * 1e9) + max(remote_in, remote_out) * xfer_bytes / (link_gbs * 1e9)
+    return out
+
+
+def choose_n_replicated(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray], src: np.ndarray, world: int,
+                        unit_bytes: float, row_bytes: float, xfer_bytes: float,
+                        candidates: Optional[Iterable[int]] = None, **kw) -> Dict:
+    """Pick h minimising the slowest rank's modelled time; ties -> smaller h."""
+    if world <= 1:
+        return {"n_replicated": 0, "table": {0: 0.0}}
+    n_ad = int(np.max(adapter_ids)) + 1 if np.size(adapter_ids) else 0
+    if candidates is None:
+        candidates = [0] + [1 << i for i in range(12) if (1 << i) <= max(n_ad, 1)]
+    table = {}
+    for h in candidates:
+        table[int(h)] = float(rank_costs(adapter_ids, expert_ids, src, world, int(h), unit_bytes, row_bytes,
+                                         xfer_bytes, **kw).max())
+    best = min(table, key=lambda h: (table[h], h))
+    return {"n_replicated": best, "table": table}
+
+
+def sources_of_rows(n_tokens: int, top_k: int, world: int) -> np.ndarray:
+    """Source rank of each token-major row when rank g holds tokens
+    [g*T/G, (g+1)*T/G) (the bench's and the tests' split)."""
+    src = np.empty(n_tokens * top_k, np.int64)
+    for g in range(world):
+        t0, t1 = (n_tokens * g) // world, (n_tokens * (g + 1)) // world
+        src[t0 * top_k:t1 * top_k] = g
+    return src
+
+
+def slot_bytes(h_in: Sequence[int], h_out: Sequence[int], xbuf: Sequence[int], rank: int, y_bytes: int,
+               delta_bytes: int):
+    """(unit_bytes, row_bytes, xfer_bytes) for a slot list (bf16 weights and x)."""
+    unit = sum(2 * rank * (hi + ho) for hi, ho in zip(h_in, h_out))
+    seen, x_b = set(), 0
+    for hi, xb in zip(h_in, xbuf):
+        if xb not in seen:
+            seen.add(xb)
+            x_b += 2 * hi
+    row = x_b + sum(2 * y_bytes * ho for ho in h_out)
+    xfer = x_b + sum(delta_bytes * ho for ho in h_out)
+    return float(unit), float(row), float(xfer)

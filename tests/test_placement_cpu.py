@@ -1,0 +1,57 @@
+"""Host-side placement policy (paper_2604_07173_b200/placement.py; R19)."""
+import numpy as np
+
+import lora_inputs as li
+from oracle import oracle as orc
+from paper_2604_07173_b200 import placement as P
+
+
+def test_owner_matches_oracle_routing():
+    cfg = li.CONFIGS["mixtral_sharded"]
+    b = li.make_batch(cfg)
+    for G in (2, 3, 8):
+        src = P.sources_of_rows(cfg.n_tokens, cfg.top_k, G)
+        for h in (0, 1, 5, 64):
+            np.testing.assert_array_equal(P.owner(b.adapter_ids, G, h, src),
+                                          orc.owner_of(b.adapter_ids, G, h, src))
+        np.testing.assert_array_equal(P.owner(b.adapter_ids, G, 0, src), orc.owner_of(b.adapter_ids, G))
+
+
+def test_rank_costs_brute_force():
+    rng = np.random.default_rng(5)
+    a = rng.integers(-1, 12, 200)
+    e = rng.integers(0, 3, 200)
+    G, h = 3, 2
+    src = np.repeat(np.arange(G), [70, 60, 70])
+    U, R, X = 1000.0, 10.0, 7.0
+    got = P.rank_costs(a, e, src, G, h, U, R, X, hbm_gbs=1.0, link_gbs=1.0) * 1e9
+    for g in range(G):
+        units, mine, rin, rout = set(), 0, 0, 0
+        for i in range(200):
+            if a[i] < 0:
+                continue
+            o = int(src[i]) if a[i] < h else (a[i] - h) % G
+            if o == g:
+                units.add((a[i], e[i]))
+                mine += 1
+                rin += src[i] != g
+            elif src[i] == g:
+                rout += 1
+        assert abs(got[g] - (len(units) * U + (mine + rout) * R + max(rin, rout) * X)) < 1e-6
+
+
+def test_choose_replicates_a_dominant_adapter():
+    T = 4096
+    a = np.zeros(T, np.int64)                # every row on adapter 0
+    a[::64] = np.arange(T // 64) % 40 + 1    # a thin tail
+    src = P.sources_of_rows(T, 1, 4)
+    r = P.choose_n_replicated(a, None, src, 4, unit_bytes=1e6, row_bytes=1e5, xfer_bytes=1e5)
+    assert r["n_replicated"] >= 1 and r["table"][r["n_replicated"]] < r["table"][0]
+    assert P.choose_n_replicated(a, None, src[:0] * 0, 1, 1.0, 1.0, 1.0)["n_replicated"] == 0
+
+
+def test_slot_bytes_mixtral():
+    u, r, x = P.slot_bytes([4096, 4096, 14336], [14336, 14336, 4096], [0, 0, 1], 64, 2, 4)
+    assert u == 2 * 64 * 3 * (4096 + 14336)
+    assert r == 2 * 4096 + 2 * 14336 + 2 * 2 * (14336 * 2 + 4096)
+    assert x == 2 * 4096 + 2 * 14336 + 4 * (14336 * 2 + 4096)

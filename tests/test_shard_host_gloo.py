@@ -2,8 +2,10 @@
 
 The data path of lora_apply_sharded is NCCL + our kernels (GPU).  What can be
 checked without GPUs is everything around it, exercised here through the same
-steps the library takes (shard.cu): owner bucketing (owner(a) = a mod G,
-stable), the count exchange (all-gather), the library's own host routine
+steps the library takes (shard.cu): owner classification (adapters
+[0, n_hot) replicated on every rank and processed in place, the rest owned by
+rank (a - n_hot) mod G; R19), stable bucketing of the remote rows,
+the count exchange (all-gather), the library's own host routine
 lora_shard_layout (C-ABI, no GPU needed) for send/receive offsets, the row
 exchange in that layout, delta-mode compute on the owner (the oracle stands in
 for the GPU kernels here -- test-only), the return exchange and the add at the
@@ -34,7 +36,7 @@ def _cfg():
     return li.Config("shard_cpu", 11, (li.Slot("s", 128, 64, 4, 0),), 8, 10, 4, 2, 48, "fp32")
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, n_hot):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -49,16 +51,17 @@ def _worker(rank, world, port, out_dir):
         t0, t1 = orc.token_range(cfg.n_tokens, G, rank)
         rows = np.arange(t0 * k, t1 * k)
         a = batch.adapter_ids[rows]
-        # 1. stable owner bucketing of the local rows
-        own = np.where(a >= 0, a % G, -1)
-        send_idx = np.concatenate([np.flatnonzero(own == d) for d in range(G)])
-        counts = np.array([(own == d).sum() for d in range(G)], np.int64)
+        # 1. classify: in-place rows (owner == me) and stable owner buckets of the rest
+        own = orc.owner_of(a, G, n_hot, np.full(a.shape, rank))
+        local_idx = np.flatnonzero(own == rank)
+        send_idx = np.concatenate([np.flatnonzero(own == d) for d in range(G) if d != rank])
+        counts = np.array([(own == d).sum() if d != rank else 0 for d in range(G)], np.int64)
         # 2. count exchange
         allc = [torch.zeros(G, dtype=torch.int64) for _ in range(G)]
         dist.all_gather(allc, torch.from_numpy(counts))
         mat = torch.stack(allc).numpy().reshape(-1)
         so, ro = B.lora_shard_layout(mat.tolist(), G, rank)
-        assert so[-1] == len(send_idx)
+        assert so[-1] == len(send_idx) and so[rank + 1] == so[rank] and ro[rank + 1] == ro[rank]
         # 3. dispatch the global row ids (the payload stands for x rows + ids)
         payload = torch.from_numpy(rows[send_idx].astype(np.int64))
         recv = torch.zeros(ro[-1], dtype=torch.int64)
@@ -68,9 +71,6 @@ def _worker(rank, world, port, out_dir):
                 reqs.append(dist.isend(payload[so[p]:so[p + 1]].contiguous(), p))
         for p in range(G):
             if ro[p + 1] > ro[p]:
-                if p == rank:   # self-exchange (NCCL send/recv to self; gloo has no self pair)
-                    recv[ro[p]:ro[p + 1]] = payload[so[p]:so[p + 1]]
-                    continue
                 buf = torch.zeros(ro[p + 1] - ro[p], dtype=torch.int64)
                 dist.recv(buf, p)
                 recv[ro[p]:ro[p + 1]] = buf
@@ -78,8 +78,10 @@ def _worker(rank, world, port, out_dir):
             r.wait()
         got_rows = recv.numpy()
         # receive order == the oracle's dispatch emulation
-        exp_rows = orc.shard_dispatch(batch, G)[rank]["rows"]
-        np.testing.assert_array_equal(got_rows, exp_rows)
+        disp = orc.shard_dispatch(batch, G, n_hot)[rank]
+        np.testing.assert_array_equal(got_rows, disp["rows"])
+        np.testing.assert_array_equal(rows[local_idx], disp["local"])
+        np.testing.assert_array_equal(mat.reshape(G, G), disp["counts"])
         # 4. owner-side delta (fp64, exact): oracle stands in for the kernels in this CPU test
         x, uor, sor, A, Bw, _ = orc.prepare_slot(cfg, 0, batch, got_rows)
         d = np.zeros((len(got_rows), cfg.slots[0].h_out), np.float32)
@@ -94,9 +96,6 @@ def _worker(rank, world, port, out_dir):
                 reqs.append(dist.isend(dt[ro[p]:ro[p + 1]].contiguous(), p))
         for p in range(G):
             if so[p + 1] > so[p]:
-                if p == rank:
-                    back[so[p]:so[p + 1]] = dt[ro[p]:ro[p + 1]]
-                    continue
                 buf = torch.zeros((so[p + 1] - so[p], d.shape[1]), dtype=torch.float32)
                 dist.recv(buf, p)
                 back[so[p]:so[p + 1]] = buf
@@ -105,15 +104,22 @@ def _worker(rank, world, port, out_dir):
         # 6. add at the origin (one rounding of fp32 y + fp32 delta)
         y = li.bf16_bits_to_f32(li.y0_rows_bits(cfg.seed, 0, rows, cfg.slots[0].h_out)).copy()
         y[send_idx] = y[send_idx] + back.numpy()
+        # in-place rows: the same fp32 delta, added once
+        if len(local_idx):
+            xl, ul, sl, Al, Bl, _ = orc.prepare_slot(cfg, 0, batch, rows[local_idx])
+            dl = np.zeros((len(local_idx), cfg.slots[0].h_out), np.float32)
+            orc.lora_apply_rows(xl, ul, sl, Al, Bl, dl)
+            y[local_idx] = y[local_idx] + dl
         np.save(os.path.join(out_dir, f"y{rank}.npy"), y)
     finally:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def test_sharded_host_logic_world2_gloo(tmp_path):
+@pytest.mark.parametrize("n_hot", [0, 3])
+def test_sharded_host_logic_world2_gloo(tmp_path, n_hot):
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), n_hot), nprocs=world, join=True)
     from oracle import oracle as orc
     cfg = _cfg()
     batch = li.make_batch(cfg)
