@@ -113,6 +113,14 @@ lora_status_t lora_server_destroy(lora_server_t *s);
  * next lora_plan_build. */
 lora_status_t lora_server_set_small_seg_max(lora_server_t *s, int32_t n);
 
+/* on != 0 (default; env LORA_SERIAL=1 at create sets 0): the tcgen05 chain of
+ * an apply runs on an internal side stream forked from / joined to the
+ * caller's stream, concurrently with the CUDA-core chain (disjoint rows).
+ * on == 0 serialises every kernel on the caller's stream (the per-kernel
+ * profiling mode bench.py uses for roofline durations).  Results are
+ * identical either way. */
+lora_status_t lora_server_set_concurrent(lora_server_t *s, int32_t on);
+
 /* Sticky device error check: synchronises `stream`; returns
  * LORA_ERR_ID_OUT_OF_RANGE (and clears the flag) if any apply since the last
  * check met an out-of-range id, LORA_ERR_CUDA on a CUDA error, else LORA_OK. */

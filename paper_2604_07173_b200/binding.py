@@ -47,6 +47,7 @@ SIGNATURES = {
     "lora_server_fill_synthetic": (ctypes.c_int, [_vp, _u64, _vp]),
     "lora_server_destroy": (ctypes.c_int, [_vp]),
     "lora_server_set_small_seg_max": (ctypes.c_int, [_vp, _i32]),
+    "lora_server_set_concurrent": (ctypes.c_int, [_vp, _i32]),
     "lora_server_check": (ctypes.c_int, [_vp, _vp]),
     "lora_last_error": (ctypes.c_char_p, [_vp]),
     "lora_plan_create": (ctypes.c_int, [_vp, _i32, _pp]),
@@ -151,6 +152,10 @@ def lora_server_destroy(s: int):
 
 def lora_server_set_small_seg_max(s: int, n: int):
     _check(lib.lora_server_set_small_seg_max(s, n), s)
+
+
+def lora_server_set_concurrent(s: int, on: bool):
+    _check(lib.lora_server_set_concurrent(s, int(bool(on))), s)
 
 
 def lora_server_check(s: int, stream=None) -> int:

@@ -195,7 +195,8 @@ struct QueuePos {
   }
 };
 
-// producer lane: fetch the next item (or -1) and publish it
+// producer lane: fetch the next item (or -1) and publish it.  (Fetching the
+// following item ahead of time was measured slower: long items, worse tail.)
 template <int QD>
 LORA_DEVINL long long wq_push_next(WorkQueue<QD>& q, QueuePos& p, unsigned long long* counter, long long n_items) {
   long long it = (long long)atomicAdd(counter, 1ull);

@@ -11,6 +11,7 @@ constexpr int kMaxPlanRows = 16384;  // single-CTA segmenter capacity (128 KB of
 constexpr int kGroupRows = 8;        // rows per CUDA-core work group
 constexpr int kTileRows = 128;       // rows per tcgen05 tile (UMMA M / N)
 constexpr int kMaxTasks = 96;        // slots per multi-slot launch (param space)
+constexpr int kTaskTable = 2048;     // item-range -> task lookup entries (param space)
 
 enum { kCntValid = 0, kCntSegs = 1, kCntGroups = 2, kCntTiles = 3, kCntWords = 8 };
 // work-counter slots of the persistent kernels
@@ -84,7 +85,34 @@ struct MultiArgs {
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const float* scale;      // [n_adapters] s_a
   SlotTask t[kMaxTasks];
+  // task of each global shrink chunk (kc) / expand column range (ci) index,
+  // filled by the host when total_kc / total_ci <= kTaskTable
+  uint8_t kc_task[kTaskTable];
+  uint8_t ci_task[kTaskTable];
 };
+
+#ifdef __CUDACC__
+// task owning global expand column-range index g (ci_base prefix)
+__device__ __forceinline__ int find_task_ci(const MultiArgs& a, int g) {
+  if (a.total_ci <= kTaskTable) return a.ci_task[g];
+  int lo = 0, hi = a.n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.t[mid].ci_base <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+// task owning global shrink chunk index g (kc_base prefix)
+__device__ __forceinline__ int find_task_kc(const MultiArgs& a, int g) {
+  if (a.total_kc <= kTaskTable) return a.kc_task[g];
+  int lo = 0, hi = a.n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.t[mid].kc_base <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+#endif
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,

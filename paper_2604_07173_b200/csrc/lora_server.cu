@@ -296,6 +296,12 @@ extern "C" lora_status_t lora_server_set_small_seg_max(lora_server_t* s, int32_t
   return LORA_OK;
 }
 
+extern "C" lora_status_t lora_server_set_concurrent(lora_server_t* s, int32_t on) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  s->concurrent_tc = on != 0;
+  return LORA_OK;
+}
+
 extern "C" lora_status_t lora_server_check(lora_server_t* s, void* stream) {
   if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
   CK(s, cudaSetDevice(s->device));
@@ -406,6 +412,15 @@ lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapt
   return LORA_OK;
 }
 
+// item-range -> task lookup tables of a launch (kernels.h find_task_kc / find_task_ci)
+static void fill_task_tables(MultiArgs& a) {
+  for (int i = 0; i < a.n_tasks; ++i) {
+    const SlotTask& t = a.t[i];
+    for (int k = 0; k < t.n_kc && t.kc_base + k < kTaskTable; ++k) a.kc_task[t.kc_base + k] = (uint8_t)i;
+    for (int k = 0; k < t.n_ci && t.ci_base + k < kTaskTable; ++k) a.ci_task[t.ci_base + k] = (uint8_t)i;
+  }
+}
+
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
                                void* const* y, lora_dtype_t y_dtype, cudaStream_t st, int store) {
   if (!p || p->s != s) return fail(s, LORA_ERR_INVALID_ARG, "plan does not belong to this server");
@@ -469,6 +484,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     }
     args.total_kc = kc;
     args.total_ci = ci;
+    fill_task_tables(args);
     const int grid = s->sm_count;
     // The CUDA-core shrink hands out (task, group) items round-robin; order the
     // tasks by decreasing h_in so the longest items go first and the tail of
@@ -479,12 +495,15 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       for (int i = 0; i < nb; ++i) order[i] = i;
       std::stable_sort(order.begin(), order.end(),
                        [&](int a, int b) { return args.t[a].h_in > args.t[b].h_in; });
-      int kc2 = 0;
+      int kc2 = 0, ci2 = 0;
       for (int i = 0; i < nb; ++i) {
         sargs.t[i] = args.t[order[i]];
         sargs.t[i].kc_base = kc2;
+        sargs.t[i].ci_base = ci2;
         kc2 += sargs.t[i].n_kc;
+        ci2 += sargs.t[i].n_ci;
       }
+      fill_task_tables(sargs);
     }
     // The tcgen05 chain and the CUDA-core chain touch disjoint rows: run the
     // tcgen05 chain on the side stream (fork/join with events, graph-capturable)

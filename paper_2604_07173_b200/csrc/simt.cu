@@ -54,14 +54,23 @@ struct SimtCfg {
   static constexpr int NST_RAW = (SMEM_BUDGET - RED_BYTES) / S_STAGE;
   static constexpr int NST = NST_RAW > 8 ? 8 : (NST_RAW < 2 ? 2 : NST_RAW);
   static constexpr int SHRINK_SMEM = 1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8;
-  // expand
-  static constexpr int SC_MAX = NCT;        // one B row (output column) per consumer thread per stage
+  // expand: CPT output columns per consumer thread (c = ct + i*NCT); at r <= 32
+  // two columns share one FFMA2 (more B and y bytes per stage at small r)
+  static constexpr int CPT = R >= 64 ? 1 : 2;
+  static constexpr int SC_MAX = NCT * CPT;
   static constexpr int B_STAGE = SC_MAX * R * 2;
   static constexpr int V_BYTES = GR * R * 4;  // v rows of the group (fp32)
   static constexpr int E_STAGE = B_STAGE + 1024 * ((V_BYTES + 1023) / 1024);
-  static constexpr int NSTE_RAW = SMEM_BUDGET / E_STAGE;
-  static constexpr int NSTE = NSTE_RAW > 16 ? 16 : NSTE_RAW;
-  static constexpr int EXPAND_SMEM = 1024 + NSTE * E_STAGE + 2 * NSTE * 8 + 3 * kQD * 8;
+  // bf16 y tiles (cp.async) in a ring of YD slots, fetched YD-1 stages ahead,
+  // each with a 64-byte record {item, stage, row indices}
+  static constexpr int YD = R >= 32 ? 2 : 4;
+  static constexpr int Y_SLOT = GR * SC_MAX * 2;
+  static constexpr int META = 64;
+  static constexpr int NSTE_RAW = (SMEM_BUDGET - YD * (Y_SLOT + META) - 1024) / E_STAGE;
+  static constexpr int NSTE = NSTE_RAW > 16 ? 16 : (NSTE_RAW < 2 ? 2 : NSTE_RAW);
+  static constexpr int EXPAND_SMEM = 1024 + NSTE * E_STAGE + YD * (Y_SLOT + META) + 2 * NSTE * 8 + 3 * kQD * 8;
+  // the look-ahead pops items the producer has published only if YD - 1 <= NSTE
+  static_assert(YD - 1 <= NSTE, "y look-ahead deeper than the B pipeline");
   static_assert(S_STAGE % 1024 == 0 && E_STAGE % 1024 == 0, "stage alignment");
   static_assert(SHRINK_SMEM <= 112 * 1024 && EXPAND_SMEM <= 112 * 1024, "two CTAs per SM");
 };
@@ -71,11 +80,6 @@ LORA_DEVINL uint8_t* align1024(uint8_t* p) {
   return p + (((a + 1023u) & ~1023u) - a);
 }
 
-LORA_DEVINL int find_task_ci(const MultiArgs& args, int g) {
-  int t = 0;
-  while (t + 1 < args.n_tasks && args.t[t + 1].ci_base <= g) ++t;
-  return t;
-}
 
 LORA_DEVINL long long unit_of_key(int key, int E, const Placement& pl) {
   const int a = key / E, e = key - a * E;
@@ -251,8 +255,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
 // ---------------------------------------------------------------------------
 // expand + scale + scatter-accumulate
 // ---------------------------------------------------------------------------
-// Consumer-side walk over this CTA's (item, stage) sequence, so the y loads of
-// the next stage can be issued one stage ahead.
+// Consumer-side walk over this CTA's (item, stage) sequence.
 struct ExpandPos {
   long long it;
   int st, n_st;
@@ -265,9 +268,32 @@ struct ExpandPos {
   float s_a;
 };
 
+// y[row][c] for one (row, column) result d (already scaled).  Modes: store
+// fp32 / bf16 (sharded delta), fp32 accumulate (direct load), bf16 accumulate
+// with the old value taken from the stage's smem y tile.
+LORA_DEVINL void expand_out(const ExpandPos& p, int y_store, int y_fp32, uint32_t rows, int r, int col, float d,
+                            uint32_t ytile, int pitch) {
+  int row;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(row) : "r"(rows + r * 4));
+  const long long o = (long long)row * p.h_out + p.c0 + col;
+  if (y_store == 1) {
+    reinterpret_cast<float*>(p.y)[o] = d;
+  } else if (y_store == 2) {
+    reinterpret_cast<uint16_t*>(p.y)[o] = f32_to_bf16_rne(d);
+  } else if (y_fp32) {
+    float* yp = reinterpret_cast<float*>(p.y) + o;
+    *yp = *yp + d;
+  } else {
+    uint16_t old;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(old) : "r"(ytile + r * pitch + col * 2));
+    reinterpret_cast<uint16_t*>(p.y)[o] = f32_to_bf16_rne(bf16_to_f32(old) + d);
+  }
+}
+
+// r = 64: one column per thread, FFMA2 over pairs of k (two accumulators for ILP)
 template <int R, int NR>
-LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int cr, const ExpandPos& p, const uint32_t* yraw,
-                              const int* yrow, int y_store, int y_fp32) {
+LORA_DEVINL void expand_stage1(uint32_t b_s, uint32_t v_s, int cr, const ExpandPos& p, uint32_t rows,
+                               uint32_t ytile, int pitch, int y_store, int y_fp32) {
   float2 acc[NR][2];
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
@@ -288,20 +314,70 @@ LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int cr, const ExpandPo
       acc[r][ch & 1] = a;
     }
   }
-  const long long c = p.c0 + cr;
+  if (cr >= p.sc) return;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const float d = p.s_a * ((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
-    const long long o = (long long)yrow[r] * p.h_out + c;
-    if (y_store == 1)
-      reinterpret_cast<float*>(p.y)[o] = d;
-    else if (y_store == 2)
-      reinterpret_cast<uint16_t*>(p.y)[o] = f32_to_bf16_rne(d);
-    else if (y_fp32)
-      reinterpret_cast<float*>(p.y)[o] = __uint_as_float(yraw[r]) + d;
-    else
-      reinterpret_cast<uint16_t*>(p.y)[o] = f32_to_bf16_rne(bf16_to_f32((uint16_t)yraw[r]) + d);
+    expand_out(p, y_store, y_fp32, rows, r, cr, d, ytile, pitch);
   }
+}
+
+// r <= 32: CPT columns per thread (c = ct + i*NCT), FFMA2 over pairs of columns
+template <int R, int NR, int CPT, int NCT>
+LORA_DEVINL void expand_stage_pairs(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
+                                    uint32_t ytile, int pitch, int y_store, int y_fp32) {
+  constexpr int NP = CPT / 2;
+  float2 acc[NP][NR];
+#pragma unroll
+  for (int q = 0; q < NP; ++q)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[q][r] = make_float2(0.f, 0.f);
+#pragma unroll 1
+  for (int ch = 0; ch < R / 8; ++ch) {
+    uint4 w[CPT];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int c = ct + i * NCT;
+      w[i] = lds128(b_s + c * (R * 2) + (swz_row_chunk(c, ch, R * 2) << 4));
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const float4 v0 = lds128f(v_s + (r * R + ch * 8) * 4);
+      const float4 v1 = lds128f(v_s + (r * R + ch * 8 + 4) * 4);
+      const float vk[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const uint32_t a[4] = {w[2 * q].x, w[2 * q].y, w[2 * q].z, w[2 * q].w};
+        const uint32_t b[4] = {w[2 * q + 1].x, w[2 * q + 1].y, w[2 * q + 1].z, w[2 * q + 1].w};
+        float2 s = acc[q][r];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          s = __ffma2_rn(make_float2(vk[2 * j], vk[2 * j]), make_float2(bf16lo(a[j]), bf16lo(b[j])), s);
+          s = __ffma2_rn(make_float2(vk[2 * j + 1], vk[2 * j + 1]), make_float2(bf16hi(a[j]), bf16hi(b[j])), s);
+        }
+        acc[q][r] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const int c0 = ct + 2 * q * NCT, c1 = c0 + NCT;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (c0 < p.sc) expand_out(p, y_store, y_fp32, rows, r, c0, p.s_a * acc[q][r].x, ytile, pitch);
+      if (c1 < p.sc) expand_out(p, y_store, y_fp32, rows, r, c1, p.s_a * acc[q][r].y, ytile, pitch);
+    }
+  }
+}
+
+template <int R, int NR>
+LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
+                              uint32_t ytile, int pitch, int y_store, int y_fp32) {
+  using C = SimtCfg<R>;
+  if constexpr (C::CPT == 1)
+    expand_stage1<R, NR>(b_s, v_s, ct, p, rows, ytile, pitch, y_store, y_fp32);
+  else
+    expand_stage_pairs<R, NR, C::CPT, C::NCT>(b_s, v_s, ct, p, rows, ytile, pitch, y_store, y_fp32);
 }
 
 template <int R>
@@ -315,7 +391,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   using C = SimtCfg<R>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NSTE * C::E_STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NSTE * C::E_STAGE + C::YD * (C::Y_SLOT + C::META));
   uint64_t* empty = full + C::NSTE;
   WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::NSTE), empty + C::NSTE + kQD,
                     empty + C::NSTE + 2 * kQD};
@@ -373,7 +449,12 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   wq_finish(pd.wctr + kWqSimtExpand, pd.wdone + kWqSimtExpand);
 }
 
-// consumer warps of simt_expand_kernel
+// consumer warps of simt_expand_kernel.  A look-ahead cursor runs YD-1
+// stages ahead of the stage being computed: for each position it records
+// {item, stage, rows} in a ring slot and (bf16 y) fetches the y tile with
+// cp.async, so the y latency hides behind YD-1 stages of B.  Per stage: wait
+// for B + v, for the slot's cp.async group, one named barrier over the
+// consumer warps; issue the next look-ahead slot; compute; write y.
 template <int R>
 __device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, const PlanDev& pd, uint8_t* smem,
                                                       uint64_t* full, uint64_t* empty, WorkQueue<kQD>& wq,
@@ -381,6 +462,10 @@ __device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, con
   using C = SimtCfg<R>;
   const int lane = lane_id();
   const int ct = threadIdx.x;
+  uint8_t* ysm = smem + C::NSTE * C::E_STAGE;   // [YD][GR][SC_MAX] bf16
+  uint8_t* meta = ysm + C::YD * C::Y_SLOT;      // [YD] {long long it; int st; int pad; int rows[GR]}
+  const bool ytile = !(args.y_fp32 || args.y_store);
+  constexpr int pitch = C::SC_MAX * 2;
   int stage = 0;
   uint32_t phase = 0;
 
@@ -401,55 +486,80 @@ __device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, con
     p.perm_rows = pd.perm + g.x;
     p.s_a = args.scale[g.z / t.E];
   };
-  // raw y bits of the stage at `p` for this thread's column.  Kept raw (the
-  // conversion happens at use), so the loads stay in flight across the next
-  // barrier wait and compute.
-  uint32_t yv[C::GR];
-  int yrow[C::GR];
-  auto load_y = [&](const ExpandPos& p) {
-    if (args.y_store || ct >= p.sc) return;
-    const long long c = p.c0 + ct;
-#pragma unroll
-    for (int r = 0; r < C::GR; ++r) {
-      if (r < p.rows) {
-        const long long o = (long long)yrow[r] * p.h_out + c;
-        if (args.y_fp32)
-          yv[r] = reinterpret_cast<const uint32_t*>(p.y)[o];
-        else
-          yv[r] = reinterpret_cast<const uint16_t*>(p.y)[o];
-      }
+  // record position `p` in ring slot `slot` and start its y tile
+  auto issue = [&](const ExpandPos& p, int slot) {
+    uint8_t* m = meta + slot * C::META;
+    if (ct == 0) {
+      *reinterpret_cast<long long*>(m) = p.it;
+      *reinterpret_cast<int*>(m + 8) = p.st;
+    }
+    if (p.it >= n_items) return;
+    if (ct < C::GR) reinterpret_cast<int*>(m + 16)[ct] = ct < p.rows ? __ldg(p.perm_rows + ct) : 0;
+    if (!ytile) return;
+    const int cpr = p.sc >> 3;  // 16-byte chunks per row
+    const int n = p.rows * cpr;
+    uint8_t* dst = ysm + slot * C::Y_SLOT;
+    for (int q = ct; q < n; q += C::NCT) {
+      const int r = q / cpr, ch = q - r * cpr;
+      const long long row = __ldg(p.perm_rows + r);
+      cp_async16(dst + r * pitch + ch * 16,
+                 static_cast<const uint16_t*>(p.y) + row * p.h_out + p.c0 + ch * 8, 16);
     }
   };
-  auto load_rows = [&](const ExpandPos& p) {
-#pragma unroll
-    for (int r = 0; r < C::GR; ++r) yrow[r] = r < p.rows ? p.perm_rows[r] : 0;
-  };
-
   QueuePos qp;
-  ExpandPos cur;
+  ExpandPos la;  // look-ahead cursor
+  auto advance = [&](ExpandPos& p) {
+    if (p.it >= n_items) return;
+    if (p.st + 1 < p.n_st) {
+      p.st += 1;
+      p.c0 += p.sc;
+    } else {
+      const long long nit = wq_pop(wq, qp);
+      locate(nit < 0 ? n_items : nit, p);
+    }
+  };
   {
     const long long it0 = wq_pop(wq, qp);
-    locate(it0 < 0 ? n_items : it0, cur);
+    locate(it0 < 0 ? n_items : it0, la);
   }
-  if (cur.it < n_items) {
-    load_rows(cur);
-    load_y(cur);
+#pragma unroll 1
+  for (int k = 0; k < C::YD - 1; ++k) {
+    issue(la, k);
+    cp_async_commit();
+    advance(la);
   }
-  while (cur.it < n_items) {
+  named_bar_sync(1, C::NCT);
+  ExpandPos cur;
+  cur.it = -1;
+  int ys = 0;
+  for (;;) {
+    cp_async_wait<C::YD - 2>();
+    named_bar_sync(1, C::NCT);  // slot ys (record + y tile) complete and visible; slot ys-1 free
+    uint8_t* m = meta + ys * C::META;
+    const long long it = *reinterpret_cast<const long long*>(m);
+    if (it >= n_items) break;
+    const int st = *reinterpret_cast<const int*>(m + 8);
+    if (it != cur.it) locate(it, cur);  // cur.c0 stays the item's first column
+    ExpandPos at = cur;
+    at.st = st;
+    at.c0 = cur.c0 + (long long)st * cur.sc;
+    issue(la, ys == 0 ? C::YD - 1 : ys - 1);
+    cp_async_commit();
+    advance(la);
     mbar_wait(&full[stage], phase);
     const uint32_t b_s = smem_u32(smem + stage * C::E_STAGE);
     const uint32_t v_s = b_s + C::B_STAGE;
-    if (ct < cur.sc) {
-      switch (cur.rows) {
-        case 1: expand_stage<R, 1>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-        case 2: expand_stage<R, 2>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-        case 3: expand_stage<R, 3>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-        case 4: expand_stage<R, 4>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-        case 5: expand_stage<R, 5>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-        case 6: expand_stage<R, 6>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-        case 7: expand_stage<R, 7>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-        default: expand_stage<R, 8>(b_s, v_s, ct, cur, yv, yrow, args.y_store, args.y_fp32); break;
-      }
+    const uint32_t yt = smem_u32(ysm + ys * C::Y_SLOT);
+    const uint32_t rows = smem_u32(m + 16);
+    switch (at.rows) {
+      case 1: expand_stage<R, 1>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      case 2: expand_stage<R, 2>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      case 3: expand_stage<R, 3>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      case 4: expand_stage<R, 4>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      case 5: expand_stage<R, 5>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      case 6: expand_stage<R, 6>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      case 7: expand_stage<R, 7>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      default: expand_stage<R, 8>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -457,18 +567,9 @@ __device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, con
       stage = 0;
       phase ^= 1;
     }
-    // next stage of this item, or this CTA's next item; issue its y loads now
-    if (cur.st + 1 < cur.n_st) {
-      cur.st += 1;
-      cur.c0 += cur.sc;
-    } else {
-      const long long nit = wq_pop(wq, qp);
-      if (nit < 0) break;
-      locate(nit, cur);
-      load_rows(cur);
-    }
-    load_y(cur);
+    ys = ys + 1 == C::YD ? 0 : ys + 1;
   }
+  cp_async_wait<0>();
 }
 
 template <typename K>
@@ -534,7 +635,14 @@ int simt_sj_max(int rank) {
     default: return SimtCfg<64>::SJ_MAX;
   }
 }
-int simt_sc_max(int rank) { return SimtCfg<64>::SC_MAX + 0 * rank; }
+int simt_sc_max(int rank) {
+  switch (rank) {
+    case 8: return SimtCfg<8>::SC_MAX;
+    case 16: return SimtCfg<16>::SC_MAX;
+    case 32: return SimtCfg<32>::SC_MAX;
+    default: return SimtCfg<64>::SC_MAX;
+  }
+}
 int simt_shrink_smem(int rank) {
   switch (rank) {
     case 8: return SimtCfg<8>::SHRINK_SMEM;

@@ -97,16 +97,6 @@ LORA_DEVINL uint8_t* align1024(uint8_t* p) {
   return p + (((a + 1023u) & ~1023u) - a);
 }
 
-LORA_DEVINL int find_task_kc(const MultiArgs& args, int g) {
-  int t = 0;
-  while (t + 1 < args.n_tasks && args.t[t + 1].kc_base <= g) ++t;
-  return t;
-}
-LORA_DEVINL int find_task_ci(const MultiArgs& args, int g) {
-  int t = 0;
-  while (t + 1 < args.n_tasks && args.t[t + 1].ci_base <= g) ++t;
-  return t;
-}
 LORA_DEVINL long long unit_of_key(int key, int E, const Placement& pl) {
   const int a = key / E, e = key - a * E;
   return pl.local_index(a) * E + e;
