@@ -134,6 +134,9 @@ LORA_DEVINL void cp_async16(void* smem_dst, const void* gsrc, uint32_t src_bytes
                "r"(src_bytes)
                : "memory");
 }
+LORA_DEVINL void cp_async16_u32(uint32_t smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
+}
 LORA_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 LORA_DEVINL void cp_async_wait() {

@@ -10,7 +10,7 @@ namespace lora {
 constexpr int kMaxPlanRows = 16384;  // single-CTA segmenter capacity (128 KB of composites)
 constexpr int kGroupRows = 8;        // rows per CUDA-core work group
 constexpr int kTileRows = 128;       // rows per tcgen05 tile (UMMA M / N)
-constexpr int kMaxTasks = 96;        // slots per multi-slot launch (param space)
+constexpr int kMaxTasks = 128;       // slots per multi-slot launch (param space; 32 layers x q,k,v,o)
 constexpr int kTaskTable = 2048;     // item-range -> task lookup entries (param space)
 
 enum { kCntValid = 0, kCntSegs = 1, kCntGroups = 2, kCntTiles = 3, kCntWords = 8 };

@@ -63,14 +63,24 @@ struct SimtCfg {
   static constexpr int E_STAGE = B_STAGE + 1024 * ((V_BYTES + 1023) / 1024);
   // bf16 y tiles (cp.async) in a ring of YD slots, fetched YD-1 stages ahead,
   // each with a 64-byte record {item, stage, row indices}
+  // At r <= 32 (bf16 y) the stage's results are written back into its tile
+  // and leave with coalesced 16-byte stores during the next stage: one extra
+  // slot keeps the tile alive until then.
   static constexpr int YD = R >= 32 ? 2 : 4;
+  static constexpr int YS = CPT > 1 ? YD + 1 : YD;
   static constexpr int Y_SLOT = GR * SC_MAX * 2;
-  static constexpr int META = 64;
-  static constexpr int NSTE_RAW = (SMEM_BUDGET - YD * (Y_SLOT + META) - 1024) / E_STAGE;
+  static constexpr int META = 128;  // StageRec
+  // every byte of the 112 KB two-CTA share not used by the fixed parts goes to B stages
+  static constexpr int E_FIXED = 1024 + YS * (Y_SLOT + META) + 2 * 16 * 8 + 3 * kQD * 8 + kQD * 80;
+  static constexpr int NSTE_RAW = (112 * 1024 - E_FIXED) / E_STAGE;
   static constexpr int NSTE = NSTE_RAW > 16 ? 16 : (NSTE_RAW < 2 ? 2 : NSTE_RAW);
-  static constexpr int EXPAND_SMEM = 1024 + NSTE * E_STAGE + YD * (Y_SLOT + META) + 2 * NSTE * 8 + 3 * kQD * 8;
+  static constexpr int EXPAND_SMEM =
+      1024 + NSTE * E_STAGE + YS * (Y_SLOT + META) + 2 * NSTE * 8 + 3 * kQD * 8 + kQD * 80;
   // the look-ahead pops items the producer has published only if YD - 1 <= NSTE
-  static_assert(YD - 1 <= NSTE, "y look-ahead deeper than the B pipeline");
+  // The producer publishes an item after issuing its first stage; at stage s
+  // (after releasing it) the consumers' look-ahead takes the item holding
+  // stage s+YD, whose first stage needs stage s+YD-NSTE released: YD <= NSTE.
+  static_assert(YD <= NSTE, "y look-ahead deeper than the B pipeline");
   static_assert(S_STAGE % 1024 == 0 && E_STAGE % 1024 == 0, "stage alignment");
   static_assert(SHRINK_SMEM <= 112 * 1024 && EXPAND_SMEM <= 112 * 1024, "two CTAs per SM");
 };
@@ -268,19 +278,34 @@ struct ExpandPos {
   float s_a;
 };
 
-// y[row][c] for one (row, column) result d (already scaled).  Modes: store
-// fp32 / bf16 (sharded delta), fp32 accumulate (direct load), bf16 accumulate
-// with the old value taken from the stage's smem y tile.
-LORA_DEVINL void expand_out(const ExpandPos& p, int y_store, int y_fp32, uint32_t rows, int r, int col, float d,
-                            uint32_t ytile, int pitch) {
+// y[row][c] for one (row, column) result d (already scaled).  Output mode M
+// (compile time): 0 bf16 accumulate with the old value from the stage's smem
+// y tile, 1 fp32 store and 2 bf16 store (sharded delta), 3 fp32 accumulate.
+enum { kOutBf16Acc = 0, kOutF32Store = 1, kOutBf16Store = 2, kOutF32Acc = 3 };
+template <int M, bool TILE>
+LORA_DEVINL void expand_out(const ExpandPos& p, uint32_t rows, int r, int col, float d, uint32_t ytile, int pitch) {
+  if constexpr (TILE) {
+    // result back into the stage's smem tile; the tile leaves with bulk stores
+    const uint32_t a = ytile + r * pitch + col * 2;
+    uint16_t v;
+    if constexpr (M == kOutBf16Acc) {
+      uint16_t old;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(old) : "r"(a));
+      v = f32_to_bf16_rne(bf16_to_f32(old) + d);
+    } else {
+      v = f32_to_bf16_rne(d);
+    }
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+    return;
+  }
   int row;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(row) : "r"(rows + r * 4));
   const long long o = (long long)row * p.h_out + p.c0 + col;
-  if (y_store == 1) {
+  if constexpr (M == kOutF32Store) {
     reinterpret_cast<float*>(p.y)[o] = d;
-  } else if (y_store == 2) {
+  } else if constexpr (M == kOutBf16Store) {
     reinterpret_cast<uint16_t*>(p.y)[o] = f32_to_bf16_rne(d);
-  } else if (y_fp32) {
+  } else if constexpr (M == kOutF32Acc) {
     float* yp = reinterpret_cast<float*>(p.y) + o;
     *yp = *yp + d;
   } else {
@@ -291,9 +316,9 @@ LORA_DEVINL void expand_out(const ExpandPos& p, int y_store, int y_fp32, uint32_
 }
 
 // r = 64: one column per thread, FFMA2 over pairs of k (two accumulators for ILP)
-template <int R, int NR>
+template <int R, int NR, int M>
 LORA_DEVINL void expand_stage1(uint32_t b_s, uint32_t v_s, int cr, const ExpandPos& p, uint32_t rows,
-                               uint32_t ytile, int pitch, int y_store, int y_fp32) {
+                               uint32_t ytile, int pitch) {
   float2 acc[NR][2];
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
@@ -318,43 +343,50 @@ LORA_DEVINL void expand_stage1(uint32_t b_s, uint32_t v_s, int cr, const ExpandP
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const float d = p.s_a * ((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
-    expand_out(p, y_store, y_fp32, rows, r, cr, d, ytile, pitch);
+    expand_out<M, false>(p, rows, r, cr, d, ytile, pitch);
   }
 }
 
-// r <= 32: CPT columns per thread (c = ct + i*NCT), FFMA2 over pairs of columns
-template <int R, int NR, int CPT, int NCT>
+// r <= 32: CPT columns per thread (c = ct + i*NCT), FFMA2 over pairs of
+// columns.  The B chunk of a column pair is widened to fp32 once and reused
+// for every row of the group.
+template <int R, int NR, int CPT, int NCT, int M>
 LORA_DEVINL void expand_stage_pairs(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
-                                    uint32_t ytile, int pitch, int y_store, int y_fp32) {
+                                    uint32_t ytile, int pitch) {
   constexpr int NP = CPT / 2;
+  constexpr bool TILE = M == kOutBf16Acc || M == kOutBf16Store;
   float2 acc[NP][NR];
 #pragma unroll
   for (int q = 0; q < NP; ++q)
 #pragma unroll
     for (int r = 0; r < NR; ++r) acc[q][r] = make_float2(0.f, 0.f);
-#pragma unroll 1
+#pragma unroll
   for (int ch = 0; ch < R / 8; ++ch) {
-    uint4 w[CPT];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      const int c = ct + i * NCT;
-      w[i] = lds128(b_s + c * (R * 2) + (swz_row_chunk(c, ch, R * 2) << 4));
-    }
+    for (int q = 0; q < NP; ++q) {
+      const int ca = ct + 2 * q * NCT, cb = ca + NCT;
+      const uint4 wa = lds128(b_s + ca * (R * 2) + (swz_row_chunk(ca, ch, R * 2) << 4));
+      const uint4 wb = lds128(b_s + cb * (R * 2) + (swz_row_chunk(cb, ch, R * 2) << 4));
+      const uint32_t a[4] = {wa.x, wa.y, wa.z, wa.w}, b[4] = {wb.x, wb.y, wb.z, wb.w};
+      float2 bb[8];  // bb[k] = (B[ca][k], B[cb][k]) for the 8 k of this chunk
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const float4 v0 = lds128f(v_s + (r * R + ch * 8) * 4);
-      const float4 v1 = lds128f(v_s + (r * R + ch * 8 + 4) * 4);
-      const float vk[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      for (int j = 0; j < 4; ++j) {
+        bb[2 * j] = make_float2(bf16lo(a[j]), bf16lo(b[j]));
+        bb[2 * j + 1] = make_float2(bf16hi(a[j]), bf16hi(b[j]));
+      }
 #pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        const uint32_t a[4] = {w[2 * q].x, w[2 * q].y, w[2 * q].z, w[2 * q].w};
-        const uint32_t b[4] = {w[2 * q + 1].x, w[2 * q + 1].y, w[2 * q + 1].z, w[2 * q + 1].w};
+      for (int r = 0; r < NR; ++r) {
+        const float4 v0 = lds128f(v_s + (r * R + ch * 8) * 4);
+        const float4 v1 = lds128f(v_s + (r * R + ch * 8 + 4) * 4);
         float2 s = acc[q][r];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          s = __ffma2_rn(make_float2(vk[2 * j], vk[2 * j]), make_float2(bf16lo(a[j]), bf16lo(b[j])), s);
-          s = __ffma2_rn(make_float2(vk[2 * j + 1], vk[2 * j + 1]), make_float2(bf16hi(a[j]), bf16hi(b[j])), s);
-        }
+        s = __ffma2_rn(make_float2(v0.x, v0.x), bb[0], s);
+        s = __ffma2_rn(make_float2(v0.y, v0.y), bb[1], s);
+        s = __ffma2_rn(make_float2(v0.z, v0.z), bb[2], s);
+        s = __ffma2_rn(make_float2(v0.w, v0.w), bb[3], s);
+        s = __ffma2_rn(make_float2(v1.x, v1.x), bb[4], s);
+        s = __ffma2_rn(make_float2(v1.y, v1.y), bb[5], s);
+        s = __ffma2_rn(make_float2(v1.z, v1.z), bb[6], s);
+        s = __ffma2_rn(make_float2(v1.w, v1.w), bb[7], s);
         acc[q][r] = s;
       }
     }
@@ -364,26 +396,50 @@ LORA_DEVINL void expand_stage_pairs(uint32_t b_s, uint32_t v_s, int ct, const Ex
     const int c0 = ct + 2 * q * NCT, c1 = c0 + NCT;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      if (c0 < p.sc) expand_out(p, y_store, y_fp32, rows, r, c0, p.s_a * acc[q][r].x, ytile, pitch);
-      if (c1 < p.sc) expand_out(p, y_store, y_fp32, rows, r, c1, p.s_a * acc[q][r].y, ytile, pitch);
+      if (c0 < p.sc) expand_out<M, TILE>(p, rows, r, c0, p.s_a * acc[q][r].x, ytile, pitch);
+      if (c1 < p.sc) expand_out<M, TILE>(p, rows, r, c1, p.s_a * acc[q][r].y, ytile, pitch);
     }
   }
 }
 
-template <int R, int NR>
+template <int R, int NR, int M>
 LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
-                              uint32_t ytile, int pitch, int y_store, int y_fp32) {
+                              uint32_t ytile, int pitch) {
   using C = SimtCfg<R>;
   if constexpr (C::CPT == 1)
-    expand_stage1<R, NR>(b_s, v_s, ct, p, rows, ytile, pitch, y_store, y_fp32);
+    expand_stage1<R, NR, M>(b_s, v_s, ct, p, rows, ytile, pitch);
   else
-    expand_stage_pairs<R, NR, C::CPT, C::NCT>(b_s, v_s, ct, p, rows, ytile, pitch, y_store, y_fp32);
+    expand_stage_pairs<R, NR, C::CPT, C::NCT, M>(b_s, v_s, ct, p, rows, ytile, pitch);
 }
 
-template <int R>
-__device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, const PlanDev& pd, uint8_t* smem,
-                                                      uint64_t* full, uint64_t* empty, WorkQueue<kQD>& wq,
-                                                      int n_groups, long long n_items);
+// One expand work item as resolved by the producer lane (work-queue entry):
+// everything the consumers need, so they never wait on a dependent global
+// load for an item.
+struct ExpandRec {
+  long long it;  // -1: end of the stream
+  int task, ci;
+  int4 g;        // group {row_begin, nrows, key, seg}
+  float s_a;
+  int pad;
+  int rows[kGroupRows];
+};
+static_assert(sizeof(ExpandRec) <= 80, "record size");
+
+// One stage of the look-ahead ring (smem), written when its y tile is issued.
+struct StageRec {
+  long long it;  // item (>= n_items: end)
+  long long c0;  // first column
+  void* y;
+  int st, sc, rows, h_out;
+  float s_a;
+  int pad;
+  int row[kGroupRows];
+};
+static_assert(sizeof(StageRec) <= 128, "stage record size");
+
+template <int R, int M>
+__device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, uint8_t* smem, uint64_t* full,
+                                                      uint64_t* empty, WorkQueue<kQD>& wq, const ExpandRec* recs);
 
 template <int R>
 __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
@@ -391,10 +447,11 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   using C = SimtCfg<R>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NSTE * C::E_STAGE + C::YD * (C::Y_SLOT + C::META));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NSTE * C::E_STAGE + C::YS * (C::Y_SLOT + C::META));
   uint64_t* empty = full + C::NSTE;
   WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::NSTE), empty + C::NSTE + kQD,
                     empty + C::NSTE + 2 * kQD};
+  ExpandRec* recs = reinterpret_cast<ExpandRec*>(empty + C::NSTE + 3 * kQD);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NSTE; ++s) {
@@ -406,22 +463,31 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   }
   __syncthreads();
 
-  const int n_groups = pd.counts[kCntGroups];
-  const long long n_items = (long long)n_groups * args.total_ci;
   const int warp = warp_id(), lane = lane_id();
 
   if (warp == C::NWC) {
-    // ===================== producer: B rows + the group's v rows =====================
+    // ===================== producer: resolve items, B rows + the group's v rows =====================
     if (lane == 0) {
+      const int n_groups = pd.counts[kCntGroups];
+      const long long n_items = (long long)n_groups * args.total_ci;
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       QueuePos qp;
+      unsigned long long* ctr = pd.wctr + kWqSimtExpand;
       for (;;) {
-        const long long it = wq_push_next(wq, qp, pd.wctr + kWqSimtExpand, n_items);
-        if (it < 0) break;
+        long long it = (long long)atomicAdd(ctr, 1ull);
+        if (it >= n_items) it = -1;
+        mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
+        ExpandRec& rc = recs[qp.slot];
+        if (it < 0) {
+          rc.it = -1;
+          mbar_arrive(&wq.full[qp.slot]);
+          break;
+        }
         const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
-        const SlotTask& t = args.t[find_task_ci(args, cig)];
+        const int ti = find_task_ci(args, cig);
+        const SlotTask& t = args.t[ti];
         const int ci = cig - t.ci_base;
         const int4 g = pd.groups[gi];
         const long long unit = unit_of_key(g.z, t.E, args.pl);
@@ -439,127 +505,187 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
             stage = 0;
             phase ^= 1;
           }
+          if (st == 0) {
+            // publish the record after the first copies are in flight (the
+            // look-ahead waits for it only YD-1 <= NSTE-1 stages ahead)
+            rc.it = it;
+            rc.task = ti;
+            rc.ci = ci;
+            rc.g = g;
+            rc.s_a = args.scale[g.z / t.E];
+#pragma unroll
+            for (int r = 0; r < C::GR; ++r) rc.rows[r] = r < g.y ? __ldg(pd.perm + g.x + r) : 0;
+            mbar_arrive(&wq.full[qp.slot]);
+            qp.advance(kQD);
+          }
         }
       }
     }
   } else {
-    simt_expand_consumers<R>(args, pd, smem, full, empty, wq, n_groups, n_items);
+    if (args.y_store == 1)
+      simt_expand_consumers<R, kOutF32Store>(args, smem, full, empty, wq, recs);
+    else if (args.y_store == 2)
+      simt_expand_consumers<R, kOutBf16Store>(args, smem, full, empty, wq, recs);
+    else if (args.y_fp32)
+      simt_expand_consumers<R, kOutF32Acc>(args, smem, full, empty, wq, recs);
+    else
+      simt_expand_consumers<R, kOutBf16Acc>(args, smem, full, empty, wq, recs);
   }
   __syncthreads();
   wq_finish(pd.wctr + kWqSimtExpand, pd.wdone + kWqSimtExpand);
 }
 
 // consumer warps of simt_expand_kernel.  A look-ahead cursor runs YD-1
-// stages ahead of the stage being computed: for each position it records
-// {item, stage, rows} in a ring slot and (bf16 y) fetches the y tile with
-// cp.async, so the y latency hides behind YD-1 stages of B.  Per stage: wait
-// for B + v, for the slot's cp.async group, one named barrier over the
-// consumer warps; issue the next look-ahead slot; compute; write y.
-template <int R>
-__device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, const PlanDev& pd, uint8_t* smem,
-                                                      uint64_t* full, uint64_t* empty, WorkQueue<kQD>& wq,
-                                                      int n_groups, long long n_items) {
+// stages ahead of the stage being computed: for each position it writes a
+// StageRec into a ring slot and (bf16 y) fetches the y tile with cp.async, so
+// the y latency hides behind YD-1 stages of B.  Per stage: wait for the
+// slot's cp.async group, one named barrier over the consumer warps, issue the
+// next look-ahead slot, wait for B + v, compute, write y (r <= 32: back into
+// the tile, which all threads store to y with 16-byte stores at the next stage).
+template <int R, int M>
+__device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, uint8_t* smem, uint64_t* full,
+                                                      uint64_t* empty, WorkQueue<kQD>& wq, const ExpandRec* recs) {
   using C = SimtCfg<R>;
   const int lane = lane_id();
   const int ct = threadIdx.x;
-  uint8_t* ysm = smem + C::NSTE * C::E_STAGE;   // [YD][GR][SC_MAX] bf16
-  uint8_t* meta = ysm + C::YD * C::Y_SLOT;      // [YD] {long long it; int st; int pad; int rows[GR]}
-  const bool ytile = !(args.y_fp32 || args.y_store);
+  uint8_t* ysm = smem + C::NSTE * C::E_STAGE;   // [YS][GR][SC_MAX] bf16
+  uint8_t* meta = ysm + C::YS * C::Y_SLOT;      // [YS] StageRec
+  constexpr bool ytile = M == kOutBf16Acc;
+  constexpr bool TILE = C::CPT > 1 && (M == kOutBf16Acc || M == kOutBf16Store);
+  constexpr int YS = TILE ? C::YD + 1 : C::YD;
+  static_assert(YS <= C::YS, "y ring");
   constexpr int pitch = C::SC_MAX * 2;
+  const long long END = 1ll << 62;
   int stage = 0;
   uint32_t phase = 0;
 
-  auto locate = [&](long long it, ExpandPos& p) {
-    p.it = it;
-    p.st = 0;
-    if (it >= n_items) return;
-    const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
-    const SlotTask& t = args.t[find_task_ci(args, cig)];
-    const int ci = cig - t.ci_base;
-    const int4 g = pd.groups[gi];
-    p.n_st = t.CI / t.SC;
-    p.sc = t.SC;
-    p.rows = g.y;
-    p.h_out = t.h_out;
-    p.c0 = (long long)ci * t.CI;
-    p.y = t.y;
-    p.perm_rows = pd.perm + g.x;
-    p.s_a = args.scale[g.z / t.E];
-  };
-  // record position `p` in ring slot `slot` and start its y tile
-  auto issue = [&](const ExpandPos& p, int slot) {
-    uint8_t* m = meta + slot * C::META;
-    if (ct == 0) {
-      *reinterpret_cast<long long*>(m) = p.it;
-      *reinterpret_cast<int*>(m + 8) = p.st;
+  // look-ahead cursor: the queue record of its item stays held until it moves on
+  QueuePos qp;
+  int la_slot = -1;
+  long long la_it = END;
+  int la_st = 0, la_nst = 0;
+  auto take = [&]() {  // next item from the queue into the cursor
+    mbar_wait(&wq.full[qp.slot], qp.phase);
+    la_slot = qp.slot;
+    qp.advance(kQD);
+    const ExpandRec& rc = recs[la_slot];
+    la_it = rc.it < 0 ? END : rc.it;
+    la_st = 0;
+    if (la_it != END) {
+      const SlotTask& t = args.t[rc.task];
+      la_nst = t.CI / t.SC;
     }
-    if (p.it >= n_items) return;
-    if (ct < C::GR) reinterpret_cast<int*>(m + 16)[ct] = ct < p.rows ? __ldg(p.perm_rows + ct) : 0;
-    if (!ytile) return;
-    const int cpr = p.sc >> 3;  // 16-byte chunks per row
-    const int n = p.rows * cpr;
-    uint8_t* dst = ysm + slot * C::Y_SLOT;
+  };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0 && la_slot >= 0) mbar_arrive(&wq.empty[la_slot]);
+  };
+  // write the cursor's position into ring slot `slot` and start its y tile
+  auto issue = [&](int slot) {
+    StageRec* m = reinterpret_cast<StageRec*>(meta + slot * C::META);
+    if (la_it == END) {
+      if (ct == 0) m->it = END;
+      return;
+    }
+    const ExpandRec& rc = recs[la_slot];
+    const SlotTask& t = args.t[rc.task];
+    const long long c0 = (long long)rc.ci * t.CI + (long long)la_st * t.SC;
+    if (ct == 0) {
+      m->it = la_it;
+      m->c0 = c0;
+      m->y = t.y;
+      m->st = la_st;
+      m->sc = t.SC;
+      m->rows = rc.g.y;
+      m->h_out = t.h_out;
+      m->s_a = rc.s_a;
+    }
+    if (ct < C::GR) m->row[ct] = rc.rows[ct];
+    if constexpr (!ytile) return;
+    const int cpr = t.SC >> 3;  // 16-byte chunks per row
+    const int n = rc.g.y * cpr;
+    const uint16_t* yb = static_cast<const uint16_t*>(t.y) + c0;
+    const uint32_t dst = smem_u32(ysm + slot * C::Y_SLOT);
     for (int q = ct; q < n; q += C::NCT) {
       const int r = q / cpr, ch = q - r * cpr;
-      const long long row = __ldg(p.perm_rows + r);
-      cp_async16(dst + r * pitch + ch * 16,
-                 static_cast<const uint16_t*>(p.y) + row * p.h_out + p.c0 + ch * 8, 16);
+      cp_async16_u32(dst + r * pitch + ch * 16, yb + (long long)rc.rows[r] * t.h_out + ch * 8);
     }
   };
-  QueuePos qp;
-  ExpandPos la;  // look-ahead cursor
-  auto advance = [&](ExpandPos& p) {
-    if (p.it >= n_items) return;
-    if (p.st + 1 < p.n_st) {
-      p.st += 1;
-      p.c0 += p.sc;
+  auto advance = [&]() {
+    if (la_it == END) return;
+    if (la_st + 1 < la_nst) {
+      ++la_st;
     } else {
-      const long long nit = wq_pop(wq, qp);
-      locate(nit < 0 ? n_items : nit, p);
+      release();
+      take();
     }
   };
-  {
-    const long long it0 = wq_pop(wq, qp);
-    locate(it0 < 0 ? n_items : it0, la);
-  }
+  take();
 #pragma unroll 1
   for (int k = 0; k < C::YD - 1; ++k) {
-    issue(la, k);
+    issue(k);
     cp_async_commit();
-    advance(la);
+    advance();
   }
-  named_bar_sync(1, C::NCT);
-  ExpandPos cur;
-  cur.it = -1;
+
+  ExpandPos prev;  // TILE: the stage whose tile is stored next
+  prev.it = END;
+  int prev_slot = 0;
+  // TILE: the finished tile of `prev` goes to y with coalesced 16-byte stores
+  // by all consumer threads (the barrier before this made it final; the
+  // look-ahead refills its slot only after the next barrier)
+  auto store_prev = [&]() {
+    if constexpr (TILE) {
+      if (prev.it != END) {
+        const int* rws = reinterpret_cast<const StageRec*>(meta + prev_slot * C::META)->row;
+        const uint32_t src = smem_u32(ysm + prev_slot * C::Y_SLOT);
+        const int cpr = prev.sc >> 3;
+        const int n = prev.rows * cpr;
+        uint16_t* yb = static_cast<uint16_t*>(prev.y) + prev.c0;
+        for (int q = ct; q < n; q += C::NCT) {
+          const int r = q / cpr, ch = q - r * cpr;
+          const uint4 v = lds128(src + r * pitch + ch * 16);
+          *reinterpret_cast<uint4*>(yb + (long long)rws[r] * prev.h_out + ch * 8) = v;
+        }
+      }
+    }
+  };
   int ys = 0;
   for (;;) {
     cp_async_wait<C::YD - 2>();
-    named_bar_sync(1, C::NCT);  // slot ys (record + y tile) complete and visible; slot ys-1 free
-    uint8_t* m = meta + ys * C::META;
-    const long long it = *reinterpret_cast<const long long*>(m);
-    if (it >= n_items) break;
-    const int st = *reinterpret_cast<const int*>(m + 8);
-    if (it != cur.it) locate(it, cur);  // cur.c0 stays the item's first column
-    ExpandPos at = cur;
-    at.st = st;
-    at.c0 = cur.c0 + (long long)st * cur.sc;
-    issue(la, ys == 0 ? C::YD - 1 : ys - 1);
+    named_bar_sync(1, C::NCT);  // slot ys complete and visible; previous stage's tile final
+    store_prev();
+    const StageRec* m = reinterpret_cast<const StageRec*>(meta + ys * C::META);
+    ExpandPos at;
+    at.it = m->it;
+    if (at.it == END) break;
+    at.c0 = m->c0;
+    at.y = m->y;
+    at.st = m->st;
+    at.sc = m->sc;
+    at.rows = m->rows;
+    at.h_out = m->h_out;
+    at.s_a = m->s_a;
+    {
+      int ns = ys + C::YD - 1;
+      if (ns >= YS) ns -= YS;
+      issue(ns);
+    }
     cp_async_commit();
-    advance(la);
     mbar_wait(&full[stage], phase);
     const uint32_t b_s = smem_u32(smem + stage * C::E_STAGE);
     const uint32_t v_s = b_s + C::B_STAGE;
     const uint32_t yt = smem_u32(ysm + ys * C::Y_SLOT);
-    const uint32_t rows = smem_u32(m + 16);
+    const uint32_t rows = smem_u32(m->row);
     switch (at.rows) {
-      case 1: expand_stage<R, 1>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
-      case 2: expand_stage<R, 2>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
-      case 3: expand_stage<R, 3>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
-      case 4: expand_stage<R, 4>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
-      case 5: expand_stage<R, 5>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
-      case 6: expand_stage<R, 6>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
-      case 7: expand_stage<R, 7>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
-      default: expand_stage<R, 8>(b_s, v_s, ct, at, rows, yt, pitch, args.y_store, args.y_fp32); break;
+      case 1: expand_stage<R, 1, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
+      case 2: expand_stage<R, 2, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
+      case 3: expand_stage<R, 3, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
+      case 4: expand_stage<R, 4, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
+      case 5: expand_stage<R, 5, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
+      case 6: expand_stage<R, 6, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
+      case 7: expand_stage<R, 7, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
+      default: expand_stage<R, 8, M>(b_s, v_s, ct, at, rows, yt, pitch); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -567,7 +693,12 @@ __device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, con
       stage = 0;
       phase ^= 1;
     }
-    ys = ys + 1 == C::YD ? 0 : ys + 1;
+    // move the look-ahead on only after releasing this stage: the producer
+    // publishes an item after issuing its first stage, which may need this slot
+    advance();
+    prev = at;
+    prev_slot = ys;
+    ys = ys + 1 == YS ? 0 : ys + 1;
   }
   cp_async_wait<0>();
 }

@@ -380,15 +380,31 @@ def test_argument_errors_enqueue_nothing(B):
         B.lora_server_destroy(s)
 
 
-@pytest.mark.parametrize("loopback,y_dtype", [(False, "bf16"), (True, "fp32"), (True, "bf16")])
-def test_sharded_g1(B, monkeypatch, loopback, y_dtype):
+@pytest.mark.parametrize("rank", [8, 16, 32])
+def test_small_rank_bf16_full_parity(B, rank):
+    """r <= 32 takes the CUDA-core path with two columns per thread and the
+    smem-tile + bulk-store output (bf16 y); every element checked."""
+    cfg = _mid_cfg(rank=rank)
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        ys = _run_multi(B, s, cfg, b, [0, 1])
+        for i in range(2):
+            U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"r={rank} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+@pytest.mark.parametrize("loopback,y_dtype,rank", [(False, "bf16", 64), (True, "fp32", 64), (True, "bf16", 64),
+                                                   (True, "bf16", 16)])
+def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank):
     """Sharded server at G = 1.  In place (no exchange): bit-identical to the
     unsharded server.  Loopback (LORA_SHARD_LOOPBACK=1 sends every row through
     the NCCL exchange to itself, so one GPU runs the bucket / pack / send-recv
     / owner delta apply / return / scatter-add path): fp32 y bit-identical to
     the unsharded server (R18); bf16 y returns bf16 deltas (R19) and is held
     to the oracle tolerance, every row checked."""
-    cfg = dataclasses.replace(_mid_cfg(), y_dtype=y_dtype)
+    cfg = dataclasses.replace(_mid_cfg(rank=rank), y_dtype=y_dtype)
     if loopback:
         monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
     b = li.make_batch(cfg)
