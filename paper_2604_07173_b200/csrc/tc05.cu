@@ -369,31 +369,59 @@ LORA_DEVINL void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 }
 LORA_DEVINL void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+LORA_DEVINL void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+// 2 x 256-bit global load / store (64 contiguous bytes; full 32-byte sectors)
+LORA_DEVINL void ldg256x2(const void* p, uint32_t* r) {
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "l"(static_cast<const char*>(p) + 32));
+}
+LORA_DEVINL void stg256x2(void* p, const uint32_t* w) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(static_cast<char*>(p) + 32), "r"(w[8]),
+               "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+               : "memory");
+}
+
 // ===========================================================================
-// expand (swap-AB).  Per 128-column sub-tile: D[128 cols x N rows] in TMEM
-// (four accumulators).  Two epilogue groups of 8 warps take alternate
-// sub-tiles, so two sub-tiles are in the epilogue at any time; each group
-// moves D through its fp32 staging tile in shared memory (lane = column,
-// conflict-free) and read-modify-writes y with 16-byte vector accesses, the
-// y loads of its next sub-tile in flight.
+// expand.  Per 128-column sub-tile: D[128 rows x 128 cols] = v_tile . Bt_sub^T
+// in TMEM (four accumulators): TMEM lane = tile row, so every epilogue thread
+// owns one row and 32 consecutive output columns -- it reads its 64-byte
+// y segment (two 256-bit loads, issued one sub-tile ahead), adds s_a * D and
+// writes the segment back with two 256-bit stores.  No transposing staging
+// tile, every access a full 32-byte sector.  16 epilogue warps: TMEM lane quadrant = warp % 4,
+// column block = warp / 4.
 // ===========================================================================
 struct ExpandCfg {
-  static constexpr int EPI_WARPS = 16;  // warps 0-15: epilogue, group = warp / 8
-  static constexpr int GROUP_THREADS = 256;
+  static constexpr int EPI_WARPS = 16;
+  static constexpr int EPI_THREADS = EPI_WARPS * 32;
   static constexpr int TMA_WARP = 16;   // warp 16: v tile + Bt bulk copies
   static constexpr int MMA_WARP = 17;   // warp 17: TMEM alloc + MMA
   static constexpr int THREADS = 18 * 32;
-  static constexpr int MSUB = 128;                     // output columns per MMA (M)
+  static constexpr int MSUB = 128;                     // output columns per MMA (N)
   static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
-  static constexpr int NST = 3;
-  static constexpr int V_TILE = kTileRows * 128;       // 16 KB (N <= 128 rows x 64 bf16)
-  static constexpr int STG_PITCH = MSUB * 4 + 16;      // fp32 staging row (+16 B: fewer bank conflicts)
-  static constexpr int STG = kTileRows * STG_PITCH;    // 66 KB per group
+  static constexpr int NST = 6;
+  static constexpr int V_TILE = kTileRows * 128;       // 16 KB (M = 128 rows x 64 bf16)
   static constexpr int NACC = 4;
-  static constexpr int ACC_COLS = kTileRows;           // N columns per accumulator
+  static constexpr int ACC_COLS = MSUB;                // N columns per accumulator
   static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 512
-  static constexpr int PF = kTileRows * (MSUB / 8) / GROUP_THREADS;  // 16-byte bf16 chunks per thread (8)
-  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 2 * STG + 512;
+  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 512;
 };
 
 __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
@@ -401,9 +429,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   using C = ExpandCfg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE] swizzled MMA operand
-  uint8_t* stg = vtile + 2 * C::V_TILE;        // [group][128][STG_PITCH] fp32 delta staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + 2 * C::STG);
+  uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE] swizzled MMA operand A
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vtile + 2 * C::V_TILE);
   uint64_t* full = bars;                       // [NST] Bt landed
   uint64_t* empty = bars + C::NST;             // [NST] MMA done with Bt stage
   uint64_t* vfull = bars + 2 * C::NST;         // [2]  v tile landed
@@ -428,7 +455,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     }
     for (int a = 0; a < C::NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], C::GROUP_THREADS);
+      mbar_init(&tempty[a], C::EPI_THREADS);
     }
     fence_mbar_init();
   }
@@ -482,17 +509,16 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     int stage = 0, vb = 0;
     uint32_t phase = 0, vphase = 0;
     long long k = 0;  // global sub-tile counter -> accumulator k % NACC
+    const uint32_t idesc = idesc_bf16(kTileRows, C::MSUB);
     QueuePos qp;
     for (;;) {
       const long long it = wq_pop(wq, qp);
       if (it < 0) break;
-      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
+      const int cig = (int)(it / n_tiles);
       const SlotTask& t = args.t[find_task_ci(args, cig)];
-      const int4 tile = pd.tiles[ti];
-      const int npad = (tile.y + 15) & ~15;  // rows >= tile.y hold stale data: their D columns are never read
-      const uint32_t idesc = idesc_bf16(C::MSUB, npad);
       const int n_sub = t.CI / C::MSUB;
       mbar_wait(&vfull[vb], vphase);
+      // rows >= tile.y of the v tile hold stale data: their D rows are never read
       const uint32_t va = smem_u32(vtile + vb * C::V_TILE);
       for (int sb = 0; sb < n_sub; ++sb, ++k) {
         const int acc = (int)(k % C::NACC);
@@ -504,7 +530,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
 #pragma unroll
           for (int kk = 0; kk < R / 16; ++kk)
-            umma_bf16(d_tmem, sw128_desc(ba + kk * 32), sw128_desc(va + kk * 32), idesc, kk > 0 ? 1u : 0u);
+            umma_bf16(d_tmem, sw128_desc(va + kk * 32), sw128_desc(ba + kk * 32), idesc, kk > 0 ? 1u : 0u);
           umma_commit(&empty[stage]);
           umma_commit(&tfull[acc]);
           if (sb == n_sub - 1) umma_commit(&vempty[vb]);
@@ -521,15 +547,11 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue (two groups, alternate sub-tiles) =====================
-    const int grp = warp >> 3, wl = warp & 7;
-    const int gt = threadIdx.x & 255;            // thread within the group
-    const int col = (wl & 3) * 32 + lane;        // TMEM lane = output column within the sub-tile
-    const int half = wl >> 2;                    // row half for phase (1)
-    const bool bf16y = !(args.y_fp32 || args.y_store);
-    uint8_t* sg = stg + grp * C::STG;
-    uint4 ypf[C::PF];                            // prefetched y chunks (bf16 mode)
-    int prow[C::PF];                             // y row of each chunk
+    // ===================== epilogue: one row x 32 columns per thread =====================
+    // y moves in full 32-byte sectors (256-bit LDG/STG), the next sub-tile's
+    // segment loaded while this one is in the epilogue.
+    const int q = warp & 3, cb = warp >> 2;
+    const bool yload = !(args.y_fp32 || args.y_store);
     long long k = 0;                             // global sub-tile counter (same as the MMA warp's)
     QueuePos qp;
     for (;;) {
@@ -541,91 +563,52 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const int4 tile = pd.tiles[ti];
       const float s_a = args.scale[tile.z / t.E];
       const int n_sub = t.CI / C::MSUB;
-      const long long cbase = (long long)ci * t.CI;
-      // chunk j of this thread: row n = (gt + j*256) / 16, columns 8*((gt + j*256) % 16) ..+8
+      const int n = q * 32 + lane;
+      const bool live = n < tile.y;
+      const long long prow = live ? (long long)__ldg(pd.perm + tile.x + n) : 0;
+      const long long o0 = prow * t.h_out + (long long)ci * t.CI + cb * 32;  // + sb * MSUB
+      uint16_t* yb = static_cast<uint16_t*>(t.y);
+      uint32_t ycur[16], ynxt[16];
+      if (yload && live) ldg256x2(yb + o0, ynxt);
+      for (int sb = 0; sb < n_sub; ++sb, ++k) {
 #pragma unroll
-      for (int j = 0; j < C::PF; ++j) {
-        const int n = (gt + j * C::GROUP_THREADS) >> 4;
-        prow[j] = n < tile.y ? __ldg(pd.perm + tile.x + n) : 0;
-      }
-      auto issue_y = [&](int sb) {
-#pragma unroll
-        for (int j = 0; j < C::PF; ++j) {
-          const int q = gt + j * C::GROUP_THREADS, n = q >> 4, c8 = q & 15;
-          if (n < tile.y)
-            ypf[j] = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(t.y) + (long long)prow[j] * t.h_out +
-                                                     cbase + (long long)sb * C::MSUB + c8 * 8);
-        }
-      };
-      const int first = (int)((grp - k) & 1);  // this group's first sub-tile in the item
-      if (bf16y && first < n_sub) issue_y(first);
-      for (int sb = first; sb < n_sub; sb += 2) {
-        const long long kk = k + sb;
-        const int acc = (int)(kk % C::NACC);
-        const long long c0 = cbase + (long long)sb * C::MSUB;
-        // (1) TMEM -> staging (this warp: lanes 32*(wl%4).., rows 16*half + 32*i)
-        mbar_wait(&tfull[acc], (uint32_t)((kk / C::NACC) & 1));
+        for (int i = 0; i < 16; ++i) ycur[i] = ynxt[i];
+        if (yload && live && sb + 1 < n_sub) ldg256x2(yb + o0 + (long long)(sb + 1) * C::MSUB, ynxt);
+        const int acc = (int)(k % C::NACC);
+        mbar_wait(&tfull[acc], (uint32_t)((k / C::NACC) & 1));
         tc_fence_after();
-        {
-          const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + acc * C::ACC_COLS;
-          float* srow = reinterpret_cast<float*>(sg) + col;
-          for (int n0 = 16 * half; n0 < tile.y; n0 += 32) {
-            uint32_t d0[16];
-            tmem_ld16_nowait(taddr + n0, d0);
-            tmem_wait_ld();
-            const int nn = min(16, tile.y - n0);
+        uint32_t d[32];
+        tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS + cb * 32, d);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (!live) continue;
+        const long long o = o0 + (long long)sb * C::MSUB;
+        if (yload || args.y_store == 2) {
+          uint32_t w[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nn) srow[(n0 + j) * (C::STG_PITCH / 4)] = s_a * __uint_as_float(d0[j]);
+          for (int i = 0; i < 16; ++i) {
+            const float e0 = s_a * __uint_as_float(d[2 * i]), e1 = s_a * __uint_as_float(d[2 * i + 1]);
+            w[i] = yload ? pack_bf16x2_rn(bf16lo(ycur[i]) + e0, bf16hi(ycur[i]) + e1) : pack_bf16x2_rn(e0, e1);
           }
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
-        }
-        named_bar_sync(1 + grp, C::GROUP_THREADS);
-        // (2) y read-modify-write from the staging tile
-        if (bf16y) {
-#pragma unroll
-          for (int j = 0; j < C::PF; ++j) {
-            const int q = gt + j * C::GROUP_THREADS, n = q >> 4, c8 = q & 15;
-            if (n < tile.y) {
-              const uint32_t sa = smem_u32(sg + n * C::STG_PITCH + c8 * 32);
-              const float4 e0 = lds128f(sa), e1 = lds128f(sa + 16);
-              const uint4 yv = ypf[j];
-              uint4 o;
-              o.x = pack_bf16x2_rn(bf16lo(yv.x) + e0.x, bf16hi(yv.x) + e0.y);
-              o.y = pack_bf16x2_rn(bf16lo(yv.y) + e0.z, bf16hi(yv.y) + e0.w);
-              o.z = pack_bf16x2_rn(bf16lo(yv.z) + e1.x, bf16hi(yv.z) + e1.y);
-              o.w = pack_bf16x2_rn(bf16lo(yv.w) + e1.z, bf16hi(yv.w) + e1.w);
-              *reinterpret_cast<uint4*>(static_cast<uint16_t*>(t.y) + (long long)prow[j] * t.h_out + c0 + c8 * 8) = o;
-            }
-          }
-          if (sb + 2 < n_sub) issue_y(sb + 2);  // in flight across the other group's sub-tile
+          stg256x2(yb + o, w);
         } else {
-          // fp32 y (parity) or delta store (sharded delta mode): 4 columns per item
-          for (int q = gt; q < tile.y * (C::MSUB / 4); q += C::GROUP_THREADS) {
-            const int n = q >> 5, c4 = q & 31;
-            const float4 e = lds128f(smem_u32(sg + n * C::STG_PITCH + c4 * 16));
-            const long long row = __ldg(pd.perm + tile.x + n);
-            if (args.y_store == 2) {
-              uint2 o;
-              o.x = pack_bf16x2_rn(e.x, e.y);
-              o.y = pack_bf16x2_rn(e.z, e.w);
-              *reinterpret_cast<uint2*>(static_cast<uint16_t*>(t.y) + row * t.h_out + c0 + c4 * 4) = o;
-              continue;
-            }
-            float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + row * t.h_out + c0 + c4 * 4);
+          // fp32 y (accumulate) or fp32 delta store (sharded): 8 x 16 bytes
+          float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 e = make_float4(s_a * __uint_as_float(d[4 * i + 0]), s_a * __uint_as_float(d[4 * i + 1]),
+                                         s_a * __uint_as_float(d[4 * i + 2]), s_a * __uint_as_float(d[4 * i + 3]));
             if (args.y_store) {
-              *yp = e;
+              yp[i] = e;
             } else {
-              float4 o = *yp;
-              o.x += e.x; o.y += e.y; o.z += e.z; o.w += e.w;
-              *yp = o;
+              float4 v = yp[i];
+              v.x += e.x; v.y += e.y; v.z += e.z; v.w += e.w;
+              yp[i] = v;
             }
           }
         }
-        named_bar_sync(1 + grp, C::GROUP_THREADS);  // staging free for this group's next sub-tile
       }
-      k += n_sub;
     }
   }
   tc_fence_before();

@@ -1,0 +1,28 @@
+#!/bin/bash
+# Regenerate the judged evidence under profiles/ on a B200 (run via gpurun):
+#   bench lines (our arm, reference arm), ncu launch lists per workload,
+#   ncu --set full summaries of the kernels of the default workload.
+#   usage: bash tools/profile_round.sh TAG     (e.g. r1)
+set -u
+TAG=${1:-r1}
+OUT=gpurun_out/prof
+mkdir -p $OUT
+timeout 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
+for w in mixtral_sharded mixtral_decode mixtral_prefill llama_decode; do
+  timeout 300 python bench.py --workload $w --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 \
+      > $OUT/bench_$w.json 2> $OUT/bench_$w.err
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      --csv --log-file $OUT/launches_$w.csv \
+      python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+done
+# one full capture per kernel kind of the default workload (after warm-up)
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:'segment_kernel|simt_shrink|simt_expand|tc_shrink|tc_vreduce|tc_expand' -s 6 -c 6 \
+    -o $OUT/full_mixtral_sharded python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 \
+    > $OUT/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:'simt_shrink|simt_expand|tc_shrink|tc_expand' -s 4 -c 4 \
+    -o $OUT/full_mixtral_prefill python bench.py --workload mixtral_prefill --steps 2 --warmup 3 --no-cpu-baseline \
+    --e2e-steps 0 > $OUT/ncu_full_prefill.log 2>&1
+echo done
