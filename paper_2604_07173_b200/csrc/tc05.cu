@@ -424,6 +424,9 @@ struct ExpandCfg {
   static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 512;
 };
 
+// output mode M (compile time): 0 bf16 accumulate, 1 fp32 delta store, 2 bf16
+// delta store (sharded), 3 fp32 accumulate
+template <int M>
 __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     tc_expand_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   using C = ExpandCfg;
@@ -548,10 +551,12 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     }
   } else {
     // ===================== epilogue: one row x 32 columns per thread =====================
-    // y moves in full 32-byte sectors (256-bit LDG/STG), the next sub-tile's
-    // segment loaded while this one is in the epilogue.
+    // y moves in full 32-byte sectors (256-bit LDG/STG); the segments of the
+    // next two sub-tiles of the item are in flight while one is in the
+    // epilogue.  (A look-ahead across items, peeking the queue, measured slower:
+    // register pressure.)
     const int q = warp & 3, cb = warp >> 2;
-    const bool yload = !(args.y_fp32 || args.y_store);
+    constexpr bool yload = M == 0;
     long long k = 0;                             // global sub-tile counter (same as the MMA warp's)
     QueuePos qp;
     for (;;) {
@@ -568,46 +573,71 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const long long prow = live ? (long long)__ldg(pd.perm + tile.x + n) : 0;
       const long long o0 = prow * t.h_out + (long long)ci * t.CI + cb * 32;  // + sb * MSUB
       uint16_t* yb = static_cast<uint16_t*>(t.y);
-      uint32_t ycur[16], ynxt[16];
-      if (yload && live) ldg256x2(yb + o0, ynxt);
-      for (int sb = 0; sb < n_sub; ++sb, ++k) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) ycur[i] = ynxt[i];
-        if (yload && live && sb + 1 < n_sub) ldg256x2(yb + o0 + (long long)(sb + 1) * C::MSUB, ynxt);
+      // three segment buffers with compile-time roles (a register rotation
+      // would wait for the newest load): step sb consumes buf[sb % 3] and
+      // starts the load of sub-tile sb + 2 into buf[(sb + 2) % 3]
+      auto step = [&](int sb, uint32_t (&ya)[16], uint32_t (&yn)[16]) {
+        if (sb >= n_sub) return;
+        if (yload && live && sb + 2 < n_sub) ldg256x2(yb + o0 + (long long)(sb + 2) * C::MSUB, yn);
         const int acc = (int)(k % C::NACC);
         mbar_wait(&tfull[acc], (uint32_t)((k / C::NACC) & 1));
+        ++k;
         tc_fence_after();
-        uint32_t d[32];
-        tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS + cb * 32, d);
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        if (!live) continue;
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS + cb * 32;
         const long long o = o0 + (long long)sb * C::MSUB;
-        if (yload || args.y_store == 2) {
-          uint32_t w[16];
+        if constexpr (M == 0 || M == 2) {
+          // two halves of 16 columns: ya[] becomes the output in place
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float e0 = s_a * __uint_as_float(d[2 * i]), e1 = s_a * __uint_as_float(d[2 * i + 1]);
-            w[i] = yload ? pack_bf16x2_rn(bf16lo(ycur[i]) + e0, bf16hi(ycur[i]) + e1) : pack_bf16x2_rn(e0, e1);
-          }
-          stg256x2(yb + o, w);
-        } else {
-          // fp32 y (accumulate) or fp32 delta store (sharded): 8 x 16 bytes
-          float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + o);
+          for (int h = 0; h < 2; ++h) {
+            uint32_t d[16];
+            tmem_ld16_nowait(ta + h * 16, d);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 e = make_float4(s_a * __uint_as_float(d[4 * i + 0]), s_a * __uint_as_float(d[4 * i + 1]),
-                                         s_a * __uint_as_float(d[4 * i + 2]), s_a * __uint_as_float(d[4 * i + 3]));
-            if (args.y_store) {
-              yp[i] = e;
-            } else {
-              float4 v = yp[i];
-              v.x += e.x; v.y += e.y; v.z += e.z; v.w += e.w;
-              yp[i] = v;
+            for (int i = 0; i < 8; ++i) {
+              const float e0 = s_a * __uint_as_float(d[2 * i]), e1 = s_a * __uint_as_float(d[2 * i + 1]);
+              const uint32_t yv = ya[h * 8 + i];
+              ya[h * 8 + i] = yload ? pack_bf16x2_rn(bf16lo(yv) + e0, bf16hi(yv) + e1) : pack_bf16x2_rn(e0, e1);
             }
           }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          if (live) stg256x2(yb + o, ya);
+        } else {
+          // fp32 y (accumulate) or fp32 delta store (sharded): 2 halves x 4 x 16 bytes
+          float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + o);
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            uint32_t d[16];
+            tmem_ld16_nowait(ta + h * 16, d);
+            tmem_wait_ld();
+            if (live) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 e = make_float4(s_a * __uint_as_float(d[4 * i + 0]), s_a * __uint_as_float(d[4 * i + 1]),
+                                             s_a * __uint_as_float(d[4 * i + 2]), s_a * __uint_as_float(d[4 * i + 3]));
+                if constexpr (M == 1) {
+                  yp[h * 4 + i] = e;
+                } else {
+                  float4 v = yp[h * 4 + i];
+                  v.x += e.x; v.y += e.y; v.z += e.z; v.w += e.w;
+                  yp[h * 4 + i] = v;
+                }
+              }
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
         }
+      };
+      uint32_t b0[16], b1[16], b2[16];
+      if (yload && live) {
+        ldg256x2(yb + o0, b0);
+        if (n_sub > 1) ldg256x2(yb + o0 + C::MSUB, b1);
+      }
+      for (int sb = 0; sb < n_sub; sb += 3) {
+        step(sb, b0, b2);
+        step(sb + 1, b1, b0);
+        step(sb + 2, b2, b1);
       }
     }
   }
@@ -650,10 +680,13 @@ cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid
 }
 
 cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
-  static unsigned long long mask = 0;
-  cudaError_t e = set_smem_once(tc_expand_kernel, ExpandCfg::SMEM, mask);
+  static unsigned long long mask[4] = {0, 0, 0, 0};
+  const int m = args.y_store == 1 ? 1 : args.y_store == 2 ? 2 : args.y_fp32 ? 3 : 0;
+  auto kern = m == 0 ? tc_expand_kernel<0> : m == 1 ? tc_expand_kernel<1> : m == 2 ? tc_expand_kernel<2>
+                                                                                     : tc_expand_kernel<3>;
+  cudaError_t e = set_smem_once(kern, ExpandCfg::SMEM, mask[m]);
   if (e != cudaSuccess) return e;
-  tc_expand_kernel<<<grid, ExpandCfg::THREADS, ExpandCfg::SMEM, stream>>>(args, pd);
+  kern<<<grid, ExpandCfg::THREADS, ExpandCfg::SMEM, stream>>>(args, pd);
   return cudaGetLastError();
 }
 
