@@ -75,6 +75,18 @@ struct SlotTask {
   int KI, SJ, n_kc;    // shrink: j-range per item, j per stage, items per row group
   int CI, SC, n_ci;    // expand: c-range per item, c rows per stage, items per row group
   int kc_base, ci_base;// prefix over tasks of n_kc / n_ci
+  long long x_off;     // RemoteIn mode: byte offset of this slot's x rows in a source's send buffer
+};
+
+// Owner side of a peer-to-peer sharded apply (shard.cu): received row r is
+// not copied to the owner -- it stays in source s's registered send buffer
+// (NVLink peer mapping) and the shrink kernels read it from there.
+constexpr int kMaxWorld = 8;
+struct RemoteIn {
+  int G;                         // 0: rows are local (t.x + row * h_in)
+  int ro[kMaxWorld + 1];         // received-row offsets per source
+  int rowbase[kMaxWorld];        // row in source s's send buffer = r + rowbase[s]
+  const char* src[kMaxWorld];    // source s's send buffer (peer pointer)
 };
 
 struct MultiArgs {
@@ -84,6 +96,7 @@ struct MultiArgs {
   int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const float* scale;      // [n_adapters] s_a
+  RemoteIn rin;            // x rows read from peers (sharded P2P owner), G = 0 otherwise
   SlotTask t[kMaxTasks];
   // task of each global shrink chunk (kc) / expand column range (ci) index,
   // filled by the host when total_kc / total_ci <= kTaskTable
@@ -92,6 +105,13 @@ struct MultiArgs {
 };
 
 #ifdef __CUDACC__
+// address of x row `row` of task t (local, or in a source's send buffer)
+__device__ __forceinline__ const uint16_t* x_row(const MultiArgs& a, const SlotTask& t, int row) {
+  if (a.rin.G == 0) return t.x + (long long)row * t.h_in;
+  int s = 0;
+  while (s + 1 < a.rin.G && a.rin.ro[s + 1] <= row) ++s;
+  return reinterpret_cast<const uint16_t*>(a.rin.src[s] + t.x_off) + (long long)(row + a.rin.rowbase[s]) * t.h_in;
+}
 // task owning global expand column-range index g (ci_base prefix)
 __device__ __forceinline__ int find_task_ci(const MultiArgs& a, int g) {
   if (a.total_ci <= kTaskTable) return a.ci_task[g];

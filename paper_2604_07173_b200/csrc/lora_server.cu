@@ -201,8 +201,9 @@ lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int ran
 
 // delta mode for the sharded owner: d[i] receives s*(xA)B (stored, not added) as fp32 or bf16
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
-                                void* const* d, cudaStream_t st, bool bf16) {
-  return apply_multi_impl(s, p, n, slots, x, d, bf16 ? LORA_BF16 : LORA_FP32, st, bf16 ? 2 : 1);
+                                void* const* d, cudaStream_t st, bool bf16, const RemoteIn* rin,
+                                const long long* x_off) {
+  return apply_multi_impl(s, p, n, slots, x, d, bf16 ? LORA_BF16 : LORA_FP32, st, bf16 ? 2 : 1, rin, x_off);
 }
 
 static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, const void* A, const void* B,
@@ -422,7 +423,8 @@ static void fill_task_tables(MultiArgs& a) {
 }
 
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
-                               void* const* y, lora_dtype_t y_dtype, cudaStream_t st, int store) {
+                               void* const* y, lora_dtype_t y_dtype, cudaStream_t st, int store, const RemoteIn* rin,
+                               const long long* x_off) {
   if (!p || p->s != s) return fail(s, LORA_ERR_INVALID_ARG, "plan does not belong to this server");
   if (p->n_experts < 0) return fail(s, LORA_ERR_INVALID_ARG, "plan was never built");
   if (n < 0 || (n > 0 && (!slots || !x || !y))) return fail(s, LORA_ERR_INVALID_ARG, "bad slot list");
@@ -458,6 +460,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.y_store = store;
     args.pl = placement(s);
     args.scale = s->d_scale;
+    if (rin) args.rin = *rin;
     int kc = 0, ci = 0;
     for (int i = 0; i < nb; ++i) {
       const SlotInfo& si = s->slots[slots[b0 + i]];
@@ -465,6 +468,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       t.At = si.At;
       t.Bt = si.Bt;
       t.x = static_cast<const uint16_t*>(x[b0 + i]);
+      t.x_off = x_off ? x_off[b0 + i] : 0;
       t.y = y[b0 + i];
       t.vpart_off = (long long)si.kc_prefix * p->max_rows * s->r;
       t.vbf_off = (long long)slots[b0 + i] * p->max_rows * s->r;

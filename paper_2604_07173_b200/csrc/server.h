@@ -75,7 +75,7 @@ lora_status_t fail(lora_server* s, lora_status_t st, const std::string& msg);
 lora_status_t cuda_fail(lora_server* s, cudaError_t e, const char* where);
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
                                const void* const* x, void* const* y, lora_dtype_t y_dtype, cudaStream_t st,
-                               int store = 0);
+                               int store = 0, const RemoteIn* rin = nullptr, const long long* x_off = nullptr);
 lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapter_ids, const int32_t* expert_ids,
                               int T, int E, cudaStream_t st);
 lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out);
@@ -87,4 +87,5 @@ void lora_shard_free(lora_server* s);
 lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot);
 inline lora::Placement placement(const lora_server* s) { return lora::Placement{s->world, s->shard_rank, s->n_hot}; }
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
-                                const void* const* x, void* const* d, cudaStream_t st, bool bf16);
+                                const void* const* x, void* const* d, cudaStream_t st, bool bf16,
+                                const lora::RemoteIn* rin = nullptr, const long long* x_off = nullptr);

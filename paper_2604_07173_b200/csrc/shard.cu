@@ -51,6 +51,7 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -79,6 +80,7 @@ NcclApi& nccl() {
   SYM(Send, "ncclSend");
   SYM(Recv, "ncclRecv");
   SYM(AllGather, "ncclAllGather");
+  SYM(AllReduce, "ncclAllReduce");
   SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
   api.ok = true;
@@ -205,6 +207,68 @@ __global__ void scatter_add4_kernel(void* __restrict__ y, int y_fp32, const void
   }
 }
 
+// Peer-to-peer transport (ShardState::p2p).  Owner side: the ids of received
+// row r are read from source s's registered send buffer (NVLink peer mapping).
+struct PeerRows {
+  int G;
+  int off[kMaxWorld + 1];   // row ranges per peer
+  int rowbase[kMaxWorld];   // row in the peer's buffer = r + rowbase[p]
+  const char* base[kMaxWorld];
+};
+LORA_DEVINL int peer_of(const PeerRows& pr, int r) {
+  int p = 0;
+  while (p + 1 < pr.G && pr.off[p + 1] <= r) ++p;
+  return p;
+}
+
+// ids_recv[r] = a, ids_recv[Rmax + r] = e of received row r (send buffer ids: [2][max_rows])
+__global__ void pull_ids_kernel(PeerRows pr, int max_rows, int32_t* __restrict__ ids_recv, long long Rmax, int n) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int p = peer_of(pr, r);
+    const int32_t* ids = reinterpret_cast<const int32_t*>(pr.base[p]);
+    const int row = r + pr.rowbase[p];
+    ids_recv[r] = ids[row];
+    ids_recv[Rmax + r] = ids[max_rows + row];
+  }
+}
+
+// Source side: y[idx[j]] = round(y + delta) where the delta of send-order row j
+// sits in owner p's registered delta buffer (peer mapping), row j + rowbase[p]
+// of the slot region at byte offset slot_off.  The NVLink read is fused with
+// the accumulate.  4 columns per thread.
+__global__ void pull_scatter_add4_kernel(void* __restrict__ y, int y_fp32, PeerRows pr, long long slot_off, int d_bf16,
+                                         const int32_t* __restrict__ idx, int n, int width) {
+  const int q4 = width >> 2;
+  for (int j = blockIdx.y; j < n; j += gridDim.y) {
+    const long long row = idx[j];
+    const int p = peer_of(pr, j);
+    const long long drow = (long long)(j + pr.rowbase[p]) * q4;
+    const char* dbase = pr.base[p] + slot_off;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < q4; c += gridDim.x * blockDim.x) {
+      float4 v;
+      if (d_bf16) {
+        const uint2 b = reinterpret_cast<const uint2*>(dbase)[drow + c];
+        v = make_float4(bf16lo(b.x), bf16hi(b.x), bf16lo(b.y), bf16hi(b.y));
+      } else {
+        v = reinterpret_cast<const float4*>(dbase)[drow + c];
+      }
+      if (y_fp32) {
+        float4* yp = reinterpret_cast<float4*>(y) + row * q4 + c;
+        float4 o = *yp;
+        o.x += v.x; o.y += v.y; o.z += v.z; o.w += v.w;
+        *yp = o;
+      } else {
+        uint2* yp = reinterpret_cast<uint2*>(y) + row * q4 + c;
+        const uint2 o = *yp;
+        uint2 r;
+        r.x = pack_bf16x2_rn(bf16lo(o.x) + v.x, bf16hi(o.x) + v.y);
+        r.y = pack_bf16x2_rn(bf16lo(o.y) + v.z, bf16hi(o.y) + v.w);
+        *yp = r;
+      }
+    }
+  }
+}
+
 int grid_of(long long n) {
   long long g = (n + 255) / 256;
   return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
@@ -222,11 +286,35 @@ struct ShardState {
   lora_plan* local_plan = nullptr;  // plan over this rank's rows processed in place
   bool fp32_return = false;
   bool loopback = false;
+  // peer-to-peer transport: registered (IPC-exported) buffers, mapped on every rank
+  bool p2p = true;
+  void* sendbuf = nullptr;  // [2][max_rows] ids + per distinct x buffer [max_rows][h_in] bf16, send order
+  void* dbuf = nullptr;     // per slot [Rmax][h_out] deltas of received rows
+  size_t send_cap = 0, d_cap = 0;
+  std::vector<char*> peer_send, peer_d;  // index = rank (own rank: the local pointers)
+  int* d_bar = nullptr;                   // barrier word (NCCL all-reduce)
 };
+
+// Release the peer mappings and the registered buffers.
+static void p2p_release(ShardState* sh, int me) {
+  for (size_t p = 0; p < sh->peer_send.size(); ++p)
+    if ((int)p != me) {
+      if (sh->peer_send[p]) cudaIpcCloseMemHandle(sh->peer_send[p]);
+      if (sh->peer_d[p]) cudaIpcCloseMemHandle(sh->peer_d[p]);
+    }
+  sh->peer_send.clear();
+  sh->peer_d.clear();
+  cudaFree(sh->sendbuf);
+  cudaFree(sh->dbuf);
+  sh->sendbuf = sh->dbuf = nullptr;
+  sh->send_cap = sh->d_cap = 0;
+}
 
 void lora_shard_free(lora_server* s) {
   if (!s || !s->shard) return;
   ShardState* sh = s->shard;
+  p2p_release(sh, s->shard_rank);
+  cudaFree(sh->d_bar);
   if (sh->comm && nccl().ok) nccl().CommDestroy(sh->comm);
   cudaFree(sh->buf);
   if (sh->plan) plan_destroy_impl(sh->plan);
@@ -283,6 +371,9 @@ extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, in
   sh->fp32_return = f32 && f32[0] && std::strcmp(f32, "0") != 0;
   const char* lb = std::getenv("LORA_SHARD_LOOPBACK");
   sh->loopback = lb && lb[0] && std::strcmp(lb, "0") != 0;
+  const char* tr = std::getenv("LORA_SHARD_TRANSPORT");
+  sh->p2p = !(tr && std::strcmp(tr, "nccl") == 0);
+  if (world > kMaxWorld) sh->p2p = false;
   ncclUniqueId id;
   std::memcpy(&id, nccl_unique_id, 128);
   cudaSetDevice(s->device);
@@ -292,6 +383,12 @@ extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, in
     lora_server_destroy(s);
     *out = nullptr;
     return fail(nullptr, LORA_ERR_CUDA, "stream / event creation failed");
+  }
+  ok = ok && cudaMalloc(&sh->d_bar, sizeof(int)) == cudaSuccess && cudaMemset(sh->d_bar, 0, sizeof(int)) == cudaSuccess;
+  if (!ok) {
+    lora_server_destroy(s);
+    *out = nullptr;
+    return fail(nullptr, LORA_ERR_CUDA, "barrier word allocation failed");
   }
   ncclResult_t r = api.CommInitRank(&sh->comm, world, id, rank);
   if (r != ncclSuccess) {
@@ -307,6 +404,75 @@ extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, in
     lora_server_destroy(s);
     *out = nullptr;
     return fail(nullptr, st, m);
+  }
+  return LORA_OK;
+}
+
+// Grow the registered P2P buffers to (need_send, need_d) bytes -- collective:
+// every rank computes the same sizes from the same slot list.  Exports IPC
+// handles, all-gathers them over NCCL and maps every peer's buffers; if any
+// rank cannot map a peer, every rank falls back to the NCCL transport.
+static lora_status_t p2p_register(lora_server* s, size_t need_send, size_t need_d, cudaStream_t st) {
+  ShardState* sh = s->shard;
+  NcclApi& api = nccl();
+  const int G = s->world, me = s->shard_rank;
+  if (need_send <= sh->send_cap && need_d <= sh->d_cap) return LORA_OK;
+  cudaStreamSynchronize(st);
+  cudaStreamSynchronize(sh->cs);
+  p2p_release(sh, me);
+  need_send = std::max(need_send, (size_t)1 << 20);
+  need_d = std::max(need_d, (size_t)1 << 20);
+  if (cudaMalloc(&sh->sendbuf, need_send) != cudaSuccess || cudaMalloc(&sh->dbuf, need_d) != cudaSuccess) {
+    cudaGetLastError();
+    p2p_release(sh, me);
+    return fail(s, LORA_ERR_OOM, "P2P buffer allocation failed");
+  }
+  sh->send_cap = need_send;
+  sh->d_cap = need_d;
+  sh->peer_send.assign(G, nullptr);
+  sh->peer_d.assign(G, nullptr);
+  sh->peer_send[me] = static_cast<char*>(sh->sendbuf);
+  sh->peer_d[me] = static_cast<char*>(sh->dbuf);
+  if (G == 1) return LORA_OK;
+  // handle exchange: [G][2][64 bytes]
+  std::vector<cudaIpcMemHandle_t> h(2 * G);
+  if (cudaIpcGetMemHandle(&h[2 * me], sh->sendbuf) != cudaSuccess ||
+      cudaIpcGetMemHandle(&h[2 * me + 1], sh->dbuf) != cudaSuccess)
+    return fail(s, LORA_ERR_CUDA, "cudaIpcGetMemHandle failed");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  char* dh = nullptr;
+  if (cudaMalloc(&dh, 128 * G + 4) != cudaSuccess) return fail(s, LORA_ERR_OOM, "handle buffer");
+  cudaMemcpy(dh + 128 * me, &h[2 * me], 128, cudaMemcpyHostToDevice);
+  ncclResult_t r = api.AllGather(dh + 128 * me, dh, 128, ncclUint8, sh->comm, st);
+  if (r != ncclSuccess) {
+    cudaFree(dh);
+    return fail(s, LORA_ERR_NCCL, std::string("handle all-gather: ") + api.GetErrorString(r));
+  }
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h.data(), dh, 128 * G, cudaMemcpyDeviceToHost);
+  int ok = 1;
+  for (int p = 0; p < G; ++p) {
+    if (p == me) continue;
+    void* a = nullptr;
+    void* b = nullptr;
+    if (cudaIpcOpenMemHandle(&a, h[2 * p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&b, h[2 * p + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+    }
+    sh->peer_send[p] = static_cast<char*>(a);
+    sh->peer_d[p] = static_cast<char*>(b);
+  }
+  // every rank must agree on the transport
+  int* dok = reinterpret_cast<int*>(dh + 128 * G);
+  cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
+  r = api.AllReduce(dok, dok, 1, ncclInt32, ncclMin, sh->comm, st);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(dh);
+  if (r != ncclSuccess || !ok) {
+    p2p_release(sh, me);
+    sh->p2p = false;  // NCCL send/recv from now on, on every rank
   }
   return LORA_OK;
 }
@@ -418,29 +584,74 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   bool exchange = false;
   for (int v : cnt) exchange = exchange || v > 0;
 
+  // peer-to-peer transport: registered buffer layout (identical on every rank)
+  size_t p_ids = 0, p_need_send = 0, p_need_d = 0;
+  std::vector<size_t> p_xo(xd.size()), p_doff(n);
+  p_need_send = al(sizeof(int32_t) * 2 * s->max_rows);
+  for (size_t j = 0; j < xd.size(); ++j) {
+    p_xo[j] = p_need_send;
+    p_need_send += al((size_t)s->max_rows * x_hin[j] * 2);
+  }
+  for (int i = 0; i < n; ++i) {
+    p_doff[i] = p_need_d;
+    p_need_d += al((size_t)Rmax * s->slots[slots[i]].h_out * dsz);
+  }
+  if (exchange && sh->p2p) {
+    const lora_status_t rr = p2p_register(s, p_need_send, p_need_d, st);
+    if (rr != LORA_OK) return rr;
+  }
+  const bool p2p = exchange && sh->p2p;
+  // row maps: my send-order rows for owner p; rows I receive from source p
+  PeerRows pr_in{}, pr_out{};
+  if (p2p) {
+    pr_in.G = pr_out.G = G;
+    for (int p = 0; p <= G; ++p) {
+      pr_in.off[p] = (int)ro[p];
+      pr_out.off[p] = (int)so[p];
+    }
+    for (int p = 0; p < G; ++p) {
+      int before_me_in_p = 0, before_me_at_p = 0;
+      for (int q = 0; q < me; ++q) before_me_in_p += cnt[p * G + q];  // p's rows for owners < me
+      for (int q = 0; q < me; ++q) before_me_at_p += cnt[q * G + p];  // rows owner p receives from sources < me
+      pr_in.rowbase[p] = before_me_in_p - (int)ro[p];
+      pr_in.base[p] = sh->peer_send[p];
+      pr_out.rowbase[p] = before_me_at_p - (int)so[p];
+      pr_out.base[p] = sh->peer_d[p];
+    }
+  }
+  (void)p_ids;
+
   // 3. (comm stream) pack + dispatch, overlapped with the in-place apply
   if (exchange) {
     CKS(cudaEventRecord(sh->ev[0], st));
     CKS(cudaStreamWaitEvent(cs, sh->ev[0], 0));
+    // P2P: pack straight into the registered send buffer the owners read from
+    int32_t* ids_dst = p2p ? static_cast<int32_t*>(sh->sendbuf) : d_ids_send;
     if (n_send > 0) {
       const int pi = prof_start(s, cs);
       gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(adapter_ids),
-                                                            reinterpret_cast<uint32_t*>(d_ids_send), d_send_idx,
+                                                            reinterpret_cast<uint32_t*>(ids_dst), d_send_idx,
                                                             n_send);
       if (expert_ids)
         gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(expert_ids),
-                                                              reinterpret_cast<uint32_t*>(d_ids_send + s->max_rows),
+                                                              reinterpret_cast<uint32_t*>(ids_dst + s->max_rows),
                                                               d_send_idx, n_send);
       else
-        CKS(cudaMemsetAsync(d_ids_send + s->max_rows, 0, sizeof(int32_t) * n_send, cs));
+        CKS(cudaMemsetAsync(ids_dst + s->max_rows, 0, sizeof(int32_t) * n_send, cs));
       for (size_t j = 0; j < xd.size(); ++j) {
         const int chunks = x_hin[j] / 8;  // 16-byte chunks per bf16 row
         gather_rows16_kernel<<<dim3((chunks + 255) / 256, std::min(n_send, 65535)), 256, 0, cs>>>(
-            static_cast<const uint4*>(xd[j]), reinterpret_cast<uint4*>(base + o_xs[j]), d_send_idx, n_send, chunks);
+            static_cast<const uint4*>(xd[j]),
+            reinterpret_cast<uint4*>(p2p ? static_cast<char*>(sh->sendbuf) + p_xo[j] : base + o_xs[j]), d_send_idx,
+            n_send, chunks);
       }
       prof_stop(s, pi, kKShardGather, cs);
       CKS(cudaGetLastError());
     }
+    if (p2p) {
+      // every source's send buffer complete before any owner reads it
+      CKN(api.AllReduce(sh->d_bar, sh->d_bar, 1, ncclInt32, ncclSum, sh->comm, cs));
+    } else {
     CKN(api.GroupStart());
     for (int p = 0; p < G; ++p) {
       const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
@@ -458,6 +669,7 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
       }
     }
     CKN(api.GroupEnd());
+    }
     CKS(cudaEventRecord(sh->ev[1], cs));
   }
 
@@ -475,17 +687,52 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
 
   // 5. received rows: owner-side plan + delta-mode apply
   CKS(cudaStreamWaitEvent(st, sh->ev[1], 0));
+  if (p2p && n_recv > 0) {
+    pull_ids_kernel<<<grid_of(n_recv), 256, 0, st>>>(pr_in, s->max_rows, d_ids_recv, Rmax, n_recv);
+    CKS(cudaGetLastError());
+  }
   rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, st);
   if (rc != LORA_OK) return rc;
   if (n_recv > 0) {
     std::vector<const void*> xs(n);
     std::vector<void*> ds(n);
-    for (int i = 0; i < n; ++i) {
-      xs[i] = base + o_xr[x_of[i]];
-      ds[i] = base + o_d[i];
+    std::vector<long long> xo(n);
+    RemoteIn rin{};
+    if (p2p) {
+      // the shrink kernels read each received x row from its source's send
+      // buffer over NVLink (the dispatch is fused into the shrink's loads)
+      rin.G = G;
+      for (int p = 0; p <= G; ++p) rin.ro[p] = pr_in.off[p];
+      for (int p = 0; p < G; ++p) {
+        rin.rowbase[p] = pr_in.rowbase[p];
+        rin.src[p] = sh->peer_send[p];
+      }
     }
-    rc = apply_multi_delta(s, sh->plan, n, slots, xs.data(), ds.data(), st, d_bf16);
+    for (int i = 0; i < n; ++i) {
+      xs[i] = p2p ? sh->sendbuf : base + o_xr[x_of[i]];
+      xo[i] = p2p ? (long long)p_xo[x_of[i]] : 0;
+      ds[i] = p2p ? static_cast<char*>(sh->dbuf) + p_doff[i] : base + o_d[i];
+    }
+    rc = apply_multi_delta(s, sh->plan, n, slots, xs.data(), ds.data(), st, d_bf16, p2p ? &rin : nullptr,
+                           p2p ? xo.data() : nullptr);
     if (rc != LORA_OK) return rc;
+  }
+  if (p2p) {
+    // every owner's deltas complete before any source reads them
+    CKN(api.AllReduce(sh->d_bar, sh->d_bar, 1, ncclInt32, ncclSum, sh->comm, st));
+    if (n_send > 0) {
+      for (int i = 0; i < n; ++i) {
+        const int ho = s->slots[slots[i]].h_out;
+        const int pi = prof_start(s, st);
+        pull_scatter_add4_kernel<<<dim3((ho / 4 + 255) / 256, std::min(n_send, 65535)), 256, 0, st>>>(
+            y[i], y_dtype == LORA_FP32, pr_out, (long long)p_doff[i], d_bf16 ? 1 : 0, d_send_idx, n_send, ho);
+        prof_stop(s, pi, kKShardScatter, st);
+      }
+      CKS(cudaGetLastError());
+    }
+    CKS(cudaEventRecord(sh->ev[3], st));
+    if (s->debug_sync) CKS(cudaStreamSynchronize(st));
+    return LORA_OK;
   }
 
   // 6. (comm stream) return the deltas

@@ -214,9 +214,9 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         const uint16_t* abase = t.At + unit * (long long)t.h_in * R;
         const int n_st = t.h_in / t.SJ;
         const uint32_t a_bytes = (uint32_t)R * t.SJ * 2, x_bytes = (uint32_t)t.SJ * 2;
-        long long xrow[C::GR];
+        const uint16_t* xrow[C::GR];
 #pragma unroll
-        for (int r = 0; r < C::GR; ++r) xrow[r] = r < g.y ? (long long)pd.perm[g.x + r] * t.h_in : 0;
+        for (int r = 0; r < C::GR; ++r) xrow[r] = r < g.y ? x_row(args, t, pd.perm[g.x + r]) : t.x;
         for (int st = 0; st < n_st; ++st) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::S_STAGE;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
           const long long jofs = (long long)st * t.SJ;
 #pragma unroll
           for (int r = 0; r < C::GR; ++r)
-            if (r < g.y) bulk_g2s(sX + r * x_bytes, t.x + xrow[r] + jofs, x_bytes, &full[stage]);
+            if (r < g.y) bulk_g2s(sX + r * x_bytes, xrow[r] + jofs, x_bytes, &full[stage]);
           if (++stage == C::NST) {
             stage = 0;
             phase ^= 1;

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       for (int i = 0; i < 8; ++i) {
         const int n = (pt >> 3) + 16 * i;
         const bool valid = n < tile.y;
-        xsrc[i] = t.x + (valid ? (long long)pd.perm[tile.x + n] * t.h_in : 0) + (long long)kc * t.KI + (pt & 7) * 8;
+        xsrc[i] = (valid ? x_row(args, t, pd.perm[tile.x + n]) : t.x) + (long long)kc * t.KI + (pt & 7) * 8;
         xbytes[i] = valid ? 16u : 0u;
       }
       for (int st = 0; st < n_st; ++st) {

@@ -395,18 +395,22 @@ def test_small_rank_bf16_full_parity(B, rank):
         B.lora_server_destroy(s)
 
 
-@pytest.mark.parametrize("loopback,y_dtype,rank", [(False, "bf16", 64), (True, "fp32", 64), (True, "bf16", 64),
-                                                   (True, "bf16", 16)])
-def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank):
+@pytest.mark.parametrize("loopback,y_dtype,rank,transport", [
+    (False, "bf16", 64, "p2p"), (True, "fp32", 64, "p2p"), (True, "bf16", 64, "p2p"), (True, "bf16", 16, "p2p"),
+    (True, "fp32", 64, "nccl"), (True, "bf16", 64, "nccl")])
+def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
     """Sharded server at G = 1.  In place (no exchange): bit-identical to the
     unsharded server.  Loopback (LORA_SHARD_LOOPBACK=1 sends every row through
-    the NCCL exchange to itself, so one GPU runs the bucket / pack / send-recv
-    / owner delta apply / return / scatter-add path): fp32 y bit-identical to
-    the unsharded server (R18); bf16 y returns bf16 deltas (R19) and is held
-    to the oracle tolerance, every row checked."""
+    the exchange to itself, so one GPU runs the bucket / pack / transport /
+    owner delta apply / return / scatter-add path) with either transport:
+    p2p (registered buffers; the owner's shrink reads x rows from the source's
+    send buffer, the source pulls deltas fused with the add) or nccl (grouped
+    send/recv).  fp32 y: bit-identical to the unsharded server (R18); bf16 y
+    returns bf16 deltas (R19) and is held to the oracle tolerance, every row."""
     cfg = dataclasses.replace(_mid_cfg(rank=rank), y_dtype=y_dtype)
     if loopback:
         monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
+    monkeypatch.setenv("LORA_SHARD_TRANSPORT", transport)
     b = li.make_batch(cfg)
     s = U.make_server(B, cfg)
     T = b.n_rows
