@@ -233,6 +233,16 @@ lora_status_t lora_apply_sharded(lora_server_t *s, int32_t n, const int32_t *slo
 lora_status_t lora_shard_layout(const int64_t *counts, int32_t world, int32_t rank,
                                 int64_t *send_off, int64_t *recv_off);
 
+/* Host-only helper (no GPU needed) for the peer-to-peer transport: from the
+ * same count matrix, for every peer p:
+ *   in_rowbase[p]:  received row r (from source p, r in [recv_off[p],
+ *                   recv_off[p+1])) is row r + in_rowbase[p] of p's send
+ *                   buffer (p's rows ordered by owner);
+ *   out_rowbase[p]: this rank's send-order row j (for owner p) has its delta
+ *                   in row j + out_rowbase[p] of owner p's delta buffer. */
+lora_status_t lora_shard_peer_rows(const int64_t *counts, int32_t world, int32_t rank,
+                                   int64_t *in_rowbase, int64_t *out_rowbase);
+
 /* Synthetic activation rows for benchmarks and tests: dst is bf16 [rows][width]
  * (device), element (i, c) = the counter-based generator of DESIGN.md "Input
  * recipe" with major = row_base + i, minor = c, the given tag and shift.  Async. */

@@ -62,6 +62,7 @@ SIGNATURES = {
     "lora_nccl_unique_id": (ctypes.c_int, [_vp]),
     "lora_server_create_sharded": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _pp]),
     "lora_apply_sharded": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
+    "lora_shard_peer_rows": (ctypes.c_int, [_pi64, _i32, _i32, _pi64, _pi64]),
     "lora_shard_layout": (ctypes.c_int, [_pi64, _i32, _i32, _pi64, _pi64]),
     "lora_synth_fill_rows": (ctypes.c_int, [_vp, _i64, _i32, _u64, _u32, _i32, _i64, _vp]),
     "lora_profile_enable": (ctypes.c_int, [_vp, _i32]),
@@ -245,6 +246,15 @@ def lora_shard_layout(counts, world: int, rank: int):
     ro = (ctypes.c_int64 * (world + 1))()
     _check(lib.lora_shard_layout(c, world, rank, so, ro))
     return list(so), list(ro)
+
+
+def lora_shard_peer_rows(counts, world: int, rank: int):
+    """counts: flat world*world ints (src-major). Returns (in_rowbase, out_rowbase) per peer."""
+    c = (ctypes.c_int64 * (world * world))(*[int(v) for v in counts])
+    rin = (ctypes.c_int64 * world)()
+    rout = (ctypes.c_int64 * world)()
+    _check(lib.lora_shard_peer_rows(c, world, rank, rin, rout))
+    return list(rin), list(rout)
 
 
 def lora_synth_fill_rows(dst, rows: int, width: int, seed: int, tag: int, shift: int, row_base: int = 0,

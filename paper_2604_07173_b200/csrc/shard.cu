@@ -341,6 +341,23 @@ extern "C" lora_status_t lora_shard_layout(const int64_t* counts, int32_t world,
   return LORA_OK;
 }
 
+extern "C" lora_status_t lora_shard_peer_rows(const int64_t* counts, int32_t world, int32_t rank, int64_t* in_rowbase,
+                                              int64_t* out_rowbase) {
+  if (!counts || !in_rowbase || !out_rowbase || world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_shard_peer_rows: bad argument");
+  std::vector<int64_t> so(world + 1), ro(world + 1);
+  lora_status_t st = lora_shard_layout(counts, world, rank, so.data(), ro.data());
+  if (st != LORA_OK) return st;
+  for (int p = 0; p < world; ++p) {
+    int64_t before_me_in_p = 0, before_me_at_p = 0;
+    for (int q = 0; q < rank; ++q) before_me_in_p += counts[(size_t)p * world + q];  // p's rows for owners < rank
+    for (int q = 0; q < rank; ++q) before_me_at_p += counts[(size_t)q * world + p];  // owner p's rows from sources < rank
+    in_rowbase[p] = before_me_in_p - ro[p];
+    out_rowbase[p] = before_me_at_p - so[p];
+  }
+  return LORA_OK;
+}
+
 extern "C" lora_status_t lora_nccl_unique_id(void* out128) {
   if (!out128) return fail(nullptr, LORA_ERR_INVALID_ARG, "NULL out");
   NcclApi& api = nccl();
@@ -585,7 +602,7 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   for (int v : cnt) exchange = exchange || v > 0;
 
   // peer-to-peer transport: registered buffer layout (identical on every rank)
-  size_t p_ids = 0, p_need_send = 0, p_need_d = 0;
+  size_t p_need_send = 0, p_need_d = 0;
   std::vector<size_t> p_xo(xd.size()), p_doff(n);
   p_need_send = al(sizeof(int32_t) * 2 * s->max_rows);
   for (size_t j = 0; j < xd.size(); ++j) {
@@ -609,17 +626,15 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
       pr_in.off[p] = (int)ro[p];
       pr_out.off[p] = (int)so[p];
     }
+    std::vector<int64_t> rb_in(G), rb_out(G);
+    lora_shard_peer_rows(c64.data(), G, me, rb_in.data(), rb_out.data());
     for (int p = 0; p < G; ++p) {
-      int before_me_in_p = 0, before_me_at_p = 0;
-      for (int q = 0; q < me; ++q) before_me_in_p += cnt[p * G + q];  // p's rows for owners < me
-      for (int q = 0; q < me; ++q) before_me_at_p += cnt[q * G + p];  // rows owner p receives from sources < me
-      pr_in.rowbase[p] = before_me_in_p - (int)ro[p];
+      pr_in.rowbase[p] = (int)rb_in[p];
       pr_in.base[p] = sh->peer_send[p];
-      pr_out.rowbase[p] = before_me_at_p - (int)so[p];
+      pr_out.rowbase[p] = (int)rb_out[p];
       pr_out.base[p] = sh->peer_d[p];
     }
   }
-  (void)p_ids;
 
   // 3. (comm stream) pack + dispatch, overlapped with the in-place apply
   if (exchange) {

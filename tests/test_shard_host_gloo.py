@@ -134,3 +134,62 @@ def test_sharded_host_logic_world2_gloo(tmp_path, n_hot):
     # and the oracle's single rounding of (y + delta), within the north-star tolerance
     y_ref = orc.apply_slot(cfg, 0, batch)
     assert np.abs(y_sharded - y_ref).max() <= 1e-2 * np.abs(y_ref).max() + 1e-3
+
+
+def _p2p_worker(rank, world, port, out_dir, n_hot):
+    """The P2P transport's address maps (lora_shard_peer_rows, used by
+    shard.cu) on emulated peer memory: every rank's send buffer (global row
+    ids in send order) and delta buffer (global row ids in receive order) are
+    all-gathered; reading them through the row maps must give the oracle's
+    receive order on the owner side and each source's own rows back."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_07173_b200 import build
+        build.build()
+        from paper_2604_07173_b200 import binding as B
+        from oracle import oracle as orc
+
+        cfg = _cfg()
+        batch = li.make_batch(cfg)
+        k, G = batch.top_k, world
+        t0, t1 = orc.token_range(cfg.n_tokens, G, rank)
+        rows = np.arange(t0 * k, t1 * k)
+        a = batch.adapter_ids[rows]
+        own = orc.owner_of(a, G, n_hot, np.full(a.shape, rank))
+        send_rows = np.concatenate([rows[own == d] for d in range(G) if d != rank] + [np.zeros(0, np.int64)])
+        counts = np.array([(own == d).sum() if d != rank else 0 for d in range(G)], np.int64)
+        allc = [torch.zeros(G, dtype=torch.int64) for _ in range(G)]
+        dist.all_gather(allc, torch.from_numpy(counts))
+        mat = torch.stack(allc).numpy().reshape(-1)
+        so, ro = B.lora_shard_layout(mat.tolist(), G, rank)
+        rb_in, rb_out = B.lora_shard_peer_rows(mat.tolist(), G, rank)
+        cap = cfg.n_tokens * k
+
+        def gather_padded(v):
+            buf = torch.full((cap,), -7, dtype=torch.int64)
+            buf[:len(v)] = torch.from_numpy(np.asarray(v, np.int64))
+            out = [torch.zeros(cap, dtype=torch.int64) for _ in range(G)]
+            dist.all_gather(out, buf)
+            return [o.numpy() for o in out]
+
+        peer_send = gather_padded(send_rows)
+        # owner: received row r from source s is row r + rb_in[s] of s's send buffer
+        recv = np.array([peer_send[s][r + rb_in[s]] for s in range(G) for r in range(ro[s], ro[s + 1])], np.int64)
+        disp = orc.shard_dispatch(batch, G, n_hot)[rank]
+        np.testing.assert_array_equal(recv, disp["rows"])
+        # owner's delta buffer holds its received rows in receive order
+        peer_d = gather_padded(recv)
+        back = np.array([peer_d[p][j + rb_out[p]] for p in range(G) for j in range(so[p], so[p + 1])], np.int64)
+        np.testing.assert_array_equal(back, send_rows)
+        np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([len(recv), len(back)]))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_hot", [(2, 0), (3, 0), (3, 2)])
+def test_p2p_row_maps_gloo(tmp_path, world, n_hot):
+    mp.spawn(_p2p_worker, args=(world, _free_port(), str(tmp_path), n_hot), nprocs=world, join=True)
+    tot = sum(int(np.load(tmp_path / f"ok{r}.npy")[0]) for r in range(world))
+    assert tot > 0  # rows actually crossed ranks
