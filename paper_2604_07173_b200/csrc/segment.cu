@@ -86,13 +86,18 @@ LORA_DEVINL int cnt_get(const Cnt16& c, int d) {
   return (int)((w >> ((d & 3) * 16)) & 0xFFFFull);
 }
 
+// Composite buffers are padded with one word per 32 (index i lives at
+// i + i/32): thread t's contiguous run t*EPT.. then falls in 32 distinct banks
+// across a warp (EPT in 1..16), so the blocked-layout loads are conflict-free.
+LORA_DEVINL int pad32(int i) { return i + (i >> 5); }
+
 // one stable counting-sort pass on digit (v >> shift) & 15; blocked layout
 template <int EPT>
 __device__ void radix_pass(const uint32_t* in, uint32_t* out, int shift, unsigned long long* wtot, int* dbase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Cnt16 c = {{0, 0, 0, 0}};
 #pragma unroll 4
-  for (int r = 0; r < EPT; ++r) cnt_add(c, (in[tid * EPT + r] >> shift) & 15);
+  for (int r = 0; r < EPT; ++r) cnt_add(c, (in[pad32(tid * EPT + r)] >> shift) & 15);
   Cnt16 inc = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -138,9 +143,9 @@ __device__ void radix_pass(const uint32_t* in, uint32_t* out, int shift, unsigne
   for (int w = 0; w < 4; ++w) pre.w[w] = wtot[warp * 4 + w] + inc.w[w];
 #pragma unroll 4
   for (int r = 0; r < EPT; ++r) {
-    const uint32_t v = in[tid * EPT + r];
+    const uint32_t v = in[pad32(tid * EPT + r)];
     const int d = (v >> shift) & 15;
-    out[dbase[d] + cnt_get(pre, d)] = v;
+    out[pad32(dbase[d] + cnt_get(pre, d))] = v;
     cnt_add(pre, d);
   }
   __syncthreads();
@@ -160,7 +165,7 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
     int key = -1;
     if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad);
     nv += key >= 0;
-    A[i] = ((uint32_t)(key >= 0 ? key : K) << ib) | (uint32_t)i;
+    A[pad32(i)] = ((uint32_t)(key >= 0 ? key : K) << ib) | (uint32_t)i;
   }
   if (bad) atomicOr(err_flag, 1);
   int total;
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   int* segoff_s;  // [P+1] segment offsets in shared memory
   if constexpr (radix) {
     uint32_t* A = reinterpret_cast<uint32_t*>(seg_smem);
-    uint32_t* B = A + P + 4;  // each buffer P+4 ints: the free one later holds P+1 segment offsets
+    uint32_t* B = A + pad32(P) + 4;  // each buffer pad32(P)+4 ints: the free one later holds P+1 segment offsets
     const int K = n_adapters * E;
     uint32_t* res = nullptr;
     switch (EPT) {
@@ -303,11 +308,11 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   const int n_valid = s_nvalid;
   const uint32_t idx_mask = (1u << ib) - 1u;
   auto key_at = [&](int j) -> int {
-    if constexpr (radix) return (int)(srt32[j] >> ib);
+    if constexpr (radix) return (int)(srt32[pad32(j)] >> ib);
     else return (int)(srt64[j] >> 32);
   };
   auto row_at = [&](int j) -> int {
-    if constexpr (radix) return (int)(srt32[j] & idx_mask);
+    if constexpr (radix) return (int)(srt32[pad32(j)] & idx_mask);
     else return (int)(srt64[j] & 0xffffffffu);
   };
 
@@ -398,7 +403,7 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
   const int kb = bits_for((long long)n_adapters * E);  // key K = n_adapters*E marks "no LoRA" (sorts last)
   const int radix = (ib + kb <= 32) ? 1 : 0;
   // radix: two u32 buffers (+1 int for the last segment offset); bitonic: u64 buffer + P+1 ints
-  const int smem = radix ? (2 * P + 8) * 4 : P * 8 + (P + 1) * 4;
+  const int smem = radix ? (2 * (P + P / 32) + 8) * 4 : P * 8 + (P + 1) * 4;
   static unsigned long long attr_set = 0;  // per-device bitmask
   int dev = 0;
   cudaGetDevice(&dev);
