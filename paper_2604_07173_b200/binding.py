@@ -72,6 +72,10 @@ SIGNATURES = {
 }
 N_KERNEL_KINDS = 9
 for _name, (_res, _args) in SIGNATURES.items():
+    # LORA_BINDING_LENIENT=1: tolerate symbols an older build lacks (A/B timing of
+    # library versions with tools/ab_run.sh only; the tests require every symbol)
+    if os.environ.get("LORA_BINDING_LENIENT") == "1" and not hasattr(lib, _name):
+        continue
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args

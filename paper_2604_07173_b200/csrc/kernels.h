@@ -75,7 +75,6 @@ struct SlotTask {
   int KI, SJ, n_kc;    // shrink: j-range per item, j per stage, items per row group
   int CI, SC, n_ci;    // expand: c-range per item, c rows per stage, items per row group
   int kc_base, ci_base;// prefix over tasks of n_kc / n_ci
-  long long x_off;     // RemoteIn mode: byte offset of this slot's x rows in a source's send buffer
 };
 
 // Owner side of a peer-to-peer sharded apply (shard.cu): received row r is
@@ -96,21 +95,25 @@ struct MultiArgs {
   int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const float* scale;      // [n_adapters] s_a
-  RemoteIn rin;            // x rows read from peers (sharded P2P owner), G = 0 otherwise
   SlotTask t[kMaxTasks];
   // task of each global shrink chunk (kc) / expand column range (ci) index,
   // filled by the host when total_kc / total_ci <= kTaskTable
   uint8_t kc_task[kTaskTable];
   uint8_t ci_task[kTaskTable];
+  RemoteIn rin;                // x rows read from peers (sharded P2P owner), G = 0 otherwise
+  long long x_off[kMaxTasks];  // RemoteIn mode: byte offset of each task's x rows in a source's send buffer
 };
 
 #ifdef __CUDACC__
-// address of x row `row` of task t (local, or in a source's send buffer)
-__device__ __forceinline__ const uint16_t* x_row(const MultiArgs& a, const SlotTask& t, int row) {
-  if (a.rin.G == 0) return t.x + (long long)row * t.h_in;
+// address of x row `row` of task t (local, or -- REMOTE -- in a source's send
+// buffer); REMOTE is a compile-time kernel variant so the local path is unchanged
+template <bool REMOTE>
+__device__ __forceinline__ const uint16_t* x_row(const MultiArgs& a, int task, int row) {
+  const SlotTask& t = a.t[task];
+  if (!REMOTE) return t.x + (long long)row * t.h_in;
   int s = 0;
   while (s + 1 < a.rin.G && a.rin.ro[s + 1] <= row) ++s;
-  return reinterpret_cast<const uint16_t*>(a.rin.src[s] + t.x_off) + (long long)(row + a.rin.rowbase[s]) * t.h_in;
+  return reinterpret_cast<const uint16_t*>(a.rin.src[s] + a.x_off[task]) + (long long)(row + a.rin.rowbase[s]) * t.h_in;
 }
 // task owning global expand column-range index g (ci_base prefix)
 __device__ __forceinline__ int find_task_ci(const MultiArgs& a, int g) {

@@ -468,7 +468,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       t.At = si.At;
       t.Bt = si.Bt;
       t.x = static_cast<const uint16_t*>(x[b0 + i]);
-      t.x_off = x_off ? x_off[b0 + i] : 0;
+      args.x_off[i] = x_off ? x_off[b0 + i] : 0;
       t.y = y[b0 + i];
       t.vpart_off = (long long)si.kc_prefix * p->max_rows * s->r;
       t.vbf_off = (long long)slots[b0 + i] * p->max_rows * s->r;
@@ -502,6 +502,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       int kc2 = 0, ci2 = 0;
       for (int i = 0; i < nb; ++i) {
         sargs.t[i] = args.t[order[i]];
+        sargs.x_off[i] = args.x_off[order[i]];
         sargs.t[i].kc_base = kc2;
         sargs.t[i].ci_base = ci2;
         kc2 += sargs.t[i].n_kc;

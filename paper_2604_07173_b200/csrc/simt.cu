@@ -172,7 +172,7 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
   }
 }
 
-template <int R>
+template <int R, bool REMOTE>
 __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
     simt_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   using C = SimtCfg<R>;
@@ -214,9 +214,16 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         const uint16_t* abase = t.At + unit * (long long)t.h_in * R;
         const int n_st = t.h_in / t.SJ;
         const uint32_t a_bytes = (uint32_t)R * t.SJ * 2, x_bytes = (uint32_t)t.SJ * 2;
-        const uint16_t* xrow[C::GR];
+        // x row r of the group: t.x + xrow[r] (REMOTE: xrow[r] is relative to t.x,
+        // pointing into a source's send buffer)
+        long long xrow[C::GR];
 #pragma unroll
-        for (int r = 0; r < C::GR; ++r) xrow[r] = r < g.y ? x_row(args, t, pd.perm[g.x + r]) : t.x;
+        for (int r = 0; r < C::GR; ++r) {
+          if constexpr (REMOTE)
+            xrow[r] = r < g.y ? x_row<true>(args, ti, pd.perm[g.x + r]) - t.x : 0;
+          else
+            xrow[r] = r < g.y ? (long long)pd.perm[g.x + r] * t.h_in : 0;
+        }
         for (int st = 0; st < n_st; ++st) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::S_STAGE;
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
           const long long jofs = (long long)st * t.SJ;
 #pragma unroll
           for (int r = 0; r < C::GR; ++r)
-            if (r < g.y) bulk_g2s(sX + r * x_bytes, xrow[r] + jofs, x_bytes, &full[stage]);
+            if (r < g.y) bulk_g2s(sX + r * x_bytes, t.x + xrow[r] + jofs, x_bytes, &full[stage]);
           if (++stage == C::NST) {
             stage = 0;
             phase ^= 1;
@@ -718,10 +725,12 @@ cudaError_t set_smem_once(K kernel, int bytes, unsigned long long& mask) {
 template <int R>
 cudaError_t launch_shrink_t(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   using C = SimtCfg<R>;
-  static unsigned long long mask = 0;
-  cudaError_t e = set_smem_once(simt_shrink_kernel<R>, C::SHRINK_SMEM, mask);
+  static unsigned long long mask[2] = {0, 0};
+  const bool remote = args.rin.G > 0;
+  auto kern = remote ? simt_shrink_kernel<R, true> : simt_shrink_kernel<R, false>;
+  cudaError_t e = set_smem_once(kern, C::SHRINK_SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
-  simt_shrink_kernel<R><<<2 * grid, C::THREADS, C::SHRINK_SMEM, stream>>>(args, pd);
+  kern<<<2 * grid, C::THREADS, C::SHRINK_SMEM, stream>>>(args, pd);
   return cudaGetLastError();
 }
 

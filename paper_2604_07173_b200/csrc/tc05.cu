@@ -126,6 +126,7 @@ struct ShrinkCfg {
   static constexpr int SMEM = 1024 + NST * STAGE + 256;
 };
 
+template <bool REMOTE>
 __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
     tc_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   using C = ShrinkCfg;
@@ -181,7 +182,8 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       }
       if (it < 0) break;
       const int kcg = (int)(it / n_tiles), ti = (int)(it - (long long)kcg * n_tiles);
-      const SlotTask& t = args.t[find_task_kc(args, kcg)];
+      const int task = find_task_kc(args, kcg);
+      const SlotTask& t = args.t[task];
       const int kc = kcg - t.kc_base;
       const int4 tile = pd.tiles[ti];
       const long long unit = unit_of_key(tile.z, t.E, args.pl);
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       for (int i = 0; i < 8; ++i) {
         const int n = (pt >> 3) + 16 * i;
         const bool valid = n < tile.y;
-        xsrc[i] = (valid ? x_row(args, t, pd.perm[tile.x + n]) : t.x) + (long long)kc * t.KI + (pt & 7) * 8;
+        xsrc[i] = (valid ? x_row<REMOTE>(args, task, pd.perm[tile.x + n]) : t.x) + (long long)kc * t.KI + (pt & 7) * 8;
         xbytes[i] = valid ? 16u : 0u;
       }
       for (int st = 0; st < n_st; ++st) {
@@ -369,6 +371,12 @@ LORA_DEVINL void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 }
 LORA_DEVINL void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+LORA_DEVINL void tmem_ld8_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
 LORA_DEVINL void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -586,22 +594,25 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS + cb * 32;
         const long long o = o0 + (long long)sb * C::MSUB;
         if constexpr (M == 0 || M == 2) {
-          // two halves of 16 columns: ya[] becomes the output in place
+          // four quarters of 8 columns into a separate output w[]: a pending
+          // store locks its source registers, so the y buffers stay free for
+          // the next loads
+          uint32_t w[16];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t d[16];
-            tmem_ld16_nowait(ta + h * 16, d);
+          for (int h = 0; h < 4; ++h) {
+            uint32_t d[8];
+            tmem_ld8_nowait(ta + h * 8, d);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 4; ++i) {
               const float e0 = s_a * __uint_as_float(d[2 * i]), e1 = s_a * __uint_as_float(d[2 * i + 1]);
-              const uint32_t yv = ya[h * 8 + i];
-              ya[h * 8 + i] = yload ? pack_bf16x2_rn(bf16lo(yv) + e0, bf16hi(yv) + e1) : pack_bf16x2_rn(e0, e1);
+              const uint32_t yv = ya[h * 4 + i];
+              w[h * 4 + i] = yload ? pack_bf16x2_rn(bf16lo(yv) + e0, bf16hi(yv) + e1) : pack_bf16x2_rn(e0, e1);
             }
           }
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
-          if (live) stg256x2(yb + o, ya);
+          if (live) stg256x2(yb + o, w);
         } else {
           // fp32 y (accumulate) or fp32 delta store (sharded): 2 halves x 4 x 16 bytes
           float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + o);
@@ -667,10 +678,12 @@ cudaError_t set_smem_once(K kernel, int bytes, unsigned long long& mask) {
 bool tc_available() { return true; }
 
 cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
-  static unsigned long long mask = 0;
-  cudaError_t e = set_smem_once(tc_shrink_kernel, ShrinkCfg::SMEM, mask);
+  static unsigned long long mask[2] = {0, 0};
+  const bool remote = args.rin.G > 0;
+  auto kern = remote ? tc_shrink_kernel<true> : tc_shrink_kernel<false>;
+  cudaError_t e = set_smem_once(kern, ShrinkCfg::SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
-  tc_shrink_kernel<<<grid, ShrinkCfg::THREADS, ShrinkCfg::SMEM, stream>>>(args, pd);
+  kern<<<grid, ShrinkCfg::THREADS, ShrinkCfg::SMEM, stream>>>(args, pd);
   return cudaGetLastError();
 }
 
