@@ -424,12 +424,17 @@ struct ExpandCfg {
   static constexpr int THREADS = 18 * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (N)
   static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
-  static constexpr int NST = 6;
+  static constexpr int NST = 4;
   static constexpr int V_TILE = kTileRows * 128;       // 16 KB (M = 128 rows x 64 bf16)
+  // bf16 output: y tiles [128 rows][128 cols] (16-byte chunks XOR-swizzled by
+  // row) in a ring of YS slots, fetched YD-1 sub-tiles ahead
+  static constexpr int YD = 3;
+  static constexpr int YS = YD + 1;
+  static constexpr int Y_TILE = kTileRows * MSUB * 2;  // 32 KB
   static constexpr int NACC = 4;
   static constexpr int ACC_COLS = MSUB;                // N columns per accumulator
   static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 512
-  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + 512;
+  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + YS * Y_TILE + 512;
 };
 
 // output mode M (compile time): 0 bf16 accumulate, 1 fp32 delta store, 2 bf16
@@ -441,7 +446,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE] swizzled MMA operand A
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vtile + 2 * C::V_TILE);
+  uint8_t* yring = vtile + 2 * C::V_TILE;      // [YS][Y_TILE] bf16 y tiles (bf16 output modes)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(yring + C::YS * C::Y_TILE);
   uint64_t* full = bars;                       // [NST] Bt landed
   uint64_t* empty = bars + C::NST;             // [NST] MMA done with Bt stage
   uint64_t* vfull = bars + 2 * C::NST;         // [2]  v tile landed
@@ -558,6 +564,95 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       }
     }
   } else {
+    if constexpr (M == 0 || M == 2) {
+    // ===================== epilogue, bf16 output: coalesced y tiles =====================
+    // Per sub-tile the 128 x 128 y tile is fetched with coalesced cp.async
+    // (16 chunks of 16 bytes per row; YD-1 sub-tiles ahead) into a smem ring;
+    // thread (row, 32 columns) adds s_a * D from TMEM in place; the tile
+    // leaves with coalesced 16-byte stores.  Two named barriers per sub-tile
+    // over the 512 epilogue threads; the ring has one spare slot, so the
+    // slot refilled at sub-tile sb was stored out two sub-tiles ago.
+    const int q = warp & 3, cb = warp >> 2;
+    const int et = threadIdx.x;                  // 0 .. EPI_THREADS-1
+    const int n = q * 32 + lane;                 // this thread's tile row (TMEM lane)
+    const int cc = et & 15;                      // chunk column of this thread's copies
+    const uint32_t ybase = smem_u32(yring);
+    long long k = 0;                             // global sub-tile counter (same as the MMA warp's)
+    int kk = 0;                                  // this CTA's sub-tile sequence number (ring slot)
+    QueuePos qp;
+    for (;;) {
+      const long long it = wq_pop(wq, qp);
+      if (it < 0) break;
+      const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
+      const SlotTask& t = args.t[find_task_ci(args, cig)];
+      const int ci = cig - t.ci_base;
+      const int4 tile = pd.tiles[ti];
+      const float s_a = args.scale[tile.z / t.E];
+      const int n_sub = t.CI / C::MSUB;
+      uint16_t* yb = static_cast<uint16_t*>(t.y);
+      // this thread's copy rows: r_j = et / 16 + 32 j
+      long long coff[4];
+      bool cval[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = (et >> 4) + 32 * j;
+        cval[j] = r < tile.y;
+        coff[j] = (cval[j] ? (long long)__ldg(pd.perm + tile.x + r) * t.h_out : 0) + (long long)ci * t.CI + cc * 8;
+      }
+      auto slot_of = [&](int seq) { return ybase + (uint32_t)(seq % C::YS) * C::Y_TILE; };
+      auto chunk_addr = [&](uint32_t sl, int r, int c) { return sl + r * (C::MSUB * 2) + ((c ^ (r & 15)) << 4); };
+      auto issue2 = [&](int sb) {
+        if (M == 0 && sb < n_sub) {
+          const uint32_t sl = slot_of(kk + sb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (cval[j]) cp_async16_u32(chunk_addr(sl, (et >> 4) + 32 * j, cc), yb + coff[j] + (long long)sb * C::MSUB);
+        }
+        cp_async_commit();
+      };
+#pragma unroll 1
+      for (int j = 0; j < C::YD - 1; ++j) issue2(j);
+      for (int sb = 0; sb < n_sub; ++sb, ++k) {
+        issue2(sb + C::YD - 1);
+        const uint32_t sl = slot_of(kk + sb);
+        const int acc = (int)(k % C::NACC);
+        mbar_wait(&tfull[acc], (uint32_t)((k / C::NACC) & 1));
+        tc_fence_after();
+        if (M == 0) cp_async_wait<C::YD - 1>();
+        named_bar_sync(1, C::EPI_THREADS);  // tile sb complete and visible
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS + cb * 32;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          uint32_t d[8];
+          tmem_ld8_nowait(ta + h * 8, d);
+          const uint32_t a = chunk_addr(sl, n, cb * 4 + h);
+          uint4 yv = make_uint4(0, 0, 0, 0);
+          if (M == 0) yv = lds128(a);
+          tmem_wait_ld();
+          const uint32_t y4[4] = {yv.x, yv.y, yv.z, yv.w};
+          uint32_t w4[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float e0 = s_a * __uint_as_float(d[2 * i]), e1 = s_a * __uint_as_float(d[2 * i + 1]);
+            w4[i] = M == 0 ? pack_bf16x2_rn(bf16lo(y4[i]) + e0, bf16hi(y4[i]) + e1) : pack_bf16x2_rn(e0, e1);
+          }
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(w4[0]), "r"(w4[1]), "r"(w4[2]),
+                       "r"(w4[3])
+                       : "memory");
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        named_bar_sync(1, C::EPI_THREADS);  // results in the tile
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (cval[j])
+            *reinterpret_cast<uint4*>(yb + coff[j] + (long long)sb * C::MSUB) =
+                lds128(chunk_addr(sl, (et >> 4) + 32 * j, cc));
+      }
+      cp_async_wait<0>();
+      kk += n_sub;
+    }
+    } else {
     // ===================== epilogue: one row x 32 columns per thread =====================
     // y moves in full 32-byte sectors (256-bit LDG/STG); the segments of the
     // next two sub-tiles of the item are in flight while one is in the
@@ -650,6 +745,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         step(sb + 1, b1, b0);
         step(sb + 2, b2, b1);
       }
+    }
     }
   }
   tc_fence_before();
