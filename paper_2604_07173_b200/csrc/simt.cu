@@ -42,15 +42,18 @@ struct SimtCfg {
   static constexpr int THREADS = NCT + 32;
   static constexpr int GR = kGroupRows;  // rows per group
   static constexpr int SMEM_BUDGET = 110 * 1024;  // per CTA, two CTAs per SM
-  // shrink
-  static constexpr int KL = R < 32 ? R : 32;  // lanes along k
-  static constexpr int KPL = R / KL;          // k per lane
-  static constexpr int NJG = NCT / KL;        // j-groups
-  static constexpr int SJ_MAX = 8192 / R;     // 16 KB of A per stage
+  // shrink.  r = 64: 32 lanes along k, 2 k per lane.  r <= 32: 4 k per lane
+  // (an x element widened once feeds 4 products; two k share an FFMA2), the
+  // j-groups of a warp pre-reduced with shuffles (SMALL_K).
+  static constexpr bool SMALL_K = R <= 32;
+  static constexpr int KL = SMALL_K ? R / 4 : 32;  // lanes along k
+  static constexpr int KPL = R / KL;               // k per lane
+  static constexpr int NJG = NCT / KL;             // j-groups
+  static constexpr int SJ_MAX = 8192 / R;          // 16 KB of A per stage
   static constexpr int A_STAGE = R * SJ_MAX * 2;
   static constexpr int X_STAGE = GR * SJ_MAX * 2;
   static constexpr int S_STAGE = A_STAGE + X_STAGE;
-  static constexpr int RED_BYTES = NJG * GR * R * 4;
+  static constexpr int RED_BYTES = (SMALL_K ? NWC : NJG) * GR * R * 4;
   static constexpr int NST_RAW = (SMEM_BUDGET - RED_BYTES) / S_STAGE;
   static constexpr int NST = NST_RAW > 8 ? 8 : (NST_RAW < 2 ? 2 : NST_RAW);
   static constexpr int SHRINK_SMEM = 1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8;
@@ -172,6 +175,114 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
   }
 }
 
+// r <= 32: thread (kl, jg) accumulates k = 4 kl .. 4 kl + 3 for NR rows over
+// its j-chunks; acc[r][p] = (k0, k1) of pair p.  Lanes of a warp holding the
+// same k are reduced with xor shuffles, then the warps through shared memory.
+template <int R, int NR>
+LORA_DEVINL void shrink_item_small(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
+                                   uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane) {
+  using C = SimtCfg<R>;
+  static_assert(C::KPL == 4, "four k per lane");
+  const int ct = threadIdx.x, warp = ct >> 5;
+  const int kl = ct % C::KL, jg = ct / C::KL;
+  const int n_st = t.h_in / t.SJ;
+  const int nchunk = t.SJ >> 3;
+  float2 acc[NR][2];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+
+  for (int st = 0; st < n_st; ++st) {
+    mbar_wait(&full[stage], phase);
+    const uint32_t a_s = smem_u32(smem + stage * C::S_STAGE);
+    const uint32_t x_s = a_s + C::A_STAGE;
+    for (int c = jg; c < nchunk; c += C::NJG) {
+      const int tile = c >> 3, q = c & 7;
+      // A[j][k] of chunk c (8 j) for this lane's 4 k (raw), widened per half of
+      // 4 j as k pairs; x read per half (8 bytes = 4 j per row)
+      uint4 u[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = kl * 4 + kk;
+        u[kk] = lds128(a_s + tile * (R * 128) + k * 128 + ((q ^ (k & 7)) << 4));
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float2 w[4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const uint32_t a0 = h ? (i ? u[0].w : u[0].z) : (i ? u[0].y : u[0].x);
+          const uint32_t a1 = h ? (i ? u[1].w : u[1].z) : (i ? u[1].y : u[1].x);
+          const uint32_t a2 = h ? (i ? u[2].w : u[2].z) : (i ? u[2].y : u[2].x);
+          const uint32_t a3 = h ? (i ? u[3].w : u[3].z) : (i ? u[3].y : u[3].x);
+          w[2 * i][0] = make_float2(bf16lo(a0), bf16lo(a1));
+          w[2 * i][1] = make_float2(bf16lo(a2), bf16lo(a3));
+          w[2 * i + 1][0] = make_float2(bf16hi(a0), bf16hi(a1));
+          w[2 * i + 1][1] = make_float2(bf16hi(a2), bf16hi(a3));
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          uint32_t x0, x1;
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(x_s + r * (t.SJ * 2) + (c << 4) + h * 8));
+          const float xf[4] = {bf16lo(x0), bf16hi(x0), bf16lo(x1), bf16hi(x1)};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[r][0] = __ffma2_rn(make_float2(xf[j], xf[j]), w[j][0], acc[r][0]);
+            acc[r][1] = __ffma2_rn(make_float2(xf[j], xf[j]), w[j][1], acc[r][1]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == C::NST) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+
+  // lanes kl + KL * m (m = 0 .. 32/KL-1) hold the same k: xor-reduce over m
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      float2 v = acc[r][p];
+#pragma unroll
+      for (int o = C::KL; o < 32; o <<= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+      }
+      acc[r][p] = v;
+    }
+  named_bar_sync(1, C::NCT);
+  if (lane < C::KL) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        float* d = red + (warp * NR + r) * R + kl * 4 + 2 * p;
+        d[0] = acc[r][p].x;
+        d[1] = acc[r][p].y;
+      }
+  }
+  named_bar_sync(1, C::NCT);
+  float* vp = vpart_base + (long long)g.x * R;
+  for (int idx = ct; idx < NR * R; idx += C::NCT) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < C::NWC; ++w) s += red[w * NR * R + idx];
+    vp[idx] = s;
+  }
+}
+
+template <int R, int NR>
+LORA_DEVINL void shrink_dispatch(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
+                                 uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane) {
+  if constexpr (SimtCfg<R>::SMALL_K)
+    shrink_item_small<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane);
+  else
+    shrink_item<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane);
+}
+
 template <int R, bool REMOTE>
 __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
     simt_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
@@ -254,14 +365,14 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       const int4 g = pd.groups[gi];
       float* vb = pd.vpart + t.vpart_off;
       switch (g.y) {
-        case 1: shrink_item<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 2: shrink_item<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 3: shrink_item<R, 3>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 4: shrink_item<R, 4>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 5: shrink_item<R, 5>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 6: shrink_item<R, 6>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 7: shrink_item<R, 7>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        default: shrink_item<R, 8>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 1: shrink_dispatch<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 2: shrink_dispatch<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 3: shrink_dispatch<R, 3>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 4: shrink_dispatch<R, 4>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 5: shrink_dispatch<R, 5>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 6: shrink_dispatch<R, 6>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 7: shrink_dispatch<R, 7>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        default: shrink_dispatch<R, 8>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
       }
     }
   }
