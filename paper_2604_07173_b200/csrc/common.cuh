@@ -5,6 +5,8 @@
 // nothing with this file.
 #pragma once
 
+#include <utility>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -149,9 +151,31 @@ LORA_DEVINL void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Programmatic dependent launch
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while its predecessor on the stream is still running; pdl_wait() blocks
+// until that predecessor grid has completed (its writes visible), and
+// pdl_launch_dependents() lets the next PDL kernel be scheduled.  Both are
+// no-ops for kernels launched normally.
 LORA_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 LORA_DEVINL void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// host: launch with programmatic stream serialization when LORA_PDL=1 (else a plain launch)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // 128-bit loads
 LORA_DEVINL uint4 lds128(uint32_t addr) {

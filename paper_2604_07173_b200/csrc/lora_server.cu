@@ -200,6 +200,17 @@ lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int ran
 }
 
 // delta mode for the sharded owner: d[i] receives s*(xA)B (stored, not added) as fp32 or bf16
+namespace lora {
+// Programmatic dependent launch of the shrink / expand / v-reduce kernels
+// (prologues and the expand's first weight copies overlapping the previous
+// kernel's tail).  Measured neutral to slightly negative on one B200 (early
+// CTAs of the other chain compete for SMs), so opt-in: LORA_PDL=1.
+bool pdl_enabled() {
+  static const bool on = env_flag("LORA_PDL");
+  return on;
+}
+}  // namespace lora
+
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
                                 void* const* d, cudaStream_t st, bool bf16, const RemoteIn* rin,
                                 const long long* x_off) {

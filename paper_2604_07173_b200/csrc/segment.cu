@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
                    int E, int n_adapters, int kb, int ib, SegParams sp, PlanDev pd,
                    int* __restrict__ err_flag) {
   extern __shared__ __align__(16) uint8_t seg_smem[];
+  pdl_launch_dependents();  // the shrink kernels may launch now; they wait for this grid
   const Placement pl = sp.pl;
   __shared__ int scan_tmp[40];
   __shared__ unsigned long long wtot[32 * 4];

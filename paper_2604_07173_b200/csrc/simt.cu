@@ -303,6 +303,8 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();               // the plan (segmenter) is complete
+  pdl_launch_dependents();  // the expand may launch as SMs free up
 
   const int n_groups = pd.counts[kCntGroups];
   const long long n_items = (long long)n_groups * args.n_tasks;
@@ -593,6 +595,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       uint32_t phase = 0;
       QueuePos qp;
       unsigned long long* ctr = pd.wctr + kWqSimtExpand;
+      bool shrink_done = false;
       for (;;) {
         long long it = (long long)atomicAdd(ctr, 1ull);
         if (it >= n_items) it = -1;
@@ -618,6 +621,10 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
           uint8_t* sb = smem + stage * C::E_STAGE;
           mbar_arrive_expect_tx(&full[stage], bytes + vbytes);
           bulk_g2s_hint(sb, bbase + (long long)st * t.SC * R, bytes, &full[stage], pol);
+          if (!shrink_done) {
+            pdl_wait();  // v rows come from the shrink (the B rows above do not)
+            shrink_done = true;
+          }
           bulk_g2s(sb + C::B_STAGE, vsrc, vbytes, &full[stage]);
           if (++stage == C::NSTE) {
             stage = 0;
@@ -841,7 +848,8 @@ cudaError_t launch_shrink_t(const MultiArgs& args, const PlanDev& pd, int grid, 
   auto kern = remote ? simt_shrink_kernel<R, true> : simt_shrink_kernel<R, false>;
   cudaError_t e = set_smem_once(kern, C::SHRINK_SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
-  kern<<<2 * grid, C::THREADS, C::SHRINK_SMEM, stream>>>(args, pd);
+  e = launch_pdl(kern, dim3(2 * grid), dim3(C::THREADS), C::SHRINK_SMEM, stream, args, pd);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -851,7 +859,8 @@ cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, 
   static unsigned long long mask = 0;
   cudaError_t e = set_smem_once(simt_expand_kernel<R>, C::EXPAND_SMEM, mask);
   if (e != cudaSuccess) return e;
-  simt_expand_kernel<R><<<2 * grid, C::THREADS, C::EXPAND_SMEM, stream>>>(args, pd);
+  e = launch_pdl(simt_expand_kernel<R>, dim3(2 * grid), dim3(C::THREADS), C::EXPAND_SMEM, stream, args, pd);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  pdl_wait();               // the plan (segmenter) is complete
+  pdl_launch_dependents();  // the v reduction may launch
   const int n_tiles = pd.counts[kCntTiles];
   const long long n_items = (long long)n_tiles * args.total_kc;
 
@@ -331,6 +333,8 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
 // q ^ (n & 7)), so the expand loads its MMA operand with one bulk copy.
 // ===========================================================================
 __global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
+  pdl_wait();               // the tcgen05 shrink's partials are complete
+  pdl_launch_dependents();
   const int n_tiles = pd.counts[kCntTiles];
   const long long per_task = (long long)n_tiles * kTileRows * (R / 8);
   const long long total = per_task * args.n_tasks;
@@ -491,6 +495,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const uint64_t pol = policy_evict_first();
       int stage = 0, vb = 0;
       uint32_t phase = 0, vphase = 0;
+      bool vready = false;
       QueuePos qp;
       for (;;) {
         const long long it = wq_push_next(wq, qp, pd.wctr + kWqTcExpand, n_items);
@@ -500,6 +505,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         const int ci = cig - t.ci_base;
         const int4 tile = pd.tiles[ti];
         mbar_wait(&vempty[vb], vphase ^ 1);
+        if (!vready) {
+          pdl_wait();  // the v tiles come from the v reduction (the Bt rows do not)
+          vready = true;
+        }
         mbar_arrive_expect_tx(&vfull[vb], (uint32_t)tile.y * 128);
         bulk_g2s(vtile + vb * C::V_TILE, pd.vbf + t.vbf_off + (long long)tile.x * R, (uint32_t)tile.y * 128,
                  &vfull[vb]);
@@ -779,12 +788,14 @@ cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid,
   auto kern = remote ? tc_shrink_kernel<true> : tc_shrink_kernel<false>;
   cudaError_t e = set_smem_once(kern, ShrinkCfg::SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
-  kern<<<grid, ShrinkCfg::THREADS, ShrinkCfg::SMEM, stream>>>(args, pd);
+  e = launch_pdl(kern, dim3(grid), dim3(ShrinkCfg::THREADS), ShrinkCfg::SMEM, stream, args, pd);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
-  tc_vreduce_kernel<<<grid * 4, 256, 0, stream>>>(args, pd);
+  cudaError_t e = launch_pdl(tc_vreduce_kernel, dim3(grid * 4), dim3(256), 0, stream, args, pd);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -795,7 +806,8 @@ cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid,
                                                                                      : tc_expand_kernel<3>;
   cudaError_t e = set_smem_once(kern, ExpandCfg::SMEM, mask[m]);
   if (e != cudaSuccess) return e;
-  kern<<<grid, ExpandCfg::THREADS, ExpandCfg::SMEM, stream>>>(args, pd);
+  e = launch_pdl(kern, dim3(grid), dim3(ExpandCfg::THREADS), ExpandCfg::SMEM, stream, args, pd);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
