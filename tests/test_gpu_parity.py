@@ -267,6 +267,38 @@ def test_mixtral_sharded_config_at_g1_sampled(B):
         B.lora_server_destroy(s)
 
 
+@pytest.mark.slow
+def test_mixtral_sharded_config_p2p_loopback_sampled(B, monkeypatch):
+    """Config 5 at full size through the sharded server's peer-to-peer path
+    (loopback: every row goes through the registered send buffer, the owner's
+    shrink reads it remotely, the deltas come back through the pull-scatter)."""
+    monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
+    monkeypatch.setenv("LORA_SHARD_TRANSPORT", "p2p")
+    cfg = li.CONFIGS["mixtral_sharded"]
+    b = li.make_batch(cfg)
+    T = b.n_rows
+    c = B.make_config([sl.h_in for sl in cfg.slots], [sl.h_out for sl in cfg.slots],
+                      [sl.n_experts for sl in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), T, 0)
+    sh = B.lora_server_create_sharded(c, 0, 1, B.lora_nccl_unique_id())
+    try:
+        B.lora_server_fill_synthetic(sh, cfg.seed)
+        ad, ex = U.ids_dev(b)
+        xs = {}
+        for i, sl in enumerate(cfg.slots):
+            if sl.xbuf not in xs:
+                xs[sl.xbuf] = U.x_dev(B, cfg, i, T)
+        ys = [U.y0_dev(B, cfg, i, T) for i in range(3)]
+        B.lora_apply_sharded(sh, [0, 1, 2], [xs[sl.xbuf] for sl in cfg.slots], ad, ex, ys, B.LORA_BF16, T)
+        torch.cuda.synchronize()
+        assert B.lora_server_check(sh) == B.LORA_OK
+        rows = U.sample_rows(b, 24, E=cfg.n_experts)
+        for i in range(3):
+            ref = oracle.apply_slot(cfg, i, b, rows=rows)
+            U.assert_parity(ys[i][torch.from_numpy(rows).to(U.DEV)], ref, f"p2p loopback slot {i}")
+    finally:
+        B.lora_server_destroy(sh)
+
+
 # ---------------------------------------------------------------------------
 # invariants and API equivalences (bit-exact)
 # ---------------------------------------------------------------------------
