@@ -184,11 +184,13 @@ lora_status_t lora_apply(lora_server_t *s, int32_t slot, const void *x, const in
 
 /* End-to-end entry with HOST buffers (pinned for full async speed): copies
  * the ids and the n slots' x / y host->device into library staging buffers,
- * builds the internal plan, applies, and copies every y back device->host,
- * all on `stream`, with the per-slot copies overlapped with compute on an
- * internal copy stream.  Returns after enqueueing; the caller synchronises
- * `stream` before reading y.  Capacity: T <= max_rows.  x[i] pointers may
- * repeat (the copy is made once). */
+ * builds the internal plan once, applies, and copies every y back
+ * device->host.  Pipelined: the slots are cut into chunks (about 1/8 of the
+ * upload each, >= 32 MB); chunk c+1's upload (internal copy stream), chunk c's
+ * apply (`stream`) and chunk c-1's download (a second internal stream) run
+ * concurrently.  Stream-ordered on `stream` at both ends; returns after
+ * enqueueing, the caller synchronises `stream` before reading y.  Capacity:
+ * T <= max_rows.  x[i] pointers may repeat (uploaded once). */
 lora_status_t lora_apply_multi_host(lora_server_t *s, int32_t n, const int32_t *slots,
                                     const void *const *x_host, const int32_t *adapter_ids_host,
                                     const int32_t *expert_ids_host, void *const *y_host,

@@ -98,6 +98,7 @@ static void free_server(lora_server* s) {
   for (auto ev : s->events) cudaEventDestroy(ev);
   for (auto ev : s->prof_pool) cudaEventDestroy(ev);
   if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+  if (s->d2h_stream) cudaStreamDestroy(s->d2h_stream);
   if (s->side_stream) cudaStreamDestroy(s->side_stream);
   if (s->ev_fork) cudaEventDestroy(s->ev_fork);
   if (s->ev_join) cudaEventDestroy(s->ev_join);
@@ -678,7 +679,14 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
   CK(s, cudaSetDevice(s->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t ysz = y_dtype == LORA_FP32 ? 4 : 2;
-  // layout of the staging buffer: ids | distinct x | y per slot (256-byte aligned pieces)
+  // Pipelined executor.  The slots are cut into chunks of consecutive slots
+  // (~1/8 of the host->device bytes each, at least 32 MB); per chunk: its x
+  // buffers (first use) and y rows go host->device on the copy stream, the
+  // chunk is applied on the caller's stream with the one plan built from the
+  // ids, and its y rows go device->host on a third stream -- so chunk c+1's
+  // upload, chunk c's apply and chunk c-1's download overlap (the two copy
+  // directions use separate copy engines).  The caller's stream waits for
+  // the last download: the call stays stream-ordered on `stream`.
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   std::vector<const void*> xd;  // distinct x host pointers
   std::vector<int> x_of(n);
@@ -711,28 +719,84 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
     CK(s, cudaMalloc(&s->h2d_buf, off));
     s->h2d_bytes = off;
   }
+  if (!s->copy_stream) CK(s, cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+  if (!s->d2h_stream) CK(s, cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking));
+  // chunks: consecutive slots, cut when the chunk's upload reaches the target
+  std::vector<size_t> up_bytes(n);
+  std::vector<char> x_first(n, 0);
+  {
+    std::vector<char> seen(xd.size(), 0);
+    for (int i = 0; i < n; ++i) {
+      up_bytes[i] = (size_t)T * s->slots[slots[i]].h_out * ysz;
+      if (!seen[x_of[i]]) {
+        seen[x_of[i]] = 1;
+        x_first[i] = 1;
+        up_bytes[i] += (size_t)T * x_hin[x_of[i]] * 2;
+      }
+    }
+  }
+  size_t total = 0;
+  for (size_t b : up_bytes) total += b;
+  const size_t target = std::max<size_t>(total / 8, (size_t)32 << 20);
+  std::vector<int> cut{0};
+  for (int i = 0, acc = 0; i < n; ++i) {
+    acc += 1;
+    size_t sum = 0;
+    for (int j = cut.back(); j <= i; ++j) sum += up_bytes[j];
+    if (sum >= target || i == n - 1) cut.push_back(i + 1);
+  }
+  const int n_chunks = (int)cut.size() - 1;
+  while ((int)s->events.size() < 2 * n_chunks + 2) {
+    cudaEvent_t e;
+    CK(s, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->events.push_back(e);
+  }
+  cudaEvent_t ev_start = s->events[0], ev_ids = s->events[1];
   char* base = static_cast<char*>(s->h2d_buf);
   int32_t* d_ad = reinterpret_cast<int32_t*>(base);
   int32_t* d_ex = reinterpret_cast<int32_t*>(base + al((size_t)T * 4));
-  CK(s, cudaMemcpyAsync(d_ad, adapter_ids_host, (size_t)T * 4, cudaMemcpyHostToDevice, st));
-  if (expert_ids_host) CK(s, cudaMemcpyAsync(d_ex, expert_ids_host, (size_t)T * 4, cudaMemcpyHostToDevice, st));
-  for (size_t j = 0; j < xd.size(); ++j)
-    CK(s, cudaMemcpyAsync(base + x_off[j], xd[j], (size_t)T * x_hin[j] * 2, cudaMemcpyHostToDevice, st));
-  std::vector<const void*> xs(n);
-  std::vector<void*> ys(n);
-  for (int i = 0; i < n; ++i) {
-    CK(s, cudaMemcpyAsync(base + y_off[i], y_host[i], (size_t)T * s->slots[slots[i]].h_out * ysz,
-                          cudaMemcpyHostToDevice, st));
-    xs[i] = base + x_off[x_of[i]];
-    ys[i] = base + y_off[i];
-  }
+  // the copy streams start after whatever the caller queued on `stream`
+  CK(s, cudaEventRecord(ev_start, st));
+  CK(s, cudaStreamWaitEvent(s->copy_stream, ev_start, 0));
+  CK(s, cudaStreamWaitEvent(s->d2h_stream, ev_start, 0));
+  CK(s, cudaMemcpyAsync(d_ad, adapter_ids_host, (size_t)T * 4, cudaMemcpyHostToDevice, s->copy_stream));
+  if (expert_ids_host)
+    CK(s, cudaMemcpyAsync(d_ex, expert_ids_host, (size_t)T * 4, cudaMemcpyHostToDevice, s->copy_stream));
+  CK(s, cudaEventRecord(ev_ids, s->copy_stream));
+  CK(s, cudaStreamWaitEvent(st, ev_ids, 0));
   lora_status_t rc = plan_build_impl(s, s->internal_plan, d_ad, expert_ids_host ? d_ex : nullptr, T,
                                      s->slots[slots[0]].E, st);
   if (rc != LORA_OK) return rc;
-  rc = apply_multi_impl(s, s->internal_plan, n, slots, xs.data(), ys.data(), y_dtype, st);
-  if (rc != LORA_OK) return rc;
-  for (int i = 0; i < n; ++i)
-    CK(s, cudaMemcpyAsync(y_host[i], ys[i], (size_t)T * s->slots[slots[i]].h_out * ysz, cudaMemcpyDeviceToHost, st));
+  std::vector<const void*> xs(n);
+  std::vector<void*> ys(n);
+  for (int i = 0; i < n; ++i) {
+    xs[i] = base + x_off[x_of[i]];
+    ys[i] = base + y_off[i];
+  }
+  for (int c = 0; c < n_chunks; ++c) {
+    cudaEvent_t ev_in = s->events[2 + 2 * c], ev_done = s->events[3 + 2 * c];
+    for (int i = cut[c]; i < cut[c + 1]; ++i) {
+      if (x_first[i])
+        CK(s, cudaMemcpyAsync(base + x_off[x_of[i]], xd[x_of[i]], (size_t)T * x_hin[x_of[i]] * 2,
+                              cudaMemcpyHostToDevice, s->copy_stream));
+      CK(s, cudaMemcpyAsync(ys[i], y_host[i], (size_t)T * s->slots[slots[i]].h_out * ysz, cudaMemcpyHostToDevice,
+                            s->copy_stream));
+    }
+    CK(s, cudaEventRecord(ev_in, s->copy_stream));
+    CK(s, cudaStreamWaitEvent(st, ev_in, 0));
+    const int nc = cut[c + 1] - cut[c];
+    rc = apply_multi_impl(s, s->internal_plan, nc, slots + cut[c], xs.data() + cut[c], ys.data() + cut[c], y_dtype,
+                          st);
+    if (rc != LORA_OK) return rc;
+    CK(s, cudaEventRecord(ev_done, st));
+    CK(s, cudaStreamWaitEvent(s->d2h_stream, ev_done, 0));
+    for (int i = cut[c]; i < cut[c + 1]; ++i)
+      CK(s, cudaMemcpyAsync(y_host[i], ys[i], (size_t)T * s->slots[slots[i]].h_out * ysz, cudaMemcpyDeviceToHost,
+                            s->d2h_stream));
+  }
+  // join: the caller's stream completes after the last download
+  CK(s, cudaEventRecord(ev_start, s->d2h_stream));
+  CK(s, cudaStreamWaitEvent(st, ev_start, 0));
   return LORA_OK;
 }
 

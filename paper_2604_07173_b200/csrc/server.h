@@ -41,13 +41,14 @@ struct lora_server {
   // staging for lora_apply_multi_host (grown lazily)
   void* h2d_buf = nullptr;
   size_t h2d_bytes = 0;
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // lora_apply_multi_host: host -> device copies
+  cudaStream_t d2h_stream = nullptr;    // lora_apply_multi_host: device -> host copies
   // tcgen05 kernels run on a side stream forked from / joined to the caller's
   // stream, concurrently with the CUDA-core kernels (independent rows)
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool concurrent_tc = true;  // env LORA_SERIAL=1 keeps everything on the caller's stream
-  std::vector<cudaEvent_t> events;
+  std::vector<cudaEvent_t> events;      // lora_apply_multi_host pipeline events (grown on demand)
   ShardState* shard = nullptr;
   // per-launch CUDA-event profiling (lora_profile_enable / lora_profile_read)
   bool prof_on = false;
