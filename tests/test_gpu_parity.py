@@ -325,6 +325,37 @@ def test_determinism_and_multi_equals_single(B):
         B.lora_server_destroy(s)
 
 
+@pytest.mark.parametrize("case", ["single_row", "one_segment", "all_no_lora", "ragged_mixed"])
+def test_edge_cases(B, case):
+    """Degenerate batches: one row; one (adapter, expert) unit holding every
+    row (one segment -> tcgen05 tiles with a near-equal split); no row with a
+    LoRA (y untouched, bit-exact); an odd row count mixing -1 rows, every
+    element checked against the oracle."""
+    T = {"single_row": 1, "one_segment": 300, "all_no_lora": 64, "ragged_mixed": 257}[case]
+    cfg = dataclasses.replace(_mid_cfg(), top_k=1, n_tokens=T)
+    r = np.arange(T)
+    if case == "single_row":
+        a, e = np.array([3]), np.array([1])
+    elif case == "one_segment":
+        a, e = np.full(T, 7), np.full(T, 2)
+    elif case == "all_no_lora":
+        a, e = np.full(T, -1), np.zeros(T)
+    else:
+        a, e = (r % 3) - 1, r % 4
+    b = li.Batch(a.astype(np.int32), e.astype(np.int32), T, 1)
+    s = U.make_server(B, cfg)
+    try:
+        y0 = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        ys = _run_multi(B, s, cfg, b, [0, 1])
+        for i in range(2):
+            if case == "all_no_lora":
+                assert torch.equal(ys[i], y0[i])
+            else:
+                U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"{case} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
 def test_permutation_equivariance_bit_exact(B):
     cfg = _mid_cfg()
     b = li.make_batch(cfg)
