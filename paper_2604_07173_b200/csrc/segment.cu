@@ -8,14 +8,15 @@
 //
 // One CTA of 1024 threads, everything in shared memory (T <= 16384).
 //  * Fast path: 32-bit composites (key << ib) | row with an LSD radix sort on
-//    the key bits, 4 bits per pass.  Each pass is a stable block-wide counting
-//    sort: thread t owns a contiguous block of elements, per-digit counts are
-//    packed 16 x 16 bit into four 64-bit words and scanned with warp shuffles.
+//    the key bits, 8 bits per pass.  Each pass is a stable block-wide counting
+//    sort (warp-synchronous multisplit + a block scan over (digit, warp)).
 //    Rows enter in index order and every pass is stable, so ties keep the
 //    original row order -- bit-exact with the stable-sort definition.
 //  * Fallback (key bits + row bits > 32): 64-bit composites sorted with a
 //    bitonic network; composites are unique, so any correct sort of them is
 //    the stable sort by key.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -67,86 +68,71 @@ LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* 
 }
 
 // ---------------------------------------------------------------------------
-// radix path: 16 digit counters x 16 bit packed in four 64-bit words
+// radix path
 // ---------------------------------------------------------------------------
-struct Cnt16 {
-  unsigned long long w[4];
-};
-LORA_DEVINL void cnt_add(Cnt16& c, int d) {
-  const unsigned long long inc = 1ull << ((d & 3) * 16);
-  const int q = d >> 2;
-  c.w[0] += q == 0 ? inc : 0ull;
-  c.w[1] += q == 1 ? inc : 0ull;
-  c.w[2] += q == 2 ? inc : 0ull;
-  c.w[3] += q == 3 ? inc : 0ull;
-}
-LORA_DEVINL int cnt_get(const Cnt16& c, int d) {
-  const int q = d >> 2;
-  const unsigned long long w = q == 0 ? c.w[0] : q == 1 ? c.w[1] : q == 2 ? c.w[2] : c.w[3];
-  return (int)((w >> ((d & 3) * 16)) & 0xFFFFull);
-}
-
 // Composite buffers are padded with one word per 32 (index i lives at
 // i + i/32): thread t's contiguous run t*EPT.. then falls in 32 distinct banks
-// across a warp (EPT in 1..16), so the blocked-layout loads are conflict-free.
+// across a warp (EPT in 1..16), so the blocked-layout accesses are conflict-free.
 LORA_DEVINL int pad32(int i) { return i + (i >> 5); }
 
-// one stable counting-sort pass on digit (v >> shift) & 15; blocked layout
+// One stable counting-sort pass on an 8-bit digit (v >> shift) & 255 --
+// warp-synchronous multisplit.  Warp w owns the contiguous index range
+// [w*32*EPT, (w+1)*32*EPT) and walks it in rounds of 32 consecutive elements
+// (lane order = index order); lanes with equal digits find each other (peer
+// mask from 8 ballots; match.any's cost grows with the number of distinct
+// values) and take ranks in lane order on top of the warp's running count for
+// that digit.  A block scan over (digit, warp) in digit-major order then
+// gives every (warp, digit) its output base.  cnt: [32 warps][256] ints.
 template <int EPT>
-__device__ void radix_pass(const uint32_t* in, uint32_t* out, int shift, unsigned long long* wtot, int* dbase) {
+__device__ void radix_pass8(const uint32_t* in, uint32_t* out, int shift, int* cnt, int* scan_tmp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  Cnt16 c = {{0, 0, 0, 0}};
-#pragma unroll 4
-  for (int r = 0; r < EPT; ++r) cnt_add(c, (in[pad32(tid * EPT + r)] >> shift) & 15);
-  Cnt16 inc = c;
+  int* wc = cnt + warp * 256;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int q = 0; q < 8; ++q) wc[lane + 32 * q] = 0;
+  __syncwarp();
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t v[EPT];
+  int loc[EPT];
+  const int base_idx = warp * 32 * EPT;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const unsigned long long t = __shfl_up_sync(0xffffffffu, inc.w[w], o);
-      if (lane >= o) inc.w[w] += t;
-    }
-  }
-  if (lane == 31) {
-#pragma unroll
-    for (int w = 0; w < 4; ++w) wtot[warp * 4 + w] = inc.w[w];
-  }
-#pragma unroll
-  for (int w = 0; w < 4; ++w) inc.w[w] -= c.w[w];  // exclusive prefix within the warp (no borrow across fields)
-  __syncthreads();
-  if (warp == 0) {
-    Cnt16 own, x;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) own.w[w] = x.w[w] = wtot[lane * 4 + w];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, x.w[w], o);
-        if (lane >= o) x.w[w] += t;
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int w = 0; w < 4; ++w) wtot[lane * 4 + w] = x.w[w] - own.w[w];  // exclusive warp offsets
-    if (lane == 31) {
-      int base = 0;
-      for (int d = 0; d < 16; ++d) {
-        dbase[d] = base;
-        base += cnt_get(x, d);
-      }
-    }
-  }
-  __syncthreads();
-  Cnt16 pre;
-#pragma unroll
-  for (int w = 0; w < 4; ++w) pre.w[w] = wtot[warp * 4 + w] + inc.w[w];
-#pragma unroll 4
   for (int r = 0; r < EPT; ++r) {
-    const uint32_t v = in[pad32(tid * EPT + r)];
-    const int d = (v >> shift) & 15;
-    out[pad32(dbase[d] + cnt_get(pre, d))] = v;
-    cnt_add(pre, d);
+    v[r] = in[pad32(base_idx + r * 32 + lane)];
+    const int d = (v[r] >> shift) & 255;
+    // lanes with the same digit: AND over the 8 digit bits of (ballot or its complement)
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint32_t m = __ballot_sync(0xffffffffu, (d >> b) & 1);
+      peers &= ((d >> b) & 1) ? m : ~m;
+    }
+    const int before = wc[d];
+    loc[r] = before + __popc(peers & lt);
+    __syncwarp();
+    if ((peers & lt) == 0) wc[d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive scan over (digit, warp), digit-major: thread t sums digit t/4, warps 8(t%4) .. +8
+  const int d0 = tid >> 2, w0 = (tid & 3) * 8;
+  int c[8], sum = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    c[q] = cnt[(w0 + q) * 256 + d0];
+    sum += c[q];
+  }
+  int total;
+  int run = block_exclusive_scan(sum, scan_tmp, &total);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    cnt[(w0 + q) * 256 + d0] = run;
+    run += c[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int d = (v[r] >> shift) & 255;
+    out[pad32(wc[d] + loc[r])] = v[r];
   }
   __syncthreads();
 }
@@ -155,8 +141,8 @@ __device__ void radix_pass(const uint32_t* in, uint32_t* out, int shift, unsigne
 template <int EPT>
 __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids,
                                 int T, int E, int n_adapters, const Placement& pl, int K, int kb, int ib,
-                                uint32_t* A, uint32_t* B, unsigned long long* wtot, int* dbase, int* err_flag,
-                                int* n_valid_out, int* scan_tmp) {
+                                uint32_t* A, uint32_t* B, int* cnt, int* err_flag, int* n_valid_out,
+                                int* scan_tmp) {
   const int tid = threadIdx.x;
   int bad = 0, nv = 0;
 #pragma unroll
@@ -173,8 +159,8 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
   *n_valid_out = total;
   uint32_t* in = A;
   uint32_t* out = B;
-  for (int sh = 0; sh < kb; sh += 4) {
-    radix_pass<EPT>(in, out, ib + sh, wtot, dbase);
+  for (int sh = 0; sh < kb; sh += 8) {
+    radix_pass8<EPT>(in, out, ib + sh, cnt, scan_tmp);
     uint32_t* t = in;
     in = out;
     out = t;
@@ -269,8 +255,6 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   pdl_launch_dependents();  // the shrink kernels may launch now; they wait for this grid
   const Placement pl = sp.pl;
   __shared__ int scan_tmp[40];
-  __shared__ unsigned long long wtot[32 * 4];
-  __shared__ int dbase[16];
   __shared__ int s_nvalid;
   const int tid = threadIdx.x;
   const int EPT = P / kSegThreads;
@@ -282,14 +266,15 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   if constexpr (radix) {
     uint32_t* A = reinterpret_cast<uint32_t*>(seg_smem);
     uint32_t* B = A + pad32(P) + 4;  // each buffer pad32(P)+4 ints: the free one later holds P+1 segment offsets
+    int* cnt = reinterpret_cast<int*>(B + pad32(P) + 4);  // [32 warps][256] digit counts
     const int K = n_adapters * E;
     uint32_t* res = nullptr;
     switch (EPT) {
-      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
-      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, wtot, dbase, err_flag, &s_nvalid, scan_tmp); break;
+      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
     }
     srt32 = res;
     segoff_s = reinterpret_cast<int*>(res == A ? B : A);  // the free buffer (P + 1 ints reserved)
@@ -404,12 +389,13 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
   const int kb = bits_for((long long)n_adapters * E);  // key K = n_adapters*E marks "no LoRA" (sorts last)
   const int radix = (ib + kb <= 32) ? 1 : 0;
   // radix: two u32 buffers (+1 int for the last segment offset); bitonic: u64 buffer + P+1 ints
-  const int smem = radix ? (2 * (P + P / 32) + 8) * 4 : P * 8 + (P + 1) * 4;
+  const int smem = radix ? (2 * (P + P / 32) + 8 + 32 * 256) * 4 : P * 8 + (P + 1) * 4;
   static unsigned long long attr_set = 0;  // per-device bitmask
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set & (1ull << dev))) {
-    const int mx = kMaxPlanRows * 8 + (kMaxPlanRows + 1) * 4;
+    const int mx = std::max((2 * (kMaxPlanRows + kMaxPlanRows / 32) + 8 + 32 * 256) * 4,
+                            kMaxPlanRows * 8 + (kMaxPlanRows + 1) * 4);
     cudaError_t e = cudaFuncSetAttribute(segment_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(segment_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
