@@ -17,7 +17,9 @@ Pins (tests/test_oracle_pins.py): float64 dense brute force W + s*A*B and its
 PEFT transpose, exact-integer probes against numpy int64 matmul, rank-1 outer
 products, a hand-worked golden example (tests/golden/), a = -1 zero delta,
 permutation equivariance, linearity in s, and for ``segment`` a pure-Python
-sorted()+groupby brute force plus hand-written golden cases.
+sorted()+groupby brute force plus hand-written golden cases; ``owner_of`` /
+``shard_dispatch`` against a per-row brute force of the routing rule and its
+partition / count-matrix invariants.
 """
 from __future__ import annotations
 
