@@ -74,6 +74,12 @@ typedef struct {
                                 every rank (popularity-aware placement for skewed traffic,
                                 P:291; adapter ids are assumed ordered by popularity); 0 =
                                 plain striping.  Ignored by lora_server_create. */
+  int32_t n_resident;        /* single-GPU servers: 0 => every adapter resident in device memory;
+                                0 < n_resident < n_adapters => resident-adapter cache (P:519-531,
+                                Sec. 5.3): all adapters live in pinned host memory in the kernel
+                                layout, n_resident of them in device memory; lora_server_require
+                                makes a batch's adapters resident (LRU eviction, per-slot async
+                                host->device copies that the applies of each slot wait for). */
 } lora_config_t;
 
 /* ------------------------------------------------------------------------- */
@@ -112,6 +118,20 @@ lora_status_t lora_server_destroy(lora_server_t *s);
  * rank 64; other ranks always use the CUDA-core path.  Takes effect at the
  * next lora_plan_build. */
 lora_status_t lora_server_set_small_seg_max(lora_server_t *s, int32_t n);
+
+/* Resident-adapter cache (cfg->n_resident > 0): make the n adapters in
+ * `adapters` (host ids, duplicates allowed, at most n_resident distinct)
+ * resident before the next applies.  Missing adapters take free cache slots
+ * or evict the least recently required adapters not in this set; their
+ * weights are copied host->device on an internal copy stream, slot by slot
+ * (layer-wise), after the work already queued on `stream`; every later apply
+ * of a slot on `stream` waits only for that slot's copies, so loading the
+ * next layers overlaps applying the first.  *n_loaded (may be NULL) receives
+ * the number of adapters copied.  Rows whose adapter is not resident at plan
+ * build are treated as out of range (skipped and flagged).  Without a cache:
+ * no-op.  Single stream per server. */
+lora_status_t lora_server_require(lora_server_t *s, const int32_t *adapters, int32_t n, int32_t *n_loaded,
+                                  void *stream);
 
 /* on != 0 (default; env LORA_SERIAL=1 at create sets 0): the tcgen05 chain of
  * an apply runs on an internal side stream forked from / joined to the

@@ -32,7 +32,7 @@ class LoraConfig(ctypes.Structure):
                 ("h_out", ctypes.POINTER(ctypes.c_int32)), ("n_experts", ctypes.POINTER(ctypes.c_int32)),
                 ("rank", ctypes.c_int32), ("n_adapters", ctypes.c_int32),
                 ("scale", ctypes.POINTER(ctypes.c_float)), ("max_rows", ctypes.c_int32),
-                ("device", ctypes.c_int32), ("n_replicated", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("n_replicated", ctypes.c_int32), ("n_resident", ctypes.c_int32)]
 
 
 _vp, _i32, _i64, _u64, _u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32
@@ -48,6 +48,7 @@ SIGNATURES = {
     "lora_server_destroy": (ctypes.c_int, [_vp]),
     "lora_server_set_small_seg_max": (ctypes.c_int, [_vp, _i32]),
     "lora_server_set_concurrent": (ctypes.c_int, [_vp, _i32]),
+    "lora_server_require": (ctypes.c_int, [_vp, _pi32, _i32, _pi32, _vp]),
     "lora_server_check": (ctypes.c_int, [_vp, _vp]),
     "lora_last_error": (ctypes.c_char_p, [_vp]),
     "lora_plan_create": (ctypes.c_int, [_vp, _i32, _pp]),
@@ -121,13 +122,13 @@ def _ptr_array(items):
 
 
 def make_config(h_in: Sequence[int], h_out: Sequence[int], n_experts: Sequence[int], rank: int, n_adapters: int,
-                scale=None, max_rows: int = 4096, device: int = 0, n_replicated: int = 0):
+                scale=None, max_rows: int = 4096, device: int = 0, n_replicated: int = 0, n_resident: int = 0):
     n = len(h_in)
     keep = {"h_in": (ctypes.c_int32 * n)(*h_in), "h_out": (ctypes.c_int32 * n)(*h_out),
             "E": (ctypes.c_int32 * n)(*n_experts)}
     keep["scale"] = (ctypes.c_float * n_adapters)(*[float(v) for v in scale]) if scale is not None else None
     cfg = LoraConfig(n, keep["h_in"], keep["h_out"], keep["E"], rank, n_adapters,
-                     keep["scale"] if keep["scale"] is not None else None, max_rows, device, n_replicated)
+                     keep["scale"] if keep["scale"] is not None else None, max_rows, device, n_replicated, n_resident)
     cfg._keep = keep  # keep the arrays alive
     return cfg
 
@@ -157,6 +158,15 @@ def lora_server_destroy(s: int):
 
 def lora_server_set_small_seg_max(s: int, n: int):
     _check(lib.lora_server_set_small_seg_max(s, n), s)
+
+
+def lora_server_require(s: int, adapters, stream=None) -> int:
+    """Make the adapters (host ids) resident; returns how many were copied in."""
+    import numpy as _np
+    a = _np.ascontiguousarray(_np.asarray(adapters, dtype=_np.int32))
+    out = ctypes.c_int32(0)
+    _check(lib.lora_server_require(s, a.ctypes.data_as(_pi32), int(a.size), ctypes.byref(out), _stream(stream)), s)
+    return int(out.value)
 
 
 def lora_server_set_concurrent(s: int, on: bool):

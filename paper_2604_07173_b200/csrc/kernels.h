@@ -61,7 +61,20 @@ struct SegParams {
   int tc_enabled;  // rank 64 and not forced off
   int tile_rows;
   Placement pl;    // rows whose adapter this rank does not store are rejected (flagged)
+  const int32_t* cache;  // resident-cache mode: [n_adapters] cache slot or -1 (not resident: rejected)
 };
+
+// key a*E+e -> unit index in the device store: the adapter's resident cache
+// slot (cache mode) or its local index under the placement
+__host__ __device__ inline long long store_unit(int key, int E, const Placement& pl, const int32_t* cache) {
+  const int a = key / E, e = key - a * E;
+#ifdef __CUDA_ARCH__
+  if (cache) return (long long)__ldg(cache + a) * E + e;
+#else
+  if (cache) return (long long)cache[a] * E + e;
+#endif
+  return pl.local_index(a) * E + e;
+}
 
 // One slot inside a (multi-slot) launch.
 struct SlotTask {
@@ -94,6 +107,7 @@ struct MultiArgs {
   int y_fp32;
   int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
+  const int32_t* cache;    // resident-cache mode: unit = cache[a]*E + e (nullptr: placement)
   const float* scale;      // [n_adapters] s_a
   SlotTask t[kMaxTasks];
   // task of each global shrink chunk (kc) / expand column range (ci) index,
@@ -150,7 +164,7 @@ bool tc_available();
 // synthetic fill / weight relayout (synth_fill.cu)
 cudaError_t launch_fill_store(uint16_t* At, uint16_t* Bt, int h_in, int h_out, int E, int r, long long units,
                               int slot, unsigned long long seed, const Placement& pl, int n_adapters,
-                              cudaStream_t stream);
+                              cudaStream_t stream, long long adapter_base = 0);
 cudaError_t launch_fill_rows(uint16_t* dst, long long rows, int width, unsigned long long seed, unsigned tag,
                              int shift, long long row_base, cudaStream_t stream);
 cudaError_t launch_relayout_A(const uint16_t* src, uint16_t* At, long long units, int h_in, int r,

@@ -95,6 +95,10 @@ static void free_server(lora_server* s) {
   cudaFree(s->d_scale);
   cudaFree(s->d_err);
   cudaFree(s->h2d_buf);
+  for (auto p : s->hostA) cudaFreeHost(p);
+  for (auto p : s->hostB) cudaFreeHost(p);
+  cudaFree(s->d_cache);
+  for (auto ev : s->slot_ready) cudaEventDestroy(ev);
   for (auto ev : s->events) cudaEventDestroy(ev);
   for (auto ev : s->prof_pool) cudaEventDestroy(ev);
   if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
@@ -130,6 +134,9 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   s->shard_rank = rank;
   s->n_hot = world > 1 ? std::max(0, std::min(n_hot, cfg->n_adapters)) : 0;
   s->n_adapters_local = placement(s).n_local(cfg->n_adapters);
+  if (world == 1 && cfg->n_resident > 0 && cfg->n_resident < cfg->n_adapters) s->n_resident = cfg->n_resident;
+  // device store: every local adapter, or the cache slots
+  const int store_adapters = s->n_resident ? s->n_resident : s->n_adapters_local;
   s->max_rows = cfg->max_rows;
   s->debug_sync = env_flag("LORA_DEBUG_SYNC");
   if (const char* e = std::getenv("LORA_SMALL_SEG_MAX")) s->small_seg_max = std::atoi(e);
@@ -149,7 +156,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
     sl.h_in = cfg->h_in[i];
     sl.h_out = cfg->h_out[i];
     sl.E = cfg->n_experts[i];
-    sl.units = (long long)s->n_adapters_local * sl.E;
+    sl.units = (long long)store_adapters * sl.E;
     // shrink items of ~128 KB of A, expand items of ~128 KB of B
     sl.KI = best_divisor(sl.h_in, 64, std::max(64, 65536 / r));
     sl.SJ = best_divisor(sl.KI, 64, simt_sj_max(r));
@@ -182,6 +189,41 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   }
   cudaMemcpy(s->d_scale, sc.data(), sizeof(float) * cfg->n_adapters, cudaMemcpyHostToDevice);
   cudaMemset(s->d_err, 0, sizeof(int));
+  if (s->n_resident) {
+    // pinned host backing store in the kernel layout, cache table (all absent)
+    for (int i = 0; i < cfg->n_slots; ++i) {
+      const SlotInfo& sl = s->slots[i];
+      uint16_t* ha = nullptr;
+      uint16_t* hb = nullptr;
+      const size_t na = (size_t)cfg->n_adapters * sl.E * sl.h_in * r, nb = (size_t)cfg->n_adapters * sl.E * sl.h_out * r;
+      if (cudaMallocHost(&ha, na * 2) != cudaSuccess || cudaMallocHost(&hb, nb * 2) != cudaSuccess) {
+        cudaGetLastError();
+        if (ha) cudaFreeHost(ha);
+        free_server(s);
+        return fail(nullptr, LORA_ERR_OOM, "pinned host backing store allocation failed");
+      }
+      std::memset(ha, 0, na * 2);
+      std::memset(hb, 0, nb * 2);
+      s->hostA.push_back(ha);
+      s->hostB.push_back(hb);
+      cudaEvent_t ev;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        free_server(s);
+        return fail(nullptr, LORA_ERR_CUDA, "event creation failed");
+      }
+      s->slot_ready.push_back(ev);
+    }
+    s->slot_pending.assign(cfg->n_slots, 0);
+    s->h_cache.assign(cfg->n_adapters, -1);
+    s->cache_owner.assign(s->n_resident, -1);
+    s->cache_use.assign(s->n_resident, 0);
+    if (cudaMalloc(&s->d_cache, sizeof(int32_t) * cfg->n_adapters) != cudaSuccess ||
+        cudaMemcpy(s->d_cache, s->h_cache.data(), sizeof(int32_t) * cfg->n_adapters, cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+      free_server(s);
+      return fail(nullptr, LORA_ERR_OOM, "cache table allocation failed");
+    }
+  }
   lora_status_t ps = plan_create_impl(s, cfg->max_rows, &s->internal_plan);
   if (ps != LORA_OK) {
     std::string m = s->last_error;
@@ -218,6 +260,8 @@ lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const
   return apply_multi_impl(s, p, n, slots, x, d, bf16 ? LORA_BF16 : LORA_FP32, st, bf16 ? 2 : 1, rin, x_off);
 }
 
+static lora_status_t cache_reset(lora_server* s);
+
 static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, const void* A, const void* B,
                                int on_device, cudaStream_t st) {
   SlotInfo& sl = s->slots[slot];
@@ -232,7 +276,8 @@ static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, con
     const int a = a_begin + i;
     const Placement pl = placement(s);
     if (!pl.owns(a)) continue;  // not stored on this rank
-    const long long lu = pl.local_index(a) * sl.E;
+    // cache mode: relayout in cache slot 0's area, then into the host backing store
+    const long long lu = s->n_resident ? 0 : pl.local_index(a) * sl.E;
     for (int pass = 0; pass < 2; ++pass) {
       const void* src = pass == 0 ? A : B;
       if (!src) continue;
@@ -243,11 +288,16 @@ static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, con
       if (e == cudaSuccess)
         e = pass == 0 ? launch_relayout_A(stage, sl.At + lu * a_unit, sl.E, sl.h_in, r, st)
                       : launch_relayout_B(stage, sl.Bt + lu * b_unit, sl.E, sl.h_out, r, st);
+      if (e == cudaSuccess && s->n_resident) {
+        uint16_t* host = pass == 0 ? s->hostA[slot] + (size_t)a * sl.E * a_unit : s->hostB[slot] + (size_t)a * sl.E * b_unit;
+        e = cudaMemcpyAsync(host, pass == 0 ? sl.At : sl.Bt, (size_t)sl.E * ue * 2, cudaMemcpyDeviceToHost, st);
+      }
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) rc = cuda_fail(s, e, "lora_server_load");
     }
   }
   cudaFree(stage);
+  if (rc == LORA_OK && s->n_resident) rc = cache_reset(s);
   return rc;
 }
 
@@ -286,11 +336,108 @@ extern "C" lora_status_t lora_server_fill_synthetic(lora_server_t* s, uint64_t s
   if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
   CK(s, cudaSetDevice(s->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s->n_resident) {
+    // generate n_resident adapters at a time in the device cache area, copy them
+    // to the host backing store; the cache is empty afterwards
+    CK(s, cudaStreamSynchronize(st));
+    for (size_t i = 0; i < s->slots.size(); ++i) {
+      SlotInfo& sl = s->slots[i];
+      const size_t ua = (size_t)sl.E * sl.h_in * s->r, ub = (size_t)sl.E * sl.h_out * s->r;  // per adapter
+      for (int a0 = 0; a0 < s->n_adapters; a0 += s->n_resident) {
+        const int na = std::min(s->n_resident, s->n_adapters - a0);
+        CK(s, launch_fill_store(sl.At, sl.Bt, sl.h_in, sl.h_out, sl.E, s->r, (long long)na * sl.E, (int)i, seed,
+                                Placement{1, 0, 0}, s->n_adapters, st, a0));
+        CK(s, cudaMemcpyAsync(s->hostA[i] + (size_t)a0 * ua, sl.At, (size_t)na * ua * 2, cudaMemcpyDeviceToHost, st));
+        CK(s, cudaMemcpyAsync(s->hostB[i] + (size_t)a0 * ub, sl.Bt, (size_t)na * ub * 2, cudaMemcpyDeviceToHost, st));
+      }
+    }
+    CK(s, cudaStreamSynchronize(st));
+    return cache_reset(s);
+  }
   for (size_t i = 0; i < s->slots.size(); ++i) {
     SlotInfo& sl = s->slots[i];
     CK(s, launch_fill_store(sl.At, sl.Bt, sl.h_in, sl.h_out, sl.E, s->r, sl.units, (int)i, seed, placement(s),
                             s->n_adapters, st));
   }
+  return LORA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// resident-adapter cache (cfg->n_resident > 0; P:519-531 layer-wise loading)
+// ---------------------------------------------------------------------------
+static lora_status_t cache_reset(lora_server* s) {
+  std::fill(s->h_cache.begin(), s->h_cache.end(), -1);
+  std::fill(s->cache_owner.begin(), s->cache_owner.end(), -1);
+  std::fill(s->cache_use.begin(), s->cache_use.end(), 0);
+  CK(s, cudaMemcpy(s->d_cache, s->h_cache.data(), sizeof(int32_t) * s->n_adapters, cudaMemcpyHostToDevice));
+  return LORA_OK;
+}
+
+extern "C" lora_status_t lora_server_require(lora_server_t* s, const int32_t* adapters, int32_t n, int32_t* n_loaded,
+                                             void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (n_loaded) *n_loaded = 0;
+  if (!s->n_resident || n <= 0) return LORA_OK;
+  if (!adapters) return fail(s, LORA_ERR_INVALID_ARG, "adapters is NULL");
+  std::vector<int> need;
+  for (int i = 0; i < n; ++i) {
+    const int a = adapters[i];
+    if (a < 0) continue;  // no LoRA
+    if (a >= s->n_adapters) return fail(s, LORA_ERR_INVALID_ARG, "adapter id out of range");
+    need.push_back(a);
+  }
+  std::sort(need.begin(), need.end());
+  need.erase(std::unique(need.begin(), need.end()), need.end());
+  if ((int)need.size() > s->n_resident)
+    return fail(s, LORA_ERR_UNSUPPORTED, "more distinct adapters than resident cache slots");
+  CK(s, cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long tick = ++s->cache_tick;
+  std::vector<std::pair<int, int>> loads;  // (adapter, cache slot)
+  for (int a : need)
+    if (s->h_cache[a] >= 0) s->cache_use[s->h_cache[a]] = tick;
+  for (int a : need) {
+    if (s->h_cache[a] >= 0) continue;
+    int victim = -1;
+    for (int c = 0; c < s->n_resident; ++c) {  // an empty slot, else the least recently required
+      if (s->cache_owner[c] < 0) {
+        victim = c;
+        break;
+      }
+      if (s->cache_use[c] < tick && (victim < 0 || s->cache_use[c] < s->cache_use[victim])) victim = c;
+    }
+    if (victim < 0) return fail(s, LORA_ERR_UNSUPPORTED, "no evictable cache slot");
+    if (s->cache_owner[victim] >= 0) s->h_cache[s->cache_owner[victim]] = -1;
+    s->cache_owner[victim] = a;
+    s->cache_use[victim] = tick;
+    s->h_cache[a] = victim;
+    loads.push_back({a, victim});
+  }
+  if (loads.empty()) return LORA_OK;
+  if (!s->copy_stream) CK(s, cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+  if (s->events.empty()) {
+    cudaEvent_t e;
+    CK(s, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->events.push_back(e);
+  }
+  // evicted slots may still be read by work already queued on `stream`
+  CK(s, cudaEventRecord(s->events[0], st));
+  CK(s, cudaStreamWaitEvent(s->copy_stream, s->events[0], 0));
+  for (size_t i = 0; i < s->slots.size(); ++i) {  // slot (layer) order: the first layers land first
+    SlotInfo& sl = s->slots[i];
+    const size_t ua = (size_t)sl.E * sl.h_in * s->r, ub = (size_t)sl.E * sl.h_out * s->r;
+    for (auto& ac : loads) {
+      CK(s, cudaMemcpyAsync(sl.At + (size_t)ac.second * ua, s->hostA[i] + (size_t)ac.first * ua, ua * 2,
+                            cudaMemcpyHostToDevice, s->copy_stream));
+      CK(s, cudaMemcpyAsync(sl.Bt + (size_t)ac.second * ub, s->hostB[i] + (size_t)ac.first * ub, ub * 2,
+                            cudaMemcpyHostToDevice, s->copy_stream));
+    }
+    CK(s, cudaEventRecord(s->slot_ready[i], s->copy_stream));
+    s->slot_pending[i] = 1;
+  }
+  // the new table, in stream order (pageable source: copied out at the call)
+  CK(s, cudaMemcpyAsync(s->d_cache, s->h_cache.data(), sizeof(int32_t) * s->n_adapters, cudaMemcpyHostToDevice, st));
+  if (n_loaded) *n_loaded = (int32_t)loads.size();
   return LORA_OK;
 }
 
@@ -409,6 +556,7 @@ lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapt
   CK(s, cudaSetDevice(s->device));
   const int pi = prof_start(s, st);
   sp.pl = placement(s);
+  sp.cache = s->d_cache;
   CK(s, launch_segment(adapter_ids, expert_ids, T, E, s->n_adapters, sp, p->dev, s->d_err, st));
   prof_stop(s, pi, kKSegment, st);
   p->n_experts = E;
@@ -462,6 +610,14 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
   }
   if (n == 0 || p->T == 0) return LORA_OK;
   CK(s, cudaSetDevice(s->device));
+  if (s->n_resident) {
+    // resident cache: wait for the pending host->device copies of these slots only
+    for (int i = 0; i < n; ++i)
+      if (s->slot_pending[slots[i]]) {
+        CK(s, cudaStreamWaitEvent(st, s->slot_ready[slots[i]], 0));
+        s->slot_pending[slots[i]] = 0;
+      }
+  }
   const bool tc = tc_enabled(s);
   for (int b0 = 0; b0 < n; b0 += kMaxTasks) {
     const int nb = std::min(kMaxTasks, n - b0);
@@ -471,6 +627,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.y_fp32 = y_dtype == LORA_FP32;
     args.y_store = store;
     args.pl = placement(s);
+    args.cache = s->d_cache;
     args.scale = s->d_scale;
     if (rin) args.rin = *rin;
     int kc = 0, ci = 0;

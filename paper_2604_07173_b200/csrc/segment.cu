@@ -58,11 +58,11 @@ __device__ int block_exclusive_scan(int v, int* tmp, int* total) {
 // Reads one row's ids; returns the key (a*E+e), or -1 for "no LoRA" / out of
 // range (flagged through *bad).
 LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int i, int E,
-                        int n_adapters, const Placement& pl, int& bad) {
+                        int n_adapters, const Placement& pl, int& bad, const int32_t* cache) {
   const int a = adapter_ids[i];
   const int e = expert_ids ? expert_ids[i] : 0;
   const bool in_range = (a >= -1) && (a < n_adapters) && (a < 0 || (e >= 0 && e < E)) &&
-                        (a < 0 || pl.owns(a));
+                        (a < 0 || pl.owns(a)) && (a < 0 || !cache || cache[a] >= 0);
   if (!in_range) bad = 1;
   return (in_range && a >= 0) ? a * E + e : -1;
 }
@@ -140,7 +140,7 @@ __device__ void radix_pass8(const uint32_t* in, uint32_t* out, int shift, int* c
 // builds composites and sorts them; returns the buffer holding the result
 template <int EPT>
 __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids,
-                                int T, int E, int n_adapters, const Placement& pl, int K, int kb, int ib,
+                                int T, int E, int n_adapters, const Placement& pl, const int32_t* cache, int K, int kb, int ib,
                                 uint32_t* A, uint32_t* B, int* cnt, int* err_flag, int* n_valid_out,
                                 int* scan_tmp) {
   const int tid = threadIdx.x;
@@ -149,7 +149,7 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
   for (int r = 0; r < EPT; ++r) {
     const int i = tid * EPT + r;
     int key = -1;
-    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad);
+    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad, cache);
     nv += key >= 0;
     A[pad32(i)] = ((uint32_t)(key >= 0 ? key : K) << ib) | (uint32_t)i;
   }
@@ -176,7 +176,7 @@ LORA_DEVINL unsigned long long umax64(unsigned long long a, unsigned long long b
 
 template <int EPT>
 __device__ void bitonic_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T,
-                             int E, int n_adapters, const Placement& pl, unsigned long long* sm, int* err_flag,
+                             int E, int n_adapters, const Placement& pl, const int32_t* cache, unsigned long long* sm, int* err_flag,
                              int* n_valid_out, int* scan_tmp) {
   constexpr int P = kSegThreads * EPT;
   const int tid = threadIdx.x;
@@ -186,7 +186,7 @@ __device__ void bitonic_sort(const int32_t* __restrict__ adapter_ids, const int3
   for (int r = 0; r < EPT; ++r) {
     const int i = tid * EPT + r;
     int key = -1;
-    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad);
+    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad, cache);
     nv += key >= 0;
     v[r] = key >= 0 ? (((unsigned long long)(unsigned)key << 32) | (unsigned)i) : ~0ull;
   }
@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   extern __shared__ __align__(16) uint8_t seg_smem[];
   pdl_launch_dependents();  // the shrink kernels may launch now; they wait for this grid
   const Placement pl = sp.pl;
+  const int32_t* cache = sp.cache;
   __shared__ int scan_tmp[40];
   __shared__ int s_nvalid;
   const int tid = threadIdx.x;
@@ -270,22 +271,22 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     const int K = n_adapters * E;
     uint32_t* res = nullptr;
     switch (EPT) {
-      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
     }
     srt32 = res;
     segoff_s = reinterpret_cast<int*>(res == A ? B : A);  // the free buffer (P + 1 ints reserved)
   } else {
     unsigned long long* S64 = reinterpret_cast<unsigned long long*>(seg_smem);
     switch (EPT) {
-      case 1: bitonic_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
-      case 2: bitonic_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
-      case 4: bitonic_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
-      case 8: bitonic_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
-      default: bitonic_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 1: bitonic_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: bitonic_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: bitonic_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, S64, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: bitonic_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, S64, err_flag, &s_nvalid, scan_tmp); break;
+      default: bitonic_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, S64, err_flag, &s_nvalid, scan_tmp); break;
     }
     srt64 = S64;
     segoff_s = reinterpret_cast<int*>(S64 + P);

@@ -50,6 +50,17 @@ struct lora_server {
   bool concurrent_tc = true;  // env LORA_SERIAL=1 keeps everything on the caller's stream
   std::vector<cudaEvent_t> events;      // lora_apply_multi_host pipeline events (grown on demand)
   ShardState* shard = nullptr;
+  // resident-adapter cache (n_resident > 0): host backing store per slot in the
+  // kernel layout, device cache-slot table, LRU state, per-slot load events
+  int n_resident = 0;
+  std::vector<uint16_t*> hostA, hostB;  // pinned, [n_adapters][E][...] per slot
+  int32_t* d_cache = nullptr;           // [n_adapters] cache slot or -1
+  std::vector<int32_t> h_cache;         // host mirror of d_cache
+  std::vector<int> cache_owner;         // [n_resident] adapter in each cache slot, -1 empty
+  std::vector<long long> cache_use;     // [n_resident] last require tick
+  long long cache_tick = 0;
+  std::vector<cudaEvent_t> slot_ready;  // per slot: its copies done
+  std::vector<char> slot_pending;       // per slot: a wait is owed by the next apply
   // per-launch CUDA-event profiling (lora_profile_enable / lora_profile_read)
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_pool;

@@ -94,10 +94,6 @@ LORA_DEVINL uint8_t* align1024(uint8_t* p) {
 }
 
 
-LORA_DEVINL long long unit_of_key(int key, int E, const Placement& pl) {
-  const int a = key / E, e = key - a * E;
-  return pl.local_index(a) * E + e;
-}
 
 LORA_DEVINL void unpack8(const uint4& w, float* f) {
   f[0] = bf16lo(w.x); f[1] = bf16hi(w.x);
@@ -323,7 +319,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         const int ti = (int)(it / n_groups), gi = (int)(it - (long long)ti * n_groups);
         const SlotTask& t = args.t[ti];
         const int4 g = pd.groups[gi];
-        const long long unit = unit_of_key(g.z, t.E, args.pl);
+        const long long unit = store_unit(g.z, t.E, args.pl, args.cache);
         const uint16_t* abase = t.At + unit * (long long)t.h_in * R;
         const int n_st = t.h_in / t.SJ;
         const uint32_t a_bytes = (uint32_t)R * t.SJ * 2, x_bytes = (uint32_t)t.SJ * 2;
@@ -611,7 +607,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         const SlotTask& t = args.t[ti];
         const int ci = cig - t.ci_base;
         const int4 g = pd.groups[gi];
-        const long long unit = unit_of_key(g.z, t.E, args.pl);
+        const long long unit = store_unit(g.z, t.E, args.pl, args.cache);
         const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
         const float* vsrc = pd.vpart + t.vpart_off + (long long)g.x * R;
         const int n_st = t.CI / t.SC;

@@ -45,15 +45,15 @@ LORA_DEVINL unsigned long long hash_base(unsigned long long seed, unsigned tag, 
 }
 
 // map a local unit index of this rank's store to the global unit id a*E+e (-1: padding)
-LORA_DEVINL long long global_unit(long long u, int E, const Placement& pl, int n_adapters) {
+LORA_DEVINL long long global_unit(long long u, int E, const Placement& pl, int n_adapters, long long adapter_base) {
   const long long al = u / E, e = u - al * E;
-  const long long a = pl.global_adapter(al);
+  const long long a = pl.global_adapter(al) + adapter_base;
   return a < n_adapters ? a * E + e : -1;
 }
 
 // one thread = 8 consecutive store elements (one 16-byte chunk)
 __global__ void fill_A_kernel(uint16_t* __restrict__ At, long long units, int h_in, int r, unsigned long long seed,
-                              unsigned tag, float scale, int E, Placement pl, int n_adapters) {
+                              unsigned tag, float scale, int E, Placement pl, int n_adapters, long long adapter_base) {
   const long long n_chunks = units * h_in * r / 8;
   const int tiles = h_in >> 6;
   for (long long ch = blockIdx.x * (long long)blockDim.x + threadIdx.x; ch < n_chunks;
@@ -65,7 +65,7 @@ __global__ void fill_A_kernel(uint16_t* __restrict__ At, long long units, int h_
     const int q = pc ^ (k & 7);
     const long long u = tile / tiles;
     const int j0 = (int)(tile - u * tiles) * 64 + q * 8;
-    const long long gu = global_unit(u, E, pl, n_adapters);
+    const long long gu = global_unit(u, E, pl, n_adapters, adapter_base);
     uint16_t v[8];
     if (gu < 0) {
 #pragma unroll
@@ -85,7 +85,7 @@ __global__ void fill_A_kernel(uint16_t* __restrict__ At, long long units, int h_
 }
 
 __global__ void fill_B_kernel(uint16_t* __restrict__ Bt, long long units, int h_out, int r, unsigned long long seed,
-                              unsigned tag, float scale, int E, Placement pl, int n_adapters) {
+                              unsigned tag, float scale, int E, Placement pl, int n_adapters, long long adapter_base) {
   const long long n_chunks = units * h_out * r / 8;
   const int cpr = r / 8;  // chunks per row
   for (long long ch = blockIdx.x * (long long)blockDim.x + threadIdx.x; ch < n_chunks;
@@ -95,7 +95,7 @@ __global__ void fill_B_kernel(uint16_t* __restrict__ Bt, long long units, int h_
     const long long u = row / h_out;
     const int c = (int)(row - u * h_out);
     const int q = swz_row_chunk(c, pc, r * 2);
-    const long long gu = global_unit(u, E, pl, n_adapters);
+    const long long gu = global_unit(u, E, pl, n_adapters, adapter_base);
     uint16_t v[8];
     if (gu < 0) {
 #pragma unroll
@@ -171,15 +171,15 @@ static int shift_of(int width) { return 7 + (int)ceil(log2((double)width) / 2.0)
 
 cudaError_t launch_fill_store(uint16_t* At, uint16_t* Bt, int h_in, int h_out, int E, int r, long long units,
                               int slot, unsigned long long seed, const Placement& pl, int n_adapters,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, long long adapter_base) {
   const float sa = ldexpf(1.0f, -shift_of(h_in));
   const float sb = ldexpf(1.0f, -shift_of(r));
   const unsigned tagA = (1u << 16) | (unsigned)slot, tagB = (2u << 16) | (unsigned)slot;
   const long long na = units * h_in * r / 8, nb = units * h_out * r / 8;
   fill_A_kernel<<<grid_for(na, 256), 256, 0, stream>>>(At, units, h_in, r, seed, tagA, sa, E, pl,
-                                                        n_adapters);
+                                                        n_adapters, adapter_base);
   fill_B_kernel<<<grid_for(nb, 256), 256, 0, stream>>>(Bt, units, h_out, r, seed, tagB, sb, E, pl,
-                                                        n_adapters);
+                                                        n_adapters, adapter_base);
   return cudaGetLastError();
 }
 

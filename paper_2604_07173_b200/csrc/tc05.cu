@@ -97,10 +97,6 @@ LORA_DEVINL uint8_t* align1024(uint8_t* p) {
   return p + (((a + 1023u) & ~1023u) - a);
 }
 
-LORA_DEVINL long long unit_of_key(int key, int E, const Placement& pl) {
-  const int a = key / E, e = key - a * E;
-  return pl.local_index(a) * E + e;
-}
 
 constexpr int R = 64;  // tcgen05 path rank
 constexpr int kQD = 4;  // work-queue depth
@@ -188,7 +184,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       const SlotTask& t = args.t[task];
       const int kc = kcg - t.kc_base;
       const int4 tile = pd.tiles[ti];
-      const long long unit = unit_of_key(tile.z, t.E, args.pl);
+      const long long unit = store_unit(tile.z, t.E, args.pl, args.cache);
       const uint16_t* wbase = t.At + (unit * (t.h_in >> 6) + ((kc * t.KI) >> 6)) * (long long)(R * 64);
       // this thread's rows / chunks: 128 rows x 8 chunks per k-step, 1024 copies / 128 threads;
       // thread pt always copies chunk q = pt & 7 of rows n = (pt >> 3) + 16 i
@@ -516,7 +512,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           vb = 0;
           vphase ^= 1;
         }
-        const long long unit = unit_of_key(tile.z, t.E, args.pl);
+        const long long unit = store_unit(tile.z, t.E, args.pl, args.cache);
         const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
         const int n_sub = t.CI / C::MSUB;
         for (int sb = 0; sb < n_sub; ++sb) {

@@ -356,6 +356,53 @@ def test_edge_cases(B, case):
         B.lora_server_destroy(s)
 
 
+@pytest.mark.parametrize("rank", [16, 64])
+def test_resident_cache_matches_full_store(B, rank):
+    """Resident-adapter cache (n_resident = 6 of 24 adapters, weights in
+    pinned host memory, lora_server_require with LRU eviction and per-slot
+    copies): bit-identical to the fully resident server on batches drawn from
+    changing adapter subsets; a repeated subset copies nothing; a row whose
+    adapter is not resident is skipped and flagged."""
+    cfg = _mid_cfg(rank=rank, T=400)
+    full = U.make_server(B, cfg)
+    c = B.make_config([sl.h_in for sl in cfg.slots], [sl.h_out for sl in cfg.slots],
+                      [sl.n_experts for sl in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), 400, 0,
+                      n_resident=6)
+    cs = B.lora_server_create(c)
+    try:
+        B.lora_server_fill_synthetic(cs, cfg.seed)
+        rng = np.random.default_rng(11)
+        T = 400
+        subsets = [[0, 1, 2, 3], [0, 1, 2, 3], [4, 5, 6, 7, 8, 9], [0, 5, 23, 12], [12, 13, 14, 15, 16, 17]]
+        expect_loads = [4, 0, 6, None, None]
+        for it, sub in enumerate(subsets):
+            a = rng.choice(np.array(sub + [-1]), T).astype(np.int32)
+            e = rng.integers(0, cfg.n_experts, T).astype(np.int32)
+            b = li.Batch(a, e, T, 1)
+            loaded = B.lora_server_require(cs, sub)
+            if expect_loads[it] is not None:
+                assert loaded == expect_loads[it], (it, loaded)
+            y_full = _run_multi(B, full, cfg, b, [0, 1])
+            y_cache = _run_multi(B, cs, cfg, b, [0, 1])
+            for i in range(2):
+                assert torch.equal(y_cache[i], y_full[i]), (it, i)
+        # adapter 20 is not resident: its rows are skipped and flagged
+        a = np.full(T, 12, np.int32)
+        a[5] = 20
+        b = li.Batch(a, np.zeros(T, np.int32), T, 1)
+        y0 = U.y0_dev(B, cfg, 0, T)
+        x = U.x_dev(B, cfg, 0, T)
+        ad = torch.from_numpy(a).to(U.DEV)
+        ex = torch.zeros(T, dtype=torch.int32, device=U.DEV)
+        y = y0.clone()
+        B.lora_apply(cs, 0, x, ad, ex, y, B.LORA_BF16, T)
+        assert B.lora_server_check(cs) == B.LORA_ERR_ID_OUT_OF_RANGE
+        assert torch.equal(y[5], y0[5])
+    finally:
+        B.lora_server_destroy(cs)
+        B.lora_server_destroy(full)
+
+
 def test_permutation_equivariance_bit_exact(B):
     cfg = _mid_cfg()
     b = li.make_batch(cfg)
