@@ -238,7 +238,7 @@ def run_ours(args, cfg, batch, slots):
     sharded = world > 1 or args.force_sharded
     if args.force_sharded and world == 1:
         os.environ["LORA_SHARD_LOOPBACK"] = "1"  # every row through the NCCL exchange (to itself)
-    n_rep, rep_table = 0, None
+    n_rep, rep_table, ep_mode = 0, None, False
     if sharded:
         # popularity-aware placement (R19): replicate the hottest
         # adapters on every rank; auto = the host cost model's choice
@@ -246,12 +246,13 @@ def run_ours(args, cfg, batch, slots):
         ub, rb, xb = PL.slot_bytes([cfg.slots[i].h_in for i in slots], [cfg.slots[i].h_out for i in slots],
                                    [cfg.slots[i].xbuf for i in slots], cfg.rank, ysz, ysz)
         src = PL.sources_of_rows(cfg.n_tokens, k, world)
-        ch = PL.choose_n_replicated(batch.adapter_ids, batch.expert_ids if E > 1 else None, src, world, ub, rb, xb)
+        ch = PL.choose_placement(batch.adapter_ids, batch.expert_ids if E > 1 else None, src, world, ub, rb, xb)
         n_rep = ch["n_replicated"] if args.n_replicated < 0 else args.n_replicated
+        ep_mode = ch["expert_parallel"] if args.n_replicated < 0 else False
         rep_table = {str(h): round(v * 1e3, 4) for h, v in ch["table"].items()}
     c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots],
                       [s.n_experts for s in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), max(T, 1), local,
-                      n_replicated=n_rep)
+                      n_replicated=n_rep, expert_parallel=ep_mode)
     if sharded:
         uid = [B.lora_nccl_unique_id() if rank == 0 else None]
         if world > 1:
@@ -438,6 +439,7 @@ def run_ours(args, cfg, batch, slots):
                        "rank": cfg.rank, "adapters": cfg.n_adapters,
                        "parallelism": f"adapter-sharded dp{world} (NCCL all-to-all)" if sharded else "single GPU",
                        "n_replicated": n_rep if sharded else None,
+                       "expert_parallel": ep_mode if sharded else None,
                        "placement_model_ms": rep_table,
                        "l2": f"inputs larger than L2 ({alg['total'] / 1e9:.1f} GB touched per step)"},
             "e2e": e2e,

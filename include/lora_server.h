@@ -74,6 +74,10 @@ typedef struct {
                                 every rank (popularity-aware placement for skewed traffic,
                                 P:291; adapter ids are assumed ordered by popularity); 0 =
                                 plain striping.  Ignored by lora_server_create. */
+  int32_t expert_parallel;   /* sharded servers: 0 => LoRA Data Parallel (adapter striping, with
+                                n_replicated); 1 => expert parallel: unit (a, e) owned by rank
+                                e mod world, every adapter (all slots must share one
+                                expert count).  Ignored by lora_server_create. */
   int32_t n_resident;        /* single-GPU servers: 0 => every adapter resident in device memory;
                                 0 < n_resident < n_adapters => resident-adapter cache (P:519-531,
                                 Sec. 5.3): all adapters live in pinned host memory in the kernel

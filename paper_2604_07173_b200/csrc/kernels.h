@@ -17,12 +17,17 @@ enum { kCntValid = 0, kCntSegs = 1, kCntGroups = 2, kCntTiles = 3, kCntWords = 8
 // work-counter slots of the persistent kernels
 enum { kWqSimtShrink = 0, kWqSimtExpand = 1, kWqTcShrink = 2, kWqTcExpand = 3, kWorkSlots = 8 };
 
-// Adapter placement of a (sharded) server.  Adapters [0, n_hot) are replicated
-// on every rank (popularity-aware placement); adapter
-// a >= n_hot is owned by rank (a - n_hot) mod world (LoRA Data Parallel
-// striping).  An unsharded server is {1, 0, 0}.
+// Unit placement of a (sharded) server; a unit is (adapter a, expert e).
+//  * LoRA Data Parallel (ep = 0): adapters [0, n_hot) are
+//    replicated on every rank (popularity-aware placement);
+//    adapter a >= n_hot is owned by rank (a - n_hot) mod world, all experts.
+//  * Expert parallel (ep = 1, Table 1 EP row):
+//    unit (a, e) is owned by rank e mod world, every adapter (all slots of
+//    the server share one expert count, checked at create).
+// An unsharded server is {1, 0, 0, 0}.
 struct Placement {
-  int world, rank, n_hot;
+  int world, rank, n_hot, ep;
+  // adapter-level view (ep = 0)
   __host__ __device__ bool owns(int a) const { return a < n_hot || (a - n_hot) % world == rank; }
   __host__ __device__ int owner(int a) const { return a < n_hot ? rank : (a - n_hot) % world; }
   __host__ __device__ long long local_index(int a) const {
@@ -32,11 +37,31 @@ struct Placement {
   __host__ __device__ long long global_adapter(long long li) const {
     return li < n_hot ? li : (long long)n_hot + (li - n_hot) * world + rank;
   }
-  // adapters stored on this rank
+  // adapters stored on this rank (ep = 0)
   __host__ __device__ int n_local(int n_adapters) const {
     const int h = n_hot < n_adapters ? n_hot : n_adapters;
     const int rest = n_adapters - h;
     return h + (rest > rank ? (rest - rank + world - 1) / world : 0);
+  }
+  // unit-level view (both modes)
+  __host__ __device__ int experts_local(int E) const { return ep ? (E > rank ? (E - 1 - rank) / world + 1 : 0) : E; }
+  __host__ __device__ bool owns_unit(int a, int e) const { return ep ? e % world == rank : owns(a); }
+  __host__ __device__ int owner_unit(int a, int e) const { return ep ? e % world : owner(a); }
+  __host__ __device__ long long local_unit(int a, int e, int E) const {
+    return ep ? (long long)a * experts_local(E) + e / world : local_index(a) * E + e;
+  }
+  // inverse of local_unit: global key a*E+e of local unit u (-1: none)
+  __host__ __device__ long long global_key(long long u, int E, int n_adapters) const {
+    const int el = experts_local(E);
+    if (el == 0) return -1;
+    const long long al = u / el, ei = u - al * el;
+    const long long a = ep ? al : global_adapter(al);
+    const long long e = ep ? ei * world + rank : ei;
+    return a < n_adapters ? a * E + e : -1;
+  }
+  // units stored on this rank
+  __host__ __device__ long long n_local_units(int n_adapters, int E) const {
+    return ep ? (long long)n_adapters * experts_local(E) : (long long)n_local(n_adapters) * E;
   }
 };
 
@@ -73,7 +98,7 @@ __host__ __device__ inline long long store_unit(int key, int E, const Placement&
 #else
   if (cache) return (long long)cache[a] * E + e;
 #endif
-  return pl.local_index(a) * E + e;
+  return pl.local_unit(a, e, E);
 }
 
 // One slot inside a (multi-slot) launch.

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <set>
@@ -110,7 +111,8 @@ static void free_server(lora_server* s) {
 }
 
 // allocate the store; world/rank select the owned adapters (a mod world == rank)
-static lora_status_t create_common(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot) {
+static lora_status_t create_common(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot,
+                                   int ep = 0) {
   lora_status_t v = validate_config(cfg);
   if (v != LORA_OK) return v;
   if (!out) return fail(nullptr, LORA_ERR_INVALID_ARG, "out is NULL");
@@ -132,7 +134,14 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   s->n_adapters = cfg->n_adapters;
   s->world = world;
   s->shard_rank = rank;
-  s->n_hot = world > 1 ? std::max(0, std::min(n_hot, cfg->n_adapters)) : 0;
+  s->ep = (world > 1 && ep) ? 1 : 0;
+  s->n_hot = (world > 1 && !s->ep) ? std::max(0, std::min(n_hot, cfg->n_adapters)) : 0;
+  if (s->ep)
+    for (int i = 1; i < cfg->n_slots; ++i)
+      if (cfg->n_experts[i] != cfg->n_experts[0]) {
+        delete s;
+        return fail(nullptr, LORA_ERR_UNSUPPORTED, "expert parallel needs one expert count for every slot");
+      }
   s->n_adapters_local = placement(s).n_local(cfg->n_adapters);
   if (world == 1 && cfg->n_resident > 0 && cfg->n_resident < cfg->n_adapters) s->n_resident = cfg->n_resident;
   // device store: every local adapter, or the cache slots
@@ -156,7 +165,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
     sl.h_in = cfg->h_in[i];
     sl.h_out = cfg->h_out[i];
     sl.E = cfg->n_experts[i];
-    sl.units = (long long)store_adapters * sl.E;
+    sl.units = s->n_resident ? (long long)store_adapters * sl.E : placement(s).n_local_units(cfg->n_adapters, sl.E);
     // shrink items of ~128 KB of A, expand items of ~128 KB of B
     sl.KI = best_divisor(sl.h_in, 64, std::max(64, 65536 / r));
     sl.SJ = best_divisor(sl.KI, 64, simt_sj_max(r));
@@ -238,8 +247,9 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   return LORA_OK;
 }
 
-lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot) {
-  return create_common(cfg, world, rank, out, n_hot);
+lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot,
+                                    int ep) {
+  return create_common(cfg, world, rank, out, n_hot, ep);
 }
 
 // delta mode for the sharded owner: d[i] receives s*(xA)B (stored, not added) as fp32 or bf16
@@ -272,28 +282,34 @@ static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, con
   const size_t stage_elems = (size_t)sl.E * std::max(a_unit, b_unit);
   CK(s, cudaMalloc(&stage, stage_elems * 2));
   lora_status_t rc = LORA_OK;
+  const Placement pl = placement(s);
   for (int i = 0; i < n && rc == LORA_OK; ++i) {
     const int a = a_begin + i;
-    const Placement pl = placement(s);
-    if (!pl.owns(a)) continue;  // not stored on this rank
-    // cache mode: relayout in cache slot 0's area, then into the host backing store
-    const long long lu = s->n_resident ? 0 : pl.local_index(a) * sl.E;
-    for (int pass = 0; pass < 2; ++pass) {
-      const void* src = pass == 0 ? A : B;
-      if (!src) continue;
-      const size_t ue = pass == 0 ? a_unit : b_unit;
-      const uint16_t* from = static_cast<const uint16_t*>(src) + (size_t)i * sl.E * ue;
-      cudaError_t e = cudaMemcpyAsync(stage, from, (size_t)sl.E * ue * 2,
-                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess)
-        e = pass == 0 ? launch_relayout_A(stage, sl.At + lu * a_unit, sl.E, sl.h_in, r, st)
-                      : launch_relayout_B(stage, sl.Bt + lu * b_unit, sl.E, sl.h_out, r, st);
-      if (e == cudaSuccess && s->n_resident) {
-        uint16_t* host = pass == 0 ? s->hostA[slot] + (size_t)a * sl.E * a_unit : s->hostB[slot] + (size_t)a * sl.E * b_unit;
-        e = cudaMemcpyAsync(host, pass == 0 ? sl.At : sl.Bt, (size_t)sl.E * ue * 2, cudaMemcpyDeviceToHost, st);
+    // the owned experts of adapter a, as runs of consecutive units in the store
+    // (all E for the adapter-level placements, every world-th one for EP)
+    for (int e = 0; e < sl.E && rc == LORA_OK; ++e) {
+      if (!pl.owns_unit(a, e)) continue;
+      const int run = pl.ep ? 1 : sl.E;  // adapter-level: one run of E units
+      // cache mode: relayout in cache slot 0's area, then into the host backing store
+      const long long lu = s->n_resident ? 0 : pl.local_unit(a, e, sl.E);
+      for (int pass = 0; pass < 2; ++pass) {
+        const void* src = pass == 0 ? A : B;
+        if (!src) continue;
+        const size_t ue = pass == 0 ? a_unit : b_unit;
+        const uint16_t* from = static_cast<const uint16_t*>(src) + ((size_t)i * sl.E + e) * ue;
+        cudaError_t err = cudaMemcpyAsync(stage, from, (size_t)run * ue * 2,
+                                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+        if (err == cudaSuccess)
+          err = pass == 0 ? launch_relayout_A(stage, sl.At + lu * a_unit, run, sl.h_in, r, st)
+                          : launch_relayout_B(stage, sl.Bt + lu * b_unit, run, sl.h_out, r, st);
+        if (err == cudaSuccess && s->n_resident) {
+          uint16_t* host = pass == 0 ? s->hostA[slot] + (size_t)a * sl.E * a_unit : s->hostB[slot] + (size_t)a * sl.E * b_unit;
+          err = cudaMemcpyAsync(host, pass == 0 ? sl.At : sl.Bt, (size_t)run * ue * 2, cudaMemcpyDeviceToHost, st);
+        }
+        if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+        if (err != cudaSuccess) rc = cuda_fail(s, err, "lora_server_load");
       }
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) rc = cuda_fail(s, e, "lora_server_load");
+      if (!pl.ep) break;  // the run covered every expert of the adapter
     }
   }
   cudaFree(stage);
@@ -303,7 +319,18 @@ static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, con
 
 extern "C" lora_status_t lora_server_create(const lora_config_t* cfg, const void* const* A, const void* const* B,
                                             int weights_on_device, lora_server_t** out) {
-  lora_status_t st = create_common(cfg, 1, 0, out, 0);
+  // Test hook LORA_FAKE_WORLD="world,rank[,ep[,n_hot]]": store only what that
+  // rank of a sharded server would own (no communicator; rows of units it
+  // does not own are rejected like out-of-range ids), so the sharded store
+  // layouts can be checked against the oracle on one GPU.
+  int fw = 1, fr = 0, fep = 0, fhot = 0;
+  if (const char* f = std::getenv("LORA_FAKE_WORLD")) {
+    if (std::sscanf(f, "%d,%d,%d,%d", &fw, &fr, &fep, &fhot) < 2 || fw < 1 || fr < 0 || fr >= fw) {
+      fw = 1;
+      fr = 0;
+    }
+  }
+  lora_status_t st = create_common(cfg, fw, fr, out, fhot, fep);
   if (st != LORA_OK) return st;
   lora_server* s = *out;
   for (int i = 0; i < cfg->n_slots; ++i) {
@@ -786,7 +813,7 @@ extern "C" lora_status_t lora_plan_stats(const lora_plan_t* p, int32_t* out4, vo
 extern "C" lora_status_t lora_apply_plan(lora_server_t* s, const lora_plan_t* p, int32_t slot, const void* x, void* y,
                                          lora_dtype_t y_dtype, void* stream) {
   if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
-  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  if (s->shard) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
   const void* xs[1] = {x};
   void* ys[1] = {y};
   return apply_multi_impl(s, p, 1, &slot, xs, ys, y_dtype, static_cast<cudaStream_t>(stream));
@@ -796,7 +823,7 @@ extern "C" lora_status_t lora_apply_plan_multi(lora_server_t* s, const lora_plan
                                                const void* const* x, void* const* y, lora_dtype_t y_dtype,
                                                void* stream) {
   if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
-  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  if (s->shard) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
   return apply_multi_impl(s, p, n, slots, x, y, y_dtype, static_cast<cudaStream_t>(stream));
 }
 
@@ -804,7 +831,7 @@ extern "C" lora_status_t lora_apply(lora_server_t* s, int32_t slot, const void* 
                                     const int32_t* expert_ids, void* y, lora_dtype_t y_dtype, int32_t T,
                                     void* stream) {
   if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
-  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  if (s->shard) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
   if (slot < 0 || slot >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   lora_status_t rc = plan_build_impl(s, s->internal_plan, adapter_ids, expert_ids, T, s->slots[slot].E, st);
@@ -822,7 +849,7 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
                                                const int32_t* expert_ids_host, void* const* y_host,
                                                lora_dtype_t y_dtype, int32_t T, void* stream) {
   if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
-  if (s->world > 1) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  if (s->shard) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
   if (n < 1 || !slots || !x_host || !y_host || (T > 0 && !adapter_ids_host))
     return fail(s, LORA_ERR_INVALID_ARG, "NULL argument");
   if (T < 0 || T > s->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");

@@ -62,7 +62,7 @@ LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* 
   const int a = adapter_ids[i];
   const int e = expert_ids ? expert_ids[i] : 0;
   const bool in_range = (a >= -1) && (a < n_adapters) && (a < 0 || (e >= 0 && e < E)) &&
-                        (a < 0 || pl.owns(a)) && (a < 0 || !cache || cache[a] >= 0);
+                        (a < 0 || pl.owns_unit(a, e)) && (a < 0 || !cache || cache[a] >= 0);
   if (!in_range) bad = 1;
   return (in_range && a >= 0) ? a * E + e : -1;
 }

@@ -31,6 +31,7 @@ struct lora_server {
   int small_seg_max = 8;
   int world = 1, shard_rank = 0;
   int n_hot = 0;  // adapters [0, n_hot) replicated on every rank of a sharded server
+  int ep = 0;     // 1: expert-parallel ownership (unit (a, e) on rank e mod world)
   bool debug_sync = false;
   std::vector<SlotInfo> slots;
   int total_kc = 0;        // sum of n_kc over all slots
@@ -96,8 +97,11 @@ void plan_destroy_impl(lora_plan* p);
 
 // shard.cu / lora_server.cu cross-file helpers (C++ linkage)
 void lora_shard_free(lora_server* s);
-lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot);
-inline lora::Placement placement(const lora_server* s) { return lora::Placement{s->world, s->shard_rank, s->n_hot}; }
+lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot,
+                                    int ep);
+inline lora::Placement placement(const lora_server* s) {
+  return lora::Placement{s->world, s->shard_rank, s->n_hot, s->ep};
+}
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
                                 const void* const* x, void* const* d, cudaStream_t st, bool bf16,
                                 const lora::RemoteIn* rin = nullptr, const long long* x_off = nullptr);

@@ -100,8 +100,8 @@ constexpr int kBucketThreads = 1024;
 // through the exchange as well, so a single GPU exercises the NCCL path.
 // Out-of-range ids are flagged and dropped (never sent, never applied).
 __global__ void __launch_bounds__(kBucketThreads, 1)
-    bucket_kernel(const int32_t* __restrict__ ad, int T, Placement pl, int n_adapters, int loopback,
-                  int32_t* __restrict__ ad_local,
+    bucket_kernel(const int32_t* __restrict__ ad, const int32_t* __restrict__ ex, int T, Placement pl, int n_adapters,
+                  int loopback, int32_t* __restrict__ ad_local,
                   int32_t* __restrict__ send_idx, int32_t* __restrict__ counts, int* __restrict__ err) {
   __shared__ int s_tmp[32];
   __shared__ int s_base;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
     const int a = ad[r];
     const bool ok = a >= -1 && a < n_adapters;
     if (!ok) bad = 1;
-    ad_local[r] = (!loopback && ok && a >= 0 && pl.owner(a) == pl.rank) ? a : -1;
+    ad_local[r] = (!loopback && ok && a >= 0 && pl.owner_unit(a, ex ? ex[r] : 0) == pl.rank) ? a : -1;
   }
   if (bad) atomicOr(err, 1);
   __syncthreads();
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
     int c = 0;
     for (int r = r0; r < r1; ++r) {
       const int a = ad[r];
-      c += (a >= 0 && a < n_adapters && pl.owner(a) == o);
+      c += (a >= 0 && a < n_adapters && pl.owner_unit(a, ex ? ex[r] : 0) == o);
     }
     // block exclusive scan of c
     int x = c;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
     const int tot = s_tmp[31];
     for (int r = r0; r < r1; ++r) {
       const int a = ad[r];
-      if (a >= 0 && a < n_adapters && pl.owner(a) == o) send_idx[pos++] = r;
+      if (a >= 0 && a < n_adapters && pl.owner_unit(a, ex ? ex[r] : 0) == o) send_idx[pos++] = r;
     }
     __syncthreads();
     if (tid == 0) {
@@ -379,7 +379,7 @@ extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, in
   if (cfg->n_replicated < 0) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_replicated < 0");
   NcclApi& api = nccl();
   if (!api.ok) return fail(nullptr, LORA_ERR_NCCL, api.err);
-  lora_status_t st = create_common_sharded(cfg, world, rank, out, cfg->n_replicated);
+  lora_status_t st = create_common_sharded(cfg, world, rank, out, cfg->n_replicated, cfg->expert_parallel);
   if (st != LORA_OK) return st;
   lora_server* s = *out;
   s->shard = new ShardState();
@@ -580,7 +580,7 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   CKS(cudaStreamWaitEvent(st, sh->ev[3], 0));
   if (T > 0) {
     const int pi = prof_start(s, st);
-    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, T, pl, s->n_adapters, sh->loopback, d_ad_local, d_send_idx, d_counts,
+    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, expert_ids, T, pl, s->n_adapters, sh->loopback, d_ad_local, d_send_idx, d_counts,
                                                  s->d_err);
     prof_stop(s, pi, kKShardBucket, st);
   } else {

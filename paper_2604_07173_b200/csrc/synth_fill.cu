@@ -46,9 +46,10 @@ LORA_DEVINL unsigned long long hash_base(unsigned long long seed, unsigned tag, 
 
 // map a local unit index of this rank's store to the global unit id a*E+e (-1: padding)
 LORA_DEVINL long long global_unit(long long u, int E, const Placement& pl, int n_adapters, long long adapter_base) {
-  const long long al = u / E, e = u - al * E;
-  const long long a = pl.global_adapter(al) + adapter_base;
-  return a < n_adapters ? a * E + e : -1;
+  const long long k = pl.global_key(u, E, n_adapters);
+  if (k < 0) return -1;
+  const long long gk = k + adapter_base * E;  // resident-cache fill: unsharded, adapters shifted
+  return gk < (long long)n_adapters * E ? gk : -1;
 }
 
 // one thread = 8 consecutive store elements (one 16-byte chunk)

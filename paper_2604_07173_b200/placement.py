@@ -19,16 +19,21 @@ from typing import Dict, Iterable, Optional, Sequence
 import numpy as np
 
 
-def owner(adapter_ids: np.ndarray, world: int, n_hot: int, src: np.ndarray) -> np.ndarray:
-    """Rank that processes each row (-1 for rows without an adapter)."""
+def owner(adapter_ids: np.ndarray, world: int, n_hot: int, src: np.ndarray, expert_ids=None,
+          ep: bool = False) -> np.ndarray:
+    """Rank that processes each row (-1 for rows without an adapter).  ep:
+    expert parallel, owner = e mod world (include/lora_server.h)."""
     a = np.asarray(adapter_ids, np.int64)
+    if ep:
+        e = np.zeros_like(a) if expert_ids is None else np.asarray(expert_ids, np.int64)
+        return np.where(a >= 0, e % world, -1)
     own = np.where(a >= 0, (a - n_hot) % world, -1)
     return np.where((a >= 0) & (a < n_hot), np.asarray(src, np.int64), own)
 
 
 def rank_costs(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray], src: np.ndarray, world: int, n_hot: int,
                unit_bytes: float, row_bytes: float, xfer_bytes: float, hbm_gbs: float = 6500.0,
-               link_gbs: float = 700.0) -> np.ndarray:
+               link_gbs: float = 700.0, ep: bool = False) -> np.ndarray:
     """Modelled time (s) per rank of one sharded apply.
 
     unit_bytes: weight bytes of one (adapter, expert) unit over all slots;
@@ -37,7 +42,7 @@ def rank_costs(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray], src: n
     a = np.asarray(adapter_ids, np.int64)
     e = np.zeros_like(a) if expert_ids is None else np.asarray(expert_ids, np.int64)
     src = np.asarray(src, np.int64)
-    own = owner(a, world, n_hot, src)
+    own = owner(a, world, n_hot, src, e, ep)
     valid = a >= 0
     n_e = int(e.max()) + 1 if e.size else 1
     key = a * n_e + e
@@ -68,6 +73,21 @@ def choose_n_replicated(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray
                                          xfer_bytes, **kw).max())
     best = min(table, key=lambda h: (table[h], h))
     return {"n_replicated": best, "table": table}
+
+
+def choose_placement(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray], src: np.ndarray, world: int,
+                     unit_bytes: float, row_bytes: float, xfer_bytes: float, **kw) -> Dict:
+    """Best of LoRA Data Parallel with replication (choose_n_replicated) and
+    expert parallel (MoE only), by the slowest rank's modelled time."""
+    dp = choose_n_replicated(adapter_ids, expert_ids, src, world, unit_bytes, row_bytes, xfer_bytes, **kw)
+    out = {"expert_parallel": False, "n_replicated": dp["n_replicated"], "table": dict(dp["table"])}
+    if world > 1 and expert_ids is not None:
+        t_ep = float(rank_costs(adapter_ids, expert_ids, src, world, 0, unit_bytes, row_bytes, xfer_bytes, ep=True,
+                                **kw).max())
+        out["table"]["ep"] = t_ep
+        if t_ep < dp["table"][dp["n_replicated"]]:
+            out.update(expert_parallel=True, n_replicated=0)
+    return out
 
 
 def sources_of_rows(n_tokens: int, top_k: int, world: int) -> np.ndarray:

@@ -202,6 +202,27 @@ def _run_multi(B, s, cfg, batch, slot_ids, y0="random", host=False):
     return ys
 
 
+def _run_multi_unchecked(B, s, cfg, batch, slot_ids):
+    """_run_multi without asserting a clean sticky flag (rows may be rejected)."""
+    T = batch.n_rows
+    ad, ex = U.ids_dev(batch)
+    E = cfg.slots[slot_ids[0]].n_experts
+    xs = {}
+    for i in slot_ids:
+        if cfg.slots[i].xbuf not in xs:
+            xs[cfg.slots[i].xbuf] = U.x_dev(B, cfg, i, T)
+    ys = [U.y0_dev(B, cfg, i, T) for i in slot_ids]
+    p = B.lora_plan_create(s, T)
+    try:
+        B.lora_plan_build(s, p, ad, ex if E > 1 else None, T, E)
+        B.lora_apply_plan_multi(s, p, list(slot_ids), [xs[cfg.slots[i].xbuf] for i in slot_ids], ys,
+                                B.LORA_FP32 if cfg.y_dtype == "fp32" else B.LORA_BF16)
+        torch.cuda.synchronize()
+    finally:
+        B.lora_plan_destroy(p)
+    return ys
+
+
 @pytest.mark.parametrize("name,y0,small_max", [("tiny", "random", None), ("tiny", "zero", None),
                                                 ("tiny_dense", "random", None), ("tiny", "random", -1)])
 def test_tiny_all_elements(B, name, y0, small_max):
@@ -401,6 +422,36 @@ def test_resident_cache_matches_full_store(B, rank):
     finally:
         B.lora_server_destroy(cs)
         B.lora_server_destroy(full)
+
+
+@pytest.mark.parametrize("world,rank,ep,n_hot", [(2, 0, 0, 0), (2, 1, 0, 0), (3, 2, 0, 4), (2, 1, 1, 0), (3, 1, 1, 0)])
+def test_sharded_store_layouts_fake_world(B, monkeypatch, world, rank, ep, n_hot):
+    """The store of one rank of a sharded server (LORA_FAKE_WORLD test hook:
+    same placement, no communicator) for LoRA Data Parallel striping, with
+    replicated hot adapters, and expert parallel: rows of the units that rank
+    owns match the oracle, every other row is skipped (y untouched) and
+    flagged."""
+    monkeypatch.setenv("LORA_FAKE_WORLD", f"{world},{rank},{ep},{n_hot}")
+    cfg = _mid_cfg(T=500)
+    b = li.make_batch(cfg)
+    T = b.n_rows
+    s = U.make_server(B, cfg)
+    try:
+        src = np.full(T, rank)
+        own = orc.owner_of(b.adapter_ids, world, n_hot, src, b.expert_ids, bool(ep))
+        mine = own == rank
+        y0 = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        ys = _run_multi_unchecked(B, s, cfg, b, [0, 1])
+        assert B.lora_server_check(s) == (B.LORA_ERR_ID_OUT_OF_RANGE if np.any(own >= 0) and not np.all(mine | (own < 0)) else B.LORA_OK)
+        rows = np.flatnonzero(mine)
+        assert rows.size > 0
+        other = torch.from_numpy(np.flatnonzero(~mine)).to(U.DEV)
+        for i in range(2):
+            ref = oracle.apply_slot(cfg, i, b, rows=rows)
+            U.assert_parity(ys[i][torch.from_numpy(rows).to(U.DEV)], ref, f"fake world slot {i}")
+            assert torch.equal(ys[i][other], y0[i][other])
+    finally:
+        B.lora_server_destroy(s)
 
 
 def test_permutation_equivariance_bit_exact(B):

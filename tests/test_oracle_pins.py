@@ -310,8 +310,9 @@ def test_apply_slot_tiny_runs():
     assert y.shape == (64, 256) and np.isfinite(y).all()
 
 
-@pytest.mark.parametrize("world,n_hot", [(1, 0), (2, 0), (3, 2), (4, 5)])
-def test_shard_dispatch_pins(world, n_hot):
+@pytest.mark.parametrize("world,n_hot,ep", [(1, 0, False), (2, 0, False), (3, 2, False), (4, 5, False),
+                                            (2, 0, True), (3, 0, True)])
+def test_shard_dispatch_pins(world, n_hot, ep):
     """shard_dispatch / owner_of against a per-row brute force of the routing
     rule (R19) and its invariants: the exchanged rows and
     the rows kept in place partition every rank's valid rows, the count matrix
@@ -321,7 +322,7 @@ def test_shard_dispatch_pins(world, n_hot):
     cfg = li.Config("pin_shard", 13, (li.Slot("s", 64, 64, 4, 0),), 8, 12, 4, 2, 41, "fp32", no_lora_frac=0.1)
     b = li.make_batch(cfg)
     k = b.top_k
-    disp = orc.shard_dispatch(b, world, n_hot)
+    disp = orc.shard_dispatch(b, world, n_hot, ep)
     src = np.empty(b.n_rows, np.int64)
     for g in range(world):
         t0, t1 = (cfg.n_tokens * g) // world, (cfg.n_tokens * (g + 1)) // world
@@ -334,7 +335,10 @@ def test_shard_dispatch_pins(world, n_hot):
             if src[i] != s_ or b.adapter_ids[i] < 0:
                 continue
             a = int(b.adapter_ids[i])
-            o = s_ if a < n_hot else (a - n_hot) % world
+            if ep:
+                o = int(b.expert_ids[i]) % world
+            else:
+                o = s_ if a < n_hot else (a - n_hot) % world
             (exp_local if o == s_ else exp_recv)[o].append(i)
     for d in range(world):
         np.testing.assert_array_equal(disp[d]["rows"], np.array(exp_recv[d], np.int64))
@@ -347,7 +351,8 @@ def test_shard_dispatch_pins(world, n_hot):
     for s_ in range(world):
         n_valid_s = int(np.sum(valid & (src == s_)))
         assert counts[s_].sum() + len(disp[s_]["local"]) == n_valid_s
-    hot_moved = [i for d in range(world) for i in disp[d]["rows"] if b.adapter_ids[i] < n_hot]
-    assert hot_moved == []
+    if not ep:
+        hot_moved = [i for d in range(world) for i in disp[d]["rows"] if b.adapter_ids[i] < n_hot]
+        assert hot_moved == []
     if world == 1:
         assert len(disp[0]["rows"]) == 0

@@ -136,7 +136,7 @@ def test_sharded_host_logic_world2_gloo(tmp_path, n_hot):
     assert np.abs(y_sharded - y_ref).max() <= 1e-2 * np.abs(y_ref).max() + 1e-3
 
 
-def _p2p_worker(rank, world, port, out_dir, n_hot):
+def _p2p_worker(rank, world, port, out_dir, n_hot, ep=False):
     """The P2P transport's address maps (lora_shard_peer_rows, used by
     shard.cu) on emulated peer memory: every rank's send buffer (global row
     ids in send order) and delta buffer (global row ids in receive order) are
@@ -156,7 +156,7 @@ def _p2p_worker(rank, world, port, out_dir, n_hot):
         t0, t1 = orc.token_range(cfg.n_tokens, G, rank)
         rows = np.arange(t0 * k, t1 * k)
         a = batch.adapter_ids[rows]
-        own = orc.owner_of(a, G, n_hot, np.full(a.shape, rank))
+        own = orc.owner_of(a, G, n_hot, np.full(a.shape, rank), batch.expert_ids[rows], ep)
         send_rows = np.concatenate([rows[own == d] for d in range(G) if d != rank] + [np.zeros(0, np.int64)])
         counts = np.array([(own == d).sum() if d != rank else 0 for d in range(G)], np.int64)
         allc = [torch.zeros(G, dtype=torch.int64) for _ in range(G)]
@@ -176,7 +176,7 @@ def _p2p_worker(rank, world, port, out_dir, n_hot):
         peer_send = gather_padded(send_rows)
         # owner: received row r from source s is row r + rb_in[s] of s's send buffer
         recv = np.array([peer_send[s][r + rb_in[s]] for s in range(G) for r in range(ro[s], ro[s + 1])], np.int64)
-        disp = orc.shard_dispatch(batch, G, n_hot)[rank]
+        disp = orc.shard_dispatch(batch, G, n_hot, ep)[rank]
         np.testing.assert_array_equal(recv, disp["rows"])
         # owner's delta buffer holds its received rows in receive order
         peer_d = gather_padded(recv)
@@ -188,8 +188,8 @@ def _p2p_worker(rank, world, port, out_dir, n_hot):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n_hot", [(2, 0), (3, 0), (3, 2)])
-def test_p2p_row_maps_gloo(tmp_path, world, n_hot):
-    mp.spawn(_p2p_worker, args=(world, _free_port(), str(tmp_path), n_hot), nprocs=world, join=True)
+@pytest.mark.parametrize("world,n_hot,ep", [(2, 0, False), (3, 0, False), (3, 2, False), (2, 0, True)])
+def test_p2p_row_maps_gloo(tmp_path, world, n_hot, ep):
+    mp.spawn(_p2p_worker, args=(world, _free_port(), str(tmp_path), n_hot, ep), nprocs=world, join=True)
     tot = sum(int(np.load(tmp_path / f"ok{r}.npy")[0]) for r in range(world))
     assert tot > 0  # rows actually crossed ranks
