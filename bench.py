@@ -290,9 +290,26 @@ def run_ours(args, cfg, batch, slots):
         else:
             B.lora_apply_sharded(s, slots, x_list, ad, ex if E > 1 else None, ys, dt_code, T, stream)
 
+    run_step = step
+    graph = None
+    if args.graph and not sharded:
+        # the whole step (plan build + multi-slot apply, including the fork /
+        # join of the tcgen05 side stream) captured once, replayed each step
+        g_stream = torch.cuda.Stream()
+        g_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(g_stream):
+            step_on = lambda st: (B.lora_plan_build(s, plan, ad, ex if E > 1 else None, T, E, st),
+                                  B.lora_apply_plan_multi(s, plan, slots, x_list, ys, dt_code, st))
+            step_on(g_stream)  # warm the lazy allocations outside the capture
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=g_stream):
+                step_on(g_stream)
+        torch.cuda.current_stream().wait_stream(g_stream)
+        run_step = graph.replay
     torch.cuda.synchronize()
     for _ in range(args.warmup):
-        step()
+        run_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -305,7 +322,7 @@ def run_ours(args, cfg, batch, slots):
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            run_step()
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -438,6 +455,7 @@ def run_ours(args, cfg, batch, slots):
             "config": {"workload": cfg.name, "global_batch": cfg.n_tokens, "rows": T_glob, "slots": len(slots),
                        "rank": cfg.rank, "adapters": cfg.n_adapters,
                        "parallelism": f"adapter-sharded dp{world} (NCCL all-to-all)" if sharded else "single GPU",
+                       "cuda_graph": bool(graph is not None),
                        "n_replicated": n_rep if sharded else None,
                        "expert_parallel": ep_mode if sharded else None,
                        "placement_model_ms": rep_table,
@@ -475,6 +493,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n-replicated", type=int, default=-1,
                     help="sharded server: adapters [0, h) stored on every rank; -1 = cost-model choice")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch every step eagerly (default: one step captured in a CUDA graph, replayed)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the sharded server even at N=1 with every row sent through the NCCL exchange "
                          "(loopback; exercises the N>1 code path)")

@@ -454,6 +454,42 @@ def test_sharded_store_layouts_fake_world(B, monkeypatch, world, rank, ep, n_hot
         B.lora_server_destroy(s)
 
 
+def test_cuda_graph_replay_bit_exact(B):
+    """A step (plan build + multi-slot apply, including the fork/join of the
+    tcgen05 side stream) captured in a CUDA graph and replayed gives the
+    eager result bit for bit (bench.py times the replay)."""
+    cfg = _mid_cfg()
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        T = b.n_rows
+        y_eager = _run_multi(B, s, cfg, b, [0, 1])
+        ad, ex = U.ids_dev(b)
+        xs = [U.x_dev(B, cfg, i, T) for i in range(2)]
+        ys = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        y_init = [y.clone() for y in ys]
+        p = B.lora_plan_create(s, T)
+        g_stream = torch.cuda.Stream()
+        g_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(g_stream):
+            B.lora_plan_build(s, p, ad, ex, T, cfg.n_experts, g_stream)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=g_stream):
+                B.lora_plan_build(s, p, ad, ex, T, cfg.n_experts, g_stream)
+                B.lora_apply_plan_multi(s, p, [0, 1], xs, ys, B.LORA_BF16, g_stream)
+        torch.cuda.current_stream().wait_stream(g_stream)
+        for y, y0 in zip(ys, y_init):
+            y.copy_(y0)
+        graph.replay()
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(ys[i], y_eager[i])
+        B.lora_plan_destroy(p)
+    finally:
+        B.lora_server_destroy(s)
+
+
 def test_permutation_equivariance_bit_exact(B):
     cfg = _mid_cfg()
     b = li.make_batch(cfg)
