@@ -75,7 +75,6 @@ struct PlanDev {
   int4* tiles;       // [max_rows]   tcgen05 tiles    {row_begin, nrows, key, seg}
   float* vpart;      // shrink partial sums, per slot region [n_kc][max_rows][r]
   uint16_t* vbf;     // tcgen05 path: complete v rounded to bf16, per slot region [max_rows][r]
-  int* tc_cnt;       // tcgen05 shrink arrival counters [kMaxTasks][max_rows] (self-resetting)
   unsigned long long* wctr;  // [kWorkSlots] dynamic item counters of the persistent kernels (self-resetting)
   unsigned int* wdone;       // [kWorkSlots] finished-CTA counters
   int max_rows;

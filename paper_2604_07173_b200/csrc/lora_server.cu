@@ -530,7 +530,6 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
             cudaMalloc(&d.tiles, sizeof(int4) * max_rows) == cudaSuccess &&
             cudaMalloc(&d.vpart, sizeof(float) * (size_t)s->total_kc * max_rows * s->r) == cudaSuccess &&
             cudaMalloc(&d.vbf, sizeof(uint16_t) * s->slots.size() * (size_t)max_rows * s->r) == cudaSuccess &&
-            cudaMalloc(&d.tc_cnt, sizeof(int) * (size_t)kMaxTasks * max_rows) == cudaSuccess &&
             cudaMalloc(&d.wctr, sizeof(unsigned long long) * kWorkSlots) == cudaSuccess &&
             cudaMalloc(&d.wdone, sizeof(unsigned int) * kWorkSlots) == cudaSuccess;
   if (!ok) {
@@ -539,7 +538,6 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
     return fail(s, LORA_ERR_OOM, "plan allocation failed");
   }
   cudaMemset(d.counts, 0, sizeof(int32_t) * kCntWords);
-  cudaMemset(d.tc_cnt, 0, sizeof(int) * (size_t)kMaxTasks * max_rows);
   cudaMemset(d.wctr, 0, sizeof(unsigned long long) * kWorkSlots);
   cudaMemset(d.wdone, 0, sizeof(unsigned int) * kWorkSlots);
   cudaMemset(d.seg_off, 0, sizeof(int32_t) * (max_rows + 1));
@@ -557,7 +555,6 @@ void plan_destroy_impl(lora_plan* p) {
   cudaFree(p->dev.tiles);
   cudaFree(p->dev.vpart);
   cudaFree(p->dev.vbf);
-  cudaFree(p->dev.tc_cnt);
   cudaFree(p->dev.wctr);
   cudaFree(p->dev.wdone);
   delete p;
