@@ -236,6 +236,22 @@ lora_status_t lora_nccl_unique_id(void *out128);
 lora_status_t lora_server_create_sharded(const lora_config_t *cfg, int32_t rank, int32_t world,
                                          const void *nccl_unique_id, lora_server_t **out);
 
+/* Host control plane for a sharded server without NCCL: a blocking host
+ * all-gather supplied by the caller (e.g. an MPI / gloo / socket collective).
+ * Every rank contributes `bytes` bytes from `send`; `recv` receives
+ * world * bytes, rank-major.  Return 0 on success. */
+typedef int (*lora_host_allgather_fn)(void *ctx, const void *send, void *recv, int64_t bytes);
+
+/* As lora_server_create_sharded, with the control plane (counts exchange,
+ * IPC-handle exchange, the two barriers of an apply) on the caller's host
+ * all-gather instead of NCCL; the data path is the peer-to-peer transport
+ * (registered buffers mapped with CUDA IPC; peers on the same or other GPUs).
+ * Each barrier synchronises the stream on the host (two extra host syncs per
+ * apply).  world <= 8.  Used by the multi-process tests on one GPU. */
+lora_status_t lora_server_create_sharded_host(const lora_config_t *cfg, int32_t rank, int32_t world,
+                                              lora_host_allgather_fn allgather, void *ctx,
+                                              lora_server_t **out);
+
 /* Collective apply on a sharded server: every rank passes its OWN rows
  * (T local rows, device pointers, same slot list on every rank).  Rows whose
  * adapter this rank stores (its own or a replicated one) are applied in place;

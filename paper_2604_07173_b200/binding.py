@@ -63,6 +63,7 @@ SIGNATURES = {
     "lora_apply_multi_host": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
     "lora_nccl_unique_id": (ctypes.c_int, [_vp]),
     "lora_server_create_sharded": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _pp]),
+    "lora_server_create_sharded_host": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _vp, _pp]),
     "lora_apply_sharded": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
     "lora_shard_peer_rows": (ctypes.c_int, [_pi64, _i32, _i32, _pi64, _pi64]),
     "lora_shard_layout": (ctypes.c_int, [_pi64, _i32, _i32, _pi64, _pi64]),
@@ -157,6 +158,7 @@ def lora_server_fill_synthetic(s: int, seed: int, stream=None):
 
 def lora_server_destroy(s: int):
     _check(lib.lora_server_destroy(s))
+    _host_callbacks.pop(s, None)
 
 
 def lora_server_set_small_seg_max(s: int, n: int):
@@ -245,6 +247,30 @@ def lora_server_create_sharded(cfg: LoraConfig, rank: int, world: int, unique_id
     out = ctypes.c_void_p()
     idb = ctypes.create_string_buffer(bytes(unique_id), 128)
     _check(lib.lora_server_create_sharded(ctypes.byref(cfg), rank, world, idb, ctypes.byref(out)))
+    return out.value
+
+
+# host control plane: int (*)(void* ctx, const void* send, void* recv, int64_t bytes)
+HOST_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+_host_callbacks = {}  # server handle -> ctypes callback (kept alive while the server lives)
+
+
+def lora_server_create_sharded_host(cfg: LoraConfig, rank: int, world: int, allgather) -> int:
+    """allgather(data: bytes) -> bytes of world * len(data), rank-major (a blocking host collective)."""
+    def cb(ctx, send, recv, nbytes):
+        try:
+            out = allgather(ctypes.string_at(send, nbytes))
+            if len(out) != world * nbytes:
+                return 1
+            ctypes.memmove(recv, out, len(out))
+            return 0
+        except Exception:  # never raise across the C ABI
+            return 1
+    fn = HOST_ALLGATHER(cb)
+    out = ctypes.c_void_p()
+    _check(lib.lora_server_create_sharded_host(ctypes.byref(cfg), rank, world, ctypes.cast(fn, ctypes.c_void_p), None,
+                                               ctypes.byref(out)))
+    _host_callbacks[out.value] = fn
     return out.value
 
 

@@ -293,7 +293,47 @@ struct ShardState {
   size_t send_cap = 0, d_cap = 0;
   std::vector<char*> peer_send, peer_d;  // index = rank (own rank: the local pointers)
   int* d_bar = nullptr;                   // barrier word (NCCL all-reduce)
+  // host control plane (lora_server_create_sharded_host): no NCCL at all
+  lora_host_allgather_fn host_ag = nullptr;
+  void* host_ctx = nullptr;
 };
+
+// Control plane.  Blocking all-gather of small host blobs (IPC handles,
+// agreement flags): the caller's host collective, or NCCL through a device
+// scratch buffer.
+static lora_status_t ctl_allgather(lora_server* s, const void* send_h, void* recv_h, size_t bytes, cudaStream_t st) {
+  ShardState* sh = s->shard;
+  const int G = s->world, me = s->shard_rank;
+  if (sh->host_ag) {
+    cudaStreamSynchronize(st);
+    if (sh->host_ag(sh->host_ctx, send_h, recv_h, (int64_t)bytes) != 0)
+      return fail(s, LORA_ERR_NCCL, "host all-gather callback failed");
+    return LORA_OK;
+  }
+  NcclApi& api = nccl();
+  char* d = nullptr;
+  if (cudaMalloc(&d, bytes * G) != cudaSuccess) return fail(s, LORA_ERR_OOM, "control buffer");
+  cudaMemcpy(d + bytes * me, send_h, bytes, cudaMemcpyHostToDevice);
+  const ncclResult_t r = api.AllGather(d + bytes * me, d, bytes, ncclUint8, sh->comm, st);
+  cudaStreamSynchronize(st);
+  if (r == ncclSuccess) cudaMemcpy(recv_h, d, bytes * G, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return r == ncclSuccess ? LORA_OK : fail(s, LORA_ERR_NCCL, std::string("all-gather: ") + api.GetErrorString(r));
+}
+
+// Barrier in the order of `st`: an NCCL all-reduce of one word (no host
+// sync), or -- host control plane -- a stream synchronize and a host barrier.
+static lora_status_t ctl_barrier(lora_server* s, cudaStream_t st) {
+  ShardState* sh = s->shard;
+  if (sh->host_ag) {
+    char b = 0;
+    std::vector<char> all(s->world);
+    return ctl_allgather(s, &b, all.data(), 1, st);
+  }
+  NcclApi& api = nccl();
+  const ncclResult_t r = api.AllReduce(sh->d_bar, sh->d_bar, 1, ncclInt32, ncclSum, sh->comm, st);
+  return r == ncclSuccess ? LORA_OK : fail(s, LORA_ERR_NCCL, std::string("barrier: ") + api.GetErrorString(r));
+}
 
 // Release the peer mappings and the registered buffers.
 static void p2p_release(ShardState* sh, int me) {
@@ -370,20 +410,41 @@ extern "C" lora_status_t lora_nccl_unique_id(void* out128) {
   return LORA_OK;
 }
 
+static lora_status_t create_sharded_impl(const lora_config_t* cfg, int32_t rank, int32_t world,
+                                         const void* nccl_unique_id, lora_host_allgather_fn host_ag, void* host_ctx,
+                                         lora_server_t** out);
+
 extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, int32_t rank, int32_t world,
                                                     const void* nccl_unique_id, lora_server_t** out) {
-  if (!cfg || !out || !nccl_unique_id || world < 1 || rank < 0 || rank >= world)
+  if (!nccl_unique_id) return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded: NULL unique id");
+  return create_sharded_impl(cfg, rank, world, nccl_unique_id, nullptr, nullptr, out);
+}
+
+extern "C" lora_status_t lora_server_create_sharded_host(const lora_config_t* cfg, int32_t rank, int32_t world,
+                                                         lora_host_allgather_fn allgather, void* ctx,
+                                                         lora_server_t** out) {
+  if (!allgather) return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded_host: NULL all-gather");
+  if (world > kMaxWorld) return fail(nullptr, LORA_ERR_UNSUPPORTED, "host control plane: world > 8");
+  return create_sharded_impl(cfg, rank, world, nullptr, allgather, ctx, out);
+}
+
+static lora_status_t create_sharded_impl(const lora_config_t* cfg, int32_t rank, int32_t world,
+                                         const void* nccl_unique_id, lora_host_allgather_fn host_ag, void* host_ctx,
+                                         lora_server_t** out) {
+  if (!cfg || !out || world < 1 || rank < 0 || rank >= world)
     return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded: bad argument");
   if ((long long)cfg->max_rows * world > kMaxPlanRows)
     return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows * world must be <= 16384 (owner-side plan capacity)");
   if (cfg->n_replicated < 0) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_replicated < 0");
   NcclApi& api = nccl();
-  if (!api.ok) return fail(nullptr, LORA_ERR_NCCL, api.err);
+  if (!host_ag && !api.ok) return fail(nullptr, LORA_ERR_NCCL, api.err);
   lora_status_t st = create_common_sharded(cfg, world, rank, out, cfg->n_replicated, cfg->expert_parallel);
   if (st != LORA_OK) return st;
   lora_server* s = *out;
   s->shard = new ShardState();
   ShardState* sh = s->shard;
+  sh->host_ag = host_ag;
+  sh->host_ctx = host_ctx;
   const char* f32 = std::getenv("LORA_SHARD_FP32");
   sh->fp32_return = f32 && f32[0] && std::strcmp(f32, "0") != 0;
   const char* lb = std::getenv("LORA_SHARD_LOOPBACK");
@@ -391,8 +452,7 @@ extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, in
   const char* tr = std::getenv("LORA_SHARD_TRANSPORT");
   sh->p2p = !(tr && std::strcmp(tr, "nccl") == 0);
   if (world > kMaxWorld) sh->p2p = false;
-  ncclUniqueId id;
-  std::memcpy(&id, nccl_unique_id, 128);
+  if (host_ag) sh->p2p = true;  // the only transport without NCCL
   cudaSetDevice(s->device);
   bool ok = cudaStreamCreateWithFlags(&sh->cs, cudaStreamNonBlocking) == cudaSuccess;
   for (auto& e : sh->ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
@@ -407,12 +467,16 @@ extern "C" lora_status_t lora_server_create_sharded(const lora_config_t* cfg, in
     *out = nullptr;
     return fail(nullptr, LORA_ERR_CUDA, "barrier word allocation failed");
   }
-  ncclResult_t r = api.CommInitRank(&sh->comm, world, id, rank);
-  if (r != ncclSuccess) {
-    std::string m = std::string("ncclCommInitRank: ") + api.GetErrorString(r);
-    lora_server_destroy(s);
-    *out = nullptr;
-    return fail(nullptr, LORA_ERR_NCCL, m);
+  if (!host_ag) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, 128);
+    ncclResult_t r = api.CommInitRank(&sh->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      std::string m = std::string("ncclCommInitRank: ") + api.GetErrorString(r);
+      lora_server_destroy(s);
+      *out = nullptr;
+      return fail(nullptr, LORA_ERR_NCCL, m);
+    }
   }
   st = plan_create_impl(s, cfg->max_rows * world, &sh->plan);
   if (st == LORA_OK) st = plan_create_impl(s, cfg->max_rows, &sh->local_plan);
@@ -457,16 +521,9 @@ static lora_status_t p2p_register(lora_server* s, size_t need_send, size_t need_
       cudaIpcGetMemHandle(&h[2 * me + 1], sh->dbuf) != cudaSuccess)
     return fail(s, LORA_ERR_CUDA, "cudaIpcGetMemHandle failed");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  char* dh = nullptr;
-  if (cudaMalloc(&dh, 128 * G + 4) != cudaSuccess) return fail(s, LORA_ERR_OOM, "handle buffer");
-  cudaMemcpy(dh + 128 * me, &h[2 * me], 128, cudaMemcpyHostToDevice);
-  ncclResult_t r = api.AllGather(dh + 128 * me, dh, 128, ncclUint8, sh->comm, st);
-  if (r != ncclSuccess) {
-    cudaFree(dh);
-    return fail(s, LORA_ERR_NCCL, std::string("handle all-gather: ") + api.GetErrorString(r));
-  }
-  cudaStreamSynchronize(st);
-  cudaMemcpy(h.data(), dh, 128 * G, cudaMemcpyDeviceToHost);
+  std::vector<cudaIpcMemHandle_t> mine(h.begin() + 2 * me, h.begin() + 2 * me + 2);
+  lora_status_t rc = ctl_allgather(s, mine.data(), h.data(), 128, st);
+  if (rc != LORA_OK) return rc;
   int ok = 1;
   for (int p = 0; p < G; ++p) {
     if (p == me) continue;
@@ -481,14 +538,13 @@ static lora_status_t p2p_register(lora_server* s, size_t need_send, size_t need_
     sh->peer_d[p] = static_cast<char*>(b);
   }
   // every rank must agree on the transport
-  int* dok = reinterpret_cast<int*>(dh + 128 * G);
-  cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
-  r = api.AllReduce(dok, dok, 1, ncclInt32, ncclMin, sh->comm, st);
-  cudaStreamSynchronize(st);
-  cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
-  cudaFree(dh);
-  if (r != ncclSuccess || !ok) {
+  std::vector<int> oks(G, 0);
+  rc = ctl_allgather(s, &ok, oks.data(), sizeof(int), st);
+  if (rc != LORA_OK) return rc;
+  for (int v : oks) ok = ok && v;
+  if (!ok) {
     p2p_release(sh, me);
+    if (sh->host_ag) return fail(s, LORA_ERR_UNSUPPORTED, "peer mapping failed and the host control plane has no fallback");
     sh->p2p = false;  // NCCL send/recv from now on, on every rank
   }
   return LORA_OK;
@@ -588,10 +644,17 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   }
   CKS(cudaGetLastError());
   // 2. counts exchange (all-gather) + the one host sync
-  CKN(api.AllGather(d_counts, d_counts + G, G, ncclInt32, sh->comm, st));
   std::vector<int32_t> cnt(G * G);
-  CKS(cudaMemcpyAsync(cnt.data(), d_counts + G, sizeof(int32_t) * G * G, cudaMemcpyDeviceToHost, st));
-  CKS(cudaStreamSynchronize(st));
+  if (sh->host_ag) {
+    std::vector<int32_t> mine(G);
+    CKS(cudaMemcpyAsync(mine.data(), d_counts, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
+    const lora_status_t cr = ctl_allgather(s, mine.data(), cnt.data(), sizeof(int32_t) * G, st);
+    if (cr != LORA_OK) return cr;
+  } else {
+    CKN(api.AllGather(d_counts, d_counts + G, G, ncclInt32, sh->comm, st));
+    CKS(cudaMemcpyAsync(cnt.data(), d_counts + G, sizeof(int32_t) * G * G, cudaMemcpyDeviceToHost, st));
+    CKS(cudaStreamSynchronize(st));
+  }
   std::vector<int64_t> c64(cnt.begin(), cnt.end()), so(G + 1), ro(G + 1);
   lora_status_t lr = lora_shard_layout(c64.data(), G, me, so.data(), ro.data());
   if (lr != LORA_OK) return fail(s, lr, "count exchange produced an invalid matrix");
@@ -665,8 +728,10 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
     }
     if (p2p) {
       // every source's send buffer complete before any owner reads it
-      CKN(api.AllReduce(sh->d_bar, sh->d_bar, 1, ncclInt32, ncclSum, sh->comm, cs));
+      const lora_status_t br = ctl_barrier(s, cs);
+      if (br != LORA_OK) return br;
     } else {
+      if (sh->host_ag) return fail(s, LORA_ERR_UNSUPPORTED, "host control plane needs the peer-to-peer transport");
     CKN(api.GroupStart());
     for (int p = 0; p < G; ++p) {
       const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
@@ -734,7 +799,8 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   }
   if (p2p) {
     // every owner's deltas complete before any source reads them
-    CKN(api.AllReduce(sh->d_bar, sh->d_bar, 1, ncclInt32, ncclSum, sh->comm, st));
+    const lora_status_t br = ctl_barrier(s, st);
+    if (br != LORA_OK) return br;
     if (n_send > 0) {
       for (int i = 0; i < n; ++i) {
         const int ho = s->slots[slots[i]].h_out;
