@@ -145,9 +145,11 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
                                 int* scan_tmp) {
   const int tid = threadIdx.x;
   int bad = 0, nv = 0;
+  // composites in row order; rows read coalesced (row r*1024 + tid) -- the
+  // passes below read the array by index, not by thread
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const int i = tid * EPT + r;
+    const int i = r * kSegThreads + tid;
     int key = -1;
     if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad, cache);
     nv += key >= 0;
@@ -155,7 +157,7 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
   }
   if (bad) atomicOr(err_flag, 1);
   int total;
-  block_exclusive_scan(nv, scan_tmp, &total);
+  block_exclusive_scan(nv, scan_tmp, &total);  // its barriers also publish A
   *n_valid_out = total;
   uint32_t* in = A;
   uint32_t* out = B;
