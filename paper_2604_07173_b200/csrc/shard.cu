@@ -750,6 +750,15 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
     }
     CKN(api.GroupEnd());
     }
+    // owner side, still on the communication stream: the received rows' ids
+    // (P2P: pulled from the sources' send buffers) and their plan -- built
+    // while the in-place apply runs on the caller's stream
+    if (p2p && n_recv > 0) {
+      pull_ids_kernel<<<grid_of(n_recv), 256, 0, cs>>>(pr_in, s->max_rows, d_ids_recv, Rmax, n_recv);
+      CKS(cudaGetLastError());
+    }
+    const lora_status_t pr = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, cs);
+    if (pr != LORA_OK) return pr;
     CKS(cudaEventRecord(sh->ev[1], cs));
   }
 
@@ -767,12 +776,6 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
 
   // 5. received rows: owner-side plan + delta-mode apply
   CKS(cudaStreamWaitEvent(st, sh->ev[1], 0));
-  if (p2p && n_recv > 0) {
-    pull_ids_kernel<<<grid_of(n_recv), 256, 0, st>>>(pr_in, s->max_rows, d_ids_recv, Rmax, n_recv);
-    CKS(cudaGetLastError());
-  }
-  rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, st);
-  if (rc != LORA_OK) return rc;
   if (n_recv > 0) {
     std::vector<const void*> xs(n);
     std::vector<void*> ds(n);
