@@ -9,16 +9,18 @@
 // and their rows never leave their rank.
 //
 // One collective apply (every rank, same slot list):
-//   1. classify the local rows: owner(a) == this rank (replicated or own
-//      adapter) -> processed in place; the rest bucketed by owner (stable)
-//   2. all-gather of the G send counts -> full G x G matrix; ONE D2H sync
-//   3. (comm stream) pack + grouped ncclSend/ncclRecv of x rows and ids
-//      (receive order: source rank ascending, then the source's local order),
-//      overlapped with 4. on the caller's stream
-//   4. in-place rows: plan + multi-slot apply straight into the caller's y
-//   5. received rows: plan + apply in delta mode (delta stored, not added)
-//   6. (comm stream) reverse grouped send/recv of the deltas
-//   7. y[origin row] = round(y + delta)
+//   1. classify the local rows: owner == this rank (replicated or own units)
+//      -> processed in place; the rest bucketed by owner (stable)
+//   2. all-gather of the G send counts -> full G x G matrix, read back
+//      asynchronously; the in-place plan + apply are enqueued before the host
+//      waits for it (the GPU works through the one host round trip)
+//   3. (comm stream) pack of x rows and ids into the send buffer, transport
+//      (P2P: a barrier; NCCL: grouped send/recv), then the owner side's ids
+//      and plan -- all overlapped with the in-place apply
+//   4. received rows: delta-mode apply (P2P: the shrink reads the x rows from
+//      the sources' send buffers over NVLink)
+//   5. deltas back (P2P: barrier, then each source pulls its deltas fused with
+//      the add; NCCL: reverse send/recv, then y[origin row] = round(y + delta))
 // Deltas travel as fp32 when y is fp32 (sharded == unsharded bit for bit,
 // DESIGN.md R18) and as bf16 when y is bf16 (half the NVLink bytes, one extra
 // rounding of the delta: DESIGN.md R19), unless LORA_SHARD_FP32=1.
@@ -296,6 +298,7 @@ struct ShardState {
   // host control plane (lora_server_create_sharded_host): no NCCL at all
   lora_host_allgather_fn host_ag = nullptr;
   void* host_ctx = nullptr;
+  int32_t* h_cnt = nullptr;  // pinned [world][world] counts (async read-back)
 };
 
 // Control plane.  Blocking all-gather of small host blobs (IPC handles,
@@ -355,6 +358,7 @@ void lora_shard_free(lora_server* s) {
   ShardState* sh = s->shard;
   p2p_release(sh, s->shard_rank);
   cudaFree(sh->d_bar);
+  if (sh->h_cnt) cudaFreeHost(sh->h_cnt);
   if (sh->comm && nccl().ok) nccl().CommDestroy(sh->comm);
   cudaFree(sh->buf);
   if (sh->plan) plan_destroy_impl(sh->plan);
@@ -462,6 +466,7 @@ static lora_status_t create_sharded_impl(const lora_config_t* cfg, int32_t rank,
     return fail(nullptr, LORA_ERR_CUDA, "stream / event creation failed");
   }
   ok = ok && cudaMalloc(&sh->d_bar, sizeof(int)) == cudaSuccess && cudaMemset(sh->d_bar, 0, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMallocHost(&sh->h_cnt, sizeof(int32_t) * world * world) == cudaSuccess;
   if (!ok) {
     lora_server_destroy(s);
     *out = nullptr;
@@ -643,17 +648,31 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
     CKS(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * G, st));
   }
   CKS(cudaGetLastError());
-  // 2. counts exchange (all-gather) + the one host sync
+  // 2. counts exchange (all-gather) + the one host wait.  NCCL control plane:
+  //    the matrix comes back asynchronously into pinned memory; the in-place
+  //    rows' plan and apply are enqueued before the host waits for it, so the
+  //    GPU keeps working through the host round trip.
   std::vector<int32_t> cnt(G * G);
+  if (!sh->host_ag) {
+    CKN(api.AllGather(d_counts, d_counts + G, G, ncclInt32, sh->comm, st));
+    CKS(cudaMemcpyAsync(sh->h_cnt, d_counts + G, sizeof(int32_t) * G * G, cudaMemcpyDeviceToHost, st));
+  }
+  CKS(cudaEventRecord(sh->ev[0], st));  // bucket outputs + counts ready (the pack waits on this)
+  // 3. rows this rank stores the adapter of: applied in place (independent of the counts)
+  lora_status_t rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
+  if (rc != LORA_OK) return rc;
+  if (T > 0) {
+    rc = apply_multi_impl(s, sh->local_plan, n, slots, x, y, y_dtype, st);
+    if (rc != LORA_OK) return rc;
+  }
   if (sh->host_ag) {
     std::vector<int32_t> mine(G);
     CKS(cudaMemcpyAsync(mine.data(), d_counts, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
     const lora_status_t cr = ctl_allgather(s, mine.data(), cnt.data(), sizeof(int32_t) * G, st);
     if (cr != LORA_OK) return cr;
   } else {
-    CKN(api.AllGather(d_counts, d_counts + G, G, ncclInt32, sh->comm, st));
-    CKS(cudaMemcpyAsync(cnt.data(), d_counts + G, sizeof(int32_t) * G * G, cudaMemcpyDeviceToHost, st));
-    CKS(cudaStreamSynchronize(st));
+    CKS(cudaEventSynchronize(sh->ev[0]));
+    std::memcpy(cnt.data(), sh->h_cnt, sizeof(int32_t) * G * G);
   }
   std::vector<int64_t> c64(cnt.begin(), cnt.end()), so(G + 1), ro(G + 1);
   lora_status_t lr = lora_shard_layout(c64.data(), G, me, so.data(), ro.data());
@@ -701,7 +720,6 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
 
   // 3. (comm stream) pack + dispatch, overlapped with the in-place apply
   if (exchange) {
-    CKS(cudaEventRecord(sh->ev[0], st));
     CKS(cudaStreamWaitEvent(cs, sh->ev[0], 0));
     // P2P: pack straight into the registered send buffer the owners read from
     int32_t* ids_dst = p2p ? static_cast<int32_t*>(sh->sendbuf) : d_ids_send;
@@ -762,13 +780,6 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
     CKS(cudaEventRecord(sh->ev[1], cs));
   }
 
-  // 4. rows this rank stores the adapter of: applied in place
-  lora_status_t rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
-  if (rc != LORA_OK) return rc;
-  if (T > 0) {
-    rc = apply_multi_impl(s, sh->local_plan, n, slots, x, y, y_dtype, st);
-    if (rc != LORA_OK) return rc;
-  }
   if (!exchange) {
     CKS(cudaEventRecord(sh->ev[3], st));
     return LORA_OK;
