@@ -438,6 +438,8 @@ def run_ours(args, cfg, batch, slots):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom,
                     "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
+                    "peak_note": "MEASURED_PEAKS hbm_gbs is a copy (read + write) figure; a read-dominated "
+                                 "stream can exceed it (tools/bw_probe.cu: 7.35 TB/s bulk-copy read stream)",
                     "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS,
                     "timing": f"CUDA events on the launching stream, {n_prof} steps right after the timed region "
                               "with the kernels serialised (lora_server_set_concurrent(0))"}
