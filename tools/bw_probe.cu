@@ -1,6 +1,6 @@
 // bw_probe.cu -- microbenchmark of the 1-D TMA bulk-copy streaming pipeline
 // used by the CUDA-core kernels (stage size / depth / consumer work), vs a
-// plain vectorised LDG read.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
+// plain vectorised LDG read.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Ipaper_2604_07173_b200/csrc
 //   -I../paper_2604_07173_b200/csrc bw_probe.cu -o bw_probe
 #include <cstdio>
 #include <vector>
