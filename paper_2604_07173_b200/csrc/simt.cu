@@ -26,6 +26,9 @@
 // Work items (device-side counts, no host sync):
 //   shrink item = (slot task, row group)            -> vpart[0][row][0:r]  (v = x A_u)
 //   expand item = (slot task, c-chunk of CI, group) -> y[perm[row]][c-chunk] += s_a v B_u
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -85,6 +88,18 @@ struct SimtCfg {
   // stage s+YD, whose first stage needs stage s+YD-NSTE released: YD <= NSTE.
   static_assert(YD <= NSTE, "y look-ahead deeper than the B pipeline");
   static_assert(S_STAGE % 1024 == 0 && E_STAGE % 1024 == 0, "stage alignment");
+  // staged-tile expand (r <= 16, simt_expand_tile_kernel): the y tile of a
+  // stage travels with its B rows and v rows in one stage buffer, loaded by
+  // the producer's bulk copies (one per group row), so y is prefetched as
+  // deep as B.  Stage = B | v (1 KB aligned) | y tile [GR][SC_MAX] bf16.
+  static constexpr int TV_OFF = B_STAGE;
+  static constexpr int TY_OFF = B_STAGE + 1024 * ((V_BYTES + 1023) / 1024);
+  static constexpr int T_STAGE = TY_OFF + Y_SLOT;
+  static constexpr int T_FIXED = 1024 + 2 * 16 * 8 + 3 * kQD * 8 + kQD * 80;
+  static constexpr int TNST_RAW = (112 * 1024 - T_FIXED) / T_STAGE;
+  static constexpr int TNST = TNST_RAW > 8 ? 8 : (TNST_RAW < 2 ? 2 : TNST_RAW);
+  static constexpr int TILE_SMEM = 1024 + TNST * T_STAGE + 2 * TNST * 8 + 3 * kQD * 8 + kQD * 80;
+  static_assert(T_STAGE % 1024 == 0 && TILE_SMEM <= 112 * 1024, "tile stage layout");
   static_assert(SHRINK_SMEM <= 112 * 1024 && EXPAND_SMEM <= 112 * 1024, "two CTAs per SM");
 };
 
@@ -824,6 +839,196 @@ __device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, uin
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// staged-tile expand (r <= 16).  At small r a stage carries few B bytes (16 KB
+// at r = 16) against up to 8 KB of y read + 8 KB written, so the y latency
+// cannot hide behind a consumer-issued look-ahead of a few short stages.  Here
+// the producer lane bulk-copies each group row's y chunk into the stage buffer
+// next to the B rows and the v rows (one mbarrier transaction for all), so y
+// is in flight exactly as deep as B.  Consumers compute the stage into the
+// tile (s_a * v B + y, rounded once), then -- after one named barrier -- store
+// the tile with coalesced 16-byte stores and release the stage.
+// ---------------------------------------------------------------------------
+template <int R, int M>
+__device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args, uint8_t* smem, uint64_t* full,
+                                                           uint64_t* empty, WorkQueue<kQD>& wq,
+                                                           const ExpandRec* recs) {
+  using C = SimtCfg<R>;
+  constexpr bool TILE = M == kOutBf16Acc || M == kOutBf16Store;
+  constexpr int pitch = C::SC_MAX * 2;
+  const int lane = lane_id();
+  const int ct = threadIdx.x;
+  // store pass mapping: 16-byte chunk ch of rows rsub, rsub + 4, ... (cpr <= 64)
+  const int rsub = ct >> 6, sch = ct & 63;
+  static_assert(C::SC_MAX / 8 <= 64 && C::NCT == 256, "store pass mapping");
+  int stage = 0;
+  uint32_t phase = 0;
+  QueuePos qp;
+  for (;;) {
+    mbar_wait(&wq.full[qp.slot], qp.phase);
+    const ExpandRec& rc = recs[qp.slot];
+    if (rc.it < 0) break;
+    const SlotTask& t = args.t[rc.task];
+    const int nr = rc.g.y;
+    ExpandPos p;
+    p.it = rc.it;
+    p.sc = t.SC;
+    p.rows = nr;
+    p.h_out = t.h_out;
+    p.y = t.y;
+    p.s_a = rc.s_a;
+    const uint32_t rows = smem_u32(rc.rows);
+    const int n_st = t.CI / t.SC;
+    for (int st = 0; st < n_st; ++st) {
+      p.st = st;
+      p.c0 = (long long)rc.ci * t.CI + (long long)st * t.SC;
+      mbar_wait(&full[stage], phase);
+      const uint32_t b_s = smem_u32(smem + stage * C::T_STAGE);
+      const uint32_t v_s = b_s + C::TV_OFF;
+      const uint32_t yt = b_s + C::TY_OFF;
+      switch (nr) {
+        case 1: expand_stage<R, 1, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+        case 2: expand_stage<R, 2, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+        case 3: expand_stage<R, 3, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+        case 4: expand_stage<R, 4, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+        case 5: expand_stage<R, 5, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+        case 6: expand_stage<R, 6, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+        case 7: expand_stage<R, 7, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+        default: expand_stage<R, 8, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
+      }
+      if constexpr (TILE) {
+        named_bar_sync(1, C::NCT);  // the whole tile is final
+        if (sch < (p.sc >> 3)) {
+          uint16_t* yb = static_cast<uint16_t*>(p.y) + p.c0 + sch * 8;
+          for (int r = rsub; r < nr; r += 4) {
+            const uint4 v = lds128(yt + r * pitch + sch * 16);
+            *reinterpret_cast<uint4*>(yb + (long long)rc.rows[r] * p.h_out) = v;
+          }
+        }
+        fence_proxy_async_smem();  // the tile is refilled by bulk copies after the release
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == C::TNST) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&wq.empty[qp.slot]);
+    qp.advance(kQD);
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
+    simt_expand_tile_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
+  using C = SimtCfg<R>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::TNST * C::T_STAGE);
+  uint64_t* empty = full + C::TNST;
+  WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::TNST), empty + C::TNST + kQD,
+                    empty + C::TNST + 2 * kQD};
+  ExpandRec* recs = reinterpret_cast<ExpandRec*>(empty + C::TNST + 3 * kQD);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::TNST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NWC);
+    }
+    wq.init(C::NWC);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int warp = warp_id(), lane = lane_id();
+  if (warp == C::NWC) {
+    // ===================== producer: resolve items; B rows, v rows, y chunks =====================
+    if (lane == 0) {
+      const int n_groups = pd.counts[kCntGroups];
+      const long long n_items = (long long)n_groups * args.total_ci;
+      const bool load_y = args.y_store == 0 && !args.y_fp32;
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      QueuePos qp;
+      unsigned long long* ctr = pd.wctr + kWqSimtExpand;
+      bool shrink_done = false;
+      for (;;) {
+        long long it = (long long)atomicAdd(ctr, 1ull);
+        if (it >= n_items) it = -1;
+        mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
+        ExpandRec& rc = recs[qp.slot];
+        if (it < 0) {
+          rc.it = -1;
+          mbar_arrive(&wq.full[qp.slot]);
+          break;
+        }
+        const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
+        const int ti = find_task_ci(args, cig);
+        const SlotTask& t = args.t[ti];
+        const int ci = cig - t.ci_base;
+        const int4 g = pd.groups[gi];
+        const long long unit = store_unit(g.z, t.E, args.pl, args.cache);
+        const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
+        const float* vsrc = pd.vpart + t.vpart_off + (long long)g.x * R;
+        const int n_st = t.CI / t.SC;
+        const uint32_t bytes = (uint32_t)t.SC * R * 2, vbytes = (uint32_t)g.y * R * 4;
+        const uint32_t ybytes = load_y ? (uint32_t)t.SC * 2 : 0u;
+        int rows[C::GR];
+#pragma unroll
+        for (int r = 0; r < C::GR; ++r) rows[r] = r < g.y ? __ldg(pd.perm + g.x + r) : 0;
+        const uint16_t* ybase = static_cast<const uint16_t*>(t.y) + (long long)ci * t.CI;
+        for (int st = 0; st < n_st; ++st) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sb = smem + stage * C::T_STAGE;
+          mbar_arrive_expect_tx(&full[stage], bytes + vbytes + ybytes * g.y);
+          bulk_g2s_hint(sb, bbase + (long long)st * t.SC * R, bytes, &full[stage], pol);
+          if (!shrink_done) {
+            pdl_wait();  // v rows come from the shrink (the B rows above do not)
+            shrink_done = true;
+          }
+          bulk_g2s(sb + C::TV_OFF, vsrc, vbytes, &full[stage]);
+          if (ybytes) {
+#pragma unroll
+            for (int r = 0; r < C::GR; ++r)
+              if (r < g.y)
+                bulk_g2s(sb + C::TY_OFF + r * (C::SC_MAX * 2),
+                         ybase + (long long)rows[r] * t.h_out + (long long)st * t.SC, ybytes, &full[stage]);
+          }
+          if (++stage == C::TNST) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (st == 0) {
+            rc.it = it;
+            rc.task = ti;
+            rc.ci = ci;
+            rc.g = g;
+            rc.s_a = args.scale[g.z / t.E];
+#pragma unroll
+            for (int r = 0; r < C::GR; ++r) rc.rows[r] = rows[r];
+            mbar_arrive(&wq.full[qp.slot]);
+            qp.advance(kQD);
+          }
+        }
+      }
+    }
+  } else {
+    if (args.y_store == 1)
+      simt_expand_tile_consumers<R, kOutF32Store>(args, smem, full, empty, wq, recs);
+    else if (args.y_store == 2)
+      simt_expand_tile_consumers<R, kOutBf16Store>(args, smem, full, empty, wq, recs);
+    else if (args.y_fp32)
+      simt_expand_tile_consumers<R, kOutF32Acc>(args, smem, full, empty, wq, recs);
+    else
+      simt_expand_tile_consumers<R, kOutBf16Acc>(args, smem, full, empty, wq, recs);
+  }
+  __syncthreads();
+  wq_finish(pd.wctr + kWqSimtExpand, pd.wdone + kWqSimtExpand);
+}
+
 template <typename K>
 cudaError_t set_smem_once(K kernel, int bytes, unsigned long long& mask) {
   int dev = 0;
@@ -849,9 +1054,28 @@ cudaError_t launch_shrink_t(const MultiArgs& args, const PlanDev& pd, int grid, 
   return cudaGetLastError();
 }
 
+// staged-tile expand for r <= 16 (LORA_EXPAND_V1=1: the look-ahead kernel at every r)
+inline bool use_tile_expand(int r) {
+  static const int v1 = [] {
+    const char* e = getenv("LORA_EXPAND_V1");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return r <= 16 && !v1;
+}
+
 template <int R>
 cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   using C = SimtCfg<R>;
+  if constexpr (R <= 16) {
+    if (use_tile_expand(R)) {
+    static unsigned long long tmask = 0;
+    cudaError_t e = set_smem_once(simt_expand_tile_kernel<R>, C::TILE_SMEM, tmask);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(simt_expand_tile_kernel<R>, dim3(2 * grid), dim3(C::THREADS), C::TILE_SMEM, stream, args, pd);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+    }
+  }
   static unsigned long long mask = 0;
   cudaError_t e = set_smem_once(simt_expand_kernel<R>, C::EXPAND_SMEM, mask);
   if (e != cudaSuccess) return e;
@@ -909,8 +1133,8 @@ int simt_shrink_smem(int rank) {
 }
 int simt_expand_smem(int rank) {
   switch (rank) {
-    case 8: return SimtCfg<8>::EXPAND_SMEM;
-    case 16: return SimtCfg<16>::EXPAND_SMEM;
+    case 8: return std::max(SimtCfg<8>::EXPAND_SMEM, SimtCfg<8>::TILE_SMEM);
+    case 16: return std::max(SimtCfg<16>::EXPAND_SMEM, SimtCfg<16>::TILE_SMEM);
     case 32: return SimtCfg<32>::EXPAND_SMEM;
     default: return SimtCfg<64>::EXPAND_SMEM;
   }
