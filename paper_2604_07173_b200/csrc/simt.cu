@@ -59,7 +59,7 @@ struct SimtCfg {
   static constexpr int RED_BYTES = (SMALL_K ? NWC : NJG) * GR * R * 4;
   static constexpr int NST_RAW = (SMEM_BUDGET - RED_BYTES) / S_STAGE;
   static constexpr int NST = NST_RAW > 8 ? 8 : (NST_RAW < 2 ? 2 : NST_RAW);
-  static constexpr int SHRINK_SMEM = 1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8;
+  static constexpr int SHRINK_SMEM = 1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8 + kQD * 16;
   // expand: CPT output columns per consumer thread (c = ct + i*NCT); at r <= 32
   // two columns share one FFMA2 (more B and y bytes per stage at small r)
   static constexpr int CPT = R >= 64 ? 1 : 2;
@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NST * C::S_STAGE + C::RED_BYTES);
   uint64_t* empty = full + C::NST;
   WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::NST), empty + C::NST + kQD, empty + C::NST + 2 * kQD};
+  int4* gq = reinterpret_cast<int4*>(empty + C::NST + 3 * kQD);  // [kQD] group of each queued item
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NST; ++s) {
@@ -329,11 +330,19 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
       uint32_t phase = 0;
       QueuePos qp;
       for (;;) {
-        const long long it = wq_push_next(wq, qp, pd.wctr + kWqSimtShrink, n_items);
+        // the producer resolves the item's group and publishes it with the
+        // item, so consumers never wait on a global load per item
+        long long it = (long long)atomicAdd(pd.wctr + kWqSimtShrink, 1ull);
+        if (it >= n_items) it = -1;
+        const int ti = it < 0 ? 0 : (int)(it / n_groups);
+        const int4 g = it < 0 ? make_int4(0, 0, 0, 0) : pd.groups[(int)(it - (long long)ti * n_groups)];
+        mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
+        wq.item[qp.slot] = it;
+        gq[qp.slot] = g;
+        mbar_arrive(&wq.full[qp.slot]);
+        qp.advance(kQD);
         if (it < 0) break;
-        const int ti = (int)(it / n_groups), gi = (int)(it - (long long)ti * n_groups);
         const SlotTask& t = args.t[ti];
-        const int4 g = pd.groups[gi];
         const long long unit = store_unit(g.z, t.E, args.pl, args.cache);
         const uint16_t* abase = t.At + unit * (long long)t.h_in * R;
         const int n_st = t.h_in / t.SJ;
@@ -371,11 +380,15 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
     uint32_t phase = 0;
     QueuePos qp;
     for (;;) {
-      const long long it = wq_pop(wq, qp);
+      mbar_wait(&wq.full[qp.slot], qp.phase);
+      const long long it = wq.item[qp.slot];
+      const int4 g = gq[qp.slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wq.empty[qp.slot]);
+      qp.advance(kQD);
       if (it < 0) break;
-      const int ti = (int)(it / n_groups), gi = (int)(it - (long long)ti * n_groups);
+      const int ti = (int)(it / n_groups);
       const SlotTask& t = args.t[ti];
-      const int4 g = pd.groups[gi];
       float* vb = pd.vpart + t.vpart_off;
       switch (g.y) {
         case 1: shrink_dispatch<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
