@@ -16,6 +16,7 @@
 //    bitonic network; composites are unique, so any correct sort of them is
 //    the stable sort by key.
 #include <algorithm>
+#include <cstdio>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -25,6 +26,13 @@ namespace lora {
 namespace {
 
 constexpr int kSegThreads = 1024;
+
+#ifdef LORA_SEG_PROF
+__device__ long long g_seg_t[16];
+#define SEG_T(k) do { if (threadIdx.x == 0) g_seg_t[k] = clock64(); } while (0)
+#else
+#define SEG_T(k) do {} while (0)
+#endif
 
 // Block-wide exclusive scan of one int per thread.  Returns the exclusive
 // prefix; *total receives the block sum.  `tmp` holds >= 33 ints.
@@ -55,16 +63,17 @@ __device__ int block_exclusive_scan(int v, int* tmp, int* total) {
   return warp_excl + x - v;
 }
 
-// Reads one row's ids; returns the key (a*E+e), or -1 for "no LoRA" / out of
+// Key of one row (a*E+e), or -1 for "no LoRA" / out of
 // range (flagged through *bad).
-LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int i, int E,
-                        int n_adapters, const Placement& pl, int& bad, const int32_t* cache) {
-  const int a = adapter_ids[i];
-  const int e = expert_ids ? expert_ids[i] : 0;
+LORA_DEVINL int key_of(int a, int e, int E, int n_adapters, const Placement& pl, int& bad, const int32_t* cache) {
   const bool in_range = (a >= -1) && (a < n_adapters) && (a < 0 || (e >= 0 && e < E)) &&
                         (a < 0 || pl.owns_unit(a, e)) && (a < 0 || !cache || cache[a] >= 0);
   if (!in_range) bad = 1;
   return (in_range && a >= 0) ? a * E + e : -1;
+}
+LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int i, int E,
+                        int n_adapters, const Placement& pl, int& bad, const int32_t* cache) {
+  return key_of(adapter_ids[i], expert_ids ? expert_ids[i] : 0, E, n_adapters, pl, bad, cache);
 }
 
 // ---------------------------------------------------------------------------
@@ -146,23 +155,34 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
   const int tid = threadIdx.x;
   int bad = 0, nv = 0;
   // composites in row order; rows read coalesced (row r*1024 + tid) -- the
-  // passes below read the array by index, not by thread
+  // passes below read the array by index, not by thread.  All id loads are
+  // issued before any key is formed (one memory latency, not EPT).
+  int ad[EPT], ex[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = r * kSegThreads + tid;
+    ad[r] = i < T ? __ldg(adapter_ids + i) : -1;
+    ex[r] = (i < T && expert_ids) ? __ldg(expert_ids + i) : 0;
+  }
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int i = r * kSegThreads + tid;
     int key = -1;
-    if (i < T) key = row_key(adapter_ids, expert_ids, i, E, n_adapters, pl, bad, cache);
+    if (i < T) key = key_of(ad[r], ex[r], E, n_adapters, pl, bad, cache);
     nv += key >= 0;
     A[pad32(i)] = ((uint32_t)(key >= 0 ? key : K) << ib) | (uint32_t)i;
   }
   if (bad) atomicOr(err_flag, 1);
   int total;
+  SEG_T(1);
   block_exclusive_scan(nv, scan_tmp, &total);  // its barriers also publish A
+  SEG_T(2);
   *n_valid_out = total;
   uint32_t* in = A;
   uint32_t* out = B;
   for (int sh = 0; sh < kb; sh += 8) {
     radix_pass8<EPT>(in, out, ib + sh, cnt, scan_tmp);
+    SEG_T(3 + sh / 8);
     uint32_t* t = in;
     in = out;
     out = t;
@@ -255,6 +275,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
                    int* __restrict__ err_flag) {
   extern __shared__ __align__(16) uint8_t seg_smem[];
   pdl_launch_dependents();  // the shrink kernels may launch now; they wait for this grid
+  SEG_T(0);
   const Placement pl = sp.pl;
   const int32_t* cache = sp.cache;
   __shared__ int scan_tmp[40];
@@ -305,14 +326,16 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     else return (int)(srt64[j] & 0xffffffffu);
   };
 
+  SEG_T(6);
   // 3. perm + segment heads (each thread a contiguous chunk, so the scan is in order)
   const int chunk = (n_valid + kSegThreads - 1) / kSegThreads;
   const int j0 = min(tid * chunk, n_valid), j1 = min(j0 + chunk, n_valid);
+  // perm written coalesced (position tid + 1024 m), heads counted per chunk
+  for (int j = tid; j < n_valid; j += kSegThreads) pd.perm[j] = row_at(j);
   int heads = 0;
   int prev = j0 > 0 ? key_at(j0 - 1) : -1;
   for (int j = j0; j < j1; ++j) {
     const int k = key_at(j);
-    pd.perm[j] = row_at(j);
     heads += (j == 0 || k != prev);
     prev = k;
   }
@@ -335,6 +358,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   }
   __syncthreads();
 
+  SEG_T(7);
   // 4. work lists: CUDA-core groups (<= kGroupRows rows) and tcgen05 tiles (<= sp.tile_rows)
   const int schunk = (S + kSegThreads - 1) / kSegThreads;
   const int s0 = min(tid * schunk, S), s1 = min(s0 + schunk, S);
@@ -367,6 +391,14 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       r += len;
     }
   }
+  SEG_T(8);
+#ifdef LORA_SEG_PROF
+  if (tid == 0) {
+    printf("seg T=%d K=%d EPT=%d cycles: ids %lld scan %lld p0 %lld p1 %lld sorted %lld perm+segs %lld lists %lld\n", T,
+           n_adapters * E, EPT, g_seg_t[1] - g_seg_t[0], g_seg_t[2] - g_seg_t[1], g_seg_t[3] - g_seg_t[2],
+           kb > 8 ? g_seg_t[4] - g_seg_t[3] : 0ll, g_seg_t[6] - g_seg_t[2], g_seg_t[7] - g_seg_t[6], g_seg_t[8] - g_seg_t[7]);
+  }
+#endif
   if (tid == 0) {
     pd.counts[kCntValid] = n_valid;
     pd.counts[kCntSegs] = S;
