@@ -8,6 +8,8 @@
 namespace lora {
 
 constexpr int kMaxPlanRows = 16384;  // single-CTA segmenter capacity (128 KB of composites)
+constexpr int kSegMultiMin = 4096;   // T at or above which the multi-CTA segmenter runs
+constexpr int kSegHistMax = 1 << 18; // K * C bound of the multi-CTA segmenter's histogram
 constexpr int kGroupRows = 8;        // rows per CUDA-core work group
 constexpr int kTileRows = 128;       // rows per tcgen05 tile (UMMA M / N)
 constexpr int kMaxTasks = 128;       // slots per multi-slot launch (param space; 32 layers x q,k,v,o)
@@ -77,6 +79,11 @@ struct PlanDev {
   uint16_t* vbf;     // tcgen05 path: complete v rounded to bf16, per slot region [max_rows][r]
   unsigned long long* wctr;  // [kWorkSlots] dynamic item counters of the persistent kernels (self-resetting)
   unsigned int* wdone;       // [kWorkSlots] finished-CTA counters
+  // multi-CTA segmenter scratch
+  uint32_t* lsort;           // [max_rows rounded up to 4096] per-CTA sorted composites (key << 12 | local row)
+  int32_t* lrank;            // [same] rank of each sorted entry inside its key's run
+  int32_t* hist;             // [kSegHistMax] run lengths, key-major [K][C] (kept zero between builds)
+  int32_t* offs;             // [kSegHistMax] exclusive prefix of hist
   int max_rows;
 };
 

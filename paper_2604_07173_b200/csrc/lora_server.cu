@@ -532,6 +532,14 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
             cudaMalloc(&d.vbf, sizeof(uint16_t) * s->slots.size() * (size_t)max_rows * s->r) == cudaSuccess &&
             cudaMalloc(&d.wctr, sizeof(unsigned long long) * kWorkSlots) == cudaSuccess &&
             cudaMalloc(&d.wdone, sizeof(unsigned int) * kWorkSlots) == cudaSuccess;
+  if (ok) {  // multi-CTA segmenter scratch (used for T >= kSegMultiMin)
+    const size_t cap = (size_t)(max_rows + 4095) / 4096 * 4096;  // whole CTAs of rows
+    ok = cudaMalloc(&d.lsort, sizeof(uint32_t) * cap) == cudaSuccess &&
+         cudaMalloc(&d.lrank, sizeof(int32_t) * cap) == cudaSuccess &&
+         cudaMalloc(&d.hist, sizeof(int32_t) * kSegHistMax) == cudaSuccess &&
+         cudaMalloc(&d.offs, sizeof(int32_t) * kSegHistMax) == cudaSuccess;
+    if (ok) cudaMemset(d.hist, 0, sizeof(int32_t) * kSegHistMax);
+  }
   if (!ok) {
     cudaGetLastError();
     plan_destroy_impl(p);
@@ -557,6 +565,10 @@ void plan_destroy_impl(lora_plan* p) {
   cudaFree(p->dev.vbf);
   cudaFree(p->dev.wctr);
   cudaFree(p->dev.wdone);
+  cudaFree(p->dev.lsort);
+  cudaFree(p->dev.lrank);
+  cudaFree(p->dev.hist);
+  cudaFree(p->dev.offs);
   delete p;
 }
 

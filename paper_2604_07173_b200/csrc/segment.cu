@@ -17,6 +17,7 @@
 //    the stable sort by key.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -82,7 +83,7 @@ LORA_DEVINL int row_key(const int32_t* __restrict__ adapter_ids, const int32_t* 
 // Composite buffers are padded with one word per 32 (index i lives at
 // i + i/32): thread t's contiguous run t*EPT.. then falls in 32 distinct banks
 // across a warp (EPT in 1..16), so the blocked-layout accesses are conflict-free.
-LORA_DEVINL int pad32(int i) { return i + (i >> 5); }
+__host__ __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 
 // One stable counting-sort pass on an 8-bit digit (v >> shift) & 255 --
 // warp-synchronous multisplit.  Warp w owns the contiguous index range
@@ -407,6 +408,229 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// multi-CTA path (T >= kSegMultiMin): one CTA is instruction-bound on the
+// composites and passes, so the rows are split over C CTAs.
+//   seg_local_kernel   (C CTAs): CTA c sorts its RPC rows by key (stable, the
+//                      radix passes above on composites key << 12 | local row),
+//                      stores them with each entry's rank inside its key's
+//                      run, and the run lengths into hist[key][c]
+//   seg_scan_kernel    (1 CTA):  exclusive prefix of hist in (key, c) order --
+//                      offs[key][c] = rows of smaller keys + rows of this key
+//                      in CTAs before c (this is what keeps the sort stable)
+//                      -- zeroes hist for the next build, and builds the
+//                      segments and the work lists from the key totals
+//   seg_scatter_kernel (C CTAs): perm[offs[key][c] + rank] = row
+// ---------------------------------------------------------------------------
+constexpr int kLocBits = 12;        // local row bits (RPC <= 4096)
+constexpr int kSegKeysMax = 36864;
+constexpr int kSegHistSmall = 16384;  // one scan round of the histogram  // key-space bound (the scan CTA keeps K + 1 key starts in smem)
+
+// first index in the sorted composites [0, n) whose key is >= k
+LORA_DEVINL int lower_key(const uint32_t* srt, int n, uint32_t k) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((srt[pad32(mid)] >> kLocBits) < k) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(kSegThreads, 1)
+    seg_local_kernel(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T, int E,
+                     int n_adapters, int kb, int C, SegParams sp, PlanDev pd, int* __restrict__ err_flag) {
+  constexpr int RPC = kSegThreads * EPT;
+  extern __shared__ __align__(16) uint8_t seg_smem[];
+  __shared__ int scan_tmp[40];
+  uint32_t* A = reinterpret_cast<uint32_t*>(seg_smem);
+  uint32_t* B = A + pad32(RPC) + 4;
+  int* cnt = reinterpret_cast<int*>(B + pad32(RPC) + 4);
+  const int tid = threadIdx.x, c = blockIdx.x;
+  const int row0 = c * RPC;
+  const uint32_t K = (uint32_t)n_adapters * E;
+  if (blockIdx.x == 0) SEG_T(12);
+  int ad[EPT], ex[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = row0 + r * kSegThreads + tid;
+    ad[r] = i < T ? __ldg(adapter_ids + i) : -1;
+    ex[r] = (i < T && expert_ids) ? __ldg(expert_ids + i) : 0;
+  }
+  int bad = 0;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int l = r * kSegThreads + tid;
+    int key = -1;
+    if (row0 + l < T) key = key_of(ad[r], ex[r], E, n_adapters, sp.pl, bad, sp.cache);
+    A[pad32(l)] = ((key >= 0 ? (uint32_t)key : K) << kLocBits) | (uint32_t)l;
+  }
+  if (bad) atomicOr(err_flag, 1);
+  __syncthreads();
+  uint32_t* in = A;
+  uint32_t* out = B;
+  for (int sh = 0; sh < kb; sh += 8) {
+    radix_pass8<EPT>(in, out, kLocBits + sh, cnt, scan_tmp);
+    uint32_t* t = in;
+    in = out;
+    out = t;
+  }
+  if (blockIdx.x == 0) SEG_T(13);
+  // sorted: each entry's rank inside its run; the run head records the length
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int p = r * kSegThreads + tid;
+    const uint32_t v = in[pad32(p)];
+    const uint32_t k = v >> kLocBits;
+    int rank = 0;
+    if (k < K) {
+      const int start = lower_key(in, RPC, k);
+      rank = p - start;
+      if (rank == 0) pd.hist[(long long)k * C + c] = lower_key(in, RPC, k + 1) - p;
+    }
+    pd.lsort[row0 + p] = v;
+    pd.lrank[row0 + p] = rank;
+  }
+#ifdef LORA_SEG_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    printf("local EPT=%d K=%u cycles: sort %lld runs %lld\n", EPT, K, g_seg_t[13] - g_seg_t[12], clock64() - g_seg_t[13]);
+#endif
+}
+
+__global__ void __launch_bounds__(kSegThreads, 1)
+    seg_scan_kernel(int K, int C, SegParams sp, PlanDev pd) {
+  extern __shared__ __align__(16) uint8_t seg_smem[];
+  __shared__ int scan_tmp[40];
+  constexpr int CH = 16;                  // entries per thread per round
+  constexpr int ROUND = kSegThreads * CH;
+  int* kstart = reinterpret_cast<int*>(seg_smem);  // [pad32(K + 1)] first sorted position of each key
+  int* stage = kstart + pad32(K + 1) + 4;          // [pad32(ROUND)]
+  const int tid = threadIdx.x;
+  const long long N = (long long)K * C;
+  int carry = 0;
+  SEG_T(9);
+  for (long long base = 0; base < N; base += ROUND) {
+    const int n = (int)min((long long)ROUND, N - base);
+    {
+      // all loads of the round in flight at once, then the zeroing stores
+      int h[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int i = q * kSegThreads + tid;
+        h[q] = i < n ? __ldcg(pd.hist + base + i) : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int i = q * kSegThreads + tid;
+        if (i < n) {
+          pd.hist[base + i] = 0;
+          stage[pad32(i)] = h[q];
+        }
+      }
+    }
+    __syncthreads();
+    int v[CH], sum = 0;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const int i = tid * CH + q;
+      v[q] = i < n ? stage[pad32(i)] : 0;
+      sum += v[q];
+    }
+    int total;
+    int run = carry + block_exclusive_scan(sum, scan_tmp, &total);
+    // key starts: the entries (k, c = 0) of this thread's run, k = kk, kk + 1, ...
+    const int e0 = (int)base + tid * CH;
+    int kk = (e0 + C - 1) / C;
+    int next = kk * C;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const int i = tid * CH + q;
+      stage[pad32(i)] = run;
+      if (i < n && e0 + q == next) {
+        kstart[pad32(kk++)] = run;
+        next += C;
+      }
+      run += v[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const int i = q * kSegThreads + tid;
+      if (i < n) pd.offs[base + i] = stage[pad32(i)];
+    }
+    carry += total;
+    __syncthreads();
+  }
+  const int n_valid = carry;
+  if (tid == 0) kstart[pad32(K)] = n_valid;
+  __syncthreads();
+  SEG_T(10);
+
+  // segments = keys with rows, in key order; work lists as in the one-CTA path
+  const int kchunk = (K + kSegThreads - 1) / kSegThreads;
+  const int k0 = min(tid * kchunk, K), k1 = min(k0 + kchunk, K);
+  int heads = 0, ng = 0, nt = 0;
+  for (int k = k0; k < k1; ++k) {
+    const int size = kstart[pad32(k + 1)] - kstart[pad32(k)];
+    if (size == 0) continue;
+    ++heads;
+    if (sp.tc_enabled && size > sp.small_max)
+      nt += (size + sp.tile_rows - 1) / sp.tile_rows;
+    else
+      ng += (size + kGroupRows - 1) / kGroupRows;
+  }
+  int S, NG, NT;
+  int seg = block_exclusive_scan(heads, scan_tmp, &S);
+  int g = block_exclusive_scan(ng, scan_tmp, &NG);
+  int t = block_exclusive_scan(nt, scan_tmp, &NT);
+  for (int k = k0; k < k1; ++k) {
+    const int b = kstart[pad32(k)], size = kstart[pad32(k + 1)] - b;
+    if (size == 0) continue;
+    pd.seg_off[seg] = b;
+    pd.seg_key[seg] = k;
+    const bool tc = sp.tc_enabled && size > sp.small_max;
+    const int cap = tc ? sp.tile_rows : kGroupRows;
+    const int np = (size + cap - 1) / cap;
+    const int base = size / np, extra = size % np;
+    int r = b;
+    for (int q = 0; q < np; ++q) {
+      const int len = base + (q < extra ? 1 : 0);
+      const int4 w = make_int4(r, len, k, seg);
+      if (tc)
+        pd.tiles[t++] = w;
+      else
+        pd.groups[g++] = w;
+      r += len;
+    }
+    ++seg;
+  }
+  SEG_T(11);
+#ifdef LORA_SEG_PROF
+  if (tid == 0) printf("scan K=%d C=%d cycles: flat %lld keys %lld\n", K, C, g_seg_t[10] - g_seg_t[9], g_seg_t[11] - g_seg_t[10]);
+#endif
+  if (tid == 0) {
+    pd.seg_off[S] = n_valid;
+    pd.counts[kCntValid] = n_valid;
+    pd.counts[kCntSegs] = S;
+    pd.counts[kCntGroups] = NG;
+    pd.counts[kCntTiles] = NT;
+  }
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(kSegThreads) seg_scatter_kernel(int T, int K, int C, PlanDev pd) {
+  constexpr int RPC = kSegThreads * EPT;
+  pdl_launch_dependents();  // the shrink kernels may launch now; they wait for this grid
+  const int c = blockIdx.x, row0 = c * RPC;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int p = r * kSegThreads + threadIdx.x;
+    const uint32_t v = pd.lsort[row0 + p];
+    const int k = (int)(v >> kLocBits);
+    if (k < K) pd.perm[pd.offs[(long long)k * C + c] + pd.lrank[row0 + p]] = row0 + (int)(v & ((1u << kLocBits) - 1u));
+  }
+}
+
 int bits_for(long long v) {  // bits needed to represent v (v >= 0)
   int b = 0;
   while ((1LL << b) <= v) ++b;
@@ -418,6 +642,61 @@ int bits_for(long long v) {  // bits needed to represent v (v >= 0)
 cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,
                            const SegParams& sp, const PlanDev& pd, int* err_flag,
                            cudaStream_t stream) {
+  // multi-CTA path: K * C within the histogram bound, local composites radix-able
+  {
+    const long long K = (long long)n_adapters * E;
+    const int kb = bits_for(K);
+    const char* fe = getenv("LORA_SEG_MULTI");  // test hook: 1 forces, 0 disables the multi-CTA path
+    const int forced = fe ? atoi(fe) : -1;
+    const bool want = forced < 0 ? T >= kSegMultiMin : forced == 1;
+    int ept = 0;
+    if (want && pd.hist && T > 0 && kb + kLocBits <= 32 && K > 0 && K <= kSegKeysMax) {
+      // rows per CTA: the fewest (1024, 2048) that keep the histogram K x C
+      // within one scan round (the one-CTA scan is slow beyond that, measured:
+      // T = 8192, K = 16384 is faster on the one-CTA kernel); a forced run
+      // (test hook) falls back to 4096 rows per CTA
+      const char* ee = getenv("LORA_SEG_EPT");  // tuning hook
+      const int pick = ee ? atoi(ee) : 0;
+      for (int e : {1, 2, 4}) {
+        const long long C = (T + e * kSegThreads - 1) / (e * kSegThreads);
+        const bool fits = pick ? e == pick : (K * C <= kSegHistSmall || (forced == 1 && e == 4));
+        if (fits) {
+          if (K * C <= kSegHistMax) ept = e;
+          break;
+        }
+      }
+    }
+    if (ept) {
+      const int C = (T + ept * kSegThreads - 1) / (ept * kSegThreads);
+      const int rpc = ept * kSegThreads;
+      const int lsm = (2 * (rpc + rpc / 32 + 4) + 32 * 256) * 4;
+      const int ssm = (int)((pad32((int)K + 1) + 4) * 4 + (16 * kSegThreads + 16 * kSegThreads / 32) * 4);
+      static unsigned long long mset = 0;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (!(mset & (1ull << dev))) {
+        const int lmax = (2 * (4096 + 128 + 4) + 32 * 256) * 4;
+        const int smax = (pad32(kSegKeysMax + 1) + 4) * 4 + (16 * kSegThreads + 16 * kSegThreads / 32) * 4;
+        cudaError_t e = cudaFuncSetAttribute(seg_local_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lmax);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(seg_local_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, lmax);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(seg_local_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lmax);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(seg_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (e != cudaSuccess) return e;
+        mset |= 1ull << dev;
+      }
+      {
+        auto local = ept == 1 ? seg_local_kernel<1> : ept == 2 ? seg_local_kernel<2> : seg_local_kernel<4>;
+        auto scatter = ept == 1 ? seg_scatter_kernel<1> : ept == 2 ? seg_scatter_kernel<2> : seg_scatter_kernel<4>;
+        local<<<C, kSegThreads, lsm, stream>>>(adapter_ids, expert_ids, T, E, n_adapters, kb, C, sp, pd, err_flag);
+        seg_scan_kernel<<<1, kSegThreads, ssm, stream>>>((int)K, C, sp, pd);
+        scatter<<<C, kSegThreads, 0, stream>>>(T, (int)K, C, pd);
+        return cudaGetLastError();
+      }
+    }
+  }
   int P = kSegThreads;  // at least one composite per thread
   while (P < T) P <<= 1;
   const int ib = bits_for(P - 1);

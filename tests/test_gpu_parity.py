@@ -95,6 +95,41 @@ def test_segment_bit_exact_adversarial(B, case):
         B.lora_server_destroy(s)
 
 
+@pytest.mark.parametrize("T,n_ad,E", [(1, 16, 1), (1023, 64, 8), (2049, 16, 1), (4097, 2048, 8), (5000, 7, 3),
+                                      (8192, 2048, 8), (16384, 64, 8), (16384, 4096, 4)])
+@pytest.mark.parametrize("multi", ["1", "0"])
+def test_segment_multi_cta_path(B, monkeypatch, T, n_ad, E, multi):
+    """Both segmenter paths (LORA_SEG_MULTI test hook: 1 = the multi-CTA
+    local-sort / scan / scatter kernels at any T, 0 = the one-CTA kernel) give
+    the oracle's stable segmentation bit-exactly, incl. -1 rows, Zipf-skewed
+    and ragged batches, and a key space that makes the histogram wide."""
+    monkeypatch.setenv("LORA_SEG_MULTI", multi)
+    rng = np.random.default_rng(T + n_ad)
+    zipf = rng.choice(n_ad, size=T, p=li.zipf_probs(n_ad))
+    a = np.where(rng.random(T) < 0.1, -1, zipf).astype(np.int32)
+    e = rng.integers(0, E, T).astype(np.int32)
+    cfg = li.Config("seg", 9, (li.Slot("s", 64, 64, E, 0),), 8, n_ad, E, 1, T, "fp32")
+    s = U.make_server(B, cfg, max_rows=T, fill=False)
+    p = B.lora_plan_create(s, T)
+    try:
+        # a first build on other ids: the second must not see its histogram
+        a0 = torch.from_numpy(rng.integers(0, n_ad, T).astype(np.int32)).to(U.DEV)
+        B.lora_plan_build(s, p, a0, None if E == 1 else torch.zeros(T, dtype=torch.int32, device=U.DEV), T, E)
+        B.lora_plan_build(s, p, torch.from_numpy(a).to(U.DEV), torch.from_numpy(e).to(U.DEV) if E > 1 else None,
+                          T, E)
+        perm = torch.empty(T, dtype=torch.int32, device=U.DEV)
+        off = torch.empty(T + 1, dtype=torch.int32, device=U.DEV)
+        keys = torch.empty(T, dtype=torch.int32, device=U.DEV)
+        nv, ns = B.lora_plan_export(s, p, perm, off, keys)
+        rp, ro, rk = oracle.segment(a, e if E > 1 else None, E)
+        np.testing.assert_array_equal(perm[:nv].cpu().numpy(), rp)
+        np.testing.assert_array_equal(off[:ns + 1].cpu().numpy(), ro)
+        np.testing.assert_array_equal(keys[:ns].cpu().numpy(), rk)
+    finally:
+        B.lora_plan_destroy(p)
+        B.lora_server_destroy(s)
+
+
 # ---------------------------------------------------------------------------
 # generator identity (the CUDA fill implements the same recipe)
 # ---------------------------------------------------------------------------
