@@ -667,6 +667,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.scale = s->d_scale;
     if (rin) args.rin = *rin;
     int kc = 0, ci = 0;
+    bool any_split = false;
     for (int i = 0; i < nb; ++i) {
       const SlotInfo& si = s->slots[slots[b0 + i]];
       SlotTask& t = args.t[i];
@@ -683,13 +684,21 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       t.KI = si.KI;
       t.SJ = si.SJ;
       t.n_kc = si.n_kc;
+      if (tc && p->T >= kTcWideKRows) {
+        // large batches have tcgen05 tiles enough to fill the GPU without
+        // splitting K: a tile's item takes (up to) 4096 of h_in, so gate/up
+        // write v directly and only wide inputs leave partials to reduce
+        t.KI = best_divisor(si.h_in, 128, 4096);
+        t.n_kc = si.h_in / t.KI;
+      }
       t.CI = si.CI;
       t.SC = si.SC;
       t.n_ci = si.n_ci;
       t.kc_base = kc;
       t.ci_base = ci;
-      kc += si.n_kc;
+      kc += t.n_kc;
       ci += si.n_ci;
+      any_split |= t.n_kc > 1;
     }
     args.total_kc = kc;
     args.total_ci = ci;
@@ -729,9 +738,11 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       pi = prof_start(s, tst);
       CK(s, launch_tc_shrink(args, p->dev, grid, tst));
       prof_stop(s, pi, kKTcShrink, tst);
-      pi = prof_start(s, tst);
-      CK(s, launch_tc_vreduce(args, p->dev, grid, tst));
-      prof_stop(s, pi, kKTcVreduce, tst);
+      if (any_split) {  // tiles of a task with n_kc == 1 got their v from the shrink
+        pi = prof_start(s, tst);
+        CK(s, launch_tc_vreduce(args, p->dev, grid, tst));
+        prof_stop(s, pi, kKTcVreduce, tst);
+      }
       pi = prof_start(s, tst);
       CK(s, launch_tc_expand(args, p->dev, grid, tst));
       prof_stop(s, pi, kKTcExpand, tst);

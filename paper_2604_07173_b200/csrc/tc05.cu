@@ -122,6 +122,20 @@ struct ShrinkCfg {
   static constexpr int SMEM = 1024 + NST * STAGE + 256;
 };
 
+// v row n of a tile (R fp32 sums) rounded to bf16 into the pre-swizzled
+// expand operand: 16-byte chunk q of the row at q ^ (n & 7)
+LORA_DEVINL void store_vbf_row(uint16_t* dst_row, int n, const float* v) {
+#pragma unroll
+  for (int q = 0; q < R / 8; ++q) {
+    uint4 w;
+    w.x = pack_bf16x2_rn(v[8 * q], v[8 * q + 1]);
+    w.y = pack_bf16x2_rn(v[8 * q + 2], v[8 * q + 3]);
+    w.z = pack_bf16x2_rn(v[8 * q + 4], v[8 * q + 5]);
+    w.w = pack_bf16x2_rn(v[8 * q + 6], v[8 * q + 7]);
+    *reinterpret_cast<uint4*>(dst_row + ((q ^ (n & 7)) * 8)) = w;
+  }
+}
+
 template <bool REMOTE>
 __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
     tc_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
@@ -302,10 +316,16 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (row_in_tile < tile.y) {
-        float4* dst = reinterpret_cast<float4*>(pd.vpart + t.vpart_off +
-                                                ((long long)kc * pd.max_rows + tile.x + row_in_tile) * R);
+        if (t.n_kc == 1) {
+          // the whole K in one accumulator: v rounded to bf16 here (no reduction pass)
+          store_vbf_row(pd.vbf + t.vbf_off + ((long long)tile.x + row_in_tile) * R, row_in_tile, v);
+        } else {
+          float4* dst = reinterpret_cast<float4*>(pd.vpart + t.vpart_off +
+                                                  ((long long)kc * pd.max_rows + tile.x + row_in_tile) * R);
 #pragma unroll
-        for (int c = 0; c < C::ACC_COLS / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          for (int c = 0; c < C::ACC_COLS / 4; ++c)
+            dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        }
       }
       if (++acc == 2) {
         acc = 0;
@@ -344,6 +364,7 @@ __global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__
     const int4 tile = pd.tiles[ti];
     if (n >= tile.y) continue;
     const SlotTask& t = args.t[task];
+    if (t.n_kc == 1) continue;  // written by the shrink epilogue
     const float* src = pd.vpart + t.vpart_off + ((long long)tile.x + n) * R + q * 8;
     float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int kc = 0; kc < t.n_kc; ++kc) {
