@@ -10,7 +10,7 @@ namespace lora {
 constexpr int kMaxPlanRows = 16384;  // single-CTA segmenter capacity (128 KB of composites)
 constexpr int kSegMultiMin = 4096;   // T at or above which the multi-CTA segmenter runs
 constexpr int kSegHistMax = 1 << 18; // K * C bound of the multi-CTA segmenter's histogram
-constexpr int kTcWideKRows = 4096;  // plan rows from which tcgen05 shrink items take up to 4096 of h_in
+constexpr int kTcWideKRows = 4096;  // plan rows from which tcgen05 shrink items take the whole h_in
 constexpr int kGroupRows = 8;        // rows per CUDA-core work group
 constexpr int kTileRows = 128;       // rows per tcgen05 tile (UMMA M / N)
 constexpr int kMaxTasks = 128;       // slots per multi-slot launch (param space; 32 layers x q,k,v,o)
