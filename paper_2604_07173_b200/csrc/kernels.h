@@ -188,7 +188,7 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
                            const SegParams& sp, const PlanDev& pd, int* err_flag, cudaStream_t stream);
 cudaError_t launch_simt_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_simt_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
-cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid, cudaStream_t stream);
 cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 bool tc_available();

@@ -738,7 +738,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     int pi;
     if (tc) {
       pi = prof_start(s, tst);
-      CK(s, launch_tc_shrink(args, p->dev, grid, tst));
+      CK(s, launch_tc_shrink(args, p->dev, p->T, grid, tst));
       prof_stop(s, pi, kKTcShrink, tst);
       if (any_split) {  // tiles of a task with n_kc == 1 got their v from the shrink
         pi = prof_start(s, tst);

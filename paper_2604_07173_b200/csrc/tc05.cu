@@ -21,6 +21,12 @@
 //
 // UMMA operands are K-major SWIZZLE_128B (rows of 128 B, 8-row groups 1024 B
 // apart); the instruction descriptor selects bf16 x bf16 -> fp32.
+#include <cstdlib>
+#include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -101,6 +107,26 @@ LORA_DEVINL uint8_t* align1024(uint8_t* p) {
 constexpr int R = 64;  // tcgen05 path rank
 constexpr int kQD = 4;  // work-queue depth
 
+// x tensor maps of a tcgen05 shrink launch (one per task): 2-D [T rows][h_in]
+// bf16, box {64 columns, 1 row}, SWIZZLE_128B -- the layout a TMA tile::gather4
+// lands is then exactly the canonical SW128 K-major operand (row n of the tile
+// at smem row n, 16-byte chunk q at q ^ (n & 7); measured, tools/gather4_probe.cu)
+constexpr int kTcMapTasks = 8;
+struct TcMaps {
+  CUtensorMap x[kTcMapTasks];
+  int use;  // 1: x rows by gather4 from one producer warp; 0: cp.async gathers
+};
+
+// 4 rows (r0..r3) x 64 columns from col of map into smem dst (512 bytes)
+LORA_DEVINL void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2, int r3,
+                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
 // ===========================================================================
 // shrink
 // ===========================================================================
@@ -138,7 +164,7 @@ LORA_DEVINL void store_vbf_row(uint16_t* dst_row, int n, const float* v) {
 
 template <bool REMOTE>
 __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
-    tc_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
+    tc_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd, const __grid_constant__ TcMaps maps) {
   using C = ShrinkCfg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -155,8 +181,9 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     wq.init(C::EPI_WARPS + 1 + 3);  // epilogue, MMA and the producer warps that pop (warp PROD_WARP0 fetches)
+    const bool g4 = !REMOTE && maps.use;
     for (int s = 0; s < C::NST; ++s) {
-      mbar_init(&full[s], C::PROD_THREADS + 1);
+      mbar_init(&full[s], g4 ? 1 : C::PROD_THREADS + 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -200,9 +227,41 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       const int4 tile = pd.tiles[ti];
       const long long unit = store_unit(tile.z, t.E, args.pl, args.cache);
       const uint16_t* wbase = t.At + (unit * (t.h_in >> 6) + ((kc * t.KI) >> 6)) * (long long)(R * 64);
+      const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
+      if (!REMOTE && maps.use) {
+        // one warp: lane l gathers tile rows 4l .. 4l+3 (rows past the tile
+        // repeat its first row; their accumulator rows are never read)
+        if (warp != C::PROD_WARP0) continue;
+        int rr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int n = lane * 4 + i;
+          rr[i] = pd.perm[tile.x + (n < tile.y ? n : 0)];
+        }
+        const CUtensorMap* xm = &maps.x[task];
+        for (int st = 0; st < n_st; ++st) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sbase = smem + stage * C::STAGE;
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * (C::W_SUB + C::X_SUB));
+            bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB,
+                     wbase + (long long)st * C::KS_PER_STAGE * (R * 64), C::KS_PER_STAGE * C::W_SUB, &full[stage]);
+          }
+          __syncwarp();
+          const int col = kc * t.KI + st * C::KS_PER_STAGE * C::KSTEP;
+#pragma unroll
+          for (int ks = 0; ks < C::KS_PER_STAGE; ++ks)
+            tma_gather4(smem_u32(sbase + ks * C::X_SUB + lane * 512), xm, col + ks * C::KSTEP, rr[0], rr[1], rr[2],
+                        rr[3], &full[stage]);
+          if (++stage == C::NST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        continue;
+      }
       // this thread's rows / chunks: 128 rows x 8 chunks per k-step, 1024 copies / 128 threads;
       // thread pt always copies chunk q = pt & 7 of rows n = (pt >> 3) + 16 i
-      const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
       const uint16_t* xsrc[8];
       uint32_t xbytes[8];
 #pragma unroll
@@ -799,13 +858,54 @@ cudaError_t set_smem_once(K kernel, int bytes, unsigned long long& mask) {
 
 bool tc_available() { return true; }
 
-cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// x rows by TMA gather4 (opt-in, LORA_TC_GATHER4=1) when every task's x can be
+// described by a tensor map (local rows, at most kTcMapTasks tasks).  Measured
+// on B200: correct, but one gather4 moves 4 x 128 B and the TMA unit then
+// sustains far less than 128 threads of 16-byte cp.async (prefill tc shrink
+// 439 us vs 152 us; config 5 438 vs 116 us), so cp.async stays the default.
+static void make_x_maps(const MultiArgs& args, int x_rows, TcMaps& m) {
+  std::memset(&m, 0, sizeof(m));
+  const char* env = getenv("LORA_TC_GATHER4");
+  if (!(env && env[0] == '1') || args.rin.G > 0 || args.n_tasks > kTcMapTasks || x_rows < 1) return;
+  auto enc = tensor_map_encoder();
+  if (!enc) return;
+  for (int i = 0; i < args.n_tasks; ++i) {
+    const SlotTask& t = args.t[i];
+    cuuint64_t dims[2] = {(cuuint64_t)t.h_in, (cuuint64_t)x_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)t.h_in * 2};
+    cuuint32_t box[2] = {64, 1};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&m.x[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(t.x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return;  // m.use stays 0
+  }
+  m.use = 1;
+}
+
+cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid, cudaStream_t stream) {
   static unsigned long long mask[2] = {0, 0};
   const bool remote = args.rin.G > 0;
   auto kern = remote ? tc_shrink_kernel<true> : tc_shrink_kernel<false>;
   cudaError_t e = set_smem_once(kern, ShrinkCfg::SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kern, dim3(grid), dim3(ShrinkCfg::THREADS), ShrinkCfg::SMEM, stream, args, pd);
+  TcMaps maps;
+  make_x_maps(args, x_rows, maps);
+  e = launch_pdl(kern, dim3(grid), dim3(ShrinkCfg::THREADS), ShrinkCfg::SMEM, stream, args, pd, maps);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
