@@ -150,6 +150,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   s->debug_sync = env_flag("LORA_DEBUG_SYNC");
   if (const char* e = std::getenv("LORA_SMALL_SEG_MAX")) s->small_seg_max = std::atoi(e);
   if (const char* e = std::getenv("LORA_TC_KI_MAX")) s->tc_ki_max = std::max(128, std::atoi(e));
+  if (const char* e = std::getenv("LORA_TC_CI_MAX")) s->tc_ci_max = std::atoi(e);
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
   if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -725,6 +726,19 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
         ci2 += sargs.t[i].n_ci;
       }
       fill_task_tables(sargs);
+    }
+    if (tc && s->tc_ci_max > 0) {
+      // tcgen05 expand items: CI columns of one tile (tuning hook LORA_TC_CI_MAX)
+      int ci3 = 0;
+      for (int i = 0; i < nb; ++i) {
+        SlotTask& t = args.t[i];
+        t.CI = best_divisor(t.h_out, 128, s->tc_ci_max);
+        t.n_ci = t.h_out / t.CI;
+        t.ci_base = ci3;
+        ci3 += t.n_ci;
+      }
+      args.total_ci = ci3;
+      fill_task_tables(args);
     }
     // The tcgen05 chain and the CUDA-core chain touch disjoint rows: run the
     // tcgen05 chain on the side stream (fork/join with events, graph-capturable)

@@ -29,6 +29,7 @@ struct lora_server {
   int max_rows = 0;
   int sm_count = 148;
   int small_seg_max = 8;
+  int tc_ci_max = 8192;    // tcgen05 expand: max h_out per item (measured best of 1024..8192; env LORA_TC_CI_MAX, 0 = slot CI)
   int tc_ki_max = 1 << 20;  // large-batch tcgen05 shrink: max h_in per item, default the whole h_in (env LORA_TC_KI_MAX)
   int world = 1, shard_rank = 0;
   int n_hot = 0;  // adapters [0, n_hot) replicated on every rank of a sharded server
