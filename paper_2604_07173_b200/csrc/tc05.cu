@@ -137,12 +137,21 @@ struct ShrinkCfg {
   static constexpr int PROD_THREADS = 128;
   static constexpr int THREADS = 9 * 32;
   static constexpr int KSTEP = 64;                         // K per SW128 atom
-  static constexpr int KS_PER_STAGE = 2;                   // k-steps per stage
+#ifndef LORA_TCS_KS
+#define LORA_TCS_KS 2
+#endif
+#ifndef LORA_TCS_NST
+#define LORA_TCS_NST 4
+#endif
+#ifndef LORA_TCS_LAG
+#define LORA_TCS_LAG 2
+#endif
+  static constexpr int KS_PER_STAGE = LORA_TCS_KS;         // k-steps per stage
   static constexpr int X_SUB = kTileRows * 128;            // 16 KB per k-step
   static constexpr int W_SUB = R * 128;                    // 8 KB per k-step
   static constexpr int STAGE = KS_PER_STAGE * (X_SUB + W_SUB);
-  static constexpr int NST = 4;
-  static constexpr int LAG = 2;                            // cp.async groups kept in flight
+  static constexpr int NST = LORA_TCS_NST;
+  static constexpr int LAG = LORA_TCS_LAG;                 // cp.async groups kept in flight
   static constexpr int ACC_COLS = 64;                      // N = r
   static constexpr int TMEM_COLS = 128;                    // 2 accumulators
   static constexpr int SMEM = 1024 + NST * STAGE + 256;
