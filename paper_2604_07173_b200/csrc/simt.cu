@@ -95,10 +95,14 @@ struct SimtCfg {
   static constexpr int TV_OFF = B_STAGE;
   static constexpr int TY_OFF = B_STAGE + 1024 * ((V_BYTES + 1023) / 1024);
   static constexpr int T_STAGE = TY_OFF + Y_SLOT;
-  static constexpr int T_FIXED = 1024 + 2 * 16 * 8 + 3 * kQD * 8 + kQD * 80;
+  // + a resolver warp running kRQ items ahead of the producer (ring of
+  // resolved ExpandRec records with full/empty barriers)
+  static constexpr int TILE_THREADS = NCT + 64;
+  static constexpr int kRQ = 4;
+  static constexpr int T_FIXED = 1024 + 2 * 16 * 8 + 3 * kQD * 8 + kQD * 80 + kRQ * (80 + 16);
   static constexpr int TNST_RAW = (112 * 1024 - T_FIXED) / T_STAGE;
   static constexpr int TNST = TNST_RAW > 8 ? 8 : (TNST_RAW < 2 ? 2 : TNST_RAW);
-  static constexpr int TILE_SMEM = 1024 + TNST * T_STAGE + 2 * TNST * 8 + 3 * kQD * 8 + kQD * 80;
+  static constexpr int TILE_SMEM = 1024 + TNST * T_STAGE + 2 * TNST * 8 + 3 * kQD * 8 + kQD * 80 + kRQ * (80 + 16);
   static_assert(T_STAGE % 1024 == 0 && TILE_SMEM <= 112 * 1024, "tile stage layout");
   static_assert(SHRINK_SMEM <= 112 * 1024 && EXPAND_SMEM <= 112 * 1024, "two CTAs per SM");
 };
@@ -934,7 +938,7 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
 }
 
 template <int R>
-__global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
+__global__ void __launch_bounds__(SimtCfg<R>::TILE_THREADS, 2)
     simt_expand_tile_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   using C = SimtCfg<R>;
   extern __shared__ uint8_t smem_raw[];
@@ -944,11 +948,18 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::TNST), empty + C::TNST + kQD,
                     empty + C::TNST + 2 * kQD};
   ExpandRec* recs = reinterpret_cast<ExpandRec*>(empty + C::TNST + 3 * kQD);
+  ExpandRec* rres = recs + kQD;                                    // [kRQ] resolved items
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(rres + C::kRQ);   // [kRQ]
+  uint64_t* rempty = rfull + C::kRQ;                               // [kRQ]
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::TNST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NWC);
+    }
+    for (int s = 0; s < C::kRQ; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], 1);
     }
     wq.init(C::NWC);
     fence_mbar_init();
@@ -956,21 +967,69 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   __syncthreads();
 
   const int warp = warp_id(), lane = lane_id();
-  if (warp == C::NWC) {
-    // ===================== producer: resolve items; B rows, v rows, y chunks =====================
+  const int n_groups = pd.counts[kCntGroups];
+  const long long n_items = (long long)n_groups * args.total_ci;
+  if (warp == C::NWC + 1) {
+    // ===================== resolver: claims items and resolves their group, rows, scale
+    // up to kRQ items ahead of the producer, so the producer's copies never wait on
+    // the dependent claim -> group -> row-index loads of an item =====================
     if (lane == 0) {
-      const int n_groups = pd.counts[kCntGroups];
-      const long long n_items = (long long)n_groups * args.total_ci;
+      unsigned long long* ctr = pd.wctr + kWqSimtExpand;
+      QueuePos rp;
+      for (;;) {
+        long long it = (long long)atomicAdd(ctr, 1ull);
+        if (it >= n_items) it = -1;
+        int ti = 0, ci = 0;
+        int4 g = make_int4(0, 0, 0, 0);
+        float s_a = 0.f;
+        int rows[C::GR];
+#pragma unroll
+        for (int r = 0; r < C::GR; ++r) rows[r] = 0;
+        if (it >= 0) {
+          const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
+          ti = find_task_ci(args, cig);
+          const SlotTask& t = args.t[ti];
+          ci = cig - t.ci_base;
+          g = pd.groups[gi];
+          s_a = args.scale[g.z / t.E];
+#pragma unroll
+          for (int r = 0; r < C::GR; ++r) rows[r] = r < g.y ? __ldg(pd.perm + g.x + r) : 0;
+        }
+        mbar_wait(&rempty[rp.slot], rp.phase ^ 1);
+        ExpandRec& q = rres[rp.slot];
+        q.it = it;
+        q.task = ti;
+        q.ci = ci;
+        q.g = g;
+        q.s_a = s_a;
+#pragma unroll
+        for (int r = 0; r < C::GR; ++r) q.rows[r] = rows[r];
+        mbar_arrive(&rfull[rp.slot]);
+        rp.advance(C::kRQ);
+        if (it < 0) break;
+      }
+    }
+  } else if (warp == C::NWC) {
+    // ===================== producer: B rows, v rows, y chunks of resolved items =====================
+    if (lane == 0) {
       const bool load_y = args.y_store == 0 && !args.y_fp32;
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      QueuePos qp;
-      unsigned long long* ctr = pd.wctr + kWqSimtExpand;
+      QueuePos qp, rp;
       bool shrink_done = false;
       for (;;) {
-        long long it = (long long)atomicAdd(ctr, 1ull);
-        if (it >= n_items) it = -1;
+        mbar_wait(&rfull[rp.slot], rp.phase);
+        const ExpandRec& q = rres[rp.slot];
+        const long long it = q.it;
+        const int ti = q.task, ci = q.ci;
+        const int4 g = q.g;
+        const float s_a = q.s_a;
+        int rows[C::GR];
+#pragma unroll
+        for (int r = 0; r < C::GR; ++r) rows[r] = q.rows[r];
+        mbar_arrive(&rempty[rp.slot]);
+        rp.advance(C::kRQ);
         mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
         ExpandRec& rc = recs[qp.slot];
         if (it < 0) {
@@ -978,20 +1037,13 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
           mbar_arrive(&wq.full[qp.slot]);
           break;
         }
-        const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
-        const int ti = find_task_ci(args, cig);
         const SlotTask& t = args.t[ti];
-        const int ci = cig - t.ci_base;
-        const int4 g = pd.groups[gi];
         const long long unit = store_unit(g.z, t.E, args.pl, args.cache);
         const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
         const float* vsrc = pd.vpart + t.vpart_off + (long long)g.x * R;
         const int n_st = t.CI / t.SC;
         const uint32_t bytes = (uint32_t)t.SC * R * 2, vbytes = (uint32_t)g.y * R * 4;
         const uint32_t ybytes = load_y ? (uint32_t)t.SC * 2 : 0u;
-        int rows[C::GR];
-#pragma unroll
-        for (int r = 0; r < C::GR; ++r) rows[r] = r < g.y ? __ldg(pd.perm + g.x + r) : 0;
         const uint16_t* ybase = static_cast<const uint16_t*>(t.y) + (long long)ci * t.CI;
         for (int st = 0; st < n_st; ++st) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -1019,7 +1071,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
             rc.task = ti;
             rc.ci = ci;
             rc.g = g;
-            rc.s_a = args.scale[g.z / t.E];
+            rc.s_a = s_a;
 #pragma unroll
             for (int r = 0; r < C::GR; ++r) rc.rows[r] = rows[r];
             mbar_arrive(&wq.full[qp.slot]);
@@ -1084,7 +1136,8 @@ cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, 
     static unsigned long long tmask = 0;
     cudaError_t e = set_smem_once(simt_expand_tile_kernel<R>, C::TILE_SMEM, tmask);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(simt_expand_tile_kernel<R>, dim3(2 * grid), dim3(C::THREADS), C::TILE_SMEM, stream, args, pd);
+    e = launch_pdl(simt_expand_tile_kernel<R>, dim3(2 * grid), dim3(C::TILE_THREADS), C::TILE_SMEM, stream, args,
+                   pd);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
     }
