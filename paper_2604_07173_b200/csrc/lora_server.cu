@@ -727,8 +727,9 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       }
       fill_task_tables(sargs);
     }
-    if (tc && s->tc_ci_max > 0) {
-      // tcgen05 expand items: CI columns of one tile (tuning hook LORA_TC_CI_MAX)
+    if (tc && s->tc_ci_max > 0 && p->T >= kTcWideKRows) {
+      // large batches: tcgen05 expand items of up to tc_ci_max columns of one
+      // tile (decode-sized batches have few tiles and keep the slot's CI)
       int ci3 = 0;
       for (int i = 0; i < nb; ++i) {
         SlotTask& t = args.t[i];

@@ -59,7 +59,15 @@ struct SimtCfg {
   static constexpr int RED_BYTES = (SMALL_K ? NWC : NJG) * GR * R * 4;
   static constexpr int NST_RAW = (SMEM_BUDGET - RED_BYTES) / S_STAGE;
   static constexpr int NST = NST_RAW > 8 ? 8 : (NST_RAW < 2 ? 2 : NST_RAW);
-  static constexpr int SHRINK_SMEM = 1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8 + kQD * 16;
+  // + at r <= 32 a resolver warp running kSRQ items ahead of the producer
+  // (ShrinkRes ring; measured: Llama r = 16 shrink 253 -> 232 us, but at r = 64
+  // the extra warp's register cap costs spills: 178 -> 239 us, so r = 64 keeps
+  // the producer resolving its own items)
+  static constexpr bool SHRINK_RESOLVER = R <= 32;
+  static constexpr int kSRQ = 4;
+  static constexpr int SHRINK_THREADS = NCT + (SHRINK_RESOLVER ? 64 : 32);
+  static constexpr int SHRINK_SMEM =
+      1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8 + kQD * 16 + kSRQ * (96 + 16);
   // expand: CPT output columns per consumer thread (c = ct + i*NCT); at r <= 32
   // two columns share one FFMA2 (more B and y bytes per stage at small r)
   static constexpr int CPT = R >= 64 ? 1 : 2;
@@ -298,8 +306,17 @@ LORA_DEVINL void shrink_dispatch(uint8_t* smem, uint64_t* full, uint64_t* empty,
     shrink_item<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane);
 }
 
+// a shrink item as resolved by the resolver warp: group and x row offsets
+struct ShrinkRes {
+  long long it;  // -1: end of the stream
+  int ti, pad;
+  int4 g;
+  long long xrow[kGroupRows];
+};
+static_assert(sizeof(ShrinkRes) == 96, "resolved record size");
+
 template <int R, bool REMOTE>
-__global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
+__global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
     simt_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   using C = SimtCfg<R>;
   extern __shared__ uint8_t smem_raw[];
@@ -309,11 +326,18 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   uint64_t* empty = full + C::NST;
   WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::NST), empty + C::NST + kQD, empty + C::NST + 2 * kQD};
   int4* gq = reinterpret_cast<int4*>(empty + C::NST + 3 * kQD);  // [kQD] group of each queued item
+  ShrinkRes* rres = reinterpret_cast<ShrinkRes*>(gq + kQD);        // [kSRQ] resolved items
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(rres + C::kSRQ);   // [kSRQ]
+  uint64_t* rempty = rfull + C::kSRQ;                              // [kSRQ]
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NWC);
+    }
+    for (int s = 0; s < C::kSRQ; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], 1);
     }
     wq.init(C::NWC);
     fence_mbar_init();
@@ -326,20 +350,72 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   const long long n_items = (long long)n_groups * args.n_tasks;
   const int warp = warp_id(), lane = lane_id();
 
-  if (warp == C::NWC) {
+  // claim the next item and resolve its group and x rows: x row r of the group
+  // is t.x + xrow[r] (REMOTE: xrow[r] is relative to t.x, pointing into a
+  // source's send buffer)
+  auto resolve = [&](long long& it, int& ti, int4& g, long long* xrow) {
+    it = (long long)atomicAdd(pd.wctr + kWqSimtShrink, 1ull);
+    if (it >= n_items) it = -1;
+    ti = it < 0 ? 0 : (int)(it / n_groups);
+    g = it < 0 ? make_int4(0, 0, 0, 0) : pd.groups[(int)(it - (long long)ti * n_groups)];
+    const SlotTask& t = args.t[ti];
+#pragma unroll
+    for (int r = 0; r < C::GR; ++r) {
+      if constexpr (REMOTE)
+        xrow[r] = r < g.y ? x_row<true>(args, ti, pd.perm[g.x + r]) - t.x : 0;
+      else
+        xrow[r] = r < g.y ? (long long)pd.perm[g.x + r] * t.h_in : 0;
+    }
+  };
+
+  if (C::SHRINK_RESOLVER && warp == C::NWC + 1) {
+    // ===================== resolver: up to kSRQ items ahead of the producer =====================
+    if (lane == 0) {
+      QueuePos rp;
+      for (;;) {
+        long long it;
+        int ti;
+        int4 g;
+        long long xrow[C::GR];
+        resolve(it, ti, g, xrow);
+        mbar_wait(&rempty[rp.slot], rp.phase ^ 1);
+        ShrinkRes& q = rres[rp.slot];
+        q.it = it;
+        q.ti = ti;
+        q.g = g;
+#pragma unroll
+        for (int r = 0; r < C::GR; ++r) q.xrow[r] = xrow[r];
+        mbar_arrive(&rfull[rp.slot]);
+        rp.advance(C::kSRQ);
+        if (it < 0) break;
+      }
+    }
+  } else if (warp == C::NWC) {
     // ===================== producer =====================
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      QueuePos qp;
+      QueuePos qp, rp;
       for (;;) {
-        // the producer resolves the item's group and publishes it with the
-        // item, so consumers never wait on a global load per item
-        long long it = (long long)atomicAdd(pd.wctr + kWqSimtShrink, 1ull);
-        if (it >= n_items) it = -1;
-        const int ti = it < 0 ? 0 : (int)(it / n_groups);
-        const int4 g = it < 0 ? make_int4(0, 0, 0, 0) : pd.groups[(int)(it - (long long)ti * n_groups)];
+        long long it;
+        int ti;
+        int4 g;
+        long long xrow[C::GR];
+        if constexpr (C::SHRINK_RESOLVER) {
+          mbar_wait(&rfull[rp.slot], rp.phase);
+          const ShrinkRes& q = rres[rp.slot];
+          it = q.it;
+          ti = q.ti;
+          g = q.g;
+#pragma unroll
+          for (int r = 0; r < C::GR; ++r) xrow[r] = q.xrow[r];
+          mbar_arrive(&rempty[rp.slot]);
+          rp.advance(C::kSRQ);
+        } else {
+          resolve(it, ti, g, xrow);
+        }
+        // the item and its group go to the consumers through the queue
         mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
         wq.item[qp.slot] = it;
         gq[qp.slot] = g;
@@ -351,16 +427,6 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
         const uint16_t* abase = t.At + unit * (long long)t.h_in * R;
         const int n_st = t.h_in / t.SJ;
         const uint32_t a_bytes = (uint32_t)R * t.SJ * 2, x_bytes = (uint32_t)t.SJ * 2;
-        // x row r of the group: t.x + xrow[r] (REMOTE: xrow[r] is relative to t.x,
-        // pointing into a source's send buffer)
-        long long xrow[C::GR];
-#pragma unroll
-        for (int r = 0; r < C::GR; ++r) {
-          if constexpr (REMOTE)
-            xrow[r] = r < g.y ? x_row<true>(args, ti, pd.perm[g.x + r]) - t.x : 0;
-          else
-            xrow[r] = r < g.y ? (long long)pd.perm[g.x + r] * t.h_in : 0;
-        }
         for (int st = 0; st < n_st; ++st) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::S_STAGE;
@@ -1114,7 +1180,7 @@ cudaError_t launch_shrink_t(const MultiArgs& args, const PlanDev& pd, int grid, 
   auto kern = remote ? simt_shrink_kernel<R, true> : simt_shrink_kernel<R, false>;
   cudaError_t e = set_smem_once(kern, C::SHRINK_SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kern, dim3(2 * grid), dim3(C::THREADS), C::SHRINK_SMEM, stream, args, pd);
+  e = launch_pdl(kern, dim3(2 * grid), dim3(C::SHRINK_THREADS), C::SHRINK_SMEM, stream, args, pd);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
