@@ -85,11 +85,14 @@ struct SimtCfg {
   static constexpr int Y_SLOT = GR * SC_MAX * 2;
   static constexpr int META = 128;  // StageRec
   // every byte of the 112 KB two-CTA share not used by the fixed parts goes to B stages
-  static constexpr int E_FIXED = 1024 + YS * (Y_SLOT + META) + 2 * 16 * 8 + 3 * kQD * 8 + kQD * 80;
-  static constexpr int NSTE_RAW = (112 * 1024 - E_FIXED) / E_STAGE;
+  // + a resolver warp kERQ items ahead of the producer (ExpandRec ring + barriers)
+  static constexpr int kERQ = 2;
+  static constexpr int E_THREADS = NCT + 64;
+  static constexpr int E_FIXED = 1024 + YS * (Y_SLOT + META) + 3 * kQD * 8 + kQD * 80 + kERQ * (80 + 16);
+  static constexpr int NSTE_RAW = (112 * 1024 - E_FIXED) / (E_STAGE + 16);  // a stage + its two barriers
   static constexpr int NSTE = NSTE_RAW > 16 ? 16 : (NSTE_RAW < 2 ? 2 : NSTE_RAW);
   static constexpr int EXPAND_SMEM =
-      1024 + NSTE * E_STAGE + YS * (Y_SLOT + META) + 2 * NSTE * 8 + 3 * kQD * 8 + kQD * 80;
+      1024 + NSTE * E_STAGE + YS * (Y_SLOT + META) + 2 * NSTE * 8 + 3 * kQD * 8 + kQD * 80 + kERQ * (80 + 16);
   // the look-ahead pops items the producer has published only if YD - 1 <= NSTE
   // The producer publishes an item after issuing its first stage; at stage s
   // (after releasing it) the consumers' look-ahead takes the item holding
@@ -113,6 +116,7 @@ struct SimtCfg {
   static constexpr int TILE_SMEM = 1024 + TNST * T_STAGE + 2 * TNST * 8 + 3 * kQD * 8 + kQD * 80 + kRQ * (80 + 16);
   static_assert(T_STAGE % 1024 == 0 && TILE_SMEM <= 112 * 1024, "tile stage layout");
   static_assert(SHRINK_SMEM <= 112 * 1024 && EXPAND_SMEM <= 112 * 1024, "two CTAs per SM");
+  static_assert(R != 64 || NSTE == 3, "r = 64 expand keeps three 34 KB stages");
 };
 
 LORA_DEVINL uint8_t* align1024(uint8_t* p) {
@@ -651,12 +655,70 @@ struct StageRec {
 };
 static_assert(sizeof(StageRec) <= 128, "stage record size");
 
+// Expand resolver warp (lane 0): claims items and resolves their group, row
+// indices and scale up to nrq items ahead of the copy-issuing producer, so
+// the producer never waits on an item's dependent claim -> group -> row loads.
+__device__ __forceinline__ void expand_resolver(const MultiArgs& args, const PlanDev& pd, int n_groups,
+                                                long long n_items, ExpandRec* rres, uint64_t* rfull,
+                                                uint64_t* rempty, int nrq) {
+  unsigned long long* ctr = pd.wctr + kWqSimtExpand;
+  QueuePos rp;
+  for (;;) {
+    long long it = (long long)atomicAdd(ctr, 1ull);
+    if (it >= n_items) it = -1;
+    int ti = 0, ci = 0;
+    int4 g = make_int4(0, 0, 0, 0);
+    float s_a = 0.f;
+    int rows[kGroupRows];
+#pragma unroll
+    for (int r = 0; r < kGroupRows; ++r) rows[r] = 0;
+    if (it >= 0) {
+      const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
+      ti = find_task_ci(args, cig);
+      const SlotTask& t = args.t[ti];
+      ci = cig - t.ci_base;
+      g = pd.groups[gi];
+      s_a = args.scale[g.z / t.E];
+#pragma unroll
+      for (int r = 0; r < kGroupRows; ++r) rows[r] = r < g.y ? __ldg(pd.perm + g.x + r) : 0;
+    }
+    mbar_wait(&rempty[rp.slot], rp.phase ^ 1);
+    ExpandRec& q = rres[rp.slot];
+    q.it = it;
+    q.task = ti;
+    q.ci = ci;
+    q.g = g;
+    q.s_a = s_a;
+#pragma unroll
+    for (int r = 0; r < kGroupRows; ++r) q.rows[r] = rows[r];
+    mbar_arrive(&rfull[rp.slot]);
+    rp.advance(nrq);
+    if (it < 0) break;
+  }
+}
+
+// producer side: the next resolved item (copied out, slot released)
+__device__ __forceinline__ void expand_take(ExpandRec* rres, uint64_t* rfull, uint64_t* rempty, QueuePos& rp, int nrq,
+                                            long long& it, int& ti, int& ci, int4& g, float& s_a, int* rows) {
+  mbar_wait(&rfull[rp.slot], rp.phase);
+  const ExpandRec& q = rres[rp.slot];
+  it = q.it;
+  ti = q.task;
+  ci = q.ci;
+  g = q.g;
+  s_a = q.s_a;
+#pragma unroll
+  for (int r = 0; r < kGroupRows; ++r) rows[r] = q.rows[r];
+  mbar_arrive(&rempty[rp.slot]);
+  rp.advance(nrq);
+}
+
 template <int R, int M>
 __device__ __forceinline__ void simt_expand_consumers(const MultiArgs& args, uint8_t* smem, uint64_t* full,
                                                       uint64_t* empty, WorkQueue<kQD>& wq, const ExpandRec* recs);
 
 template <int R>
-__global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
+__global__ void __launch_bounds__(SimtCfg<R>::E_THREADS, 2)
     simt_expand_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   using C = SimtCfg<R>;
   extern __shared__ uint8_t smem_raw[];
@@ -666,11 +728,18 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   WorkQueue<kQD> wq{reinterpret_cast<long long*>(empty + C::NSTE), empty + C::NSTE + kQD,
                     empty + C::NSTE + 2 * kQD};
   ExpandRec* recs = reinterpret_cast<ExpandRec*>(empty + C::NSTE + 3 * kQD);
+  ExpandRec* rres = recs + kQD;                                    // [kERQ] resolved items
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(rres + C::kERQ);  // [kERQ]
+  uint64_t* rempty = rfull + C::kERQ;                              // [kERQ]
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NSTE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NWC);
+    }
+    for (int s = 0; s < C::kERQ; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], 1);
     }
     wq.init(C::NWC);
     fence_mbar_init();
@@ -678,21 +747,26 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
   __syncthreads();
 
   const int warp = warp_id(), lane = lane_id();
+  const int n_groups = pd.counts[kCntGroups];
+  const long long n_items = (long long)n_groups * args.total_ci;
 
-  if (warp == C::NWC) {
-    // ===================== producer: resolve items, B rows + the group's v rows =====================
+  if (warp == C::NWC + 1) {
+    if (lane == 0) expand_resolver(args, pd, n_groups, n_items, rres, rfull, rempty, C::kERQ);
+  } else if (warp == C::NWC) {
+    // ===================== producer: B rows + the group's v rows of resolved items =====================
     if (lane == 0) {
-      const int n_groups = pd.counts[kCntGroups];
-      const long long n_items = (long long)n_groups * args.total_ci;
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      QueuePos qp;
-      unsigned long long* ctr = pd.wctr + kWqSimtExpand;
+      QueuePos qp, rp;
       bool shrink_done = false;
       for (;;) {
-        long long it = (long long)atomicAdd(ctr, 1ull);
-        if (it >= n_items) it = -1;
+        long long it;
+        int ti, ci;
+        int4 g;
+        float s_a;
+        int rows[C::GR];
+        expand_take(rres, rfull, rempty, rp, C::kERQ, it, ti, ci, g, s_a, rows);
         mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
         ExpandRec& rc = recs[qp.slot];
         if (it < 0) {
@@ -700,11 +774,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
           mbar_arrive(&wq.full[qp.slot]);
           break;
         }
-        const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
-        const int ti = find_task_ci(args, cig);
         const SlotTask& t = args.t[ti];
-        const int ci = cig - t.ci_base;
-        const int4 g = pd.groups[gi];
         const long long unit = store_unit(g.z, t.E, args.pl, args.cache);
         const uint16_t* bbase = t.Bt + (unit * t.h_out + (long long)ci * t.CI) * R;
         const float* vsrc = pd.vpart + t.vpart_off + (long long)g.x * R;
@@ -731,9 +801,9 @@ __global__ void __launch_bounds__(SimtCfg<R>::THREADS, 2)
             rc.task = ti;
             rc.ci = ci;
             rc.g = g;
-            rc.s_a = args.scale[g.z / t.E];
+            rc.s_a = s_a;
 #pragma unroll
-            for (int r = 0; r < C::GR; ++r) rc.rows[r] = r < g.y ? __ldg(pd.perm + g.x + r) : 0;
+            for (int r = 0; r < C::GR; ++r) rc.rows[r] = rows[r];
             mbar_arrive(&wq.full[qp.slot]);
             qp.advance(kQD);
           }
@@ -1036,45 +1106,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::TILE_THREADS, 2)
   const int n_groups = pd.counts[kCntGroups];
   const long long n_items = (long long)n_groups * args.total_ci;
   if (warp == C::NWC + 1) {
-    // ===================== resolver: claims items and resolves their group, rows, scale
-    // up to kRQ items ahead of the producer, so the producer's copies never wait on
-    // the dependent claim -> group -> row-index loads of an item =====================
-    if (lane == 0) {
-      unsigned long long* ctr = pd.wctr + kWqSimtExpand;
-      QueuePos rp;
-      for (;;) {
-        long long it = (long long)atomicAdd(ctr, 1ull);
-        if (it >= n_items) it = -1;
-        int ti = 0, ci = 0;
-        int4 g = make_int4(0, 0, 0, 0);
-        float s_a = 0.f;
-        int rows[C::GR];
-#pragma unroll
-        for (int r = 0; r < C::GR; ++r) rows[r] = 0;
-        if (it >= 0) {
-          const int cig = (int)(it / n_groups), gi = (int)(it - (long long)cig * n_groups);
-          ti = find_task_ci(args, cig);
-          const SlotTask& t = args.t[ti];
-          ci = cig - t.ci_base;
-          g = pd.groups[gi];
-          s_a = args.scale[g.z / t.E];
-#pragma unroll
-          for (int r = 0; r < C::GR; ++r) rows[r] = r < g.y ? __ldg(pd.perm + g.x + r) : 0;
-        }
-        mbar_wait(&rempty[rp.slot], rp.phase ^ 1);
-        ExpandRec& q = rres[rp.slot];
-        q.it = it;
-        q.task = ti;
-        q.ci = ci;
-        q.g = g;
-        q.s_a = s_a;
-#pragma unroll
-        for (int r = 0; r < C::GR; ++r) q.rows[r] = rows[r];
-        mbar_arrive(&rfull[rp.slot]);
-        rp.advance(C::kRQ);
-        if (it < 0) break;
-      }
-    }
+    if (lane == 0) expand_resolver(args, pd, n_groups, n_items, rres, rfull, rempty, C::kRQ);
   } else if (warp == C::NWC) {
     // ===================== producer: B rows, v rows, y chunks of resolved items =====================
     if (lane == 0) {
@@ -1085,17 +1117,12 @@ __global__ void __launch_bounds__(SimtCfg<R>::TILE_THREADS, 2)
       QueuePos qp, rp;
       bool shrink_done = false;
       for (;;) {
-        mbar_wait(&rfull[rp.slot], rp.phase);
-        const ExpandRec& q = rres[rp.slot];
-        const long long it = q.it;
-        const int ti = q.task, ci = q.ci;
-        const int4 g = q.g;
-        const float s_a = q.s_a;
+        long long it;
+        int ti, ci;
+        int4 g;
+        float s_a;
         int rows[C::GR];
-#pragma unroll
-        for (int r = 0; r < C::GR; ++r) rows[r] = q.rows[r];
-        mbar_arrive(&rempty[rp.slot]);
-        rp.advance(C::kRQ);
+        expand_take(rres, rfull, rempty, rp, C::kRQ, it, ti, ci, g, s_a, rows);
         mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
         ExpandRec& rc = recs[qp.slot];
         if (it < 0) {
@@ -1211,7 +1238,7 @@ cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, 
   static unsigned long long mask = 0;
   cudaError_t e = set_smem_once(simt_expand_kernel<R>, C::EXPAND_SMEM, mask);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(simt_expand_kernel<R>, dim3(2 * grid), dim3(C::THREADS), C::EXPAND_SMEM, stream, args, pd);
+  e = launch_pdl(simt_expand_kernel<R>, dim3(2 * grid), dim3(C::E_THREADS), C::EXPAND_SMEM, stream, args, pd);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
