@@ -447,6 +447,17 @@ def run_ours(args, cfg, batch, slots):
             b = per_kind_bytes.get(n)
             if b:
                 kern[n]["algorithmic_GBs"] = b * n_prof / kern[n]["launches"] / (kern[n]["ms_per_launch"] * 1e-3) / 1e9
+    if sharded and roofline is None:
+        # sharded step: the slowest rank's algorithmic HBM bytes (placement
+        # model, SURVEY 8d per rank) over the max-over-ranks step time
+        rb_ = PL.rank_hbm_bytes(batch.adapter_ids, batch.expert_ids if E > 1 else None, src, world, n_rep, ub, rb,
+                                ep=ep_mode)
+        achieved = float(rb_.max()) / (ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": None, "kernel": "step (slowest rank, all kernels)",
+                    "algorithmic_bytes_per_launch": float(rb_.max()), "peak_source": peak_src,
+                    "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS,
+                    "timing": "CUDA events on the launching stream over the timed region, max over ranks"}
     # kernels per step counted in the profiling pass (same steps, same launches)
     launches = int(round(sum(n for n, _ in prof.values()) / n_prof * args.steps))
     step_gbs = alg["total"] / (ms * 1e-3) / 1e9

@@ -31,6 +31,26 @@ def owner(adapter_ids: np.ndarray, world: int, n_hot: int, src: np.ndarray, expe
     return np.where((a >= 0) & (a < n_hot), np.asarray(src, np.int64), own)
 
 
+def rank_hbm_bytes(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray], src: np.ndarray, world: int,
+                   n_hot: int, unit_bytes: float, row_bytes: float, ep: bool = False) -> np.ndarray:
+    """Algorithmic HBM bytes per rank of one sharded apply (SURVEY 8d per
+    rank): each unit the rank serves read once, each row it serves read and
+    written once, each of its rows served elsewhere accumulated once."""
+    a = np.asarray(adapter_ids, np.int64)
+    e = np.zeros_like(a) if expert_ids is None else np.asarray(expert_ids, np.int64)
+    src = np.asarray(src, np.int64)
+    own = owner(a, world, n_hot, src, e, ep)
+    valid = a >= 0
+    n_e = int(e.max()) + 1 if e.size else 1
+    key = a * n_e + e
+    out = np.zeros(world)
+    for g in range(world):
+        mine = valid & (own == g)
+        remote_out = int(np.sum(valid & (src == g) & (own != g)))
+        out[g] = np.unique(key[mine]).size * unit_bytes + int(mine.sum()) * row_bytes + remote_out * row_bytes
+    return out
+
+
 def rank_costs(adapter_ids: np.ndarray, expert_ids: Optional[np.ndarray], src: np.ndarray, world: int, n_hot: int,
                unit_bytes: float, row_bytes: float, xfer_bytes: float, hbm_gbs: float = 6500.0,
                link_gbs: float = 700.0, ep: bool = False) -> np.ndarray:
