@@ -629,6 +629,7 @@ def test_small_rank_bf16_full_parity(B, rank):
 
 @pytest.mark.parametrize("loopback,y_dtype,rank,transport", [
     (False, "bf16", 64, "p2p"), (True, "fp32", 64, "p2p"), (True, "bf16", 64, "p2p"), (True, "bf16", 16, "p2p"),
+    (True, "fp32", 16, "p2p"), (True, "fp32", 8, "nccl"),
     (True, "fp32", 64, "nccl"), (True, "bf16", 64, "nccl")])
 def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
     """Sharded server at G = 1.  In place (no exchange): bit-identical to the
