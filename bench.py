@@ -148,11 +148,11 @@ def oracle_sample(cfg, batch, slots, n_tokens):
     return [orc.prepare_slot(cfg, i, batch, rows) for i in slots]
 
 
-def oracle_time(prepared):
+def oracle_time(prepared, n_threads: int = 0):
     from oracle import oracle as orc
     t0 = time.perf_counter()
     for (x, uor, sor, A, B, y) in prepared:
-        orc.lora_apply_rows(x, uor, sor, A, B, y.copy())
+        orc.lora_apply_rows(x, uor, sor, A, B, y.copy(), n_threads=n_threads)
     return time.perf_counter() - t0
 
 
@@ -169,10 +169,15 @@ def cpu_baseline(cfg, batch, slots, budget_s=10.0):
             break
         n = min(batch.n_tokens, max(n * 2, int(n * (budget_s / 4) / max(dt, 1e-3))))
     n, dt = best
+    # the same oracle on one thread (--threads 1 and --threads nproc)
+    n1 = max(1, min(n, int(n * 2.0 / max(dt * orc.max_threads(), 1e-3))))
+    dt1 = oracle_time(prep if n1 == n else oracle_sample(cfg, batch, slots, n1), n_threads=1)
     return {"value": n / dt, "unit": UNIT, "cores": orc.max_threads(), "kind": "oracle",
             "sample": f"first {n} of {batch.n_tokens} tokens ({n * batch.top_k} rows) of the {cfg.name} batch, "
                       f"{len(slots)} slots; plain-C fp64 oracle, OpenMP over rows; input generation excluded; "
-                      f"one pass = {dt:.2f} s"}
+                      f"one pass = {dt:.2f} s",
+            "single_thread": {"value": n1 / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"first {n1} tokens, one pass = {dt1:.2f} s"}}
 
 
 def run_reference(args, cfg, batch, slots):

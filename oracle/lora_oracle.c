@@ -85,12 +85,14 @@ int oracle_lora_apply(int64_t T, int32_t h_in, int32_t h_out, int32_t r,
     for (int64_t i = 0; i < T; ++i)
         if (unit_of_row[i] >= U) return -1;
 #ifdef _OPENMP
-    if (n_threads > 0) omp_set_num_threads(n_threads);
+    /* per-call thread count (a num_threads clause, so the library default is
+       not changed for later calls) */
+    const int nt = n_threads > 0 ? n_threads : omp_get_max_threads();
 #else
     (void)n_threads;
 #endif
     int bad = 0;
-#pragma omp parallel
+#pragma omp parallel num_threads(nt)
     {
         double *v = (double *)malloc(sizeof(double) * (size_t)r);
         double *d = (double *)malloc(sizeof(double) * (size_t)h_out);
