@@ -513,11 +513,17 @@ struct ExpandCfg {
   static constexpr int THREADS = 18 * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (N)
   static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
-  static constexpr int NST = 4;
+#ifndef LORA_TCE_NST
+#define LORA_TCE_NST 2
+#endif
+#ifndef LORA_TCE_YD
+#define LORA_TCE_YD 4
+#endif
+  static constexpr int NST = LORA_TCE_NST;
   static constexpr int V_TILE = kTileRows * 128;       // 16 KB (M = 128 rows x 64 bf16)
   // bf16 output: y tiles [128 rows][128 cols] (16-byte chunks XOR-swizzled by
   // row) in a ring of YS slots, fetched YD-1 sub-tiles ahead
-  static constexpr int YD = 3;
+  static constexpr int YD = LORA_TCE_YD;
   static constexpr int YS = YD + 1;
   static constexpr int Y_TILE = kTileRows * MSUB * 2;  // 32 KB
   static constexpr int NACC = 4;
