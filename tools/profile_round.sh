@@ -25,4 +25,8 @@ timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'simt_shrink|simt_expand|tc_shrink|tc_expand' -s 4 -c 4 \
     -o $OUT/full_mixtral_prefill python bench.py --workload mixtral_prefill --steps 2 --warmup 3 --no-cpu-baseline \
     --e2e-steps 0 > $OUT/ncu_full_prefill.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:'simt_shrink|simt_expand' -s 4 -c 2 \
+    -o $OUT/full_llama_decode python bench.py --workload llama_decode --steps 2 --warmup 3 --no-cpu-baseline \
+    --e2e-steps 0 > $OUT/ncu_full_llama.log 2>&1
 echo done
