@@ -75,7 +75,13 @@ struct SimtCfg {
       1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8 + kQD * 16 + kSRQ * (96 + 16);
   // expand: CPT output columns per consumer thread (c = ct + i*NCT); at r <= 32
   // two columns share one FFMA2 (more B and y bytes per stage at small r)
-  static constexpr int CPT = R >= 64 ? 1 : 2;
+#ifndef LORA_SMALLR_CPT
+#define LORA_SMALLR_CPT 2
+#endif
+  // r <= 16: LORA_SMALLR_CPT columns per thread (4 = 32 KB B stages, staged-tile
+  // expand only; measured slower: Llama expand 185 -> 238 us)
+  static constexpr int CPT = R >= 64 ? 1 : (R <= 16 ? LORA_SMALLR_CPT : 2);
+  static constexpr bool LOOKAHEAD_OK = CPT <= 2;  // the look-ahead expand's y ring fits
   static constexpr int SC_MAX = NCT * CPT;
   static constexpr int B_STAGE = SC_MAX * R * 2;
   static constexpr int V_BYTES = GR * R * 4;  // v rows of the group (fp32)
@@ -102,7 +108,7 @@ struct SimtCfg {
   // The producer publishes an item after issuing its first stage; at stage s
   // (after releasing it) the consumers' look-ahead takes the item holding
   // stage s+YD, whose first stage needs stage s+YD-NSTE released: YD <= NSTE.
-  static_assert(YD <= NSTE, "y look-ahead deeper than the B pipeline");
+  static_assert(!LOOKAHEAD_OK || YD <= NSTE, "y look-ahead deeper than the B pipeline");
   static_assert(S_STAGE % 1024 == 0 && E_STAGE % 1024 == 0, "stage alignment");
   // staged-tile expand (r <= 16, simt_expand_tile_kernel): the y tile of a
   // stage travels with its B rows and v rows in one stage buffer, loaded by
@@ -120,7 +126,7 @@ struct SimtCfg {
   static constexpr int TNST = TNST_RAW > 8 ? 8 : (TNST_RAW < 2 ? 2 : TNST_RAW);
   static constexpr int TILE_SMEM = 1024 + TNST * T_STAGE + 2 * TNST * 8 + 3 * kQD * 8 + kQD * 80 + kRQ * (80 + 16);
   static_assert(T_STAGE % 1024 == 0 && TILE_SMEM <= 112 * 1024, "tile stage layout");
-  static_assert(SHRINK_SMEM <= 112 * 1024 && EXPAND_SMEM <= 112 * 1024, "two CTAs per SM");
+  static_assert(SHRINK_SMEM <= 112 * 1024 && (!LOOKAHEAD_OK || EXPAND_SMEM <= 112 * 1024), "two CTAs per SM");
   static_assert(R != 64 || NSTE == 3, "r = 64 expand keeps three 34 KB stages");
 };
 
@@ -1016,9 +1022,10 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
   constexpr int pitch = C::SC_MAX * 2;
   const int lane = lane_id();
   const int ct = threadIdx.x;
-  // store pass mapping: 16-byte chunk ch of rows rsub, rsub + 4, ... (cpr <= 64)
-  const int rsub = ct >> 6, sch = ct & 63;
-  static_assert(C::SC_MAX / 8 <= 64 && C::NCT == 256, "store pass mapping");
+  // store pass mapping: 16-byte chunk sch of rows rsub, rsub + RSTEP, ...
+  constexpr int CPRM = C::SC_MAX / 8, RSTEP = C::NCT / CPRM;
+  const int rsub = ct / CPRM, sch = ct % CPRM;
+  static_assert(C::NCT % CPRM == 0, "store pass mapping");
   int stage = 0;
   uint32_t phase = 0;
   QueuePos qp;
@@ -1058,7 +1065,7 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
         named_bar_sync(1, C::NCT);  // the whole tile is final
         if (sch < (p.sc >> 3)) {
           uint16_t* yb = static_cast<uint16_t*>(p.y) + p.c0 + sch * 8;
-          for (int r = rsub; r < nr; r += 4) {
+          for (int r = rsub; r < nr; r += RSTEP) {
             const uint4 v = lds128(yt + r * pitch + sch * 16);
             *reinterpret_cast<uint4*>(yb + (long long)rc.rows[r] * p.h_out) = v;
           }
@@ -1230,22 +1237,25 @@ template <int R>
 cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   using C = SimtCfg<R>;
   if constexpr (R <= 16) {
-    if (use_tile_expand(R)) {
-    static unsigned long long tmask = 0;
-    cudaError_t e = set_smem_once(simt_expand_tile_kernel<R>, C::TILE_SMEM, tmask);
-    if (e != cudaSuccess) return e;
-    e = launch_pdl(simt_expand_tile_kernel<R>, dim3(2 * grid), dim3(C::TILE_THREADS), C::TILE_SMEM, stream, args,
-                   pd);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    if (!C::LOOKAHEAD_OK || use_tile_expand(R)) {
+      static unsigned long long tmask = 0;
+      cudaError_t e = set_smem_once(simt_expand_tile_kernel<R>, C::TILE_SMEM, tmask);
+      if (e != cudaSuccess) return e;
+      e = launch_pdl(simt_expand_tile_kernel<R>, dim3(2 * grid), dim3(C::TILE_THREADS), C::TILE_SMEM, stream, args,
+                     pd);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
     }
   }
-  static unsigned long long mask = 0;
-  cudaError_t e = set_smem_once(simt_expand_kernel<R>, C::EXPAND_SMEM, mask);
-  if (e != cudaSuccess) return e;
-  e = launch_pdl(simt_expand_kernel<R>, dim3(2 * grid), dim3(C::E_THREADS), C::EXPAND_SMEM, stream, args, pd);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  if constexpr (C::LOOKAHEAD_OK) {
+    static unsigned long long mask = 0;
+    cudaError_t e = set_smem_once(simt_expand_kernel<R>, C::EXPAND_SMEM, mask);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(simt_expand_kernel<R>, dim3(2 * grid), dim3(C::E_THREADS), C::EXPAND_SMEM, stream, args, pd);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
@@ -1297,8 +1307,8 @@ int simt_shrink_smem(int rank) {
 }
 int simt_expand_smem(int rank) {
   switch (rank) {
-    case 8: return std::max(SimtCfg<8>::EXPAND_SMEM, SimtCfg<8>::TILE_SMEM);
-    case 16: return std::max(SimtCfg<16>::EXPAND_SMEM, SimtCfg<16>::TILE_SMEM);
+    case 8: return SimtCfg<8>::LOOKAHEAD_OK ? std::max(SimtCfg<8>::EXPAND_SMEM, SimtCfg<8>::TILE_SMEM) : SimtCfg<8>::TILE_SMEM;
+    case 16: return SimtCfg<16>::LOOKAHEAD_OK ? std::max(SimtCfg<16>::EXPAND_SMEM, SimtCfg<16>::TILE_SMEM) : SimtCfg<16>::TILE_SMEM;
     case 32: return SimtCfg<32>::EXPAND_SMEM;
     default: return SimtCfg<64>::EXPAND_SMEM;
   }
