@@ -138,6 +138,7 @@ struct MultiArgs {
   int total_kc, total_ci;  // sums of n_kc / n_ci
   int y_fp32;
   int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16
+  int tc_cap_k;            // > 0: tcgen05 kernels use at most max(8, tiles * tc_cap_k) CTAs (rest exit at once)
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const int32_t* cache;    // resident-cache mode: unit = cache[a]*E + e (nullptr: placement)
   const float* scale;      // [n_adapters] s_a

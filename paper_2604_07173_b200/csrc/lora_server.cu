@@ -151,6 +151,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (const char* e = std::getenv("LORA_SMALL_SEG_MAX")) s->small_seg_max = std::atoi(e);
   if (const char* e = std::getenv("LORA_TC_KI_MAX")) s->tc_ki_max = std::max(128, std::atoi(e));
   if (const char* e = std::getenv("LORA_TC_CI_MAX")) s->tc_ci_max = std::atoi(e);
+  if (const char* e = std::getenv("LORA_TC_CAP_K")) s->tc_cap_k = std::atoi(e);
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
   if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -664,6 +665,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.n_tasks = nb;
     args.y_fp32 = y_dtype == LORA_FP32;
     args.y_store = store;
+    args.tc_cap_k = s->concurrent_tc ? s->tc_cap_k : 0;
     args.pl = placement(s);
     args.cache = s->d_cache;
     args.scale = s->d_scale;

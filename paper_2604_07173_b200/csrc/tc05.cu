@@ -127,6 +127,14 @@ LORA_DEVINL void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int 
       : "memory");
 }
 
+// CTAs that do work in a tcgen05 launch: with tc_cap_k > 0 a few tiles use a
+// few SMs and leave the others to the concurrent CUDA-core chain
+LORA_DEVINL bool tc_cta_idle(const MultiArgs& args, const PlanDev& pd) {
+  if (args.tc_cap_k <= 0) return false;
+  const long long cap = (long long)pd.counts[kCntTiles] * args.tc_cap_k;
+  return blockIdx.x >= (cap < 8 ? 8 : cap);
+}
+
 // ===========================================================================
 // shrink
 // ===========================================================================
@@ -187,6 +195,11 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
   WorkQueue<kQD> wq{wq_items, reinterpret_cast<uint64_t*>(wq_items + kQD),
                     reinterpret_cast<uint64_t*>(wq_items + kQD) + kQD};
 
+  pdl_wait();  // the plan (segmenter) is complete
+  if (tc_cta_idle(args, pd)) {
+    wq_finish(pd.wctr + kWqTcShrink, pd.wdone + kWqTcShrink);
+    return;
+  }
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     wq.init(C::EPI_WARPS + 1 + 3);  // epilogue, MMA and the producer warps that pop (warp PROD_WARP0 fetches)
@@ -554,6 +567,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   WorkQueue<kQD> wq{wq_items, reinterpret_cast<uint64_t*>(wq_items + kQD),
                     reinterpret_cast<uint64_t*>(wq_items + kQD) + kQD};
 
+  if (tc_cta_idle(args, pd)) {
+    wq_finish(pd.wctr + kWqTcExpand, pd.wdone + kWqTcExpand);
+    return;
+  }
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     wq.init(C::EPI_WARPS + 1);  // epilogue + MMA warps pop; the TMA warp fetches
