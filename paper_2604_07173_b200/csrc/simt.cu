@@ -69,7 +69,10 @@ struct SimtCfg {
   // the extra warp's register cap costs spills: 178 -> 239 us, so r = 64 keeps
   // the producer resolving its own items)
   static constexpr bool SHRINK_RESOLVER = R <= 32;
-  static constexpr int kSRQ = 4;
+#ifndef LORA_RESOLVE_DEPTH
+#define LORA_RESOLVE_DEPTH 1  // items resolved ahead (measured on Llama decode: 1 < 2 < 4 < 8 in step time)
+#endif
+  static constexpr int kSRQ = LORA_RESOLVE_DEPTH;
   static constexpr int SHRINK_THREADS = NCT + (SHRINK_RESOLVER ? 64 : 32);
   static constexpr int SHRINK_SMEM =
       1024 + NST * S_STAGE + RED_BYTES + 2 * NST * 8 + 3 * kQD * 8 + kQD * 16 + kSRQ * (96 + 16);
@@ -120,7 +123,7 @@ struct SimtCfg {
   // + a resolver warp running kRQ items ahead of the producer (ring of
   // resolved ExpandRec records with full/empty barriers)
   static constexpr int TILE_THREADS = NCT + 64;
-  static constexpr int kRQ = 4;
+  static constexpr int kRQ = LORA_RESOLVE_DEPTH;
   static constexpr int T_FIXED = 1024 + 2 * 16 * 8 + 3 * kQD * 8 + kQD * 80 + kRQ * (80 + 16);
   static constexpr int TNST_RAW = (112 * 1024 - T_FIXED) / T_STAGE;
   static constexpr int TNST = TNST_RAW > 8 ? 8 : (TNST_RAW < 2 ? 2 : TNST_RAW);
