@@ -100,7 +100,10 @@ struct SimtCfg {
   static constexpr int META = 128;  // StageRec
   // every byte of the 112 KB two-CTA share not used by the fixed parts goes to B stages
   // + a resolver warp kERQ items ahead of the producer (ExpandRec ring + barriers)
-  static constexpr int kERQ = 2;
+#ifndef LORA_ERQ
+#define LORA_ERQ 2
+#endif
+  static constexpr int kERQ = LORA_ERQ;
   static constexpr int E_THREADS = NCT + 64;
   static constexpr int E_FIXED = 1024 + YS * (Y_SLOT + META) + 3 * kQD * 8 + kQD * 80 + kERQ * (80 + 16);
   static constexpr int NSTE_RAW = (112 * 1024 - E_FIXED) / (E_STAGE + 16);  // a stage + its two barriers
