@@ -32,6 +32,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef LORA_TILE_MAX_R
+#define LORA_TILE_MAX_R 64  // staged-tile expand at every rank (measured: r = 64 expand 1302 -> 1254 us on config 5)
+#endif
+
 namespace lora {
 
 namespace {
@@ -1024,7 +1028,8 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
                                                            uint64_t* empty, WorkQueue<kQD>& wq,
                                                            const ExpandRec* recs) {
   using C = SimtCfg<R>;
-  constexpr bool TILE = M == kOutBf16Acc || M == kOutBf16Store;
+  // CPT == 1 (r = 64): results go to y straight from registers (expand_stage1)
+  constexpr bool TILE = C::CPT > 1 && (M == kOutBf16Acc || M == kOutBf16Store);
   constexpr int pitch = C::SC_MAX * 2;
   const int lane = lane_id();
   const int ct = threadIdx.x;
@@ -1230,19 +1235,19 @@ cudaError_t launch_shrink_t(const MultiArgs& args, const PlanDev& pd, int grid, 
   return cudaGetLastError();
 }
 
-// staged-tile expand for r <= 16 (LORA_EXPAND_V1=1: the look-ahead kernel at every r)
+// staged-tile expand for r <= LORA_TILE_MAX_R (16; LORA_EXPAND_V1=1: the look-ahead kernel at every r)
 inline bool use_tile_expand(int r) {
   static const int v1 = [] {
     const char* e = getenv("LORA_EXPAND_V1");
     return e && e[0] == '1' ? 1 : 0;
   }();
-  return r <= 16 && !v1;
+  return r <= LORA_TILE_MAX_R && !v1;
 }
 
 template <int R>
 cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   using C = SimtCfg<R>;
-  if constexpr (R <= 16) {
+  if constexpr (R <= LORA_TILE_MAX_R) {
     if (!C::LOOKAHEAD_OK || use_tile_expand(R)) {
       static unsigned long long tmask = 0;
       cudaError_t e = set_smem_once(simt_expand_tile_kernel<R>, C::TILE_SMEM, tmask);
