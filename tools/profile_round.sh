@@ -29,4 +29,9 @@ timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'simt_shrink|simt_expand' -s 4 -c 2 \
     -o $OUT/full_llama_decode python bench.py --workload llama_decode --steps 2 --warmup 3 --no-cpu-baseline \
     --e2e-steps 0 > $OUT/ncu_full_llama.log 2>&1
+# summaries on the box; the .ncu-rep files stay there (gpurun_out/ is capped at 64 MiB)
+for r in full_mixtral_sharded full_mixtral_prefill full_llama_decode; do
+  [ -f $OUT/$r.ncu-rep ] && python tools/ncu_summary.py $OUT/$r.ncu-rep > $OUT/sum_$r.txt 2>&1
+done
+mkdir -p /tmp/ncu_reps && mv $OUT/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
 echo done
