@@ -55,3 +55,34 @@ def test_slot_bytes_mixtral():
     assert u == 2 * 64 * 3 * (4096 + 14336)
     assert r == 2 * 4096 + 2 * 14336 + 2 * 2 * (14336 * 2 + 4096)
     assert x == 2 * 4096 + 2 * 14336 + 4 * (14336 * 2 + 4096)
+
+
+def test_rank_hbm_bytes_brute_force():
+    """Per-rank algorithmic bytes of a sharded apply (bench.py's sharded
+    roofline): touched units once, served rows once, own rows served
+    elsewhere accumulated once -- per-row brute force, DP with replication
+    and expert parallel."""
+    rng = np.random.default_rng(9)
+    n = 300
+    a = rng.integers(-1, 16, n)
+    e = rng.integers(0, 4, n)
+    G = 4
+    src = np.repeat(np.arange(G), n // G)
+    U, R = 500.0, 3.0
+    for h, ep in ((0, False), (3, False), (0, True)):
+        got = P.rank_hbm_bytes(a, e, src, G, h, U, R, ep=ep)
+        for g in range(G):
+            units, mine, rout = set(), 0, 0
+            for i in range(n):
+                if a[i] < 0:
+                    continue
+                if ep:
+                    o = int(e[i]) % G
+                else:
+                    o = int(src[i]) if a[i] < h else (a[i] - h) % G
+                if o == g:
+                    units.add((a[i], e[i]))
+                    mine += 1
+                elif src[i] == g:
+                    rout += 1
+            assert abs(got[g] - (len(units) * U + (mine + rout) * R)) < 1e-6, (h, ep, g)
