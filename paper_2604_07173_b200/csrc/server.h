@@ -29,7 +29,7 @@ struct lora_server {
   int max_rows = 0;
   int sm_count = 148;
   int small_seg_max = 8;
-  int tc_cap_k = 4;        // tcgen05 CTAs per tile when both chains run (measured 0/1/2/4: config 5 2.52/2.52/2.51/2.49 ms; env LORA_TC_CAP_K, 0 = all SMs)
+  int tc_cap_k = 2;        // tcgen05 CTAs per tile when both chains run (measured 1/2/4/8 with the staged-tile expand: Mixtral decode 0.478/0.482/0.489/0.494 ms, prefill 0.576/0.561/-/- ms; env LORA_TC_CAP_K, 0 = all SMs)
   int tc_ci_max = 8192;    // tcgen05 expand: max h_out per item (measured best of 1024..8192; env LORA_TC_CI_MAX, 0 = slot CI)
   int tc_ki_max = 1 << 20;  // large-batch tcgen05 shrink: max h_in per item, default the whole h_in (env LORA_TC_KI_MAX)
   int world = 1, shard_rank = 0;
