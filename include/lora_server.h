@@ -195,8 +195,11 @@ lora_status_t lora_apply_plan(lora_server_t *s, const lora_plan_t *p, int32_t sl
 
 /* Several slots sharing one plan in ONE set of launches (e.g. gate, up, down
  * of a MoE layer, or the 128 q/k/v/o slots of a Llama decode step).  slots[n]
- * must be distinct; x[i] / y[i] as in lora_apply_plan (x pointers may repeat,
- * y pointers must be distinct).  slots / x / y are host arrays. */
+ * must be distinct; x[i] / y[i] as in lora_apply_plan.  x buffers may be
+ * shared between slots (e.g. q/k/v); every y byte range (T * h_out elements)
+ * must be disjoint from every other y range and from every x range of the
+ * call (the slots' kernels run concurrently) -- else LORA_ERR_INVALID_ARG,
+ * nothing enqueued.  slots / x / y are host arrays. */
 lora_status_t lora_apply_plan_multi(lora_server_t *s, const lora_plan_t *p, int32_t n,
                                     const int32_t *slots, const void *const *x, void *const *y,
                                     lora_dtype_t y_dtype, void *stream);

@@ -10,6 +10,8 @@ Functions
 - ``lora_apply_rows``    a2-a4 for a set of rows (plain C loops, fp64, lora_oracle.c)
 - ``apply_slot``         convenience: regenerate the touched units of one slot from
                           the seeded generator and run ``lora_apply_rows``
+- ``apply_slot_all_rows`` the same over every row of a batch, regenerating at
+                          most ``unit_chunk`` units at a time (full-size configs)
 - ``shard_dispatch``     the sharded server's dispatch-order rule, so
                           per-rank segment indices can be predicted without GPUs
 
@@ -157,6 +159,39 @@ def apply_slot(cfg: li.Config, slot_index: int, batch: li.Batch, rows: Optional[
     float32 (y_dtype fp32) or bf16 bits (bf16)."""
     args = prepare_slot(cfg, slot_index, batch, rows, y0, seed)
     return lora_apply_rows(*args, n_threads=n_threads)
+
+
+def apply_slot_all_rows(cfg: li.Config, slot_index: int, batch: li.Batch, y0: str = "random",
+                        n_threads: int = 0, seed: Optional[int] = None, unit_chunk: int = 256) -> np.ndarray:
+    """``apply_slot`` over every row of ``batch`` with bounded host memory.
+
+    The rows are partitioned by their unit (a, e); each call of ``apply_slot``
+    covers the rows of at most ``unit_chunk`` distinct units (rows with a = -1
+    go with the first call), so at most ``unit_chunk`` units' A/B are
+    regenerated at a time (config 5 touches ~2100 units of 5 MB per slot).
+    Each row's arithmetic is exactly that of ``lora_apply_rows`` -- only the
+    set of rows per call changes -- so the result equals ``apply_slot(cfg,
+    slot_index, batch)`` bit for bit (pinned in tests/test_oracle_pins.py)."""
+    E = cfg.slots[slot_index].n_experts
+    a = batch.adapter_ids.astype(np.int64)
+    key = np.where(a >= 0, a * E + batch.expert_ids.astype(np.int64), -1)
+    units = np.unique(key[key >= 0])
+    chunks = [units[i:i + unit_chunk] for i in range(0, max(units.size, 1), unit_chunk)]
+    out = None
+    for ci, ch in enumerate(chunks):
+        m = np.isin(key, ch)
+        if ci == 0:
+            m |= key < 0
+        rows = np.flatnonzero(m)
+        if rows.size == 0:
+            continue
+        y = apply_slot(cfg, slot_index, batch, rows=rows, y0=y0, n_threads=n_threads, seed=seed)
+        if out is None:
+            out = np.empty((batch.n_rows, y.shape[1]), y.dtype)
+        out[rows] = y
+    if out is None:  # empty batch
+        out = np.zeros((0, cfg.slots[slot_index].h_out), np.float32 if cfg.y_dtype == "fp32" else np.uint16)
+    return out
 
 
 def prepare_slot(cfg: li.Config, slot_index: int, batch: li.Batch, rows: Optional[Sequence[int]] = None,

@@ -629,7 +629,10 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
   if (n < 0 || (n > 0 && (!slots || !x || !y))) return fail(s, LORA_ERR_INVALID_ARG, "bad slot list");
   if (y_dtype != LORA_BF16 && y_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "y_dtype");
   std::set<int> seen;
-  std::set<const void*> ys;
+  // byte ranges of every y (written) and every x (read) of the launch: the
+  // slots' kernels run concurrently (two chains, any order of items), so a y
+  // may overlap no other y and no x of ANY slot of the call
+  std::vector<std::pair<uintptr_t, uintptr_t>> yr, xr;
   for (int i = 0; i < n; ++i) {
     const int sl = slots[i];
     if (sl < 0 || sl >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
@@ -639,12 +642,23 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     if (p->T > 0) {
       if (!x[i] || !y[i]) return fail(s, LORA_ERR_INVALID_ARG, "x or y is NULL");
       if (!aligned16(x[i]) || !aligned16(y[i])) return fail(s, LORA_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
-      if (!ys.insert(y[i]).second) return fail(s, LORA_ERR_INVALID_ARG, "y pointers must be distinct");
       const SlotInfo& si = s->slots[sl];
-      const char* xb = static_cast<const char*>(x[i]);
-      const char* yb = static_cast<const char*>(y[i]);
+      const uintptr_t xb = reinterpret_cast<uintptr_t>(x[i]), yb = reinterpret_cast<uintptr_t>(y[i]);
       const size_t xl = (size_t)p->T * si.h_in * 2, yl = (size_t)p->T * si.h_out * (y_dtype == LORA_FP32 ? 4 : 2);
-      if (xb < yb + yl && yb < xb + xl) return fail(s, LORA_ERR_INVALID_ARG, "x and y overlap");
+      if (!rin) xr.push_back({xb, xb + xl});  // (remote x rows live in peer buffers)
+      yr.push_back({yb, yb + yl});
+    }
+  }
+  if (!yr.empty()) {
+    std::sort(yr.begin(), yr.end());
+    for (size_t k = 1; k < yr.size(); ++k)
+      if (yr[k].first < yr[k - 1].second) return fail(s, LORA_ERR_INVALID_ARG, "y buffers of two slots overlap");
+    // y ranges are disjoint and sorted (so are their ends): the last y starting
+    // before an x range ends is the only one that can overlap it
+    for (const auto& r : xr) {
+      auto it = std::lower_bound(yr.begin(), yr.end(), std::make_pair(r.second, uintptr_t(0)));
+      if (it != yr.begin() && std::prev(it)->second > r.first)
+        return fail(s, LORA_ERR_INVALID_ARG, "an x buffer overlaps a y buffer of the same call");
     }
   }
   if (n == 0 || p->T == 0) return LORA_OK;
@@ -693,7 +707,9 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
         // splitting K: a tile's item takes the whole h_in (measured best vs
         // 1024 / 4096 / 7168 caps: prefill 0.634 / 0.583 / 0.577 / 0.569 ms)
         // and writes v directly; no reduction pass
-        t.KI = best_divisor(si.h_in, 128, s->tc_ki_max);
+        // (never below the slot's own KI: the partial-sum regions are sized
+        // and placed by the slot's n_kc)
+        t.KI = best_divisor(si.h_in, 128, std::max(s->tc_ki_max, si.KI));
         t.n_kc = si.h_in / t.KI;
       }
       t.CI = si.CI;

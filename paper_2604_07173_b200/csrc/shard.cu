@@ -103,7 +103,7 @@ constexpr int kBucketThreads = 1024;
 // Out-of-range ids are flagged and dropped (never sent, never applied).
 __global__ void __launch_bounds__(kBucketThreads, 1)
     bucket_kernel(const int32_t* __restrict__ ad, const int32_t* __restrict__ ex, int T, Placement pl, int n_adapters,
-                  int loopback, int32_t* __restrict__ ad_local,
+                  int E, int loopback, int32_t* __restrict__ ad_local,
                   int32_t* __restrict__ send_idx, int32_t* __restrict__ counts, int* __restrict__ err) {
   __shared__ int s_tmp[32];
   __shared__ int s_base;
@@ -111,10 +111,16 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
   const int chunk = (T + kBucketThreads - 1) / kBucketThreads;
   const int r0 = min(tid * chunk, T), r1 = min(r0 + chunk, T);
   if (tid == 0) s_base = 0;
+  // a row is routable iff both ids are in range: a in [0, n_adapters), e in [0, E)
+  auto routable = [&](int r, int a) {
+    if (a < 0 || a >= n_adapters) return false;
+    const int e = ex ? ex[r] : 0;
+    return e >= 0 && e < E;
+  };
   int bad = 0;
   for (int r = r0; r < r1; ++r) {
     const int a = ad[r];
-    const bool ok = a >= -1 && a < n_adapters;
+    const bool ok = a == -1 || routable(r, a);
     if (!ok) bad = 1;
     ad_local[r] = (!loopback && ok && a >= 0 && pl.owner_unit(a, ex ? ex[r] : 0) == pl.rank) ? a : -1;
   }
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
     int c = 0;
     for (int r = r0; r < r1; ++r) {
       const int a = ad[r];
-      c += (a >= 0 && a < n_adapters && pl.owner_unit(a, ex ? ex[r] : 0) == o);
+      c += (routable(r, a) && pl.owner_unit(a, ex ? ex[r] : 0) == o);
     }
     // block exclusive scan of c
     int x = c;
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
     const int tot = s_tmp[31];
     for (int r = r0; r < r1; ++r) {
       const int a = ad[r];
-      if (a >= 0 && a < n_adapters && pl.owner_unit(a, ex ? ex[r] : 0) == o) send_idx[pos++] = r;
+      if (routable(r, a) && pl.owner_unit(a, ex ? ex[r] : 0) == o) send_idx[pos++] = r;
     }
     __syncthreads();
     if (tid == 0) {
@@ -521,16 +527,22 @@ static lora_status_t p2p_register(lora_server* s, size_t need_send, size_t need_
   sh->peer_d[me] = static_cast<char*>(sh->dbuf);
   if (G == 1) return LORA_OK;
   // handle exchange: [G][2][64 bytes]
+  // A rank whose export fails still takes part in both all-gathers (zeroed
+  // handles, ok = 0), so every rank reaches the same decision instead of the
+  // others blocking in the handle exchange.
   std::vector<cudaIpcMemHandle_t> h(2 * G);
+  int ok = 1;
   if (cudaIpcGetMemHandle(&h[2 * me], sh->sendbuf) != cudaSuccess ||
-      cudaIpcGetMemHandle(&h[2 * me + 1], sh->dbuf) != cudaSuccess)
-    return fail(s, LORA_ERR_CUDA, "cudaIpcGetMemHandle failed");
+      cudaIpcGetMemHandle(&h[2 * me + 1], sh->dbuf) != cudaSuccess) {
+    cudaGetLastError();
+    std::memset(&h[2 * me], 0, 2 * sizeof(cudaIpcMemHandle_t));
+    ok = 0;
+  }
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   std::vector<cudaIpcMemHandle_t> mine(h.begin() + 2 * me, h.begin() + 2 * me + 2);
   lora_status_t rc = ctl_allgather(s, mine.data(), h.data(), 128, st);
   if (rc != LORA_OK) return rc;
-  int ok = 1;
-  for (int p = 0; p < G; ++p) {
+  for (int p = 0; p < G && ok; ++p) {
     if (p == me) continue;
     void* a = nullptr;
     void* b = nullptr;
@@ -641,7 +653,7 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   CKS(cudaStreamWaitEvent(st, sh->ev[3], 0));
   if (T > 0) {
     const int pi = prof_start(s, st);
-    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, expert_ids, T, pl, s->n_adapters, sh->loopback, d_ad_local, d_send_idx, d_counts,
+    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, expert_ids, T, pl, s->n_adapters, E, sh->loopback, d_ad_local, d_send_idx, d_counts,
                                                  s->d_err);
     prof_stop(s, pi, kKShardBucket, st);
   } else {

@@ -356,3 +356,97 @@ def test_shard_dispatch_pins(world, n_hot, ep):
         assert hot_moved == []
     if world == 1:
         assert len(disp[0]["rows"]) == 0
+
+
+def test_shard_dispatch_golden_hand_cases():
+    """shard_dispatch against hand-worked routing cases (tests/golden/shard_hand.json,
+    P:288-291 / P:323-335 with DESIGN.md R18/R19), independent of owner_of's code."""
+    g = json.load(open(os.path.join(GOLDEN, "shard_hand.json")))
+    for c in g["cases"]:
+        a = np.array(c["adapter_ids"], np.int32)
+        e = np.array(c["expert_ids"], np.int32)
+        k = c["top_k"]
+        b = li.Batch(a, e, a.size // k, k)
+        disp = orc.shard_dispatch(b, c["world"], c["n_hot"], c["ep"])
+        for d in range(c["world"]):
+            assert disp[d]["rows"].tolist() == c["rows"][d], (c["name"], d)
+            assert disp[d]["local"].tolist() == c["local"][d], (c["name"], d)
+        assert disp[0]["counts"].tolist() == c["counts"], c["name"]
+
+
+# ---------------------------------------------------------------------------
+# fp64 -> bf16 rounding of values between float32 grid points (one rounding,
+# not fp64 -> fp32 -> bf16): hand cases
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("d,bits", [
+    (1.0 + 2 ** -8 + 2 ** -40, 0x3F81),        # just above the tie 1 + 2^-8 -> up
+    (1.0 + 2 ** -8 - 2 ** -40, 0x3F80),        # just below -> down
+    (1.0 + 3 * 2 ** -8 - 2 ** -40, 0x3F81),    # just below the tie between 0x3F81 / 0x3F82
+    (1.0 + 3 * 2 ** -8 + 2 ** -40, 0x3F82),
+    (-(1.0 + 2 ** -8 + 2 ** -40), 0xBF81),
+    (2.0 ** -133, 0x0001),                     # smallest bf16 subnormal
+    (2.0 ** -134, 0x0000),                     # tie between 0 and 2^-133 -> even (0)
+    (2.0 ** -134 + 2.0 ** -160, 0x0001),       # above that tie
+    (3 * 2.0 ** -134, 0x0002),                 # tie between 1 and 2 quanta -> even
+    ((2 - 2 ** -8) * 2.0 ** 127, 0x7F80),      # tie between max finite and 2^128 -> even -> inf
+    ((2 - 2 ** -8) * 2.0 ** 127 * (1 - 2 ** -40), 0x7F7F),
+    (0.1, 0x3DCD),                             # 0.1 = 0x3DCCCCCD in fp32; bf16 RNE -> 0x3DCD
+])
+def test_bf16_rounding_between_float32_grid_points(d, bits):
+    assert orc.round_bf16(d) == bits
+
+
+# ---------------------------------------------------------------------------
+# apply_slot / prepare_slot glue: row -> unit -> regenerated weights, x rows,
+# y0 rows, scale; pinned against a dense per-row brute force built from the
+# numpy (not C) generator and float64 numpy arithmetic
+# ---------------------------------------------------------------------------
+def _apply_slot_bruteforce(cfg, slot_index, batch, rows, y0):
+    sl = cfg.slots[slot_index]
+    s = cfg.scale()
+    x = li.bf16_bits_to_f32(li.x_rows_bits(cfg.seed, sl.xbuf, rows, sl.h_in)).astype(np.float64)
+    if y0 == "random":
+        y = li.bf16_bits_to_f32(li.y0_rows_bits(cfg.seed, slot_index, rows, sl.h_out)).astype(np.float64)
+    else:
+        y = np.zeros((len(rows), sl.h_out))
+    for n, i in enumerate(rows):
+        a = int(batch.adapter_ids[i])
+        if a < 0:
+            continue
+        u = a * sl.n_experts + int(batch.expert_ids[i])
+        A = li.bf16_bits_to_f32(li.unit_A_bits(cfg.seed, slot_index, u, sl.h_in, cfg.rank)).astype(np.float64)
+        Bm = li.bf16_bits_to_f32(li.unit_B_bits(cfg.seed, slot_index, u, cfg.rank, sl.h_out)).astype(np.float64)
+        W = np.random.default_rng(n).standard_normal((sl.h_in, sl.h_out))  # base weight (P:165 W' = W + AB)
+        y[n] += x[n] @ (W + float(s[a]) * (A @ Bm)) - x[n] @ W
+    return y
+
+
+@pytest.mark.parametrize("name,y0", [("tiny", "random"), ("tiny", "zero"), ("tiny_dense", "random"), ("mid", "random")])
+def test_apply_slot_against_dense_bruteforce(name, y0):
+    if name == "mid":
+        cfg = li.Config("mid", 8, (li.Slot("a", 128, 192, 4, 0), li.Slot("b", 192, 128, 4, 1)), 16, 24, 4, 2,
+                        60, "bf16")
+    else:
+        cfg = li.CONFIGS[name]
+    b = li.make_batch(cfg)
+    for si in range(len(cfg.slots)):
+        got = orc.apply_slot(cfg, si, b, y0=y0)
+        ref = _apply_slot_bruteforce(cfg, si, b, np.arange(b.n_rows), y0)
+        if cfg.y_dtype == "fp32":
+            np.testing.assert_allclose(got.astype(np.float64), ref, rtol=2 ** -23, atol=1e-12)
+        else:  # one bf16 rounding of the exact value: within half an ulp (2^-9 relative)
+            np.testing.assert_allclose(li.bf16_bits_to_f32(got).astype(np.float64), ref, rtol=2 ** -8, atol=1e-30)
+        # rows without a LoRA are exactly y0
+        none = np.flatnonzero(b.adapter_ids < 0)
+        if none.size:
+            np.testing.assert_array_equal(np.asarray(got)[none].astype(np.float64) if cfg.y_dtype == "fp32"
+                                          else li.bf16_bits_to_f32(got[none]).astype(np.float64), ref[none])
+
+
+def test_apply_slot_all_rows_equals_apply_slot():
+    cfg = li.Config("mid", 8, (li.Slot("a", 128, 192, 4, 0),), 16, 24, 4, 2, 90, "bf16", no_lora_frac=0.1)
+    b = li.make_batch(cfg)
+    for y0 in ("random", "zero"):
+        full = orc.apply_slot(cfg, 0, b, y0=y0)
+        chunked = orc.apply_slot_all_rows(cfg, 0, b, y0=y0, unit_chunk=3)
+        np.testing.assert_array_equal(full, chunked)
