@@ -55,7 +55,8 @@ typedef enum {
   LORA_ERR_CUDA = 3,
   LORA_ERR_ID_OUT_OF_RANGE = 4,
   LORA_ERR_UNSUPPORTED = 5,
-  LORA_ERR_NCCL = 6
+  LORA_ERR_NCCL = 6,
+  LORA_ERR_PEER = 7   /* sharded push path: a peer did not signal in time, or ranks disagreed on a call */
 } lora_status_t;
 
 typedef enum { LORA_BF16 = 0, LORA_FP32 = 1 } lora_dtype_t;
@@ -231,11 +232,13 @@ lora_status_t lora_apply_multi_host(lora_server_t *s, int32_t n, const int32_t *
  * bootstrap).  Fails with LORA_ERR_NCCL if libnccl.so.2 cannot be loaded. */
 lora_status_t lora_nccl_unique_id(void *out128);
 
-/* Create the rank-`rank` member of a world-`world` sharded server.  With
- * h = cfg->n_replicated, adapters a < h are stored on every rank and adapter
- * a >= h is owned by rank (a - h) mod world (LoRA Data Parallel striping,
- * P:288-291); each rank stores only the adapters it owns.  Every rank must
- * call this collectively with the same config.  max_rows * world <= 16384. */
+/* Create the rank-`rank` member of a world-`world` sharded server (world <=
+ * 8: one NVLink / NVSwitch domain).  With h = cfg->n_replicated, adapters
+ * a < h are stored on every rank and adapter a >= h is owned by rank
+ * (a - h) mod world (LoRA Data Parallel striping); with
+ * cfg->expert_parallel, unit (a, e) is owned by rank e mod world.
+ * Each rank stores only what it owns.  Every rank must call this
+ * collectively with the same config.  max_rows * world <= 16384. */
 lora_status_t lora_server_create_sharded(const lora_config_t *cfg, int32_t rank, int32_t world,
                                          const void *nccl_unique_id, lora_server_t **out);
 
@@ -245,26 +248,57 @@ lora_status_t lora_server_create_sharded(const lora_config_t *cfg, int32_t rank,
  * world * bytes, rank-major.  Return 0 on success. */
 typedef int (*lora_host_allgather_fn)(void *ctx, const void *send, void *recv, int64_t bytes);
 
-/* As lora_server_create_sharded, with the control plane (counts exchange,
- * IPC-handle exchange, the two barriers of an apply) on the caller's host
- * all-gather instead of NCCL; the data path is the peer-to-peer transport
- * (registered buffers mapped with CUDA IPC; peers on the same or other GPUs).
- * Each barrier synchronises the stream on the host (two extra host syncs per
- * apply).  world <= 8.  Used by the multi-process tests on one GPU. */
+/* As lora_server_create_sharded, with the control plane (IPC-handle and
+ * agreement exchanges of lora_shard_register) on the caller's host all-gather
+ * instead of NCCL.  Applies then need registered x / y buffers (the push path
+ * runs without any host collective).  Peers may share a GPU (the
+ * multi-process tests run two ranks on one B200). */
 lora_status_t lora_server_create_sharded_host(const lora_config_t *cfg, int32_t rank, int32_t world,
                                               lora_host_allgather_fn allgather, void *ctx,
                                               lora_server_t **out);
 
+/* Register n caller device buffers for the sharded push path (collective:
+ * every rank registers the same number of buffers, in the same roles and
+ * order, e.g. its x of gate/up, its x of down, then its y of gate, up, down).
+ * Each buffer (ptrs[i], bytes[i] bytes, inside one cudaMalloc allocation --
+ * torch's caching allocator qualifies; expandable segments do not) is
+ * exported with CUDA IPC and mapped on every peer (NVLink peer access); the
+ * first call also creates this rank's control area.  Registrations last
+ * until lora_server_destroy; the caller keeps the buffers alive until then.
+ * If any rank cannot export or map a buffer, every rank releases ALL its
+ * registrations and returns LORA_ERR_UNSUPPORTED.  Synchronises `stream`. */
+lora_status_t lora_shard_register(lora_server_t *s, int32_t n, void *const *ptrs, const int64_t *bytes,
+                                  void *stream);
+
 /* Collective apply on a sharded server: every rank passes its OWN rows
  * (T local rows, device pointers, same slot list on every rank).  Rows whose
- * adapter this rank stores (its own or a replicated one) are applied in place;
- * the others are routed to their adapter's owner (grouped NCCL send/recv over
- * NVLink, overlapped with the in-place apply), applied there, and the deltas
- * are returned and added into the caller's y.  Deltas travel as fp32 for an
- * fp32 y (result bit-identical to the unsharded server, R18) and as
- * bf16 for a bf16 y (env LORA_SHARD_FP32=1 forces fp32).  One host
- * synchronisation (the count exchange); rows with adapter id -1 stay local
- * and untouched; out-of-range ids are flagged and dropped. */
+ * unit this rank stores (its own or a replicated adapter) are applied in
+ * place; the others are applied by their unit's owner.
+ *
+ * Push path -- every x[i] and y[i] is the start of a registered buffer (of
+ * at least T rows), on every rank (one-sided pushes both ways;
+ * receive / compute / send overlapped): the counts travel through
+ * peer memory (device flags, no host synchronisation, CUDA-graph
+ * capturable); the owner's shrink reads each routed x row directly from its
+ * source's x over NVLink, and its expand epilogue adds the delta directly
+ * into the source's y row (red.add: one writer per element; bf16 y: the
+ * delta is rounded to bf16 first, R19; fp32 y: bit-identical to
+ * the unsharded server when every row takes the same kernel route, R18,
+ * except that a subnormal delta or sum is flushed to zero).  The call is
+ * stream-ordered: when `stream` reaches its end, every owner has finished
+ * adding into this rank's y.  A rank that does not arrive within
+ * LORA_SHARD_TIMEOUT_MS (default 10000) makes the others skip its rows and
+ * raise the sticky flag (lora_server_check -> LORA_ERR_PEER), as do ranks
+ * whose calls disagree (slots, buffer roles, dtype).
+ *
+ * Otherwise (NCCL control plane only): grouped ncclSend/ncclRecv of the
+ * routed x rows + ids and of the deltas (fp32 for an fp32 y, bf16 for a bf16
+ * y unless LORA_SHARD_FP32=1), one host synchronisation for the count
+ * matrix; ranks whose calls disagree all return LORA_ERR_INVALID_ARG before
+ * any row moves.
+ *
+ * Rows with adapter id -1 stay local and untouched; out-of-range ids are
+ * flagged and dropped (never sent, never applied).  n <= 128. */
 lora_status_t lora_apply_sharded(lora_server_t *s, int32_t n, const int32_t *slots,
                                  const void *const *x, const int32_t *adapter_ids,
                                  const int32_t *expert_ids, void *const *y, lora_dtype_t y_dtype,
@@ -309,7 +343,8 @@ lora_status_t lora_profile_read(lora_server_t *s, int32_t n_kinds, int32_t *laun
 
 /* Name of kernel kind k (0 segment, 1 simt_shrink, 2 tc05_shrink,
  * 3 simt_expand, 4 tc05_expand, 5 shard_bucket, 6 shard_gather,
- * 7 shard_scatter_add, 8 tc05_vreduce); "unknown" otherwise. */
+ * 7 shard_scatter_add, 8 tc05_vreduce; push path: 5 = bucket + announce,
+ * 6 = recv-prep, 7 = done + wait); "unknown" otherwise. */
 const char *lora_kernel_name(int32_t kind);
 
 /* Library version string. */

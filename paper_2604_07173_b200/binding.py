@@ -21,10 +21,10 @@ if not os.path.exists(LIB_PATH):
 lib = ctypes.CDLL(LIB_PATH)
 
 LORA_OK, LORA_ERR_INVALID_ARG, LORA_ERR_OOM, LORA_ERR_CUDA = 0, 1, 2, 3
-LORA_ERR_ID_OUT_OF_RANGE, LORA_ERR_UNSUPPORTED, LORA_ERR_NCCL = 4, 5, 6
+LORA_ERR_ID_OUT_OF_RANGE, LORA_ERR_UNSUPPORTED, LORA_ERR_NCCL, LORA_ERR_PEER = 4, 5, 6, 7
 LORA_BF16, LORA_FP32 = 0, 1
 STATUS = {0: "LORA_OK", 1: "LORA_ERR_INVALID_ARG", 2: "LORA_ERR_OOM", 3: "LORA_ERR_CUDA",
-          4: "LORA_ERR_ID_OUT_OF_RANGE", 5: "LORA_ERR_UNSUPPORTED", 6: "LORA_ERR_NCCL"}
+          4: "LORA_ERR_ID_OUT_OF_RANGE", 5: "LORA_ERR_UNSUPPORTED", 6: "LORA_ERR_NCCL", 7: "LORA_ERR_PEER"}
 
 
 class LoraConfig(ctypes.Structure):
@@ -65,6 +65,7 @@ SIGNATURES = {
     "lora_server_create_sharded": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _pp]),
     "lora_server_create_sharded_host": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _vp, _pp]),
     "lora_apply_sharded": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
+    "lora_shard_register": (ctypes.c_int, [_vp, _i32, _pp, _pi64, _vp]),
     "lora_shard_peer_rows": (ctypes.c_int, [_pi64, _i32, _i32, _pi64, _pi64]),
     "lora_shard_layout": (ctypes.c_int, [_pi64, _i32, _i32, _pi64, _pi64]),
     "lora_synth_fill_rows": (ctypes.c_int, [_vp, _i64, _i32, _u64, _u32, _i32, _i64, _vp]),
@@ -280,6 +281,13 @@ def lora_apply_sharded(s: int, slots: Sequence[int], x, adapter_ids, expert_ids,
     sl = (ctypes.c_int32 * n)(*slots)
     _check(lib.lora_apply_sharded(s, n, sl, _ptr_array(x), _ptr(adapter_ids), _ptr(expert_ids), _ptr_array(y),
                                   y_dtype, T, _stream(stream)), s)
+
+
+def lora_shard_register(s: int, bufs, nbytes: Sequence[int], stream=None):
+    """Collective: register device buffers (x / y of this rank) for the push path."""
+    n = len(bufs)
+    b = (ctypes.c_int64 * n)(*[int(v) for v in nbytes])
+    _check(lib.lora_shard_register(s, n, _ptr_array(bufs), b, _stream(stream)), s)
 
 
 def lora_shard_layout(counts, world: int, rank: int):

@@ -177,6 +177,29 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Push adds into a peer's (or this GPU's) registered y (sharded owner, one
+// writer per element, so the add is the only update of the element and the
+// result is deterministic).  System scope: the target may be another GPU's
+// memory behind an NVLink peer mapping.  bf16: one rounding of y + d_bf16
+// (d already rounded to bf16, R19); f32: red.add.f32 (FTZ on
+// subnormal operands/results, the only difference from a local fp32 add).
+LORA_DEVINL void red_add_bf16x8(void* p, uint4 v) {
+  asm volatile("red.relaxed.sys.global.add.noftz.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+LORA_DEVINL void red_add_bf16x2(void* p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+LORA_DEVINL void red_add_f32(void* p, float v) {
+  asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+LORA_DEVINL void red_add_f32x4(void* p, float4 v) {
+  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
 // 128-bit loads
 LORA_DEVINL uint4 lds128(uint32_t addr) {
   uint4 v;

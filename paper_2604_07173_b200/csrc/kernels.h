@@ -122,22 +122,26 @@ struct SlotTask {
   int kc_base, ci_base;// prefix over tasks of n_kc / n_ci
 };
 
-// Owner side of a peer-to-peer sharded apply (shard.cu): received row r is
-// not copied to the owner -- it stays in source s's registered send buffer
-// (NVLink peer mapping) and the shrink kernels read it from there.
+// Owner side of a sharded apply over registered buffers (shard.cu, the push
+// path): received row r was sent by source rank origin[r] >> 24 from its
+// local row origin[r] & 0xFFFFFF.  The shrink kernels read that x row straight
+// from the source's registered x buffer and the expand epilogues add the
+// delta straight into the source's registered y row (NVLink peer mappings),
+// so neither the rows nor the deltas are staged anywhere.
 constexpr int kMaxWorld = 8;
-struct RemoteIn {
-  int G;                         // 0: rows are local (t.x + row * h_in)
-  int ro[kMaxWorld + 1];         // received-row offsets per source
-  int rowbase[kMaxWorld];        // row in source s's send buffer = r + rowbase[s]
-  const char* src[kMaxWorld];    // source s's send buffer (peer pointer)
+constexpr int kOriginRowBits = 24;
+struct PushIn {
+  int G;                     // 0: local rows (t.x / t.y + row)
+  const int32_t* origin;     // [rows] (source << 24) | source-local row
+  char* const* reg;          // device [n_reg * G]: base of registered buffer k on rank p
 };
 
 struct MultiArgs {
   int n_tasks;
   int total_kc, total_ci;  // sums of n_kc / n_ci
   int y_fp32;
-  int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16
+  int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16;
+                           // 3 (push): adds it into the source's y row (red.add over NVLink)
   int tc_cap_k;            // > 0: tcgen05 kernels use at most max(8, tiles * tc_cap_k) CTAs (rest exit at once)
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const int32_t* cache;    // resident-cache mode: unit = cache[a]*E + e (nullptr: placement)
@@ -147,20 +151,30 @@ struct MultiArgs {
   // filled by the host when total_kc / total_ci <= kTaskTable
   uint8_t kc_task[kTaskTable];
   uint8_t ci_task[kTaskTable];
-  RemoteIn rin;                // x rows read from peers (sharded P2P owner), G = 0 otherwise
-  long long x_off[kMaxTasks];  // RemoteIn mode: byte offset of each task's x rows in a source's send buffer
+  PushIn push;                 // sharded owner over registered buffers (G = 0 otherwise)
+  int16_t xreg[kMaxTasks];     // push: registered-buffer index of each task's x and y
+  int16_t yreg[kMaxTasks];
 };
 
 #ifdef __CUDACC__
-// address of x row `row` of task t (local, or -- REMOTE -- in a source's send
-// buffer); REMOTE is a compile-time kernel variant so the local path is unchanged
+// address of x row `row` of task t (local, or -- REMOTE -- the origin row in
+// its source's registered x buffer); REMOTE is a compile-time kernel variant
+// so the local path is unchanged
 template <bool REMOTE>
 __device__ __forceinline__ const uint16_t* x_row(const MultiArgs& a, int task, int row) {
   const SlotTask& t = a.t[task];
   if (!REMOTE) return t.x + (long long)row * t.h_in;
-  int s = 0;
-  while (s + 1 < a.rin.G && a.rin.ro[s + 1] <= row) ++s;
-  return reinterpret_cast<const uint16_t*>(a.rin.src[s] + a.x_off[task]) + (long long)(row + a.rin.rowbase[s]) * t.h_in;
+  const int o = __ldg(a.push.origin + row);
+  const char* base = a.push.reg[a.xreg[task] * a.push.G + (o >> kOriginRowBits)];
+  return reinterpret_cast<const uint16_t*>(base) + (long long)(o & ((1 << kOriginRowBits) - 1)) * t.h_in;
+}
+// push mode: element 0 of the origin row of received row `row` in its source's
+// registered y buffer (bf16 or fp32, esz bytes per element)
+__device__ __forceinline__ char* y_push_row(const MultiArgs& a, int task, int row, int esz) {
+  const SlotTask& t = a.t[task];
+  const int o = __ldg(a.push.origin + row);
+  char* base = a.push.reg[a.yreg[task] * a.push.G + (o >> kOriginRowBits)];
+  return base + (long long)(o & ((1 << kOriginRowBits) - 1)) * t.h_out * esz;
 }
 // task owning global expand column-range index g (ci_base prefix)
 __device__ __forceinline__ int find_task_ci(const MultiArgs& a, int g) {
@@ -185,8 +199,10 @@ __device__ __forceinline__ int find_task_kc(const MultiArgs& a, int g) {
 #endif
 
 // launchers (return cudaGetLastError())
+// T_dev != nullptr: the row count is *T_dev (<= T, read on the device; T is the capacity)
 cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,
-                           const SegParams& sp, const PlanDev& pd, int* err_flag, cudaStream_t stream);
+                           const SegParams& sp, const PlanDev& pd, int* err_flag, cudaStream_t stream,
+                           const int* T_dev = nullptr);
 cudaError_t launch_simt_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_simt_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid, cudaStream_t stream);

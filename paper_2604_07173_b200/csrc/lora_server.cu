@@ -268,9 +268,8 @@ bool pdl_enabled() {
 }  // namespace lora
 
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
-                                void* const* d, cudaStream_t st, bool bf16, const RemoteIn* rin,
-                                const long long* x_off) {
-  return apply_multi_impl(s, p, n, slots, x, d, bf16 ? LORA_BF16 : LORA_FP32, st, bf16 ? 2 : 1, rin, x_off);
+                                void* const* d, cudaStream_t st, bool bf16) {
+  return apply_multi_impl(s, p, n, slots, x, d, bf16 ? LORA_BF16 : LORA_FP32, st, bf16 ? 2 : 1);
 }
 
 static lora_status_t cache_reset(lora_server* s);
@@ -498,10 +497,12 @@ extern "C" lora_status_t lora_server_check(lora_server_t* s, void* stream) {
   CK(s, cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   int flag = 0;
   CK(s, cudaMemcpy(&flag, s->d_err, sizeof(int), cudaMemcpyDeviceToHost));
-  if (flag) {
-    CK(s, cudaMemset(s->d_err, 0, sizeof(int)));
-    return fail(s, LORA_ERR_ID_OUT_OF_RANGE, "an adapter or expert id was out of range (row skipped)");
+  if (flag) CK(s, cudaMemset(s->d_err, 0, sizeof(int)));
+  if (s->shard) {  // peer timeouts / layout mismatches of the push path, NCCL asynchronous errors
+    const lora_status_t sr = lora_shard_check_flags(s, flag);
+    if (sr != LORA_OK) return sr;
   }
+  if (flag & 1) return fail(s, LORA_ERR_ID_OUT_OF_RANGE, "an adapter or expert id was out of range (row skipped)");
   return LORA_OK;
 }
 
@@ -584,7 +585,7 @@ static bool tc_enabled(const lora_server* s) {
 }
 
 lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapter_ids, const int32_t* expert_ids,
-                              int T, int E, cudaStream_t st) {
+                              int T, int E, cudaStream_t st, const int* T_dev) {
   if (T < 0 || T > p->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");
   if (E < 1) return fail(s, LORA_ERR_INVALID_ARG, "n_experts < 1");
   if (T > 0 && !adapter_ids) return fail(s, LORA_ERR_INVALID_ARG, "adapter_ids is NULL");
@@ -596,7 +597,7 @@ lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapt
   const int pi = prof_start(s, st);
   sp.pl = placement(s);
   sp.cache = s->d_cache;
-  CK(s, launch_segment(adapter_ids, expert_ids, T, E, s->n_adapters, sp, p->dev, s->d_err, st));
+  CK(s, launch_segment(adapter_ids, expert_ids, T, E, s->n_adapters, sp, p->dev, s->d_err, st, T_dev));
   prof_stop(s, pi, kKSegment, st);
   p->n_experts = E;
   p->T = T;
@@ -622,8 +623,8 @@ static void fill_task_tables(MultiArgs& a) {
 }
 
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
-                               void* const* y, lora_dtype_t y_dtype, cudaStream_t st, int store, const RemoteIn* rin,
-                               const long long* x_off) {
+                               void* const* y, lora_dtype_t y_dtype, cudaStream_t st, int store, const PushIn* push,
+                               const int16_t* xreg, const int16_t* yreg) {
   if (!p || p->s != s) return fail(s, LORA_ERR_INVALID_ARG, "plan does not belong to this server");
   if (p->n_experts < 0) return fail(s, LORA_ERR_INVALID_ARG, "plan was never built");
   if (n < 0 || (n > 0 && (!slots || !x || !y))) return fail(s, LORA_ERR_INVALID_ARG, "bad slot list");
@@ -645,8 +646,10 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       const SlotInfo& si = s->slots[sl];
       const uintptr_t xb = reinterpret_cast<uintptr_t>(x[i]), yb = reinterpret_cast<uintptr_t>(y[i]);
       const size_t xl = (size_t)p->T * si.h_in * 2, yl = (size_t)p->T * si.h_out * (y_dtype == LORA_FP32 ? 4 : 2);
-      if (!rin) xr.push_back({xb, xb + xl});  // (remote x rows live in peer buffers)
-      yr.push_back({yb, yb + yl});
+      if (!push) {  // (push: x rows and y rows live in the sources' registered buffers)
+        xr.push_back({xb, xb + xl});
+        yr.push_back({yb, yb + yl});
+      }
     }
   }
   if (!yr.empty()) {
@@ -683,7 +686,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.pl = placement(s);
     args.cache = s->d_cache;
     args.scale = s->d_scale;
-    if (rin) args.rin = *rin;
+    if (push) args.push = *push;
     int kc = 0, ci = 0;
     bool any_split = false;
     for (int i = 0; i < nb; ++i) {
@@ -692,7 +695,8 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       t.At = si.At;
       t.Bt = si.Bt;
       t.x = static_cast<const uint16_t*>(x[b0 + i]);
-      args.x_off[i] = x_off ? x_off[b0 + i] : 0;
+      args.xreg[i] = xreg ? xreg[b0 + i] : 0;
+      args.yreg[i] = yreg ? yreg[b0 + i] : 0;
       t.y = y[b0 + i];
       t.vpart_off = (long long)si.kc_prefix * p->max_rows * s->r;
       t.vbf_off = (long long)slots[b0 + i] * p->max_rows * s->r;
@@ -702,7 +706,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       t.KI = si.KI;
       t.SJ = si.SJ;
       t.n_kc = si.n_kc;
-      if (tc && p->T >= kTcWideKRows) {
+      if (tc && (p->T_hint > 0 ? p->T_hint : p->T) >= kTcWideKRows) {
         // large batches have tcgen05 tiles enough to fill the GPU without
         // splitting K: a tile's item takes the whole h_in (measured best vs
         // 1024 / 4096 / 7168 caps: prefill 0.634 / 0.583 / 0.577 / 0.569 ms)
@@ -737,7 +741,8 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       int kc2 = 0, ci2 = 0;
       for (int i = 0; i < nb; ++i) {
         sargs.t[i] = args.t[order[i]];
-        sargs.x_off[i] = args.x_off[order[i]];
+        sargs.xreg[i] = args.xreg[order[i]];
+        sargs.yreg[i] = args.yreg[order[i]];
         sargs.t[i].kc_base = kc2;
         sargs.t[i].ci_base = ci2;
         kc2 += sargs.t[i].n_kc;
@@ -745,7 +750,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       }
       fill_task_tables(sargs);
     }
-    if (tc && s->tc_ci_max > 0 && p->T >= kTcWideKRows) {
+    if (tc && s->tc_ci_max > 0 && (p->T_hint > 0 ? p->T_hint : p->T) >= kTcWideKRows) {
       // large batches: tcgen05 expand items of up to tc_ci_max columns of one
       // tile (decode-sized batches have few tiles and keep the slot's CI)
       int ci3 = 0;

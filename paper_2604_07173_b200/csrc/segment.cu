@@ -273,10 +273,22 @@ template <bool radix>
 __global__ void __launch_bounds__(kSegThreads, 1)
     segment_kernel(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T, int P,
                    int E, int n_adapters, int kb, int ib, SegParams sp, PlanDev pd,
-                   int* __restrict__ err_flag) {
+                   int* __restrict__ err_flag, const int* __restrict__ T_dev) {
   extern __shared__ __align__(16) uint8_t seg_smem[];
   pdl_launch_dependents();  // the shrink kernels may launch now; they wait for this grid
   SEG_T(0);
+  if (T_dev) {
+    // row count known only on the device (the sharded owner's received rows):
+    // T and P above are the capacity the shared memory was sized for; sort
+    // only the actual rows (P = the padded size of those, fewer radix rounds)
+    T = min(T, max(*T_dev, 0));
+    int p2 = kSegThreads;
+    while (p2 < T) p2 <<= 1;
+    P = p2;
+    int b = 0;
+    while ((1 << b) <= P - 1) ++b;
+    ib = b;
+  }
   const Placement pl = sp.pl;
   const int32_t* cache = sp.cache;
   __shared__ int scan_tmp[40];
@@ -641,14 +653,14 @@ int bits_for(long long v) {  // bits needed to represent v (v >= 0)
 
 cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids, int T, int E, int n_adapters,
                            const SegParams& sp, const PlanDev& pd, int* err_flag,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, const int* T_dev) {
   // multi-CTA path: K * C within the histogram bound, local composites radix-able
   {
     const long long K = (long long)n_adapters * E;
     const int kb = bits_for(K);
     const char* fe = getenv("LORA_SEG_MULTI");  // test hook: 1 forces, 0 disables the multi-CTA path
     const int forced = fe ? atoi(fe) : -1;
-    const bool want = forced < 0 ? T >= kSegMultiMin : forced == 1;
+    const bool want = !T_dev && (forced < 0 ? T >= kSegMultiMin : forced == 1);  // (device T: one CTA)
     int ept = 0;
     if (want && pd.hist && T > 0 && kb + kLocBits <= 32 && K > 0 && K <= kSegKeysMax) {
       // rows per CTA: the fewest (1024, 2048) that keep the histogram K x C
@@ -718,10 +730,10 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
   }
   if (radix)
     segment_kernel<true><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp,
-                                                           pd, err_flag);
+                                                           pd, err_flag, T_dev);
   else
     segment_kernel<false><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp,
-                                                            pd, err_flag);
+                                                            pd, err_flag, T_dev);
   return cudaGetLastError();
 }
 

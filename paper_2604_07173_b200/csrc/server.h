@@ -83,6 +83,7 @@ struct lora_plan {
   int max_rows = 0;
   int n_experts = -1;  // E the plan was last built with (-1: never built)
   int T = 0;
+  int T_hint = 0;      // > 0: row count to size the tcgen05 split by (device-side row counts: the capacity is T)
   int world = 1;
 };
 
@@ -91,20 +92,21 @@ lora_status_t fail(lora_server* s, lora_status_t st, const std::string& msg);
 lora_status_t cuda_fail(lora_server* s, cudaError_t e, const char* where);
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
                                const void* const* x, void* const* y, lora_dtype_t y_dtype, cudaStream_t st,
-                               int store = 0, const RemoteIn* rin = nullptr, const long long* x_off = nullptr);
+                               int store = 0, const PushIn* push = nullptr, const int16_t* xreg = nullptr,
+                               const int16_t* yreg = nullptr);
 lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapter_ids, const int32_t* expert_ids,
-                              int T, int E, cudaStream_t st);
+                              int T, int E, cudaStream_t st, const int* T_dev = nullptr);
 lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out);
 void plan_destroy_impl(lora_plan* p);
 }  // namespace lora
 
 // shard.cu / lora_server.cu cross-file helpers (C++ linkage)
 void lora_shard_free(lora_server* s);
+lora_status_t lora_shard_check_flags(lora_server* s, int flag);  // sticky-flag bits of the sharded path, NCCL errors
 lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot,
                                     int ep);
 inline lora::Placement placement(const lora_server* s) {
   return lora::Placement{s->world, s->shard_rank, s->n_hot, s->ep};
 }
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
-                                const void* const* x, void* const* d, cudaStream_t st, bool bf16,
-                                const lora::RemoteIn* rin = nullptr, const long long* x_off = nullptr);
+                                const void* const* x, void* const* d, cudaStream_t st, bool bf16);

@@ -1,4 +1,4 @@
-// shard.cu -- the Sharded LoRA Server: LoRA Data Parallel over NCCL / NVLink.
+// shard.cu -- the Sharded LoRA Server: LoRA Data Parallel over NVLink.
 //
 // P:288-291 (Sec. 4.1, Table 1 DP row): "evenly distribute LoRA adapters
 // across the server GPUs ... activations from client GPUs must be routed
@@ -8,24 +8,39 @@
 // the n_replicated hottest adapters are therefore stored on every rank
 // and their rows never leave their rank.
 //
-// One collective apply (every rank, same slot list):
-//   1. classify the local rows: owner == this rank (replicated or own units)
-//      -> processed in place; the rest bucketed by owner (stable)
-//   2. all-gather of the G send counts -> full G x G matrix, read back
-//      asynchronously; the in-place plan + apply are enqueued before the host
-//      waits for it (the GPU works through the one host round trip)
-//   3. (comm stream) pack of x rows and ids into the send buffer, transport
-//      (P2P: a barrier; NCCL: grouped send/recv), then the owner side's ids
-//      and plan -- all overlapped with the in-place apply
-//   4. received rows: delta-mode apply (P2P: the shrink reads the x rows from
-//      the sources' send buffers over NVLink)
-//   5. deltas back (P2P: barrier, then each source pulls its deltas fused with
-//      the add; NCCL: reverse send/recv, then y[origin row] = round(y + delta))
+// Push path (x and y registered with lora_shard_register).
+// The paper moves activations and results with one-sided pushes in both
+// directions (pull measured 2.63x slower) and overlaps receive,
+// compute and send.  Here every transfer is fused into a compute
+// kernel over NVLink peer mappings, so no row and no delta is staged:
+//   1. bucket (1 CTA): rows this rank serves -> in-place id list; the rest
+//      bucketed by owner into this rank's control area (ids + local row);
+//      announce: the count row (+ a layout hash) is written into every peer's
+//      mailbox, then a release flag carrying the apply's epoch
+//   2. in-place plan + apply of the local rows (caller's stream), concurrently
+//      on a second stream: recv-prep (waits for every peer's flag, pulls the
+//      received rows' ids and origins from the sources' control areas) and
+//      the owner-side plan, with the row count on the device
+//   3. owner apply: the shrink kernels read each received x row from its
+//      source's registered x buffer (dispatch fused into the shrink's loads),
+//      the expand epilogues add each delta into the origin row of the source's
+//      registered y with red.add (return fused into the epilogue; one writer
+//      per element)
+//   4. done: a release flag into every peer; wait: until every owner's flag
+//      for this epoch has arrived (this rank's y is final)
+// No host synchronisation, no allocation: the sharded step is captured in a
+// CUDA graph.  The epoch lives in device memory, so graph replays advance it.
+// Spin-waits give up after LORA_SHARD_TIMEOUT_MS (default 10 s): the sticky
+// flag reports LORA_ERR_PEER instead of a hang.
+//
+// Unregistered buffers (NCCL control plane only): grouped ncclSend/ncclRecv of
+// x rows + ids and of the deltas, one host sync for the count matrix.
 // Deltas travel as fp32 when y is fp32 (sharded == unsharded bit for bit,
-// DESIGN.md R18) and as bf16 when y is bf16 (half the NVLink bytes, one extra
-// rounding of the delta: DESIGN.md R19), unless LORA_SHARD_FP32=1.
+// DESIGN.md R18) and as bf16 when y is bf16 (one extra rounding of the
+// delta: DESIGN.md R19), unless LORA_SHARD_FP32=1 (NCCL path).
 // NCCL is loaded with dlopen("libnccl.so.2") (the copy torch already loaded),
 // so the library itself has no link-time NCCL dependency.
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -55,6 +70,7 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -84,6 +100,7 @@ NcclApi& nccl() {
   SYM(AllGather, "ncclAllGather");
   SYM(AllReduce, "ncclAllReduce");
   SYM(GetErrorString, "ncclGetErrorString");
+  SYM(CommGetAsyncError, "ncclCommGetAsyncError");
 #undef SYM
   api.ok = true;
   return api;
@@ -97,14 +114,15 @@ constexpr int kBucketThreads = 1024;
 // Single CTA over the T local rows (T <= 16384):
 //   ad_local[r] = a if this rank processes row r in place, else -1
 //   send_idx    = the other rows, bucketed by owner rank (stable, local order)
-//   counts[o]   = rows for owner o (0 for this rank)
+//   counts[o]   = rows for owner o (0 for this rank); counts[world] = hash
+//                 (layout hash of the call: every rank must pass the same)
 // loopback != 0 (test knob LORA_SHARD_LOOPBACK=1) sends this rank's own rows
 // through the exchange as well, so a single GPU exercises the NCCL path.
 // Out-of-range ids are flagged and dropped (never sent, never applied).
 __global__ void __launch_bounds__(kBucketThreads, 1)
     bucket_kernel(const int32_t* __restrict__ ad, const int32_t* __restrict__ ex, int T, Placement pl, int n_adapters,
                   int E, int loopback, int32_t* __restrict__ ad_local,
-                  int32_t* __restrict__ send_idx, int32_t* __restrict__ counts, int* __restrict__ err) {
+                  int32_t* __restrict__ send_idx, int32_t* __restrict__ counts, int* __restrict__ err, int hash) {
   __shared__ int s_tmp[32];
   __shared__ int s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -118,6 +136,7 @@ __global__ void __launch_bounds__(kBucketThreads, 1)
     return e >= 0 && e < E;
   };
   int bad = 0;
+  if (tid == 0) counts[pl.world] = hash;
   for (int r = r0; r < r1; ++r) {
     const int a = ad[r];
     const bool ok = a == -1 || routable(r, a);
@@ -215,96 +234,201 @@ __global__ void scatter_add4_kernel(void* __restrict__ y, int y_fp32, const void
   }
 }
 
-// Peer-to-peer transport (ShardState::p2p).  Owner side: the ids of received
-// row r are read from source s's registered send buffer (NVLink peer mapping).
-struct PeerRows {
-  int G;
-  int off[kMaxWorld + 1];   // row ranges per peer
-  int rowbase[kMaxWorld];   // row in the peer's buffer = r + rowbase[p]
-  const char* base[kMaxWorld];
-};
-LORA_DEVINL int peer_of(const PeerRows& pr, int r) {
-  int p = 0;
-  while (p + 1 < pr.G && pr.off[p + 1] <= r) ++p;
-  return p;
-}
-
-// ids_recv[r] = a, ids_recv[Rmax + r] = e of received row r (send buffer ids: [2][max_rows])
-__global__ void pull_ids_kernel(PeerRows pr, int max_rows, int32_t* __restrict__ ids_recv, long long Rmax, int n) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const int p = peer_of(pr, r);
-    const int32_t* ids = reinterpret_cast<const int32_t*>(pr.base[p]);
-    const int row = r + pr.rowbase[p];
-    ids_recv[r] = ids[row];
-    ids_recv[Rmax + r] = ids[max_rows + row];
-  }
-}
-
-// Source side: y[idx[j]] = round(y + delta) where the delta of send-order row j
-// sits in owner p's registered delta buffer (peer mapping), row j + rowbase[p]
-// of the slot region at byte offset slot_off.  The NVLink read is fused with
-// the accumulate.  4 columns per thread.
-__global__ void pull_scatter_add4_kernel(void* __restrict__ y, int y_fp32, PeerRows pr, long long slot_off, int d_bf16,
-                                         const int32_t* __restrict__ idx, int n, int width) {
-  const int q4 = width >> 2;
-  for (int j = blockIdx.y; j < n; j += gridDim.y) {
-    const long long row = idx[j];
-    const int p = peer_of(pr, j);
-    const long long drow = (long long)(j + pr.rowbase[p]) * q4;
-    const char* dbase = pr.base[p] + slot_off;
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < q4; c += gridDim.x * blockDim.x) {
-      float4 v;
-      if (d_bf16) {
-        const uint2 b = reinterpret_cast<const uint2*>(dbase)[drow + c];
-        v = make_float4(bf16lo(b.x), bf16hi(b.x), bf16lo(b.y), bf16hi(b.y));
-      } else {
-        v = reinterpret_cast<const float4*>(dbase)[drow + c];
-      }
-      if (y_fp32) {
-        float4* yp = reinterpret_cast<float4*>(y) + row * q4 + c;
-        float4 o = *yp;
-        o.x += v.x; o.y += v.y; o.z += v.z; o.w += v.w;
-        *yp = o;
-      } else {
-        uint2* yp = reinterpret_cast<uint2*>(y) + row * q4 + c;
-        const uint2 o = *yp;
-        uint2 r;
-        r.x = pack_bf16x2_rn(bf16lo(o.x) + v.x, bf16hi(o.x) + v.y);
-        r.y = pack_bf16x2_rn(bf16lo(o.y) + v.z, bf16hi(o.y) + v.w);
-        *yp = r;
-      }
-    }
-  }
-}
-
 int grid_of(long long n) {
   long long g = (n + 255) / 256;
   return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
 }
 
+// ---------------------------------------------------------------------------
+// push path: control area and kernels
+// ---------------------------------------------------------------------------
+// Per-rank control area (library memory, IPC-mapped by every peer).  Peers
+// write only their own slots: flag_cnt[p] / mbox[.][p] by source p,
+// flag_done[q] by owner q.  The send arrays are this rank's, read by owners.
+struct ShardCtl {
+  unsigned int epoch;                              // this rank's apply counter (local)
+  unsigned int pad_[7];
+  unsigned int flag_cnt[kMaxWorld];                // source p's count row for epoch v is in mbox
+  unsigned int flag_done[kMaxWorld];               // owner q finished pushing into this rank's y
+  int mbox[2][kMaxWorld][kMaxWorld + 1];           // [epoch & 1][source p][owner q | layout hash]
+};
+static_assert(sizeof(ShardCtl) % 16 == 0, "control area alignment");
+// send arrays after the header: send_row / send_a / send_e [max_rows] each
+LORA_DEVINL int32_t* ctl_send(ShardCtl* c, int max_rows, int which) {
+  return reinterpret_cast<int32_t*>(c + 1) + (size_t)which * max_rows;
+}
+
+struct PeerCtl {
+  ShardCtl* p[kMaxWorld];  // every rank's control area (own: local pointer)
+};
+
+enum { kErrId = 1, kErrPeer = 2, kErrLayout = 4 };
+
+LORA_DEVINL unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+LORA_DEVINL unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+LORA_DEVINL void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// wait until *flag has reached epoch v (monotonic counters); false on timeout
+LORA_DEVINL bool wait_flag(const unsigned int* flag, unsigned int v, unsigned long long timeout_ns) {
+  const unsigned long long t0 = globaltimer_ns();
+  while ((int)(ld_acquire_sys(flag) - v) < 0) {
+    if (globaltimer_ns() - t0 > timeout_ns) return false;
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// 1 CTA.  After bucket_kernel: epoch += 1; the send list (local row, a, e in
+// owner order) into this rank's control area; then to every peer q: this
+// rank's count row + layout hash into q's mailbox, release flag.
+__global__ void __launch_bounds__(1024) push_announce_kernel(PeerCtl pc, int me, int G, int max_rows,
+                                                             const int32_t* __restrict__ counts,
+                                                             const int32_t* __restrict__ send_idx,
+                                                             const int32_t* __restrict__ ad,
+                                                             const int32_t* __restrict__ ex) {
+  __shared__ unsigned int s_epoch;
+  ShardCtl* mine = pc.p[me];
+  if (threadIdx.x == 0) {
+    s_epoch = mine->epoch + 1;
+    mine->epoch = s_epoch;
+  }
+  int n_send = 0;
+  for (int q = 0; q < G; ++q) n_send += counts[q];
+  int32_t* srow = ctl_send(mine, max_rows, 0);
+  int32_t* sa = ctl_send(mine, max_rows, 1);
+  int32_t* se = ctl_send(mine, max_rows, 2);
+  for (int j = threadIdx.x; j < n_send; j += blockDim.x) {
+    const int r = send_idx[j];
+    srow[j] = r;
+    sa[j] = ad[r];
+    se[j] = ex ? ex[r] : 0;
+  }
+  __syncthreads();
+  const unsigned int v = s_epoch;
+  if (threadIdx.x < G) {
+    const int q = threadIdx.x;
+    int* mb = pc.p[q]->mbox[v & 1][me];
+    for (int k = 0; k <= G; ++k) mb[k] = counts[k];
+    __threadfence_system();  // the send arrays (whole CTA, ordered by the barrier) and the row before the flag
+    st_release_sys(&pc.p[q]->flag_cnt[me], v);
+  }
+}
+
+// 1 CTA (owner side, second stream).  Waits for every source's count row of
+// this epoch; received rows: by source rank ascending, then each source's
+// send order (R18).  Pulls each received row's ids from its source's
+// control area and records its origin (source << 24 | source-local row).
+// *n_recv = the received row count (0 on a timeout or a layout mismatch, with
+// the sticky error flag set).
+__global__ void __launch_bounds__(1024) push_recv_prep_kernel(PeerCtl pc, int me, int G, int max_rows, int hash,
+                                                              int32_t* __restrict__ ids_a, int32_t* __restrict__ ids_e,
+                                                              int32_t* __restrict__ origin, int* __restrict__ n_recv,
+                                                              int cap, int* __restrict__ err,
+                                                              unsigned long long timeout_ns) {
+  __shared__ int s_off[kMaxWorld + 1], s_base[kMaxWorld], s_ok;
+  ShardCtl* mine = pc.p[me];
+  const unsigned int v = mine->epoch;  // set by this rank's announce (same stream order)
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < G) {
+    if (!wait_flag(&mine->flag_cnt[threadIdx.x], v, timeout_ns)) {
+      atomicOr(err, kErrPeer);
+      s_ok = 0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int p = 0; p < G; ++p) {
+      const volatile int* row = mine->mbox[v & 1][p];
+      if (s_ok && row[G] != hash) {
+        atomicOr(err, kErrLayout);
+        s_ok = 0;
+      }
+      int base = 0;
+      for (int q = 0; q < me; ++q) base += row[q];  // p's rows for owners before me
+      s_base[p] = base;
+      s_off[p] = off;
+      off += row[me];
+    }
+    if (!s_ok || off > cap) {
+      if (off > cap) atomicOr(err, kErrLayout);
+      for (int p = 0; p <= G; ++p) s_off[p] = 0;
+      off = 0;
+    }
+    s_off[G] = off;
+    *n_recv = off;
+  }
+  __syncthreads();
+  const int n = s_off[G];
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    int p = 0;
+    while (p + 1 < G && s_off[p + 1] <= r) ++p;
+    ShardCtl* src = pc.p[p];
+    const int j = s_base[p] + (r - s_off[p]);
+    ids_a[r] = ctl_send(src, max_rows, 1)[j];
+    ids_e[r] = ctl_send(src, max_rows, 2)[j];
+    origin[r] = (p << kOriginRowBits) | ctl_send(src, max_rows, 0)[j];
+  }
+}
+
+// owner side, after its pushes: release flag "done for epoch v" into every peer
+__global__ void push_done_kernel(PeerCtl pc, int me, int G) {
+  const unsigned int v = pc.p[me]->epoch;
+  __threadfence_system();
+  if (threadIdx.x < G) st_release_sys(&pc.p[threadIdx.x]->flag_done[me], v);
+}
+
+// source side: wait until every owner has pushed this epoch's deltas
+__global__ void push_wait_kernel(PeerCtl pc, int me, int G, int* err, unsigned long long timeout_ns) {
+  ShardCtl* mine = pc.p[me];
+  const unsigned int v = mine->epoch;
+  if (threadIdx.x < G && !wait_flag(&mine->flag_done[threadIdx.x], v, timeout_ns)) atomicOr(err, kErrPeer);
+}
+
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// host state
+// ---------------------------------------------------------------------------
+struct RegBuf {
+  char* ptr;
+  size_t bytes;
+};
 
 struct ShardState {
   ncclComm_t comm = nullptr;
-  cudaStream_t cs = nullptr;  // communication stream (pack + NCCL)
+  cudaStream_t cs = nullptr;  // communication stream
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  void* buf = nullptr;        // device scratch (grown on demand)
+  void* buf = nullptr;        // device scratch (grown on demand; NCCL path)
   size_t bytes = 0;
   lora_plan* plan = nullptr;        // owner-side plan over received rows (capacity max_rows * world)
   lora_plan* local_plan = nullptr;  // plan over this rank's rows processed in place
   bool fp32_return = false;
   bool loopback = false;
-  // peer-to-peer transport: registered (IPC-exported) buffers, mapped on every rank
-  bool p2p = true;
-  void* sendbuf = nullptr;  // [2][max_rows] ids + per distinct x buffer [max_rows][h_in] bf16, send order
-  void* dbuf = nullptr;     // per slot [Rmax][h_out] deltas of received rows
-  size_t send_cap = 0, d_cap = 0;
-  std::vector<char*> peer_send, peer_d;  // index = rank (own rank: the local pointers)
-  int* d_bar = nullptr;                   // barrier word (NCCL all-reduce)
   // host control plane (lora_server_create_sharded_host): no NCCL at all
   lora_host_allgather_fn host_ag = nullptr;
   void* host_ctx = nullptr;
-  int32_t* h_cnt = nullptr;  // pinned [world][world] counts (async read-back)
+  int32_t* h_cnt = nullptr;  // pinned [world][world + 1] counts (async read-back, NCCL path)
+  // push path: registered buffers and the control areas
+  ShardCtl* ctl = nullptr;                 // this rank's control area (IPC-exported)
+  size_t ctl_bytes = 0;
+  PeerCtl peer_ctl{};
+  std::vector<RegBuf> reg;                 // this rank's registered buffers, in registration order
+  std::vector<char*> reg_peer;             // [k * world + p] base of buffer k on rank p
+  char** d_reg = nullptr;                  // device copy of reg_peer
+  std::vector<void*> opened;               // IPC mappings to close at destroy
+  int32_t* d_push = nullptr;               // owner side: [3][Rmax] ids_a | ids_e | origin, + n_recv
+  unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
 };
 
 // Control plane.  Blocking all-gather of small host blobs (IPC handles,
@@ -330,40 +454,25 @@ static lora_status_t ctl_allgather(lora_server* s, const void* send_h, void* rec
   return r == ncclSuccess ? LORA_OK : fail(s, LORA_ERR_NCCL, std::string("all-gather: ") + api.GetErrorString(r));
 }
 
-// Barrier in the order of `st`: an NCCL all-reduce of one word (no host
-// sync), or -- host control plane -- a stream synchronize and a host barrier.
-static lora_status_t ctl_barrier(lora_server* s, cudaStream_t st) {
-  ShardState* sh = s->shard;
-  if (sh->host_ag) {
-    char b = 0;
-    std::vector<char> all(s->world);
-    return ctl_allgather(s, &b, all.data(), 1, st);
-  }
-  NcclApi& api = nccl();
-  const ncclResult_t r = api.AllReduce(sh->d_bar, sh->d_bar, 1, ncclInt32, ncclSum, sh->comm, st);
-  return r == ncclSuccess ? LORA_OK : fail(s, LORA_ERR_NCCL, std::string("barrier: ") + api.GetErrorString(r));
-}
-
-// Release the peer mappings and the registered buffers.
-static void p2p_release(ShardState* sh, int me) {
-  for (size_t p = 0; p < sh->peer_send.size(); ++p)
-    if ((int)p != me) {
-      if (sh->peer_send[p]) cudaIpcCloseMemHandle(sh->peer_send[p]);
-      if (sh->peer_d[p]) cudaIpcCloseMemHandle(sh->peer_d[p]);
-    }
-  sh->peer_send.clear();
-  sh->peer_d.clear();
-  cudaFree(sh->sendbuf);
-  cudaFree(sh->dbuf);
-  sh->sendbuf = sh->dbuf = nullptr;
-  sh->send_cap = sh->d_cap = 0;
+// Release the peer mappings, the control area and the registration tables.
+static void push_release(ShardState* sh) {
+  for (void* p : sh->opened) cudaIpcCloseMemHandle(p);
+  sh->opened.clear();
+  cudaFree(sh->ctl);
+  cudaFree(sh->d_reg);
+  cudaFree(sh->d_push);
+  sh->ctl = nullptr;
+  sh->d_reg = nullptr;
+  sh->d_push = nullptr;
+  sh->reg.clear();
+  sh->reg_peer.clear();
+  sh->peer_ctl = PeerCtl{};
 }
 
 void lora_shard_free(lora_server* s) {
   if (!s || !s->shard) return;
   ShardState* sh = s->shard;
-  p2p_release(sh, s->shard_rank);
-  cudaFree(sh->d_bar);
+  push_release(sh);
   if (sh->h_cnt) cudaFreeHost(sh->h_cnt);
   if (sh->comm && nccl().ok) nccl().CommDestroy(sh->comm);
   cudaFree(sh->buf);
@@ -374,6 +483,19 @@ void lora_shard_free(lora_server* s) {
   if (sh->cs) cudaStreamDestroy(sh->cs);
   delete sh;
   s->shard = nullptr;
+}
+
+// sticky-flag bits beyond "bad id" (lora_server_check); NCCL asynchronous errors
+lora_status_t lora_shard_check_flags(lora_server* s, int flag) {
+  if (flag & kErrLayout)
+    return fail(s, LORA_ERR_PEER, "sharded apply: ranks disagreed on the call's layout (slots / buffers / dtype)");
+  if (flag & kErrPeer) return fail(s, LORA_ERR_PEER, "sharded apply: a peer did not signal in time");
+  if (s->shard && s->shard->comm && nccl().ok && nccl().CommGetAsyncError) {
+    ncclResult_t ar = ncclSuccess;
+    if (nccl().CommGetAsyncError(s->shard->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+      return fail(s, LORA_ERR_NCCL, std::string("NCCL asynchronous error: ") + nccl().GetErrorString(ar));
+  }
+  return LORA_OK;
 }
 
 extern "C" lora_status_t lora_shard_layout(const int64_t* counts, int32_t world, int32_t rank, int64_t* send_off,
@@ -434,7 +556,6 @@ extern "C" lora_status_t lora_server_create_sharded_host(const lora_config_t* cf
                                                          lora_host_allgather_fn allgather, void* ctx,
                                                          lora_server_t** out) {
   if (!allgather) return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded_host: NULL all-gather");
-  if (world > kMaxWorld) return fail(nullptr, LORA_ERR_UNSUPPORTED, "host control plane: world > 8");
   return create_sharded_impl(cfg, rank, world, nullptr, allgather, ctx, out);
 }
 
@@ -443,8 +564,10 @@ static lora_status_t create_sharded_impl(const lora_config_t* cfg, int32_t rank,
                                          lora_server_t** out) {
   if (!cfg || !out || world < 1 || rank < 0 || rank >= world)
     return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded: bad argument");
+  if (world > kMaxWorld) return fail(nullptr, LORA_ERR_UNSUPPORTED, "world > 8 (one NVLink domain of B200s)");
   if ((long long)cfg->max_rows * world > kMaxPlanRows)
     return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows * world must be <= 16384 (owner-side plan capacity)");
+  if (cfg->max_rows >= (1 << kOriginRowBits)) return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows too large");
   if (cfg->n_replicated < 0) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_replicated < 0");
   NcclApi& api = nccl();
   if (!host_ag && !api.ok) return fail(nullptr, LORA_ERR_NCCL, api.err);
@@ -459,24 +582,16 @@ static lora_status_t create_sharded_impl(const lora_config_t* cfg, int32_t rank,
   sh->fp32_return = f32 && f32[0] && std::strcmp(f32, "0") != 0;
   const char* lb = std::getenv("LORA_SHARD_LOOPBACK");
   sh->loopback = lb && lb[0] && std::strcmp(lb, "0") != 0;
-  const char* tr = std::getenv("LORA_SHARD_TRANSPORT");
-  sh->p2p = !(tr && std::strcmp(tr, "nccl") == 0);
-  if (world > kMaxWorld) sh->p2p = false;
-  if (host_ag) sh->p2p = true;  // the only transport without NCCL
+  if (const char* to = std::getenv("LORA_SHARD_TIMEOUT_MS"))
+    sh->timeout_ns = (unsigned long long)std::max(1L, std::atol(to)) * 1000000ull;
   cudaSetDevice(s->device);
   bool ok = cudaStreamCreateWithFlags(&sh->cs, cudaStreamNonBlocking) == cudaSuccess;
   for (auto& e : sh->ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaMallocHost(&sh->h_cnt, sizeof(int32_t) * world * (world + 1)) == cudaSuccess;
   if (!ok) {
     lora_server_destroy(s);
     *out = nullptr;
-    return fail(nullptr, LORA_ERR_CUDA, "stream / event creation failed");
-  }
-  ok = ok && cudaMalloc(&sh->d_bar, sizeof(int)) == cudaSuccess && cudaMemset(sh->d_bar, 0, sizeof(int)) == cudaSuccess;
-  ok = ok && cudaMallocHost(&sh->h_cnt, sizeof(int32_t) * world * world) == cudaSuccess;
-  if (!ok) {
-    lora_server_destroy(s);
-    *out = nullptr;
-    return fail(nullptr, LORA_ERR_CUDA, "barrier word allocation failed");
+    return fail(nullptr, LORA_ERR_CUDA, "stream / event / pinned allocation failed");
   }
   if (!host_ag) {
     ncclUniqueId id;
@@ -497,72 +612,154 @@ static lora_status_t create_sharded_impl(const lora_config_t* cfg, int32_t rank,
     *out = nullptr;
     return fail(nullptr, st, m);
   }
+  // the owner plan's tcgen05 shrink split follows the typical received count
+  // (about one rank's rows), not its capacity
+  sh->plan->T_hint = cfg->max_rows;
   return LORA_OK;
 }
 
-// Grow the registered P2P buffers to (need_send, need_d) bytes -- collective:
-// every rank computes the same sizes from the same slot list.  Exports IPC
-// handles, all-gathers them over NCCL and maps every peer's buffers; if any
-// rank cannot map a peer, every rank falls back to the NCCL transport.
-static lora_status_t p2p_register(lora_server* s, size_t need_send, size_t need_d, cudaStream_t st) {
+// ---------------------------------------------------------------------------
+// registration (collective): CUDA IPC export of the allocation holding each
+// buffer, all-gathered; every peer's allocations mapped once each
+// ---------------------------------------------------------------------------
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+static PFN_memGetAddressRange address_range_fn() {
+  static PFN_memGetAddressRange fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_memGetAddressRange>(f);
+  }();
+  return fn;
+}
+
+struct RegInfo {  // one exported buffer (all-gathered)
+  cudaIpcMemHandle_t h;
+  int64_t offset;   // buffer start - allocation base
+  int64_t bytes;
+};
+
+// export one buffer: handle of its allocation + offset (ok = false on failure)
+static bool export_buffer(const void* ptr, size_t bytes, RegInfo& ri) {
+  std::memset(&ri, 0, sizeof(ri));
+  auto range = address_range_fn();
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!range || range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) return false;
+  if (reinterpret_cast<uintptr_t>(ptr) + bytes > base + size) return false;
+  if (cudaIpcGetMemHandle(&ri.h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  ri.offset = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - base);
+  ri.bytes = (int64_t)bytes;
+  return true;
+}
+
+extern "C" lora_status_t lora_shard_register(lora_server_t* s, int32_t n, void* const* ptrs, const int64_t* bytes,
+                                             void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (!s->shard) return fail(s, LORA_ERR_INVALID_ARG, "not a sharded server");
+  if (n < 0 || (n > 0 && (!ptrs || !bytes))) return fail(s, LORA_ERR_INVALID_ARG, "bad buffer list");
   ShardState* sh = s->shard;
-  NcclApi& api = nccl();
   const int G = s->world, me = s->shard_rank;
-  if (need_send <= sh->send_cap && need_d <= sh->d_cap) return LORA_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaSetDevice(s->device) != cudaSuccess) return fail(s, LORA_ERR_CUDA, "cudaSetDevice");
   cudaStreamSynchronize(st);
   cudaStreamSynchronize(sh->cs);
-  p2p_release(sh, me);
-  need_send = std::max(need_send, (size_t)1 << 20);
-  need_d = std::max(need_d, (size_t)1 << 20);
-  if (cudaMalloc(&sh->sendbuf, need_send) != cudaSuccess || cudaMalloc(&sh->dbuf, need_d) != cudaSuccess) {
-    cudaGetLastError();
-    p2p_release(sh, me);
-    return fail(s, LORA_ERR_OOM, "P2P buffer allocation failed");
-  }
-  sh->send_cap = need_send;
-  sh->d_cap = need_d;
-  sh->peer_send.assign(G, nullptr);
-  sh->peer_d.assign(G, nullptr);
-  sh->peer_send[me] = static_cast<char*>(sh->sendbuf);
-  sh->peer_d[me] = static_cast<char*>(sh->dbuf);
-  if (G == 1) return LORA_OK;
-  // handle exchange: [G][2][64 bytes]
-  // A rank whose export fails still takes part in both all-gathers (zeroed
-  // handles, ok = 0), so every rank reaches the same decision instead of the
-  // others blocking in the handle exchange.
-  std::vector<cudaIpcMemHandle_t> h(2 * G);
   int ok = 1;
-  if (cudaIpcGetMemHandle(&h[2 * me], sh->sendbuf) != cudaSuccess ||
-      cudaIpcGetMemHandle(&h[2 * me + 1], sh->dbuf) != cudaSuccess) {
-    cudaGetLastError();
-    std::memset(&h[2 * me], 0, 2 * sizeof(cudaIpcMemHandle_t));
-    ok = 0;
-  }
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  std::vector<cudaIpcMemHandle_t> mine(h.begin() + 2 * me, h.begin() + 2 * me + 2);
-  lora_status_t rc = ctl_allgather(s, mine.data(), h.data(), 128, st);
-  if (rc != LORA_OK) return rc;
-  for (int p = 0; p < G && ok; ++p) {
-    if (p == me) continue;
-    void* a = nullptr;
-    void* b = nullptr;
-    if (cudaIpcOpenMemHandle(&a, h[2 * p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-        cudaIpcOpenMemHandle(&b, h[2 * p + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+  for (int i = 0; i < n; ++i)
+    if (!ptrs[i] || bytes[i] <= 0) ok = 0;
+  // the control area (first registration)
+  bool new_ctl = false;
+  if (!sh->ctl) {
+    sh->ctl_bytes = sizeof(ShardCtl) + sizeof(int32_t) * 3 * (size_t)s->max_rows;
+    if (cudaMalloc(&sh->ctl, sh->ctl_bytes) != cudaSuccess ||
+        cudaMemset(sh->ctl, 0, sh->ctl_bytes) != cudaSuccess ||
+        cudaMalloc(&sh->d_push, sizeof(int32_t) * (3 * (size_t)s->max_rows * G + 4)) != cudaSuccess) {
       cudaGetLastError();
       ok = 0;
     }
-    sh->peer_send[p] = static_cast<char*>(a);
-    sh->peer_d[p] = static_cast<char*>(b);
+    new_ctl = true;
   }
-  // every rank must agree on the transport
-  std::vector<int> oks(G, 0);
-  rc = ctl_allgather(s, &ok, oks.data(), sizeof(int), st);
+  // blob: [n | ok | pad] [ctl RegInfo] [n RegInfo]
+  const size_t blob = 16 + sizeof(RegInfo) * (1 + (size_t)n);
+  std::vector<char> mine(blob, 0), all(blob * G, 0);
+  RegInfo* ri = reinterpret_cast<RegInfo*>(mine.data() + 16);
+  if (ok && new_ctl && !export_buffer(sh->ctl, sh->ctl_bytes, ri[0])) ok = 0;
+  for (int i = 0; i < n && ok; ++i)
+    if (!export_buffer(ptrs[i], (size_t)bytes[i], ri[1 + i])) ok = 0;
+  reinterpret_cast<int32_t*>(mine.data())[0] = n;
+  reinterpret_cast<int32_t*>(mine.data())[1] = ok;
+  lora_status_t rc = ctl_allgather(s, mine.data(), all.data(), blob, st);
+  if (rc != LORA_OK) return rc;
+  for (int p = 0; p < G; ++p) {
+    const int32_t* hd = reinterpret_cast<const int32_t*>(all.data() + blob * p);
+    if (hd[0] != n) ok = 0;  // every rank must register the same number of buffers
+    if (!hd[1]) ok = 0;
+  }
+  // map every peer's allocations (each distinct handle once per peer)
+  std::vector<char*> ctl_peer(G, nullptr), peer_base((size_t)n * G, nullptr);
+  std::vector<std::pair<std::string, void*>> mapped;
+  auto open = [&](const cudaIpcMemHandle_t& h) -> char* {
+    const std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+    for (auto& m : mapped)
+      if (m.first == key) return static_cast<char*>(m.second);
+    void* a = nullptr;
+    if (cudaIpcOpenMemHandle(&a, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    mapped.push_back({key, a});
+    sh->opened.push_back(a);
+    return static_cast<char*>(a);
+  };
+  for (int p = 0; p < G && ok; ++p) {
+    const RegInfo* pr = reinterpret_cast<const RegInfo*>(all.data() + blob * p + 16);
+    if (p == me) {
+      ctl_peer[p] = reinterpret_cast<char*>(sh->ctl);
+      for (int i = 0; i < n; ++i) peer_base[(size_t)i * G + p] = static_cast<char*>(ptrs[i]);
+      continue;
+    }
+    mapped.clear();  // handles are per exporting process
+    if (new_ctl) {
+      char* b = open(pr[0].h);
+      if (!b) ok = 0;
+      ctl_peer[p] = b ? b + pr[0].offset : nullptr;
+    }
+    for (int i = 0; i < n && ok; ++i) {
+      char* b = open(pr[1 + i].h);
+      if (!b) ok = 0;
+      peer_base[(size_t)i * G + p] = b ? b + pr[1 + i].offset : nullptr;
+    }
+  }
+  // every rank must agree that every mapping worked
+  std::vector<int32_t> oks(G, 0);
+  rc = ctl_allgather(s, &ok, oks.data(), sizeof(int32_t), st);
   if (rc != LORA_OK) return rc;
   for (int v : oks) ok = ok && v;
   if (!ok) {
-    p2p_release(sh, me);
-    if (sh->host_ag) return fail(s, LORA_ERR_UNSUPPORTED, "peer mapping failed and the host control plane has no fallback");
-    sh->p2p = false;  // NCCL send/recv from now on, on every rank
+    push_release(sh);
+    return fail(s, LORA_ERR_UNSUPPORTED,
+                "lora_shard_register: a buffer could not be exported or mapped on some rank (every rank released "
+                "its registrations)");
+  }
+  if (new_ctl)
+    for (int p = 0; p < G; ++p) sh->peer_ctl.p[p] = reinterpret_cast<ShardCtl*>(ctl_peer[p]);
+  for (int i = 0; i < n; ++i) {
+    sh->reg.push_back({static_cast<char*>(ptrs[i]), (size_t)bytes[i]});
+    for (int p = 0; p < G; ++p) sh->reg_peer.push_back(peer_base[(size_t)i * G + p]);
+  }
+  cudaFree(sh->d_reg);
+  sh->d_reg = nullptr;
+  if (!sh->reg_peer.empty()) {
+    if (cudaMalloc(&sh->d_reg, sizeof(char*) * sh->reg_peer.size()) != cudaSuccess ||
+        cudaMemcpy(sh->d_reg, sh->reg_peer.data(), sizeof(char*) * sh->reg_peer.size(), cudaMemcpyHostToDevice) !=
+            cudaSuccess)
+      return fail(s, LORA_ERR_OOM, "registration table");
   }
   return LORA_OK;
 }
@@ -578,30 +775,132 @@ static lora_status_t p2p_register(lora_server* s, size_t need_send, size_t need_
     if (_r != ncclSuccess) return fail(s, LORA_ERR_NCCL, std::string(#call ": ") + api.GetErrorString(_r)); \
   } while (0)
 
-extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const int32_t* slots, const void* const* x,
-                                            const int32_t* adapter_ids, const int32_t* expert_ids, void* const* y,
-                                            lora_dtype_t y_dtype, int32_t T, void* stream) {
-  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
-  if (!s->shard) return fail(s, LORA_ERR_INVALID_ARG, "not a sharded server");
-  if (n < 1 || !slots || !x || !y || (T > 0 && !adapter_ids)) return fail(s, LORA_ERR_INVALID_ARG, "NULL argument");
-  if (T < 0 || T > s->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");
-  if (y_dtype != LORA_BF16 && y_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "y_dtype");
-  for (int i = 0; i < n; ++i)
-    if (slots[i] < 0 || slots[i] >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
+// index of a registered buffer starting at p (-1: none)
+static int reg_index(const ShardState* sh, const void* p) {
+  for (size_t k = 0; k < sh->reg.size(); ++k)
+    if (sh->reg[k].ptr == p) return (int)k;
+  return -1;
+}
+
+// FNV-1a over the call's layout: every rank must pass the same slots in the
+// same order, the same registered-buffer roles and the same y dtype
+static int layout_hash(int n, const int32_t* slots, const std::vector<int>& xk, const std::vector<int>& yk,
+                       lora_dtype_t dt) {
+  uint32_t h = 2166136261u;
+  auto mix = [&](int v) {
+    for (int b = 0; b < 4; ++b) {
+      h ^= (uint32_t)((v >> (8 * b)) & 0xFF);
+      h *= 16777619u;
+    }
+  };
+  mix(n);
+  mix((int)dt);
+  for (int i = 0; i < n; ++i) {
+    mix(slots[i]);
+    mix(xk[i]);
+    mix(yk[i]);
+  }
+  return (int)(h & 0x7FFFFFFF);
+}
+
+// ---------------------------------------------------------------------------
+// the push path
+// ---------------------------------------------------------------------------
+static lora_status_t apply_sharded_push(lora_server* s, int n, const int32_t* slots, const void* const* x,
+                                        const int32_t* adapter_ids, const int32_t* expert_ids, void* const* y,
+                                        lora_dtype_t y_dtype, int T, cudaStream_t st, const std::vector<int>& xk,
+                                        const std::vector<int>& yk) {
+  ShardState* sh = s->shard;
+  const int G = s->world, me = s->shard_rank;
   const int E = s->slots[slots[0]].E;
-  for (int i = 0; i < n; ++i)
-    if (s->slots[slots[i]].E != E) return fail(s, LORA_ERR_INVALID_ARG, "slots of one call must share n_experts");
+  const Placement pl = placement(s);
+  const long long Rmax = (long long)s->max_rows * G;
+  const int hash = layout_hash(n, slots, xk, yk, y_dtype);
+  // scratch: counts [G + 1], send_idx [max_rows], ad_local [max_rows]
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t o_counts = 0, o_send_idx = al(sizeof(int32_t) * (G + 1)),
+               o_ad_local = o_send_idx + al(sizeof(int32_t) * s->max_rows),
+               need = o_ad_local + al(sizeof(int32_t) * s->max_rows);
+  if (need > sh->bytes) {
+    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(sh->cs);
+    cudaFree(sh->buf);
+    sh->buf = nullptr;
+    sh->bytes = 0;
+    CKS(cudaMalloc(&sh->buf, need));
+    sh->bytes = need;
+  }
+  char* base = static_cast<char*>(sh->buf);
+  int32_t* d_counts = reinterpret_cast<int32_t*>(base + o_counts);
+  int32_t* d_send_idx = reinterpret_cast<int32_t*>(base + o_send_idx);
+  int32_t* d_ad_local = reinterpret_cast<int32_t*>(base + o_ad_local);
+  int32_t* ids_a = sh->d_push;
+  int32_t* ids_e = ids_a + Rmax;
+  int32_t* origin = ids_e + Rmax;
+  int* n_recv = origin + Rmax;
+
+  // 1. bucket + announce
+  int pi = prof_start(s, st);
+  bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, expert_ids, T, pl, s->n_adapters, E, sh->loopback,
+                                              d_ad_local, d_send_idx, d_counts, s->d_err, hash);
+  push_announce_kernel<<<1, 1024, 0, st>>>(sh->peer_ctl, me, G, s->max_rows, d_counts, d_send_idx, adapter_ids,
+                                           expert_ids);
+  prof_stop(s, pi, kKShardBucket, st);
+  CKS(cudaGetLastError());
+  // 2. owner side on the communication stream (overlaps the in-place apply)
+  CKS(cudaEventRecord(sh->ev[0], st));
+  CKS(cudaStreamWaitEvent(sh->cs, sh->ev[0], 0));
+  pi = prof_start(s, sh->cs);
+  push_recv_prep_kernel<<<1, 1024, 0, sh->cs>>>(sh->peer_ctl, me, G, s->max_rows, hash, ids_a, ids_e, origin, n_recv,
+                                                (int)Rmax, s->d_err, sh->timeout_ns);
+  prof_stop(s, pi, kKShardGather, sh->cs);
+  CKS(cudaGetLastError());
+  lora_status_t rc = plan_build_impl(s, sh->plan, ids_a, ids_e, (int)Rmax, E, sh->cs, n_recv);
+  if (rc != LORA_OK) return rc;
+  CKS(cudaEventRecord(sh->ev[1], sh->cs));
+  //    in-place rows (this rank's own or replicated units)
+  rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
+  if (rc != LORA_OK) return rc;
+  if (T > 0) {
+    rc = apply_multi_impl(s, sh->local_plan, n, slots, x, y, y_dtype, st);
+    if (rc != LORA_OK) return rc;
+  }
+  // 3. owner apply: remote-x shrink, push-add expand
+  CKS(cudaStreamWaitEvent(st, sh->ev[1], 0));
+  PushIn push{G, origin, sh->d_reg};
+  std::vector<int16_t> xr(n), yr(n);
+  for (int i = 0; i < n; ++i) {
+    xr[i] = (int16_t)xk[i];
+    yr[i] = (int16_t)yk[i];
+  }
+  rc = apply_multi_impl(s, sh->plan, n, slots, x, y, y_dtype, st, 3, &push, xr.data(), yr.data());
+  if (rc != LORA_OK) return rc;
+  // 4. done -> peers; wait for every owner's pushes into this rank's y
+  pi = prof_start(s, st);
+  push_done_kernel<<<1, 32, 0, st>>>(sh->peer_ctl, me, G);
+  push_wait_kernel<<<1, 32, 0, st>>>(sh->peer_ctl, me, G, s->d_err, sh->timeout_ns);
+  prof_stop(s, pi, kKShardScatter, st);
+  CKS(cudaGetLastError());
+  if (s->debug_sync) CKS(cudaStreamSynchronize(st));
+  return LORA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the NCCL path (unregistered buffers)
+// ---------------------------------------------------------------------------
+static lora_status_t apply_sharded_nccl(lora_server* s, int n, const int32_t* slots, const void* const* x,
+                                        const int32_t* adapter_ids, const int32_t* expert_ids, void* const* y,
+                                        lora_dtype_t y_dtype, int T, cudaStream_t st) {
   NcclApi& api = nccl();
   const int G = s->world, me = s->shard_rank;
   const Placement pl = placement(s);
   ShardState* sh = s->shard;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaStream_t cs = sh->cs;
-  CKS(cudaSetDevice(s->device));
+  const int E = s->slots[slots[0]].E;
   const bool d_bf16 = (y_dtype == LORA_BF16) && !sh->fp32_return;
   const size_t dsz = d_bf16 ? 2 : 4;
 
-  // distinct x buffers
+  // distinct x buffers (send-buffer regions, one NCCL message each)
   std::vector<const void*> xd;
   std::vector<int> x_of(n);
   for (int i = 0; i < n; ++i) {
@@ -612,12 +911,16 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   }
   std::vector<int> x_hin(xd.size());
   for (int i = 0; i < n; ++i) x_hin[x_of[i]] = s->slots[slots[i]].h_in;
+  // the message layout depends on this x de-duplication: every rank must get
+  // the same pattern (checked through the hash word of the count exchange)
+  std::vector<int> yk(n, 0);
+  const int hash = layout_hash(n, slots, x_of, yk, y_dtype);
 
   // scratch layout (worst case: every rank sends every row to me -> G*T rows)
   const long long Rmax = (long long)s->max_rows * G;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   size_t off = 0;
-  const size_t o_counts = off; off += al(sizeof(int32_t) * G * (G + 1));
+  const size_t o_counts = off; off += al(sizeof(int32_t) * (G + 1) * (G + 1));
   const size_t o_send_idx = off; off += al(sizeof(int32_t) * s->max_rows);
   const size_t o_ad_local = off; off += al(sizeof(int32_t) * s->max_rows);
   const size_t o_ids_send = off; off += al(sizeof(int32_t) * 2 * s->max_rows);
@@ -642,7 +945,7 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
     sh->bytes = off;
   }
   char* base = static_cast<char*>(sh->buf);
-  int32_t* d_counts = reinterpret_cast<int32_t*>(base + o_counts);  // [G] mine, then [G][G] gathered
+  int32_t* d_counts = reinterpret_cast<int32_t*>(base + o_counts);  // [G+1] mine, then [G][G+1] gathered
   int32_t* d_send_idx = reinterpret_cast<int32_t*>(base + o_send_idx);
   int32_t* d_ad_local = reinterpret_cast<int32_t*>(base + o_ad_local);
   int32_t* d_ids_send = reinterpret_cast<int32_t*>(base + o_ids_send);  // [2][max_rows] (a | e) in send order
@@ -651,198 +954,96 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   // 1. classify + bucket.  The previous call's comm-stream work (reads of the
   //    scratch) must be done before it is overwritten: ev[3] was recorded last.
   CKS(cudaStreamWaitEvent(st, sh->ev[3], 0));
-  if (T > 0) {
-    const int pi = prof_start(s, st);
-    bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, expert_ids, T, pl, s->n_adapters, E, sh->loopback, d_ad_local, d_send_idx, d_counts,
-                                                 s->d_err);
-    prof_stop(s, pi, kKShardBucket, st);
-  } else {
-    CKS(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * G, st));
-  }
+  const int pi = prof_start(s, st);
+  bucket_kernel<<<1, kBucketThreads, 0, st>>>(adapter_ids, expert_ids, T, pl, s->n_adapters, E, sh->loopback,
+                                              d_ad_local, d_send_idx, d_counts, s->d_err, hash);
+  prof_stop(s, pi, kKShardBucket, st);
   CKS(cudaGetLastError());
-  // 2. counts exchange (all-gather) + the one host wait.  NCCL control plane:
-  //    the matrix comes back asynchronously into pinned memory; the in-place
-  //    rows' plan and apply are enqueued before the host waits for it, so the
-  //    GPU keeps working through the host round trip.
-  std::vector<int32_t> cnt(G * G);
-  if (!sh->host_ag) {
-    CKN(api.AllGather(d_counts, d_counts + G, G, ncclInt32, sh->comm, st));
-    CKS(cudaMemcpyAsync(sh->h_cnt, d_counts + G, sizeof(int32_t) * G * G, cudaMemcpyDeviceToHost, st));
-  }
+  // 2. counts exchange (all-gather) + the one host wait; the in-place rows'
+  //    plan and apply are enqueued before the host waits for the matrix.
+  CKN(api.AllGather(d_counts, d_counts + (G + 1), G + 1, ncclInt32, sh->comm, st));
+  CKS(cudaMemcpyAsync(sh->h_cnt, d_counts + (G + 1), sizeof(int32_t) * G * (G + 1), cudaMemcpyDeviceToHost, st));
   CKS(cudaEventRecord(sh->ev[0], st));  // bucket outputs + counts ready (the pack waits on this)
-  // 3. rows this rank stores the adapter of: applied in place (independent of the counts)
   lora_status_t rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
   if (rc != LORA_OK) return rc;
   if (T > 0) {
     rc = apply_multi_impl(s, sh->local_plan, n, slots, x, y, y_dtype, st);
     if (rc != LORA_OK) return rc;
   }
-  if (sh->host_ag) {
-    std::vector<int32_t> mine(G);
-    CKS(cudaMemcpyAsync(mine.data(), d_counts, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
-    const lora_status_t cr = ctl_allgather(s, mine.data(), cnt.data(), sizeof(int32_t) * G, st);
-    if (cr != LORA_OK) return cr;
-  } else {
-    CKS(cudaEventSynchronize(sh->ev[0]));
-    std::memcpy(cnt.data(), sh->h_cnt, sizeof(int32_t) * G * G);
+  CKS(cudaEventSynchronize(sh->ev[0]));
+  std::vector<int64_t> c64((size_t)G * G), so(G + 1), ro(G + 1);
+  for (int p = 0; p < G; ++p) {
+    if (sh->h_cnt[p * (G + 1) + G] != hash)  // every rank sees every hash: all fail together
+      return fail(s, LORA_ERR_INVALID_ARG, "sharded apply: ranks disagree on the call's layout (slots / x buffers / "
+                                           "dtype); nothing exchanged");
+    for (int q = 0; q < G; ++q) c64[(size_t)p * G + q] = sh->h_cnt[p * (G + 1) + q];
   }
-  std::vector<int64_t> c64(cnt.begin(), cnt.end()), so(G + 1), ro(G + 1);
   lora_status_t lr = lora_shard_layout(c64.data(), G, me, so.data(), ro.data());
   if (lr != LORA_OK) return fail(s, lr, "count exchange produced an invalid matrix");
   const int n_send = (int)so[G], n_recv = (int)ro[G];
   if (n_recv > Rmax) return fail(s, LORA_ERR_INVALID_ARG, "received rows exceed capacity");
-  // every rank sees the same matrix, so every rank takes the same branch
-  bool exchange = false;
-  for (int v : cnt) exchange = exchange || v > 0;
-
-  // peer-to-peer transport: registered buffer layout (identical on every rank)
-  size_t p_need_send = 0, p_need_d = 0;
-  std::vector<size_t> p_xo(xd.size()), p_doff(n);
-  p_need_send = al(sizeof(int32_t) * 2 * s->max_rows);
-  for (size_t j = 0; j < xd.size(); ++j) {
-    p_xo[j] = p_need_send;
-    p_need_send += al((size_t)s->max_rows * x_hin[j] * 2);
-  }
-  for (int i = 0; i < n; ++i) {
-    p_doff[i] = p_need_d;
-    p_need_d += al((size_t)Rmax * s->slots[slots[i]].h_out * dsz);
-  }
-  if (exchange && sh->p2p) {
-    const lora_status_t rr = p2p_register(s, p_need_send, p_need_d, st);
-    if (rr != LORA_OK) return rr;
-  }
-  const bool p2p = exchange && sh->p2p;
-  // row maps: my send-order rows for owner p; rows I receive from source p
-  PeerRows pr_in{}, pr_out{};
-  if (p2p) {
-    pr_in.G = pr_out.G = G;
-    for (int p = 0; p <= G; ++p) {
-      pr_in.off[p] = (int)ro[p];
-      pr_out.off[p] = (int)so[p];
-    }
-    std::vector<int64_t> rb_in(G), rb_out(G);
-    lora_shard_peer_rows(c64.data(), G, me, rb_in.data(), rb_out.data());
-    for (int p = 0; p < G; ++p) {
-      pr_in.rowbase[p] = (int)rb_in[p];
-      pr_in.base[p] = sh->peer_send[p];
-      pr_out.rowbase[p] = (int)rb_out[p];
-      pr_out.base[p] = sh->peer_d[p];
-    }
-  }
-
-  // 3. (comm stream) pack + dispatch, overlapped with the in-place apply
-  if (exchange) {
-    CKS(cudaStreamWaitEvent(cs, sh->ev[0], 0));
-    // P2P: pack straight into the registered send buffer the owners read from
-    int32_t* ids_dst = p2p ? static_cast<int32_t*>(sh->sendbuf) : d_ids_send;
-    if (n_send > 0) {
-      const int pi = prof_start(s, cs);
-      gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(adapter_ids),
-                                                            reinterpret_cast<uint32_t*>(ids_dst), d_send_idx,
-                                                            n_send);
-      if (expert_ids)
-        gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(expert_ids),
-                                                              reinterpret_cast<uint32_t*>(ids_dst + s->max_rows),
-                                                              d_send_idx, n_send);
-      else
-        CKS(cudaMemsetAsync(ids_dst + s->max_rows, 0, sizeof(int32_t) * n_send, cs));
-      for (size_t j = 0; j < xd.size(); ++j) {
-        const int chunks = x_hin[j] / 8;  // 16-byte chunks per bf16 row
-        gather_rows16_kernel<<<dim3((chunks + 255) / 256, std::min(n_send, 65535)), 256, 0, cs>>>(
-            static_cast<const uint4*>(xd[j]),
-            reinterpret_cast<uint4*>(p2p ? static_cast<char*>(sh->sendbuf) + p_xo[j] : base + o_xs[j]), d_send_idx,
-            n_send, chunks);
-      }
-      prof_stop(s, pi, kKShardGather, cs);
-      CKS(cudaGetLastError());
-    }
-    if (p2p) {
-      // every source's send buffer complete before any owner reads it
-      const lora_status_t br = ctl_barrier(s, cs);
-      if (br != LORA_OK) return br;
-    } else {
-      if (sh->host_ag) return fail(s, LORA_ERR_UNSUPPORTED, "host control plane needs the peer-to-peer transport");
-    CKN(api.GroupStart());
-    for (int p = 0; p < G; ++p) {
-      const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
-      if (ns) {
-        CKN(api.Send(d_ids_send + so[p], ns, ncclInt32, p, sh->comm, cs));
-        CKN(api.Send(d_ids_send + s->max_rows + so[p], ns, ncclInt32, p, sh->comm, cs));
-        for (size_t j = 0; j < xd.size(); ++j)
-          CKN(api.Send(base + o_xs[j] + so[p] * x_hin[j] * 2, ns * x_hin[j], ncclBfloat16, p, sh->comm, cs));
-      }
-      if (nr) {
-        CKN(api.Recv(d_ids_recv + ro[p], nr, ncclInt32, p, sh->comm, cs));
-        CKN(api.Recv(d_ids_recv + Rmax + ro[p], nr, ncclInt32, p, sh->comm, cs));
-        for (size_t j = 0; j < xd.size(); ++j)
-          CKN(api.Recv(base + o_xr[j] + ro[p] * x_hin[j] * 2, nr * x_hin[j], ncclBfloat16, p, sh->comm, cs));
-      }
-    }
-    CKN(api.GroupEnd());
-    }
-    // owner side, still on the communication stream: the received rows' ids
-    // (P2P: pulled from the sources' send buffers) and their plan -- built
-    // while the in-place apply runs on the caller's stream
-    if (p2p && n_recv > 0) {
-      pull_ids_kernel<<<grid_of(n_recv), 256, 0, cs>>>(pr_in, s->max_rows, d_ids_recv, Rmax, n_recv);
-      CKS(cudaGetLastError());
-    }
-    const lora_status_t pr = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, cs);
-    if (pr != LORA_OK) return pr;
-    CKS(cudaEventRecord(sh->ev[1], cs));
-  }
-
+  bool exchange = false;  // every rank sees the same matrix, so every rank takes the same branch
+  for (int64_t v : c64) exchange = exchange || v > 0;
   if (!exchange) {
     CKS(cudaEventRecord(sh->ev[3], st));
     return LORA_OK;
   }
 
-  // 5. received rows: owner-side plan + delta-mode apply
+  // 3. (comm stream) pack + grouped send/recv, overlapped with the in-place apply
+  CKS(cudaStreamWaitEvent(cs, sh->ev[0], 0));
+  if (n_send > 0) {
+    const int pg = prof_start(s, cs);
+    gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(adapter_ids),
+                                                          reinterpret_cast<uint32_t*>(d_ids_send), d_send_idx, n_send);
+    if (expert_ids)
+      gather_words_kernel<<<grid_of(n_send), 256, 0, cs>>>(reinterpret_cast<const uint32_t*>(expert_ids),
+                                                            reinterpret_cast<uint32_t*>(d_ids_send + s->max_rows),
+                                                            d_send_idx, n_send);
+    else
+      CKS(cudaMemsetAsync(d_ids_send + s->max_rows, 0, sizeof(int32_t) * n_send, cs));
+    for (size_t j = 0; j < xd.size(); ++j) {
+      const int chunks = x_hin[j] / 8;  // 16-byte chunks per bf16 row
+      gather_rows16_kernel<<<dim3((chunks + 255) / 256, std::min(n_send, 65535)), 256, 0, cs>>>(
+          static_cast<const uint4*>(xd[j]), reinterpret_cast<uint4*>(base + o_xs[j]), d_send_idx, n_send, chunks);
+    }
+    prof_stop(s, pg, kKShardGather, cs);
+    CKS(cudaGetLastError());
+  }
+  CKN(api.GroupStart());
+  for (int p = 0; p < G; ++p) {
+    const size_t ns = so[p + 1] - so[p], nr = ro[p + 1] - ro[p];
+    if (ns) {
+      CKN(api.Send(d_ids_send + so[p], ns, ncclInt32, p, sh->comm, cs));
+      CKN(api.Send(d_ids_send + s->max_rows + so[p], ns, ncclInt32, p, sh->comm, cs));
+      for (size_t j = 0; j < xd.size(); ++j)
+        CKN(api.Send(base + o_xs[j] + so[p] * x_hin[j] * 2, ns * x_hin[j], ncclBfloat16, p, sh->comm, cs));
+    }
+    if (nr) {
+      CKN(api.Recv(d_ids_recv + ro[p], nr, ncclInt32, p, sh->comm, cs));
+      CKN(api.Recv(d_ids_recv + Rmax + ro[p], nr, ncclInt32, p, sh->comm, cs));
+      for (size_t j = 0; j < xd.size(); ++j)
+        CKN(api.Recv(base + o_xr[j] + ro[p] * x_hin[j] * 2, nr * x_hin[j], ncclBfloat16, p, sh->comm, cs));
+    }
+  }
+  CKN(api.GroupEnd());
+  //    owner side, still on the communication stream: the received rows' plan
+  rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, cs);
+  if (rc != LORA_OK) return rc;
+  CKS(cudaEventRecord(sh->ev[1], cs));
+
+  // 4. received rows: delta-mode apply
   CKS(cudaStreamWaitEvent(st, sh->ev[1], 0));
   if (n_recv > 0) {
     std::vector<const void*> xs(n);
     std::vector<void*> ds(n);
-    std::vector<long long> xo(n);
-    RemoteIn rin{};
-    if (p2p) {
-      // the shrink kernels read each received x row from its source's send
-      // buffer over NVLink (the dispatch is fused into the shrink's loads)
-      rin.G = G;
-      for (int p = 0; p <= G; ++p) rin.ro[p] = pr_in.off[p];
-      for (int p = 0; p < G; ++p) {
-        rin.rowbase[p] = pr_in.rowbase[p];
-        rin.src[p] = sh->peer_send[p];
-      }
-    }
     for (int i = 0; i < n; ++i) {
-      xs[i] = p2p ? sh->sendbuf : base + o_xr[x_of[i]];
-      xo[i] = p2p ? (long long)p_xo[x_of[i]] : 0;
-      ds[i] = p2p ? static_cast<char*>(sh->dbuf) + p_doff[i] : base + o_d[i];
+      xs[i] = base + o_xr[x_of[i]];
+      ds[i] = base + o_d[i];
     }
-    rc = apply_multi_delta(s, sh->plan, n, slots, xs.data(), ds.data(), st, d_bf16, p2p ? &rin : nullptr,
-                           p2p ? xo.data() : nullptr);
+    rc = apply_multi_delta(s, sh->plan, n, slots, xs.data(), ds.data(), st, d_bf16);
     if (rc != LORA_OK) return rc;
   }
-  if (p2p) {
-    // every owner's deltas complete before any source reads them
-    const lora_status_t br = ctl_barrier(s, st);
-    if (br != LORA_OK) return br;
-    if (n_send > 0) {
-      for (int i = 0; i < n; ++i) {
-        const int ho = s->slots[slots[i]].h_out;
-        const int pi = prof_start(s, st);
-        pull_scatter_add4_kernel<<<dim3((ho / 4 + 255) / 256, std::min(n_send, 65535)), 256, 0, st>>>(
-            y[i], y_dtype == LORA_FP32, pr_out, (long long)p_doff[i], d_bf16 ? 1 : 0, d_send_idx, n_send, ho);
-        prof_stop(s, pi, kKShardScatter, st);
-      }
-      CKS(cudaGetLastError());
-    }
-    CKS(cudaEventRecord(sh->ev[3], st));
-    if (s->debug_sync) CKS(cudaStreamSynchronize(st));
-    return LORA_OK;
-  }
-
-  // 6. (comm stream) return the deltas
+  // 5. (comm stream) return the deltas
   CKS(cudaEventRecord(sh->ev[2], st));
   CKS(cudaStreamWaitEvent(cs, sh->ev[2], 0));
   const ncclDataType_t dt = d_bf16 ? ncclBfloat16 : ncclFloat32;
@@ -859,18 +1060,54 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   CKS(cudaEventRecord(sh->ev[3], cs));
   CKS(cudaStreamWaitEvent(st, sh->ev[3], 0));
 
-  // 7. add the returned deltas at the origin rows
+  // 6. add the returned deltas at the origin rows
   if (n_send > 0) {
     for (int i = 0; i < n; ++i) {
       const int ho = s->slots[slots[i]].h_out;
-      const int pi = prof_start(s, st);
+      const int ps = prof_start(s, st);
       scatter_add4_kernel<<<dim3((ho / 4 + 255) / 256, std::min(n_send, 65535)), 256, 0, st>>>(
           y[i], y_dtype == LORA_FP32, base + o_dr[i], d_bf16 ? 1 : 0, d_send_idx, n_send, ho);
-      prof_stop(s, pi, kKShardScatter, st);
+      prof_stop(s, ps, kKShardScatter, st);
     }
     CKS(cudaGetLastError());
   }
   CKS(cudaEventRecord(sh->ev[3], st));
   if (s->debug_sync) CKS(cudaStreamSynchronize(st));
   return LORA_OK;
+}
+
+extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const int32_t* slots, const void* const* x,
+                                            const int32_t* adapter_ids, const int32_t* expert_ids, void* const* y,
+                                            lora_dtype_t y_dtype, int32_t T, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (!s->shard) return fail(s, LORA_ERR_INVALID_ARG, "not a sharded server");
+  if (n < 1 || !slots || !x || !y || (T > 0 && !adapter_ids)) return fail(s, LORA_ERR_INVALID_ARG, "NULL argument");
+  if (T < 0 || T > s->max_rows) return fail(s, LORA_ERR_INVALID_ARG, "T must be in [0, max_rows]");
+  if (y_dtype != LORA_BF16 && y_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "y_dtype");
+  if (n > kMaxTasks) return fail(s, LORA_ERR_UNSUPPORTED, "at most 128 slots per sharded apply");
+  for (int i = 0; i < n; ++i)
+    if (slots[i] < 0 || slots[i] >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
+  const int E = s->slots[slots[0]].E;
+  for (int i = 0; i < n; ++i)
+    if (s->slots[slots[i]].E != E) return fail(s, LORA_ERR_INVALID_ARG, "slots of one call must share n_experts");
+  ShardState* sh = s->shard;
+  CKS(cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // registered buffers -> the push path (x and y must lie inside their
+  // registered buffers for T rows)
+  std::vector<int> xk(n, -1), yk(n, -1);
+  bool all_reg = sh->ctl != nullptr;
+  for (int i = 0; i < n && all_reg; ++i) {
+    xk[i] = reg_index(sh, x[i]);
+    yk[i] = reg_index(sh, y[i]);
+    const SlotInfo& si = s->slots[slots[i]];
+    const size_t ysz = y_dtype == LORA_FP32 ? 4 : 2;
+    all_reg = xk[i] >= 0 && yk[i] >= 0 && sh->reg[xk[i]].bytes >= (size_t)T * si.h_in * 2 &&
+              sh->reg[yk[i]].bytes >= (size_t)T * si.h_out * ysz;
+  }
+  if (all_reg) return apply_sharded_push(s, n, slots, x, adapter_ids, expert_ids, y, y_dtype, T, st, xk, yk);
+  if (sh->host_ag)
+    return fail(s, LORA_ERR_INVALID_ARG, "host control plane: x and y must be registered (lora_shard_register)");
+  if (!sh->comm) return fail(s, LORA_ERR_NCCL, "no NCCL communicator");
+  return apply_sharded_nccl(s, n, slots, x, adapter_ids, expert_ids, y, y_dtype, T, st);
 }

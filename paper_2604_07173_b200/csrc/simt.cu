@@ -515,12 +515,17 @@ struct ExpandPos {
   void* y;
   const int32_t* perm_rows;
   float s_a;
+  char* prow[kGroupRows];  // push modes: the origin row of each group row in its source's y
 };
 
 // y[row][c] for one (row, column) result d (already scaled).  Output mode M
 // (compile time): 0 bf16 accumulate with the old value from the stage's smem
 // y tile, 1 fp32 store and 2 bf16 store (sharded delta), 3 fp32 accumulate.
-enum { kOutBf16Acc = 0, kOutF32Store = 1, kOutBf16Store = 2, kOutF32Acc = 3 };
+// 4 / 5: push -- bf16 / fp32 delta added into the origin row of the source's
+// registered y (red.add over NVLink, sharded owner; p.prow).
+enum { kOutBf16Acc = 0, kOutF32Store = 1, kOutBf16Store = 2, kOutF32Acc = 3, kOutBf16Push = 4, kOutF32Push = 5 };
+constexpr bool out_push(int m) { return m == kOutBf16Push || m == kOutF32Push; }
+constexpr bool out_bf16_tile(int m) { return m == kOutBf16Acc || m == kOutBf16Store || m == kOutBf16Push; }
 template <int M, bool TILE>
 LORA_DEVINL void expand_out(const ExpandPos& p, uint32_t rows, int r, int col, float d, uint32_t ytile, int pitch) {
   if constexpr (TILE) {
@@ -535,6 +540,10 @@ LORA_DEVINL void expand_out(const ExpandPos& p, uint32_t rows, int r, int col, f
       v = f32_to_bf16_rne(d);
     }
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+    return;
+  }
+  if constexpr (M == kOutF32Push) {
+    red_add_f32(p.prow[r] + (p.c0 + col) * 4, d);
     return;
   }
   int row;
@@ -578,6 +587,16 @@ LORA_DEVINL void expand_stage1(uint32_t b_s, uint32_t v_s, int cr, const ExpandP
       acc[r][ch & 1] = a;
     }
   }
+  if constexpr (M == kOutBf16Push) {
+    // column pairs (cr, cr + 1) meet in the even lane: one 4-byte red per pair
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const float d = p.s_a * ((acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y));
+      const float dn = __shfl_xor_sync(0xffffffffu, d, 1);
+      if (!(cr & 1) && cr < p.sc) red_add_bf16x2(p.prow[r] + (p.c0 + cr) * 2, pack_bf16x2_rn(d, dn));
+    }
+    return;
+  }
   if (cr >= p.sc) return;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
@@ -593,7 +612,7 @@ template <int R, int NR, int CPT, int NCT, int M>
 LORA_DEVINL void expand_stage_pairs(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
                                     uint32_t ytile, int pitch) {
   constexpr int NP = CPT / 2;
-  constexpr bool TILE = M == kOutBf16Acc || M == kOutBf16Store;
+  constexpr bool TILE = out_bf16_tile(M);
   float2 acc[NP][NR];
 #pragma unroll
   for (int q = 0; q < NP; ++q)
@@ -1029,7 +1048,7 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
                                                            const ExpandRec* recs) {
   using C = SimtCfg<R>;
   // CPT == 1 (r = 64): results go to y straight from registers (expand_stage1)
-  constexpr bool TILE = C::CPT > 1 && (M == kOutBf16Acc || M == kOutBf16Store);
+  constexpr bool TILE = C::CPT > 1 && out_bf16_tile(M);
   constexpr int pitch = C::SC_MAX * 2;
   const int lane = lane_id();
   const int ct = threadIdx.x;
@@ -1053,6 +1072,11 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
     p.h_out = t.h_out;
     p.y = t.y;
     p.s_a = rc.s_a;
+    if constexpr (out_push(M)) {
+#pragma unroll
+      for (int r = 0; r < C::GR; ++r)
+        p.prow[r] = r < nr ? y_push_row(args, rc.task, rc.rows[r], M == kOutF32Push ? 4 : 2) : nullptr;
+    }
     const uint32_t rows = smem_u32(rc.rows);
     const int n_st = t.CI / t.SC;
     for (int st = 0; st < n_st; ++st) {
@@ -1078,7 +1102,10 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
           uint16_t* yb = static_cast<uint16_t*>(p.y) + p.c0 + sch * 8;
           for (int r = rsub; r < nr; r += RSTEP) {
             const uint4 v = lds128(yt + r * pitch + sch * 16);
-            *reinterpret_cast<uint4*>(yb + (long long)rc.rows[r] * p.h_out) = v;
+            if constexpr (M == kOutBf16Push)
+              red_add_bf16x8(p.prow[r] + (p.c0 + sch * 8) * 2, v);  // r < nr: prow set
+            else
+              *reinterpret_cast<uint4*>(yb + (long long)rc.rows[r] * p.h_out) = v;
           }
         }
         fence_proxy_async_smem();  // the tile is refilled by bulk copies after the release
@@ -1197,7 +1224,13 @@ __global__ void __launch_bounds__(SimtCfg<R>::TILE_THREADS, 2)
       }
     }
   } else {
-    if (args.y_store == 1)
+    if (args.y_store == 3) {
+      if (args.y_fp32)
+        simt_expand_tile_consumers<R, kOutF32Push>(args, smem, full, empty, wq, recs);
+      else
+        simt_expand_tile_consumers<R, kOutBf16Push>(args, smem, full, empty, wq, recs);
+      __threadfence_system();  // this thread's pushes performed before the owner signals completion
+    } else if (args.y_store == 1)
       simt_expand_tile_consumers<R, kOutF32Store>(args, smem, full, empty, wq, recs);
     else if (args.y_store == 2)
       simt_expand_tile_consumers<R, kOutBf16Store>(args, smem, full, empty, wq, recs);
@@ -1226,7 +1259,7 @@ template <int R>
 cudaError_t launch_shrink_t(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   using C = SimtCfg<R>;
   static unsigned long long mask[2] = {0, 0};
-  const bool remote = args.rin.G > 0;
+  const bool remote = args.push.G > 0;
   auto kern = remote ? simt_shrink_kernel<R, true> : simt_shrink_kernel<R, false>;
   cudaError_t e = set_smem_once(kern, C::SHRINK_SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
@@ -1248,7 +1281,7 @@ template <int R>
 cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   using C = SimtCfg<R>;
   if constexpr (R <= LORA_TILE_MAX_R) {
-    if (!C::LOOKAHEAD_OK || use_tile_expand(R)) {
+    if (!C::LOOKAHEAD_OK || use_tile_expand(R) || args.y_store == 3) {  // (push: staged-tile kernel only)
       static unsigned long long tmask = 0;
       cudaError_t e = set_smem_once(simt_expand_tile_kernel<R>, C::TILE_SMEM, tmask);
       if (e != cudaSuccess) return e;

@@ -546,7 +546,9 @@ struct ExpandCfg {
 };
 
 // output mode M (compile time): 0 bf16 accumulate, 1 fp32 delta store, 2 bf16
-// delta store (sharded), 3 fp32 accumulate
+// delta store (sharded), 3 fp32 accumulate, 4 / 5 bf16 / fp32 push (sharded
+// owner: the delta is added into the origin row of the source's registered y
+// with red.add over NVLink)
 template <int M>
 __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     tc_expand_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
@@ -681,7 +683,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       }
     }
   } else {
-    if constexpr (M == 0 || M == 2) {
+    if constexpr (M == 0 || M == 2 || M == 4) {
     // ===================== epilogue, bf16 output: coalesced y tiles =====================
     // Per sub-tile the 128 x 128 y tile is fetched with coalesced cp.async
     // (16 chunks of 16 bytes per row; YD-1 sub-tiles ahead) into a smem ring;
@@ -701,7 +703,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const long long it = wq_pop(wq, qp);
       if (it < 0) break;
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
-      const SlotTask& t = args.t[find_task_ci(args, cig)];
+      const int task = find_task_ci(args, cig);
+      const SlotTask& t = args.t[task];
       const int ci = cig - t.ci_base;
       const int4 tile = pd.tiles[ti];
       const float s_a = args.scale[tile.z / t.E];
@@ -710,11 +713,16 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       // this thread's copy rows: r_j = et / 16 + 32 j
       long long coff[4];
       bool cval[4];
+      uint16_t* ppush[4];  // push: the origin rows in the sources' y (+ this thread's chunk column)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int r = (et >> 4) + 32 * j;
         cval[j] = r < tile.y;
-        coff[j] = (cval[j] ? (long long)__ldg(pd.perm + tile.x + r) * t.h_out : 0) + (long long)ci * t.CI + cc * 8;
+        const int prow = cval[j] ? __ldg(pd.perm + tile.x + r) : 0;
+        coff[j] = (long long)prow * t.h_out + (long long)ci * t.CI + cc * 8;
+        if constexpr (M == 4)
+          ppush[j] = cval[j] ? reinterpret_cast<uint16_t*>(y_push_row(args, task, prow, 2)) + (long long)ci * t.CI + cc * 8
+                             : nullptr;
       }
       auto slot_of = [&](int seq) { return ybase + (uint32_t)(seq % C::YS) * C::Y_TILE; };
       auto chunk_addr = [&](uint32_t sl, int r, int c) { return sl + r * (C::MSUB * 2) + ((c ^ (r & 15)) << 4); };
@@ -762,13 +770,18 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         named_bar_sync(1, C::EPI_THREADS);  // results in the tile
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (cval[j])
-            *reinterpret_cast<uint4*>(yb + coff[j] + (long long)sb * C::MSUB) =
-                lds128(chunk_addr(sl, (et >> 4) + 32 * j, cc));
+          if (cval[j]) {
+            const uint4 v = lds128(chunk_addr(sl, (et >> 4) + 32 * j, cc));
+            if constexpr (M == 4)
+              red_add_bf16x8(ppush[j] + (long long)sb * C::MSUB, v);
+            else
+              *reinterpret_cast<uint4*>(yb + coff[j] + (long long)sb * C::MSUB) = v;
+          }
       }
       cp_async_wait<0>();
       kk += n_sub;
     }
+    if constexpr (M == 4) __threadfence_system();  // pushes performed before the owner signals completion
     } else {
     // ===================== epilogue: one row x 32 columns per thread =====================
     // y moves in full 32-byte sectors (256-bit LDG/STG); the segments of the
@@ -783,7 +796,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const long long it = wq_pop(wq, qp);
       if (it < 0) break;
       const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
-      const SlotTask& t = args.t[find_task_ci(args, cig)];
+      const int task = find_task_ci(args, cig);
+      const SlotTask& t = args.t[task];
       const int ci = cig - t.ci_base;
       const int4 tile = pd.tiles[ti];
       const float s_a = args.scale[tile.z / t.E];
@@ -793,6 +807,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
       const long long prow = live ? (long long)__ldg(pd.perm + tile.x + n) : 0;
       const long long o0 = prow * t.h_out + (long long)ci * t.CI + cb * 32;  // + sb * MSUB
       uint16_t* yb = static_cast<uint16_t*>(t.y);
+      // push (M = 5): this row's columns in the origin row of the source's y
+      float* ypush = nullptr;
+      if constexpr (M == 5)
+        if (live) ypush = reinterpret_cast<float*>(y_push_row(args, task, (int)prow, 4)) + (long long)ci * t.CI + cb * 32;
       // three segment buffers with compile-time roles (a register rotation
       // would wait for the newest load): step sb consumes buf[sb % 3] and
       // starts the load of sub-tile sb + 2 into buf[(sb + 2) % 3]
@@ -827,7 +845,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           if (live) stg256x2(yb + o, w);
         } else {
           // fp32 y (accumulate) or fp32 delta store (sharded): 2 halves x 4 x 16 bytes
-          float4* yp = reinterpret_cast<float4*>(static_cast<float*>(t.y) + o);
+          float4* yp = M == 5 ? reinterpret_cast<float4*>(ypush + (long long)sb * C::MSUB)
+                              : reinterpret_cast<float4*>(static_cast<float*>(t.y) + o);
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
             uint32_t d[16];
@@ -840,6 +859,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
                                              s_a * __uint_as_float(d[4 * i + 2]), s_a * __uint_as_float(d[4 * i + 3]));
                 if constexpr (M == 1) {
                   yp[h * 4 + i] = e;
+                } else if constexpr (M == 5) {
+                  red_add_f32x4(yp + h * 4 + i, e);
                 } else {
                   float4 v = yp[h * 4 + i];
                   v.x += e.x; v.y += e.y; v.z += e.z; v.w += e.w;
@@ -863,6 +884,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         step(sb + 2, b2, b1);
       }
     }
+    if constexpr (M == 5) __threadfence_system();  // pushes performed before the owner signals completion
     }
   }
   tc_fence_before();
@@ -912,7 +934,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 static void make_x_maps(const MultiArgs& args, int x_rows, TcMaps& m) {
   std::memset(&m, 0, sizeof(m));
   const char* env = getenv("LORA_TC_GATHER4");
-  if (!(env && env[0] == '1') || args.rin.G > 0 || args.n_tasks > kTcMapTasks || x_rows < 1) return;
+  if (!(env && env[0] == '1') || args.push.G > 0 || args.n_tasks > kTcMapTasks || x_rows < 1) return;
   auto enc = tensor_map_encoder();
   if (!enc) return;
   for (int i = 0; i < args.n_tasks; ++i) {
@@ -931,7 +953,7 @@ static void make_x_maps(const MultiArgs& args, int x_rows, TcMaps& m) {
 
 cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid, cudaStream_t stream) {
   static unsigned long long mask[2] = {0, 0};
-  const bool remote = args.rin.G > 0;
+  const bool remote = args.push.G > 0;
   auto kern = remote ? tc_shrink_kernel<true> : tc_shrink_kernel<false>;
   cudaError_t e = set_smem_once(kern, ShrinkCfg::SMEM, mask[remote]);
   if (e != cudaSuccess) return e;
@@ -949,10 +971,15 @@ cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid
 }
 
 cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
-  static unsigned long long mask[4] = {0, 0, 0, 0};
-  const int m = args.y_store == 1 ? 1 : args.y_store == 2 ? 2 : args.y_fp32 ? 3 : 0;
-  auto kern = m == 0 ? tc_expand_kernel<0> : m == 1 ? tc_expand_kernel<1> : m == 2 ? tc_expand_kernel<2>
-                                                                                     : tc_expand_kernel<3>;
+  static unsigned long long mask[6] = {0, 0, 0, 0, 0, 0};
+  const int m = args.y_store == 3 ? (args.y_fp32 ? 5 : 4)
+                                  : args.y_store == 1 ? 1 : args.y_store == 2 ? 2 : args.y_fp32 ? 3 : 0;
+  auto kern = m == 0   ? tc_expand_kernel<0>
+              : m == 1 ? tc_expand_kernel<1>
+              : m == 2 ? tc_expand_kernel<2>
+              : m == 3 ? tc_expand_kernel<3>
+              : m == 4 ? tc_expand_kernel<4>
+                       : tc_expand_kernel<5>;
   cudaError_t e = set_smem_once(kern, ExpandCfg::SMEM, mask[m]);
   if (e != cudaSuccess) return e;
   e = launch_pdl(kern, dim3(grid), dim3(ExpandCfg::THREADS), ExpandCfg::SMEM, stream, args, pd);

@@ -48,6 +48,11 @@ def y0_dev(B, cfg: li.Config, slot_index: int, T: int, kind: str = "random", fp3
     return y
 
 
+def register(B, sh, bufs):
+    """Register device buffers (x / y) of a sharded server for the push path."""
+    B.lora_shard_register(sh, bufs, [t.numel() * t.element_size() for t in bufs])
+
+
 def ids_dev(batch: li.Batch):
     return (torch.from_numpy(batch.adapter_ids).to(DEV), torch.from_numpy(batch.expert_ids).to(DEV))
 

@@ -1,11 +1,12 @@
-"""The sharded server's peer-to-peer data path with two real ranks on ONE GPU.
+"""The sharded server's push path with two real ranks on ONE GPU.
 
 Two processes, each a rank of a world-2 sharded server on cuda:0, with the
 host control plane (lora_server_create_sharded_host over a gloo all-gather):
-each rank registers its send / delta buffers and maps the other process's
-through CUDA IPC; the owner's shrink kernels read the received x rows from
-the other process's send buffer, each source pulls its deltas from the
-owner's buffer fused with the add.  Checked: fp32 y bit-identical to the
+each rank registers its x / y buffers (lora_shard_register: CUDA IPC, mapped
+by the other process); the counts travel through the control areas (device
+flags), the owner's shrink kernels read the received x rows from the other
+process's x, and the owner's expand epilogue adds the deltas into the other
+process's y (red.add).  Checked: fp32 y bit-identical to the
 unsharded server on every row when every segment takes the CUDA-core route
 (R18; a tcgen05 segment rounds v to bf16, and a unit's rows can be
 split between the local and the received plan), every case within the
@@ -80,8 +81,13 @@ def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep):
         ad = torch.from_numpy(b.adapter_ids[r0:r1].copy()).cuda()
         ex = torch.from_numpy(b.expert_ids[r0:r1].copy()).cuda()
         dt = B.LORA_FP32 if y_dtype == "fp32" else B.LORA_BF16
-        for _ in range(2):  # the second call reuses the registered buffers
-            yy = [y.clone() for y in ys]
+        yy = [y.clone() for y in ys]
+        B.lora_shard_register(s, xs + yy, [t.numel() * t.element_size() for t in xs + yy])
+        for _ in range(3):  # later calls reuse the registrations; the epoch advances
+            for v, v0 in zip(yy, ys):
+                v.copy_(v0)
+            torch.cuda.synchronize()
+            dist.barrier()  # (no rank may overwrite its y while a peer still pushes into it)
             B.lora_apply_sharded(s, [0, 1], xs, ad, ex, yy, dt, T)
             torch.cuda.synchronize()
         assert B.lora_server_check(s) == B.LORA_OK

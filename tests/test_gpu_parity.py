@@ -324,12 +324,12 @@ def test_mixtral_sharded_config_at_g1_sampled(B):
 
 
 @pytest.mark.slow
-def test_mixtral_sharded_config_p2p_loopback_sampled(B, monkeypatch):
-    """Config 5 at full size through the sharded server's peer-to-peer path
-    (loopback: every row goes through the registered send buffer, the owner's
-    shrink reads it remotely, the deltas come back through the pull-scatter)."""
+def test_mixtral_sharded_config_push_loopback_sampled(B, monkeypatch):
+    """Config 5 at full size through the sharded server's push path
+    (loopback: every row goes through bucket / announce / recv-prep, the
+    owner's shrink reads x rows through the registered mapping, the expand
+    epilogue red.adds the deltas into the registered y)."""
     monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
-    monkeypatch.setenv("LORA_SHARD_TRANSPORT", "p2p")
     cfg = li.CONFIGS["mixtral_sharded"]
     b = li.make_batch(cfg)
     T = b.n_rows
@@ -344,13 +344,14 @@ def test_mixtral_sharded_config_p2p_loopback_sampled(B, monkeypatch):
             if sl.xbuf not in xs:
                 xs[sl.xbuf] = U.x_dev(B, cfg, i, T)
         ys = [U.y0_dev(B, cfg, i, T) for i in range(3)]
+        U.register(B, sh, list(xs.values()) + ys)
         B.lora_apply_sharded(sh, [0, 1, 2], [xs[sl.xbuf] for sl in cfg.slots], ad, ex, ys, B.LORA_BF16, T)
         torch.cuda.synchronize()
         assert B.lora_server_check(sh) == B.LORA_OK
         rows = U.sample_rows(b, 24, E=cfg.n_experts)
         for i in range(3):
             ref = oracle.apply_slot(cfg, i, b, rows=rows)
-            U.assert_parity(ys[i][torch.from_numpy(rows).to(U.DEV)], ref, f"p2p loopback slot {i}")
+            U.assert_parity(ys[i][torch.from_numpy(rows).to(U.DEV)], ref, f"push loopback slot {i}")
     finally:
         B.lora_server_destroy(sh)
 
@@ -628,22 +629,22 @@ def test_small_rank_bf16_full_parity(B, rank):
 
 
 @pytest.mark.parametrize("loopback,y_dtype,rank,transport", [
-    (False, "bf16", 64, "p2p"), (True, "fp32", 64, "p2p"), (True, "bf16", 64, "p2p"), (True, "bf16", 16, "p2p"),
-    (True, "fp32", 16, "p2p"), (True, "fp32", 8, "nccl"),
+    (False, "bf16", 64, "push"), (True, "fp32", 64, "push"), (True, "bf16", 64, "push"), (True, "bf16", 16, "push"),
+    (True, "fp32", 16, "push"), (True, "fp32", 8, "nccl"),
     (True, "fp32", 64, "nccl"), (True, "bf16", 64, "nccl")])
 def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
     """Sharded server at G = 1.  In place (no exchange): bit-identical to the
     unsharded server.  Loopback (LORA_SHARD_LOOPBACK=1 sends every row through
-    the exchange to itself, so one GPU runs the bucket / pack / transport /
-    owner delta apply / return / scatter-add path) with either transport:
-    p2p (registered buffers; the owner's shrink reads x rows from the source's
-    send buffer, the source pulls deltas fused with the add) or nccl (grouped
-    send/recv).  fp32 y: bit-identical to the unsharded server (R18); bf16 y
-    returns bf16 deltas (R19) and is held to the oracle tolerance, every row."""
+    the exchange to itself, so one GPU runs the whole sharded path) with
+    either path: push (x / y registered: device-side counts, the owner's
+    shrink reads x rows through the registered mapping, the expand epilogue
+    red.adds the deltas into the registered y) or nccl (unregistered: grouped
+    send/recv + scatter-add).  fp32 y: bit-identical to the unsharded server
+    (R18); bf16 y returns bf16 deltas (R19) and is held to the oracle
+    tolerance, every row.  Three calls: buffers and the epoch are reused."""
     cfg = dataclasses.replace(_mid_cfg(rank=rank), y_dtype=y_dtype)
     if loopback:
         monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
-    monkeypatch.setenv("LORA_SHARD_TRANSPORT", transport)
     b = li.make_batch(cfg)
     s = U.make_server(B, cfg)
     T = b.n_rows
@@ -656,9 +657,14 @@ def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
         y_ref = _run_multi(B, s, cfg, b, [0, 1])
         ad, ex = U.ids_dev(b)
         xs = [U.x_dev(B, cfg, i, T) for i in range(2)]
+        y0 = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        ys = [v.clone() for v in y0]
+        if transport == "push":
+            U.register(B, sh, xs + ys)
         dt = B.LORA_FP32 if y_dtype == "fp32" else B.LORA_BF16
-        for rep in range(2):  # second call reuses the grown scratch and the comm stream
-            ys = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        for rep in range(3):
+            for v, v0 in zip(ys, y0):
+                v.copy_(v0)
             B.lora_apply_sharded(sh, [0, 1], xs, ad, ex, ys, dt, T)
             torch.cuda.synchronize()
             assert B.lora_server_check(sh) == B.LORA_OK
@@ -667,6 +673,50 @@ def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
                     U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"loopback bf16 slot {i}")
                 else:
                     assert torch.equal(ys[i], y_ref[i]), f"slot {i} rep {rep}"
+    finally:
+        B.lora_server_destroy(sh)
+        B.lora_server_destroy(s)
+
+
+def test_sharded_push_graph_capture(B, monkeypatch):
+    """The push path has no host synchronisation: a sharded step captured in a
+    CUDA graph and replayed (the epoch advances in device memory) gives the
+    eager result bit for bit, replay after replay."""
+    monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
+    cfg = dataclasses.replace(_mid_cfg(rank=64), y_dtype="fp32")
+    b = li.make_batch(cfg)
+    T = b.n_rows
+    c = B.make_config([sl.h_in for sl in cfg.slots], [sl.h_out for sl in cfg.slots],
+                      [sl.n_experts for sl in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), T, 0)
+    sh = B.lora_server_create_sharded(c, 0, 1, B.lora_nccl_unique_id())
+    s = U.make_server(B, cfg)
+    try:
+        B.lora_server_fill_synthetic(sh, cfg.seed)
+        y_ref = _run_multi(B, s, cfg, b, [0, 1])
+        ad, ex = U.ids_dev(b)
+        xs = [U.x_dev(B, cfg, i, T) for i in range(2)]
+        y0 = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        ys = [v.clone() for v in y0]
+        U.register(B, sh, xs + ys)
+        g_stream = torch.cuda.Stream()
+        g_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(g_stream):
+            B.lora_apply_sharded(sh, [0, 1], xs, ad, ex, ys, B.LORA_FP32, T, g_stream)  # warm-up (eager)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=g_stream):
+                B.lora_apply_sharded(sh, [0, 1], xs, ad, ex, ys, B.LORA_FP32, T, g_stream)
+        torch.cuda.current_stream().wait_stream(g_stream)
+        torch.cuda.synchronize()
+        for rep in range(3):
+            for v, v0 in zip(ys, y0):
+                v.copy_(v0)
+            torch.cuda.synchronize()
+            graph.replay()
+            torch.cuda.synchronize()
+            assert B.lora_server_check(sh) == B.LORA_OK
+            for i in range(2):
+                assert torch.equal(ys[i], y_ref[i]), f"replay {rep} slot {i}"
     finally:
         B.lora_server_destroy(sh)
         B.lora_server_destroy(s)

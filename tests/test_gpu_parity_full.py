@@ -86,12 +86,11 @@ def test_full_config_every_row(B, name):
         B.lora_server_destroy(s)
 
 
-def test_config5_p2p_loopback_every_row(B, monkeypatch):
-    """Config 5 through the sharded server's exchange path at full size
-    (loopback: every row through the registered send buffer, the owner's
-    remote-x shrink and the return), every row against the oracle."""
+def test_config5_push_loopback_every_row(B, monkeypatch):
+    """Config 5 through the sharded server's push path at full size
+    (loopback: every row through bucket / announce / recv-prep, the owner's
+    remote-x shrink and the push-add expand), every row against the oracle."""
     monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
-    monkeypatch.setenv("LORA_SHARD_TRANSPORT", "p2p")
     cfg = li.CONFIGS["mixtral_sharded"]
     b = li.make_batch(cfg)
     T = b.n_rows
@@ -105,8 +104,11 @@ def test_config5_p2p_loopback_every_row(B, monkeypatch):
         for i, sl in enumerate(cfg.slots):
             if sl.xbuf not in xs:
                 xs[sl.xbuf] = U.x_dev(B, cfg, i, T)
+        ys = [U.y0_dev(B, cfg, i, T) for i in range(3)]
+        U.register(B, sh, list(xs.values()) + ys)
         for y0 in ("random", "zero"):
-            ys = [U.y0_dev(B, cfg, i, T, y0) for i in range(3)]
+            for i in range(3):
+                ys[i].copy_(U.y0_dev(B, cfg, i, T, y0))
             B.lora_apply_sharded(sh, [0, 1, 2], [xs[sl.xbuf] for sl in cfg.slots], ad, ex, ys, B.LORA_BF16, T)
             torch.cuda.synchronize()
             assert B.lora_server_check(sh) == B.LORA_OK
@@ -291,13 +293,12 @@ def _mid_cfg(rank=64, T=600, y_dtype="bf16"):
                      T // 2, y_dtype)
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["push", "nccl"])
 def test_sharded_bad_expert_id_on_routed_row(B, monkeypatch, transport):
     """A routed row (loopback: every row is routed) with a valid adapter and an
     out-of-range expert id is flagged and dropped: its y row is unchanged, the
     other rows match the unsharded server, lora_server_check reports it."""
     monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
-    monkeypatch.setenv("LORA_SHARD_TRANSPORT", transport)
     cfg = _mid_cfg(y_dtype="fp32")
     b = li.make_batch(cfg)
     T = b.n_rows
@@ -318,8 +319,12 @@ def test_sharded_bad_expert_id_on_routed_row(B, monkeypatch, transport):
         ad = torch.from_numpy(b.adapter_ids).to(U.DEV)
         ex = torch.from_numpy(ex_bad).to(U.DEV)
         xs = [U.x_dev(B, cfg, i, T) for i in range(2)]
+        ys = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        if transport == "push":
+            U.register(B, sh, xs + ys)
         for rep in range(2):   # the second call must not see a stale delta either
-            ys = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+            for i in range(2):
+                ys[i].copy_(U.y0_dev(B, cfg, i, T))
             B.lora_apply_sharded(sh, [0, 1], xs, ad, ex, ys, B.LORA_FP32, T)
             torch.cuda.synchronize()
             assert B.lora_server_check(sh) == B.LORA_ERR_ID_OUT_OF_RANGE
