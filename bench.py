@@ -17,6 +17,7 @@ Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import os
 import subprocess
@@ -536,10 +537,15 @@ def run_sharded(args, cfg, batch, slots):
 
     # popularity-aware placement (R19): replicate the hottest adapters
     # on every rank; auto = the host cost model's choice
-    ub, rb, xb = PL.slot_bytes([cfg.slots[i].h_in for i in slots], [cfg.slots[i].h_out for i in slots],
-                               [cfg.slots[i].xbuf for i in slots], cfg.rank, ysz, ysz)
+    hs, ho, xbf = ([cfg.slots[i].h_in for i in slots], [cfg.slots[i].h_out for i in slots],
+                   [cfg.slots[i].xbuf for i in slots])
+    ub, rb, xb = PL.slot_bytes(hs, ho, xbf, cfg.rank, ysz, ysz)
+    _, _, xpb, dpb = PL.slot_bytes_push(hs, ho, xbf, cfg.rank, ysz, ysz)
     src = PL.sources_of_rows(cfg.n_tokens, k, world)
-    ch = PL.choose_placement(batch.adapter_ids, batch.expert_ids if E > 1 else None, src, world, ub, rb, xb)
+    # cost model of the path that will run (push when x / y get registered)
+    push_kw = {} if args.no_register else {"x_bytes": xpb, "d_bytes": dpb}
+    ch = PL.choose_placement(batch.adapter_ids, batch.expert_ids if E > 1 else None, src, world, ub, rb, xb,
+                             **push_kw)
     n_rep = ch["n_replicated"] if args.n_replicated < 0 else args.n_replicated
     ep_mode = ch["expert_parallel"] if args.n_replicated < 0 else False
     rep_table = {str(h): round(v * 1e3, 4) for h, v in ch["table"].items()}
@@ -633,6 +639,18 @@ def run_sharded(args, cfg, batch, slots):
 
     ms = max_over_ranks(ms_local)
     value = cfg.n_tokens / (ms / 1e3)
+    # per-kernel durations on this rank (kernels serialised, eager launches)
+    n_prof = 5
+    B.lora_server_set_concurrent(s, False)
+    B.lora_profile_enable(s, n_prof * 48 + 16)
+    for _ in range(n_prof):
+        step()
+    torch.cuda.synchronize()
+    prof = B.lora_profile_read(s)
+    B.lora_profile_enable(s, 0)
+    B.lora_server_set_concurrent(s, True)
+    if world > 1:
+        dist.barrier()
 
     e2e = None
     if args.e2e_steps > 0:
@@ -702,10 +720,14 @@ def run_sharded(args, cfg, batch, slots):
                                if registered else "unregistered: NCCL send/recv transport",
                        "cuda_graph": graph is not None, "n_replicated": n_rep, "expert_parallel": ep_mode,
                        "placement_model_ms": rep_table,
+                       "hybrid_layouts_model_ms": {k_: round(v_ * 1e3, 4) for k_, v_ in PL.hybrid_table(
+                           batch.adapter_ids, batch.expert_ids, src, world, ub, rb, xpb, dpb).items()}
+                       if E > 1 and world > 1 else None,
                        "l2": "inputs larger than L2"},
             "e2e": e2e,
-            "gpu_launches": None,
+            "gpu_launches": int(round(sum(n_ for n_, _ in prof.values()) / n_prof * args.steps)),
             "roofline": roofline,
+            "kernels_rank0": {k_: {"launches": n_, "ms_per_step": t_ / n_prof} for k_, (n_, t_) in prof.items()},
             "device_errors": int(ok),
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
@@ -729,6 +751,7 @@ def relaunch_under_torchrun(n: int) -> int:
 
 
 def main():
+    faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)

@@ -85,6 +85,12 @@ typedef struct {
                                 layout, n_resident of them in device memory; lora_server_require
                                 makes a batch's adapters resident (LRU eviction, per-slot async
                                 host->device copies that the applies of each slot wait for). */
+  int32_t pp_stages;         /* sharded servers with expert_parallel: y pipeline stages of hybrid
+                                EP_x-PP_y: the world is y groups of x = world / y ranks,
+                                layer l belongs to group l mod y (interleaved), unit (a, e) of a
+                                layer-l slot is owned by rank (l mod y) * x + e mod x.  0 or 1 =
+                                pure expert parallel.  world % y == 0. */
+  const int32_t *slot_layer; /* [n_slots] layer index of each slot (hybrid placement); NULL = 0 */
 } lora_config_t;
 
 /* ------------------------------------------------------------------------- */

@@ -228,19 +228,22 @@ def token_range(n_tokens: int, world: int, rank: int) -> Tuple[int, int]:
 
 
 def owner_of(adapter_ids: np.ndarray, world: int, n_hot: int = 0, src=None, expert_ids=None,
-             ep: bool = False) -> np.ndarray:
+             ep: bool = False, pp: int = 1, layer: int = 0) -> np.ndarray:
     """Rank that processes each row (R19).
 
     LoRA Data Parallel stripes the adapters over the G server
     GPUs; adapters [0, n_hot) -- the most popular ones, P:291 -- are
     replicated on every rank, so their rows are processed by the rank that
     holds them (``src``).  Otherwise owner(a) = (a - n_hot) mod G.  Expert
-    parallel (``ep``): owner = e mod G.  Rows with a = -1 stay at
-    their origin (owner -1)."""
+    parallel (``ep``): owner = e mod G.  Hybrid EP_x-PP_y
+    (``ep`` with ``pp`` = y > 1): y groups of x = G / y ranks,
+    layers interleaved over the groups (layer l -> group l mod y), owner =
+    (l mod y) * x + e mod x.  Rows with a = -1 stay at their origin (owner -1)."""
     a = np.asarray(adapter_ids, dtype=np.int64)
     if ep:
         e = np.zeros_like(a) if expert_ids is None else np.asarray(expert_ids, dtype=np.int64)
-        return np.where(a >= 0, e % world, -1)
+        x = world // max(pp, 1)
+        return np.where(a >= 0, (layer % max(pp, 1)) * x + e % x, -1)
     own = np.where(a >= 0, (a - n_hot) % world, -1)
     if n_hot > 0:
         if src is None:
@@ -249,7 +252,8 @@ def owner_of(adapter_ids: np.ndarray, world: int, n_hot: int = 0, src=None, expe
     return own
 
 
-def shard_dispatch(batch: li.Batch, world: int, n_hot: int = 0, ep: bool = False) -> List[Dict[str, np.ndarray]]:
+def shard_dispatch(batch: li.Batch, world: int, n_hot: int = 0, ep: bool = False, pp: int = 1,
+                   layer: int = 0) -> List[Dict[str, np.ndarray]]:
     """Per owner rank: the global row indices it receives, in receive order.
 
     Rows whose owner is their own source rank are processed in place and are
@@ -262,7 +266,7 @@ def shard_dispatch(batch: li.Batch, world: int, n_hot: int = 0, ep: bool = False
     for g in range(world):
         t0, t1 = token_range(batch.n_tokens, world, g)
         src_of_row[t0 * k:t1 * k] = g
-    own = owner_of(batch.adapter_ids, world, n_hot, src_of_row, batch.expert_ids, ep)
+    own = owner_of(batch.adapter_ids, world, n_hot, src_of_row, batch.expert_ids, ep, pp, layer)
     counts = np.zeros((world, world), np.int64)
     for s in range(world):
         for d in range(world):

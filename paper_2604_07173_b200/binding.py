@@ -33,7 +33,8 @@ class LoraConfig(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("n_adapters", ctypes.c_int32),
                 ("scale", ctypes.POINTER(ctypes.c_float)), ("max_rows", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("n_replicated", ctypes.c_int32), ("expert_parallel", ctypes.c_int32),
-                ("n_resident", ctypes.c_int32)]
+                ("n_resident", ctypes.c_int32), ("pp_stages", ctypes.c_int32),
+                ("slot_layer", ctypes.POINTER(ctypes.c_int32))]
 
 
 _vp, _i32, _i64, _u64, _u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32
@@ -126,14 +127,15 @@ def _ptr_array(items):
 
 def make_config(h_in: Sequence[int], h_out: Sequence[int], n_experts: Sequence[int], rank: int, n_adapters: int,
                 scale=None, max_rows: int = 4096, device: int = 0, n_replicated: int = 0, n_resident: int = 0,
-                expert_parallel: bool = False):
+                expert_parallel: bool = False, pp_stages: int = 0, slot_layer=None):
     n = len(h_in)
     keep = {"h_in": (ctypes.c_int32 * n)(*h_in), "h_out": (ctypes.c_int32 * n)(*h_out),
-            "E": (ctypes.c_int32 * n)(*n_experts)}
+            "E": (ctypes.c_int32 * n)(*n_experts),
+            "layer": (ctypes.c_int32 * n)(*slot_layer) if slot_layer is not None else None}
     keep["scale"] = (ctypes.c_float * n_adapters)(*[float(v) for v in scale]) if scale is not None else None
     cfg = LoraConfig(n, keep["h_in"], keep["h_out"], keep["E"], rank, n_adapters,
                      keep["scale"] if keep["scale"] is not None else None, max_rows, device, n_replicated,
-                     int(bool(expert_parallel)), n_resident)
+                     int(bool(expert_parallel)), n_resident, pp_stages, keep["layer"])
     cfg._keep = keep  # keep the arrays alive
     return cfg
 

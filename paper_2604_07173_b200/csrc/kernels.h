@@ -25,11 +25,17 @@ enum { kWqSimtShrink = 0, kWqSimtExpand = 1, kWqTcShrink = 2, kWqTcExpand = 3, k
 //    replicated on every rank (popularity-aware placement);
 //    adapter a >= n_hot is owned by rank (a - n_hot) mod world, all experts.
 //  * Expert parallel (ep = 1, Table 1 EP row):
-//    unit (a, e) is owned by rank e mod world, every adapter (all slots of
-//    the server share one expert count, checked at create).
-// An unsharded server is {1, 0, 0, 0}.
+//    unit (a, e) is owned by rank gbase + e mod x, every adapter (all slots of
+//    the server share one expert count, checked at create).  Pure EP: x =
+//    world, gbase = 0.  Hybrid EP_x-PP_y (Table 1 last row): the
+//    world is y groups of x ranks, layer l belongs to group l mod y
+//    (interleaved), gbase = (l mod y) * x; ranks outside the group store no
+//    unit of that layer.
+// An unsharded server is {1, 0, 0, 0, 1, 0}.
 struct Placement {
   int world, rank, n_hot, ep;
+  int x = 1;      // ep: expert-parallel degree (ranks per group)
+  int gbase = 0;  // ep: first rank of the group that owns this layer
   // adapter-level view (ep = 0)
   __host__ __device__ bool owns(int a) const { return a < n_hot || (a - n_hot) % world == rank; }
   __host__ __device__ int owner(int a) const { return a < n_hot ? rank : (a - n_hot) % world; }
@@ -46,12 +52,18 @@ struct Placement {
     const int rest = n_adapters - h;
     return h + (rest > rank ? (rest - rank + world - 1) / world : 0);
   }
+  // this rank's position in the owning group (ep), -1 if outside it
+  __host__ __device__ int erank() const { return (rank >= gbase && rank < gbase + x) ? rank - gbase : -1; }
   // unit-level view (both modes)
-  __host__ __device__ int experts_local(int E) const { return ep ? (E > rank ? (E - 1 - rank) / world + 1 : 0) : E; }
-  __host__ __device__ bool owns_unit(int a, int e) const { return ep ? e % world == rank : owns(a); }
-  __host__ __device__ int owner_unit(int a, int e) const { return ep ? e % world : owner(a); }
+  __host__ __device__ int experts_local(int E) const {
+    if (!ep) return E;
+    const int r = erank();
+    return (r >= 0 && E > r) ? (E - 1 - r) / x + 1 : 0;
+  }
+  __host__ __device__ bool owns_unit(int a, int e) const { return ep ? gbase + e % x == rank : owns(a); }
+  __host__ __device__ int owner_unit(int a, int e) const { return ep ? gbase + e % x : owner(a); }
   __host__ __device__ long long local_unit(int a, int e, int E) const {
-    return ep ? (long long)a * experts_local(E) + e / world : local_index(a) * E + e;
+    return ep ? (long long)a * experts_local(E) + e / x : local_index(a) * E + e;
   }
   // inverse of local_unit: global key a*E+e of local unit u (-1: none)
   __host__ __device__ long long global_key(long long u, int E, int n_adapters) const {
@@ -59,7 +71,7 @@ struct Placement {
     if (el == 0) return -1;
     const long long al = u / el, ei = u - al * el;
     const long long a = ep ? al : global_adapter(al);
-    const long long e = ep ? ei * world + rank : ei;
+    const long long e = ep ? ei * x + erank() : ei;
     return a < n_adapters ? a * E + e : -1;
   }
   // units stored on this rank

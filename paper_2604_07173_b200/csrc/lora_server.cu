@@ -142,6 +142,22 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
         delete s;
         return fail(nullptr, LORA_ERR_UNSUPPORTED, "expert parallel needs one expert count for every slot");
       }
+  if (s->ep) {
+    s->pp = cfg->pp_stages > 1 ? cfg->pp_stages : 1;
+    if (world % s->pp) {
+      delete s;
+      return fail(nullptr, LORA_ERR_INVALID_ARG, "pp_stages must divide the world size");
+    }
+  }
+  s->slot_layer.assign(cfg->n_slots, 0);
+  if (cfg->slot_layer)
+    for (int i = 0; i < cfg->n_slots; ++i) {
+      if (cfg->slot_layer[i] < 0) {
+        delete s;
+        return fail(nullptr, LORA_ERR_INVALID_ARG, "negative slot_layer");
+      }
+      s->slot_layer[i] = cfg->slot_layer[i];
+    }
   s->n_adapters_local = placement(s).n_local(cfg->n_adapters);
   if (world == 1 && cfg->n_resident > 0 && cfg->n_resident < cfg->n_adapters) s->n_resident = cfg->n_resident;
   // device store: every local adapter, or the cache slots
@@ -168,7 +184,8 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
     sl.h_in = cfg->h_in[i];
     sl.h_out = cfg->h_out[i];
     sl.E = cfg->n_experts[i];
-    sl.units = s->n_resident ? (long long)store_adapters * sl.E : placement(s).n_local_units(cfg->n_adapters, sl.E);
+    sl.units = s->n_resident ? (long long)store_adapters * sl.E
+                             : slot_placement(s, i).n_local_units(cfg->n_adapters, sl.E);
     // shrink items of ~128 KB of A, expand items of ~128 KB of B
     sl.KI = best_divisor(sl.h_in, 64, std::max(64, 65536 / r));
     sl.SJ = best_divisor(sl.KI, 64, simt_sj_max(r));
@@ -178,7 +195,9 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
     sl.n_ci = sl.h_out / sl.CI;
     sl.kc_prefix = kc_prefix;
     kc_prefix += sl.n_kc;
-    const size_t a_bytes = (size_t)sl.units * sl.h_in * r * 2, b_bytes = (size_t)sl.units * sl.h_out * r * 2;
+    // (a hybrid EP_x-PP_y rank stores no unit of the other groups' layers: 16 bytes)
+    const size_t a_bytes = std::max<size_t>(16, (size_t)sl.units * sl.h_in * r * 2),
+                 b_bytes = std::max<size_t>(16, (size_t)sl.units * sl.h_out * r * 2);
     if (cudaMalloc(&sl.At, a_bytes) != cudaSuccess || cudaMalloc(&sl.Bt, b_bytes) != cudaSuccess) {
       cudaGetLastError();
       s->slots.push_back(sl);
@@ -284,7 +303,7 @@ static lora_status_t load_slot(lora_server* s, int slot, int a_begin, int n, con
   const size_t stage_elems = (size_t)sl.E * std::max(a_unit, b_unit);
   CK(s, cudaMalloc(&stage, stage_elems * 2));
   lora_status_t rc = LORA_OK;
-  const Placement pl = placement(s);
+  const Placement pl = slot_placement(s, slot);
   for (int i = 0; i < n && rc == LORA_OK; ++i) {
     const int a = a_begin + i;
     // the owned experts of adapter a, as runs of consecutive units in the store
@@ -325,12 +344,19 @@ extern "C" lora_status_t lora_server_create(const lora_config_t* cfg, const void
   // rank of a sharded server would own (no communicator; rows of units it
   // does not own are rejected like out-of-range ids), so the sharded store
   // layouts can be checked against the oracle on one GPU.
-  int fw = 1, fr = 0, fep = 0, fhot = 0;
+  // (",pp" -- a fifth field -- overrides cfg->pp_stages: hybrid EP_x-PP_y)
+  int fw = 1, fr = 0, fep = 0, fhot = 0, fpp = 0;
   if (const char* f = std::getenv("LORA_FAKE_WORLD")) {
-    if (std::sscanf(f, "%d,%d,%d,%d", &fw, &fr, &fep, &fhot) < 2 || fw < 1 || fr < 0 || fr >= fw) {
+    if (std::sscanf(f, "%d,%d,%d,%d,%d", &fw, &fr, &fep, &fhot, &fpp) < 2 || fw < 1 || fr < 0 || fr >= fw) {
       fw = 1;
       fr = 0;
     }
+  }
+  lora_config_t cfg2;
+  if (cfg) {
+    cfg2 = *cfg;
+    if (fpp > 0) cfg2.pp_stages = fpp;
+    cfg = &cfg2;
   }
   lora_status_t st = create_common(cfg, fw, fr, out, fhot, fep);
   if (st != LORA_OK) return st;
@@ -385,8 +411,8 @@ extern "C" lora_status_t lora_server_fill_synthetic(lora_server_t* s, uint64_t s
   }
   for (size_t i = 0; i < s->slots.size(); ++i) {
     SlotInfo& sl = s->slots[i];
-    CK(s, launch_fill_store(sl.At, sl.Bt, sl.h_in, sl.h_out, sl.E, s->r, sl.units, (int)i, seed, placement(s),
-                            s->n_adapters, st));
+    CK(s, launch_fill_store(sl.At, sl.Bt, sl.h_in, sl.h_out, sl.E, s->r, sl.units, (int)i, seed,
+                            slot_placement(s, (int)i), s->n_adapters, st));
   }
   return LORA_OK;
 }
@@ -640,6 +666,8 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     if (!seen.insert(sl).second) return fail(s, LORA_ERR_INVALID_ARG, "duplicate slot in one multi apply");
     if (s->slots[sl].E != p->n_experts)
       return fail(s, LORA_ERR_INVALID_ARG, "slot n_experts differs from the plan's n_experts");
+    if (s->ep && slot_placement(s, sl).gbase != placement(s).gbase)
+      return fail(s, LORA_ERR_INVALID_ARG, "the slot's layer belongs to another pipeline group (EP_x-PP_y)");
     if (p->T > 0) {
       if (!x[i] || !y[i]) return fail(s, LORA_ERR_INVALID_ARG, "x or y is NULL");
       if (!aligned16(x[i]) || !aligned16(y[i])) return fail(s, LORA_ERR_INVALID_ARG, "x and y must be 16-byte aligned");

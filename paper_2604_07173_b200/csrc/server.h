@@ -34,7 +34,9 @@ struct lora_server {
   int tc_ki_max = 1 << 20;  // large-batch tcgen05 shrink: max h_in per item, default the whole h_in (env LORA_TC_KI_MAX)
   int world = 1, shard_rank = 0;
   int n_hot = 0;  // adapters [0, n_hot) replicated on every rank of a sharded server
-  int ep = 0;     // 1: expert-parallel ownership (unit (a, e) on rank e mod world)
+  int ep = 0;     // 1: expert-parallel ownership (unit (a, e) on rank gbase + e mod x)
+  int pp = 1;     // ep: pipeline stages y of EP_x-PP_y (x = world / y ranks per group)
+  std::vector<int> slot_layer;  // layer of each slot (group = layer mod pp)
   bool debug_sync = false;
   std::vector<SlotInfo> slots;
   int total_kc = 0;        // sum of n_kc over all slots
@@ -105,8 +107,20 @@ void lora_shard_free(lora_server* s);
 lora_status_t lora_shard_check_flags(lora_server* s, int flag);  // sticky-flag bits of the sharded path, NCCL errors
 lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int rank, lora_server** out, int n_hot,
                                     int ep);
+// this rank's placement (ep: its own group)
 inline lora::Placement placement(const lora_server* s) {
-  return lora::Placement{s->world, s->shard_rank, s->n_hot, s->ep};
+  lora::Placement p{s->world, s->shard_rank, s->n_hot, s->ep};
+  if (s->ep) {
+    p.x = s->world / s->pp;
+    p.gbase = (s->shard_rank / p.x) * p.x;
+  }
+  return p;
+}
+// placement of one slot's units (ep: the group of the slot's layer)
+inline lora::Placement slot_placement(const lora_server* s, int slot) {
+  lora::Placement p = placement(s);
+  if (s->ep) p.gbase = (s->slot_layer[slot] % s->pp) * p.x;
+  return p;
 }
 lora_status_t apply_multi_delta(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
                                 const void* const* x, void* const* d, cudaStream_t st, bool bf16);

@@ -813,7 +813,8 @@ static lora_status_t apply_sharded_push(lora_server* s, int n, const int32_t* sl
   ShardState* sh = s->shard;
   const int G = s->world, me = s->shard_rank;
   const int E = s->slots[slots[0]].E;
-  const Placement pl = placement(s);
+  const Placement pl = slot_placement(s, slots[0]);  // (EP_x-PP_y: the group of the call's layer)
+  const bool in_group = !pl.ep || pl.erank() >= 0;   // ranks outside it serve nothing, send everything
   const long long Rmax = (long long)s->max_rows * G;
   const int hash = layout_hash(n, slots, xk, yk, y_dtype);
   // scratch: counts [G + 1], send_idx [max_rows], ad_local [max_rows]
@@ -855,26 +856,31 @@ static lora_status_t apply_sharded_push(lora_server* s, int n, const int32_t* sl
                                                 (int)Rmax, s->d_err, sh->timeout_ns);
   prof_stop(s, pi, kKShardGather, sh->cs);
   CKS(cudaGetLastError());
-  lora_status_t rc = plan_build_impl(s, sh->plan, ids_a, ids_e, (int)Rmax, E, sh->cs, n_recv);
-  if (rc != LORA_OK) return rc;
+  lora_status_t rc = LORA_OK;
+  if (in_group) {
+    rc = plan_build_impl(s, sh->plan, ids_a, ids_e, (int)Rmax, E, sh->cs, n_recv);
+    if (rc != LORA_OK) return rc;
+  }
   CKS(cudaEventRecord(sh->ev[1], sh->cs));
   //    in-place rows (this rank's own or replicated units)
-  rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
-  if (rc != LORA_OK) return rc;
-  if (T > 0) {
+  if (in_group && T > 0) {
+    rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
+    if (rc != LORA_OK) return rc;
     rc = apply_multi_impl(s, sh->local_plan, n, slots, x, y, y_dtype, st);
     if (rc != LORA_OK) return rc;
   }
   // 3. owner apply: remote-x shrink, push-add expand
   CKS(cudaStreamWaitEvent(st, sh->ev[1], 0));
-  PushIn push{G, origin, sh->d_reg};
-  std::vector<int16_t> xr(n), yr(n);
-  for (int i = 0; i < n; ++i) {
-    xr[i] = (int16_t)xk[i];
-    yr[i] = (int16_t)yk[i];
+  if (in_group) {
+    PushIn push{G, origin, sh->d_reg};
+    std::vector<int16_t> xr(n), yr(n);
+    for (int i = 0; i < n; ++i) {
+      xr[i] = (int16_t)xk[i];
+      yr[i] = (int16_t)yk[i];
+    }
+    rc = apply_multi_impl(s, sh->plan, n, slots, x, y, y_dtype, st, 3, &push, xr.data(), yr.data());
+    if (rc != LORA_OK) return rc;
   }
-  rc = apply_multi_impl(s, sh->plan, n, slots, x, y, y_dtype, st, 3, &push, xr.data(), yr.data());
-  if (rc != LORA_OK) return rc;
   // 4. done -> peers; wait for every owner's pushes into this rank's y
   pi = prof_start(s, st);
   push_done_kernel<<<1, 32, 0, st>>>(sh->peer_ctl, me, G);
@@ -893,7 +899,8 @@ static lora_status_t apply_sharded_nccl(lora_server* s, int n, const int32_t* sl
                                         lora_dtype_t y_dtype, int T, cudaStream_t st) {
   NcclApi& api = nccl();
   const int G = s->world, me = s->shard_rank;
-  const Placement pl = placement(s);
+  const Placement pl = slot_placement(s, slots[0]);  // (EP_x-PP_y: the group of the call's layer)
+  const bool in_group = !pl.ep || pl.erank() >= 0;
   ShardState* sh = s->shard;
   cudaStream_t cs = sh->cs;
   const int E = s->slots[slots[0]].E;
@@ -964,9 +971,10 @@ static lora_status_t apply_sharded_nccl(lora_server* s, int n, const int32_t* sl
   CKN(api.AllGather(d_counts, d_counts + (G + 1), G + 1, ncclInt32, sh->comm, st));
   CKS(cudaMemcpyAsync(sh->h_cnt, d_counts + (G + 1), sizeof(int32_t) * G * (G + 1), cudaMemcpyDeviceToHost, st));
   CKS(cudaEventRecord(sh->ev[0], st));  // bucket outputs + counts ready (the pack waits on this)
-  lora_status_t rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
-  if (rc != LORA_OK) return rc;
-  if (T > 0) {
+  lora_status_t rc = LORA_OK;
+  if (in_group && T > 0) {
+    rc = plan_build_impl(s, sh->local_plan, d_ad_local, expert_ids, T, E, st);
+    if (rc != LORA_OK) return rc;
     rc = apply_multi_impl(s, sh->local_plan, n, slots, x, y, y_dtype, st);
     if (rc != LORA_OK) return rc;
   }
@@ -1027,11 +1035,13 @@ static lora_status_t apply_sharded_nccl(lora_server* s, int n, const int32_t* sl
   }
   CKN(api.GroupEnd());
   //    owner side, still on the communication stream: the received rows' plan
-  rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, cs);
-  if (rc != LORA_OK) return rc;
+  if (n_recv > 0) {
+    rc = plan_build_impl(s, sh->plan, d_ids_recv, d_ids_recv + Rmax, n_recv, E, cs);
+    if (rc != LORA_OK) return rc;
+  }
   CKS(cudaEventRecord(sh->ev[1], cs));
 
-  // 4. received rows: delta-mode apply
+  // 4. received rows: delta-mode apply (n_recv > 0 only inside the call's group)
   CKS(cudaStreamWaitEvent(st, sh->ev[1], 0));
   if (n_recv > 0) {
     std::vector<const void*> xs(n);
@@ -1088,8 +1098,11 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
   for (int i = 0; i < n; ++i)
     if (slots[i] < 0 || slots[i] >= (int)s->slots.size()) return fail(s, LORA_ERR_INVALID_ARG, "bad slot index");
   const int E = s->slots[slots[0]].E;
-  for (int i = 0; i < n; ++i)
+  for (int i = 0; i < n; ++i) {
     if (s->slots[slots[i]].E != E) return fail(s, LORA_ERR_INVALID_ARG, "slots of one call must share n_experts");
+    if (slot_placement(s, slots[i]).gbase != slot_placement(s, slots[0]).gbase)
+      return fail(s, LORA_ERR_INVALID_ARG, "EP_x-PP_y: the slots of one call must belong to one pipeline group");
+  }
   ShardState* sh = s->shard;
   CKS(cudaSetDevice(s->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);

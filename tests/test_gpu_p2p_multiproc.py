@@ -36,12 +36,14 @@ def _free_port():
     return p
 
 
-def _cfg(y_dtype):
-    return li.Config("mp_p2p", 8, (li.Slot("a", 512, 768, 4, 0), li.Slot("b", 768, 512, 4, 1)), 64, 24, 4, 2, 300,
-                     y_dtype)
+def _cfg(y_dtype, two_layers=False):
+    sl = (li.Slot("a", 512, 768, 4, 0), li.Slot("b", 768, 512, 4, 1))
+    if two_layers:
+        sl = sl + (li.Slot("a1", 512, 768, 4, 2), li.Slot("b1", 768, 512, 4, 3))
+    return li.Config("mp_p2p", 8, sl, 64, 24, 4, 2, 300, y_dtype)
 
 
-def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep):
+def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep, pp=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     if y_dtype == "fp32":
         # CUDA-core route for every segment: the per-row arithmetic then does not depend on how
@@ -58,14 +60,17 @@ def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep):
             dist.all_gather(out, t)
             return b"".join(o.numpy().tobytes() for o in out)
 
-        cfg = _cfg(y_dtype)
+        cfg = _cfg(y_dtype, two_layers=pp > 1)
+        n_sl = len(cfg.slots)
+        calls = [[0, 1], [2, 3]] if pp > 1 else [[0, 1]]   # one sharded apply per layer
         b = li.make_batch(cfg)
         k = b.top_k
         t0, t1 = (cfg.n_tokens * rank) // world, (cfg.n_tokens * (rank + 1)) // world
         r0, r1 = t0 * k, t1 * k
         T = r1 - r0
-        c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots], [4, 4], cfg.rank,
-                          cfg.n_adapters, cfg.scale(), T, 0, n_replicated=n_hot, expert_parallel=ep)
+        c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots], [4] * n_sl, cfg.rank,
+                          cfg.n_adapters, cfg.scale(), T, 0, n_replicated=n_hot, expert_parallel=ep, pp_stages=pp,
+                          slot_layer=[i // 2 for i in range(n_sl)])
         s = B.lora_server_create_sharded_host(c, rank, world, allgather)
         B.lora_server_fill_synthetic(s, cfg.seed)
         xs, ys = [], []
@@ -88,10 +93,11 @@ def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep):
                 v.copy_(v0)
             torch.cuda.synchronize()
             dist.barrier()  # (no rank may overwrite its y while a peer still pushes into it)
-            B.lora_apply_sharded(s, [0, 1], xs, ad, ex, yy, dt, T)
+            for cl in calls:
+                B.lora_apply_sharded(s, cl, [xs[i] for i in cl], ad, ex, [yy[i] for i in cl], dt, T)
             torch.cuda.synchronize()
         assert B.lora_server_check(s) == B.LORA_OK
-        for i in range(2):
+        for i in range(n_sl):
             np.save(os.path.join(out_dir, f"y{i}_{rank}.npy"), yy[i].cpu().numpy())
         B.lora_server_destroy(s)
     finally:
@@ -99,20 +105,23 @@ def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("y_dtype,n_hot,ep", [("fp32", 0, False), ("fp32", 3, False), ("bf16", 0, False),
-                                              ("fp32", 0, True)])
-def test_p2p_two_ranks_one_gpu(tmp_path, y_dtype, n_hot, ep):
+@pytest.mark.parametrize("y_dtype,n_hot,ep,world,pp", [("fp32", 0, False, 2, 0), ("fp32", 3, False, 2, 0),
+                                                       ("bf16", 0, False, 2, 0), ("fp32", 0, True, 2, 0),
+                                                       ("fp32", 0, True, 4, 2)])
+def test_p2p_two_ranks_one_gpu(tmp_path, y_dtype, n_hot, ep, world, pp):
+    """(world 4, pp 2: hybrid EP2-PP2 over four processes, one sharded apply
+    per layer; each layer's rows are served by its group's two ranks, every
+    rank sends.)"""
     from tests import gpu_util as U
     from oracle import oracle as orc
-    world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), y_dtype, n_hot, ep), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), y_dtype, n_hot, ep, pp), nprocs=world, join=True)
     B = U.binding()
-    cfg = _cfg(y_dtype)
+    cfg = _cfg(y_dtype, two_layers=pp > 1)
     b = li.make_batch(cfg)
     T = b.n_rows
     s = U.make_server(B, cfg, small_max=-1 if y_dtype == "fp32" else None)
     try:
-        for i in range(2):
+        for i in range(len(cfg.slots)):
             got = np.concatenate([np.load(tmp_path / f"y{i}_{r}.npy") for r in range(world)])
             U.assert_parity(torch.from_numpy(got), orc.apply_slot(cfg, i, b), f"p2p 2-rank slot {i}")
             if y_dtype == "fp32":

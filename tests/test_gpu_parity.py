@@ -720,3 +720,43 @@ def test_sharded_push_graph_capture(B, monkeypatch):
     finally:
         B.lora_server_destroy(sh)
         B.lora_server_destroy(s)
+
+
+@pytest.mark.parametrize("rank", [0, 1, 2, 3])
+def test_hybrid_ep2_pp2_store_fake_world(B, monkeypatch, rank):
+    """Hybrid EP_x-PP_y placement with x = 2, y = 2 on a world of
+    4 (LORA_FAKE_WORLD test hook, fifth field = pp stages): layers 0 and 1
+    (two slots each) interleave over the two groups (layer l -> ranks
+    (l mod 2) * 2 + e mod 2).  This rank's own layer: the rows whose expert it
+    owns match the oracle, the rest stay untouched and are flagged.  The
+    other group's layer: the apply is rejected (no unit stored)."""
+    monkeypatch.setenv("LORA_FAKE_WORLD", f"4,{rank},1,0,2")
+    cfg = li.Config("hyb", 8, (li.Slot("a0", 512, 768, 4, 0), li.Slot("b0", 768, 512, 4, 1),
+                               li.Slot("a1", 512, 768, 4, 2), li.Slot("b1", 768, 512, 4, 3)), 64, 24, 4, 2, 250, "bf16")
+    b = li.make_batch(cfg)
+    T = b.n_rows
+    c = B.make_config([sl.h_in for sl in cfg.slots], [sl.h_out for sl in cfg.slots], [4] * 4, cfg.rank,
+                      cfg.n_adapters, cfg.scale(), T, 0, expert_parallel=True, pp_stages=2, slot_layer=[0, 0, 1, 1])
+    s = B.lora_server_create(c)
+    try:
+        B.lora_server_fill_synthetic(s, cfg.seed)
+        my_layer = rank // 2
+        for layer in (0, 1):
+            sl = [2 * layer, 2 * layer + 1]
+            if layer != my_layer:
+                with pytest.raises(B.LoraError):
+                    _run_multi_unchecked(B, s, cfg, b, sl)
+                continue
+            own = orc.owner_of(b.adapter_ids, 4, 0, None, b.expert_ids, True, 2, layer)
+            y0 = [U.y0_dev(B, cfg, i, T) for i in sl]
+            ys = _run_multi_unchecked(B, s, cfg, b, sl)
+            assert B.lora_server_check(s) == B.LORA_ERR_ID_OUT_OF_RANGE   # the other rank's rows
+            rows = np.flatnonzero(own == rank)
+            other = torch.from_numpy(np.flatnonzero(own != rank)).to(U.DEV)
+            assert rows.size > 0
+            for j, i in enumerate(sl):
+                U.assert_parity(ys[j][torch.from_numpy(rows).to(U.DEV)], oracle.apply_slot(cfg, i, b, rows=rows),
+                                f"hybrid rank {rank} slot {i}")
+                assert torch.equal(ys[j][other], y0[j][other])
+    finally:
+        B.lora_server_destroy(s)

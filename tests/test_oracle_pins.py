@@ -367,7 +367,7 @@ def test_shard_dispatch_golden_hand_cases():
         e = np.array(c["expert_ids"], np.int32)
         k = c["top_k"]
         b = li.Batch(a, e, a.size // k, k)
-        disp = orc.shard_dispatch(b, c["world"], c["n_hot"], c["ep"])
+        disp = orc.shard_dispatch(b, c["world"], c["n_hot"], c["ep"], c.get("pp", 1), c.get("layer", 0))
         for d in range(c["world"]):
             assert disp[d]["rows"].tolist() == c["rows"][d], (c["name"], d)
             assert disp[d]["local"].tolist() == c["local"][d], (c["name"], d)

@@ -86,3 +86,64 @@ def test_rank_hbm_bytes_brute_force():
                 elif src[i] == g:
                     rout += 1
             assert abs(got[g] - (len(units) * U + (mine + rout) * R)) < 1e-6, (h, ep, g)
+
+
+def test_rank_costs_push_brute_force():
+    """Push-path model: a row's x read and y RMW land on its SOURCE's HBM,
+    owners pay the units they serve; link bytes in/out per rank; per-row
+    brute force for DP with replication, EP and hybrid EP_x-PP_y."""
+    rng = np.random.default_rng(6)
+    n = 240
+    a = rng.integers(-1, 12, n)
+    e = rng.integers(0, 4, n)
+    G = 4
+    src = np.repeat(np.arange(G), n // G)
+    U, R, X, D = 1000.0, 10.0, 7.0, 3.0
+    for h, ep, pp, layer in ((0, False, 1, 0), (2, False, 1, 0), (0, True, 1, 0), (0, True, 2, 1), (0, True, 2, 0)):
+        got = P.rank_costs_push(a, e, src, G, h, U, R, X, D, hbm_gbs=1.0, link_gbs=1.0, fixed_s=0.0, ep=ep, pp=pp,
+                                layer=layer) * 1e9
+        for g in range(G):
+            units, own_rows, rin, rout = set(), 0, 0, 0
+            for i in range(n):
+                if a[i] < 0:
+                    continue
+                if ep:
+                    x = G // pp
+                    o = (layer % pp) * x + int(e[i]) % x
+                else:
+                    o = int(src[i]) if a[i] < h else (a[i] - h) % G
+                if src[i] == g:
+                    own_rows += 1
+                if o == g:
+                    units.add((a[i], e[i]))
+                    rin += src[i] != g
+                elif src[i] == g:
+                    rout += 1
+            hbm = len(units) * U + own_rows * R
+            link = max(rin * X + rout * D, rout * X + rin * D)
+            assert abs(got[g] - max(hbm, link)) < 1e-6, (h, ep, pp, g)
+
+
+def test_hybrid_owner_matches_oracle_routing():
+    b = li.make_batch(li.CONFIGS["mixtral_decode"])
+    for y in (1, 2, 4, 8):
+        for layer in (0, 1, 5):
+            x = 8 // y
+            own = np.where(b.adapter_ids >= 0, (layer % y) * x + b.expert_ids % x, -1)
+            np.testing.assert_array_equal(own, orc.owner_of(b.adapter_ids, 8, 0, None, b.expert_ids, True, y, layer))
+
+
+def test_push_model_predicts_config5_efficiency():
+    """The push-path model (registered buffers, transfers fused into the
+    kernels) at G = 8 on config 5 -- the design target of >= 0.70 strong-
+    scaling efficiency (north star)."""
+    cfg = li.CONFIGS["mixtral_sharded"]
+    b = li.make_batch(cfg)
+    u, r, x, d = P.slot_bytes_push([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots],
+                                   [s.xbuf for s in cfg.slots], 64, 2, 2)
+    t1 = P.rank_costs_push(b.adapter_ids, b.expert_ids, np.zeros(b.n_rows, int), 1, 0, u, r, x, d, fixed_s=0)[0]
+    for G in (2, 4, 8):
+        src = P.sources_of_rows(cfg.n_tokens, 2, G)
+        ch = P.choose_placement(b.adapter_ids, b.expert_ids, src, G, u, r, 0.0, x_bytes=x, d_bytes=d)
+        tg = min(ch["table"].values())
+        assert t1 / (G * tg) >= 0.70, (G, t1 / (G * tg))
