@@ -155,6 +155,8 @@ struct MultiArgs {
   int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16;
                            // 3 (push): adds it into the source's y row (red.add over NVLink)
   int tc_cap_k;            // > 0: tcgen05 kernels use at most max(8, tiles * tc_cap_k) CTAs (rest exit at once)
+  int tc_flags;            // tcgen05 expand L2 policies (env LORA_TCE_FLAGS): bit 0 Bt evict_last (else
+                           // evict_first), bit 1 y loads evict_first, bit 2 y stores evict_first
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const int32_t* cache;    // resident-cache mode: unit = cache[a]*E + e (nullptr: placement)
   const float* scale;      // [n_adapters] s_a
@@ -163,6 +165,8 @@ struct MultiArgs {
   // filled by the host when total_kc / total_ci <= kTaskTable
   uint8_t kc_task[kTaskTable];
   uint8_t ci_task[kTaskTable];
+  int8_t tc_pair[kMaxTasks];   // tcgen05 shrink launch: partner task sharing this task's x / h_in / KI (its
+                               // A tiles ride in the same N = 2r MMA; the partner has no items), -1 none
   PushIn push;                 // sharded owner over registered buffers (G = 0 otherwise)
   int16_t xreg[kMaxTasks];     // push: registered-buffer index of each task's x and y
   int16_t yreg[kMaxTasks];

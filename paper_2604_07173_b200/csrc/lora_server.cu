@@ -168,6 +168,8 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (const char* e = std::getenv("LORA_TC_KI_MAX")) s->tc_ki_max = std::max(128, std::atoi(e));
   if (const char* e = std::getenv("LORA_TC_CI_MAX")) s->tc_ci_max = std::atoi(e);
   if (const char* e = std::getenv("LORA_TC_CAP_K")) s->tc_cap_k = std::atoi(e);
+  if (const char* e = std::getenv("LORA_TCE_FLAGS")) s->tc_flags = std::atoi(e);
+  if (const char* e = std::getenv("LORA_TC_PAIR")) s->tc_pair = std::atoi(e) != 0;
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
   if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -711,6 +713,8 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.y_fp32 = y_dtype == LORA_FP32;
     args.y_store = store;
     args.tc_cap_k = s->concurrent_tc ? s->tc_cap_k : 0;
+    args.tc_flags = s->tc_flags;
+    std::memset(args.tc_pair, -1, sizeof(args.tc_pair));  // (set per tcgen05 shrink launch below)
     args.pl = placement(s);
     args.cache = s->d_cache;
     args.scale = s->d_scale;
@@ -803,8 +807,42 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     }
     int pi;
     if (tc) {
+      // gate + up (slots sharing x, h_in, KI): one item per pair (x gathered
+      // once, N = 2r MMA); the partner's items are dropped from the shrink's
+      // item space (env LORA_TC_PAIR=0 disables)
+      MultiArgs targs = args;
+      std::memset(targs.tc_pair, -1, sizeof(targs.tc_pair));
+      if (s->tc_pair) {
+        std::vector<char> taken(nb, 0);
+        for (int i = 0; i < nb; ++i) {
+          if (taken[i]) continue;
+          for (int j = i + 1; j < nb; ++j) {
+            const SlotTask &a = args.t[i], &b = args.t[j];
+            if (!taken[j] && a.x == b.x && a.h_in == b.h_in && a.KI == b.KI && a.n_kc == b.n_kc && a.E == b.E &&
+                args.xreg[i] == args.xreg[j]) {
+              targs.tc_pair[i] = (int8_t)j;
+              taken[i] = taken[j] = 1;
+              break;
+            }
+          }
+        }
+        int kc4 = 0;
+        for (int i = 0; i < nb; ++i) {
+          SlotTask& t = targs.t[i];
+          const bool partner = taken[i] && targs.tc_pair[i] < 0;
+          t.kc_base = kc4;
+          kc4 += partner ? 0 : t.n_kc;
+        }
+        // (a partner keeps its n_kc: the primary's epilogue stores its v with it)
+        targs.total_kc = kc4;
+        for (int i = 0; i < nb; ++i) {
+          const bool partner = taken[i] && targs.tc_pair[i] < 0;
+          for (int k = 0; !partner && k < targs.t[i].n_kc && targs.t[i].kc_base + k < kTaskTable; ++k)
+            targs.kc_task[targs.t[i].kc_base + k] = (uint8_t)i;
+        }
+      }
       pi = prof_start(s, tst);
-      CK(s, launch_tc_shrink(args, p->dev, p->T, grid, tst));
+      CK(s, launch_tc_shrink(targs, p->dev, p->T, grid, tst));
       prof_stop(s, pi, kKTcShrink, tst);
       if (any_split) {  // tiles of a task with n_kc == 1 got their v from the shrink
         pi = prof_start(s, tst);

@@ -138,7 +138,12 @@ LORA_DEVINL bool tc_cta_idle(const MultiArgs& args, const PlanDev& pd) {
 // ===========================================================================
 // shrink
 // ===========================================================================
-struct ShrinkCfg {
+// PAIR: two slots that share x, h_in and the row plan (gate and up of a MoE
+// layer) in one item -- the gathered x tile feeds one
+// N = 2r MMA whose B operand is the two slots' A tiles back to back, so x is
+// read once for both.
+template <bool PAIR>
+struct ShrinkCfgT {
   static constexpr int EPI_WARPS = 4;   // warps 0-3: epilogue (TMEM lanes 0-127)
   static constexpr int MMA_WARP = 4;    // warp 4: TMEM alloc + MMA issue
   static constexpr int PROD_WARP0 = 5;  // warps 5-8: activation gather (+ weight bulk copy)
@@ -154,16 +159,22 @@ struct ShrinkCfg {
 #ifndef LORA_TCS_LAG
 #define LORA_TCS_LAG 2
 #endif
+#ifndef LORA_TCSP_NST
+#define LORA_TCSP_NST 3
+#endif
   static constexpr int KS_PER_STAGE = LORA_TCS_KS;         // k-steps per stage
+  static constexpr int NW = PAIR ? 2 : 1;                  // A tiles per k-step
   static constexpr int X_SUB = kTileRows * 128;            // 16 KB per k-step
-  static constexpr int W_SUB = R * 128;                    // 8 KB per k-step
-  static constexpr int STAGE = KS_PER_STAGE * (X_SUB + W_SUB);
-  static constexpr int NST = LORA_TCS_NST;
-  static constexpr int LAG = LORA_TCS_LAG;                 // cp.async groups kept in flight
-  static constexpr int ACC_COLS = 64;                      // N = r
-  static constexpr int TMEM_COLS = 128;                    // 2 accumulators
+  static constexpr int W_SUB = R * 128;                    // 8 KB per k-step and slot
+  static constexpr int STAGE = KS_PER_STAGE * (X_SUB + NW * W_SUB);
+  static constexpr int NST = PAIR ? LORA_TCSP_NST : LORA_TCS_NST;
+  static constexpr int LAG = LORA_TCS_LAG < NST - 1 ? LORA_TCS_LAG : NST - 1;  // cp.async groups kept in flight
+  static constexpr int ACC_COLS = NW * R;                  // N = r (pair: 2r)
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;           // 2 accumulators
   static constexpr int SMEM = 1024 + NST * STAGE + 256;
+  static_assert(SMEM <= 227 * 1024, "shrink stages exceed shared memory");
 };
+using ShrinkCfg = ShrinkCfgT<false>;
 
 // v row n of a tile (R fp32 sums) rounded to bf16 into the pre-swizzled
 // expand operand: 16-byte chunk q of the row at q ^ (n & 7)
@@ -179,10 +190,10 @@ LORA_DEVINL void store_vbf_row(uint16_t* dst_row, int n, const float* v) {
   }
 }
 
-template <bool REMOTE>
+template <bool REMOTE, bool PAIR>
 __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
     tc_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd, const __grid_constant__ TcMaps maps) {
-  using C = ShrinkCfg;
+  using C = ShrinkCfgT<PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::NST * C::STAGE);
@@ -248,9 +259,12 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       const int kc = kcg - t.kc_base;
       const int4 tile = pd.tiles[ti];
       const long long unit = store_unit(tile.z, t.E, args.pl, args.cache);
-      const uint16_t* wbase = t.At + (unit * (t.h_in >> 6) + ((kc * t.KI) >> 6)) * (long long)(R * 64);
+      const long long woff = (unit * (t.h_in >> 6) + ((kc * t.KI) >> 6)) * (long long)(R * 64);
+      const uint16_t* wbase = t.At + woff;
+      const int pj = PAIR ? args.tc_pair[task] : -1;          // partner slot (same x, h_in, plan)
+      const uint16_t* wbase2 = pj >= 0 ? args.t[pj].At + woff : nullptr;
       const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
-      if (!REMOTE && maps.use) {
+      if (!PAIR && !REMOTE && maps.use) {
         // one warp: lane l gathers tile rows 4l .. 4l+3 (rows past the tile
         // repeat its first row; their accumulator rows are never read)
         if (warp != C::PROD_WARP0) continue;
@@ -297,9 +311,28 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sbase = smem + stage * C::STAGE;
         if (pt == 0) {
-          mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
-          bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB,
-                   wbase + (long long)st * C::KS_PER_STAGE * (R * 64), C::KS_PER_STAGE * C::W_SUB, &full[stage]);
+          // W region of a stage: per k-step [NW][R rows x 128 B] -- for a pair the
+          // two slots' A tiles back to back, one N = 2r operand
+          if (pj >= 0) {
+            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * 2 * C::W_SUB);
+#pragma unroll
+            for (int ks = 0; ks < C::KS_PER_STAGE; ++ks) {
+              uint8_t* wd = sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB;
+              const long long wo = (long long)(st * C::KS_PER_STAGE + ks) * (R * 64);
+              bulk_g2s(wd, wbase + wo, C::W_SUB, &full[stage]);
+              bulk_g2s(wd + C::W_SUB, wbase2 + wo, C::W_SUB, &full[stage]);
+            }
+          } else if (C::NW == 1) {
+            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
+            bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB,
+                     wbase + (long long)st * C::KS_PER_STAGE * (R * 64), C::KS_PER_STAGE * C::W_SUB, &full[stage]);
+          } else {  // an unpaired task in a pair launch: one A tile per k-step, N = r
+            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
+#pragma unroll
+            for (int ks = 0; ks < C::KS_PER_STAGE; ++ks)
+              bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB,
+                       wbase + (long long)(st * C::KS_PER_STAGE + ks) * (R * 64), C::W_SUB, &full[stage]);
+          }
         }
         const int j0 = st * C::KS_PER_STAGE * C::KSTEP;
 #pragma unroll
@@ -335,14 +368,15 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    constexpr uint32_t idesc = idesc_bf16(128, C::ACC_COLS);
     QueuePos qp;
     for (;;) {
       const long long it = wq_pop(wq, qp);
       if (it < 0) break;
       const int kcg = (int)(it / n_tiles);
-      const SlotTask& t = args.t[find_task_kc(args, kcg)];
+      const int task = find_task_kc(args, kcg);
+      const SlotTask& t = args.t[task];
       const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
+      const uint32_t idesc = idesc_bf16(128, (PAIR && args.tc_pair[task] >= 0) ? 2 * R : R);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
@@ -354,7 +388,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
 #pragma unroll
           for (int ks = 0; ks < C::KS_PER_STAGE; ++ks) {
             const uint32_t xa = sbase + ks * C::X_SUB;
-            const uint32_t wa = sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::W_SUB;
+            const uint32_t wa = sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB;
 #pragma unroll
             for (int k = 0; k < C::KSTEP / 16; ++k) {
               umma_bf16(d_tmem, sw128_desc(xa + k * 32), sw128_desc(wa + k * 32), idesc,
@@ -385,29 +419,35 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       const long long it = wq_pop(wq, qp);
       if (it < 0) break;
       const int kcg = (int)(it / n_tiles), ti = (int)(it - (long long)kcg * n_tiles);
-      const SlotTask& t = args.t[find_task_kc(args, kcg)];
+      const int task = find_task_kc(args, kcg);
+      const SlotTask& t = args.t[task];
       const int kc = kcg - t.kc_base;
       const int4 tile = pd.tiles[ti];
+      const int pj = PAIR ? args.tc_pair[task] : -1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      float v[C::ACC_COLS];
-      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS;
+      // columns [0, R) are this task's v, [R, 2R) the partner's (pair)
+#pragma unroll 1
+      for (int half = 0; half < (pj >= 0 ? 2 : 1); ++half) {
+        const SlotTask& th = half ? args.t[pj] : t;
+        float v[R];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS + half * R;
 #pragma unroll
-      for (int c = 0; c < C::ACC_COLS; c += 16) tmem_ld16(taddr + c, v + c);
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-      if (row_in_tile < tile.y) {
-        if (t.n_kc == 1) {
-          // the whole K in one accumulator: v rounded to bf16 here (no reduction pass)
-          store_vbf_row(pd.vbf + t.vbf_off + ((long long)tile.x + row_in_tile) * R, row_in_tile, v);
-        } else {
-          float4* dst = reinterpret_cast<float4*>(pd.vpart + t.vpart_off +
-                                                  ((long long)kc * pd.max_rows + tile.x + row_in_tile) * R);
+        for (int c = 0; c < R; c += 16) tmem_ld16(taddr + c, v + c);
+        if (row_in_tile < tile.y) {
+          if (t.n_kc == 1) {
+            // the whole K in one accumulator: v rounded to bf16 here (no reduction pass)
+            store_vbf_row(pd.vbf + th.vbf_off + ((long long)tile.x + row_in_tile) * R, row_in_tile, v);
+          } else {
+            float4* dst = reinterpret_cast<float4*>(pd.vpart + th.vpart_off +
+                                                    ((long long)kc * pd.max_rows + tile.x + row_in_tile) * R);
 #pragma unroll
-          for (int c = 0; c < C::ACC_COLS / 4; ++c)
-            dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            for (int c = 0; c < R / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -602,7 +642,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   if (warp == C::TMA_WARP) {
     // ===================== producer: v tile + Bt sub-tiles =====================
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = (args.tc_flags & 1) ? policy_evict_last() : policy_evict_first();
       int stage = 0, vb = 0;
       uint32_t phase = 0, vphase = 0;
       bool vready = false;
@@ -696,6 +736,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
     const int n = q * 32 + lane;                 // this thread's tile row (TMEM lane)
     const int cc = et & 15;                      // chunk column of this thread's copies
     const uint32_t ybase = smem_u32(yring);
+    const bool ypol_ld = (args.tc_flags & 2) != 0, ypol_st = (args.tc_flags & 4) != 0;
+    const uint64_t ypol = policy_evict_first();
     long long k = 0;                             // global sub-tile counter (same as the MMA warp's)
     int kk = 0;                                  // this CTA's sub-tile sequence number (ring slot)
     QueuePos qp;
@@ -731,7 +773,13 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           const uint32_t sl = slot_of(kk + sb);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (cval[j]) cp_async16_u32(chunk_addr(sl, (et >> 4) + 32 * j, cc), yb + coff[j] + (long long)sb * C::MSUB);
+            if (cval[j]) {
+              if (ypol_ld)
+                cp_async16_u32_hint(chunk_addr(sl, (et >> 4) + 32 * j, cc), yb + coff[j] + (long long)sb * C::MSUB,
+                                    ypol);
+              else
+                cp_async16_u32(chunk_addr(sl, (et >> 4) + 32 * j, cc), yb + coff[j] + (long long)sb * C::MSUB);
+            }
         }
         cp_async_commit();
       };
@@ -774,6 +822,8 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
             const uint4 v = lds128(chunk_addr(sl, (et >> 4) + 32 * j, cc));
             if constexpr (M == 4)
               red_add_bf16x8(ppush[j] + (long long)sb * C::MSUB, v);
+            else if (ypol_st)
+              st_global_v4_hint(yb + coff[j] + (long long)sb * C::MSUB, v, ypol);
             else
               *reinterpret_cast<uint4*>(yb + coff[j] + (long long)sb * C::MSUB) = v;
           }
@@ -952,14 +1002,19 @@ static void make_x_maps(const MultiArgs& args, int x_rows, TcMaps& m) {
 }
 
 cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid, cudaStream_t stream) {
-  static unsigned long long mask[2] = {0, 0};
+  static unsigned long long mask[4] = {0, 0, 0, 0};
   const bool remote = args.push.G > 0;
-  auto kern = remote ? tc_shrink_kernel<true> : tc_shrink_kernel<false>;
-  cudaError_t e = set_smem_once(kern, ShrinkCfg::SMEM, mask[remote]);
+  bool pair = false;
+  for (int i = 0; i < args.n_tasks; ++i) pair = pair || args.tc_pair[i] >= 0;
+  auto kern = remote ? (pair ? tc_shrink_kernel<true, true> : tc_shrink_kernel<true, false>)
+                     : (pair ? tc_shrink_kernel<false, true> : tc_shrink_kernel<false, false>);
+  const int smem = pair ? ShrinkCfgT<true>::SMEM : ShrinkCfgT<false>::SMEM;
+  cudaError_t e = set_smem_once(kern, smem, mask[remote * 2 + pair]);
   if (e != cudaSuccess) return e;
   TcMaps maps;
   make_x_maps(args, x_rows, maps);
-  e = launch_pdl(kern, dim3(grid), dim3(ShrinkCfg::THREADS), ShrinkCfg::SMEM, stream, args, pd, maps);
+  if (pair) maps.use = 0;
+  e = launch_pdl(kern, dim3(grid), dim3(ShrinkCfg::THREADS), smem, stream, args, pd, maps);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
