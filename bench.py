@@ -53,7 +53,8 @@ def algorithmic(cfg: li.Config, batch: li.Batch, slots, small_max: int = 8):
     """Algorithmic bytes per step, split by kernel.
 
     Each touched unit's A and B are read once, each valid row's x once per
-    slot, its y read + written once; a segment of more than `small_max` rows
+    distinct x buffer (slots sharing x -- gate/up, q/k/v -- need it once),
+    its y read + written once; a segment of more than `small_max` rows
     runs on the tcgen05 kernels (rank 64, 128-multiple widths), else on the
     CUDA-core kernels -- the same dispatch rule the library applies."""
     a = batch.adapter_ids.astype(np.int64)
@@ -64,14 +65,18 @@ def algorithmic(cfg: li.Config, batch: li.Batch, slots, small_max: int = 8):
     tc_ok = r == 64 and small_max >= 0 and all(s.h_in % 128 == 0 and s.h_out % 128 == 0 for s in cfg.slots)
     out = {"segment": T * 8, "simt_shrink": 0, "simt_expand": 0, "tc05_shrink": 0, "tc05_expand": 0,
            "flops": 0, "units": {}}
+    seen_x = set()
     for i in slots:
         sl = cfg.slots[i]
         _, cnt = np.unique(a[valid] * sl.n_experts + batch.expert_ids[valid], return_counts=True)
         out["units"][sl.name] = int(cnt.size)
         big = (cnt > small_max) if tc_ok else np.zeros(cnt.size, bool)
+        # x is an input of the step: slots sharing it (gate/up, q/k/v) need it read once
+        x_once = sl.xbuf not in seen_x
+        seen_x.add(sl.xbuf)
         for path, m in (("simt", ~big), ("tc05", big)):
             U, rows = int(m.sum()), int(cnt[m].sum())
-            out[path + "_shrink"] += U * sl.h_in * r * 2 + rows * sl.h_in * 2
+            out[path + "_shrink"] += U * sl.h_in * r * 2 + (rows * sl.h_in * 2 if x_once else 0)
             out[path + "_expand"] += U * sl.h_out * r * 2 + rows * sl.h_out * 2 * ysz
         out["flops"] += 2 * Tv * r * (sl.h_in + sl.h_out)
     out["shrink"] = out["simt_shrink"] + out["tc05_shrink"]

@@ -97,12 +97,14 @@ struct PlanDev {
   int32_t* lrank;            // [same] rank of each sorted entry inside its key's run
   int32_t* hist;             // [kSegHistMax] run lengths, key-major [K][C] (kept zero between builds)
   int32_t* offs;             // [kSegHistMax] exclusive prefix of hist
+  unsigned int* gcnt;        // [kMaxTasks][max_rows] K-split CUDA-core shrink: arrivals per (task, group), self-resetting
   int max_rows;
 };
 
 struct SegParams {
   int small_max;   // segments with more rows than this go to tcgen05 (if enabled)
   int tc_enabled;  // rank 64 and not forced off
+  int tc_min_rows; // tcgen05 tiles only if the large segments hold at least this many rows in total
   int tile_rows;
   Placement pl;    // rows whose adapter this rank does not store are rejected (flagged)
   const int32_t* cache;  // resident-cache mode: [n_adapters] cache slot or -1 (not resident: rejected)
@@ -155,8 +157,14 @@ struct MultiArgs {
   int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16;
                            // 3 (push): adds it into the source's y row (red.add over NVLink)
   int tc_cap_k;            // > 0: tcgen05 kernels use at most max(8, tiles * tc_cap_k) CTAs (rest exit at once)
-  int tc_flags;            // tcgen05 expand L2 policies (env LORA_TCE_FLAGS): bit 0 Bt evict_last (else
-                           // evict_first), bit 1 y loads evict_first, bit 2 y stores evict_first
+  int n_cls;               // CUDA-core shrink item order: runs of consecutive tasks with one h_in
+  int16_t cls_first[kMaxTasks + 1];  // (the launch's tasks sorted by h_in): items of a run are group-major,
+                                     // so slots sharing x (q/k/v, gate/up) read a group's x rows back to back
+  int simt_split_items;    // CUDA-core shrink: split each group's h_in into n_kc items (partials + a
+                           // deterministic last-arriver sum) when groups * tasks < this (0: never)
+  int tc_flags;            // L2 policies (env LORA_TCE_FLAGS): tcgen05 expand bit 0 Bt evict_last (else
+                           // evict_first), bit 1 y loads evict_first, bit 2 y stores evict_first; CUDA-core
+                           // kernels bit 3 expand B evict_last, bit 4 shrink A evict_last (else evict_first)
   Placement pl;            // adapter placement (unit = pl.local_index(a)*E + e)
   const int32_t* cache;    // resident-cache mode: unit = cache[a]*E + e (nullptr: placement)
   const float* scale;      // [n_adapters] s_a

@@ -171,6 +171,9 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (const char* e = std::getenv("LORA_TCE_FLAGS")) s->tc_flags = std::atoi(e);
   if (const char* e = std::getenv("LORA_TC_PAIR")) s->tc_pair = std::atoi(e) != 0;
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
+  s->simt_split_items = 2 * 2 * s->sm_count;  // fewer whole-K items than 2 per CUDA-core CTA: split K
+  if (const char* e = std::getenv("LORA_TC_MIN_ROWS")) s->tc_min_rows = std::atoi(e);
+  if (const char* e = std::getenv("LORA_SIMT_SPLIT")) s->simt_split_items = std::atoi(e);
   if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -563,7 +566,8 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
             cudaMalloc(&d.vpart, sizeof(float) * (size_t)s->total_kc * max_rows * s->r) == cudaSuccess &&
             cudaMalloc(&d.vbf, sizeof(uint16_t) * s->slots.size() * (size_t)max_rows * s->r) == cudaSuccess &&
             cudaMalloc(&d.wctr, sizeof(unsigned long long) * kWorkSlots) == cudaSuccess &&
-            cudaMalloc(&d.wdone, sizeof(unsigned int) * kWorkSlots) == cudaSuccess;
+            cudaMalloc(&d.wdone, sizeof(unsigned int) * kWorkSlots) == cudaSuccess &&
+            cudaMalloc(&d.gcnt, sizeof(unsigned int) * kMaxTasks * (size_t)max_rows) == cudaSuccess;
   if (ok) {  // multi-CTA segmenter scratch (used for T >= kSegMultiMin)
     const size_t cap = (size_t)(max_rows + 4095) / 4096 * 4096;  // whole CTAs of rows
     ok = cudaMalloc(&d.lsort, sizeof(uint32_t) * cap) == cudaSuccess &&
@@ -580,6 +584,7 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
   cudaMemset(d.counts, 0, sizeof(int32_t) * kCntWords);
   cudaMemset(d.wctr, 0, sizeof(unsigned long long) * kWorkSlots);
   cudaMemset(d.wdone, 0, sizeof(unsigned int) * kWorkSlots);
+  cudaMemset(d.gcnt, 0, sizeof(unsigned int) * kMaxTasks * (size_t)max_rows);
   cudaMemset(d.seg_off, 0, sizeof(int32_t) * (max_rows + 1));
   *out = p;
   return LORA_OK;
@@ -597,6 +602,7 @@ void plan_destroy_impl(lora_plan* p) {
   cudaFree(p->dev.vbf);
   cudaFree(p->dev.wctr);
   cudaFree(p->dev.wdone);
+  cudaFree(p->dev.gcnt);
   cudaFree(p->dev.lsort);
   cudaFree(p->dev.lrank);
   cudaFree(p->dev.hist);
@@ -620,6 +626,7 @@ lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapt
   SegParams sp;
   sp.small_max = s->small_seg_max < 0 ? kMaxPlanRows : s->small_seg_max;
   sp.tc_enabled = tc_enabled(s) ? 1 : 0;
+  sp.tc_min_rows = s->tc_min_rows;
   sp.tile_rows = kTileRows;
   CK(s, cudaSetDevice(s->device));
   const int pi = prof_start(s, st);
@@ -714,6 +721,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     args.y_store = store;
     args.tc_cap_k = s->concurrent_tc ? s->tc_cap_k : 0;
     args.tc_flags = s->tc_flags;
+    args.simt_split_items = s->simt_split_items;
     std::memset(args.tc_pair, -1, sizeof(args.tc_pair));  // (set per tcgen05 shrink launch below)
     args.pl = placement(s);
     args.cache = s->d_cache;
@@ -781,6 +789,15 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
         ci2 += sargs.t[i].n_ci;
       }
       fill_task_tables(sargs);
+      // runs of consecutive tasks reading one x (q/k/v of a layer, gate/up):
+      // their items interleave group by group.  (Runs of all equal-h_in
+      // tasks measured slower on Llama decode, 229 -> 248 us: a hot unit's
+      // groups then lie 128 items apart and its A is re-read from DRAM.)
+      sargs.n_cls = 0;
+      for (int i = 0; i < nb; ++i)
+        if (i == 0 || sargs.t[i].x != sargs.t[i - 1].x || sargs.xreg[i] != sargs.xreg[i - 1])
+          sargs.cls_first[sargs.n_cls++] = (int16_t)i;
+      sargs.cls_first[sargs.n_cls] = (int16_t)nb;
     }
     if (tc && s->tc_ci_max > 0 && (p->T_hint > 0 ? p->T_hint : p->T) >= kTcWideKRows) {
       // large batches: tcgen05 expand items of up to tc_ci_max columns of one

@@ -375,10 +375,20 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   // 4. work lists: CUDA-core groups (<= kGroupRows rows) and tcgen05 tiles (<= sp.tile_rows)
   const int schunk = (S + kSegThreads - 1) / kSegThreads;
   const int s0 = min(tid * schunk, S), s1 = min(s0 + schunk, S);
+  // the tcgen05 chain only pays off with enough rows in large segments
+  // (a handful of tiles run latency-bound on a few SMs): else all groups
+  int big = 0;
+  for (int s = s0; s < s1; ++s) {
+    const int size = segoff_s[s + 1] - segoff_s[s];
+    if (size > sp.small_max) big += size;
+  }
+  int BIG;
+  (void)block_exclusive_scan(big, scan_tmp, &BIG);
+  const bool use_tc = sp.tc_enabled && BIG >= sp.tc_min_rows;
   int ng = 0, nt = 0;
   for (int s = s0; s < s1; ++s) {
     const int size = segoff_s[s + 1] - segoff_s[s];
-    if (sp.tc_enabled && size > sp.small_max)
+    if (use_tc && size > sp.small_max)
       nt += (size + sp.tile_rows - 1) / sp.tile_rows;
     else
       ng += (size + kGroupRows - 1) / kGroupRows;
@@ -388,7 +398,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   int t = block_exclusive_scan(nt, scan_tmp, &NT);
   for (int s = s0; s < s1; ++s) {
     const int b = segoff_s[s], size = segoff_s[s + 1] - b, key = key_at(b);
-    const bool tc = sp.tc_enabled && size > sp.small_max;
+    const bool tc = use_tc && size > sp.small_max;
     const int cap = tc ? sp.tile_rows : kGroupRows;
     const int n = (size + cap - 1) / cap;
     // near-equal split: the first (size % n) pieces get one extra row
@@ -581,12 +591,20 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   // segments = keys with rows, in key order; work lists as in the one-CTA path
   const int kchunk = (K + kSegThreads - 1) / kSegThreads;
   const int k0 = min(tid * kchunk, K), k1 = min(k0 + kchunk, K);
+  int big = 0;
+  for (int k = k0; k < k1; ++k) {
+    const int size = kstart[pad32(k + 1)] - kstart[pad32(k)];
+    if (size > sp.small_max) big += size;
+  }
+  int BIG;
+  (void)block_exclusive_scan(big, scan_tmp, &BIG);
+  const bool use_tc = sp.tc_enabled && BIG >= sp.tc_min_rows;  // (as in the one-CTA path)
   int heads = 0, ng = 0, nt = 0;
   for (int k = k0; k < k1; ++k) {
     const int size = kstart[pad32(k + 1)] - kstart[pad32(k)];
     if (size == 0) continue;
     ++heads;
-    if (sp.tc_enabled && size > sp.small_max)
+    if (use_tc && size > sp.small_max)
       nt += (size + sp.tile_rows - 1) / sp.tile_rows;
     else
       ng += (size + kGroupRows - 1) / kGroupRows;
@@ -600,7 +618,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     if (size == 0) continue;
     pd.seg_off[seg] = b;
     pd.seg_key[seg] = k;
-    const bool tc = sp.tc_enabled && size > sp.small_max;
+    const bool tc = use_tc && size > sp.small_max;
     const int cap = tc ? sp.tile_rows : kGroupRows;
     const int np = (size + cap - 1) / cap;
     const int base = size / np, extra = size % np;

@@ -164,14 +164,49 @@ LORA_DEVINL float2 dot8_acc2(float2 acc, const float* a, const float* b) {
 // ---------------------------------------------------------------------------
 // shrink: item = (task, group); v[row][k] = sum_j x[perm[row]][j] A_u[j][k]
 // ---------------------------------------------------------------------------
+// K-split (small batches, see simt_shrink_kernel): the item covers k-chunk kc
+// (KI of h_in, n_st stages) and writes a partial sum into region kc; the last
+// of the group's n_kc items to arrive sums the partials in kc order (the same
+// order whichever CTA is last, so the result is deterministic) into region 0.
+struct SplitCtx {
+  int n_st;               // stages of this item
+  int kc, n_kc;           // chunk of this item, chunks of the group (n_kc == 1: whole K, no partials)
+  long long kc_stride;    // floats between two kc regions (max_rows * R)
+  unsigned int* cnt;      // arrivals of the group's items
+  int* s_last;            // smem flag
+};
+
+template <int NCT>
+LORA_DEVINL void split_finish(float* vbase, int n, const SplitCtx& sc) {
+  __threadfence();                 // this thread's partial writes, before the arrival
+  named_bar_sync(1, NCT);
+  if (threadIdx.x == 0) {
+    const unsigned int old = atomicAdd(sc.cnt, 1u);
+    const int last = old == (unsigned int)(sc.n_kc - 1);
+    if (last) {
+      *sc.cnt = 0u;                // self-resetting for the next launch
+      __threadfence();
+    }
+    *sc.s_last = last;
+  }
+  named_bar_sync(1, NCT);
+  if (*sc.s_last) {
+    for (int idx = threadIdx.x; idx < n; idx += NCT) {
+      float s = 0.f;
+      for (int kc = 0; kc < sc.n_kc; ++kc) s += __ldcg(vbase + kc * sc.kc_stride + idx);
+      vbase[idx] = s;
+    }
+  }
+}
+
 template <int R, int NR>
 LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
                              uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base,
-                             int lane) {
+                             int lane, const SplitCtx& sc) {
   using C = SimtCfg<R>;
   const int ct = threadIdx.x;
   const int kl = ct % C::KL, jg = ct / C::KL;
-  const int n_st = t.h_in / t.SJ;
+  const int n_st = sc.n_st;
   const int nchunk = t.SJ >> 3;  // 16-byte chunks along j per stage
   float2 acc[C::KPL][NR];
 #pragma unroll
@@ -219,8 +254,9 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
     float s = 0.f;
 #pragma unroll 4
     for (int q = 0; q < C::NJG; ++q) s += red[q * NR * R + idx];
-    vp[idx] = s;
+    vp[sc.kc * sc.kc_stride + idx] = s;
   }
+  if (sc.n_kc > 1) split_finish<C::NCT>(vp, NR * R, sc);
 }
 
 // r <= 32: thread (kl, jg) accumulates k = 4 kl .. 4 kl + 3 for NR rows over
@@ -228,12 +264,13 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
 // same k are reduced with xor shuffles, then the warps through shared memory.
 template <int R, int NR>
 LORA_DEVINL void shrink_item_small(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
-                                   uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane) {
+                                   uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane,
+                                   const SplitCtx& sc) {
   using C = SimtCfg<R>;
   static_assert(C::KPL == 4, "four k per lane");
   const int ct = threadIdx.x, warp = ct >> 5;
   const int kl = ct % C::KL, jg = ct / C::KL;
-  const int n_st = t.h_in / t.SJ;
+  const int n_st = sc.n_st;
   const int nchunk = t.SJ >> 3;
   float2 acc[NR][2];
 #pragma unroll
@@ -318,23 +355,25 @@ LORA_DEVINL void shrink_item_small(uint8_t* smem, uint64_t* full, uint64_t* empt
     float s = 0.f;
 #pragma unroll
     for (int w = 0; w < C::NWC; ++w) s += red[w * NR * R + idx];
-    vp[idx] = s;
+    vp[sc.kc * sc.kc_stride + idx] = s;
   }
+  if (sc.n_kc > 1) split_finish<C::NCT>(vp, NR * R, sc);
 }
 
 template <int R, int NR>
 LORA_DEVINL void shrink_dispatch(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
-                                 uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane) {
+                                 uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane,
+                                 const SplitCtx& sc) {
   if constexpr (SimtCfg<R>::SMALL_K)
-    shrink_item_small<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane);
+    shrink_item_small<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
   else
-    shrink_item<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane);
+    shrink_item<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
 }
 
 // a shrink item as resolved by the resolver warp: group and x row offsets
 struct ShrinkRes {
   long long it;  // -1: end of the stream
-  int ti, pad;
+  int ti, kc;    // task, k-chunk (K-split; 0 otherwise)
   int4 g;
   long long xrow[kGroupRows];
 };
@@ -372,17 +411,46 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
   pdl_launch_dependents();  // the expand may launch as SMs free up
 
   const int n_groups = pd.counts[kCntGroups];
-  const long long n_items = (long long)n_groups * args.n_tasks;
+  // Small batches have few (task, group) items, and one item streams a whole
+  // unit's A through one CTA (1.8 MB for Mixtral down, ~130 us): with fewer
+  // than simt_split_items items the groups' h_in is split into the slots' n_kc
+  // chunks of KI (items = groups x sum n_kc), partial sums + last-arriver sum.
+  const bool split = (long long)n_groups * args.n_tasks < args.simt_split_items;
+  const long long n_items = (long long)n_groups * (split ? args.total_kc : args.n_tasks);
   const int warp = warp_id(), lane = lane_id();
+  __shared__ int s_last;
+  // item -> (task, k-chunk, group index)
+  auto decode = [&](long long it, int& ti, int& kc, int& gi) {
+    if (split) {
+      const int q = (int)(it / n_groups);
+      gi = (int)(it - (long long)q * n_groups);
+      ti = find_task_kc(args, q);
+      kc = q - args.t[ti].kc_base;
+      return;
+    }
+    // runs of tasks with one h_in, longest first; inside a run group-major,
+    // so the tasks that share x (q/k/v of a layer, gate/up) read a group's
+    // x rows back to back (L2 hits instead of DRAM re-reads)
+    int c = 0;
+    while (c + 1 < args.n_cls && (long long)args.cls_first[c + 1] * n_groups <= it) ++c;
+    const int first = args.cls_first[c], nt = args.cls_first[c + 1] - first;
+    const long long local = it - (long long)first * n_groups;
+    gi = (int)(local / nt);
+    ti = first + (int)(local - (long long)gi * nt);
+    kc = 0;
+  };
 
   // claim the next item and resolve its group and x rows: x row r of the group
   // is t.x + xrow[r] (REMOTE: xrow[r] is relative to t.x, pointing into a
-  // source's send buffer)
-  auto resolve = [&](long long& it, int& ti, int4& g, long long* xrow) {
+  // source's registered x)
+  auto resolve = [&](long long& it, int& ti, int& kc, int4& g, long long* xrow) {
     it = (long long)atomicAdd(pd.wctr + kWqSimtShrink, 1ull);
     if (it >= n_items) it = -1;
-    ti = it < 0 ? 0 : (int)(it / n_groups);
-    g = it < 0 ? make_int4(0, 0, 0, 0) : pd.groups[(int)(it - (long long)ti * n_groups)];
+    int gi = 0;
+    ti = 0;
+    kc = 0;
+    if (it >= 0) decode(it, ti, kc, gi);
+    g = it < 0 ? make_int4(0, 0, 0, 0) : pd.groups[gi];
     const SlotTask& t = args.t[ti];
 #pragma unroll
     for (int r = 0; r < C::GR; ++r) {
@@ -399,14 +467,15 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
       QueuePos rp;
       for (;;) {
         long long it;
-        int ti;
+        int ti, kc;
         int4 g;
         long long xrow[C::GR];
-        resolve(it, ti, g, xrow);
+        resolve(it, ti, kc, g, xrow);
         mbar_wait(&rempty[rp.slot], rp.phase ^ 1);
         ShrinkRes& q = rres[rp.slot];
         q.it = it;
         q.ti = ti;
+        q.kc = kc;
         q.g = g;
 #pragma unroll
         for (int r = 0; r < C::GR; ++r) q.xrow[r] = xrow[r];
@@ -418,13 +487,13 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
   } else if (warp == C::NWC) {
     // ===================== producer =====================
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = (args.tc_flags & 16) ? policy_evict_last() : policy_evict_first();  // A (bit 4)
       int stage = 0;
       uint32_t phase = 0;
       QueuePos qp, rp;
       for (;;) {
         long long it;
-        int ti;
+        int ti, kc;
         int4 g;
         long long xrow[C::GR];
         if constexpr (C::SHRINK_RESOLVER) {
@@ -432,13 +501,14 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
           const ShrinkRes& q = rres[rp.slot];
           it = q.it;
           ti = q.ti;
+          kc = q.kc;
           g = q.g;
 #pragma unroll
           for (int r = 0; r < C::GR; ++r) xrow[r] = q.xrow[r];
           mbar_arrive(&rempty[rp.slot]);
           rp.advance(C::kSRQ);
         } else {
-          resolve(it, ti, g, xrow);
+          resolve(it, ti, kc, g, xrow);
         }
         // the item and its group go to the consumers through the queue
         mbar_wait(&wq.empty[qp.slot], qp.phase ^ 1);
@@ -449,8 +519,9 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
         if (it < 0) break;
         const SlotTask& t = args.t[ti];
         const long long unit = store_unit(g.z, t.E, args.pl, args.cache);
-        const uint16_t* abase = t.At + unit * (long long)t.h_in * R;
-        const int n_st = t.h_in / t.SJ;
+        const long long j0 = split ? (long long)kc * t.KI : 0;   // first j of this item
+        const uint16_t* abase = t.At + (unit * (long long)t.h_in + j0) * R;
+        const int n_st = (split ? t.KI : t.h_in) / t.SJ;
         const uint32_t a_bytes = (uint32_t)R * t.SJ * 2, x_bytes = (uint32_t)t.SJ * 2;
         for (int st = 0; st < n_st; ++st) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -458,7 +529,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
           uint8_t* sX = sA + C::A_STAGE;
           mbar_arrive_expect_tx(&full[stage], a_bytes + x_bytes * g.y);
           bulk_g2s_hint(sA, abase + (long long)st * t.SJ * R, a_bytes, &full[stage], pol);
-          const long long jofs = (long long)st * t.SJ;
+          const long long jofs = j0 + (long long)st * t.SJ;
 #pragma unroll
           for (int r = 0; r < C::GR; ++r)
             if (r < g.y) bulk_g2s(sX + r * x_bytes, t.x + xrow[r] + jofs, x_bytes, &full[stage]);
@@ -482,18 +553,26 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
       if (lane == 0) mbar_arrive(&wq.empty[qp.slot]);
       qp.advance(kQD);
       if (it < 0) break;
-      const int ti = (int)(it / n_groups);
+      int ti, kc, gi;
+      decode(it, ti, kc, gi);
       const SlotTask& t = args.t[ti];
       float* vb = pd.vpart + t.vpart_off;
+      SplitCtx sc;
+      sc.n_st = (split ? t.KI : t.h_in) / t.SJ;
+      sc.kc = kc;
+      sc.n_kc = split ? t.n_kc : 1;
+      sc.kc_stride = (long long)pd.max_rows * R;
+      sc.cnt = pd.gcnt + (long long)ti * pd.max_rows + gi;
+      sc.s_last = &s_last;
       switch (g.y) {
-        case 1: shrink_dispatch<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 2: shrink_dispatch<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 3: shrink_dispatch<R, 3>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 4: shrink_dispatch<R, 4>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 5: shrink_dispatch<R, 5>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 6: shrink_dispatch<R, 6>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        case 7: shrink_dispatch<R, 7>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
-        default: shrink_dispatch<R, 8>(smem, full, empty, red, stage, phase, t, g, vb, lane); break;
+        case 1: shrink_dispatch<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+        case 2: shrink_dispatch<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+        case 3: shrink_dispatch<R, 3>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+        case 4: shrink_dispatch<R, 4>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+        case 5: shrink_dispatch<R, 5>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+        case 6: shrink_dispatch<R, 6>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+        case 7: shrink_dispatch<R, 7>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+        default: shrink_dispatch<R, 8>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
       }
     }
   }
@@ -1161,7 +1240,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::TILE_THREADS, 2)
     // ===================== producer: B rows, v rows, y chunks of resolved items =====================
     if (lane == 0) {
       const bool load_y = args.y_store == 0 && !args.y_fp32;
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = (args.tc_flags & 8) ? policy_evict_last() : policy_evict_first();  // B (bit 3)
       int stage = 0;
       uint32_t phase = 0;
       QueuePos qp, rp;

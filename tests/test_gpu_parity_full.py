@@ -449,3 +449,28 @@ def test_cross_slot_aliasing_rejected(B):
         B.lora_plan_destroy(p)
     finally:
         B.lora_server_destroy(s)
+
+
+def test_tc_min_rows_heuristic(B, monkeypatch):
+    """Default LORA_TC_MIN_ROWS (256): with fewer rows than that in large
+    segments every segment takes the CUDA-core route (no tcgen05 tiles); with
+    more, the large segments go to tcgen05.  Results within the oracle's
+    tolerance either way."""
+    monkeypatch.delenv("LORA_TC_MIN_ROWS", raising=False)
+    cfg = _mid_cfg(T=400)
+    s = U.make_server(B, cfg)
+    try:
+        for n_big, want_tiles in ((100, False), (300, True)):
+            T = 400
+            a = np.arange(T, dtype=np.int32) % cfg.n_adapters   # small segments
+            a[:n_big] = 5
+            e = (np.arange(T, dtype=np.int32) // cfg.n_adapters) % 4   # 96 keys of <= 5 rows
+            e[:n_big] = 1
+            b = li.Batch(a, e, T, 1)
+            c2 = dataclasses.replace(cfg, top_k=1, n_tokens=T)
+            ys, stats = _run(B, s, c2, b, [0, 1], "random")
+            assert (stats[3] > 0) == want_tiles, (n_big, stats)
+            for i in range(2):
+                U.assert_parity(ys[i], orc.apply_slot(c2, i, b), f"min-rows {n_big} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
