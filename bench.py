@@ -162,6 +162,17 @@ def oracle_time(prepared, n_threads: int = 0):
     return time.perf_counter() - t0
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (lscpu / /proc/cpuinfo), for the oracle's timing."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(cfg, batch, slots, budget_s=10.0):
     """Grow the token sample until one oracle pass costs ~budget_s (or the batch ends)."""
     from oracle import oracle as orc
@@ -178,7 +189,7 @@ def cpu_baseline(cfg, batch, slots, budget_s=10.0):
     # the same oracle on one thread (--threads 1 and --threads nproc)
     n1 = max(1, min(n, int(n * 2.0 / max(dt * orc.max_threads(), 1e-3))))
     dt1 = oracle_time(prep if n1 == n else oracle_sample(cfg, batch, slots, n1), n_threads=1)
-    return {"value": n / dt, "unit": UNIT, "cores": orc.max_threads(), "kind": "oracle",
+    return {"value": n / dt, "unit": UNIT, "cores": orc.max_threads(), "kind": "oracle", "cpu": cpu_model(),
             "sample": f"first {n} of {batch.n_tokens} tokens ({n * batch.top_k} rows) of the {cfg.name} batch, "
                       f"{len(slots)} slots; plain-C fp64 oracle, OpenMP over rows; input generation excluded; "
                       f"one pass = {dt:.2f} s",
@@ -204,13 +215,16 @@ def run_reference(args, cfg, batch, slots):
         oracle_time(prep)
     times = [oracle_time(prep) for _ in range(args.steps)]
     ms = 1e3 * float(np.mean(times))
+    ms_median, ms_min = 1e3 * float(np.median(times)), 1e3 * float(np.min(times))
     value = n / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "ms_median": ms_median, "ms_min": ms_min,
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg.name, "global_batch": cfg.n_tokens, "sample_tokens": n,
                        "rows": n * batch.top_k, "parallelism": "cpu"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc.max_threads(), "kind": "oracle",
+                             "cpu": cpu_model(),
                              "sample": f"first {n} of {cfg.n_tokens} tokens of {cfg.name}, {len(slots)} slots, "
                                        f"input generation excluded"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -157,9 +157,6 @@ struct MultiArgs {
   int y_store;             // 0: y += delta; sharded delta mode stores s*(xA)B into y: 1 as fp32, 2 as bf16;
                            // 3 (push): adds it into the source's y row (red.add over NVLink)
   int tc_cap_k;            // > 0: tcgen05 kernels use at most max(8, tiles * tc_cap_k) CTAs (rest exit at once)
-  int n_cls;               // CUDA-core shrink item order: runs of consecutive tasks with one h_in
-  int16_t cls_first[kMaxTasks + 1];  // (the launch's tasks sorted by h_in): items of a run are group-major,
-                                     // so slots sharing x (q/k/v, gate/up) read a group's x rows back to back
   int simt_split_items;    // CUDA-core shrink: split each group's h_in into n_kc items (partials + a
                            // deterministic last-arriver sum) when groups * tasks < this (0: never)
   int tc_flags;            // L2 policies (env LORA_TCE_FLAGS): tcgen05 expand bit 0 Bt evict_last (else

@@ -283,10 +283,14 @@ lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int ran
 namespace lora {
 // Programmatic dependent launch of the shrink / expand / v-reduce kernels
 // (prologues and the expand's first weight copies overlapping the previous
-// kernel's tail).  Measured neutral to slightly negative on one B200 (early
-// CTAs of the other chain compete for SMs), so opt-in: LORA_PDL=1.
+// kernel's tail).  Measured in round 2 with the paired tcgen05 shrink and the
+// K-split CUDA-core shrink: prefill 0.530 -> 0.526 ms, Llama decode 0.412 ->
+// 0.407 ms, config 5 unchanged, so on by default (LORA_PDL=0 disables).
 bool pdl_enabled() {
-  static const bool on = env_flag("LORA_PDL");
+  static const bool on = [] {
+    const char* v = std::getenv("LORA_PDL");
+    return !(v && v[0] == '0');
+  }();
   return on;
 }
 }  // namespace lora
@@ -789,15 +793,6 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
         ci2 += sargs.t[i].n_ci;
       }
       fill_task_tables(sargs);
-      // runs of consecutive tasks reading one x (q/k/v of a layer, gate/up):
-      // their items interleave group by group.  (Runs of all equal-h_in
-      // tasks measured slower on Llama decode, 229 -> 248 us: a hot unit's
-      // groups then lie 128 items apart and its A is re-read from DRAM.)
-      sargs.n_cls = 0;
-      for (int i = 0; i < nb; ++i)
-        if (i == 0 || sargs.t[i].x != sargs.t[i - 1].x || sargs.xreg[i] != sargs.xreg[i - 1])
-          sargs.cls_first[sargs.n_cls++] = (int16_t)i;
-      sargs.cls_first[sargs.n_cls] = (int16_t)nb;
     }
     if (tc && s->tc_ci_max > 0 && (p->T_hint > 0 ? p->T_hint : p->T) >= kTcWideKRows) {
       // large batches: tcgen05 expand items of up to tc_ci_max columns of one

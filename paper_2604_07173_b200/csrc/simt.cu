@@ -63,8 +63,11 @@ struct SimtCfg {
   // per-stage overhead; measured Llama shrink 233 -> 224 us)
   static constexpr int SJ_MAX = (R == 16 ? LORA_SMALLR_A_STAGE : 16384) / (2 * R);
   static constexpr int A_STAGE = R * SJ_MAX * 2;
-  static constexpr int X_STAGE = GR * SJ_MAX * 2;
-  static constexpr int S_STAGE = A_STAGE + X_STAGE;
+  // r <= 32 (MMA consumers): x rows padded by 16 bytes so the ldmatrix row
+  // addresses of one 8x8 matrix fall in distinct banks
+  static constexpr int X_PITCH = SMALL_K ? SJ_MAX * 2 + 16 : SJ_MAX * 2;
+  static constexpr int X_STAGE = GR * X_PITCH;
+  static constexpr int S_STAGE = (A_STAGE + X_STAGE + 1023) / 1024 * 1024;
   static constexpr int RED_BYTES = (SMALL_K ? NWC : NJG) * GR * R * 4;
   static constexpr int NST_RAW = (SMEM_BUDGET - RED_BYTES) / S_STAGE;
   static constexpr int NST = NST_RAW > 8 ? 8 : (NST_RAW < 2 ? 2 : NST_RAW);
@@ -360,12 +363,106 @@ LORA_DEVINL void shrink_item_small(uint8_t* smem, uint64_t* full, uint64_t* empt
   if (sc.n_kc > 1) split_finish<C::NCT>(vp, NR * R, sc);
 }
 
+// ---------------------------------------------------------------------------
+// r <= 32: the shrink and expand on the legacy tensor path (mma.sync
+// m16n8k16 bf16 -> fp32, fed by ldmatrix from the pre-swizzled stages).  At
+// small r the CUDA-core FMA formulation is instruction-bound (ncu: 60 % issue
+// active, math-pipe throttle, bf16 unpacking per weight element); one MMA
+// covers 16 rank values x 8 group rows x 16 j with ~3 instructions per 512 B
+// of weights, so the kernels become bound by their byte streams again.
+// ---------------------------------------------------------------------------
+LORA_DEVINL void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+LORA_DEVINL void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+// D[16 x 8] += A[16 x 16] . B[16 x 8]  (A row-major, B "col": rows of B^T)
+LORA_DEVINL void mma16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Shrink item, r <= 32: D[k x n] += A_u^T[k x 16 j] . x^T[16 j x n] per
+// 16-j step, M = 16 rank values (r = 32: two M tiles; r = 8: rows 8-15
+// duplicate 0-7, ignored), N = the group's 8 rows (rows >= NR hold stale smem:
+// their columns are never read), steps dealt round-robin to the 8 consumer
+// warps; per-warp partials reduced through shared memory as before.
+template <int R>
+LORA_DEVINL void shrink_item_mma(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
+                                 uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane,
+                                 const SplitCtx& sc) {
+  using C = SimtCfg<R>;
+  constexpr int MT = (R + 15) / 16;
+  const int warp = threadIdx.x >> 5;
+  const int nsteps = t.SJ >> 4;  // 16-j steps per stage
+  float acc[MT][4];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+  // this lane's ldmatrix rows: A (weights) row k of matrix (lane >> 3), x row lane & 7
+  const int ka = (lane & 7) + ((lane >> 3) & 1) * 8;  // 0..15
+  const int ca = lane >> 4;                           // chunk offset 0 / 1
+  const int xn = lane & 7, xc = (lane >> 3) & 1;
+  for (int st = 0; st < sc.n_st; ++st) {
+    mbar_wait(&full[stage], phase);
+    const uint32_t a_s = smem_u32(smem + stage * C::S_STAGE);
+    const uint32_t x_s = a_s + C::A_STAGE;
+    for (int q = warp; q < nsteps; q += C::NWC) {
+      const int j0 = q << 4;
+      const int tile = j0 >> 6, c0 = (j0 & 63) >> 3;
+      uint32_t b0, b1;
+      ldsm_x2(x_s + xn * C::X_PITCH + ((j0 + xc * 8) << 1), b0, b1);
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int k = R >= 16 ? m * 16 + ka : (ka & 7);
+        const int ch = c0 + ca;
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(a_s + tile * (R * 128) + k * 128 + ((ch ^ (k & 7)) << 4), a0, a1, a2, a3);
+        mma16816(acc[m], a0, a1, a2, a3, b0, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == C::NST) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  // D fragment: acc[m][0..1] -> k = m*16 + lane/4, rows 2*(lane%4) + {0,1}; [2..3] -> k + 8
+  named_bar_sync(1, C::NCT);
+  float* rw = red + warp * (C::GR * R);
+  const int kq = lane >> 2, nq = (lane & 3) * 2;
+#pragma unroll
+  for (int m = 0; m < MT; ++m) {
+    rw[(nq + 0) * R + m * 16 + kq] = acc[m][0];
+    rw[(nq + 1) * R + m * 16 + kq] = acc[m][1];
+    if (R >= 16) {
+      rw[(nq + 0) * R + m * 16 + kq + 8] = acc[m][2];
+      rw[(nq + 1) * R + m * 16 + kq + 8] = acc[m][3];
+    }
+  }
+  named_bar_sync(1, C::NCT);
+  float* vp = vpart_base + (long long)g.x * R;
+  const int n_out = g.y * R;
+  for (int idx = threadIdx.x; idx < n_out; idx += C::NCT) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < C::NWC; ++w) s += red[w * (C::GR * R) + idx];
+    vp[sc.kc * sc.kc_stride + idx] = s;
+  }
+  if (sc.n_kc > 1) split_finish<C::NCT>(vp, n_out, sc);
+}
+
 template <int R, int NR>
 LORA_DEVINL void shrink_dispatch(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
                                  uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane,
                                  const SplitCtx& sc) {
   if constexpr (SimtCfg<R>::SMALL_K)
-    shrink_item_small<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
+    shrink_item_mma<R>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
   else
     shrink_item<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
 }
@@ -428,15 +525,13 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
       kc = q - args.t[ti].kc_base;
       return;
     }
-    // runs of tasks with one h_in, longest first; inside a run group-major,
-    // so the tasks that share x (q/k/v of a layer, gate/up) read a group's
-    // x rows back to back (L2 hits instead of DRAM re-reads)
-    int c = 0;
-    while (c + 1 < args.n_cls && (long long)args.cls_first[c + 1] * n_groups <= it) ++c;
-    const int first = args.cls_first[c], nt = args.cls_first[c + 1] - first;
-    const long long local = it - (long long)first * n_groups;
-    gi = (int)(local / nt);
-    ti = first + (int)(local - (long long)gi * nt);
+    // task-major: a slot's groups back to back, so the groups of one unit
+    // (segments > 8 rows) stream that unit's A at about the same time (L2
+    // hits).  Interleaving the slots that share x group by group measured
+    // slower (Llama decode shrink 229 -> 248 us by h_in runs, 286 us by x runs).
+    const int q = (int)(it / n_groups);
+    gi = (int)(it - (long long)q * n_groups);
+    ti = q;
     kc = 0;
   };
 
@@ -532,7 +627,9 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
           const long long jofs = j0 + (long long)st * t.SJ;
 #pragma unroll
           for (int r = 0; r < C::GR; ++r)
-            if (r < g.y) bulk_g2s(sX + r * x_bytes, t.x + xrow[r] + jofs, x_bytes, &full[stage]);
+            if (r < g.y)
+              bulk_g2s(sX + r * (C::SMALL_K ? (uint32_t)C::X_PITCH : x_bytes), t.x + xrow[r] + jofs, x_bytes,
+                       &full[stage]);
           if (++stage == C::NST) {
             stage = 0;
             phase ^= 1;
@@ -564,6 +661,10 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
       sc.kc_stride = (long long)pd.max_rows * R;
       sc.cnt = pd.gcnt + (long long)ti * pd.max_rows + gi;
       sc.s_last = &s_last;
+      if constexpr (C::SMALL_K) {  // MMA consumers: one code path for any group size
+        shrink_item_mma<R>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc);
+        continue;
+      }
       switch (g.y) {
         case 1: shrink_dispatch<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
         case 2: shrink_dispatch<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;

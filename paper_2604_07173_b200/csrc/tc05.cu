@@ -157,7 +157,7 @@ struct ShrinkCfgT {
 #define LORA_TCS_NST 4
 #endif
 #ifndef LORA_TCS_LAG
-#define LORA_TCS_LAG 2
+#define LORA_TCS_LAG 1  // cp.async groups left in flight per producer thread (measured: config 5 tc shrink 130 -> 118 us vs 2, prefill equal)
 #endif
 #ifndef LORA_TCSP_NST
 #define LORA_TCSP_NST 3

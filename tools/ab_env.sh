@@ -10,7 +10,7 @@ for w in $WS; do
       n=${v%%:*}; envs=${v#*:}
       f=gpurun_out/ab/${w}_${n}_$rep.json
       env ${envs//,/ } timeout 120 python bench.py --workload $w --steps 50 --warmup 5 --no-cpu-baseline \
-          --e2e-steps 0 > $f 2> ${f%.json}.err
+          --e2e-steps 0 --no-secondary > $f 2> ${f%.json}.err
       python - "$w" "$n" "$rep" $f <<'PY' >> gpurun_out/ab/summary.txt
 import json, sys
 w, n, rep, f = sys.argv[1:]

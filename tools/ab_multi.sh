@@ -9,7 +9,7 @@ for w in $WS; do
     for n in "$@"; do
       cp tools/ab/lib_$n.so paper_2604_07173_b200/liblora_server.so
       LORA_BINDING_LENIENT=1 timeout 120 python bench.py --workload $w --steps 50 --warmup 5 --no-cpu-baseline \
-          --e2e-steps 0 > gpurun_out/ab/${w}_${n}_$rep.json 2> gpurun_out/ab/${w}_${n}_$rep.err
+          --e2e-steps 0 --no-secondary > gpurun_out/ab/${w}_${n}_$rep.json 2> gpurun_out/ab/${w}_${n}_$rep.err
       python - "$w" "$n" "$rep" gpurun_out/ab/${w}_${n}_$rep.json <<'PY' >> gpurun_out/ab/summary.txt
 import json, sys
 w, n, rep, f = sys.argv[1:]
