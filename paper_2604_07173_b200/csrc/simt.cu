@@ -262,114 +262,13 @@ LORA_DEVINL void shrink_item(uint8_t* smem, uint64_t* full, uint64_t* empty, flo
   if (sc.n_kc > 1) split_finish<C::NCT>(vp, NR * R, sc);
 }
 
-// r <= 32: thread (kl, jg) accumulates k = 4 kl .. 4 kl + 3 for NR rows over
-// its j-chunks; acc[r][p] = (k0, k1) of pair p.  Lanes of a warp holding the
-// same k are reduced with xor shuffles, then the warps through shared memory.
-template <int R, int NR>
-LORA_DEVINL void shrink_item_small(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
-                                   uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane,
-                                   const SplitCtx& sc) {
-  using C = SimtCfg<R>;
-  static_assert(C::KPL == 4, "four k per lane");
-  const int ct = threadIdx.x, warp = ct >> 5;
-  const int kl = ct % C::KL, jg = ct / C::KL;
-  const int n_st = sc.n_st;
-  const int nchunk = t.SJ >> 3;
-  float2 acc[NR][2];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
-
-  for (int st = 0; st < n_st; ++st) {
-    mbar_wait(&full[stage], phase);
-    const uint32_t a_s = smem_u32(smem + stage * C::S_STAGE);
-    const uint32_t x_s = a_s + C::A_STAGE;
-    for (int c = jg; c < nchunk; c += C::NJG) {
-      const int tile = c >> 3, q = c & 7;
-      // A[j][k] of chunk c (8 j) for this lane's 4 k (raw), widened per half of
-      // 4 j as k pairs; x read per half (8 bytes = 4 j per row)
-      uint4 u[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = kl * 4 + kk;
-        u[kk] = lds128(a_s + tile * (R * 128) + k * 128 + ((q ^ (k & 7)) << 4));
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float2 w[4][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const uint32_t a0 = h ? (i ? u[0].w : u[0].z) : (i ? u[0].y : u[0].x);
-          const uint32_t a1 = h ? (i ? u[1].w : u[1].z) : (i ? u[1].y : u[1].x);
-          const uint32_t a2 = h ? (i ? u[2].w : u[2].z) : (i ? u[2].y : u[2].x);
-          const uint32_t a3 = h ? (i ? u[3].w : u[3].z) : (i ? u[3].y : u[3].x);
-          w[2 * i][0] = make_float2(bf16lo(a0), bf16lo(a1));
-          w[2 * i][1] = make_float2(bf16lo(a2), bf16lo(a3));
-          w[2 * i + 1][0] = make_float2(bf16hi(a0), bf16hi(a1));
-          w[2 * i + 1][1] = make_float2(bf16hi(a2), bf16hi(a3));
-        }
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          uint32_t x0, x1;
-          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(x_s + r * (t.SJ * 2) + (c << 4) + h * 8));
-          const float xf[4] = {bf16lo(x0), bf16hi(x0), bf16lo(x1), bf16hi(x1)};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            acc[r][0] = __ffma2_rn(make_float2(xf[j], xf[j]), w[j][0], acc[r][0]);
-            acc[r][1] = __ffma2_rn(make_float2(xf[j], xf[j]), w[j][1], acc[r][1]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == C::NST) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-
-  // lanes kl + KL * m (m = 0 .. 32/KL-1) hold the same k: xor-reduce over m
-#pragma unroll
-  for (int r = 0; r < NR; ++r)
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-      float2 v = acc[r][p];
-#pragma unroll
-      for (int o = C::KL; o < 32; o <<= 1) {
-        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
-      }
-      acc[r][p] = v;
-    }
-  named_bar_sync(1, C::NCT);
-  if (lane < C::KL) {
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-#pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        float* d = red + (warp * NR + r) * R + kl * 4 + 2 * p;
-        d[0] = acc[r][p].x;
-        d[1] = acc[r][p].y;
-      }
-  }
-  named_bar_sync(1, C::NCT);
-  float* vp = vpart_base + (long long)g.x * R;
-  for (int idx = ct; idx < NR * R; idx += C::NCT) {
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < C::NWC; ++w) s += red[w * NR * R + idx];
-    vp[sc.kc * sc.kc_stride + idx] = s;
-  }
-  if (sc.n_kc > 1) split_finish<C::NCT>(vp, NR * R, sc);
-}
-
 // ---------------------------------------------------------------------------
-// r <= 32: the shrink and expand on the legacy tensor path (mma.sync
-// m16n8k16 bf16 -> fp32, fed by ldmatrix from the pre-swizzled stages).  At
-// small r the CUDA-core FMA formulation is instruction-bound (ncu: 60 % issue
-// active, math-pipe throttle, bf16 unpacking per weight element); one MMA
-// covers 16 rank values x 8 group rows x 16 j with ~3 instructions per 512 B
-// of weights, so the kernels become bound by their byte streams again.
+// r <= 32: the shrink on the legacy tensor path (mma.sync m16n8k16 bf16 ->
+// fp32, fed by ldmatrix from the pre-swizzled stages).  At small r the
+// CUDA-core FMA formulation was instruction-bound (ncu on Llama decode: 60 %
+// issue active, math-pipe throttle, bf16 unpacking per weight element); one
+// MMA covers 16 rank values x 8 group rows x 16 j with ~3 instructions per
+// 512 B of weights (measured: Llama decode shrink 227 -> 195 us).
 // ---------------------------------------------------------------------------
 LORA_DEVINL void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -461,10 +360,7 @@ template <int R, int NR>
 LORA_DEVINL void shrink_dispatch(uint8_t* smem, uint64_t* full, uint64_t* empty, float* red, int& stage,
                                  uint32_t& phase, const SlotTask& t, const int4 g, float* vpart_base, int lane,
                                  const SplitCtx& sc) {
-  if constexpr (SimtCfg<R>::SMALL_K)
-    shrink_item_mma<R>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
-  else
-    shrink_item<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
+  shrink_item<R, NR>(smem, full, empty, red, stage, phase, t, g, vpart_base, lane, sc);
 }
 
 // a shrink item as resolved by the resolver warp: group and x row offsets
@@ -663,8 +559,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
       sc.s_last = &s_last;
       if constexpr (C::SMALL_K) {  // MMA consumers: one code path for any group size
         shrink_item_mma<R>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc);
-        continue;
-      }
+      } else {
       switch (g.y) {
         case 1: shrink_dispatch<R, 1>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
         case 2: shrink_dispatch<R, 2>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
@@ -674,6 +569,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
         case 6: shrink_dispatch<R, 6>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
         case 7: shrink_dispatch<R, 7>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
         default: shrink_dispatch<R, 8>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc); break;
+      }
       }
     }
   }
@@ -786,7 +682,8 @@ LORA_DEVINL void expand_stage1(uint32_t b_s, uint32_t v_s, int cr, const ExpandP
 }
 
 // r <= 32: CPT columns per thread (c = ct + i*NCT), FFMA2 over pairs of
-// columns.  The B chunk of a column pair is widened to fp32 once and reused
+// columns.  (Adjacent pairs (2 ct, 2 ct + 1) with one 32-bit smem
+// read-modify-write of the y tile per row measured equal on Llama decode.)  The B chunk of a column pair is widened to fp32 once and reused
 // for every row of the group.
 template <int R, int NR, int CPT, int NCT, int M>
 LORA_DEVINL void expand_stage_pairs(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
@@ -1266,6 +1163,10 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
       const uint32_t b_s = smem_u32(smem + stage * C::T_STAGE);
       const uint32_t v_s = b_s + C::TV_OFF;
       const uint32_t yt = b_s + C::TY_OFF;
+      // (an mma.sync formulation of this stage, D[16 c x 8 n] = Bt . v^T with a
+      // bf16 hi/lo split of v, measured slower: Llama decode expand 180 ->
+      // 223 us -- the stage's cost is the per-element y update, not the dot
+      // products -- so the expand keeps the FFMA2 consumers)
       switch (nr) {
         case 1: expand_stage<R, 1, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
         case 2: expand_stage<R, 2, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
