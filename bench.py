@@ -771,6 +771,8 @@ def relaunch_under_torchrun(n: int) -> int:
 
 def main():
     faulthandler.enable()
+    # stdout carries exactly one JSON line: keep NCCL's version banner off it
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)

@@ -170,6 +170,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (const char* e = std::getenv("LORA_TC_CAP_K")) s->tc_cap_k = std::atoi(e);
   if (const char* e = std::getenv("LORA_TCE_FLAGS")) s->tc_flags = std::atoi(e);
   if (const char* e = std::getenv("LORA_TC_PAIR")) s->tc_pair = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LORA_TC_LPT")) s->tc_lpt = std::atoi(e) != 0;
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
   s->simt_split_items = 2 * 2 * s->sm_count;  // fewer whole-K items than 2 per CUDA-core CTA: split K
   if (const char* e = std::getenv("LORA_TC_MIN_ROWS")) s->tc_min_rows = std::atoi(e);
@@ -283,15 +284,18 @@ lora_status_t create_common_sharded(const lora_config_t* cfg, int world, int ran
 namespace lora {
 // Programmatic dependent launch of the shrink / expand / v-reduce kernels
 // (prologues and the expand's first weight copies overlapping the previous
-// kernel's tail).  Measured in round 2 with the paired tcgen05 shrink and the
-// K-split CUDA-core shrink: prefill 0.530 -> 0.526 ms, Llama decode 0.412 ->
-// 0.407 ms, config 5 unchanged, so on by default (LORA_PDL=0 disables).
+// kernel's tail).  Measured in round 2: with a single kernel chain (Llama
+// decode, r = 16) 0.412 -> 0.407 ms; with the tcgen05 chain running
+// concurrently on the side stream the early CTAs compete with the other
+// chain (Mixtral decode 0.488 -> 0.565 ms), so apply_multi_impl allows it
+// only when the apply does not fork (LORA_PDL=0 disables it everywhere).
+thread_local bool g_pdl_allow = false;
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("LORA_PDL");
     return !(v && v[0] == '0');
   }();
-  return on;
+  return on && g_pdl_allow;
 }
 }  // namespace lora
 
@@ -813,6 +817,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     // so its CTAs fill the SMs the persistent CUDA-core kernels leave idle.
     const bool fork = tc && s->concurrent_tc;
     cudaStream_t tst = fork ? s->side_stream : st;
+    g_pdl_allow = !tc;  // (see pdl_enabled)
     if (fork) {
       CK(s, cudaEventRecord(s->ev_fork, st));
       CK(s, cudaStreamWaitEvent(tst, s->ev_fork, 0));
@@ -838,17 +843,36 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
             }
           }
         }
+        // item order longest first (decreasing h_in; a pair's items carry two
+        // slots' A): a long item started last would set the launch's tail --
+        // the tasks are permuted in targs (partners remapped)
+        std::vector<int> ord(nb), pos(nb);
+        for (int i = 0; i < nb; ++i) ord[i] = i;
+        auto weight = [&](int i) { return (long long)args.t[i].h_in * (targs.tc_pair[i] >= 0 ? 2 : 1); };
+        if (s->tc_lpt)
+          std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return weight(a) > weight(b); });
+        for (int i = 0; i < nb; ++i) pos[ord[i]] = i;
+        MultiArgs perm_args = targs;
+        for (int i = 0; i < nb; ++i) {
+          perm_args.t[i] = targs.t[ord[i]];
+          perm_args.xreg[i] = targs.xreg[ord[i]];
+          perm_args.yreg[i] = targs.yreg[ord[i]];
+          perm_args.tc_pair[i] = targs.tc_pair[ord[i]] >= 0 ? (int8_t)pos[targs.tc_pair[ord[i]]] : (int8_t)-1;
+        }
+        std::vector<char> ptaken(nb);
+        for (int i = 0; i < nb; ++i) ptaken[i] = taken[ord[i]];
+        targs = perm_args;
         int kc4 = 0;
         for (int i = 0; i < nb; ++i) {
           SlotTask& t = targs.t[i];
-          const bool partner = taken[i] && targs.tc_pair[i] < 0;
+          const bool partner = ptaken[i] && targs.tc_pair[i] < 0;
           t.kc_base = kc4;
           kc4 += partner ? 0 : t.n_kc;
         }
         // (a partner keeps its n_kc: the primary's epilogue stores its v with it)
         targs.total_kc = kc4;
         for (int i = 0; i < nb; ++i) {
-          const bool partner = taken[i] && targs.tc_pair[i] < 0;
+          const bool partner = ptaken[i] && targs.tc_pair[i] < 0;
           for (int k = 0; !partner && k < targs.t[i].n_kc && targs.t[i].kc_base + k < kTaskTable; ++k)
             targs.kc_task[targs.t[i].kc_base + k] = (uint8_t)i;
         }
@@ -871,6 +895,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
     pi = prof_start(s, st);
     CK(s, launch_simt_expand(s->r, args, p->dev, grid, st));
     prof_stop(s, pi, kKSimtExpand, st);
+    g_pdl_allow = false;
     if (fork) {
       CK(s, cudaEventRecord(s->ev_join, tst));
       CK(s, cudaStreamWaitEvent(st, s->ev_join, 0));

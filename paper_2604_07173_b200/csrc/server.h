@@ -34,7 +34,8 @@ struct lora_server {
   int tc_flags = 1;         // tcgen05 expand L2 policies (MultiArgs::tc_flags; env LORA_TCE_FLAGS): Bt evict_last (measured prefill 0.550 -> 0.529 ms; y evict_first hints slower)
   int tc_min_rows = 256;    // segmenter: tcgen05 tiles only with at least this many rows in large segments (env LORA_TC_MIN_ROWS)
   int simt_split_items = 0;  // MultiArgs::simt_split_items (set at create: 8 items per CUDA-core CTA; env LORA_SIMT_SPLIT)
-  bool tc_pair = true;      // tcgen05 shrink: slots sharing x in one N = 2r MMA (env LORA_TC_PAIR=0: off)
+  bool tc_pair = true;
+  bool tc_lpt = true;       // tcgen05 shrink items longest first (env LORA_TC_LPT=0: slot order)      // tcgen05 shrink: slots sharing x in one N = 2r MMA (env LORA_TC_PAIR=0: off)
   int tc_ki_max = 1 << 20;  // large-batch tcgen05 shrink: max h_in per item, default the whole h_in (env LORA_TC_KI_MAX)
   int world = 1, shard_rank = 0;
   int n_hot = 0;  // adapters [0, n_hot) replicated on every rank of a sharded server

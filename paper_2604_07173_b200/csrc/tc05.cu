@@ -313,25 +313,27 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
         if (pt == 0) {
           // W region of a stage: per k-step [NW][R rows x 128 B] -- for a pair the
           // two slots' A tiles back to back, one N = 2r operand
+          // (A tiles evict_last when args.tc_flags bit 5: a unit's A is re-read by each of its tiles)
+          const uint64_t wpol = (args.tc_flags & 32) ? policy_evict_last() : policy_evict_normal();
           if (pj >= 0) {
             mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * 2 * C::W_SUB);
 #pragma unroll
             for (int ks = 0; ks < C::KS_PER_STAGE; ++ks) {
               uint8_t* wd = sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB;
               const long long wo = (long long)(st * C::KS_PER_STAGE + ks) * (R * 64);
-              bulk_g2s(wd, wbase + wo, C::W_SUB, &full[stage]);
-              bulk_g2s(wd + C::W_SUB, wbase2 + wo, C::W_SUB, &full[stage]);
+              bulk_g2s_hint(wd, wbase + wo, C::W_SUB, &full[stage], wpol);
+              bulk_g2s_hint(wd + C::W_SUB, wbase2 + wo, C::W_SUB, &full[stage], wpol);
             }
           } else if (C::NW == 1) {
             mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
-            bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB,
-                     wbase + (long long)st * C::KS_PER_STAGE * (R * 64), C::KS_PER_STAGE * C::W_SUB, &full[stage]);
+            bulk_g2s_hint(sbase + C::KS_PER_STAGE * C::X_SUB, wbase + (long long)st * C::KS_PER_STAGE * (R * 64),
+                          C::KS_PER_STAGE * C::W_SUB, &full[stage], wpol);
           } else {  // an unpaired task in a pair launch: one A tile per k-step, N = r
             mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
 #pragma unroll
             for (int ks = 0; ks < C::KS_PER_STAGE; ++ks)
-              bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB,
-                       wbase + (long long)(st * C::KS_PER_STAGE + ks) * (R * 64), C::W_SUB, &full[stage]);
+              bulk_g2s_hint(sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB,
+                            wbase + (long long)(st * C::KS_PER_STAGE + ks) * (R * 64), C::W_SUB, &full[stage], wpol);
           }
         }
         const int j0 = st * C::KS_PER_STAGE * C::KSTEP;
