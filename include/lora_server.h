@@ -218,11 +218,14 @@ lora_status_t lora_apply(lora_server_t *s, int32_t slot, const void *x, const in
 
 /* End-to-end entry with HOST buffers (pinned for full async speed): copies
  * the ids and the n slots' x / y host->device into library staging buffers,
- * builds the internal plan once, applies, and copies every y back
- * device->host.  Pipelined: the slots are cut into chunks (about 1/8 of the
- * upload each, >= 32 MB); chunk c+1's upload (internal copy stream), chunk c's
- * apply (`stream`) and chunk c-1's download (a second internal stream) run
- * concurrently.  Stream-ordered on `stream` at both ends; returns after
+ * applies, and copies every y back device->host.  Pipelined: the rows are cut
+ * into RC chunks (RC = clamp(T / 2048, 1, 4); env LORA_HOST_ROW_CHUNKS) with
+ * one internal plan each, every row chunk's slots into groups of >= 32 MB of
+ * upload; piece p+1's upload (internal copy stream), piece p's apply
+ * (`stream`) and piece p-1's download (a second internal stream) overlap.
+ * Row chunks re-read the weights their units need (one apply per chunk); the
+ * segments, and so the kernel route of a row (CUDA-core / tcgen05), are those
+ * of its row chunk.  Stream-ordered on `stream` at both ends; returns after
  * enqueueing, the caller synchronises `stream` before reading y.  Capacity:
  * T <= max_rows.  x[i] pointers may repeat (uploaded once). */
 lora_status_t lora_apply_multi_host(lora_server_t *s, int32_t n, const int32_t *slots,

@@ -89,6 +89,7 @@ static lora_status_t validate_config(const lora_config_t* cfg) {
 static void free_server(lora_server* s) {
   if (!s) return;
   if (s->internal_plan) plan_destroy_impl(s->internal_plan);
+  for (auto hp : s->host_plans) plan_destroy_impl(hp);
   for (auto& sl : s->slots) {
     cudaFree(sl.At);
     cudaFree(sl.Bt);
@@ -1026,14 +1027,20 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
   CK(s, cudaSetDevice(s->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t ysz = y_dtype == LORA_FP32 ? 4 : 2;
-  // Pipelined executor.  The slots are cut into chunks of consecutive slots
-  // (~1/8 of the host->device bytes each, at least 32 MB); per chunk: its x
-  // buffers (first use) and y rows go host->device on the copy stream, the
-  // chunk is applied on the caller's stream with the one plan built from the
-  // ids, and its y rows go device->host on a third stream -- so chunk c+1's
-  // upload, chunk c's apply and chunk c-1's download overlap (the two copy
-  // directions use separate copy engines).  The caller's stream waits for
-  // the last download: the call stays stream-ordered on `stream`.
+  // Pipelined executor over (row chunk, slot group) pieces.  The rows are cut
+  // into RC chunks (1 for small batches, up to 4) and each chunk's slots into
+  // groups of >= 32 MB of upload; per piece: its x rows (first use of the x
+  // buffer in the row chunk) and y rows go host->device on the copy stream,
+  // the piece is applied on the caller's stream with the row chunk's plan
+  // (built once from that chunk's ids), and its y rows go device->host on a
+  // third stream -- piece p+1's upload, piece p's apply and piece p-1's
+  // download overlap (the two copy directions use separate copy engines), so
+  // the PCIe time is exposed only for the first piece's upload and the last
+  // piece's download.  Row chunks re-stream the weights of the units they
+  // touch (one apply per chunk): GPU time grows, far below the PCIe time at
+  // the sizes where RC > 1.  Each row's arithmetic depends only on its
+  // segment's route (CUDA-core / tcgen05), decided per chunk.  The caller's
+  // stream waits for the last download: the call stays stream-ordered.
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   std::vector<const void*> xd;  // distinct x host pointers
   std::vector<int> x_of(n);
@@ -1068,32 +1075,52 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
   }
   if (!s->copy_stream) CK(s, cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
   if (!s->d2h_stream) CK(s, cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking));
-  // chunks: consecutive slots, cut when the chunk's upload reaches the target
-  std::vector<size_t> up_bytes(n);
-  std::vector<char> x_first(n, 0);
-  {
+  // row chunks: RC = clamp(T / 2048, 1, 4) (env LORA_HOST_ROW_CHUNKS), one plan each
+  int RC = std::max(1, std::min(4, T / 2048));
+  if (const char* e = std::getenv("LORA_HOST_ROW_CHUNKS")) RC = std::max(1, std::min(8, std::atoi(e)));
+  RC = std::min(RC, T);
+  while ((int)s->host_plans.size() < RC) {
+    lora_plan* hp = nullptr;
+    const lora_status_t pc = plan_create_impl(s, s->max_rows, &hp);
+    if (pc != LORA_OK) return pc;
+    s->host_plans.push_back(hp);
+  }
+  std::vector<int> r0(RC + 1);
+  for (int c = 0; c <= RC; ++c) r0[c] = (int)((long long)T * c / RC);
+  // pieces: per row chunk, consecutive slots cut at >= max(1/8 of the chunk's upload, 32 MB)
+  struct Piece {
+    int rc, s0, s1;
+  };
+  std::vector<Piece> pieces;
+  std::vector<std::vector<char>> x_first(RC, std::vector<char>(n, 0));
+  for (int c = 0; c < RC; ++c) {
+    const size_t rows = (size_t)(r0[c + 1] - r0[c]);
+    std::vector<size_t> up(n);
     std::vector<char> seen(xd.size(), 0);
+    size_t total = 0;
     for (int i = 0; i < n; ++i) {
-      up_bytes[i] = (size_t)T * s->slots[slots[i]].h_out * ysz;
+      up[i] = rows * s->slots[slots[i]].h_out * ysz;
       if (!seen[x_of[i]]) {
         seen[x_of[i]] = 1;
-        x_first[i] = 1;
-        up_bytes[i] += (size_t)T * x_hin[x_of[i]] * 2;
+        x_first[c][i] = 1;
+        up[i] += rows * x_hin[x_of[i]] * 2;
+      }
+      total += up[i];
+    }
+    const size_t target = std::max<size_t>(total / 8, (size_t)32 << 20);
+    int start = 0;
+    size_t acc = 0;
+    for (int i = 0; i < n; ++i) {
+      acc += up[i];
+      if (acc >= target || i == n - 1) {
+        pieces.push_back({c, start, i + 1});
+        start = i + 1;
+        acc = 0;
       }
     }
   }
-  size_t total = 0;
-  for (size_t b : up_bytes) total += b;
-  const size_t target = std::max<size_t>(total / 8, (size_t)32 << 20);
-  std::vector<int> cut{0};
-  for (int i = 0, acc = 0; i < n; ++i) {
-    acc += 1;
-    size_t sum = 0;
-    for (int j = cut.back(); j <= i; ++j) sum += up_bytes[j];
-    if (sum >= target || i == n - 1) cut.push_back(i + 1);
-  }
-  const int n_chunks = (int)cut.size() - 1;
-  while ((int)s->events.size() < 2 * n_chunks + 2) {
+  const int n_pieces = (int)pieces.size();
+  while ((int)s->events.size() < 2 * n_pieces + 2) {
     cudaEvent_t e;
     CK(s, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     s->events.push_back(e);
@@ -1111,35 +1138,41 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
     CK(s, cudaMemcpyAsync(d_ex, expert_ids_host, (size_t)T * 4, cudaMemcpyHostToDevice, s->copy_stream));
   CK(s, cudaEventRecord(ev_ids, s->copy_stream));
   CK(s, cudaStreamWaitEvent(st, ev_ids, 0));
-  lora_status_t rc = plan_build_impl(s, s->internal_plan, d_ad, expert_ids_host ? d_ex : nullptr, T,
-                                     s->slots[slots[0]].E, st);
-  if (rc != LORA_OK) return rc;
+  const int E = s->slots[slots[0]].E;
+  for (int c = 0; c < RC; ++c) {
+    lora_status_t rc = plan_build_impl(s, s->host_plans[c], d_ad + r0[c], expert_ids_host ? d_ex + r0[c] : nullptr,
+                                       r0[c + 1] - r0[c], E, st);
+    if (rc != LORA_OK) return rc;
+  }
   std::vector<const void*> xs(n);
   std::vector<void*> ys(n);
-  for (int i = 0; i < n; ++i) {
-    xs[i] = base + x_off[x_of[i]];
-    ys[i] = base + y_off[i];
-  }
-  for (int c = 0; c < n_chunks; ++c) {
-    cudaEvent_t ev_in = s->events[2 + 2 * c], ev_done = s->events[3 + 2 * c];
-    for (int i = cut[c]; i < cut[c + 1]; ++i) {
-      if (x_first[i])
-        CK(s, cudaMemcpyAsync(base + x_off[x_of[i]], xd[x_of[i]], (size_t)T * x_hin[x_of[i]] * 2,
+  for (int pi = 0; pi < n_pieces; ++pi) {
+    const Piece& pc = pieces[pi];
+    const int a = r0[pc.rc], rows = r0[pc.rc + 1] - a;
+    cudaEvent_t ev_in = s->events[2 + 2 * pi], ev_done = s->events[3 + 2 * pi];
+    for (int i = pc.s0; i < pc.s1; ++i) {
+      const size_t hi = (size_t)x_hin[x_of[i]], ho = (size_t)s->slots[slots[i]].h_out;
+      if (x_first[pc.rc][i])
+        CK(s, cudaMemcpyAsync(base + x_off[x_of[i]] + (size_t)a * hi * 2,
+                              static_cast<const char*>(xd[x_of[i]]) + (size_t)a * hi * 2, (size_t)rows * hi * 2,
                               cudaMemcpyHostToDevice, s->copy_stream));
-      CK(s, cudaMemcpyAsync(ys[i], y_host[i], (size_t)T * s->slots[slots[i]].h_out * ysz, cudaMemcpyHostToDevice,
-                            s->copy_stream));
+      CK(s, cudaMemcpyAsync(base + y_off[i] + (size_t)a * ho * ysz, static_cast<const char*>(y_host[i]) + (size_t)a * ho * ysz,
+                            (size_t)rows * ho * ysz, cudaMemcpyHostToDevice, s->copy_stream));
+      xs[i] = base + x_off[x_of[i]] + (size_t)a * hi * 2;
+      ys[i] = base + y_off[i] + (size_t)a * ho * ysz;
     }
     CK(s, cudaEventRecord(ev_in, s->copy_stream));
     CK(s, cudaStreamWaitEvent(st, ev_in, 0));
-    const int nc = cut[c + 1] - cut[c];
-    rc = apply_multi_impl(s, s->internal_plan, nc, slots + cut[c], xs.data() + cut[c], ys.data() + cut[c], y_dtype,
-                          st);
+    const lora_status_t rc = apply_multi_impl(s, s->host_plans[pc.rc], pc.s1 - pc.s0, slots + pc.s0, xs.data() + pc.s0,
+                                              ys.data() + pc.s0, y_dtype, st);
     if (rc != LORA_OK) return rc;
     CK(s, cudaEventRecord(ev_done, st));
     CK(s, cudaStreamWaitEvent(s->d2h_stream, ev_done, 0));
-    for (int i = cut[c]; i < cut[c + 1]; ++i)
-      CK(s, cudaMemcpyAsync(y_host[i], ys[i], (size_t)T * s->slots[slots[i]].h_out * ysz, cudaMemcpyDeviceToHost,
-                            s->d2h_stream));
+    for (int i = pc.s0; i < pc.s1; ++i) {
+      const size_t ho = (size_t)s->slots[slots[i]].h_out;
+      CK(s, cudaMemcpyAsync(static_cast<char*>(y_host[i]) + (size_t)a * ho * ysz, ys[i], (size_t)rows * ho * ysz,
+                            cudaMemcpyDeviceToHost, s->d2h_stream));
+    }
   }
   // join: the caller's stream completes after the last download
   CK(s, cudaEventRecord(ev_start, s->d2h_stream));

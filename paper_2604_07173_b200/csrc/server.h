@@ -48,6 +48,7 @@ struct lora_server {
   float* d_scale = nullptr;
   int* d_err = nullptr;
   lora_plan_t* internal_plan = nullptr;
+  std::vector<lora_plan_t*> host_plans;  // lora_apply_multi_host: one plan per row chunk
   std::string last_error;
   // staging for lora_apply_multi_host (grown lazily)
   void* h2d_buf = nullptr;

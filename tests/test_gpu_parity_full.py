@@ -474,3 +474,27 @@ def test_tc_min_rows_heuristic(B, monkeypatch):
                 U.assert_parity(ys[i], orc.apply_slot(c2, i, b), f"min-rows {n_big} slot {i}")
     finally:
         B.lora_server_destroy(s)
+
+
+def test_host_entry_row_chunks(B, monkeypatch):
+    """lora_apply_multi_host with several row chunks (a 4100-row batch: two
+    chunks, one plan each, pieces of (row chunk, slot group) pipelined over
+    the copy engines) against the oracle, rows without a LoRA bit-identical."""
+    cfg = dataclasses.replace(_mid_cfg(T=4100), no_lora_frac=0.05)
+    b = li.make_batch(cfg)
+    T = b.n_rows
+    s = U.make_server(B, cfg)
+    try:
+        xh = [U.x_dev(B, cfg, i, T).cpu().pin_memory() for i in range(2)]
+        yh = [U.y0_dev(B, cfg, i, T).cpu().pin_memory() for i in range(2)]
+        y0 = [y.clone() for y in yh]
+        B.lora_apply_multi_host(s, [0, 1], xh, b.adapter_ids, b.expert_ids, yh, B.LORA_BF16, T)
+        torch.cuda.synchronize()
+        assert B.lora_server_check(s) == B.LORA_OK
+        none = torch.from_numpy(np.flatnonzero(b.adapter_ids < 0))
+        assert none.numel() > 0
+        for i in range(2):
+            U.assert_parity(yh[i], orc.apply_slot(cfg, i, b), f"host row chunks slot {i}")
+            assert torch.equal(yh[i][none], y0[i][none])
+    finally:
+        B.lora_server_destroy(s)
