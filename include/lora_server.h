@@ -247,7 +247,10 @@ lora_status_t lora_nccl_unique_id(void *out128);
  * (a - h) mod world (LoRA Data Parallel striping); with
  * cfg->expert_parallel, unit (a, e) is owned by rank e mod world.
  * Each rank stores only what it owns.  Every rank must call this
- * collectively with the same config.  max_rows * world <= 16384. */
+ * collectively with the same config.  cfg->max_rows is this rank's row
+ * capacity; its owner-side plan holds max_rows * world received rows (rows
+ * beyond that are dropped and flagged), so an unbalanced deployment sizes
+ * max_rows for the most loaded owner.  max_rows * world <= 16384. */
 lora_status_t lora_server_create_sharded(const lora_config_t *cfg, int32_t rank, int32_t world,
                                          const void *nccl_unique_id, lora_server_t **out);
 

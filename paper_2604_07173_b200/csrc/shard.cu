@@ -247,7 +247,8 @@ int grid_of(long long n) {
 // flag_done[q] by owner q.  The send arrays are this rank's, read by owners.
 struct ShardCtl {
   unsigned int epoch;                              // this rank's apply counter (local)
-  unsigned int pad_[7];
+  int stride;                                      // this rank's max_rows: the send arrays' length (read by owners)
+  unsigned int pad_[6];
   unsigned int flag_cnt[kMaxWorld];                // source p's count row for epoch v is in mbox
   unsigned int flag_done[kMaxWorld];               // owner q finished pushing into this rank's y
   int mbox[2][kMaxWorld][kMaxWorld + 1];           // [epoch & 1][source p][owner q | layout hash]
@@ -375,9 +376,10 @@ __global__ void __launch_bounds__(1024) push_recv_prep_kernel(PeerCtl pc, int me
     while (p + 1 < G && s_off[p + 1] <= r) ++p;
     ShardCtl* src = pc.p[p];
     const int j = s_base[p] + (r - s_off[p]);
-    ids_a[r] = ctl_send(src, max_rows, 1)[j];
-    ids_e[r] = ctl_send(src, max_rows, 2)[j];
-    origin[r] = (p << kOriginRowBits) | ctl_send(src, max_rows, 0)[j];
+    const int sstride = src->stride;  // the source's own max_rows (ranks may differ)
+    ids_a[r] = ctl_send(src, sstride, 1)[j];
+    ids_e[r] = ctl_send(src, sstride, 2)[j];
+    origin[r] = (p << kOriginRowBits) | ctl_send(src, sstride, 0)[j];
   }
 }
 
@@ -677,8 +679,10 @@ extern "C" lora_status_t lora_shard_register(lora_server_t* s, int32_t n, void* 
   bool new_ctl = false;
   if (!sh->ctl) {
     sh->ctl_bytes = sizeof(ShardCtl) + sizeof(int32_t) * 3 * (size_t)s->max_rows;
+    const int stride = s->max_rows;
     if (cudaMalloc(&sh->ctl, sh->ctl_bytes) != cudaSuccess ||
         cudaMemset(sh->ctl, 0, sh->ctl_bytes) != cudaSuccess ||
+        cudaMemcpy(&sh->ctl->stride, &stride, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMalloc(&sh->d_push, sizeof(int32_t) * (3 * (size_t)s->max_rows * G + 4)) != cudaSuccess) {
       cudaGetLastError();
       ok = 0;
@@ -1119,6 +1123,11 @@ extern "C" lora_status_t lora_apply_sharded(lora_server_t* s, int32_t n, const i
               sh->reg[yk[i]].bytes >= (size_t)T * si.h_out * ysz;
   }
   if (all_reg) return apply_sharded_push(s, n, slots, x, adapter_ids, expert_ids, y, y_dtype, T, st, xk, yk);
+  // once buffers are registered every call must use registered x / y: a rank
+  // taking the NCCL path while its peers push would block them (they time out)
+  if (sh->ctl)
+    return fail(s, LORA_ERR_INVALID_ARG,
+                "this server has registered buffers: x[i] / y[i] must be registered buffer starts of >= T rows");
   if (sh->host_ag)
     return fail(s, LORA_ERR_INVALID_ARG, "host control plane: x and y must be registered (lora_shard_register)");
   if (!sh->comm) return fail(s, LORA_ERR_NCCL, "no NCCL communicator");

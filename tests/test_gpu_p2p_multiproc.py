@@ -43,7 +43,23 @@ def _cfg(y_dtype, two_layers=False):
     return li.Config("mp_p2p", 8, sl, 64, 24, 4, 2, 300, y_dtype)
 
 
-def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep, pp=0):
+def _token_range(n_tokens, world, rank, empty_rank):
+    """Contiguous token split; with empty_rank >= 0 that rank holds no token
+    (its neighbours split its share)."""
+    if empty_rank < 0:
+        return (n_tokens * rank) // world, (n_tokens * (rank + 1)) // world
+    bounds = [0]
+    others = [r for r in range(world) if r != empty_rank]
+    for r in range(world):
+        if r == empty_rank:
+            bounds.append(bounds[-1])
+        else:
+            i = others.index(r)
+            bounds.append((n_tokens * (i + 1)) // len(others))
+    return bounds[rank], bounds[rank + 1]
+
+
+def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep, pp=0, empty_rank=-1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     if y_dtype == "fp32":
         # CUDA-core route for every segment: the per-row arithmetic then does not depend on how
@@ -65,19 +81,23 @@ def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep, pp=0):
         calls = [[0, 1], [2, 3]] if pp > 1 else [[0, 1]]   # one sharded apply per layer
         b = li.make_batch(cfg)
         k = b.top_k
-        t0, t1 = (cfg.n_tokens * rank) // world, (cfg.n_tokens * (rank + 1)) // world
+        t0, t1 = _token_range(cfg.n_tokens, world, rank, empty_rank)
         r0, r1 = t0 * k, t1 * k
         T = r1 - r0
+        Tb = max(T, 1)  # buffers (a rank may hold no row)
+        # capacity: every rank's max_rows must cover its own rows, and max_rows * world the rows it may
+        # receive (an empty rank still serves the others)
+        cap = max(T, (b.n_rows + world - 1) // world) if empty_rank < 0 else b.n_rows
         c = B.make_config([s.h_in for s in cfg.slots], [s.h_out for s in cfg.slots], [4] * n_sl, cfg.rank,
-                          cfg.n_adapters, cfg.scale(), T, 0, n_replicated=n_hot, expert_parallel=ep, pp_stages=pp,
+                          cfg.n_adapters, cfg.scale(), cap, 0, n_replicated=n_hot, expert_parallel=ep, pp_stages=pp,
                           slot_layer=[i // 2 for i in range(n_sl)])
         s = B.lora_server_create_sharded_host(c, rank, world, allgather)
         B.lora_server_fill_synthetic(s, cfg.seed)
         xs, ys = [], []
         for i, sl in enumerate(cfg.slots):
-            x = torch.empty((T, sl.h_in), dtype=torch.int16, device="cuda")
+            x = torch.zeros((Tb, sl.h_in), dtype=torch.int16, device="cuda")
             B.lora_synth_fill_rows(x, T, sl.h_in, cfg.seed, li.tag_of(li.KIND_X, sl.xbuf), li.shift_x(), r0)
-            y = torch.empty((T, sl.h_out), dtype=torch.int16, device="cuda")
+            y = torch.zeros((Tb, sl.h_out), dtype=torch.int16, device="cuda")
             B.lora_synth_fill_rows(y, T, sl.h_out, cfg.seed, li.tag_of(li.KIND_Y0, i), li.shift_y0(), r0)
             if y_dtype == "fp32":
                 y = ((y.to(torch.int32) << 16).view(torch.float32)).contiguous()
@@ -98,23 +118,25 @@ def _worker(rank, world, port, out_dir, y_dtype, n_hot, ep, pp=0):
             torch.cuda.synchronize()
         assert B.lora_server_check(s) == B.LORA_OK
         for i in range(n_sl):
-            np.save(os.path.join(out_dir, f"y{i}_{rank}.npy"), yy[i].cpu().numpy())
+            np.save(os.path.join(out_dir, f"y{i}_{rank}.npy"), yy[i][:T].cpu().numpy())
         B.lora_server_destroy(s)
     finally:
         dist.barrier()
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("y_dtype,n_hot,ep,world,pp", [("fp32", 0, False, 2, 0), ("fp32", 3, False, 2, 0),
-                                                       ("bf16", 0, False, 2, 0), ("fp32", 0, True, 2, 0),
-                                                       ("fp32", 0, True, 4, 2)])
-def test_p2p_two_ranks_one_gpu(tmp_path, y_dtype, n_hot, ep, world, pp):
+@pytest.mark.parametrize("y_dtype,n_hot,ep,world,pp,empty", [
+    ("fp32", 0, False, 2, 0, -1), ("fp32", 3, False, 2, 0, -1), ("bf16", 0, False, 2, 0, -1),
+    ("fp32", 0, True, 2, 0, -1), ("fp32", 0, True, 4, 2, -1), ("fp32", 0, False, 3, 0, 1)])
+def test_p2p_two_ranks_one_gpu(tmp_path, y_dtype, n_hot, ep, world, pp, empty):
     """(world 4, pp 2: hybrid EP2-PP2 over four processes, one sharded apply
     per layer; each layer's rows are served by its group's two ranks, every
-    rank sends.)"""
+    rank sends.  world 3 with rank 1 holding no row: it still owns adapters,
+    serves the others' rows and takes part in every flag exchange.)"""
     from tests import gpu_util as U
     from oracle import oracle as orc
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), y_dtype, n_hot, ep, pp), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), y_dtype, n_hot, ep, pp, empty), nprocs=world,
+             join=True)
     B = U.binding()
     cfg = _cfg(y_dtype, two_layers=pp > 1)
     b = li.make_batch(cfg)
