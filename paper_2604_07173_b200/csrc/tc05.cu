@@ -162,6 +162,9 @@ struct ShrinkCfgT {
 #ifndef LORA_TCSP_NST
 #define LORA_TCSP_NST 3
 #endif
+#ifndef LORA_TCS_NOINC
+#define LORA_TCS_NOINC 1  // producers arrive with cp.async.mbarrier.arrive.noinc instead of waiting (measured: prefill tc shrink 140 -> 136 us, config 5 115 -> 110 us)
+#endif
   static constexpr int KS_PER_STAGE = LORA_TCS_KS;         // k-steps per stage
   static constexpr int NW = PAIR ? 2 : 1;                  // A tiles per k-step
   static constexpr int X_SUB = kTileRows * 128;            // 16 KB per k-step
@@ -346,6 +349,12 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
             cp_async16(xs + n * 128 + ((q ^ (n & 7)) << 4), xsrc[i] + j0 + ks * C::KSTEP, xbytes[i]);
           }
         }
+#if LORA_TCS_NOINC
+        // the stage's barrier tracks this thread's copies itself: no wait here,
+        // every stage of the ring can be in flight (the MMA thread fences the
+        // async proxy after its wait)
+        cp_async_mbar_arrive_noinc(&full[stage]);
+#else
         cp_async_commit();
         pend_stage[npend++] = stage;
         if (npend > C::LAG) {
@@ -355,15 +364,22 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
           for (int q = 0; q < npend - 1; ++q) pend_stage[q] = pend_stage[q + 1];
           --npend;
         }
+#endif
         if (++stage == C::NST) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
+#if !LORA_TCS_NOINC
     cp_async_wait<0>();
     fence_proxy_async_smem();
     for (int q = 0; q < npend; ++q) mbar_arrive(&full[pend_stage[q]]);
+#else
+    cp_async_wait<0>();
+    (void)npend;
+    (void)pend_stage;
+#endif
   } else if (warp == C::MMA_WARP) {
     // ===================== MMA issuer =====================
     int stage = 0;
@@ -384,6 +400,9 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
       const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
       for (int st = 0; st < n_st; ++st) {
         mbar_wait(&full[stage], phase);
+#if LORA_TCS_NOINC
+        fence_proxy_async_smem();  // the producers' cp.async writes, seen through the barrier, to the MMA's async proxy
+#endif
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sbase = smem_u32(smem + stage * C::STAGE);
