@@ -17,6 +17,7 @@ Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import faulthandler
 import json
 import os
@@ -405,6 +406,24 @@ def secondaries(B, torch, dev, stream, hbm_peak, steps, warmup):
                 "points": sweep}
         else:
             r.destroy()
+    # rank sweep over the paper's range ("r typically 32-128") on config-3
+    # shapes with 128 adapters (r = 64 is config 3 itself, above)
+    sweep = {}
+    for rk in (16, 32, 128):
+        c3 = dataclasses.replace(li.CONFIGS["mixtral_decode"], name=f"mixtral_decode_r{rk}", rank=rk, n_adapters=128)
+        b3 = li.make_batch(c3)
+        slots = list(range(len(c3.slots)))
+        r = SingleRun(B, torch, c3, b3, slots, dev, stream)
+        t3, tot3 = r.time(max(5, steps // 2), 2)
+        prof3 = r.profile(3)
+        sm = summarise(c3, algorithmic(c3, b3, slots), t3, tot3, hbm_peak, prof3, 3)
+        r.destroy()
+        sweep[str(rk)] = {k: sm[k] for k in ("ms_per_step", "ms_median", "tokens_per_s", "rows", "distinct_units",
+                                             "step_GBs", "frac_measured", "kernels")}
+    out["rank_sweep"] = {
+        "workload": "config-3 shapes (Mixtral gate/up/down, top-2, 512 tokens, Zipf 1.2) with 128 adapters at "
+                    "r = 16 / 32 / 128 (P:165)",
+        "points": sweep}
     return out
 
 

@@ -66,7 +66,7 @@ typedef struct {
   const int32_t *h_in;       /* [n_slots] input width;  multiple of 64 */
   const int32_t *h_out;      /* [n_slots] output width; multiple of 64 */
   const int32_t *n_experts;  /* [n_slots] E (1 for dense slots), >= 1 */
-  int32_t rank;              /* r, uniform (one rank per model): 8, 16, 32 or 64 */
+  int32_t rank;              /* r, uniform (one rank per model): 8, 16, 32, 64 or 128 ("r typically 32-128") */
   int32_t n_adapters;        /* global adapter count n */
   const float *scale;        /* [n_adapters] host fp32 s_a; NULL => all 1.0 (R1) */
   int32_t max_rows;          /* capacity (rows) of the internal plan; 0 < max_rows <= 16384 */

@@ -308,11 +308,13 @@ LORA_DEVINL void wq_finish(unsigned long long* counter, unsigned int* done) {
 //       it is the canonical SWIZZLE_128B K-major operand for tcgen05.
 //   Bt (expand operand): [U][h_out][r] bf16, rows of r*2 bytes (one output
 //       column c per row), swizzled with the pattern of that row width
-//       (128B: q ^ (c&7); 64B: q ^ ((c>>1)&3); 32B: q ^ ((c>>2)&1); 16B: none).
+//       (256B: q ^ ((c&3)<<1); 128B: q ^ (c&7); 64B: q ^ ((c>>1)&3);
+//       32B: q ^ ((c>>2)&1); 16B: none).
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int swz_row_chunk(int row, int chunk, int row_bytes) {
   // physical 16-byte chunk index inside a row of `row_bytes` bytes
   switch (row_bytes) {
+    case 256: return chunk ^ ((row & 3) << 1);
     case 128: return chunk ^ (row & 7);
     case 64: return chunk ^ ((row >> 1) & 3);
     case 32: return chunk ^ ((row >> 2) & 1);

@@ -68,8 +68,8 @@ static lora_status_t validate_config(const lora_config_t* cfg) {
   if (!cfg) return fail(nullptr, LORA_ERR_INVALID_ARG, "cfg is NULL");
   if (cfg->n_slots < 1 || !cfg->h_in || !cfg->h_out || !cfg->n_experts)
     return fail(nullptr, LORA_ERR_INVALID_ARG, "n_slots < 1 or NULL shape arrays");
-  if (cfg->rank != 8 && cfg->rank != 16 && cfg->rank != 32 && cfg->rank != 64)
-    return fail(nullptr, LORA_ERR_UNSUPPORTED, "rank must be 8, 16, 32 or 64");
+  if (cfg->rank != 8 && cfg->rank != 16 && cfg->rank != 32 && cfg->rank != 64 && cfg->rank != 128)
+    return fail(nullptr, LORA_ERR_UNSUPPORTED, "rank must be 8, 16, 32, 64 or 128");
   if (cfg->n_adapters < 1) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_adapters < 1");
   if (cfg->max_rows < 1 || cfg->max_rows > kMaxPlanRows)
     return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows must be in [1, 16384]");

@@ -53,6 +53,11 @@ struct SimtCfg {
   // (an x element widened once feeds 4 products; two k share an FFMA2), the
   // j-groups of a warp pre-reduced with shuffles (SMALL_K).
   static constexpr bool SMALL_K = R <= 32;
+  // r <= 32 and r = 128: the shrink on mma.sync (shrink_item_mma); at r = 128
+  // the eight 16-row M tiles are one per consumer warp (OWN_M: no cross-warp
+  // reduction, no red buffer)
+  static constexpr bool MMA = R <= 32 || R >= 128;
+  static constexpr bool OWN_M = R >= 128;
   static constexpr int KL = SMALL_K ? R / 4 : 32;  // lanes along k
   static constexpr int KPL = R / KL;               // k per lane
   static constexpr int NJG = NCT / KL;             // j-groups
@@ -65,10 +70,10 @@ struct SimtCfg {
   static constexpr int A_STAGE = R * SJ_MAX * 2;
   // r <= 32 (MMA consumers): x rows padded by 16 bytes so the ldmatrix row
   // addresses of one 8x8 matrix fall in distinct banks
-  static constexpr int X_PITCH = SMALL_K ? SJ_MAX * 2 + 16 : SJ_MAX * 2;
+  static constexpr int X_PITCH = MMA ? SJ_MAX * 2 + 16 : SJ_MAX * 2;
   static constexpr int X_STAGE = GR * X_PITCH;
   static constexpr int S_STAGE = (A_STAGE + X_STAGE + 1023) / 1024 * 1024;
-  static constexpr int RED_BYTES = (SMALL_K ? NWC : NJG) * GR * R * 4;
+  static constexpr int RED_BYTES = OWN_M ? 0 : (MMA ? NWC : NJG) * GR * R * 4;
   static constexpr int NST_RAW = (SMEM_BUDGET - RED_BYTES) / S_STAGE;
   static constexpr int NST = NST_RAW > 8 ? 8 : (NST_RAW < 2 ? 2 : NST_RAW);
   // + at r <= 32 a resolver warp running kSRQ items ahead of the producer
@@ -91,8 +96,11 @@ struct SimtCfg {
   // r <= 16: LORA_SMALLR_CPT columns per thread (4 = 32 KB B stages, staged-tile
   // expand only; measured slower: Llama expand 185 -> 238 us)
   static constexpr int CPT = R >= 64 ? 1 : (R <= 16 ? LORA_SMALLR_CPT : 2);
-  static constexpr bool LOOKAHEAD_OK = CPT <= 2;  // the look-ahead expand's y ring fits
-  static constexpr int SC_MAX = NCT * CPT;
+  // r = 128: two threads per column, one k half each (expand_stage_half), so a
+  // stage holds NCT / 2 columns (32 KB of B) and two stages fit the 112 KB share
+  static constexpr bool HALF = R >= 128;
+  static constexpr bool LOOKAHEAD_OK = CPT <= 2 && !HALF;  // the look-ahead expand's y ring fits
+  static constexpr int SC_MAX = HALF ? NCT / 2 : NCT * CPT;
   static constexpr int B_STAGE = SC_MAX * R * 2;
   static constexpr int V_BYTES = GR * R * 4;  // v rows of the group (fp32)
   static constexpr int E_STAGE = B_STAGE + 1024 * ((V_BYTES + 1023) / 1024);
@@ -306,6 +314,45 @@ LORA_DEVINL void shrink_item_mma(uint8_t* smem, uint64_t* full, uint64_t* empty,
   const int ka = (lane & 7) + ((lane >> 3) & 1) * 8;  // 0..15
   const int ca = lane >> 4;                           // chunk offset 0 / 1
   const int xn = lane & 7, xc = (lane >> 3) & 1;
+  if constexpr (C::OWN_M) {
+    // r = 128: warp w computes rank rows 16 w .. 16 w + 15 over every j step
+    static_assert(MT == C::NWC, "one M tile per consumer warp");
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+    const int k = warp * 16 + ka;
+    for (int st = 0; st < sc.n_st; ++st) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t a_s = smem_u32(smem + stage * C::S_STAGE);
+      const uint32_t x_s = a_s + C::A_STAGE;
+      for (int q = 0; q < nsteps; ++q) {
+        const int j0 = q << 4;
+        const int tile = j0 >> 6, ch = ((j0 & 63) >> 3) + ca;
+        uint32_t b0, b1, a0, a1, a2, a3;
+        ldsm_x2(x_s + xn * C::X_PITCH + ((j0 + xc * 8) << 1), b0, b1);
+        ldsm_x4(a_s + tile * (R * 128) + k * 128 + ((ch ^ (k & 7)) << 4), a0, a1, a2, a3);
+        mma16816(d, a0, a1, a2, a3, b0, b1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == C::NST) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // D fragment: d[0..1] -> k = 16 w + lane/4, rows 2 (lane % 4) + {0, 1}; d[2..3] -> k + 8
+    float* vp = vpart_base + (long long)g.x * R;
+    float* vk = vp + sc.kc * sc.kc_stride + warp * 16 + (lane >> 2);
+    const int n0 = (lane & 3) * 2;
+    if (n0 < g.y) {
+      vk[n0 * R] = d[0];
+      vk[n0 * R + 8] = d[2];
+    }
+    if (n0 + 1 < g.y) {
+      vk[(n0 + 1) * R] = d[1];
+      vk[(n0 + 1) * R + 8] = d[3];
+    }
+    if (sc.n_kc > 1) split_finish<C::NCT>(vp, g.y * R, sc);
+    return;
+  }
   for (int st = 0; st < sc.n_st; ++st) {
     mbar_wait(&full[stage], phase);
     const uint32_t a_s = smem_u32(smem + stage * C::S_STAGE);
@@ -524,7 +571,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
 #pragma unroll
           for (int r = 0; r < C::GR; ++r)
             if (r < g.y)
-              bulk_g2s(sX + r * (C::SMALL_K ? (uint32_t)C::X_PITCH : x_bytes), t.x + xrow[r] + jofs, x_bytes,
+              bulk_g2s(sX + r * (C::MMA ? (uint32_t)C::X_PITCH : x_bytes), t.x + xrow[r] + jofs, x_bytes,
                        &full[stage]);
           if (++stage == C::NST) {
             stage = 0;
@@ -557,7 +604,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::SHRINK_THREADS, 2)
       sc.kc_stride = (long long)pd.max_rows * R;
       sc.cnt = pd.gcnt + (long long)ti * pd.max_rows + gi;
       sc.s_last = &s_last;
-      if constexpr (C::SMALL_K) {  // MMA consumers: one code path for any group size
+      if constexpr (C::MMA) {  // MMA consumers: one code path for any group size
         shrink_item_mma<R>(smem, full, empty, red, stage, phase, t, g, vb, lane, sc);
       } else {
       switch (g.y) {
@@ -681,6 +728,50 @@ LORA_DEVINL void expand_stage1(uint32_t b_s, uint32_t v_s, int cr, const ExpandP
   }
 }
 
+// r = 128: two threads per column (ct = 2 c + h), thread h taking the
+// interleaved 16-byte chunks 2 i + h of the column's Bt row (with the 256-byte
+// row swizzle the 8 threads of a quarter warp hit 8 distinct bank groups);
+// the two k halves meet in one shuffle before the scale.
+template <int R, int NR, int M>
+LORA_DEVINL void expand_stage_half(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
+                                   uint32_t ytile, int pitch) {
+  const int cr = ct >> 1, h = ct & 1;
+  float2 acc[NR][2];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < R / 16; ++i) {
+    const int ch = 2 * i + h;
+    const uint4 w = lds128(b_s + cr * (R * 2) + (swz_row_chunk(cr, ch, R * 2) << 4));
+    const float2 b0 = make_float2(bf16lo(w.x), bf16hi(w.x)), b1 = make_float2(bf16lo(w.y), bf16hi(w.y));
+    const float2 b2 = make_float2(bf16lo(w.z), bf16hi(w.z)), b3 = make_float2(bf16lo(w.w), bf16hi(w.w));
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const float4 v0 = lds128f(v_s + (r * R + ch * 8) * 4);
+      const float4 v1 = lds128f(v_s + (r * R + ch * 8 + 4) * 4);
+      float2 a = acc[r][i & 1];
+      a = __ffma2_rn(make_float2(v0.x, v0.y), b0, a);
+      a = __ffma2_rn(make_float2(v0.z, v0.w), b1, a);
+      a = __ffma2_rn(make_float2(v1.x, v1.y), b2, a);
+      a = __ffma2_rn(make_float2(v1.z, v1.w), b3, a);
+      acc[r][i & 1] = a;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    float part = (acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y);
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    const float d = p.s_a * part;
+    if constexpr (M == kOutBf16Push) {
+      // columns (cr, cr + 1) meet in lane 4 i: one 4-byte red per pair
+      const float dn = __shfl_xor_sync(0xffffffffu, d, 2);
+      if (!(ct & 3) && cr < p.sc) red_add_bf16x2(p.prow[r] + (p.c0 + cr) * 2, pack_bf16x2_rn(d, dn));
+    } else {
+      if (h == 0 && cr < p.sc) expand_out<M, false>(p, rows, r, cr, d, ytile, pitch);
+    }
+  }
+}
+
 // r <= 32: CPT columns per thread (c = ct + i*NCT), FFMA2 over pairs of
 // columns.  (Adjacent pairs (2 ct, 2 ct + 1) with one 32-bit smem
 // read-modify-write of the y tile per row measured equal on Llama decode.)  The B chunk of a column pair is widened to fp32 once and reused
@@ -741,7 +832,9 @@ template <int R, int NR, int M>
 LORA_DEVINL void expand_stage(uint32_t b_s, uint32_t v_s, int ct, const ExpandPos& p, uint32_t rows,
                               uint32_t ytile, int pitch) {
   using C = SimtCfg<R>;
-  if constexpr (C::CPT == 1)
+  if constexpr (C::HALF)
+    expand_stage_half<R, NR, M>(b_s, v_s, ct, p, rows, ytile, pitch);
+  else if constexpr (C::CPT == 1)
     expand_stage1<R, NR, M>(b_s, v_s, ct, p, rows, ytile, pitch);
   else
     expand_stage_pairs<R, NR, C::CPT, C::NCT, M>(b_s, v_s, ct, p, rows, ytile, pitch);
@@ -1361,7 +1454,7 @@ inline bool use_tile_expand(int r) {
 template <int R>
 cudaError_t launch_expand_t(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   using C = SimtCfg<R>;
-  if constexpr (R <= LORA_TILE_MAX_R) {
+  if constexpr (R <= LORA_TILE_MAX_R || !C::LOOKAHEAD_OK) {
     if (!C::LOOKAHEAD_OK || use_tile_expand(R) || args.y_store == 3) {  // (push: staged-tile kernel only)
       static unsigned long long tmask = 0;
       cudaError_t e = set_smem_once(simt_expand_tile_kernel<R>, C::TILE_SMEM, tmask);
@@ -1392,6 +1485,7 @@ cudaError_t launch_simt_shrink(int rank, const MultiArgs& args, const PlanDev& p
     case 16: return launch_shrink_t<16>(args, pd, grid, stream);
     case 32: return launch_shrink_t<32>(args, pd, grid, stream);
     case 64: return launch_shrink_t<64>(args, pd, grid, stream);
+    case 128: return launch_shrink_t<128>(args, pd, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1402,6 +1496,7 @@ cudaError_t launch_simt_expand(int rank, const MultiArgs& args, const PlanDev& p
     case 16: return launch_expand_t<16>(args, pd, grid, stream);
     case 32: return launch_expand_t<32>(args, pd, grid, stream);
     case 64: return launch_expand_t<64>(args, pd, grid, stream);
+    case 128: return launch_expand_t<128>(args, pd, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1411,6 +1506,7 @@ int simt_sj_max(int rank) {
     case 8: return SimtCfg<8>::SJ_MAX;
     case 16: return SimtCfg<16>::SJ_MAX;
     case 32: return SimtCfg<32>::SJ_MAX;
+    case 128: return SimtCfg<128>::SJ_MAX;
     default: return SimtCfg<64>::SJ_MAX;
   }
 }
@@ -1419,6 +1515,7 @@ int simt_sc_max(int rank) {
     case 8: return SimtCfg<8>::SC_MAX;
     case 16: return SimtCfg<16>::SC_MAX;
     case 32: return SimtCfg<32>::SC_MAX;
+    case 128: return SimtCfg<128>::SC_MAX;
     default: return SimtCfg<64>::SC_MAX;
   }
 }
@@ -1427,15 +1524,22 @@ int simt_shrink_smem(int rank) {
     case 8: return SimtCfg<8>::SHRINK_SMEM;
     case 16: return SimtCfg<16>::SHRINK_SMEM;
     case 32: return SimtCfg<32>::SHRINK_SMEM;
+    case 128: return SimtCfg<128>::SHRINK_SMEM;
     default: return SimtCfg<64>::SHRINK_SMEM;
   }
 }
 int simt_expand_smem(int rank) {
+  // the larger of the two expand kernels' dynamic shared memory
+  auto of = [](auto c) {
+    using C = decltype(c);
+    return C::LOOKAHEAD_OK ? std::max(C::EXPAND_SMEM, C::TILE_SMEM) : C::TILE_SMEM;
+  };
   switch (rank) {
-    case 8: return SimtCfg<8>::LOOKAHEAD_OK ? std::max(SimtCfg<8>::EXPAND_SMEM, SimtCfg<8>::TILE_SMEM) : SimtCfg<8>::TILE_SMEM;
-    case 16: return SimtCfg<16>::LOOKAHEAD_OK ? std::max(SimtCfg<16>::EXPAND_SMEM, SimtCfg<16>::TILE_SMEM) : SimtCfg<16>::TILE_SMEM;
-    case 32: return SimtCfg<32>::EXPAND_SMEM;
-    default: return SimtCfg<64>::EXPAND_SMEM;
+    case 8: return of(SimtCfg<8>{});
+    case 16: return of(SimtCfg<16>{});
+    case 32: return of(SimtCfg<32>{});
+    case 128: return of(SimtCfg<128>{});
+    default: return of(SimtCfg<64>{});
   }
 }
 

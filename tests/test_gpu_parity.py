@@ -140,7 +140,7 @@ def test_fill_rows_matches_generator(B):
     np.testing.assert_array_equal(x.cpu().numpy().view(np.uint16), ref)
 
 
-@pytest.mark.parametrize("rank", [8, 16, 32, 64])
+@pytest.mark.parametrize("rank", [8, 16, 32, 64, 128])
 def test_fill_store_equals_loaded_weights(B, rank):
     """Server filled on device == server loaded from numpy-generated weights (bit-exact y)."""
     E, n_ad, h_in, h_out, T = 2, 3, 128, 192, 40
@@ -169,7 +169,8 @@ def test_fill_store_equals_loaded_weights(B, rank):
 # ---------------------------------------------------------------------------
 # exact-integer probes: bit-exact on every kernel path
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("rank,small_max", [(8, None), (16, None), (64, -1), (64, 0), (64, 4)])
+@pytest.mark.parametrize("rank,small_max", [(8, None), (16, None), (32, None), (64, -1), (64, 0), (64, 4),
+                                            (128, None)])
 def test_exact_integer_probes(B, rank, small_max):
     rng = np.random.default_rng(rank * 10 + (3 if small_max is None else small_max + 2))
     E, n_ad, h_in, h_out, T = 2, 40, 128, 256, 300   # widths multiple of 128: tcgen05-eligible
@@ -628,9 +629,26 @@ def test_small_rank_bf16_full_parity(B, rank):
         B.lora_server_destroy(s)
 
 
+@pytest.mark.parametrize("y_dtype,T", [("bf16", 600), ("fp32", 600), ("bf16", 24), ("fp32", 4000)])
+def test_rank128_full_parity(B, y_dtype, T):
+    """r = 128 (the top of the paper's "r typically 32-128"): the
+    mma.sync shrink with one 16-row M tile per consumer warp and the expand
+    with two threads per output column; every element checked, with and
+    without the device K-split (T = 24: few items, split; T = 4000: whole K)."""
+    cfg = dataclasses.replace(_mid_cfg(rank=128, T=T), y_dtype=y_dtype)
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    try:
+        ys = _run_multi(B, s, cfg, b, [0, 1])
+        for i in range(2):
+            U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"r=128 {y_dtype} T={T} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
 @pytest.mark.parametrize("loopback,y_dtype,rank,transport", [
     (False, "bf16", 64, "push"), (True, "fp32", 64, "push"), (True, "bf16", 64, "push"), (True, "bf16", 16, "push"),
-    (True, "fp32", 16, "push"), (True, "fp32", 8, "nccl"),
+    (True, "fp32", 16, "push"), (True, "fp32", 8, "nccl"), (True, "bf16", 128, "push"), (True, "fp32", 128, "push"),
     (True, "fp32", 64, "nccl"), (True, "bf16", 64, "nccl")])
 def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
     """Sharded server at G = 1.  In place (no exchange): bit-identical to the
