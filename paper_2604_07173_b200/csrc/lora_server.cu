@@ -172,6 +172,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (const char* e = std::getenv("LORA_TCE_FLAGS")) s->tc_flags = std::atoi(e);
   if (const char* e = std::getenv("LORA_TC_PAIR")) s->tc_pair = std::atoi(e) != 0;
   if (const char* e = std::getenv("LORA_TC_LPT")) s->tc_lpt = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LORA_PDL_TC")) s->pdl_tc = std::atoi(e) != 0;
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
   s->simt_split_items = 2 * 2 * s->sm_count;  // fewer whole-K items than 2 per CUDA-core CTA: split K
   if (const char* e = std::getenv("LORA_TC_MIN_ROWS")) s->tc_min_rows = std::atoi(e);
@@ -878,6 +879,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
             targs.kc_task[targs.t[i].kc_base + k] = (uint8_t)i;
         }
       }
+      g_pdl_allow = s->pdl_tc;  // tcgen05 chain on its own stream: shrink -> (vreduce) -> expand
       pi = prof_start(s, tst);
       CK(s, launch_tc_shrink(targs, p->dev, p->T, grid, tst));
       prof_stop(s, pi, kKTcShrink, tst);
@@ -889,6 +891,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       pi = prof_start(s, tst);
       CK(s, launch_tc_expand(args, p->dev, grid, tst));
       prof_stop(s, pi, kKTcExpand, tst);
+      g_pdl_allow = !tc;
     }
     pi = prof_start(s, st);
     CK(s, launch_simt_shrink(s->r, sargs, p->dev, grid, st));

@@ -35,6 +35,7 @@ struct lora_server {
   int tc_min_rows = 256;    // segmenter: tcgen05 tiles only with at least this many rows in large segments (env LORA_TC_MIN_ROWS)
   int simt_split_items = 0;  // MultiArgs::simt_split_items (set at create: 8 items per CUDA-core CTA; env LORA_SIMT_SPLIT)
   bool tc_pair = true;
+  bool pdl_tc = false;      // PDL between the tcgen05 chain's kernels on a forking apply (env LORA_PDL_TC=1)
   bool tc_lpt = true;       // tcgen05 shrink items longest first (env LORA_TC_LPT=0: slot order)      // tcgen05 shrink: slots sharing x in one N = 2r MMA (env LORA_TC_PAIR=0: off)
   int tc_ki_max = 1 << 20;  // large-batch tcgen05 shrink: max h_in per item, default the whole h_in (env LORA_TC_KI_MAX)
   int world = 1, shard_rank = 0;
