@@ -35,8 +35,9 @@ __device__ long long g_seg_t[16];
 #define SEG_T(k) do {} while (0)
 #endif
 
-// Block-wide exclusive scan of one int per thread.  Returns the exclusive
-// prefix; *total receives the block sum.  `tmp` holds >= 33 ints.
+// Block-wide exclusive scan of one int per thread (NT threads).  Returns the
+// exclusive prefix; *total receives the block sum.  `tmp` holds >= 33 ints.
+template <int NT = kSegThreads>
 __device__ int block_exclusive_scan(int v, int* tmp, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = v;
@@ -48,7 +49,7 @@ __device__ int block_exclusive_scan(int v, int* tmp, int* total) {
   if (lane == 31) tmp[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int w = (lane < (kSegThreads / 32)) ? tmp[lane] : 0;
+    int w = (lane < (NT / 32)) ? tmp[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, w, o);
@@ -58,7 +59,7 @@ __device__ int block_exclusive_scan(int v, int* tmp, int* total) {
   }
   __syncthreads();
   const int warp_excl = (warp == 0) ? 0 : tmp[warp - 1];
-  const int tot = tmp[kSegThreads / 32 - 1];
+  const int tot = tmp[NT / 32 - 1];
   __syncthreads();
   *total = tot;
   return warp_excl + x - v;
@@ -92,8 +93,8 @@ __host__ __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 // mask from 8 ballots; match.any's cost grows with the number of distinct
 // values) and take ranks in lane order on top of the warp's running count for
 // that digit.  A block scan over (digit, warp) in digit-major order then
-// gives every (warp, digit) its output base.  cnt: [32 warps][256] ints.
-template <int EPT>
+// gives every (warp, digit) its output base.  cnt: [NT / 32 warps][256] ints.
+template <int EPT, int NT = kSegThreads>
 __device__ void radix_pass8(const uint32_t* in, uint32_t* out, int shift, int* cnt, int* scan_tmp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int* wc = cnt + warp * 256;
@@ -123,8 +124,11 @@ __device__ void radix_pass8(const uint32_t* in, uint32_t* out, int shift, int* c
     __syncwarp();
   }
   __syncthreads();
-  // exclusive scan over (digit, warp), digit-major: thread t sums digit t/4, warps 8(t%4) .. +8
-  const int d0 = tid >> 2, w0 = (tid & 3) * 8;
+  // exclusive scan over (digit, warp), digit-major: 256 x NT/32 entries, 8 per
+  // thread -- thread t sums digit t / (NT/256), warps 8 (t % (NT/256)) .. +8
+  static_assert(NT % 256 == 0, "radix pass thread count");
+  constexpr int DPT = NT / 256;
+  const int d0 = tid / DPT, w0 = (tid % DPT) * 8;
   int c[8], sum = 0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -132,7 +136,7 @@ __device__ void radix_pass8(const uint32_t* in, uint32_t* out, int shift, int* c
     sum += c[q];
   }
   int total;
-  int run = block_exclusive_scan(sum, scan_tmp, &total);
+  int run = block_exclusive_scan<NT>(sum, scan_tmp, &total);
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     cnt[(w0 + q) * 256 + d0] = run;
@@ -148,7 +152,7 @@ __device__ void radix_pass8(const uint32_t* in, uint32_t* out, int shift, int* c
 }
 
 // builds composites and sorts them; returns the buffer holding the result
-template <int EPT>
+template <int EPT, int NT>
 __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids,
                                 int T, int E, int n_adapters, const Placement& pl, const int32_t* cache, int K, int kb, int ib,
                                 uint32_t* A, uint32_t* B, int* cnt, int* err_flag, int* n_valid_out,
@@ -161,13 +165,13 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
   int ad[EPT], ex[EPT];
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const int i = r * kSegThreads + tid;
+    const int i = r * NT + tid;
     ad[r] = i < T ? __ldg(adapter_ids + i) : -1;
     ex[r] = (i < T && expert_ids) ? __ldg(expert_ids + i) : 0;
   }
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const int i = r * kSegThreads + tid;
+    const int i = r * NT + tid;
     int key = -1;
     if (i < T) key = key_of(ad[r], ex[r], E, n_adapters, pl, bad, cache);
     nv += key >= 0;
@@ -176,13 +180,13 @@ __device__ uint32_t* radix_sort(const int32_t* __restrict__ adapter_ids, const i
   if (bad) atomicOr(err_flag, 1);
   int total;
   SEG_T(1);
-  block_exclusive_scan(nv, scan_tmp, &total);  // its barriers also publish A
+  block_exclusive_scan<NT>(nv, scan_tmp, &total);  // its barriers also publish A
   SEG_T(2);
   *n_valid_out = total;
   uint32_t* in = A;
   uint32_t* out = B;
   for (int sh = 0; sh < kb; sh += 8) {
-    radix_pass8<EPT>(in, out, ib + sh, cnt, scan_tmp);
+    radix_pass8<EPT, NT>(in, out, ib + sh, cnt, scan_tmp);
     SEG_T(3 + sh / 8);
     uint32_t* t = in;
     in = out;
@@ -269,8 +273,10 @@ __device__ void bitonic_sort(const int32_t* __restrict__ adapter_ids, const int3
 // ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
-template <bool radix>
-__global__ void __launch_bounds__(kSegThreads, 1)
+// NT threads: 1024, or 256 / 512 for small batches (radix path only; the
+// block-wide barriers and scans of a smaller CTA are cheaper)
+template <bool radix, int NT>
+__global__ void __launch_bounds__(NT, 1)
     segment_kernel(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T, int P,
                    int E, int n_adapters, int kb, int ib, SegParams sp, PlanDev pd,
                    int* __restrict__ err_flag, const int* __restrict__ T_dev) {
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     // T and P above are the capacity the shared memory was sized for; sort
     // only the actual rows (P = the padded size of those, fewer radix rounds)
     T = min(T, max(*T_dev, 0));
-    int p2 = kSegThreads;
+    int p2 = NT;
     while (p2 < T) p2 <<= 1;
     P = p2;
     int b = 0;
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   __shared__ int scan_tmp[40];
   __shared__ int s_nvalid;
   const int tid = threadIdx.x;
-  const int EPT = P / kSegThreads;
+  const int EPT = P / NT;
 
   // 1.+2. composites + sort; afterwards key(j) / row(j) of sorted position j
   const uint32_t* srt32 = nullptr;
@@ -307,11 +313,11 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     const int K = n_adapters * E;
     uint32_t* res = nullptr;
     switch (EPT) {
-      case 1: res = radix_sort<1>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      case 2: res = radix_sort<2>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      case 4: res = radix_sort<4>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      case 8: res = radix_sort<8>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
-      default: res = radix_sort<16>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 1: res = radix_sort<1, NT>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 2: res = radix_sort<2, NT>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 4: res = radix_sort<4, NT>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      case 8: res = radix_sort<8, NT>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
+      default: res = radix_sort<16, NT>(adapter_ids, expert_ids, T, E, n_adapters, pl, cache, K, kb, ib, A, B, cnt, err_flag, &s_nvalid, scan_tmp); break;
     }
     srt32 = res;
     segoff_s = reinterpret_cast<int*>(res == A ? B : A);  // the free buffer (P + 1 ints reserved)
@@ -341,10 +347,10 @@ __global__ void __launch_bounds__(kSegThreads, 1)
 
   SEG_T(6);
   // 3. perm + segment heads (each thread a contiguous chunk, so the scan is in order)
-  const int chunk = (n_valid + kSegThreads - 1) / kSegThreads;
+  const int chunk = (n_valid + NT - 1) / NT;
   const int j0 = min(tid * chunk, n_valid), j1 = min(j0 + chunk, n_valid);
   // perm written coalesced (position tid + 1024 m), heads counted per chunk
-  for (int j = tid; j < n_valid; j += kSegThreads) pd.perm[j] = row_at(j);
+  for (int j = tid; j < n_valid; j += NT) pd.perm[j] = row_at(j);
   int heads = 0;
   int prev = j0 > 0 ? key_at(j0 - 1) : -1;
   for (int j = j0; j < j1; ++j) {
@@ -353,7 +359,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     prev = k;
   }
   int S;
-  int seg = block_exclusive_scan(heads, scan_tmp, &S);
+  int seg = block_exclusive_scan<NT>(heads, scan_tmp, &S);
   prev = j0 > 0 ? key_at(j0 - 1) : -1;
   for (int j = j0; j < j1; ++j) {
     const int k = key_at(j);
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
 
   SEG_T(7);
   // 4. work lists: CUDA-core groups (<= kGroupRows rows) and tcgen05 tiles (<= sp.tile_rows)
-  const int schunk = (S + kSegThreads - 1) / kSegThreads;
+  const int schunk = (S + NT - 1) / NT;
   const int s0 = min(tid * schunk, S), s1 = min(s0 + schunk, S);
   // the tcgen05 chain only pays off with enough rows in large segments
   // (a handful of tiles run latency-bound on a few SMs): else all groups
@@ -383,7 +389,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     if (size > sp.small_max) big += size;
   }
   int BIG;
-  (void)block_exclusive_scan(big, scan_tmp, &BIG);
+  (void)block_exclusive_scan<NT>(big, scan_tmp, &BIG);
   const bool use_tc = sp.tc_enabled && BIG >= sp.tc_min_rows;
   int ng = 0, nt = 0;
   for (int s = s0; s < s1; ++s) {
@@ -393,9 +399,11 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     else
       ng += (size + kGroupRows - 1) / kGroupRows;
   }
-  int NG, NT;
-  int g = block_exclusive_scan(ng, scan_tmp, &NG);
-  int t = block_exclusive_scan(nt, scan_tmp, &NT);
+  // both list counts in one scan (each < 2^16: T <= 16384)
+  int NGT;
+  const int gt = block_exclusive_scan<NT>(ng | (nt << 16), scan_tmp, &NGT);
+  const int NG = NGT & 0xFFFF, NTL = NGT >> 16;
+  int g = gt & 0xFFFF, t = gt >> 16;
   for (int s = s0; s < s1; ++s) {
     const int b = segoff_s[s], size = segoff_s[s + 1] - b, key = key_at(b);
     const bool tc = use_tc && size > sp.small_max;
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     pd.counts[kCntValid] = n_valid;
     pd.counts[kCntSegs] = S;
     pd.counts[kCntGroups] = NG;
-    pd.counts[kCntTiles] = NT;
+    pd.counts[kCntTiles] = NTL;
   }
 }
 
@@ -609,10 +617,11 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     else
       ng += (size + kGroupRows - 1) / kGroupRows;
   }
-  int S, NG, NT;
+  int S, NGT;
   int seg = block_exclusive_scan(heads, scan_tmp, &S);
-  int g = block_exclusive_scan(ng, scan_tmp, &NG);
-  int t = block_exclusive_scan(nt, scan_tmp, &NT);
+  const int gt = block_exclusive_scan(ng | (nt << 16), scan_tmp, &NGT);  // both counts < 2^16
+  const int NG = NGT & 0xFFFF, NT = NGT >> 16;
+  int g = gt & 0xFFFF, t = gt >> 16;
   for (int k = k0; k < k1; ++k) {
     const int b = kstart[pad32(k)], size = kstart[pad32(k + 1)] - b;
     if (size == 0) continue;
@@ -727,31 +736,45 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
       }
     }
   }
-  int P = kSegThreads;  // at least one composite per thread
+  const int kb = bits_for((long long)n_adapters * E);  // key K = n_adapters*E marks "no LoRA" (sorts last)
+  // CTA size: small batches on 256 / 512 threads (radix path), else 1024
+  // (device T: T is the capacity).  LORA_SEG_NT=1024 (tuning hook): always 1024
+  int nt = T <= 256 ? 256 : T <= 512 ? 512 : kSegThreads;
+  if (const char* e = getenv("LORA_SEG_NT")) nt = std::max(nt, atoi(e) >= kSegThreads ? kSegThreads : nt);
+  int P = nt;  // at least one composite per thread
   while (P < T) P <<= 1;
   const int ib = bits_for(P - 1);
-  const int kb = bits_for((long long)n_adapters * E);  // key K = n_adapters*E marks "no LoRA" (sorts last)
   const int radix = (ib + kb <= 32) ? 1 : 0;
+  if (!radix) {  // bitonic fallback: 1024 threads
+    nt = kSegThreads;
+    P = std::max(P, kSegThreads);
+  }
   // radix: two u32 buffers (+1 int for the last segment offset); bitonic: u64 buffer + P+1 ints
-  const int smem = radix ? (2 * (P + P / 32) + 8 + 32 * 256) * 4 : P * 8 + (P + 1) * 4;
+  const int smem = radix ? (2 * (P + P / 32) + 8 + (nt / 32) * 256) * 4 : P * 8 + (P + 1) * 4;
   static unsigned long long attr_set = 0;  // per-device bitmask
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set & (1ull << dev))) {
     const int mx = std::max((2 * (kMaxPlanRows + kMaxPlanRows / 32) + 8 + 32 * 256) * 4,
                             kMaxPlanRows * 8 + (kMaxPlanRows + 1) * 4);
-    cudaError_t e = cudaFuncSetAttribute(segment_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaError_t e = cudaFuncSetAttribute(segment_kernel<true, kSegThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(segment_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      e = cudaFuncSetAttribute(segment_kernel<false, kSegThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
     attr_set |= 1ull << dev;
   }
-  if (radix)
-    segment_kernel<true><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp,
-                                                           pd, err_flag, T_dev);
+  if (radix && nt == 256)
+    segment_kernel<true, 256><<<1, 256, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp, pd,
+                                                        err_flag, T_dev);
+  else if (radix && nt == 512)
+    segment_kernel<true, 512><<<1, 512, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp, pd,
+                                                        err_flag, T_dev);
+  else if (radix)
+    segment_kernel<true, kSegThreads><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters,
+                                                                        kb, ib, sp, pd, err_flag, T_dev);
   else
-    segment_kernel<false><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters, kb, ib, sp,
-                                                            pd, err_flag, T_dev);
+    segment_kernel<false, kSegThreads><<<1, kSegThreads, smem, stream>>>(adapter_ids, expert_ids, T, P, E, n_adapters,
+                                                                         kb, ib, sp, pd, err_flag, T_dev);
   return cudaGetLastError();
 }
 
