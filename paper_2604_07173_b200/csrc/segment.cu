@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   const int tid = threadIdx.x, c = blockIdx.x;
   const int row0 = c * RPC;
   const uint32_t K = (uint32_t)n_adapters * E;
+  pdl_launch_dependents();  // seg_scan (PDL) may be scheduled; it waits for this grid
   if (blockIdx.x == 0) SEG_T(12);
   int ad[EPT], ex[EPT];
 #pragma unroll
@@ -538,6 +539,8 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   const int tid = threadIdx.x;
   const long long N = (long long)K * C;
   int carry = 0;
+  pdl_wait();               // seg_local's histogram is complete
+  pdl_launch_dependents();  // seg_scatter (PDL) may be scheduled
   SEG_T(9);
   for (long long base = 0; base < N; base += ROUND) {
     const int n = (int)min((long long)ROUND, N - base);
@@ -661,6 +664,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_scatter_kernel(int T, int K, 
   constexpr int RPC = kSegThreads * EPT;
   pdl_launch_dependents();  // the shrink kernels may launch now; they wait for this grid
   const int c = blockIdx.x, row0 = c * RPC;
+  pdl_wait();  // seg_scan's offsets are complete
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int p = r * kSegThreads + threadIdx.x;
@@ -668,6 +672,15 @@ __global__ void __launch_bounds__(kSegThreads) seg_scatter_kernel(int T, int K, 
     const int k = (int)(v >> kLocBits);
     if (k < K) pd.perm[pd.offs[(long long)k * C + c] + pd.lrank[row0 + p]] = row0 + (int)(v & ((1u << kLocBits) - 1u));
   }
+}
+
+// PDL inside the multi-CTA segmenter chain (env LORA_SEG_PDL=0: plain launches)
+bool seg_pdl() {
+  static const bool on = [] {
+    const char* v = std::getenv("LORA_SEG_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 int bits_for(long long v) {  // bits needed to represent v (v >= 0)
@@ -729,9 +742,26 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
       {
         auto local = ept == 1 ? seg_local_kernel<1> : ept == 2 ? seg_local_kernel<2> : seg_local_kernel<4>;
         auto scatter = ept == 1 ? seg_scatter_kernel<1> : ept == 2 ? seg_scatter_kernel<2> : seg_scatter_kernel<4>;
+        // seg_local waits for everything before it on the stream (the previous
+        // applies still read the plan); seg_scan and seg_scatter are launched
+        // programmatically dependent (PDL) on their predecessor in the chain
         local<<<C, kSegThreads, lsm, stream>>>(adapter_ids, expert_ids, T, E, n_adapters, kb, C, sp, pd, err_flag);
-        seg_scan_kernel<<<1, kSegThreads, ssm, stream>>>((int)K, C, sp, pd);
-        scatter<<<C, kSegThreads, 0, stream>>>(T, (int)K, C, pd);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = seg_pdl() ? 1 : 0;
+        cudaLaunchConfig_t cfg = {};
+        cfg.blockDim = dim3(kSegThreads);
+        cfg.stream = stream;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(1);
+        cfg.dynamicSmemBytes = ssm;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, seg_scan_kernel, (int)K, C, sp, pd);
+        if (e != cudaSuccess) return e;
+        cfg.gridDim = dim3(C);
+        cfg.dynamicSmemBytes = 0;
+        e = cudaLaunchKernelEx(&cfg, scatter, T, (int)K, C, pd);
+        if (e != cudaSuccess) return e;
         return cudaGetLastError();
       }
     }
