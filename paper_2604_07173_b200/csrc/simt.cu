@@ -32,6 +32,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef LORA_EXP_PROBE
+#define LORA_EXP_PROBE 0  // staged-tile expand timing probes (A/B only; results wrong): bit 0 no consumer work, bit 1 no y loads
+#endif
 #ifndef LORA_TILE_MAX_R
 #define LORA_TILE_MAX_R 64  // staged-tile expand at every rank (measured: r = 64 expand 1302 -> 1254 us on config 5)
 #endif
@@ -1260,6 +1263,7 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
       // bf16 hi/lo split of v, measured slower: Llama decode expand 180 ->
       // 223 us -- the stage's cost is the per-element y update, not the dot
       // products -- so the expand keeps the FFMA2 consumers)
+      if (!(LORA_EXP_PROBE & 1)) {  // (timing probe bit 0: no consumer arithmetic, no y stores; results wrong)
       switch (nr) {
         case 1: expand_stage<R, 1, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
         case 2: expand_stage<R, 2, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
@@ -1270,9 +1274,10 @@ __device__ __forceinline__ void simt_expand_tile_consumers(const MultiArgs& args
         case 7: expand_stage<R, 7, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
         default: expand_stage<R, 8, M>(b_s, v_s, ct, p, rows, yt, pitch); break;
       }
+      }
       if constexpr (TILE) {
         named_bar_sync(1, C::NCT);  // the whole tile is final
-        if (sch < (p.sc >> 3)) {
+        if (!(LORA_EXP_PROBE & 1) && sch < (p.sc >> 3)) {
           uint16_t* yb = static_cast<uint16_t*>(p.y) + p.c0 + sch * 8;
           for (int r = rsub; r < nr; r += RSTEP) {
             const uint4 v = lds128(yt + r * pitch + sch * 16);
@@ -1334,7 +1339,7 @@ __global__ void __launch_bounds__(SimtCfg<R>::TILE_THREADS, 2)
   } else if (warp == C::NWC) {
     // ===================== producer: B rows, v rows, y chunks of resolved items =====================
     if (lane == 0) {
-      const bool load_y = args.y_store == 0 && !args.y_fp32;
+      const bool load_y = args.y_store == 0 && !args.y_fp32 && !(LORA_EXP_PROBE & 2);  // (probe bit 1: no y loads)
       const uint64_t pol = (args.tc_flags & 8) ? policy_evict_last() : policy_evict_first();  // B (bit 3)
       int stage = 0;
       uint32_t phase = 0;
