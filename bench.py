@@ -424,6 +424,24 @@ def secondaries(B, torch, dev, stream, hbm_peak, steps, warmup):
         "workload": "config-3 shapes (Mixtral gate/up/down, top-2, 512 tokens, Zipf 1.2) with 128 adapters at "
                     "r = 16 / 32 / 128 (P:165)",
         "points": sweep}
+    # the same at prefill shapes (config 4: 8192 tokens, 16384 rows): the
+    # tcgen05 chain at every rank (r = 64 is config 4 itself, above)
+    sweep = {}
+    for rk in (16, 32, 128):
+        c4 = dataclasses.replace(li.CONFIGS["mixtral_prefill"], name=f"mixtral_prefill_r{rk}", rank=rk)
+        b4 = li.make_batch(c4)
+        slots = list(range(len(c4.slots)))
+        r = SingleRun(B, torch, c4, b4, slots, dev, stream)
+        t4, tot4 = r.time(max(5, steps // 2), 2)
+        prof4 = r.profile(3)
+        sm = summarise(c4, algorithmic(c4, b4, slots), t4, tot4, hbm_peak, prof4, 3)
+        r.destroy()
+        sweep[str(rk)] = {k: sm[k] for k in ("ms_per_step", "ms_median", "tokens_per_s", "rows", "step_GBs",
+                                             "frac_measured", "kernels")}
+    out["prefill_rank_sweep"] = {
+        "workload": "config-4 shapes (Mixtral gate/up/down, 4 x 2048-token sequences, 64 adapters, top-2) at "
+                    "r = 16 / 32 / 128 (P:165); large segments on the tcgen05 chain at every rank",
+        "points": sweep}
     return out
 
 

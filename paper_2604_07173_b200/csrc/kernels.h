@@ -103,7 +103,7 @@ struct PlanDev {
 
 struct SegParams {
   int small_max;   // segments with more rows than this go to tcgen05 (if enabled)
-  int tc_enabled;  // rank 64 and not forced off
+  int tc_enabled;  // a tcgen05 rank (16 / 32 / 64 / 128) and not forced off
   int tc_min_rows; // tcgen05 tiles only if the large segments hold at least this many rows in total
   int tile_rows;
   Placement pl;    // rows whose adapter this rank does not store are rejected (flagged)
@@ -226,10 +226,13 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
                            const int* T_dev = nullptr);
 cudaError_t launch_simt_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 cudaError_t launch_simt_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
-cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid, cudaStream_t stream);
-cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
-cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+// tcgen05 chain at rank 16 / 32 / 64 / 128 (tc_rank_supported)
+cudaError_t launch_tc_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int x_rows, int grid,
+                             cudaStream_t stream);
+cudaError_t launch_tc_vreduce(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
+cudaError_t launch_tc_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream);
 bool tc_available();
+bool tc_rank_supported(int rank);
 
 // synthetic fill / weight relayout (synth_fill.cu)
 cudaError_t launch_fill_store(uint16_t* At, uint16_t* Bt, int h_in, int h_out, int E, int r, long long units,

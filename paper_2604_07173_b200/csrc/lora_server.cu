@@ -175,6 +175,9 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (const char* e = std::getenv("LORA_PDL_TC")) s->pdl_tc = std::atoi(e) != 0;
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
   s->simt_split_items = 2 * 2 * s->sm_count;  // fewer whole-K items than 2 per CUDA-core CTA: split K
+  // r != 64: the CUDA-core kernels are tuned for decode batches at every rank;
+  // the tcgen05 chain takes the large segments of prefill-sized batches only
+  if (s->r != 64) s->tc_min_rows = 2048;
   if (const char* e = std::getenv("LORA_TC_MIN_ROWS")) s->tc_min_rows = std::atoi(e);
   if (const char* e = std::getenv("LORA_SIMT_SPLIT")) s->simt_split_items = std::atoi(e);
   if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -620,9 +623,9 @@ void plan_destroy_impl(lora_plan* p) {
   delete p;
 }
 
-// tcgen05 path: rank 64, every slot's item widths multiples of the 128-wide MMA tiles
+// tcgen05 path: rank 16 / 32 / 64 / 128, every slot's item widths multiples of the 128-wide MMA tiles
 static bool tc_enabled(const lora_server* s) {
-  if (!tc_available() || s->r != 64 || s->small_seg_max < 0) return false;
+  if (!tc_available() || !tc_rank_supported(s->r) || s->small_seg_max < 0) return false;
   for (const auto& sl : s->slots)
     if (sl.KI % 128 || sl.CI % 128) return false;
   return true;
@@ -881,15 +884,15 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       }
       g_pdl_allow = s->pdl_tc;  // tcgen05 chain on its own stream: shrink -> (vreduce) -> expand
       pi = prof_start(s, tst);
-      CK(s, launch_tc_shrink(targs, p->dev, p->T, grid, tst));
+      CK(s, launch_tc_shrink(s->r, targs, p->dev, p->T, grid, tst));
       prof_stop(s, pi, kKTcShrink, tst);
       if (any_split) {  // tiles of a task with n_kc == 1 got their v from the shrink
         pi = prof_start(s, tst);
-        CK(s, launch_tc_vreduce(args, p->dev, grid, tst));
+        CK(s, launch_tc_vreduce(s->r, args, p->dev, grid, tst));
         prof_stop(s, pi, kKTcVreduce, tst);
       }
       pi = prof_start(s, tst);
-      CK(s, launch_tc_expand(args, p->dev, grid, tst));
+      CK(s, launch_tc_expand(s->r, args, p->dev, grid, tst));
       prof_stop(s, pi, kKTcExpand, tst);
       g_pdl_allow = !tc;
     }

@@ -9,18 +9,22 @@
 // pipelines:
 //
 //   shrink item (task, kc, tile<=128 rows):
-//       D[128 rows x 64] (TMEM, fp32) = X_tile[128 x KI] . A_u[KI x 64]
+//       D[128 rows x r] (TMEM, fp32) = X_tile[128 x KI] . A_u[KI x r]
 //       A operand = gathered activation rows (cp.async, manual 128B swizzle)
-//       B operand = pre-swizzled At store tiles (1-D TMA bulk copy)
-//       epilogue: TMEM -> regs -> vpart[kc][row][0:64] (fp32 partial sums)
-//   expand item (task, ci, tile<=128 rows), swap-AB so TMEM lanes = columns:
-//       D[128 cols x N rows] = Bt[128 cols x 64] . v^T[64 x N]   (per 128-col sub-tile)
-//       A operand = pre-swizzled Bt store rows (1-D TMA bulk copy)
-//       B operand = v tile (sum of vpart over kc, rounded to bf16, swizzled)
-//       epilogue: TMEM -> regs -> y[perm[n]][c] = round(y + s_a * D)  (coalesced over c)
+//       B operand = pre-swizzled At store tiles (1-D TMA bulk copy); gate + up
+//                   in one N = 2r MMA (x gathered once)
+//       epilogue: TMEM -> regs -> v (bf16, whole K) or vpart[kc][row][0:r]
+//   expand item (task, ci, tile<=128 rows), per 128-column sub-tile:
+//       D[128 rows x 128 cols] (TMEM lane = tile row) = v_tile[128 x r] . Bt_sub[128 cols x r]^T
+//       A operand = v tile (bf16, pre-swizzled, 1-D TMA bulk copy per K block)
+//       B operand = pre-swizzled Bt store rows (1-D TMA bulk copy; r = 128:
+//                   re-tiled into two 64-wide K blocks by the producer warp)
+//       epilogue: TMEM -> regs -> y[perm[n]][c] = round(y + s_a * D)
 //
-// UMMA operands are K-major SWIZZLE_128B (rows of 128 B, 8-row groups 1024 B
-// apart); the instruction descriptor selects bf16 x bf16 -> fp32.
+// Ranks 16 / 32 / 64 / 128 (template R): the x tiles and At tiles are K-major
+// SWIZZLE_128B at every rank (64 k per atom, N = r rows); the expand's K = r
+// operands use SWIZZLE_32B / 64B / 128B rows of min(2r, 128) bytes (KGeo).
+// The instruction descriptor selects bf16 x bf16 -> fp32.
 #include <cstdlib>
 #include <cstring>
 
@@ -104,8 +108,45 @@ LORA_DEVINL uint8_t* align1024(uint8_t* p) {
 }
 
 
-constexpr int R = 64;  // tcgen05 path rank
 constexpr int kQD = 4;  // work-queue depth
+
+// K-major operand geometry of rank R in the expand MMA (K = R) and in the
+// tcgen05 path's bf16 v store: rows of RB = min(2R, 128) bytes with the
+// matching UMMA swizzle (SWIZZLE_32B / 64B / 128B for r = 16 / 32 / >= 64;
+// 16-byte chunk c of row n at swz_row_chunk(n, c, RB)), r = 128 as KB = 2
+// blocks of 64 k.  The Bt store rows of r <= 64 already have exactly this
+// layout (common.cuh); r = 128 Bt rows are 256 bytes and are re-tiled into
+// two SWIZZLE_128B blocks by the expand's producer warp.
+template <int R>
+struct KGeo {
+  static_assert(R == 16 || R == 32 || R == 64 || R == 128, "tcgen05 ranks");
+  static constexpr int RB = R >= 64 ? 128 : R * 2;  // bytes per row of one K block (= swizzle width)
+  static constexpr int KB = R >= 64 ? R / 64 : 1;   // K blocks
+  static constexpr int KPB = RB / 32;               // 16-element MMA k-steps per K block
+  static constexpr int CPB = RB / 16;               // 16-byte chunks per row of a K block
+};
+
+// K-major shared-memory matrix descriptor (sm_100 format) for swizzle width
+// RB (128 / 64 / 32 bytes): 8-row core groups RB * 8 bytes apart
+template <int RB>
+LORA_DEVINL uint64_t kmajor_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);             // start address
+  d |= (uint64_t)1 << 16;                                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)((RB * 8) >> 4) << 32;                   // SBO: 8 rows
+  d |= (uint64_t)1 << 46;                                 // descriptor version (sm_100)
+  d |= (uint64_t)(RB == 128 ? 2 : RB == 64 ? 4 : 6) << 61;  // SWIZZLE_128B / 64B / 32B
+  return d;
+}
+
+// element offset of 16-byte chunk q (0 .. R/8-1) of sorted row `row` (row n of
+// its tile) in a slot's bf16 v region: [KB][max_rows][RB / 2]
+template <int R>
+LORA_DEVINL long long vbf_chunk(long long row, int n, int q, int max_rows) {
+  using G = KGeo<R>;
+  const int kb = q / G::CPB, c = q - kb * G::CPB;
+  return (long long)kb * max_rows * (G::RB / 2) + row * (G::RB / 2) + swz_row_chunk(n, c, G::RB) * 8;
+}
 
 // x tensor maps of a tcgen05 shrink launch (one per task): 2-D [T rows][h_in]
 // bf16, box {64 columns, 1 row}, SWIZZLE_128B -- the layout a TMA tile::gather4
@@ -142,7 +183,7 @@ LORA_DEVINL bool tc_cta_idle(const MultiArgs& args, const PlanDev& pd) {
 // layer) in one item -- the gathered x tile feeds one
 // N = 2r MMA whose B operand is the two slots' A tiles back to back, so x is
 // read once for both.
-template <bool PAIR>
+template <int R, bool PAIR>
 struct ShrinkCfgT {
   static constexpr int EPI_WARPS = 4;   // warps 0-3: epilogue (TMEM lanes 0-127)
   static constexpr int MMA_WARP = 4;    // warp 4: TMEM alloc + MMA issue
@@ -168,20 +209,22 @@ struct ShrinkCfgT {
   static constexpr int KS_PER_STAGE = LORA_TCS_KS;         // k-steps per stage
   static constexpr int NW = PAIR ? 2 : 1;                  // A tiles per k-step
   static constexpr int X_SUB = kTileRows * 128;            // 16 KB per k-step
-  static constexpr int W_SUB = R * 128;                    // 8 KB per k-step and slot
+  static constexpr int W_SUB = R * 128;                    // A rows of one k-step and slot (8 KB at r = 64)
   static constexpr int STAGE = KS_PER_STAGE * (X_SUB + NW * W_SUB);
-  static constexpr int NST = PAIR ? LORA_TCSP_NST : LORA_TCS_NST;
+  // r = 64: the measured depths; other ranks as many stages as fit (<= 6)
+  static constexpr int NST_FIT = (220 * 1024) / STAGE > 6 ? 6 : (220 * 1024) / STAGE;
+  static constexpr int NST = R == 64 ? (PAIR ? LORA_TCSP_NST : LORA_TCS_NST) : NST_FIT;
   static constexpr int LAG = LORA_TCS_LAG < NST - 1 ? LORA_TCS_LAG : NST - 1;  // cp.async groups kept in flight
   static constexpr int ACC_COLS = NW * R;                  // N = r (pair: 2r)
   static constexpr int TMEM_COLS = 2 * ACC_COLS;           // 2 accumulators
   static constexpr int SMEM = 1024 + NST * STAGE + 256;
   static_assert(SMEM <= 227 * 1024, "shrink stages exceed shared memory");
 };
-using ShrinkCfg = ShrinkCfgT<false>;
 
 // v row n of a tile (R fp32 sums) rounded to bf16 into the pre-swizzled
-// expand operand: 16-byte chunk q of the row at q ^ (n & 7)
-LORA_DEVINL void store_vbf_row(uint16_t* dst_row, int n, const float* v) {
+// expand operand (vbf_chunk layout)
+template <int R>
+LORA_DEVINL void store_vbf_row(uint16_t* vslot, long long row, int n, const float* v, int max_rows) {
 #pragma unroll
   for (int q = 0; q < R / 8; ++q) {
     uint4 w;
@@ -189,14 +232,14 @@ LORA_DEVINL void store_vbf_row(uint16_t* dst_row, int n, const float* v) {
     w.y = pack_bf16x2_rn(v[8 * q + 2], v[8 * q + 3]);
     w.z = pack_bf16x2_rn(v[8 * q + 4], v[8 * q + 5]);
     w.w = pack_bf16x2_rn(v[8 * q + 6], v[8 * q + 7]);
-    *reinterpret_cast<uint4*>(dst_row + ((q ^ (n & 7)) * 8)) = w;
+    *reinterpret_cast<uint4*>(vslot + vbf_chunk<R>(row, n, q, max_rows)) = w;
   }
 }
 
-template <bool REMOTE, bool PAIR>
-__global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
+template <int R, bool REMOTE, bool PAIR>
+__global__ void __launch_bounds__(9 * 32, 1)
     tc_shrink_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd, const __grid_constant__ TcMaps maps) {
-  using C = ShrinkCfgT<PAIR>;
+  using C = ShrinkCfgT<R, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::NST * C::STAGE);
@@ -458,7 +501,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
         if (row_in_tile < tile.y) {
           if (t.n_kc == 1) {
             // the whole K in one accumulator: v rounded to bf16 here (no reduction pass)
-            store_vbf_row(pd.vbf + th.vbf_off + ((long long)tile.x + row_in_tile) * R, row_in_tile, v);
+            store_vbf_row<R>(pd.vbf + th.vbf_off, (long long)tile.x + row_in_tile, row_in_tile, v, pd.max_rows);
           } else {
             float4* dst = reinterpret_cast<float4*>(pd.vpart + th.vpart_off +
                                                     ((long long)kc * pd.max_rows + tile.x + row_in_tile) * R);
@@ -490,6 +533,7 @@ __global__ void __launch_bounds__(ShrinkCfg::THREADS, 1)
 // the SWIZZLE_128B K-major layout (row n of a tile: 16-byte chunk q at
 // q ^ (n & 7)), so the expand loads its MMA operand with one bulk copy.
 // ===========================================================================
+template <int R>
 __global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
   pdl_wait();               // the tcgen05 shrink's partials are complete
   pdl_launch_dependents();
@@ -502,7 +546,7 @@ __global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__
     const long long rem = i - (long long)task * per_task;
     const int ti = (int)(rem / (kTileRows * (R / 8)));
     const int within = (int)(rem - (long long)ti * (kTileRows * (R / 8)));
-    const int n = within >> 3, q = within & 7;
+    const int n = within / (R / 8), q = within - n * (R / 8);
     const int4 tile = pd.tiles[ti];
     if (n >= tile.y) continue;
     const SlotTask& t = args.t[task];
@@ -520,7 +564,7 @@ __global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__
     w.y = pack_bf16x2_rn(s[2], s[3]);
     w.z = pack_bf16x2_rn(s[4], s[5]);
     w.w = pack_bf16x2_rn(s[6], s[7]);
-    *reinterpret_cast<uint4*>(pd.vbf + t.vbf_off + ((long long)tile.x + n) * R + ((q ^ (n & 7)) * 8)) = w;
+    *reinterpret_cast<uint4*>(pd.vbf + t.vbf_off + vbf_chunk<R>((long long)tile.x + n, n, q, pd.max_rows)) = w;
   }
 }
 
@@ -579,14 +623,19 @@ LORA_DEVINL void stg256x2(void* p, const uint32_t* w) {
 // tile, every access a full 32-byte sector.  16 epilogue warps: TMEM lane quadrant = warp % 4,
 // column block = warp / 4.
 // ===========================================================================
+template <int R>
 struct ExpandCfg {
+  using G = KGeo<R>;
   static constexpr int EPI_WARPS = 16;
   static constexpr int EPI_THREADS = EPI_WARPS * 32;
   static constexpr int TMA_WARP = 16;   // warp 16: v tile + Bt bulk copies
   static constexpr int MMA_WARP = 17;   // warp 17: TMEM alloc + MMA
   static constexpr int THREADS = 18 * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (N)
-  static constexpr int B_SUB = MSUB * R * 2;           // 16 KB of Bt rows
+  static constexpr int B_SUB = MSUB * R * 2;           // Bt rows of a sub-tile (16 KB at r = 64)
+  // r = 128: the producer warp re-tiles the 256-byte Bt rows into two
+  // SWIZZLE_128B K blocks with cp.async (all 32 lanes arrive on the stage)
+  static constexpr bool BT_RETILE = R > 64;
 #ifndef LORA_TCE_NST
 #define LORA_TCE_NST 2
 #endif
@@ -594,30 +643,33 @@ struct ExpandCfg {
 #define LORA_TCE_YD 4
 #endif
   static constexpr int NST = LORA_TCE_NST;
-  static constexpr int V_TILE = kTileRows * 128;       // 16 KB (M = 128 rows x 64 bf16)
+  static constexpr int V_TILE = kTileRows * R * 2;     // v tile, M = 128 rows x K = R (16 KB at r = 64)
+  static constexpr int VB = R > 64 ? 1 : 2;           // v tile buffers (r = 128: one, for shared memory)
   // bf16 output: y tiles [128 rows][128 cols] (16-byte chunks XOR-swizzled by
   // row) in a ring of YS slots, fetched YD-1 sub-tiles ahead
-  static constexpr int YD = LORA_TCE_YD;
+  static constexpr int YD = R > 64 ? 3 : LORA_TCE_YD;
   static constexpr int YS = YD + 1;
   static constexpr int Y_TILE = kTileRows * MSUB * 2;  // 32 KB
   static constexpr int NACC = 4;
   static constexpr int ACC_COLS = MSUB;                // N columns per accumulator
   static constexpr int TMEM_COLS = NACC * ACC_COLS;    // 512
-  static constexpr int SMEM = 1024 + NST * B_SUB + 2 * V_TILE + YS * Y_TILE + 512;
+  static constexpr int SMEM = 1024 + NST * B_SUB + VB * V_TILE + YS * Y_TILE + 512;
+  static_assert(SMEM <= 227 * 1024, "expand stages exceed shared memory");
 };
 
 // output mode M (compile time): 0 bf16 accumulate, 1 fp32 delta store, 2 bf16
 // delta store (sharded), 3 fp32 accumulate, 4 / 5 bf16 / fp32 push (sharded
 // owner: the delta is added into the origin row of the source's registered y
 // with red.add over NVLink)
-template <int M>
-__global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
+template <int R, int M>
+__global__ void __launch_bounds__(18 * 32, 1)
     tc_expand_kernel(const __grid_constant__ MultiArgs args, const PlanDev pd) {
-  using C = ExpandCfg;
+  using C = ExpandCfg<R>;
+  using G = KGeo<R>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* vtile = smem + C::NST * C::B_SUB;   // [2][V_TILE] swizzled MMA operand A
-  uint8_t* yring = vtile + 2 * C::V_TILE;      // [YS][Y_TILE] bf16 y tiles (bf16 output modes)
+  uint8_t* vtile = smem + C::NST * C::B_SUB;   // [VB][V_TILE] swizzled MMA operand A
+  uint8_t* yring = vtile + C::VB * C::V_TILE;  // [YS][Y_TILE] bf16 y tiles (bf16 output modes)
   uint64_t* bars = reinterpret_cast<uint64_t*>(yring + C::YS * C::Y_TILE);
   uint64_t* full = bars;                       // [NST] Bt landed
   uint64_t* empty = bars + C::NST;             // [NST] MMA done with Bt stage
@@ -638,10 +690,10 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
   if (threadIdx.x == 0) {
     wq.init(C::EPI_WARPS + 1);  // epilogue + MMA warps pop; the TMA warp fetches
     for (int s = 0; s < C::NST; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], C::BT_RETILE ? 32 : 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < C::VB; ++a) {
       mbar_init(&vfull[a], 1);
       mbar_init(&vempty[a], 1);
     }
@@ -662,28 +714,37 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
 
   if (warp == C::TMA_WARP) {
     // ===================== producer: v tile + Bt sub-tiles =====================
-    if (lane == 0) {
+    // (lane 0 alone, except for the r = 128 Bt re-tiling copies of all lanes)
+    if (lane == 0 || C::BT_RETILE) {
       const uint64_t pol = (args.tc_flags & 1) ? policy_evict_last() : policy_evict_first();
       int stage = 0, vb = 0;
       uint32_t phase = 0, vphase = 0;
       bool vready = false;
       QueuePos qp;
       for (;;) {
-        const long long it = wq_push_next(wq, qp, pd.wctr + kWqTcExpand, n_items);
+        long long it = -1;
+        if (lane == 0) it = wq_push_next(wq, qp, pd.wctr + kWqTcExpand, n_items);
+        if constexpr (C::BT_RETILE) it = __shfl_sync(0xffffffffu, it, 0);
         if (it < 0) break;
         const int cig = (int)(it / n_tiles), ti = (int)(it - (long long)cig * n_tiles);
         const SlotTask& t = args.t[find_task_ci(args, cig)];
         const int ci = cig - t.ci_base;
         const int4 tile = pd.tiles[ti];
-        mbar_wait(&vempty[vb], vphase ^ 1);
-        if (!vready) {
-          pdl_wait();  // the v tiles come from the v reduction (the Bt rows do not)
-          vready = true;
+        if (lane == 0) {
+          mbar_wait(&vempty[vb], vphase ^ 1);
+          if (!vready) {
+            pdl_wait();  // the v tiles come from the v reduction (the Bt rows do not)
+            vready = true;
+          }
+          // one bulk copy per K block: rows [tile.x, tile.x + tile.y) of the slot's v store
+          mbar_arrive_expect_tx(&vfull[vb], (uint32_t)tile.y * R * 2);
+#pragma unroll
+          for (int kb = 0; kb < G::KB; ++kb)
+            bulk_g2s(vtile + vb * C::V_TILE + kb * (kTileRows * G::RB),
+                     pd.vbf + t.vbf_off + (long long)kb * pd.max_rows * (G::RB / 2) + (long long)tile.x * (G::RB / 2),
+                     (uint32_t)tile.y * G::RB, &vfull[vb]);
         }
-        mbar_arrive_expect_tx(&vfull[vb], (uint32_t)tile.y * 128);
-        bulk_g2s(vtile + vb * C::V_TILE, pd.vbf + t.vbf_off + (long long)tile.x * R, (uint32_t)tile.y * 128,
-                 &vfull[vb]);
-        if (++vb == 2) {
+        if (++vb == C::VB) {
           vb = 0;
           vphase ^= 1;
         }
@@ -692,14 +753,31 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         const int n_sub = t.CI / C::MSUB;
         for (int sb = 0; sb < n_sub; ++sb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::B_SUB);
-          bulk_g2s_hint(smem + stage * C::B_SUB, bbase + (long long)sb * C::MSUB * R, C::B_SUB, &full[stage], pol);
+          if constexpr (C::BT_RETILE) {
+            // 128 columns x 256 bytes: physical chunk p of column c holds k chunk
+            // p ^ ((c & 3) << 1) (common.cuh); k chunk ch goes to K block ch / 8,
+            // chunk (ch % 8) ^ (c & 7) of the block's row c (SWIZZLE_128B)
+            const uint16_t* src = bbase + (long long)sb * C::MSUB * R;
+            const uint32_t dst = smem_u32(smem + stage * C::B_SUB);
+#pragma unroll 8
+            for (int i = 0; i < C::MSUB * 16 / 32; ++i) {
+              const int idx = i * 32 + lane, c = idx >> 4, pch = idx & 15;
+              const int ch = pch ^ ((c & 3) << 1);
+              cp_async16_u32(dst + (ch >> 3) * (C::MSUB * 128) + c * 128 + (((ch & 7) ^ (c & 7)) << 4),
+                             src + c * R + pch * 8);
+            }
+            cp_async_mbar_arrive_noinc(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::B_SUB);
+            bulk_g2s_hint(smem + stage * C::B_SUB, bbase + (long long)sb * C::MSUB * R, C::B_SUB, &full[stage], pol);
+          }
           if (++stage == C::NST) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+      if constexpr (C::BT_RETILE) cp_async_wait<0>();
     }
   } else if (warp == C::MMA_WARP) {
     // ===================== MMA issuer =====================
@@ -721,13 +799,17 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
         const int acc = (int)(k % C::NACC);
         mbar_wait(&tempty[acc], (uint32_t)((k / C::NACC) & 1) ^ 1);
         mbar_wait(&full[stage], phase);
+        if constexpr (C::BT_RETILE) fence_proxy_async_smem();  // the producer's cp.async writes -> the MMA's async proxy
         tc_fence_after();
         if (lane == 0) {
           const uint32_t ba = smem_u32(smem + stage * C::B_SUB);
           const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
 #pragma unroll
-          for (int kk = 0; kk < R / 16; ++kk)
-            umma_bf16(d_tmem, sw128_desc(va + kk * 32), sw128_desc(ba + kk * 32), idesc, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < R / 16; ++kk) {
+            const int kb = kk / G::KPB, ko = (kk % G::KPB) * 32;
+            umma_bf16(d_tmem, kmajor_desc<G::RB>(va + kb * (kTileRows * G::RB) + ko),
+                      kmajor_desc<G::RB>(ba + kb * (C::MSUB * G::RB) + ko), idesc, kk > 0 ? 1u : 0u);
+          }
           umma_commit(&empty[stage]);
           umma_commit(&tfull[acc]);
           if (sb == n_sub - 1) umma_commit(&vempty[vb]);
@@ -738,7 +820,7 @@ __global__ void __launch_bounds__(ExpandCfg::THREADS, 1)
           phase ^= 1;
         }
       }
-      if (++vb == 2) {
+      if (++vb == C::VB) {
         vb = 0;
         vphase ^= 1;
       }
@@ -1022,45 +1104,79 @@ static void make_x_maps(const MultiArgs& args, int x_rows, TcMaps& m) {
   m.use = 1;
 }
 
-cudaError_t launch_tc_shrink(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid, cudaStream_t stream) {
+template <int R>
+static cudaError_t launch_tc_shrink_r(const MultiArgs& args, const PlanDev& pd, int x_rows, int grid,
+                                      cudaStream_t stream) {
   static unsigned long long mask[4] = {0, 0, 0, 0};
   const bool remote = args.push.G > 0;
   bool pair = false;
   for (int i = 0; i < args.n_tasks; ++i) pair = pair || args.tc_pair[i] >= 0;
-  auto kern = remote ? (pair ? tc_shrink_kernel<true, true> : tc_shrink_kernel<true, false>)
-                     : (pair ? tc_shrink_kernel<false, true> : tc_shrink_kernel<false, false>);
-  const int smem = pair ? ShrinkCfgT<true>::SMEM : ShrinkCfgT<false>::SMEM;
+  auto kern = remote ? (pair ? tc_shrink_kernel<R, true, true> : tc_shrink_kernel<R, true, false>)
+                     : (pair ? tc_shrink_kernel<R, false, true> : tc_shrink_kernel<R, false, false>);
+  const int smem = pair ? ShrinkCfgT<R, true>::SMEM : ShrinkCfgT<R, false>::SMEM;
   cudaError_t e = set_smem_once(kern, smem, mask[remote * 2 + pair]);
   if (e != cudaSuccess) return e;
   TcMaps maps;
   make_x_maps(args, x_rows, maps);
   if (pair) maps.use = 0;
-  e = launch_pdl(kern, dim3(grid), dim3(ShrinkCfg::THREADS), smem, stream, args, pd, maps);
+  e = launch_pdl(kern, dim3(grid), dim3(ShrinkCfgT<R, false>::THREADS), smem, stream, args, pd, maps);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_vreduce(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
-  cudaError_t e = launch_pdl(tc_vreduce_kernel, dim3(grid * 4), dim3(256), 0, stream, args, pd);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_tc_expand(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
+template <int R>
+static cudaError_t launch_tc_expand_r(const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   static unsigned long long mask[6] = {0, 0, 0, 0, 0, 0};
   const int m = args.y_store == 3 ? (args.y_fp32 ? 5 : 4)
                                   : args.y_store == 1 ? 1 : args.y_store == 2 ? 2 : args.y_fp32 ? 3 : 0;
-  auto kern = m == 0   ? tc_expand_kernel<0>
-              : m == 1 ? tc_expand_kernel<1>
-              : m == 2 ? tc_expand_kernel<2>
-              : m == 3 ? tc_expand_kernel<3>
-              : m == 4 ? tc_expand_kernel<4>
-                       : tc_expand_kernel<5>;
-  cudaError_t e = set_smem_once(kern, ExpandCfg::SMEM, mask[m]);
+  auto kern = m == 0   ? tc_expand_kernel<R, 0>
+              : m == 1 ? tc_expand_kernel<R, 1>
+              : m == 2 ? tc_expand_kernel<R, 2>
+              : m == 3 ? tc_expand_kernel<R, 3>
+              : m == 4 ? tc_expand_kernel<R, 4>
+                       : tc_expand_kernel<R, 5>;
+  using C = ExpandCfg<R>;
+  cudaError_t e = set_smem_once(kern, C::SMEM, mask[m]);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kern, dim3(grid), dim3(ExpandCfg::THREADS), ExpandCfg::SMEM, stream, args, pd);
+  e = launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, stream, args, pd);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+bool tc_rank_supported(int rank) { return rank == 16 || rank == 32 || rank == 64 || rank == 128; }
+
+cudaError_t launch_tc_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int x_rows, int grid,
+                             cudaStream_t stream) {
+  switch (rank) {
+    case 16: return launch_tc_shrink_r<16>(args, pd, x_rows, grid, stream);
+    case 32: return launch_tc_shrink_r<32>(args, pd, x_rows, grid, stream);
+    case 64: return launch_tc_shrink_r<64>(args, pd, x_rows, grid, stream);
+    case 128: return launch_tc_shrink_r<128>(args, pd, x_rows, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_tc_vreduce(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
+  cudaError_t e;
+  switch (rank) {
+    case 16: e = launch_pdl(tc_vreduce_kernel<16>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
+    case 32: e = launch_pdl(tc_vreduce_kernel<32>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
+    case 64: e = launch_pdl(tc_vreduce_kernel<64>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
+    case 128: e = launch_pdl(tc_vreduce_kernel<128>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
+  switch (rank) {
+    case 16: return launch_tc_expand_r<16>(args, pd, grid, stream);
+    case 32: return launch_tc_expand_r<32>(args, pd, grid, stream);
+    case 64: return launch_tc_expand_r<64>(args, pd, grid, stream);
+    case 128: return launch_tc_expand_r<128>(args, pd, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace lora

@@ -170,8 +170,13 @@ def test_fill_store_equals_loaded_weights(B, rank):
 # exact-integer probes: bit-exact on every kernel path
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("rank,small_max", [(8, None), (16, None), (32, None), (64, -1), (64, 0), (64, 4),
-                                            (128, None)])
-def test_exact_integer_probes(B, rank, small_max):
+                                            (128, None), (16, 0), (16, 4), (32, 0), (32, 4), (128, 0), (128, 4)])
+def test_exact_integer_probes(B, monkeypatch, rank, small_max):
+    """Every kernel route bit-exact on integer-valued inputs: CUDA cores only
+    (r = 8, small_max -1), tcgen05 only (small_max 0), or both (the large
+    segment on tcgen05 at r = 16 / 32 / 64 / 128, LORA_TC_MIN_ROWS=0)."""
+    if rank != 64 and small_max is not None:
+        monkeypatch.setenv("LORA_TC_MIN_ROWS", "0")
     rng = np.random.default_rng(rank * 10 + (3 if small_max is None else small_max + 2))
     E, n_ad, h_in, h_out, T = 2, 40, 128, 256, 300   # widths multiple of 128: tcgen05-eligible
     Ai = rng.integers(-1, 2, (n_ad * E, h_in, rank))
@@ -194,7 +199,8 @@ def test_exact_integer_probes(B, rank, small_max):
         B.lora_plan_build(s, p, torch.from_numpy(a).to(U.DEV), torch.from_numpy(e).to(U.DEV), T, E)
         nv, ns, ng, nt = B.lora_plan_stats(s, p)
         # the requested kernel path is the one that ran
-        if rank != 64 or small_max == -1:
+        # (conftest sets LORA_TC_MIN_ROWS=0: the large segment takes tcgen05 at every tcgen05 rank)
+        if rank == 8 or small_max == -1:
             assert nt == 0 and ng > 0
         elif small_max == 0:
             assert ng == 0 and nt > 0
@@ -625,6 +631,39 @@ def test_small_rank_bf16_full_parity(B, rank):
         ys = _run_multi(B, s, cfg, b, [0, 1])
         for i in range(2):
             U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"r={rank} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+def _tc_rank_cfg(rank, T, y_dtype):
+    # slot c's h_in = 8192 splits K on the tcgen05 chain below 4096 rows at
+    # every rank (KI caps 4096 / 2048 / 512 at r = 16 / 32 / 128): tc_vreduce
+    return li.Config("tcr", 12, (li.Slot("a", 512, 768, 4, 0), li.Slot("b", 768, 512, 4, 1),
+                                 li.Slot("c", 8192, 256, 4, 2)), rank, 24, 4, 2, T // 2, y_dtype)
+
+
+@pytest.mark.parametrize("rank", [16, 32, 128])
+@pytest.mark.parametrize("y_dtype,T,small_max", [("bf16", 600, None), ("fp32", 600, 0), ("bf16", 4200, None)])
+def test_tc_chain_every_rank_full_parity(B, monkeypatch, rank, y_dtype, T, small_max):
+    """The tcgen05 chain at r = 16 / 32 / 128 (SWIZZLE_32B / 64B v and Bt
+    operands; r = 128: two K blocks, Bt rows re-tiled by the producer warp),
+    forced on with LORA_TC_MIN_ROWS=0: K-split + tc_vreduce (T = 600) and
+    whole-K (T = 4200 rows >= 4096) items, tcgen05 tiles beside CUDA-core
+    groups (small_max None) or every row on tcgen05 (0); every element."""
+    monkeypatch.setenv("LORA_TC_MIN_ROWS", "0")
+    cfg = _tc_rank_cfg(rank, T, y_dtype)
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg, small_max=small_max)
+    try:
+        p = B.lora_plan_create(s, cfg.n_rows)
+        ad, ex = U.ids_dev(b)
+        B.lora_plan_build(s, p, ad, ex, cfg.n_rows, 4)
+        nv, ns, ng, nt = B.lora_plan_stats(s, p)
+        B.lora_plan_destroy(p)
+        assert nt > 0, "the tcgen05 chain did not run"
+        ys = _run_multi(B, s, cfg, b, [0, 1, 2])
+        for i in range(3):
+            U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"tc r={rank} {y_dtype} T={T} slot {i}")
     finally:
         B.lora_server_destroy(s)
 

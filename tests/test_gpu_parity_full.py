@@ -86,6 +86,25 @@ def test_full_config_every_row(B, name):
         B.lora_server_destroy(s)
 
 
+@pytest.mark.parametrize("rank", [32, 128])
+def test_prefill_shapes_other_ranks_every_row(B, rank):
+    """Config 4's shapes (Mixtral gate/up/down, 8192 tokens, 16384 rows) at
+    r = 32 and r = 128: the tcgen05 chain at those ranks (SWIZZLE_64B operands;
+    r = 128: two K blocks, Bt re-tiled in the expand's producer), whole-K
+    items, the paired gate/up shrink; every row against the oracle."""
+    cfg = dataclasses.replace(li.CONFIGS["mixtral_prefill"], name=f"mixtral_prefill_r{rank}", rank=rank)
+    b = li.make_batch(cfg)
+    s = U.make_server(B, cfg)
+    slots = list(range(len(cfg.slots)))
+    try:
+        ys, stats = _run(B, s, cfg, b, slots, "random")
+        assert stats[3] > 0, stats  # the tcgen05 route ran
+        for i in slots:
+            U.assert_parity(ys[i], orc.apply_slot_all_rows(cfg, i, b, y0="random"), f"prefill r={rank} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
 def test_config5_push_loopback_every_row(B, monkeypatch):
     """Config 5 through the sharded server's push path at full size
     (loopback: every row through bucket / announce / recv-prep, the owner's
