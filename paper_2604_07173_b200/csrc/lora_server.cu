@@ -175,9 +175,11 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (const char* e = std::getenv("LORA_PDL_TC")) s->pdl_tc = std::atoi(e) != 0;
   cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
   s->simt_split_items = 2 * 2 * s->sm_count;  // fewer whole-K items than 2 per CUDA-core CTA: split K
-  // r != 64: the CUDA-core kernels are tuned for decode batches at every rank;
-  // the tcgen05 chain takes the large segments of prefill-sized batches only
-  if (s->r != 64) s->tc_min_rows = 2048;
+  // r = 16: the CUDA-core kernels beat the tcgen05 chain on decode batches
+  // (measured, config-3 shapes at 512 tokens: 179 vs 204 us), so tcgen05
+  // takes the large segments of prefill-sized batches only; r = 32 / 128
+  // gain from it at decode sizes too (286 -> 277 us, 943 -> 898 us)
+  if (s->r == 16) s->tc_min_rows = 2048;
   if (const char* e = std::getenv("LORA_TC_MIN_ROWS")) s->tc_min_rows = std::atoi(e);
   if (const char* e = std::getenv("LORA_SIMT_SPLIT")) s->simt_split_items = std::atoi(e);
   if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||

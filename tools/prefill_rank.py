@@ -12,6 +12,7 @@ import lora_inputs as li  # noqa: E402
 
 
 def main():
+    base = os.environ.get("RANK_SWEEP_BASE", "mixtral_prefill")
     import torch
     from paper_2604_07173_b200 import binding as B
     dev = torch.device("cuda", 0)
@@ -19,7 +20,7 @@ def main():
     hbm_peak, _, _ = bench.load_peaks()
     out = {}
     for rk in [int(a) for a in (sys.argv[1:] or ["16", "32", "64", "128"])]:
-        c = dataclasses.replace(li.CONFIGS["mixtral_prefill"], name=f"mixtral_prefill_r{rk}", rank=rk)
+        c = dataclasses.replace(li.CONFIGS[base], name=f"{base}_r{rk}", rank=rk)
         b = li.make_batch(c)
         slots = list(range(len(c.slots)))
         r = bench.SingleRun(B, torch, c, b, slots, dev, stream)
