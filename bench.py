@@ -56,14 +56,22 @@ def algorithmic(cfg: li.Config, batch: li.Batch, slots, small_max: int = 8):
     Each touched unit's A and B are read once, each valid row's x once per
     distinct x buffer (slots sharing x -- gate/up, q/k/v -- need it once),
     its y read + written once; a segment of more than `small_max` rows
-    runs on the tcgen05 kernels (rank 64, 128-multiple widths), else on the
-    CUDA-core kernels -- the same dispatch rule the library applies."""
+    runs on the tcgen05 kernels (rank 16 / 32 / 64 / 128, 128-multiple
+    widths, the large segments holding at least LORA_TC_MIN_ROWS rows
+    together: 256, 2048 at r = 16), else on the CUDA-core kernels -- the same
+    dispatch rule the library applies."""
     a = batch.adapter_ids.astype(np.int64)
     valid = a >= 0
     T, Tv = batch.n_rows, int(valid.sum())
     ysz = 4 if cfg.y_dtype == "fp32" else 2
     r = cfg.rank
-    tc_ok = r == 64 and small_max >= 0 and all(s.h_in % 128 == 0 and s.h_out % 128 == 0 for s in cfg.slots)
+    tc_ok = r in (16, 32, 64, 128) and small_max >= 0 and all(s.h_in % 128 == 0 and s.h_out % 128 == 0
+                                                               for s in cfg.slots)
+    if tc_ok:  # the segmenter's device-side rule over the plan (one plan per apply)
+        E0 = cfg.slots[slots[0]].n_experts
+        _, c0 = np.unique(a[valid] * E0 + batch.expert_ids[valid], return_counts=True)
+        min_rows = int(os.environ.get("LORA_TC_MIN_ROWS", 2048 if r == 16 else 256))
+        tc_ok = int(c0[c0 > small_max].sum()) >= min_rows
     out = {"segment": T * 8, "simt_shrink": 0, "simt_expand": 0, "tc05_shrink": 0, "tc05_expand": 0,
            "flops": 0, "units": {}}
     seen_x = set()
