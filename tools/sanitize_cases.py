@@ -11,6 +11,9 @@ correct one):
   mid_fp32  the same with an fp32 y (direct tcgen05 epilogue)
   wholek    4100 rows: multi-CTA segmenter, whole-K tcgen05 shrink
   llama     r = 16, 8 slots (resolver warps, staged-tile expand)
+  tc16 / tc32 / tc128   the mid config at r = 16 / 32 / 128 with the tcgen05
+            chain forced on (SWIZZLE_32B / 64B operands; r = 128: two K blocks,
+            Bt re-tiled by cp.async in the expand's producer warp)
   push      sharded server at G = 1, loopback through the push path
             (announce / recv-prep / device-T segmenter / remote-x shrink /
             red.add expand / done + wait)
@@ -87,7 +90,7 @@ def run_push(B):
 
 def main():
     B = U.binding()
-    cases = sys.argv[1:] or ["tiny", "mid", "mid_fp32", "wholek", "llama", "push"]
+    cases = sys.argv[1:] or ["tiny", "mid", "mid_fp32", "wholek", "llama", "tc16", "tc32", "tc128", "push"]
     for c in cases:
         if c == "tiny":
             run_unsharded(B, li.CONFIGS["tiny"], [0], c)
@@ -101,6 +104,10 @@ def main():
             cfg = li.CONFIGS["llama_decode"]
             cfg = li.Config("llama8", 2, cfg.slots[:8], 16, 128, 1, 1, 256, "bf16")
             run_unsharded(B, cfg, list(range(8)), c)
+        elif c in ("tc16", "tc32", "tc128"):
+            os.environ["LORA_TC_MIN_ROWS"] = "0"
+            run_unsharded(B, _mid(rank=int(c[2:])), [0, 1], c)
+            del os.environ["LORA_TC_MIN_ROWS"]
         elif c == "push":
             run_push(B)
         print(f"sanitize case {c}: OK", flush=True)
