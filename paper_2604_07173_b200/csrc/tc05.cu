@@ -642,12 +642,21 @@ struct ExpandCfg {
 #ifndef LORA_TCE_YD
 #define LORA_TCE_YD 4
 #endif
-  static constexpr int NST = LORA_TCE_NST;
+#ifndef LORA_TCE128_NST
+#define LORA_TCE128_NST 2
+#endif
+#ifndef LORA_TCE128_VB
+#define LORA_TCE128_VB 2  // r = 128 (shared memory: 2 x 32 KB Bt + VB x 32 KB v + (YD + 1) x 32 KB y):
+#endif                    // measured VB 2 / YD 2 444 us, VB 1 / YD 3 452 us, NST 3 / YD 2 452 us (prefill shapes)
+#ifndef LORA_TCE128_YD
+#define LORA_TCE128_YD 2
+#endif
+  static constexpr int NST = R > 64 ? LORA_TCE128_NST : LORA_TCE_NST;
   static constexpr int V_TILE = kTileRows * R * 2;     // v tile, M = 128 rows x K = R (16 KB at r = 64)
-  static constexpr int VB = R > 64 ? 1 : 2;           // v tile buffers (r = 128: one, for shared memory)
+  static constexpr int VB = R > 64 ? LORA_TCE128_VB : 2;  // v tile buffers
   // bf16 output: y tiles [128 rows][128 cols] (16-byte chunks XOR-swizzled by
   // row) in a ring of YS slots, fetched YD-1 sub-tiles ahead
-  static constexpr int YD = R > 64 ? 3 : LORA_TCE_YD;
+  static constexpr int YD = R > 64 ? LORA_TCE128_YD : LORA_TCE_YD;
   static constexpr int YS = YD + 1;
   static constexpr int Y_TILE = kTileRows * MSUB * 2;  // 32 KB
   static constexpr int NACC = 4;
