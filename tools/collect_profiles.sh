@@ -15,4 +15,6 @@ done
 [ -s $P/bench_push_loopback.json ] && tail -1 $P/bench_push_loopback.json > profiles/${TAG}_bench_push_loopback.json
 [ -s $P/sum_full_mixtral_prefill.txt ] && cp $P/sum_full_mixtral_prefill.txt profiles/${TAG}_ncu_summary_mixtral_prefill.txt
 [ -s $P/sum_full_llama_decode.txt ] && cp $P/sum_full_llama_decode.txt profiles/${TAG}_ncu_summary_llama_decode.txt
+[ -s $P/sum_full_prefill_r128.txt ] && cp $P/sum_full_prefill_r128.txt profiles/${TAG}_ncu_summary_prefill_r128.txt
+[ -s $P/prefill_rank.json ] && tail -1 $P/prefill_rank.json > profiles/${TAG}_prefill_rank_sweep.json
 true

@@ -37,8 +37,13 @@ timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'simt_shrink|simt_expand' -s 4 -c 2 \
     -o /tmp/full_llama_decode python bench.py --workload llama_decode --steps 2 --warmup 3 --no-cpu-baseline \
     --e2e-steps 0 --no-secondary --no-graph > $OUT/ncu_full_llama.log 2>&1
+# the tcgen05 chain at r = 128 (prefill shapes)
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:'tc_shrink|tc_expand' -s 2 -c 2 \
+    -o /tmp/full_prefill_r128 python tools/prefill_rank.py 128 > $OUT/ncu_full_r128.log 2>&1
+timeout 600 python tools/prefill_rank.py > $OUT/prefill_rank.json 2> $OUT/prefill_rank.err
 # summaries on the box; the .ncu-rep files stay in /tmp there (gpurun_out/ is capped at 64 MiB)
-for r in full_mixtral_sharded full_mixtral_prefill full_mixtral_decode full_llama_decode; do
+for r in full_mixtral_sharded full_mixtral_prefill full_mixtral_decode full_llama_decode full_prefill_r128; do
   [ -f /tmp/$r.ncu-rep ] && python tools/ncu_summary.py /tmp/$r.ncu-rep > $OUT/sum_$r.txt 2>&1
 done
 echo done
