@@ -69,7 +69,7 @@ typedef struct {
   int32_t rank;              /* r, uniform (one rank per model): 8, 16, 32, 64 or 128 ("r typically 32-128") */
   int32_t n_adapters;        /* global adapter count n */
   const float *scale;        /* [n_adapters] host fp32 s_a; NULL => all 1.0 (R1) */
-  int32_t max_rows;          /* capacity (rows) of the internal plan; 0 < max_rows <= 16384 */
+  int32_t max_rows;          /* capacity (rows) of the internal plan; 0 < max_rows <= 32768 (sharded: max_rows * world <= 16384) */
   int32_t device;            /* CUDA device ordinal */
   int32_t n_replicated;      /* sharded servers only: adapters [0, n_replicated) are stored on
                                 every rank (popularity-aware placement for skewed traffic,
@@ -167,7 +167,7 @@ const char *lora_last_error(const lora_server_t *s);
 /* Plans: a1 segmentation, reusable across the slots of one unit of work       */
 /* ------------------------------------------------------------------------- */
 
-/* Allocate a plan for up to max_rows rows (<= 16384) plus the workspace of
+/* Allocate a plan for up to max_rows rows (<= 32768) plus the workspace of
  * every slot (so one plan serves any sequence of slots). */
 lora_status_t lora_plan_create(lora_server_t *s, int32_t max_rows, lora_plan_t **out);
 lora_status_t lora_plan_destroy(lora_plan_t *p);

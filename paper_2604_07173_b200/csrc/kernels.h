@@ -7,7 +7,8 @@
 
 namespace lora {
 
-constexpr int kMaxPlanRows = 16384;  // single-CTA segmenter capacity (128 KB of composites)
+constexpr int kMaxPlanRows = 32768;  // plan capacity (rows); above kMaxOneCtaRows the multi-CTA segmenter runs
+constexpr int kMaxOneCtaRows = 16384;  // single-CTA segmenter capacity (128 KB of composites)
 constexpr int kSegMultiMin = 4096;   // T at or above which the multi-CTA segmenter runs
 constexpr int kSegHistMax = 1 << 18; // K * C bound of the multi-CTA segmenter's histogram
 constexpr int kTcWideKRows = 4096;  // plan rows from which tcgen05 shrink items take the whole h_in

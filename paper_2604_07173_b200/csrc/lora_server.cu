@@ -72,7 +72,7 @@ static lora_status_t validate_config(const lora_config_t* cfg) {
     return fail(nullptr, LORA_ERR_UNSUPPORTED, "rank must be 8, 16, 32, 64 or 128");
   if (cfg->n_adapters < 1) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_adapters < 1");
   if (cfg->max_rows < 1 || cfg->max_rows > kMaxPlanRows)
-    return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows must be in [1, 16384]");
+    return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows must be in [1, 32768]");
   for (int i = 0; i < cfg->n_slots; ++i) {
     if (cfg->h_in[i] < 64 || cfg->h_in[i] % 64 || cfg->h_out[i] < 64 || cfg->h_out[i] % 64)
       return fail(nullptr, LORA_ERR_UNSUPPORTED, "h_in / h_out must be positive multiples of 64");
@@ -564,7 +564,7 @@ extern "C" const char* lora_version(void) { return "infinilora-b200 0.1 (sm_100a
 namespace lora {
 
 lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
-  if (max_rows < 1 || max_rows > kMaxPlanRows) return fail(s, LORA_ERR_UNSUPPORTED, "max_rows must be in [1, 16384]");
+  if (max_rows < 1 || max_rows > kMaxPlanRows) return fail(s, LORA_ERR_UNSUPPORTED, "max_rows must be in [1, 32768]");
   lora_plan* p = new (std::nothrow) lora_plan();
   if (!p) return fail(s, LORA_ERR_OOM, "host allocation failed");
   p->s = s;
@@ -726,7 +726,11 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
         s->slot_pending[slots[i]] = 0;
       }
   }
-  const bool tc = tc_enabled(s);
+  // the segmenter makes tcgen05 tiles only when the large segments hold at
+  // least tc_min_rows rows: a plan of fewer rows (p->T bounds them, also for
+  // a device-side row count) runs the CUDA-core chain alone -- no side-stream
+  // fork, no empty tcgen05 launches, PDL between its kernels
+  const bool tc = tc_enabled(s) && p->T >= s->tc_min_rows;
   for (int b0 = 0; b0 < n; b0 += kMaxTasks) {
     const int nb = std::min(kMaxTasks, n - b0);
     MultiArgs args;

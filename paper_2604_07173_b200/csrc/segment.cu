@@ -6,7 +6,8 @@
 // adapter into a single GEMM" (App. A.2.2); the paper presumes the
 // segments, so this kernel is ours (R9 for the ordering contract).
 //
-// One CTA of 1024 threads, everything in shared memory (T <= 16384).
+// One CTA of 1024 threads, everything in shared memory (T <= 16384); larger
+// batches (up to 32768 rows) always take the multi-CTA path below.
 //  * Fast path: 32-bit composites (key << ib) | row with an LSD radix sort on
 //    the key bits, 8 bits per pass.  Each pass is a stable block-wide counting
 //    sort (warp-synchronous multisplit + a block scan over (digit, warp)).
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(NT, 1)
     else
       ng += (size + kGroupRows - 1) / kGroupRows;
   }
-  // both list counts in one scan (each < 2^16: T <= 16384)
+  // both list counts in one scan (each < 2^16: T <= 32768)
   int NGT;
   const int gt = block_exclusive_scan<NT>(ng | (nt << 16), scan_tmp, &NGT);
   const int NG = NGT & 0xFFFF, NTL = NGT >> 16;
@@ -700,7 +701,9 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
     const int kb = bits_for(K);
     const char* fe = getenv("LORA_SEG_MULTI");  // test hook: 1 forces, 0 disables the multi-CTA path
     const int forced = fe ? atoi(fe) : -1;
-    const bool want = !T_dev && (forced < 0 ? T >= kSegMultiMin : forced == 1);  // (device T: one CTA)
+    // beyond one CTA's capacity the multi-CTA path is the only one
+    const bool big = T > kMaxOneCtaRows;
+    const bool want = !T_dev && (big || (forced < 0 ? T >= kSegMultiMin : forced == 1));  // (device T: one CTA)
     int ept = 0;
     if (want && pd.hist && T > 0 && kb + kLocBits <= 32 && K > 0 && K <= kSegKeysMax) {
       // rows per CTA: the fewest (1024, 2048) that keep the histogram K x C
@@ -711,7 +714,7 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
       const int pick = ee ? atoi(ee) : 0;
       for (int e : {1, 2, 4}) {
         const long long C = (T + e * kSegThreads - 1) / (e * kSegThreads);
-        const bool fits = pick ? e == pick : (K * C <= kSegHistSmall || (forced == 1 && e == 4));
+        const bool fits = pick ? e == pick : (K * C <= kSegHistSmall || ((forced == 1 || big) && e == 4));
         if (fits) {
           if (K * C <= kSegHistMax) ept = e;
           break;
@@ -768,6 +771,9 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
   }
   const int kb = bits_for((long long)n_adapters * E);  // key K = n_adapters*E marks "no LoRA" (sorts last)
   // CTA size: small batches on 256 / 512 threads (radix path), else 1024
+  // one CTA holds at most kMaxOneCtaRows rows; larger batches needed the
+  // multi-CTA path (key space within kSegKeysMax / the histogram bound)
+  if (T > kMaxOneCtaRows) return cudaErrorInvalidValue;
   // (device T: T is the capacity).  LORA_SEG_NT=1024 (tuning hook): always 1024
   int nt = T <= 256 ? 256 : T <= 512 ? 512 : kSegThreads;
   if (const char* e = getenv("LORA_SEG_NT")) nt = std::max(nt, atoi(e) >= kSegThreads ? kSegThreads : nt);
@@ -785,8 +791,8 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set & (1ull << dev))) {
-    const int mx = std::max((2 * (kMaxPlanRows + kMaxPlanRows / 32) + 8 + 32 * 256) * 4,
-                            kMaxPlanRows * 8 + (kMaxPlanRows + 1) * 4);
+    const int mx = std::max((2 * (kMaxOneCtaRows + kMaxOneCtaRows / 32) + 8 + 32 * 256) * 4,
+                            kMaxOneCtaRows * 8 + (kMaxOneCtaRows + 1) * 4);
     cudaError_t e = cudaFuncSetAttribute(segment_kernel<true, kSegThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(segment_kernel<false, kSegThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);

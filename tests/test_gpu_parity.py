@@ -96,13 +96,16 @@ def test_segment_bit_exact_adversarial(B, case):
 
 
 @pytest.mark.parametrize("T,n_ad,E", [(1, 16, 1), (1023, 64, 8), (2049, 16, 1), (4097, 2048, 8), (5000, 7, 3),
-                                      (8192, 2048, 8), (16384, 64, 8), (16384, 4096, 4)])
+                                      (8192, 2048, 8), (16384, 64, 8), (16384, 4096, 4),
+                                      (16385, 64, 8), (24000, 7, 3), (32768, 2048, 8)])
 @pytest.mark.parametrize("multi", ["1", "0"])
 def test_segment_multi_cta_path(B, monkeypatch, T, n_ad, E, multi):
     """Both segmenter paths (LORA_SEG_MULTI test hook: 1 = the multi-CTA
     local-sort / scan / scatter kernels at any T, 0 = the one-CTA kernel) give
     the oracle's stable segmentation bit-exactly, incl. -1 rows, Zipf-skewed
-    and ragged batches, and a key space that makes the histogram wide."""
+    and ragged batches, and a key space that makes the histogram wide.
+    Above 16384 rows (one CTA's capacity) the multi-CTA path runs whatever the
+    hook says (plan capacity 32768 rows)."""
     monkeypatch.setenv("LORA_SEG_MULTI", multi)
     rng = np.random.default_rng(T + n_ad)
     zipf = rng.choice(n_ad, size=T, p=li.zipf_probs(n_ad))
@@ -631,6 +634,37 @@ def test_small_rank_bf16_full_parity(B, rank):
         ys = _run_multi(B, s, cfg, b, [0, 1])
         for i in range(2):
             U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"r={rank} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+@pytest.mark.parametrize("y_dtype", ["bf16", "fp32"])
+def test_beyond_one_cta_rows_full_parity(B, y_dtype):
+    """A 20000-row batch (above the one-CTA segmenter's 16384; plan capacity
+    32768): multi-CTA segmenter, tcgen05 whole-K tiles beside CUDA-core
+    groups; every element against the oracle."""
+    cfg = dataclasses.replace(_mid_cfg(rank=64, T=20000), y_dtype=y_dtype)
+    b = li.make_batch(cfg)
+    assert b.n_rows == 20000
+    s = U.make_server(B, cfg)
+    try:
+        ys = _run_multi(B, s, cfg, b, [0, 1])
+        for i in range(2):
+            U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"20000 rows {y_dtype} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_plan_capacity_bound(B):
+    """max_rows 32768 is accepted, 32769 rejected (LORA_ERR_UNSUPPORTED)."""
+    cfg = _mid_cfg(rank=16, T=600)
+    s = U.make_server(B, cfg, fill=False)
+    try:
+        p = B.lora_plan_create(s, 32768)
+        B.lora_plan_destroy(p)
+        with pytest.raises(B.LoraError) as ei:
+            B.lora_plan_create(s, 32769)
+        assert ei.value.status == B.LORA_ERR_UNSUPPORTED
     finally:
         B.lora_server_destroy(s)
 
