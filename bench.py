@@ -414,6 +414,21 @@ def secondaries(B, torch, dev, stream, hbm_peak, steps, warmup):
                 "points": sweep}
         else:
             r.destroy()
+    # SURVEY 8d variants: uniform adapter ids (3u, Llama ~110 adapters) and the
+    # 16 x 512-token prefill
+    var = {}
+    for name, cfg in li.VARIANTS.items():
+        b = li.make_batch(cfg)
+        slots = list(range(len(cfg.slots)))
+        r = SingleRun(B, torch, cfg, b, slots, dev, stream)
+        tv, totv = r.time(max(5, steps // 2), 2)
+        profv = r.profile(3)
+        sm = summarise(cfg, algorithmic(cfg, b, slots), tv, totv, hbm_peak, profv, 3)
+        r.destroy()
+        var[name] = {k: sm[k] for k in ("ms_per_step", "ms_median", "tokens_per_s", "rows", "step_GBs",
+                                        "frac_measured", "frac_nominal_8TBs", "kernels")}
+        var[name]["distinct_units"] = sum(sm["distinct_units"].values()) // max(1, len(sm["distinct_units"]))
+    out["variants"] = var
     # rank sweep over the paper's range ("r typically 32-128") on config-3
     # shapes with 128 adapters (r = 64 is config 3 itself, above)
     sweep = {}

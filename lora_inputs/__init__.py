@@ -260,6 +260,17 @@ CONFIGS: Dict[str, Config] = {
 }
 
 
+# SURVEY 8d variants of the configs: uniform adapter ids (3u; Llama ~110
+# distinct adapters) and the 16 x 512-token prefill (~77 units of 106-633 rows)
+VARIANTS: Dict[str, Config] = {
+    "mixtral_decode_uniform": dataclasses.replace(CONFIGS["mixtral_decode"], name="mixtral_decode_uniform",
+                                                  zipf_s=0.0),
+    "llama_decode_uniform": dataclasses.replace(CONFIGS["llama_decode"], name="llama_decode_uniform", zipf_s=0.0),
+    "mixtral_prefill_16x512": dataclasses.replace(CONFIGS["mixtral_prefill"], name="mixtral_prefill_16x512",
+                                                  n_seqs=16),
+}
+
+
 def with_tokens(cfg: Config, n_tokens: int, **kw) -> Config:
     """Same config at another batch size (parity sizes, batch sweeps)."""
     d = dataclasses.asdict(cfg)

@@ -62,16 +62,17 @@ def _run(B, s, cfg, batch, slot_ids, y0):
 # ---------------------------------------------------------------------------
 # every row, configs 2-5
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("name", ["llama_decode", "mixtral_decode", "mixtral_prefill", "mixtral_sharded"])
+@pytest.mark.parametrize("name", ["llama_decode", "mixtral_decode", "mixtral_prefill", "mixtral_sharded",
+                                  "mixtral_decode_uniform", "llama_decode_uniform", "mixtral_prefill_16x512"])
 def test_full_config_every_row(B, name):
-    cfg = li.CONFIGS[name]
+    cfg = li.CONFIGS[name] if name in li.CONFIGS else li.VARIANTS[name]
     b = li.make_batch(cfg)
     s = U.make_server(B, cfg)
     slots = list(range(len(cfg.slots)))
     try:
         for y0 in ("random", "zero"):
             ys, stats = _run(B, s, cfg, b, slots, y0)
-            if cfg.rank == 64:
+            if name in li.CONFIGS and cfg.rank == 64:
                 assert stats[3] > 0, stats                    # the tcgen05 route ran
                 assert stats[2] > 0 or name == "mixtral_prefill", stats   # (prefill: every segment is large)
             for i in slots:
