@@ -107,6 +107,7 @@ struct SegParams {
   int tc_enabled;  // a tcgen05 rank (16 / 32 / 64 / 128) and not forced off
   int tc_min_rows; // tcgen05 tiles only if the large segments hold at least this many rows in total
   int tile_rows;
+  int group_rows;   // rows per CUDA-core group (<= kGroupRows; env LORA_GROUP_ROWS, a test / tuning hook)
   Placement pl;    // rows whose adapter this rank does not store are rejected (flagged)
   const int32_t* cache;  // resident-cache mode: [n_adapters] cache slot or -1 (not resident: rejected)
 };

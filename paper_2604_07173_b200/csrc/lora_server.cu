@@ -182,6 +182,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   if (s->r == 16) s->tc_min_rows = 2048;
   if (const char* e = std::getenv("LORA_TC_MIN_ROWS")) s->tc_min_rows = std::atoi(e);
   if (const char* e = std::getenv("LORA_SIMT_SPLIT")) s->simt_split_items = std::atoi(e);
+  if (const char* e = std::getenv("LORA_GROUP_ROWS")) s->group_rows = std::max(1, std::min(lora::kGroupRows, std::atoi(e)));
   if (cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -643,6 +644,7 @@ lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapt
   sp.tc_enabled = tc_enabled(s) ? 1 : 0;
   sp.tc_min_rows = s->tc_min_rows;
   sp.tile_rows = kTileRows;
+  sp.group_rows = s->group_rows;
   CK(s, cudaSetDevice(s->device));
   const int pi = prof_start(s, st);
   sp.pl = placement(s);

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (use_tc && size > sp.small_max)
       nt += (size + sp.tile_rows - 1) / sp.tile_rows;
     else
-      ng += (size + kGroupRows - 1) / kGroupRows;
+      ng += (size + sp.group_rows - 1) / sp.group_rows;
   }
   // both list counts in one scan (each < 2^16: T <= 32768)
   int NGT;
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(NT, 1)
   for (int s = s0; s < s1; ++s) {
     const int b = segoff_s[s], size = segoff_s[s + 1] - b, key = key_at(b);
     const bool tc = use_tc && size > sp.small_max;
-    const int cap = tc ? sp.tile_rows : kGroupRows;
+    const int cap = tc ? sp.tile_rows : sp.group_rows;
     const int n = (size + cap - 1) / cap;
     // near-equal split: the first (size % n) pieces get one extra row
     const int base = size / n, extra = size % n;
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     if (use_tc && size > sp.small_max)
       nt += (size + sp.tile_rows - 1) / sp.tile_rows;
     else
-      ng += (size + kGroupRows - 1) / kGroupRows;
+      ng += (size + sp.group_rows - 1) / sp.group_rows;
   }
   int S, NGT;
   int seg = block_exclusive_scan(heads, scan_tmp, &S);
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     pd.seg_off[seg] = b;
     pd.seg_key[seg] = k;
     const bool tc = use_tc && size > sp.small_max;
-    const int cap = tc ? sp.tile_rows : kGroupRows;
+    const int cap = tc ? sp.tile_rows : sp.group_rows;
     const int np = (size + cap - 1) / cap;
     const int base = size / np, extra = size % np;
     int r = b;

@@ -32,6 +32,7 @@ struct lora_server {
   int tc_cap_k = 2;        // tcgen05 CTAs per tile when both chains run (measured 1/2/4/8 with the staged-tile expand: Mixtral decode 0.478/0.482/0.489/0.494 ms, prefill 0.576/0.561/-/- ms; env LORA_TC_CAP_K, 0 = all SMs)
   int tc_ci_max = 8192;    // tcgen05 expand: max h_out per item (measured best of 1024..8192; env LORA_TC_CI_MAX, 0 = slot CI)
   int tc_flags = 1;         // tcgen05 expand L2 policies (MultiArgs::tc_flags; env LORA_TCE_FLAGS): Bt evict_last (measured prefill 0.550 -> 0.529 ms; y evict_first hints slower)
+  int group_rows = 8;           // rows per CUDA-core group (kGroupRows; env LORA_GROUP_ROWS, smaller only)
   int tc_min_rows = 256;    // segmenter: tcgen05 tiles only with at least this many rows in large segments (env LORA_TC_MIN_ROWS)
   int simt_split_items = 0;  // MultiArgs::simt_split_items (set at create: 8 items per CUDA-core CTA; env LORA_SIMT_SPLIT)
   bool tc_pair = true;
