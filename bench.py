@@ -65,12 +65,12 @@ def algorithmic(cfg: li.Config, batch: li.Batch, slots, small_max: int = 8):
     T, Tv = batch.n_rows, int(valid.sum())
     ysz = 4 if cfg.y_dtype == "fp32" else 2
     r = cfg.rank
-    tc_ok = r in (16, 32, 64, 128) and small_max >= 0 and all(s.h_in % 128 == 0 and s.h_out % 128 == 0
+    tc_ok = r in (8, 16, 32, 64, 128) and small_max >= 0 and all(s.h_in % 128 == 0 and s.h_out % 128 == 0
                                                                for s in cfg.slots)
     if tc_ok:  # the segmenter's device-side rule over the plan (one plan per apply)
         E0 = cfg.slots[slots[0]].n_experts
         _, c0 = np.unique(a[valid] * E0 + batch.expert_ids[valid], return_counts=True)
-        min_rows = int(os.environ.get("LORA_TC_MIN_ROWS", 2048 if r == 16 else 256))
+        min_rows = int(os.environ.get("LORA_TC_MIN_ROWS", 2048 if r <= 16 else 256))
         tc_ok = int(c0[c0 > small_max].sum()) >= min_rows
     out = {"segment": T * 8, "simt_shrink": 0, "simt_expand": 0, "tc05_shrink": 0, "tc05_expand": 0,
            "flops": 0, "units": {}}
@@ -450,7 +450,7 @@ def secondaries(B, torch, dev, stream, hbm_peak, steps, warmup):
     # the same at prefill shapes (config 4: 8192 tokens, 16384 rows): the
     # tcgen05 chain at every rank (r = 64 is config 4 itself, above)
     sweep = {}
-    for rk in (16, 32, 128):
+    for rk in (8, 16, 32, 128):
         c4 = dataclasses.replace(li.CONFIGS["mixtral_prefill"], name=f"mixtral_prefill_r{rk}", rank=rk)
         b4 = li.make_batch(c4)
         slots = list(range(len(c4.slots)))
@@ -463,7 +463,7 @@ def secondaries(B, torch, dev, stream, hbm_peak, steps, warmup):
                                              "frac_measured", "kernels")}
     out["prefill_rank_sweep"] = {
         "workload": "config-4 shapes (Mixtral gate/up/down, 4 x 2048-token sequences, 64 adapters, top-2) at "
-                    "r = 16 / 32 / 128 (P:165); large segments on the tcgen05 chain at every rank",
+                    "r = 8 / 16 / 32 / 128 (P:165); large segments on the tcgen05 chain at every rank",
         "points": sweep}
     return out
 

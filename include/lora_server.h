@@ -126,9 +126,9 @@ lora_status_t lora_server_destroy(lora_server_t *s);
 /* Segments with more than `n` rows go to the tcgen05/TMEM kernels, the rest
  * to the CUDA-core kernels (default: env LORA_SMALL_SEG_MAX, else 8).  n < 0
  * forces the CUDA-core path for every segment.  The tcgen05 path runs at
- * ranks 16, 32, 64 and 128 (rank 8 always uses the CUDA-core path), when the
- * large segments of a batch hold at least LORA_TC_MIN_ROWS rows together
- * (default 2048 at rank 16, else 256).  Takes effect at the
+ * every rank (8 with zero-padded MMAs), when the large segments of a batch
+ * hold at least LORA_TC_MIN_ROWS rows together (default 2048 at ranks 8 and
+ * 16, else 256).  Takes effect at the
  * next lora_plan_build. */
 lora_status_t lora_server_set_small_seg_max(lora_server_t *s, int32_t n);
 

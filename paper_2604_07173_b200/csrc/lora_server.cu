@@ -179,7 +179,7 @@ static lora_status_t create_common(const lora_config_t* cfg, int world, int rank
   // (measured, config-3 shapes at 512 tokens: 179 vs 204 us), so tcgen05
   // takes the large segments of prefill-sized batches only; r = 32 / 128
   // gain from it at decode sizes too (286 -> 277 us, 943 -> 898 us)
-  if (s->r == 16) s->tc_min_rows = 2048;
+  if (s->r <= 16) s->tc_min_rows = 2048;
   if (const char* e = std::getenv("LORA_TC_MIN_ROWS")) s->tc_min_rows = std::atoi(e);
   if (const char* e = std::getenv("LORA_SIMT_SPLIT")) s->simt_split_items = std::atoi(e);
   if (const char* e = std::getenv("LORA_GROUP_ROWS")) s->group_rows = std::max(1, std::min(lora::kGroupRows, std::atoi(e)));
@@ -580,7 +580,7 @@ lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out) {
             cudaMalloc(&d.groups, sizeof(int4) * max_rows) == cudaSuccess &&
             cudaMalloc(&d.tiles, sizeof(int4) * max_rows) == cudaSuccess &&
             cudaMalloc(&d.vpart, sizeof(float) * (size_t)s->total_kc * max_rows * s->r) == cudaSuccess &&
-            cudaMalloc(&d.vbf, sizeof(uint16_t) * s->slots.size() * (size_t)max_rows * s->r) == cudaSuccess &&
+            cudaMalloc(&d.vbf, sizeof(uint16_t) * s->slots.size() * (size_t)max_rows * std::max(s->r, 16)) == cudaSuccess &&
             cudaMalloc(&d.wctr, sizeof(unsigned long long) * kWorkSlots) == cudaSuccess &&
             cudaMalloc(&d.wdone, sizeof(unsigned int) * kWorkSlots) == cudaSuccess &&
             cudaMalloc(&d.gcnt, sizeof(unsigned int) * kMaxTasks * (size_t)max_rows) == cudaSuccess;
@@ -626,7 +626,7 @@ void plan_destroy_impl(lora_plan* p) {
   delete p;
 }
 
-// tcgen05 path: rank 16 / 32 / 64 / 128, every slot's item widths multiples of the 128-wide MMA tiles
+// tcgen05 path: rank 8 / 16 / 32 / 64 / 128, every slot's item widths multiples of the 128-wide MMA tiles
 static bool tc_enabled(const lora_server* s) {
   if (!tc_available() || !tc_rank_supported(s->r) || s->small_seg_max < 0) return false;
   for (const auto& sl : s->slots)
@@ -760,7 +760,7 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
       args.yreg[i] = yreg ? yreg[b0 + i] : 0;
       t.y = y[b0 + i];
       t.vpart_off = (long long)si.kc_prefix * p->max_rows * s->r;
-      t.vbf_off = (long long)slots[b0 + i] * p->max_rows * s->r;
+      t.vbf_off = (long long)slots[b0 + i] * p->max_rows * std::max(s->r, 16);  // (r = 8: rows padded to K = 16)
       t.h_in = si.h_in;
       t.h_out = si.h_out;
       t.E = si.E;

@@ -119,11 +119,13 @@ constexpr int kQD = 4;  // work-queue depth
 // two SWIZZLE_128B blocks by the expand's producer warp.
 template <int R>
 struct KGeo {
-  static_assert(R == 16 || R == 32 || R == 64 || R == 128, "tcgen05 ranks");
-  static constexpr int RB = R >= 64 ? 128 : R * 2;  // bytes per row of one K block (= swizzle width)
-  static constexpr int KB = R >= 64 ? R / 64 : 1;   // K blocks
-  static constexpr int KPB = RB / 32;               // 16-element MMA k-steps per K block
-  static constexpr int CPB = RB / 16;               // 16-byte chunks per row of a K block
+  static_assert(R == 8 || R == 16 || R == 32 || R == 64 || R == 128, "tcgen05 ranks");
+  // r = 8: K and N padded to 16 with zeros (the MMA's minimum), rows of 32 bytes
+  static constexpr int RP = R < 16 ? 16 : R;         // padded rank
+  static constexpr int RB = RP >= 64 ? 128 : RP * 2;  // bytes per row of one K block (= swizzle width)
+  static constexpr int KB = RP >= 64 ? RP / 64 : 1;   // K blocks
+  static constexpr int KPB = RB / 32;                 // 16-element MMA k-steps per K block
+  static constexpr int CPB = RB / 16;                 // 16-byte chunks per row of a K block
 };
 
 // K-major shared-memory matrix descriptor (sm_100 format) for swizzle width
@@ -139,7 +141,7 @@ LORA_DEVINL uint64_t kmajor_desc(uint32_t smem_addr) {
   return d;
 }
 
-// element offset of 16-byte chunk q (0 .. R/8-1) of sorted row `row` (row n of
+// element offset of 16-byte chunk q (0 .. RP/8-1) of sorted row `row` (row n of
 // its tile) in a slot's bf16 v region: [KB][max_rows][RB / 2]
 template <int R>
 LORA_DEVINL long long vbf_chunk(long long row, int n, int q, int max_rows) {
@@ -209,13 +211,15 @@ struct ShrinkCfgT {
   static constexpr int KS_PER_STAGE = LORA_TCS_KS;         // k-steps per stage
   static constexpr int NW = PAIR ? 2 : 1;                  // A tiles per k-step
   static constexpr int X_SUB = kTileRows * 128;            // 16 KB per k-step
-  static constexpr int W_SUB = R * 128;                    // A rows of one k-step and slot (8 KB at r = 64)
+  static constexpr int NP = KGeo<R>::RP;                   // MMA N per slot (r = 8: rows 8-15 zero)
+  static constexpr int W_SUB = NP * 128;                   // smem A rows of one k-step and slot (8 KB at r = 64)
+  static constexpr int W_G = R * 128;                      // bytes of one k-step of a unit's At in global memory
   static constexpr int STAGE = KS_PER_STAGE * (X_SUB + NW * W_SUB);
   // r = 64: the measured depths; other ranks as many stages as fit (<= 6)
   static constexpr int NST_FIT = (220 * 1024) / STAGE > 6 ? 6 : (220 * 1024) / STAGE;
   static constexpr int NST = R == 64 ? (PAIR ? LORA_TCSP_NST : LORA_TCS_NST) : NST_FIT;
   static constexpr int LAG = LORA_TCS_LAG < NST - 1 ? LORA_TCS_LAG : NST - 1;  // cp.async groups kept in flight
-  static constexpr int ACC_COLS = NW * R;                  // N = r (pair: 2r)
+  static constexpr int ACC_COLS = NW * NP;                 // N = r (pair: 2r)
   static constexpr int TMEM_COLS = 2 * ACC_COLS;           // 2 accumulators
   static constexpr int SMEM = 1024 + NST * STAGE + 256;
   static_assert(SMEM <= 227 * 1024, "shrink stages exceed shared memory");
@@ -234,6 +238,8 @@ LORA_DEVINL void store_vbf_row(uint16_t* vslot, long long row, int n, const floa
     w.w = pack_bf16x2_rn(v[8 * q + 6], v[8 * q + 7]);
     *reinterpret_cast<uint4*>(vslot + vbf_chunk<R>(row, n, q, max_rows)) = w;
   }
+  if constexpr (R < 16)  // the K padding of the expand operand
+    *reinterpret_cast<uint4*>(vslot + vbf_chunk<R>(row, n, 1, max_rows)) = make_uint4(0, 0, 0, 0);
 }
 
 template <int R, bool REMOTE, bool PAIR>
@@ -272,6 +278,17 @@ __global__ void __launch_bounds__(9 * 32, 1)
     fence_mbar_init();
   }
   if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if constexpr (C::NP != R) {
+    // r = 8: A rows 8-15 of every slot of every stage stay zero (the bulk
+    // copies fill rows 0-7 only)
+    for (int s = 0; s < C::NST; ++s)
+      for (int i = threadIdx.x; i < C::KS_PER_STAGE * C::NW * (C::W_SUB - C::W_G) / 16; i += C::THREADS) {
+        const int per = (C::W_SUB - C::W_G) / 16, slot = i / per, o = i - slot * per;
+        *reinterpret_cast<uint4*>(smem + s * C::STAGE + C::KS_PER_STAGE * C::X_SUB + slot * C::W_SUB + C::W_G +
+                                  o * 16) = make_uint4(0, 0, 0, 0);
+      }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -325,9 +342,11 @@ __global__ void __launch_bounds__(9 * 32, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sbase = smem + stage * C::STAGE;
           if (lane == 0) {
-            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * (C::W_SUB + C::X_SUB));
-            bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB,
-                     wbase + (long long)st * C::KS_PER_STAGE * (R * 64), C::KS_PER_STAGE * C::W_SUB, &full[stage]);
+            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * (C::W_G + C::X_SUB));
+#pragma unroll
+            for (int ks = 0; ks < C::KS_PER_STAGE; ++ks)
+              bulk_g2s(sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::W_SUB,
+                       wbase + (long long)(st * C::KS_PER_STAGE + ks) * (R * 64), C::W_G, &full[stage]);
           }
           __syncwarp();
           const int col = kc * t.KI + st * C::KS_PER_STAGE * C::KSTEP;
@@ -362,24 +381,24 @@ __global__ void __launch_bounds__(9 * 32, 1)
           // (A tiles evict_last when args.tc_flags bit 5: a unit's A is re-read by each of its tiles)
           const uint64_t wpol = (args.tc_flags & 32) ? policy_evict_last() : policy_evict_normal();
           if (pj >= 0) {
-            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * 2 * C::W_SUB);
+            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * 2 * C::W_G);
 #pragma unroll
             for (int ks = 0; ks < C::KS_PER_STAGE; ++ks) {
               uint8_t* wd = sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB;
               const long long wo = (long long)(st * C::KS_PER_STAGE + ks) * (R * 64);
-              bulk_g2s_hint(wd, wbase + wo, C::W_SUB, &full[stage], wpol);
-              bulk_g2s_hint(wd + C::W_SUB, wbase2 + wo, C::W_SUB, &full[stage], wpol);
+              bulk_g2s_hint(wd, wbase + wo, C::W_G, &full[stage], wpol);
+              bulk_g2s_hint(wd + C::W_SUB, wbase2 + wo, C::W_G, &full[stage], wpol);
             }
-          } else if (C::NW == 1) {
+          } else if (C::NW == 1 && C::NP == R) {
             mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
             bulk_g2s_hint(sbase + C::KS_PER_STAGE * C::X_SUB, wbase + (long long)st * C::KS_PER_STAGE * (R * 64),
                           C::KS_PER_STAGE * C::W_SUB, &full[stage], wpol);
-          } else {  // an unpaired task in a pair launch: one A tile per k-step, N = r
-            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_SUB);
+          } else {  // an unpaired task in a pair launch (or r = 8): one A tile per k-step, N = r
+            mbar_arrive_expect_tx(&full[stage], C::KS_PER_STAGE * C::W_G);
 #pragma unroll
             for (int ks = 0; ks < C::KS_PER_STAGE; ++ks)
               bulk_g2s_hint(sbase + C::KS_PER_STAGE * C::X_SUB + ks * C::NW * C::W_SUB,
-                            wbase + (long long)(st * C::KS_PER_STAGE + ks) * (R * 64), C::W_SUB, &full[stage], wpol);
+                            wbase + (long long)(st * C::KS_PER_STAGE + ks) * (R * 64), C::W_G, &full[stage], wpol);
           }
         }
         const int j0 = st * C::KS_PER_STAGE * C::KSTEP;
@@ -437,7 +456,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
       const int task = find_task_kc(args, kcg);
       const SlotTask& t = args.t[task];
       const int n_st = t.KI / (C::KSTEP * C::KS_PER_STAGE);
-      const uint32_t idesc = idesc_bf16(128, (PAIR && args.tc_pair[task] >= 0) ? 2 * R : R);
+      const uint32_t idesc = idesc_bf16(128, (PAIR && args.tc_pair[task] >= 0) ? 2 * C::NP : C::NP);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
@@ -494,10 +513,10 @@ __global__ void __launch_bounds__(9 * 32, 1)
 #pragma unroll 1
       for (int half = 0; half < (pj >= 0 ? 2 : 1); ++half) {
         const SlotTask& th = half ? args.t[pj] : t;
-        float v[R];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS + half * R;
+        float v[C::NP];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACC_COLS + half * C::NP;
 #pragma unroll
-        for (int c = 0; c < R; c += 16) tmem_ld16(taddr + c, v + c);
+        for (int c = 0; c < C::NP; c += 16) tmem_ld16(taddr + c, v + c);
         if (row_in_tile < tile.y) {
           if (t.n_kc == 1) {
             // the whole K in one accumulator: v rounded to bf16 here (no reduction pass)
@@ -565,6 +584,9 @@ __global__ void __launch_bounds__(256) tc_vreduce_kernel(const __grid_constant__
     w.z = pack_bf16x2_rn(s[4], s[5]);
     w.w = pack_bf16x2_rn(s[6], s[7]);
     *reinterpret_cast<uint4*>(pd.vbf + t.vbf_off + vbf_chunk<R>((long long)tile.x + n, n, q, pd.max_rows)) = w;
+    if constexpr (R < 16)  // the K padding of the expand operand
+      *reinterpret_cast<uint4*>(pd.vbf + t.vbf_off + vbf_chunk<R>((long long)tile.x + n, n, 1, pd.max_rows)) =
+          make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -632,10 +654,12 @@ struct ExpandCfg {
   static constexpr int MMA_WARP = 17;   // warp 17: TMEM alloc + MMA
   static constexpr int THREADS = 18 * 32;
   static constexpr int MSUB = 128;                     // output columns per MMA (N)
-  static constexpr int B_SUB = MSUB * R * 2;           // Bt rows of a sub-tile (16 KB at r = 64)
+  static constexpr int B_SUB = MSUB * G::RP * 2;       // smem Bt rows of a sub-tile (16 KB at r = 64)
   // r = 128: the producer warp re-tiles the 256-byte Bt rows into two
-  // SWIZZLE_128B K blocks with cp.async (all 32 lanes arrive on the stage)
-  static constexpr bool BT_RETILE = R > 64;
+  // SWIZZLE_128B K blocks with cp.async (all 32 lanes arrive on the stage);
+  // r = 8: the 16-byte rows go to the data chunk of 32-byte SWIZZLE_32B rows
+  // whose other chunk stays zero (K padded to 16)
+  static constexpr bool BT_RETILE = R > 64 || R < 16;
 #ifndef LORA_TCE_NST
 #define LORA_TCE_NST 2
 #endif
@@ -652,7 +676,7 @@ struct ExpandCfg {
 #define LORA_TCE128_YD 2
 #endif
   static constexpr int NST = R > 64 ? LORA_TCE128_NST : LORA_TCE_NST;
-  static constexpr int V_TILE = kTileRows * R * 2;     // v tile, M = 128 rows x K = R (16 KB at r = 64)
+  static constexpr int V_TILE = kTileRows * G::RP * 2; // v tile, M = 128 rows x K = r (16 KB at r = 64)
   static constexpr int VB = R > 64 ? LORA_TCE128_VB : 2;  // v tile buffers
   // bf16 output: y tiles [128 rows][128 cols] (16-byte chunks XOR-swizzled by
   // row) in a ring of YS slots, fetched YD-1 sub-tiles ahead
@@ -713,6 +737,13 @@ __global__ void __launch_bounds__(18 * 32, 1)
     fence_mbar_init();
   }
   if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if constexpr (R < 16) {
+    // r = 8: the Bt stages' K padding chunks stay zero (the producer fills
+    // only each row's data chunk)
+    for (int i = threadIdx.x; i < C::NST * C::B_SUB / 16; i += C::THREADS)
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -746,7 +777,7 @@ __global__ void __launch_bounds__(18 * 32, 1)
             vready = true;
           }
           // one bulk copy per K block: rows [tile.x, tile.x + tile.y) of the slot's v store
-          mbar_arrive_expect_tx(&vfull[vb], (uint32_t)tile.y * R * 2);
+          mbar_arrive_expect_tx(&vfull[vb], (uint32_t)tile.y * G::RP * 2);
 #pragma unroll
           for (int kb = 0; kb < G::KB; ++kb)
             bulk_g2s(vtile + vb * C::V_TILE + kb * (kTileRows * G::RB),
@@ -762,7 +793,7 @@ __global__ void __launch_bounds__(18 * 32, 1)
         const int n_sub = t.CI / C::MSUB;
         for (int sb = 0; sb < n_sub; ++sb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if constexpr (C::BT_RETILE) {
+          if constexpr (C::BT_RETILE && R > 64) {
             // 128 columns x 256 bytes: physical chunk p of column c holds k chunk
             // p ^ ((c & 3) << 1) (common.cuh); k chunk ch goes to K block ch / 8,
             // chunk (ch % 8) ^ (c & 7) of the block's row c (SWIZZLE_128B)
@@ -774,6 +805,16 @@ __global__ void __launch_bounds__(18 * 32, 1)
               const int ch = pch ^ ((c & 3) << 1);
               cp_async16_u32(dst + (ch >> 3) * (C::MSUB * 128) + c * 128 + (((ch & 7) ^ (c & 7)) << 4),
                              src + c * R + pch * 8);
+            }
+            cp_async_mbar_arrive_noinc(&full[stage]);
+          } else if constexpr (C::BT_RETILE) {
+            // r = 8: column c's 16 bytes to chunk swz(c, 0) of its 32-byte row
+            const uint16_t* src = bbase + (long long)sb * C::MSUB * R;
+            const uint32_t dst = smem_u32(smem + stage * C::B_SUB);
+#pragma unroll
+            for (int i = 0; i < C::MSUB / 32; ++i) {
+              const int c = i * 32 + lane;
+              cp_async16_u32(dst + c * 32 + (swz_row_chunk(c, 0, 32) << 4), src + c * R);
             }
             cp_async_mbar_arrive_noinc(&full[stage]);
           } else {
@@ -814,7 +855,7 @@ __global__ void __launch_bounds__(18 * 32, 1)
           const uint32_t ba = smem_u32(smem + stage * C::B_SUB);
           const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
 #pragma unroll
-          for (int kk = 0; kk < R / 16; ++kk) {
+          for (int kk = 0; kk < G::RP / 16; ++kk) {
             const int kb = kk / G::KPB, ko = (kk % G::KPB) * 32;
             umma_bf16(d_tmem, kmajor_desc<G::RB>(va + kb * (kTileRows * G::RB) + ko),
                       kmajor_desc<G::RB>(ba + kb * (C::MSUB * G::RB) + ko), idesc, kk > 0 ? 1u : 0u);
@@ -1152,11 +1193,12 @@ static cudaError_t launch_tc_expand_r(const MultiArgs& args, const PlanDev& pd, 
   return cudaGetLastError();
 }
 
-bool tc_rank_supported(int rank) { return rank == 16 || rank == 32 || rank == 64 || rank == 128; }
+bool tc_rank_supported(int rank) { return rank == 8 || rank == 16 || rank == 32 || rank == 64 || rank == 128; }
 
 cudaError_t launch_tc_shrink(int rank, const MultiArgs& args, const PlanDev& pd, int x_rows, int grid,
                              cudaStream_t stream) {
   switch (rank) {
+    case 8: return launch_tc_shrink_r<8>(args, pd, x_rows, grid, stream);
     case 16: return launch_tc_shrink_r<16>(args, pd, x_rows, grid, stream);
     case 32: return launch_tc_shrink_r<32>(args, pd, x_rows, grid, stream);
     case 64: return launch_tc_shrink_r<64>(args, pd, x_rows, grid, stream);
@@ -1168,6 +1210,7 @@ cudaError_t launch_tc_shrink(int rank, const MultiArgs& args, const PlanDev& pd,
 cudaError_t launch_tc_vreduce(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   cudaError_t e;
   switch (rank) {
+    case 8: e = launch_pdl(tc_vreduce_kernel<8>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
     case 16: e = launch_pdl(tc_vreduce_kernel<16>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
     case 32: e = launch_pdl(tc_vreduce_kernel<32>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
     case 64: e = launch_pdl(tc_vreduce_kernel<64>, dim3(grid * 4), dim3(256), 0, stream, args, pd); break;
@@ -1180,6 +1223,7 @@ cudaError_t launch_tc_vreduce(int rank, const MultiArgs& args, const PlanDev& pd
 
 cudaError_t launch_tc_expand(int rank, const MultiArgs& args, const PlanDev& pd, int grid, cudaStream_t stream) {
   switch (rank) {
+    case 8: return launch_tc_expand_r<8>(args, pd, grid, stream);
     case 16: return launch_tc_expand_r<16>(args, pd, grid, stream);
     case 32: return launch_tc_expand_r<32>(args, pd, grid, stream);
     case 64: return launch_tc_expand_r<64>(args, pd, grid, stream);

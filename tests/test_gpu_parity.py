@@ -173,11 +173,12 @@ def test_fill_store_equals_loaded_weights(B, rank):
 # exact-integer probes: bit-exact on every kernel path
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("rank,small_max", [(8, None), (16, None), (32, None), (64, -1), (64, 0), (64, 4),
-                                            (128, None), (16, 0), (16, 4), (32, 0), (32, 4), (128, 0), (128, 4)])
+                                            (128, None), (16, 0), (16, 4), (32, 0), (32, 4), (128, 0), (128, 4),
+                                            (8, 0), (8, 4)])
 def test_exact_integer_probes(B, monkeypatch, rank, small_max):
     """Every kernel route bit-exact on integer-valued inputs: CUDA cores only
-    (r = 8, small_max -1), tcgen05 only (small_max 0), or both (the large
-    segment on tcgen05 at r = 16 / 32 / 64 / 128, LORA_TC_MIN_ROWS=0)."""
+    (small_max -1), tcgen05 only (small_max 0), or both (the large segment on
+    tcgen05 at r = 8 / 16 / 32 / 64 / 128, LORA_TC_MIN_ROWS=0)."""
     if rank != 64 and small_max is not None:
         monkeypatch.setenv("LORA_TC_MIN_ROWS", "0")
     rng = np.random.default_rng(rank * 10 + (3 if small_max is None else small_max + 2))
@@ -203,7 +204,7 @@ def test_exact_integer_probes(B, monkeypatch, rank, small_max):
         nv, ns, ng, nt = B.lora_plan_stats(s, p)
         # the requested kernel path is the one that ran
         # (conftest sets LORA_TC_MIN_ROWS=0: the large segment takes tcgen05 at every tcgen05 rank)
-        if rank == 8 or small_max == -1:
+        if small_max == -1:
             assert nt == 0 and ng > 0
         elif small_max == 0:
             assert ng == 0 and nt > 0
@@ -670,13 +671,13 @@ def test_plan_capacity_bound(B):
 
 
 def _tc_rank_cfg(rank, T, y_dtype):
-    # slot c's h_in = 8192 splits K on the tcgen05 chain below 4096 rows at
-    # every rank (KI caps 4096 / 2048 / 512 at r = 16 / 32 / 128): tc_vreduce
+    # slot c's h_in = 16384 splits K on the tcgen05 chain below 4096 rows at
+    # every rank (KI caps 8192 / 4096 / 2048 / 512 at r = 8 / 16 / 32 / 128): tc_vreduce
     return li.Config("tcr", 12, (li.Slot("a", 512, 768, 4, 0), li.Slot("b", 768, 512, 4, 1),
-                                 li.Slot("c", 8192, 256, 4, 2)), rank, 24, 4, 2, T // 2, y_dtype)
+                                 li.Slot("c", 16384, 256, 4, 2)), rank, 24, 4, 2, T // 2, y_dtype)
 
 
-@pytest.mark.parametrize("rank", [16, 32, 128])
+@pytest.mark.parametrize("rank", [8, 16, 32, 128])
 @pytest.mark.parametrize("y_dtype,T,small_max", [("bf16", 600, None), ("fp32", 600, 0), ("bf16", 4200, None)])
 def test_tc_chain_every_rank_full_parity(B, monkeypatch, rank, y_dtype, T, small_max):
     """The tcgen05 chain at r = 16 / 32 / 128 (SWIZZLE_32B / 64B v and Bt

@@ -87,7 +87,7 @@ def test_full_config_every_row(B, name):
         B.lora_server_destroy(s)
 
 
-@pytest.mark.parametrize("rank", [32, 128])
+@pytest.mark.parametrize("rank", [8, 32, 128])
 def test_prefill_shapes_other_ranks_every_row(B, rank):
     """Config 4's shapes (Mixtral gate/up/down, 8192 tokens, 16384 rows) at
     r = 32 and r = 128: the tcgen05 chain at those ranks (SWIZZLE_64B operands;

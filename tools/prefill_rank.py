@@ -1,6 +1,7 @@
 """Prefill-shaped (config 4: Mixtral gate/up/down, 8192 tokens, 4 sequences of
-64 adapters) step time at r = 16 / 32 / 64 / 128: r = 64 runs on the tcgen05
-chain, the other ranks on the CUDA-core kernels.  Prints one JSON line."""
+64 adapters) step time at r = 8 / 16 / 32 / 64 / 128 (large segments on the
+tcgen05 chain at every rank; RANK_SWEEP_BASE=<config> for other shapes).
+Prints one JSON line."""
 import dataclasses
 import json
 import os
@@ -19,7 +20,7 @@ def main():
     stream = torch.cuda.current_stream()
     hbm_peak, _, _ = bench.load_peaks()
     out = {}
-    for rk in [int(a) for a in (sys.argv[1:] or ["16", "32", "64", "128"])]:
+    for rk in [int(a) for a in (sys.argv[1:] or ["8", "16", "32", "64", "128"])]:
         c = dataclasses.replace(li.CONFIGS[base], name=f"{base}_r{rk}", rank=rk)
         b = li.make_batch(c)
         slots = list(range(len(c.slots)))
