@@ -838,7 +838,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="mixtral_sharded", choices=sorted(li.CONFIGS))
+    ap.add_argument("--workload", default="mixtral_sharded", choices=sorted(li.CONFIGS) + sorted(li.VARIANTS))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -859,7 +859,7 @@ def main():
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch_under_torchrun(args.gpus)
-    cfg = li.CONFIGS[args.workload]
+    cfg = li.CONFIGS[args.workload] if args.workload in li.CONFIGS else li.VARIANTS[args.workload]
     batch = li.make_batch(cfg)
     slots = list(range(len(cfg.slots)))
     if args.impl == "reference":
