@@ -38,7 +38,7 @@ def one_case(B, rng, k):
             h_in = slots[-1].h_in
         slots.append(li.Slot(f"s{i}", h_in, h_out, E, xbuf))
     n_ad = int(rng.choice([3, 16, 64, 300]))
-    n_tok = int(rng.choice([1, 7, 64, 300, 1500, 2600]))
+    n_tok = int(rng.choice([1, 7, 64, 300, 1500, 2600, 9000]))
     y_dtype = "fp32" if rng.random() < 0.4 else "bf16"
     n_seqs = int(rng.choice([0, 0, 2, 8])) if n_tok >= 8 else 0
     zipf = float(rng.choice([0.0, 1.2, 2.0]))
