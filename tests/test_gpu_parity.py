@@ -723,7 +723,7 @@ def test_rank128_full_parity(B, y_dtype, T):
 @pytest.mark.parametrize("loopback,y_dtype,rank,transport", [
     (False, "bf16", 64, "push"), (True, "fp32", 64, "push"), (True, "bf16", 64, "push"), (True, "bf16", 16, "push"),
     (True, "fp32", 16, "push"), (True, "fp32", 8, "nccl"), (True, "bf16", 128, "push"), (True, "fp32", 128, "push"),
-    (True, "fp32", 64, "nccl"), (True, "bf16", 64, "nccl")])
+    (True, "fp32", 64, "nccl"), (True, "bf16", 64, "nccl"), (True, "bf16", 8, "push"), (True, "fp32", 32, "push")])
 def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
     """Sharded server at G = 1.  In place (no exchange): bit-identical to the
     unsharded server.  Loopback (LORA_SHARD_LOOPBACK=1 sends every row through
