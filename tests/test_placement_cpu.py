@@ -147,3 +147,33 @@ def test_push_model_predicts_config5_efficiency():
         ch = P.choose_placement(b.adapter_ids, b.expert_ids, src, G, u, r, 0.0, x_bytes=x, d_bytes=d)
         tg = min(ch["table"].values())
         assert t1 / (G * tg) >= 0.70, (G, t1 / (G * tg))
+
+
+def test_bench_algorithmic_dispatch_rule(monkeypatch):
+    """bench.algorithmic attributes a slot's bytes to the tcgen05 kernels
+    exactly as the library dispatches: segments of more than small_max rows,
+    tcgen05 ranks 8-128, and only when those segments hold at least
+    LORA_TC_MIN_ROWS rows together (256, 2048 at r <= 16); hand-built batch."""
+    import bench
+    import lora_inputs as li
+    monkeypatch.delenv("LORA_TC_MIN_ROWS", raising=False)
+    # 300 rows of adapter 0 (one 300-row segment), 5 singletons
+    a = np.array([0] * 300 + [1, 2, 3, 4, 5], np.int32)
+    batch = li.Batch(a, np.zeros_like(a), a.size, 1)
+    for r, tc in ((64, True), (32, True), (128, True), (8, False), (16, False)):
+        cfg = li.Config("t", 1, (li.Slot("s", 256, 512, 1, 0),), r, 8, 1, 1, a.size, "bf16")
+        out = bench.algorithmic(cfg, batch, [0])
+        big_rows = 300
+        if tc:  # the big segment on tcgen05: its unit's A/B, rows' x and y
+            assert out["tc05_shrink"] == 256 * r * 2 + big_rows * 256 * 2
+            assert out["tc05_expand"] == 512 * r * 2 + big_rows * 512 * 2 * 2
+            assert out["simt_shrink"] == 5 * 256 * r * 2 + 5 * 256 * 2
+        else:  # r <= 16: 300 < 2048 rows in large segments -> CUDA cores only
+            assert out["tc05_shrink"] == 0 and out["tc05_expand"] == 0
+            assert out["simt_shrink"] == 6 * 256 * r * 2 + 305 * 256 * 2
+    monkeypatch.setenv("LORA_TC_MIN_ROWS", "0")
+    cfg = li.Config("t", 1, (li.Slot("s", 256, 512, 1, 0),), 16, 8, 1, 1, a.size, "bf16")
+    assert bench.algorithmic(cfg, batch, [0])["tc05_shrink"] > 0
+    monkeypatch.setenv("LORA_TC_MIN_ROWS", "400")
+    cfg = li.Config("t", 1, (li.Slot("s", 256, 512, 1, 0),), 64, 8, 1, 1, a.size, "bf16")
+    assert bench.algorithmic(cfg, batch, [0])["tc05_shrink"] == 0
