@@ -69,7 +69,7 @@ typedef struct {
   int32_t rank;              /* r, uniform (one rank per model): 8, 16, 32, 64 or 128 ("r typically 32-128") */
   int32_t n_adapters;        /* global adapter count n */
   const float *scale;        /* [n_adapters] host fp32 s_a; NULL => all 1.0 (R1) */
-  int32_t max_rows;          /* capacity (rows) of the internal plan; 0 < max_rows <= 32768 (sharded: max_rows * world <= 16384) */
+  int32_t max_rows;          /* capacity (rows) of the internal plan; 0 < max_rows <= 32768 (sharded: max_rows * world <= 32768) */
   int32_t device;            /* CUDA device ordinal */
   int32_t n_replicated;      /* sharded servers only: adapters [0, n_replicated) are stored on
                                 every rank (popularity-aware placement for skewed traffic,
@@ -252,7 +252,7 @@ lora_status_t lora_nccl_unique_id(void *out128);
  * collectively with the same config.  cfg->max_rows is this rank's row
  * capacity; its owner-side plan holds max_rows * world received rows (rows
  * beyond that are dropped and flagged), so an unbalanced deployment sizes
- * max_rows for the most loaded owner.  max_rows * world <= 16384. */
+ * max_rows for the most loaded owner.  max_rows * world <= 32768. */
 lora_status_t lora_server_create_sharded(const lora_config_t *cfg, int32_t rank, int32_t world,
                                          const void *nccl_unique_id, lora_server_t **out);
 

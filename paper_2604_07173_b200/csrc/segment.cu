@@ -470,7 +470,8 @@ LORA_DEVINL int lower_key(const uint32_t* srt, int n, uint32_t k) {
 template <int EPT>
 __global__ void __launch_bounds__(kSegThreads, 1)
     seg_local_kernel(const int32_t* __restrict__ adapter_ids, const int32_t* __restrict__ expert_ids, int T, int E,
-                     int n_adapters, int kb, int C, SegParams sp, PlanDev pd, int* __restrict__ err_flag) {
+                     int n_adapters, int kb, int C, SegParams sp, PlanDev pd, int* __restrict__ err_flag,
+                     const int* __restrict__ T_dev) {
   constexpr int RPC = kSegThreads * EPT;
   extern __shared__ __align__(16) uint8_t seg_smem[];
   __shared__ int scan_tmp[40];
@@ -480,6 +481,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   const int tid = threadIdx.x, c = blockIdx.x;
   const int row0 = c * RPC;
   const uint32_t K = (uint32_t)n_adapters * E;
+  if (T_dev) T = min(T, max(*T_dev, 0));  // device-side row count (T: the capacity the grid was sized for)
   pdl_launch_dependents();  // seg_scan (PDL) may be scheduled; it waits for this grid
   if (blockIdx.x == 0) SEG_T(12);
   int ad[EPT], ex[EPT];
@@ -703,7 +705,9 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
     const int forced = fe ? atoi(fe) : -1;
     // beyond one CTA's capacity the multi-CTA path is the only one
     const bool big = T > kMaxOneCtaRows;
-    const bool want = !T_dev && (big || (forced < 0 ? T >= kSegMultiMin : forced == 1));  // (device T: one CTA)
+    // (device-side T: the one-CTA kernel up to its capacity, the multi-CTA
+    // kernels -- sized by the capacity, rows past *T_dev masked -- beyond it)
+    const bool want = T_dev ? big : (big || (forced < 0 ? T >= kSegMultiMin : forced == 1));
     int ept = 0;
     if (want && pd.hist && T > 0 && kb + kLocBits <= 32 && K > 0 && K <= kSegKeysMax) {
       // rows per CTA: the fewest (1024, 2048) that keep the histogram K x C
@@ -748,7 +752,8 @@ cudaError_t launch_segment(const int32_t* adapter_ids, const int32_t* expert_ids
         // seg_local waits for everything before it on the stream (the previous
         // applies still read the plan); seg_scan and seg_scatter are launched
         // programmatically dependent (PDL) on their predecessor in the chain
-        local<<<C, kSegThreads, lsm, stream>>>(adapter_ids, expert_ids, T, E, n_adapters, kb, C, sp, pd, err_flag);
+        local<<<C, kSegThreads, lsm, stream>>>(adapter_ids, expert_ids, T, E, n_adapters, kb, C, sp, pd, err_flag,
+                                               T_dev);
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = seg_pdl() ? 1 : 0;

@@ -567,8 +567,8 @@ static lora_status_t create_sharded_impl(const lora_config_t* cfg, int32_t rank,
   if (!cfg || !out || world < 1 || rank < 0 || rank >= world)
     return fail(nullptr, LORA_ERR_INVALID_ARG, "lora_server_create_sharded: bad argument");
   if (world > kMaxWorld) return fail(nullptr, LORA_ERR_UNSUPPORTED, "world > 8 (one NVLink domain of B200s)");
-  if ((long long)cfg->max_rows * world > kMaxOneCtaRows)  // the owner's plan: device-side row count, one-CTA segmenter
-    return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows * world must be <= 16384 (owner-side plan capacity)");
+  if ((long long)cfg->max_rows * world > kMaxPlanRows)  // the owner's plan holds every rank's rows at worst
+    return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows * world must be <= 32768 (owner-side plan capacity)");
   if (cfg->max_rows >= (1 << kOriginRowBits)) return fail(nullptr, LORA_ERR_UNSUPPORTED, "max_rows too large");
   if (cfg->n_replicated < 0) return fail(nullptr, LORA_ERR_INVALID_ARG, "n_replicated < 0");
   NcclApi& api = nccl();

@@ -770,6 +770,40 @@ def test_sharded_g1(B, monkeypatch, loopback, y_dtype, rank, transport):
         B.lora_server_destroy(s)
 
 
+@pytest.mark.parametrize("y_dtype", ["fp32", "bf16"])
+def test_sharded_loopback_beyond_one_cta_rows(B, monkeypatch, y_dtype):
+    """A 20000-row batch through the push path's loopback: the owner-side plan
+    (capacity max_rows * world, row count known on the device) takes the
+    multi-CTA segmenter with the rows past the device count masked.  fp32:
+    bit-identical to the unsharded server; bf16: the oracle's tolerance."""
+    monkeypatch.setenv("LORA_SHARD_LOOPBACK", "1")
+    cfg = dataclasses.replace(_mid_cfg(rank=64, T=20000), y_dtype=y_dtype)
+    b = li.make_batch(cfg)
+    T = b.n_rows
+    s = U.make_server(B, cfg)
+    c = B.make_config([sl.h_in for sl in cfg.slots], [sl.h_out for sl in cfg.slots],
+                      [sl.n_experts for sl in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), T, 0)
+    sh = B.lora_server_create_sharded(c, 0, 1, B.lora_nccl_unique_id())
+    try:
+        B.lora_server_fill_synthetic(sh, cfg.seed)
+        y_ref = _run_multi(B, s, cfg, b, [0, 1])
+        ad, ex = U.ids_dev(b)
+        xs = [U.x_dev(B, cfg, i, T) for i in range(2)]
+        ys = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+        U.register(B, sh, xs + ys)
+        B.lora_apply_sharded(sh, [0, 1], xs, ad, ex, ys, B.LORA_FP32 if y_dtype == "fp32" else B.LORA_BF16, T)
+        torch.cuda.synchronize()
+        assert B.lora_server_check(sh) == B.LORA_OK
+        for i in range(2):
+            if y_dtype == "fp32":
+                assert torch.equal(ys[i], y_ref[i]), f"slot {i}"
+            else:
+                U.assert_parity(ys[i], oracle.apply_slot(cfg, i, b), f"loopback 20000 rows slot {i}")
+    finally:
+        B.lora_server_destroy(sh)
+        B.lora_server_destroy(s)
+
+
 def test_sharded_push_graph_capture(B, monkeypatch):
     """The push path has no host synchronisation: a sharded step captured in a
     CUDA graph and replayed (the epoch advances in device memory) gives the
