@@ -518,6 +518,21 @@ def run_ours(args, cfg, batch, slots):
         ems = e0.elapsed_time(e1) / args.e2e_steps
         e2e = {"value": cfg.n_tokens / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems, "api": "lora_apply_multi_host (pinned host)"}
+        # the paper's protocol: activations up, deltas down, the
+        # client adds them -- no base output over PCIe (lora_apply_multi_host_delta)
+        dh = [torch.empty_like(y).pin_memory() for y in yh]
+        h2d_d = h2d - sum(y.numel() * ysz for y in yh)
+        B.lora_apply_multi_host_delta(run.s, slots, xh_list, adh, exh if E > 1 else None, dh, run.dt, T, stream)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            B.lora_apply_multi_host_delta(run.s, slots, xh_list, adh, exh if E > 1 else None, dh, run.dt, T, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1) / args.e2e_steps
+        e2e["delta_api"] = {"value": cfg.n_tokens / (dms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d_d),
+                            "d2h_bytes_per_step": int(d2h), "ms_per_step": dms,
+                            "api": "lora_apply_multi_host_delta (pinned host; x + ids up, deltas down)"}
     run.destroy()
 
     alg = algorithmic(cfg, batch, slots, int(os.environ.get("LORA_SMALL_SEG_MAX", "8")))

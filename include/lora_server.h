@@ -213,6 +213,18 @@ lora_status_t lora_apply_plan_multi(lora_server_t *s, const lora_plan_t *p, int3
                                     const int32_t *slots, const void *const *x, void *const *y,
                                     lora_dtype_t y_dtype, void *stream);
 
+/* The deltas themselves, for a client that adds them to its own base output
+ * ("returns the updated activations", "receive the computed
+ * results ... followed by a final addition"): delta[i] row r = s_a * (x A) B
+ * for rows with an adapter, 0 for rows without (a = -1, or flagged ids);
+ * delta_dtype LORA_BF16 (each element rounded once) or LORA_FP32.  The delta
+ * buffers [T][h_out] (device) are written, never read; same plan / slot / x
+ * rules and errors as lora_apply_plan_multi (nothing enqueued on a host-side
+ * error).  Equals lora_apply_plan_multi on a zero y, bit for bit. */
+lora_status_t lora_apply_plan_multi_delta(lora_server_t *s, const lora_plan_t *p, int32_t n,
+                                          const int32_t *slots, const void *const *x, void *const *delta,
+                                          lora_dtype_t delta_dtype, void *stream);
+
 /* Convenience: plan_build on the server's internal plan + apply_plan. */
 lora_status_t lora_apply(lora_server_t *s, int32_t slot, const void *x, const int32_t *adapter_ids,
                          const int32_t *expert_ids, void *y, lora_dtype_t y_dtype, int32_t T,
@@ -234,6 +246,14 @@ lora_status_t lora_apply_multi_host(lora_server_t *s, int32_t n, const int32_t *
                                     const void *const *x_host, const int32_t *adapter_ids_host,
                                     const int32_t *expert_ids_host, void *const *y_host,
                                     lora_dtype_t y_dtype, int32_t T, void *stream);
+
+/* The same pipeline returning the deltas (lora_apply_plan_multi_delta) into
+ * HOST buffers delta_host[i] [T][h_out]: only x and the ids go up, the deltas
+ * come down (no base output crosses PCIe). */
+lora_status_t lora_apply_multi_host_delta(lora_server_t *s, int32_t n, const int32_t *slots,
+                                          const void *const *x_host, const int32_t *adapter_ids_host,
+                                          const int32_t *expert_ids_host, void *const *delta_host,
+                                          lora_dtype_t delta_dtype, int32_t T, void *stream);
 
 /* ------------------------------------------------------------------------- */
 /* Sharded LoRA Server: LoRA Data Parallel (Sec. 4.1, Table 1 DP row) */

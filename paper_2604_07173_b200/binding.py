@@ -60,8 +60,10 @@ SIGNATURES = {
     "lora_plan_stats": (ctypes.c_int, [_vp, _pi32, _vp]),
     "lora_apply_plan": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, ctypes.c_int, _vp]),
     "lora_apply_plan_multi": (ctypes.c_int, [_vp, _vp, _i32, _pi32, _pp, _pp, ctypes.c_int, _vp]),
+    "lora_apply_plan_multi_delta": (ctypes.c_int, [_vp, _vp, _i32, _pi32, _pp, _pp, ctypes.c_int, _vp]),
     "lora_apply": (ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_int, _i32, _vp]),
     "lora_apply_multi_host": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
+    "lora_apply_multi_host_delta": (ctypes.c_int, [_vp, _i32, _pi32, _pp, _vp, _vp, _pp, ctypes.c_int, _i32, _vp]),
     "lora_nccl_unique_id": (ctypes.c_int, [_vp]),
     "lora_server_create_sharded": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _pp]),
     "lora_server_create_sharded_host": (ctypes.c_int, [ctypes.POINTER(LoraConfig), _i32, _i32, _vp, _vp, _pp]),
@@ -227,6 +229,13 @@ def lora_apply_plan_multi(s: int, p: int, slots: Sequence[int], x, y, y_dtype: i
     _check(lib.lora_apply_plan_multi(s, p, n, sl, _ptr_array(x), _ptr_array(y), y_dtype, _stream(stream)), s)
 
 
+def lora_apply_plan_multi_delta(s: int, p: int, slots: Sequence[int], x, delta, delta_dtype: int, stream=None):
+    n = len(slots)
+    sl = (ctypes.c_int32 * n)(*slots)
+    _check(lib.lora_apply_plan_multi_delta(s, p, n, sl, _ptr_array(x), _ptr_array(delta), delta_dtype,
+                                           _stream(stream)), s)
+
+
 def lora_apply(s: int, slot: int, x, adapter_ids, expert_ids, y, y_dtype: int, T: int, stream=None):
     _check(lib.lora_apply(s, slot, _ptr(x), _ptr(adapter_ids), _ptr(expert_ids), _ptr(y), y_dtype, T,
                           _stream(stream)), s)
@@ -238,6 +247,15 @@ def lora_apply_multi_host(s: int, slots: Sequence[int], x_host, adapter_ids_host
     sl = (ctypes.c_int32 * n)(*slots)
     _check(lib.lora_apply_multi_host(s, n, sl, _ptr_array(x_host), _ptr(adapter_ids_host), _ptr(expert_ids_host),
                                      _ptr_array(y_host), y_dtype, T, _stream(stream)), s)
+
+
+def lora_apply_multi_host_delta(s: int, slots: Sequence[int], x_host, adapter_ids_host, expert_ids_host, delta_host,
+                                delta_dtype: int, T: int, stream=None):
+    n = len(slots)
+    sl = (ctypes.c_int32 * n)(*slots)
+    _check(lib.lora_apply_multi_host_delta(s, n, sl, _ptr_array(x_host), _ptr(adapter_ids_host),
+                                           _ptr(expert_ids_host), _ptr_array(delta_host), delta_dtype, T,
+                                           _stream(stream)), s)
 
 
 def lora_nccl_unique_id() -> bytes:

@@ -676,7 +676,7 @@ static void fill_task_tables(MultiArgs& a) {
 
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots, const void* const* x,
                                void* const* y, lora_dtype_t y_dtype, cudaStream_t st, int store, const PushIn* push,
-                               const int16_t* xreg, const int16_t* yreg) {
+                               const int16_t* xreg, const int16_t* yreg, bool zero_y) {
   if (!p || p->s != s) return fail(s, LORA_ERR_INVALID_ARG, "plan does not belong to this server");
   if (p->n_experts < 0) return fail(s, LORA_ERR_INVALID_ARG, "plan was never built");
   if (n < 0 || (n > 0 && (!slots || !x || !y))) return fail(s, LORA_ERR_INVALID_ARG, "bad slot list");
@@ -720,6 +720,9 @@ lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const 
   }
   if (n == 0 || p->T == 0) return LORA_OK;
   CK(s, cudaSetDevice(s->device));
+  if (zero_y)  // delta outputs (store modes): rows without an adapter get a zero delta
+    for (int i = 0; i < n; ++i)
+      CK(s, cudaMemsetAsync(y[i], 0, (size_t)p->T * s->slots[slots[i]].h_out * (y_dtype == LORA_FP32 ? 4 : 2), st));
   if (s->n_resident) {
     // resident cache: wait for the pending host->device copies of these slots only
     for (int i = 0; i < n; ++i)
@@ -1005,6 +1008,16 @@ extern "C" lora_status_t lora_apply_plan_multi(lora_server_t* s, const lora_plan
   return apply_multi_impl(s, p, n, slots, x, y, y_dtype, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" lora_status_t lora_apply_plan_multi_delta(lora_server_t* s, const lora_plan_t* p, int32_t n,
+                                                     const int32_t* slots, const void* const* x, void* const* delta,
+                                                     lora_dtype_t delta_dtype, void* stream) {
+  if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
+  if (s->shard) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
+  if (delta_dtype != LORA_BF16 && delta_dtype != LORA_FP32) return fail(s, LORA_ERR_UNSUPPORTED, "delta_dtype");
+  return apply_multi_impl(s, p, n, slots, x, delta, delta_dtype, static_cast<cudaStream_t>(stream),
+                          delta_dtype == LORA_BF16 ? 2 : 1, nullptr, nullptr, nullptr, true);
+}
+
 extern "C" lora_status_t lora_apply(lora_server_t* s, int32_t slot, const void* x, const int32_t* adapter_ids,
                                     const int32_t* expert_ids, void* y, lora_dtype_t y_dtype, int32_t T,
                                     void* stream) {
@@ -1022,10 +1035,10 @@ extern "C" lora_status_t lora_apply(lora_server_t* s, int32_t slot, const void* 
 // ---------------------------------------------------------------------------
 // end-to-end with host buffers
 // ---------------------------------------------------------------------------
-extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, const int32_t* slots,
-                                               const void* const* x_host, const int32_t* adapter_ids_host,
-                                               const int32_t* expert_ids_host, void* const* y_host,
-                                               lora_dtype_t y_dtype, int32_t T, void* stream) {
+static lora_status_t apply_multi_host_impl(lora_server_t* s, int32_t n, const int32_t* slots,
+                                          const void* const* x_host, const int32_t* adapter_ids_host,
+                                          const int32_t* expert_ids_host, void* const* y_host, lora_dtype_t y_dtype,
+                                          int32_t T, void* stream, bool delta) {
   if (!s) return fail(nullptr, LORA_ERR_INVALID_ARG, "server is NULL");
   if (s->shard) return fail(s, LORA_ERR_INVALID_ARG, "sharded server: use lora_apply_sharded");
   if (n < 1 || !slots || !x_host || !y_host || (T > 0 && !adapter_ids_host))
@@ -1113,7 +1126,7 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
     std::vector<char> seen(xd.size(), 0);
     size_t total = 0;
     for (int i = 0; i < n; ++i) {
-      up[i] = rows * s->slots[slots[i]].h_out * ysz;
+      up[i] = delta ? 0 : rows * s->slots[slots[i]].h_out * ysz;
       if (!seen[x_of[i]]) {
         seen[x_of[i]] = 1;
         x_first[c][i] = 1;
@@ -1170,15 +1183,18 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
         CK(s, cudaMemcpyAsync(base + x_off[x_of[i]] + (size_t)a * hi * 2,
                               static_cast<const char*>(xd[x_of[i]]) + (size_t)a * hi * 2, (size_t)rows * hi * 2,
                               cudaMemcpyHostToDevice, s->copy_stream));
-      CK(s, cudaMemcpyAsync(base + y_off[i] + (size_t)a * ho * ysz, static_cast<const char*>(y_host[i]) + (size_t)a * ho * ysz,
-                            (size_t)rows * ho * ysz, cudaMemcpyHostToDevice, s->copy_stream));
+      if (!delta)
+        CK(s, cudaMemcpyAsync(base + y_off[i] + (size_t)a * ho * ysz,
+                              static_cast<const char*>(y_host[i]) + (size_t)a * ho * ysz, (size_t)rows * ho * ysz,
+                              cudaMemcpyHostToDevice, s->copy_stream));
       xs[i] = base + x_off[x_of[i]] + (size_t)a * hi * 2;
       ys[i] = base + y_off[i] + (size_t)a * ho * ysz;
     }
     CK(s, cudaEventRecord(ev_in, s->copy_stream));
     CK(s, cudaStreamWaitEvent(st, ev_in, 0));
     const lora_status_t rc = apply_multi_impl(s, s->host_plans[pc.rc], pc.s1 - pc.s0, slots + pc.s0, xs.data() + pc.s0,
-                                              ys.data() + pc.s0, y_dtype, st);
+                                              ys.data() + pc.s0, y_dtype, st, delta ? (y_dtype == LORA_BF16 ? 2 : 1) : 0,
+                                              nullptr, nullptr, nullptr, delta);
     if (rc != LORA_OK) return rc;
     CK(s, cudaEventRecord(ev_done, st));
     CK(s, cudaStreamWaitEvent(s->d2h_stream, ev_done, 0));
@@ -1192,6 +1208,22 @@ extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, cons
   CK(s, cudaEventRecord(ev_start, s->d2h_stream));
   CK(s, cudaStreamWaitEvent(st, ev_start, 0));
   return LORA_OK;
+}
+
+extern "C" lora_status_t lora_apply_multi_host(lora_server_t* s, int32_t n, const int32_t* slots,
+                                               const void* const* x_host, const int32_t* adapter_ids_host,
+                                               const int32_t* expert_ids_host, void* const* y_host,
+                                               lora_dtype_t y_dtype, int32_t T, void* stream) {
+  return apply_multi_host_impl(s, n, slots, x_host, adapter_ids_host, expert_ids_host, y_host, y_dtype, T, stream,
+                               false);
+}
+
+extern "C" lora_status_t lora_apply_multi_host_delta(lora_server_t* s, int32_t n, const int32_t* slots,
+                                                     const void* const* x_host, const int32_t* adapter_ids_host,
+                                                     const int32_t* expert_ids_host, void* const* delta_host,
+                                                     lora_dtype_t delta_dtype, int32_t T, void* stream) {
+  return apply_multi_host_impl(s, n, slots, x_host, adapter_ids_host, expert_ids_host, delta_host, delta_dtype, T,
+                               stream, true);
 }
 
 // ---------------------------------------------------------------------------

@@ -103,7 +103,7 @@ lora_status_t cuda_fail(lora_server* s, cudaError_t e, const char* where);
 lora_status_t apply_multi_impl(lora_server* s, const lora_plan* p, int n, const int32_t* slots,
                                const void* const* x, void* const* y, lora_dtype_t y_dtype, cudaStream_t st,
                                int store = 0, const PushIn* push = nullptr, const int16_t* xreg = nullptr,
-                               const int16_t* yreg = nullptr);
+                               const int16_t* yreg = nullptr, bool zero_y = false);
 lora_status_t plan_build_impl(lora_server* s, lora_plan* p, const int32_t* adapter_ids, const int32_t* expert_ids,
                               int T, int E, cudaStream_t st, const int* T_dev = nullptr);
 lora_status_t plan_create_impl(lora_server* s, int max_rows, lora_plan** out);

@@ -518,3 +518,61 @@ def test_host_entry_row_chunks(B, monkeypatch):
             assert torch.equal(yh[i][none], y0[i][none])
     finally:
         B.lora_server_destroy(s)
+
+
+# ---------------------------------------------------------------------------
+# the delta API (the server returns s_a (x A) B; the client adds)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype,T", [("bf16", 600), ("fp32", 600), ("bf16", 4200), ("fp32", 4200)])
+def test_delta_api_equals_apply_on_zero_y(B, dtype, T):
+    """lora_apply_plan_multi_delta equals lora_apply_plan_multi on a zero y
+    bit for bit (both kernel chains, K-split and whole-K tcgen05 items), rows
+    without a LoRA get a zero delta even in a dirty output buffer, and the
+    deltas match the oracle's y0 = 0 result."""
+    cfg = dataclasses.replace(_mid_cfg(T=T), no_lora_frac=0.05, y_dtype=dtype)
+    b = li.make_batch(cfg)
+    Tr = b.n_rows
+    s = U.make_server(B, cfg)
+    dt = B.LORA_FP32 if dtype == "fp32" else B.LORA_BF16
+    tdt = torch.float32 if dtype == "fp32" else torch.int16
+    try:
+        ad, ex = U.ids_dev(b)
+        xs = [U.x_dev(B, cfg, i, Tr) for i in range(2)]
+        p = B.lora_plan_create(s, Tr)
+        B.lora_plan_build(s, p, ad, ex, Tr, 4)
+        ys = [torch.zeros((Tr, sl.h_out), dtype=tdt, device=U.DEV) for sl in cfg.slots]
+        B.lora_apply_plan_multi(s, p, [0, 1], xs, ys, dt)
+        ds = [torch.full((Tr, sl.h_out), 7, dtype=tdt, device=U.DEV) for sl in cfg.slots]  # dirty
+        B.lora_apply_plan_multi_delta(s, p, [0, 1], xs, ds, dt)
+        torch.cuda.synchronize()
+        assert B.lora_server_check(s) == B.LORA_OK
+        B.lora_plan_destroy(p)
+        none = torch.from_numpy(np.flatnonzero(b.adapter_ids < 0)).to(U.DEV)
+        assert none.numel() > 0
+        for i in range(2):
+            assert torch.equal(ds[i], ys[i]), f"slot {i}"
+            assert not ds[i][none].any()
+            U.assert_parity(ds[i], orc.apply_slot(cfg, i, b, y0="zero"), f"delta {dtype} slot {i}")
+    finally:
+        B.lora_server_destroy(s)
+
+
+def test_host_delta_equals_host_apply_on_zero_y(B):
+    """lora_apply_multi_host_delta (x and ids up, deltas down, row-chunked
+    pipeline) equals lora_apply_multi_host on a zero y bit for bit."""
+    cfg = dataclasses.replace(_mid_cfg(T=4100), no_lora_frac=0.05)
+    b = li.make_batch(cfg)
+    T = b.n_rows
+    s = U.make_server(B, cfg)
+    try:
+        xh = [U.x_dev(B, cfg, i, T).cpu().pin_memory() for i in range(2)]
+        yh = [torch.zeros((T, sl.h_out), dtype=torch.int16).pin_memory() for sl in cfg.slots]
+        dh = [torch.full((T, sl.h_out), 3, dtype=torch.int16).pin_memory() for sl in cfg.slots]
+        B.lora_apply_multi_host(s, [0, 1], xh, b.adapter_ids, b.expert_ids, yh, B.LORA_BF16, T)
+        B.lora_apply_multi_host_delta(s, [0, 1], xh, b.adapter_ids, b.expert_ids, dh, B.LORA_BF16, T)
+        torch.cuda.synchronize()
+        assert B.lora_server_check(s) == B.LORA_OK
+        for i in range(2):
+            assert torch.equal(dh[i], yh[i]), f"slot {i}"
+    finally:
+        B.lora_server_destroy(s)
