@@ -1,7 +1,8 @@
 """Randomised parity sweep (GPU): random slot shapes, ranks, expert counts,
 adapter counts, batch sizes, id distributions, y dtypes and kernel routes
-(CUDA cores only / tcgen05 forced / mixed), each compared element by element
-with the CPU oracle.  Not part of the default suite (minutes of oracle time);
+(CUDA cores only / tcgen05 forced / mixed) and entry points (in-place apply,
+delta API, the sharded push path's G = 1 loopback), each compared element by
+element with the CPU oracle.  Not part of the default suite (minutes of oracle time);
 
     python tools/fuzz_parity.py [n_cases] [seed]
 
@@ -45,6 +46,7 @@ def one_case(B, rng, k):
     cfg = li.Config(f"fuzz{k}", 100 + k, tuple(slots), rank, n_ad, E, top_k, n_tok, y_dtype, zipf_s=zipf,
                     n_seqs=n_seqs, no_lora_frac=float(rng.choice([0.0, 0.1])))
     route = str(rng.choice(["default", "tc", "simt", "tc_all"]))
+    api = str(rng.choice(["apply", "apply", "delta", "push_loopback"]))
     os.environ["LORA_TC_MIN_ROWS"] = "0" if route in ("tc", "tc_all") else os.environ.get("FUZZ_MIN_ROWS", "256")
     b = li.make_batch(cfg)
     small = {"default": None, "tc": 4, "simt": -1, "tc_all": 0}[route]
@@ -56,19 +58,39 @@ def one_case(B, rng, k):
         for i, sl in enumerate(cfg.slots):
             if sl.xbuf not in xs:
                 xs[sl.xbuf] = U.x_dev(B, cfg, i, T)
-        ys = [U.y0_dev(B, cfg, i, T) for i in range(n_slots)]
+        dt = B.LORA_FP32 if y_dtype == "fp32" else B.LORA_BF16
+        y0 = "zero" if api == "delta" else "random"
+        ys = [U.y0_dev(B, cfg, i, T, y0) for i in range(n_slots)]
         p = B.lora_plan_create(s, T)
         B.lora_plan_build(s, p, ad, ex if E > 1 else None, T, E)
         stats = B.lora_plan_stats(s, p)
-        B.lora_apply_plan_multi(s, p, list(range(n_slots)), [xs[sl.xbuf] for sl in cfg.slots], ys,
-                                B.LORA_FP32 if y_dtype == "fp32" else B.LORA_BF16)
+        xl = [xs[sl.xbuf] for sl in cfg.slots]
+        if api == "delta":
+            B.lora_apply_plan_multi_delta(s, p, list(range(n_slots)), xl, ys, dt)
+        elif api == "push_loopback":
+            os.environ["LORA_SHARD_LOOPBACK"] = "1"
+            c = B.make_config([sl.h_in for sl in cfg.slots], [sl.h_out for sl in cfg.slots],
+                              [sl.n_experts for sl in cfg.slots], cfg.rank, cfg.n_adapters, cfg.scale(), T, 0)
+            sh = B.lora_server_create_sharded(c, 0, 1, B.lora_nccl_unique_id())
+            try:
+                B.lora_server_fill_synthetic(sh, cfg.seed)
+                xd = [x.clone() for x in xl]  # one registered buffer per slot
+                U.register(B, sh, xd + ys)
+                B.lora_apply_sharded(sh, list(range(n_slots)), xd, ad, ex if E > 1 else None, ys, dt, T)
+                torch.cuda.synchronize()
+                assert B.lora_server_check(sh) == B.LORA_OK
+            finally:
+                B.lora_server_destroy(sh)
+                del os.environ["LORA_SHARD_LOOPBACK"]
+        else:
+            B.lora_apply_plan_multi(s, p, list(range(n_slots)), xl, ys, dt)
         torch.cuda.synchronize()
         assert B.lora_server_check(s) == B.LORA_OK
         B.lora_plan_destroy(p)
         for i in range(n_slots):
-            U.assert_parity(ys[i], orc.apply_slot(cfg, i, b), f"case {k} slot {i}")
+            U.assert_parity(ys[i], orc.apply_slot(cfg, i, b, y0=y0), f"case {k} slot {i}")
         print(f"case {k}: r={rank} E={E} top{top_k} slots={[(sl.h_in, sl.h_out) for sl in cfg.slots]} "
-              f"adapters={n_ad} tokens={n_tok} seqs={n_seqs} zipf={zipf} y={y_dtype} route={route} "
+              f"adapters={n_ad} tokens={n_tok} seqs={n_seqs} zipf={zipf} y={y_dtype} route={route} api={api} "
               f"plan(valid,segs,groups,tiles)={tuple(stats)} OK", flush=True)
     finally:
         B.lora_server_destroy(s)
