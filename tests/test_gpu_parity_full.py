@@ -576,3 +576,31 @@ def test_host_delta_equals_host_apply_on_zero_y(B):
             assert torch.equal(dh[i], yh[i]), f"slot {i}"
     finally:
         B.lora_server_destroy(s)
+
+
+def test_server_reuse_across_batch_sizes(B):
+    """One server and one plan reused across batches of very different sizes
+    (1 to 20000 rows: one-CTA and multi-CTA segmenter, K-split and whole-K
+    tcgen05 items, CUDA-core only, no-LoRA rows) in one stream: the
+    self-resetting device state (work counters, histograms, arrival counters)
+    carries no stale value from one build / apply to the next."""
+    base = _mid_cfg(T=20000)
+    s = U.make_server(B, base)  # max_rows = 20000
+    p = B.lora_plan_create(s, base.n_rows)
+    try:
+        for k, n_tok in enumerate((10000, 1, 300, 7, 2100, 10000, 64, 4100)):
+            cfg = dataclasses.replace(base, n_tokens=n_tok, no_lora_frac=0.05 * (k % 2))
+            b = li.make_batch(cfg, seed=50 + k)
+            T = b.n_rows
+            ad, ex = U.ids_dev(b)
+            xs = [U.x_dev(B, cfg, i, T) for i in range(2)]
+            ys = [U.y0_dev(B, cfg, i, T) for i in range(2)]
+            B.lora_plan_build(s, p, ad, ex, T, 4)
+            B.lora_apply_plan_multi(s, p, [0, 1], xs, ys, B.LORA_BF16)
+            torch.cuda.synchronize()
+            assert B.lora_server_check(s) == B.LORA_OK
+            for i in range(2):
+                U.assert_parity(ys[i], orc.apply_slot(cfg, i, b), f"reuse step {k} ({T} rows) slot {i}")
+    finally:
+        B.lora_plan_destroy(p)
+        B.lora_server_destroy(s)
