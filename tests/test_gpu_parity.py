@@ -424,7 +424,7 @@ def test_edge_cases(B, case):
         B.lora_server_destroy(s)
 
 
-@pytest.mark.parametrize("rank", [16, 64])
+@pytest.mark.parametrize("rank", [8, 16, 64, 128])
 def test_resident_cache_matches_full_store(B, rank):
     """Resident-adapter cache (n_resident = 6 of 24 adapters, weights in
     pinned host memory, lora_server_require with LRU eviction and per-slot
